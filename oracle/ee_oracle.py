@@ -1,0 +1,323 @@
+"""EE-Tuning exit-head oracle: plain, slow, fp64 CPU reference.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this
+module.  The product path (``paper_2402_00518_b200``) never imports it, and this
+module imports nothing from the product path: the two share no code.
+
+What it computes (citations are PAPER.md line numbers, "P:<line>", plus the
+section they fall in; "A<n>" are the readings listed in DESIGN.md §3):
+
+* exit architectures (§2.1 "Architectures of early exits"):
+  ``embedding``: logits = z W_out^T with z = x;
+  ``norm``:      z = RMSNorm_f(x) (RMSNorm used in experiments P:464);
+  ``mlp``:       y = x + MLP(RMSNorm_a(x)), z = RMSNorm_f(y) (pre-norm
+                 residual structure P:165-166; SwiGLU MLP as in Llama-2, A2).
+* loss: next-token negative log-likelihood (§2 "Preliminaries"),
+  averaged over valid tokens (A4), ignore_index -1 (A6).
+* exits are independent; the backbone is frozen, so gradients flow into the
+  exit parameters only and there is no gradient w.r.t. x (P:250-252, P:261,
+  §2.2 "Stage 2").
+* weighted sum of exit losses: grads of exit i scale by alpha_i (A5).
+* Adam with beta1 0.9, beta2 0.95, eps 1e-5 (§3 "Tuning"); SGD.
+* LR schedule: linear warmup then linear decay (A14).
+* Copy initialisation (§2.1 "Initialization of early exits").
+
+Every floating-point step is fp64 with no tiling, no online softmax and no
+recompute: logits are materialised.  ``np.matmul`` is the only library
+primitive used for the contractions.  bf16 inputs are widened exactly.
+
+Parity pins for every function live in ``tests/test_oracle_pins.py``.  Random
+initialisation is *not* reproduced here (it is pinned statistically on the GPU,
+P15 in DESIGN.md) -- "parity unpinned" does not apply to any function below.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+ARCHS = ("embedding", "norm", "mlp")
+IGNORE_INDEX = -1
+
+
+# ----------------------------------------------------------------------------
+# building blocks
+# ----------------------------------------------------------------------------
+
+def bf16_bits_to_f64(bits: np.ndarray) -> np.ndarray:
+    """Exact widening of bf16 bit patterns (uint16) to fp64."""
+    b = np.ascontiguousarray(bits, dtype=np.uint16).astype(np.uint32) << 16
+    return b.view(np.float32).astype(np.float64)
+
+
+def rmsnorm(x: np.ndarray, g: np.ndarray, eps: float):
+    """RMSNorm: out = g * x * r, r = (mean_j x_j^2 + eps)^-1/2.
+
+    Returns (out, r, xhat) with xhat = x * r.
+    """
+    r = 1.0 / np.sqrt(np.mean(x * x, axis=-1) + eps)
+    xhat = x * r[:, None]
+    return g[None, :] * xhat, r, xhat
+
+
+def rmsnorm_backward(dout: np.ndarray, xhat: np.ndarray, r: np.ndarray, g: np.ndarray):
+    """Backward of ``rmsnorm`` w.r.t. its input and gain.
+
+    dg = sum_t dout_t * xhat_t;
+    dx_t = r_t * (g*dout_t - xhat_t * mean_j(g_j dout_tj xhat_tj)).
+    """
+    dg = np.sum(dout * xhat, axis=0)
+    gd = g[None, :] * dout
+    mean_term = np.mean(gd * xhat, axis=-1)
+    dx = r[:, None] * (gd - xhat * mean_term[:, None])
+    return dx, dg
+
+
+def sigmoid(a: np.ndarray) -> np.ndarray:
+    return 1.0 / (1.0 + np.exp(-a))
+
+
+def silu(a: np.ndarray) -> np.ndarray:
+    """silu(a) = a / (1 + e^-a) (Llama-2 SwiGLU gate, A2)."""
+    return a * sigmoid(a)
+
+
+def silu_grad(a: np.ndarray) -> np.ndarray:
+    """d silu / da = sigma(a) * (1 + a (1 - sigma(a)))."""
+    s = sigmoid(a)
+    return s * (1.0 + a * (1.0 - s))
+
+
+# ----------------------------------------------------------------------------
+# exit head forward
+# ----------------------------------------------------------------------------
+
+def _need(params: dict, names, arch):
+    for n in names:
+        if params.get(n) is None:
+            raise ValueError(f"arch {arch!r} requires parameter {n!r}")
+
+
+def exit_forward(arch: str, params: dict, x: np.ndarray, eps: float) -> dict:
+    """Forward of one exit head up to the logits S = z W_out^T.
+
+    params (fp64 numpy): w_out [V,h]; norm/mlp: g_f [h];
+    mlp: g_a [h], w_gate [F,h], w_up [F,h], w_down [h,F].
+    """
+    if arch not in ARCHS:
+        raise ValueError(f"unknown arch {arch!r}")
+    _need(params, ["w_out"], arch)
+    act = {"x": x}
+    y = x
+    if arch == "mlp":
+        _need(params, ["g_a", "w_gate", "w_up", "w_down"], arch)
+        u, r_x, xhat = rmsnorm(x, params["g_a"], eps)       # pre-norm
+        A = u @ params["w_gate"].T
+        B = u @ params["w_up"].T
+        M = silu(A) * B                                     # SwiGLU (A2)
+        y = x + M @ params["w_down"].T                      # residual
+        act.update(u=u, r_x=r_x, xhat=xhat, A=A, B=B, M=M)
+    act["y"] = y
+    if arch in ("norm", "mlp"):
+        _need(params, ["g_f"], arch)
+        z, r_y, yhat = rmsnorm(y, params["g_f"], eps)       # Norm exit
+        act.update(r_y=r_y, yhat=yhat)
+    else:
+        z = y                                               # Embedding exit
+    act["z"] = z
+    act["S"] = z @ params["w_out"].T                        # output embedding
+    return act
+
+
+# ----------------------------------------------------------------------------
+# loss
+# ----------------------------------------------------------------------------
+
+def lm_loss_stats(S: np.ndarray, targets: np.ndarray) -> dict:
+    """Per-token softmax cross-entropy statistics from materialised logits.
+
+    m_t = max_v S_tv; lse_t = m_t + ln sum_v exp(S_tv - m_t);
+    loss_t = lse_t - S_{t,y_t} (0 where y_t = -1); conf_t = exp(m_t - lse_t)
+    (the maximum softmax probability); argmax_t = lowest v with S_tv = m_t (A9).
+    """
+    V = S.shape[1]
+    t = np.asarray(targets, dtype=np.int64)
+    if np.any((t < IGNORE_INDEX) | (t >= V)):
+        raise ValueError("target id out of range [-1, V)")
+    m = S.max(axis=1)
+    lse = m + np.log(np.sum(np.exp(S - m[:, None]), axis=1))
+    valid = t != IGNORE_INDEX
+    tl = np.where(valid, S[np.arange(S.shape[0]), np.where(valid, t, 0)], 0.0)
+    loss = np.where(valid, lse - tl, 0.0)
+    conf = np.exp(m - lse)
+    argmax = np.argmax(S, axis=1)  # numpy returns the first (lowest) index on ties
+    return dict(m=m, lse=lse, loss=loss, conf=conf, argmax=argmax.astype(np.int64),
+                valid=valid)
+
+
+# ----------------------------------------------------------------------------
+# one exit: loss and gradients (backprop into exit parameters only)
+# ----------------------------------------------------------------------------
+
+@dataclass
+class ExitResult:
+    loss: float                 # L_i = sum_t w_t loss_t / W  (A4; W global, A16)
+    grads: dict                 # same keys as the exit's parameters
+    stats: dict                 # per-token lse, loss, conf, argmax
+    act: dict = field(repr=False, default_factory=dict)
+
+
+def exit_loss_and_grads(arch: str, params: dict, x: np.ndarray, targets: np.ndarray,
+                        alpha: float, eps: float, valid_count: int | None = None,
+                        keep_act: bool = False) -> ExitResult:
+    """Loss and parameter gradients of one exit.
+
+    ``valid_count`` is W, the normaliser of the mean over valid tokens; it
+    defaults to the number of valid tokens in ``targets`` (single-GPU
+    semantics) and is the *global* count under data parallelism (A16).
+    The gradient is that of alpha * L_i (A5).
+    """
+    act = exit_forward(arch, params, x, eps)
+    st = lm_loss_stats(act["S"], targets)
+    w = st["valid"].astype(np.float64)
+    W = float(np.sum(w)) if valid_count is None else float(valid_count)
+    z = act["z"]
+    grads = {k: np.zeros_like(v) for k, v in params.items() if v is not None}
+    if W == 0.0:
+        return ExitResult(0.0, grads, st, act if keep_act else {})
+    loss = float(np.sum(w * st["loss"]) / W)
+
+    # dS_tv = alpha * w_t / W * (softmax(S_t)_v - 1[v = y_t])
+    P = np.exp(act["S"] - st["lse"][:, None])
+    onehot = np.zeros_like(P)
+    rows = np.nonzero(st["valid"])[0]
+    onehot[rows, np.asarray(targets)[rows]] = 1.0
+    dS = (alpha * w / W)[:, None] * (P - onehot)
+
+    grads["w_out"] = dS.T @ z                               # dW_out = dS^T z
+    if arch in ("norm", "mlp"):
+        dz = dS @ params["w_out"]                           # dz = dS W_out
+        dy, dg_f = rmsnorm_backward(dz, act["yhat"], act["r_y"], params["g_f"])
+        grads["g_f"] = dg_f
+        if arch == "mlp":
+            M, A, B, u = act["M"], act["A"], act["B"], act["u"]
+            grads["w_down"] = dy.T @ M                      # dW_down = dy^T M
+            dM = dy @ params["w_down"]
+            dA = dM * B * silu_grad(A)
+            dB = dM * silu(A)
+            grads["w_gate"] = dA.T @ u
+            grads["w_up"] = dB.T @ u
+            du = dA @ params["w_gate"] + dB @ params["w_up"]
+            # u = g_a * xhat  =>  dg_a = sum_t du_t * xhat_t; no dx (frozen backbone)
+            grads["g_a"] = np.sum(du * act["xhat"], axis=0)
+    return ExitResult(loss, grads, st, act if keep_act else {})
+
+
+def tune_step(arch: str, params_list, hidden_list, targets, exit_weights, eps: float,
+              valid_count: int | None = None):
+    """All exits of one step: exits are independent.
+
+    Returns (losses [E] (unweighted L_i), grads list, stats list).
+    """
+    E = len(params_list)
+    if len(hidden_list) != E or len(exit_weights) != E:
+        raise ValueError("params, hidden and exit_weights must have one entry per exit")
+    losses, grads, stats = [], [], []
+    for i in range(E):
+        r = exit_loss_and_grads(arch, params_list[i], hidden_list[i], targets,
+                                float(exit_weights[i]), eps, valid_count)
+        losses.append(r.loss)
+        grads.append(r.grads)
+        stats.append(r.stats)
+    return np.array(losses), grads, stats
+
+
+# ----------------------------------------------------------------------------
+# optimizer (state for exits only; Adam constants)
+# ----------------------------------------------------------------------------
+
+def adam_update(theta, grad, m, v, lr, beta1, beta2, eps, weight_decay, step,
+                grad_scale=1.0):
+    """Kingma & Ba Adam with bias correction, eps outside the sqrt (A14).
+
+    Returns new (theta, m, v).  ``step`` is the 1-based step count t.
+    """
+    g = grad_scale * grad
+    m = beta1 * m + (1.0 - beta1) * g
+    v = beta2 * v + (1.0 - beta2) * g * g
+    mhat = m / (1.0 - beta1 ** step)
+    vhat = v / (1.0 - beta2 ** step)
+    theta = theta - lr * mhat / (np.sqrt(vhat) + eps) - lr * weight_decay * theta
+    return theta, m, v
+
+
+def sgd_update(theta, grad, buf, lr, momentum, grad_scale=1.0):
+    """theta <- theta - lr * b with b = momentum * b + g (b = g when momentum is 0)."""
+    g = grad_scale * grad
+    buf = momentum * buf + g if buf is not None else g
+    return theta - lr * buf, buf
+
+
+def lr_at(it: int, total: int, warmup_frac: float = 0.01, lr_max: float = 1e-4,
+          lr_min: float = 1e-5) -> float:
+    """Linear warmup 0 -> lr_max over ceil(warmup_frac*total) iterations, then
+    linear decay to lr_min at ``total`` (ramp origin 0 is A14)."""
+    if total < 1 or it < 0 or it > total:
+        raise ValueError("iteration out of range")
+    w = int(math.ceil(warmup_frac * total))
+    if w > 0 and it <= w:
+        return lr_max * it / w
+    if total == w:
+        return lr_max
+    return lr_max - (lr_max - lr_min) * (it - w) / (total - w)
+
+
+def token_budget(batch: int = 16, seq: int = 2048, iters: int = 40000) -> int:
+    """16 x 2048 x 4e4 tokens."""
+    return batch * seq * iters
+
+
+# ----------------------------------------------------------------------------
+# Copy initialisation
+# ----------------------------------------------------------------------------
+
+def init_copy(arch: str, backbone: dict, after_layer: int) -> dict:
+    """Exit parameters copied from the backbone (deep copies).
+
+    backbone: ``final_norm`` [h], ``w_out`` [V,h], ``layers``: list of dicts with
+    ``mlp_norm`` [h] (pre-MLP norm gain), ``w_gate``, ``w_up``, ``w_down``.
+    Embedding/Norm copy the final-exit layer's modules; MLP copies the
+    MLP of the same layer plus its pre-MLP norm gain (A10).
+    """
+    if arch not in ARCHS:
+        raise ValueError(f"unknown arch {arch!r}")
+    if backbone.get("w_out") is None:
+        raise LookupError("structure error: backbone has no output embedding")
+    p = {"w_out": np.array(backbone["w_out"], copy=True)}
+    if arch in ("norm", "mlp"):
+        if backbone.get("final_norm") is None:
+            raise LookupError("structure error: backbone has no final norm")
+        p["g_f"] = np.array(backbone["final_norm"], copy=True)
+    if arch == "mlp":
+        layers = backbone.get("layers") or []
+        if not (1 <= after_layer <= len(layers)):
+            raise LookupError("structure error: no backbone layer to copy the MLP from")
+        L = layers[after_layer - 1]
+        for k_exit, k_bb in (("g_a", "mlp_norm"), ("w_gate", "w_gate"),
+                             ("w_up", "w_up"), ("w_down", "w_down")):
+            if L.get(k_bb) is None:
+                raise LookupError(f"structure error: layer {after_layer} has no {k_bb}")
+            p[k_exit] = np.array(L[k_bb], copy=True)
+    return p
+
+
+def original_final_logits(backbone: dict, h_last: np.ndarray, eps: float) -> np.ndarray:
+    """The original LLM's output layer on the last hidden state: final norm then
+    output embedding ("optional layer normalization module, followed by a
+    large output embedding matrix")."""
+    g = backbone["final_norm"]
+    r = 1.0 / np.sqrt(np.mean(h_last * h_last, axis=-1) + eps)
+    return (g[None, :] * (h_last * r[:, None])) @ backbone["w_out"].T

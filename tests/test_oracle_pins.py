@@ -1,0 +1,350 @@
+"""Pins for the fp64 oracle against what the paper and the mathematics fix.
+
+Each test names the pin (P1..P14 in DESIGN.md §5) and the passage it follows.
+None of these compares the oracle with itself: the references are hand-derived
+worked examples (tests/golden), closed forms, invariants, library routines
+(torch.nn.functional in fp64, scipy.special.logsumexp, torch.autograd) and
+central finite differences.
+"""
+
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as Fn
+from scipy.special import logsumexp, softmax
+
+from oracle import ee_oracle as O
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")
+
+
+def _rng(seed):
+    return np.random.default_rng(seed)
+
+
+def _params(arch, h, V, F, rng, w_std=0.5):
+    p = {"w_out": rng.normal(0, w_std, (V, h))}
+    if arch in ("norm", "mlp"):
+        p["g_f"] = 1.0 + 0.1 * rng.normal(size=h)
+    if arch == "mlp":
+        p["g_a"] = 1.0 + 0.1 * rng.normal(size=h)
+        p["w_gate"] = rng.normal(0, w_std, (F, h))
+        p["w_up"] = rng.normal(0, w_std, (F, h))
+        p["w_down"] = rng.normal(0, w_std, (h, F))
+    return p
+
+
+# --------------------------------------------------------------------------- P1, P2
+def test_P1_worked_example_embedding():
+    g = json.load(open(GOLDEN))["P1_embedding"]
+    p = {"w_out": np.array(g["w_out"])}
+    r = O.exit_loss_and_grads("embedding", p, np.array(g["z"]), np.array(g["target"]), 1.0, 0.0,
+                              keep_act=True)
+    assert r.stats["lse"][0] == pytest.approx(g["lse"], rel=1e-14)
+    assert r.loss == pytest.approx(g["loss"], rel=1e-13)
+    assert r.stats["conf"][0] == pytest.approx(g["conf"], rel=1e-13)
+    assert r.stats["argmax"][0] == g["argmax"]
+    np.testing.assert_allclose(r.grads["w_out"], np.array(g["dW_out"]), rtol=1e-13)
+    # dz is not a parameter gradient of an Embedding exit; check it via the Norm path
+    # identity dz = dS W_out using the golden dS.
+    np.testing.assert_allclose(np.array(g["dS"]) @ p["w_out"], np.array(g["dz"]), rtol=1e-12)
+
+
+def test_P2_worked_example_norm_and_scale_invariance():
+    g = json.load(open(GOLDEN))["P2_norm"]
+    p = {"w_out": np.array(g["w_out"]), "g_f": np.array(g["g_f"])}
+    x = np.array(g["x"])
+    r = O.exit_loss_and_grads("norm", p, x, np.array(g["target"]), 1.0, g["eps"], keep_act=True)
+    assert r.act["r_y"][0] == pytest.approx(g["r"], rel=1e-14)
+    np.testing.assert_allclose(r.act["yhat"][0], g["yhat"], rtol=1e-14)
+    assert r.stats["lse"][0] == pytest.approx(g["lse"], rel=1e-14)
+    assert r.loss == pytest.approx(g["loss"], rel=1e-13)
+    np.testing.assert_allclose(r.grads["g_f"], g["dg_f"], rtol=1e-12)
+    # P5: at eps = 0 RMSNorm is scale invariant, so x . dx = 0 for any cotangent.
+    dz = np.array([[0.3, -1.7]])
+    dx, _ = O.rmsnorm_backward(dz, r.act["yhat"], r.act["r_y"], p["g_f"])
+    assert abs(float(np.sum(x * dx))) < 1e-14
+
+
+# --------------------------------------------------------------------------- P3
+@pytest.mark.parametrize("arch", O.ARCHS)
+def test_P3_uniform_logits_closed_form(arch):
+    rng = _rng(3)
+    h, V, F, N = 8, 512, 12, 16
+    p = _params(arch, h, V, F, rng)
+    p["w_out"][:] = 0.0
+    x = rng.normal(size=(N, h))
+    y = rng.integers(0, V, N)
+    y[3] = -1
+    alpha = 0.7
+    r = O.exit_loss_and_grads(arch, p, x, y, alpha, 1e-5, keep_act=True)
+    assert r.loss == pytest.approx(math.log(512), rel=1e-15)       # ln V
+    assert math.log(512) == pytest.approx(6.238324625039508, rel=1e-15)
+    np.testing.assert_allclose(r.stats["conf"], 1.0 / V, rtol=1e-14)
+    # dW_out[v] = alpha/W sum_t w_t (1/V - 1[y_t = v]) z_t
+    w = (y != -1).astype(float)
+    W = w.sum()
+    onehot = np.zeros((N, V))
+    onehot[np.nonzero(w)[0], y[w > 0]] = 1
+    expect = alpha / W * ((w[:, None] * (1.0 / V - onehot)).T @ r.act["z"])
+    np.testing.assert_allclose(r.grads["w_out"], expect, rtol=1e-12, atol=1e-15)
+    # dz = dS W_out = 0 exactly, so every gradient below W_out is exactly zero.
+    for k in ("g_f", "g_a", "w_gate", "w_up", "w_down"):
+        if k in r.grads:
+            assert np.all(r.grads[k] == 0.0), k
+
+
+def test_P3_uniform_logits_vocab_32000():
+    p = {"w_out": np.zeros((32000, 8))}
+    x = _rng(0).normal(size=(3, 8))
+    r = O.exit_loss_and_grads("embedding", p, x, np.array([0, 31999, 5]), 1.0, 0.0)
+    assert r.loss == pytest.approx(10.373491181781864, rel=1e-15)   # ln 32000
+
+
+# --------------------------------------------------------------------------- P4
+@pytest.mark.parametrize("arch", O.ARCHS)
+def test_P4_softmax_ce_gradient_rows_sum_to_zero(arch):
+    rng = _rng(4)
+    h, V, F, N = 16, 40, 24, 32
+    p = _params(arch, h, V, F, rng)
+    x = rng.normal(size=(N, h))
+    y = rng.integers(0, V, N)
+    r = O.exit_loss_and_grads(arch, p, x, y, 1.3, 1e-5)
+    col = r.grads["w_out"].sum(axis=0)
+    assert np.max(np.abs(col)) <= 1e-13 * np.max(np.abs(r.grads["w_out"])) * V
+
+
+# --------------------------------------------------------------------------- P5
+def test_P5_rmsnorm_scale_invariance_and_textbook():
+    rng = _rng(5)
+    x = rng.normal(size=(7, 33))
+    g = 1 + 0.1 * rng.normal(size=33)
+    a, _, _ = O.rmsnorm(x, g, 0.0)
+    b, _, _ = O.rmsnorm(3.7 * x, g, 0.0)
+    np.testing.assert_allclose(a, b, rtol=1e-14)
+    # library routine: torch.nn.functional.rms_norm in fp64
+    ref = Fn.rms_norm(torch.from_numpy(x), (33,), torch.from_numpy(g), eps=1e-5).numpy()
+    np.testing.assert_allclose(O.rmsnorm(x, g, 1e-5)[0], ref, rtol=1e-13)
+
+
+# --------------------------------------------------------------------------- P6
+@pytest.mark.parametrize("arch", O.ARCHS)
+def test_P6_central_finite_differences(arch):
+    """Every parameter tensor of every architecture; fp64, step 1e-6."""
+    rng = _rng(6)
+    h, V, F, N = 8, 16, 12, 4
+    p = _params(arch, h, V, F, rng)
+    x = rng.normal(size=(N, h))
+    y = np.array([3, -1, 15, 0])
+    alpha, eps = 0.8, 1e-5
+    r = O.exit_loss_and_grads(arch, p, x, y, alpha, eps)
+
+    def f(pp):
+        return alpha * O.exit_loss_and_grads(arch, pp, x, y, alpha, eps).loss
+
+    step = 1e-6
+    for name, val in p.items():
+        num = np.zeros_like(val)
+        it = np.nditer(val, flags=["multi_index"])
+        for _ in it:
+            idx = it.multi_index
+            q = {k: v.copy() for k, v in p.items()}
+            q[name][idx] += step
+            fp = f(q)
+            q[name][idx] -= 2 * step
+            fm = f(q)
+            num[idx] = (fp - fm) / (2 * step)
+        err = np.linalg.norm(num - r.grads[name]) / max(np.linalg.norm(r.grads[name]), 1e-30)
+        assert err <= 1e-6, (arch, name, err)
+
+
+# --------------------------------------------------------------------------- P7
+def test_P7_copy_init_reproduces_original_head_bitwise():
+    """A Norm exit at the last layer, copy-initialised, gives exactly the
+    original model's logits and loss."""
+    rng = _rng(7)
+    h, V, N = 64, 512, 32
+    bb = {"final_norm": 1 + 0.1 * rng.normal(size=h), "w_out": rng.normal(0, h ** -0.5, (V, h)),
+          "layers": []}
+    h_last = rng.normal(size=(N, h))
+    p = O.init_copy("norm", bb, after_layer=2)
+    assert np.array_equal(p["w_out"], bb["w_out"]) and np.array_equal(p["g_f"], bb["final_norm"])
+    assert not np.shares_memory(p["w_out"], bb["w_out"])               # deep copy
+    S_exit = O.exit_forward("norm", p, h_last, 1e-5)["S"]
+    S_orig = O.original_final_logits(bb, h_last, 1e-5)
+    assert np.array_equal(S_exit, S_orig)
+    y = rng.integers(0, V, N)
+    l_exit = O.lm_loss_stats(S_exit, y)["loss"].mean()
+    l_orig = np.mean(logsumexp(S_orig, axis=1) - S_orig[np.arange(N), y])
+    assert l_exit == pytest.approx(l_orig, rel=1e-14)
+    p["w_out"][0, 0] += 1.0                                           # mutate exit ...
+    assert p["w_out"][0, 0] != bb["w_out"][0, 0]                      # ... source untouched
+
+
+def test_P7_copy_init_mlp_structure():
+    rng = _rng(8)
+    h, V, F = 8, 16, 12
+    layers = [{"mlp_norm": rng.normal(size=h), "w_gate": rng.normal(size=(F, h)),
+               "w_up": rng.normal(size=(F, h)), "w_down": rng.normal(size=(h, F))} for _ in range(3)]
+    bb = {"final_norm": rng.normal(size=h), "w_out": rng.normal(size=(V, h)), "layers": layers}
+    p = O.init_copy("mlp", bb, after_layer=2)
+    assert np.array_equal(p["w_gate"], layers[1]["w_gate"])
+    assert np.array_equal(p["g_a"], layers[1]["mlp_norm"])
+    assert np.array_equal(p["w_down"], layers[1]["w_down"])
+    pe = O.init_copy("embedding", bb, after_layer=2)
+    assert set(pe) == {"w_out"}
+    with pytest.raises(LookupError):
+        O.init_copy("mlp", bb, after_layer=4)
+    with pytest.raises(LookupError):
+        O.init_copy("norm", {"w_out": bb["w_out"], "final_norm": None}, after_layer=1)
+
+
+# --------------------------------------------------------------------------- P8, P9
+def test_P8_two_class_softplus():
+    rng = _rng(9)
+    S = rng.normal(size=(10, 2)) * 3
+    y = rng.integers(0, 2, 10)
+    st = O.lm_loss_stats(S, y)
+    other = S[np.arange(10), 1 - y]
+    np.testing.assert_allclose(st["loss"], np.logaddexp(0.0, other - S[np.arange(10), y]), rtol=1e-10,
+                               atol=1e-15)
+
+
+@pytest.mark.parametrize("arch", O.ARCHS)
+def test_P8_P9_against_torch_library_and_autograd(arch):
+    """Forward via torch.nn.functional library routines (rms_norm, silu,
+    linear, cross_entropy with ignore_index) in fp64; gradients via autograd."""
+    rng = _rng(10)
+    h, V, F, N = 24, 50, 40, 30
+    p = _params(arch, h, V, F, rng, w_std=0.3)
+    x = rng.normal(size=(N, h))
+    y = rng.integers(0, V, N)
+    y[[2, 11]] = -1
+    alpha, eps = 1.7, 1e-5
+    r = O.exit_loss_and_grads(arch, p, x, y, alpha, eps, keep_act=True)
+
+    tp = {k: torch.tensor(v, requires_grad=True) for k, v in p.items()}
+    tx = torch.tensor(x)
+    t = tx
+    if arch == "mlp":
+        u = Fn.rms_norm(tx, (h,), tp["g_a"], eps)
+        m = Fn.silu(Fn.linear(u, tp["w_gate"])) * Fn.linear(u, tp["w_up"])
+        t = tx + Fn.linear(m, tp["w_down"])
+    if arch in ("norm", "mlp"):
+        t = Fn.rms_norm(t, (h,), tp["g_f"], eps)
+    logits = Fn.linear(t, tp["w_out"])
+    loss = Fn.cross_entropy(logits, torch.tensor(y, dtype=torch.long), ignore_index=-1)
+    (alpha * loss).backward()
+    assert r.loss == pytest.approx(loss.item(), rel=1e-12)
+    np.testing.assert_allclose(r.stats["lse"], logsumexp(r.act["S"], axis=1), rtol=1e-13)
+    np.testing.assert_allclose(r.stats["conf"], softmax(r.act["S"], axis=1).max(axis=1), rtol=1e-12)
+    for k in p:
+        np.testing.assert_allclose(r.grads[k], tp[k].grad.numpy(), rtol=1e-10, atol=1e-14,
+                                   err_msg=f"{arch}:{k}")
+
+
+# --------------------------------------------------------------------------- P10, P11
+@pytest.mark.parametrize("arch", ("norm", "mlp"))
+def test_P10_data_parallel_sharding_linearity(arch):
+    """With the global valid count W, gradients over token shards sum to the
+    full-batch gradient and losses sum to the full mean (A16)."""
+    rng = _rng(11)
+    h, V, F, N = 12, 30, 20, 40
+    p = _params(arch, h, V, F, rng)
+    x = rng.normal(size=(N, h))
+    y = rng.integers(0, V, N)
+    y[[0, 7, 33]] = -1
+    full = O.exit_loss_and_grads(arch, p, x, y, 0.9, 1e-5)
+    W = int(np.sum(y != -1))
+    shards = [O.exit_loss_and_grads(arch, p, x[s], y[s], 0.9, 1e-5, valid_count=W)
+              for s in (slice(0, 13), slice(13, 29), slice(29, 40))]
+    assert sum(s.loss for s in shards) == pytest.approx(full.loss, rel=1e-13)
+    for k in p:
+        np.testing.assert_allclose(sum(s.grads[k] for s in shards), full.grads[k], rtol=1e-11,
+                                   atol=1e-15)
+
+
+def test_P11_exit_independence():
+    rng = _rng(12)
+    h, V, F, N = 8, 20, 10, 12
+    pa, pb = _params("mlp", h, V, F, rng), _params("mlp", h, V, F, rng)
+    xa, xb = rng.normal(size=(N, h)), rng.normal(size=(N, h))
+    y = rng.integers(0, V, N)
+    la, ga, _ = O.tune_step("mlp", [pa], [xa], y, [1.0], 1e-5)
+    lab, gab, _ = O.tune_step("mlp", [pa, pb], [xa, xb], y, [1.0, 0.5], 1e-5)
+    assert la[0] == lab[0]
+    for k in pa:
+        assert np.array_equal(ga[0][k], gab[0][k])
+
+
+# --------------------------------------------------------------------------- P12, P13
+def test_P12_degenerate_weights():
+    rng = _rng(13)
+    h, V, F, N = 8, 20, 10, 12
+    p = _params("mlp", h, V, F, rng)
+    x = rng.normal(size=(N, h))
+    y = rng.integers(0, V, N)
+    r = O.exit_loss_and_grads("mlp", p, x, y, 0.0, 1e-5)               # alpha = 0
+    assert r.loss > 0
+    for k, g in r.grads.items():
+        assert np.all(g == 0.0), k
+    m = np.zeros_like(p["w_out"])
+    th, _, _ = O.adam_update(p["w_out"], r.grads["w_out"], m, m.copy(), 1e-4, 0.9, 0.95, 1e-5, 0.0, 1)
+    assert np.array_equal(th, p["w_out"])                              # params bitwise unchanged
+    r2 = O.exit_loss_and_grads("mlp", p, x, np.full(N, -1), 1.0, 1e-5)  # all ignored
+    assert r2.loss == 0.0
+    for g in r2.grads.values():
+        assert np.all(g == 0.0)
+
+
+def test_P13_adam_first_step_closed_form():
+    rng = _rng(14)
+    th = rng.normal(size=1000)
+    g = rng.normal(size=1000) * 10 ** rng.uniform(-6, 1, 1000)
+    lr, eps = 1e-4, 1e-5
+    new, m, v = O.adam_update(th, g, np.zeros(1000), np.zeros(1000), lr, 0.9, 0.95, eps, 0.0, 1)
+    np.testing.assert_allclose(new, th - lr * g / (np.abs(g) + eps), rtol=1e-12, atol=1e-18)
+    np.testing.assert_allclose(m, 0.1 * g, rtol=1e-15)
+    np.testing.assert_allclose(v, 0.05 * g * g, rtol=1e-14)
+    # weight decay adds -lr*wd*theta
+    new2, _, _ = O.adam_update(th, g, np.zeros(1000), np.zeros(1000), lr, 0.9, 0.95, eps, 0.01, 1)
+    np.testing.assert_allclose(new2 - new, -lr * 0.01 * th, rtol=1e-9, atol=1e-20)
+    # SGD
+    s, _ = O.sgd_update(th, g, None, 0.5, 0.0)
+    np.testing.assert_allclose(s, th - 0.5 * g, rtol=1e-15)
+
+
+# --------------------------------------------------------------------------- P14
+def test_P14_lr_schedule_and_token_budget():
+    T = 40000
+    w = math.ceil(0.01 * T)
+    assert O.lr_at(w, T) == pytest.approx(1e-4, rel=1e-15)             # "maximum ... 10^-4"
+    assert O.lr_at(T, T) == pytest.approx(1e-5, rel=1e-15)             # "minimum of 10^-5"
+    assert O.lr_at(0, T) == 0.0
+    assert O.lr_at(w // 2, T) == pytest.approx(0.5e-4, rel=1e-15)
+    assert O.lr_at((w + T) // 2, T) == pytest.approx(0.55e-4, rel=1e-12)
+    with pytest.raises(ValueError):
+        O.lr_at(T + 1, T)
+    assert O.token_budget() == 1_310_720_000
+
+
+# --------------------------------------------------------------------------- A6, A9
+def test_targets_out_of_range_and_argmax_ties():
+    S = np.array([[1.0, 3.0, 3.0, 0.0], [2.0, 2.0, 2.0, 2.0]])
+    st = O.lm_loss_stats(S, np.array([1, -1]))
+    assert list(st["argmax"]) == [1, 0]                                # lowest index on ties
+    assert st["loss"][1] == 0.0
+    with pytest.raises(ValueError):
+        O.lm_loss_stats(S, np.array([4, 0]))
+    with pytest.raises(ValueError):
+        O.lm_loss_stats(S, np.array([-2, 0]))
+
+
+def test_bf16_widening_is_exact():
+    t = torch.randn(1000).to(torch.bfloat16)
+    bits = t.view(torch.int16).numpy().view(np.uint16)
+    np.testing.assert_array_equal(O.bf16_bits_to_f64(bits), t.to(torch.float64).numpy())
