@@ -1,0 +1,218 @@
+/*
+ * ee.h -- C-ABI of the B200-native EE-Tuning exit-head library (libee_b200.so).
+ *
+ * EE-Tuning (arXiv 2402.00518) tunes early-exit heads attached to a frozen
+ * LLM.  This library implements the data-parallel hot path of its Stage 2
+ * (§2.2) -- for every exit i: apply the exit head to the
+ * cached hidden states h_i, compute the token-level softmax cross-entropy,
+ * backpropagate into the exit-head parameters only -- plus the Stage-1
+ * initialisers (Copy / Random) and the optimizer (Adam).
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Ownership: the caller owns every buffer.  The library never allocates
+ *    device memory in these calls; scratch comes from a caller-provided
+ *    workspace sized by ee_workspace_size().
+ *  - Pointers: "device" pointers must be CUDA device (or managed) memory of the
+ *    current device; "host" pointers are ordinary host memory.  Device base
+ *    pointers must be 16-byte aligned (EE_ERR_ALIGN otherwise).
+ *  - Layout: row-major, C-contiguous.  bf16 = IEEE bfloat16 (uint16 storage).
+ *  - Asynchrony: everything is enqueued on `stream` (a cudaStream_t passed as
+ *    void*; NULL = legacy default stream).  No call synchronises the host
+ *    except ee_get_status().  Argument/shape errors are returned synchronously
+ *    and nothing is enqueued; errors only the device can see (target ids out
+ *    of range, non-finite losses) are recorded in a status word inside the
+ *    workspace and read with ee_get_status().
+ *  - Thread safety: calls are re-entrant; ee_last_error() is thread-local.
+ *  - Requires an sm_100a GPU (B200); on anything else ee_tune_step returns
+ *    EE_ERR_UNSUPPORTED.  There is no CPU fallback.
+ */
+#ifndef EE_B200_H
+#define EE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  EE_OK = 0,
+  EE_ERR_ARG = 1,         /* NULL pointer / invalid enum / negative size          */
+  EE_ERR_SHAPE = 2,       /* dimensions unsupported (see ee_head_config)          */
+  EE_ERR_ALIGN = 3,       /* base pointer not 16-byte aligned                     */
+  EE_ERR_VOCAB = 4,       /* target id outside [-1, V) (device-detected)          */
+  EE_ERR_ARCH = 5,        /* tensors present/absent do not match the arch         */
+  EE_ERR_STRUCTURE = 6,   /* Copy init: a source module is missing        */
+  EE_ERR_DIVERGED = 7,    /* non-finite loss (device-detected, carries exit idx)  */
+  EE_ERR_WORKSPACE = 8,   /* workspace NULL or smaller than ee_workspace_size()   */
+  EE_ERR_CUDA = 9,        /* a CUDA runtime/driver call failed                    */
+  EE_ERR_NCCL = 10,       /* reserved for the in-library collectives              */
+  EE_ERR_UNSUPPORTED = 11 /* no sm_100 device                                     */
+} ee_status;
+
+/* Exit architectures (§2.1 "Architectures of early exits").
+ * EMBEDDING: logits = x W_out^T
+ * NORM:      logits = RMSNorm_f(x) W_out^T
+ * MLP:       y = x + W_down(silu(W_gate u) * W_up u), u = RMSNorm_a(x);
+ *            logits = RMSNorm_f(y) W_out^T   (pre-norm residual P:165-166;
+ *            SwiGLU as in the Llama-2 backbone, reading A2)
+ * The `Layer` architecture is not implemented. */
+typedef enum { EE_ARCH_EMBEDDING = 0, EE_ARCH_NORM = 1, EE_ARCH_MLP = 2 } ee_arch;
+
+/* Initialisation of exit parameters. */
+typedef enum { EE_INIT_COPY = 0, EE_INIT_RANDOM = 1 } ee_init;
+
+/* Element type of Copy-init source tensors. */
+typedef enum { EE_DTYPE_BF16 = 0, EE_DTYPE_F32 = 1 } ee_dtype;
+
+/* Shapes of one homogeneous set of exits (all exits share arch and sizes).
+ *  hidden       h; multiple of 64, 64 <= h <= 8192.
+ *  vocab        V (full vocabulary; targets are ids in [0, V)).
+ *  ffn          F, MLP width; multiple of 128 for EE_ARCH_MLP, else ignored.
+ *  num_exits    E >= 1.
+ *  arch         ee_arch.
+ *  norm_eps     RMSNorm epsilon (A3: 1e-5).
+ *  vocab_begin, vocab_end
+ *               the rows [vocab_begin, vocab_end) of W_out held by this call
+ *               (vocab-parallel shard).  Only the unsharded case
+ *               vocab_begin = 0, vocab_end = V is implemented in this round;
+ *               anything else returns EE_ERR_UNSUPPORTED.  (vocab_end -
+ *               vocab_begin) must be a multiple of 8. */
+typedef struct {
+  int32_t hidden, vocab, ffn, num_exits;
+  int32_t arch;
+  float norm_eps;
+  int32_t vocab_begin, vocab_end;
+} ee_head_config;
+
+/* Parameters (or gradients, or optimizer moments) of ONE exit.  Device
+ * pointers, NULL when the arch has no such tensor.
+ *   g_a    [h]     pre-MLP RMSNorm gain       (MLP)
+ *   w_gate [F x h] SwiGLU gate projection     (MLP)
+ *   w_up   [F x h] SwiGLU up projection       (MLP)
+ *   w_down [h x F] down projection            (MLP)
+ *   g_f    [h]     final RMSNorm gain         (NORM, MLP)
+ *   w_out  [Vl x h] output embedding, Vl = vocab_end - vocab_begin (all archs);
+ *                  the paper's "h x V" matrix stored transposed (A7).
+ * Element types depend on the role of the struct:
+ *   "operand" params: matrices bf16, gains fp32;
+ *   master params, grads, Adam m/v: everything fp32. */
+typedef struct {
+  void *g_a, *w_gate, *w_up, *w_down, *g_f, *w_out;
+} ee_head_tensors;
+
+/* Optional per-token outputs of one exit (device, [n_tokens] each; any may be
+ * NULL).  lse = log-sum-exp of the logits; loss_tok = lse - logit[target]
+ * (0 for ignored tokens); argmax = lowest index of the max logit (A9);
+ * conf = max softmax probability = 1/sum exp(S - max). */
+typedef struct {
+  float* lse;
+  float* loss_tok;
+  int32_t* argmax;
+  float* conf;
+} ee_step_aux;
+
+/* Bytes of workspace ee_tune_step needs for n_tokens tokens with this config.
+ * The same workspace may be reused by consecutive calls on the same stream. */
+ee_status ee_workspace_size(const ee_head_config* cfg, int64_t n_tokens, size_t* bytes);
+
+/* Stage-1 initialisation of all E exits.
+ *   init = EE_INIT_COPY: copy_src[i] holds the backbone modules exit i copies
+ *     (element type src_dtype, device): Embedding/Norm -> the final-exit
+ *     layer's W_out (and final norm gain g_f); MLP -> the MLP of the
+ *     layer the exit is attached to, and that layer's pre-MLP norm gain as g_a
+ *     (A10), plus the final g_f and W_out.  A NULL source tensor that
+ *     the arch needs -> EE_ERR_STRUCTURE.  Copies are deep.
+ *   init = EE_INIT_RANDOM: matrices ~ N(0, std^2) from a counter-based Philox
+ *     stream keyed by (seed, exit, tensor); gains = 1 (A12).
+ *     copy_src may be NULL.
+ *   master_fp32[i]: fp32 master parameters (written).
+ *   operand_bf16[i]: bf16 operand copies of the matrices (written); its gain
+ *     pointers are fp32 and written too unless they alias the master gains. */
+ee_status ee_init_heads(const ee_head_config* cfg, int32_t init, const ee_head_tensors* copy_src,
+                        int32_t src_dtype, uint64_t seed, float std,
+                        ee_head_tensors* master_fp32, ee_head_tensors* operand_bf16, void* stream);
+
+/* One EE-Tuning step over all exits: per exit i, forward of the
+ * exit head on hidden[i], softmax cross-entropy against `targets`, and the
+ * gradient of exit_weights[i] * L_i w.r.t. the exit's parameters only (the
+ * backbone is frozen: no gradient w.r.t. hidden).  Exits are
+ * independent.
+ *   hidden[i]      device bf16 [n_tokens x h], read-only.
+ *   n_tokens       tokens on this rank (N = batch * seq flattened), >= 0.
+ *   targets        device int32 [n_tokens], next-token ids; -1 = ignore.
+ *   exit_weights   host float [E], alpha_i (A5).
+ *   params[i]      operand parameters (matrices bf16, gains fp32), read-only.
+ *   grads[i]       fp32 gradients, written (accumulate = 0) or added to (1).
+ *   loss_out       device float [E]: sum_t w_t loss_t / W (unweighted by
+ *                  alpha), i.e. the mean loss over valid tokens on one GPU.
+ *   aux            NULL or host array of E ee_step_aux (device buffers).
+ *   valid_count    NULL, or device int64 [1] holding W, the GLOBAL number of
+ *                  valid tokens (data parallelism, A16).  NULL = count the
+ *                  local targets.
+ *   workspace      device scratch of ws_bytes >= ee_workspace_size().
+ * Device-detected errors: a target outside [-1, V) -> EE_ERR_VOCAB; a
+ * non-finite loss -> EE_ERR_DIVERGED with the exit index (ee_get_status). */
+ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int64_t n_tokens,
+                       const int32_t* targets, const float* exit_weights,
+                       const ee_head_tensors* params, ee_head_tensors* grads, int32_t accumulate,
+                       float* loss_out, const ee_step_aux* aux, const int64_t* valid_count,
+                       void* workspace, size_t ws_bytes, void* stream);
+
+/* Number of valid targets (!= -1) -> device int64 out[0]; flags ids outside
+ * [-1, V) in the workspace status word.  Used to form the global W under
+ * data parallelism (the caller all-reduces out). */
+ee_status ee_count_valid(const int32_t* targets, int64_t n_tokens, int32_t vocab, int64_t* out,
+                         void* workspace, size_t ws_bytes, void* stream);
+
+/* Adam (Kingma bias correction, eps outside the sqrt, A14) on every
+ * tensor present in master[i], for all E exits, elementwise:
+ *   g = grad_scale*grad; m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2;
+ *   theta -= lr * (m/(1-b1^t)) / (sqrt(v/(1-b2^t)) + eps) + lr*wd*theta;
+ * then operand[i] <- bf16(theta) for matrices (and fp32 gains unless aliased).
+ * step = t >= 1.  master, m, v updated in place. */
+ee_status ee_adam_update(const ee_head_config* cfg, ee_head_tensors* master,
+                         ee_head_tensors* operand_bf16, const ee_head_tensors* grads,
+                         ee_head_tensors* m, ee_head_tensors* v, float lr, float beta1,
+                         float beta2, float eps, float weight_decay, int64_t step,
+                         float grad_scale, void* stream);
+
+/* SGD: buf = momentum*buf + g (buf may be NULL iff momentum == 0);
+ * theta -= lr * buf; operand refreshed as for Adam. */
+ee_status ee_sgd_update(const ee_head_config* cfg, ee_head_tensors* master,
+                        ee_head_tensors* operand_bf16, const ee_head_tensors* grads,
+                        ee_head_tensors* momentum_buf, float lr, float momentum,
+                        float grad_scale, void* stream);
+
+/* Reads (and clears) the device status word in `workspace`; synchronises the
+ * stream.  code = EE_OK or the first device error; exit_index = the exit it
+ * concerns (-1 if none). */
+ee_status ee_get_status(void* workspace, void* stream, int32_t* code, int32_t* exit_index);
+
+/* Learning rate at iteration `iter` of `total` (A14): linear ramp
+ * 0 -> lr_max over ceil(warmup_frac*total) iterations, then linear decay to
+ * lr_min at `total`.  Pure host function; returns NaN if iter is outside
+ * [0, total]. */
+double ee_lr_at(int64_t iter, int64_t total, double warmup_frac, double lr_max, double lr_min);
+
+/* Thread-local description of the last non-OK status returned on this thread. */
+const char* ee_last_error(void);
+
+/* Library version string. */
+const char* ee_version(void);
+
+/* ---- testing hook (used by the GPU parity tests; not part of the step) ----
+ * C[M x N] (fp32 row-major, device) = A B^T  (or += if accumulate), where the
+ * bf16 device operands are stored A: [M x K] if a_kmajor else [K x M];
+ * B: [N x K] if b_kmajor else [K x N].  Runs the same tcgen05 kernel as the
+ * step's plain-fp32 GEMMs.  K, and M (N) when MN-major, must be multiples of
+ * 8; N a multiple of 4. */
+ee_status ee_test_gemm(int32_t a_kmajor, int32_t b_kmajor, const void* A, const void* B, float* C,
+                       int32_t M, int32_t N, int32_t K, int32_t accumulate, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EE_B200_H */

@@ -1,0 +1,289 @@
+"""Python binding of libee_b200.so (include/ee.h) -- argument marshalling only.
+
+Every step of the EE-Tuning exit-head path runs in the CUDA library; this
+module converts torch tensors to device pointers, calls the C-ABI functions of
+the same names, and raises on a non-OK status.  PyTorch is used for device
+memory and streams only.  There is no CPU fallback: if the library or an sm_100
+GPU is missing, the calls raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libee_b200.so")
+
+EE_OK = 0
+STATUS_NAMES = {0: "EE_OK", 1: "EE_ERR_ARG", 2: "EE_ERR_SHAPE", 3: "EE_ERR_ALIGN",
+                4: "EE_ERR_VOCAB", 5: "EE_ERR_ARCH", 6: "EE_ERR_STRUCTURE",
+                7: "EE_ERR_DIVERGED", 8: "EE_ERR_WORKSPACE", 9: "EE_ERR_CUDA",
+                10: "EE_ERR_NCCL", 11: "EE_ERR_UNSUPPORTED"}
+ARCH = {"embedding": 0, "norm": 1, "mlp": 2}
+INIT = {"copy": 0, "random": 1}
+DTYPE = {torch.bfloat16: 0, torch.float32: 1}
+TENSOR_NAMES = ("g_a", "w_gate", "w_up", "w_down", "g_f", "w_out")
+EXPORTED = ("ee_workspace_size", "ee_init_heads", "ee_tune_step", "ee_count_valid",
+            "ee_adam_update", "ee_sgd_update", "ee_get_status", "ee_lr_at", "ee_last_error",
+            "ee_version", "ee_test_gemm")
+
+
+class EEError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class ee_head_config(ctypes.Structure):
+    _fields_ = [("hidden", ctypes.c_int32), ("vocab", ctypes.c_int32), ("ffn", ctypes.c_int32),
+                ("num_exits", ctypes.c_int32), ("arch", ctypes.c_int32),
+                ("norm_eps", ctypes.c_float), ("vocab_begin", ctypes.c_int32),
+                ("vocab_end", ctypes.c_int32)]
+
+
+class ee_head_tensors(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in TENSOR_NAMES]
+
+
+class ee_step_aux(ctypes.Structure):
+    _fields_ = [("lse", ctypes.c_void_p), ("loss_tok", ctypes.c_void_p),
+                ("argmax", ctypes.c_void_p), ("conf", ctypes.c_void_p)]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load the CUDA library (raises if it is missing: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built; run `python -m paper_2402_00518_b200.build` "
+                          "or __graft_entry__.build()")
+    lib = ctypes.CDLL(path)
+    P, I32, I64, F32, SZ = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float,
+                            ctypes.c_size_t)
+    CFG = ctypes.POINTER(ee_head_config)
+    HT = ctypes.POINTER(ee_head_tensors)
+    sig = {
+        "ee_workspace_size": (I32, [CFG, I64, ctypes.POINTER(SZ)]),
+        "ee_init_heads": (I32, [CFG, I32, HT, I32, ctypes.c_uint64, F32, HT, HT, P]),
+        "ee_tune_step": (I32, [CFG, ctypes.POINTER(P), I64, P, ctypes.POINTER(F32), HT, HT, I32,
+                               P, ctypes.POINTER(ee_step_aux), P, P, SZ, P]),
+        "ee_count_valid": (I32, [P, I64, I32, P, P, SZ, P]),
+        "ee_adam_update": (I32, [CFG, HT, HT, HT, HT, HT, F32, F32, F32, F32, F32, I64, F32, P]),
+        "ee_sgd_update": (I32, [CFG, HT, HT, HT, HT, F32, F32, F32, P]),
+        "ee_get_status": (I32, [P, P, ctypes.POINTER(I32), ctypes.POINTER(I32)]),
+        "ee_lr_at": (ctypes.c_double, [I64, I64, ctypes.c_double, ctypes.c_double,
+                                       ctypes.c_double]),
+        "ee_last_error": (ctypes.c_char_p, []),
+        "ee_version": (ctypes.c_char_p, []),
+        "ee_test_gemm": (I32, [I32, I32, P, P, P, I32, I32, I32, I32, P]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(code: int):
+    if code != EE_OK:
+        raise EEError(code, _lib.ee_last_error().decode())
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def make_config(hidden, vocab, ffn, num_exits, arch, norm_eps=1e-5, vocab_begin=0, vocab_end=None):
+    return ee_head_config(hidden, vocab, ffn, num_exits, ARCH[arch] if isinstance(arch, str) else arch,
+                          norm_eps, vocab_begin, vocab if vocab_end is None else vocab_end)
+
+
+def heads(list_of_dicts):
+    """[{name: tensor}] -> ctypes array of ee_head_tensors (missing names -> NULL)."""
+    arr = (ee_head_tensors * len(list_of_dicts))()
+    for i, d in enumerate(list_of_dicts):
+        for n in TENSOR_NAMES:
+            t = d.get(n) if d is not None else None
+            setattr(arr[i], n, None if t is None else t.data_ptr())
+    return arr
+
+
+# ---------------------------------------------------------------------------
+# thin wrappers with the C-ABI names
+# ---------------------------------------------------------------------------
+
+def ee_workspace_size(cfg, n_tokens: int) -> int:
+    load()
+    out = ctypes.c_size_t(0)
+    _check(_lib.ee_workspace_size(ctypes.byref(cfg), int(n_tokens), ctypes.byref(out)))
+    return out.value
+
+
+def ee_init_heads(cfg, init, copy_src, master, operand, seed=0, std=0.02, src_dtype=torch.bfloat16,
+                  stream=None):
+    load()
+    src = heads(copy_src) if copy_src is not None else None
+    _check(_lib.ee_init_heads(ctypes.byref(cfg), INIT[init] if isinstance(init, str) else init,
+                              src, DTYPE[src_dtype], int(seed), float(std), heads(master),
+                              heads(operand), _stream(stream)))
+
+
+def ee_tune_step(cfg, hidden, targets, exit_weights, params, grads, loss_out, workspace,
+                 accumulate=False, aux=None, valid_count=None, stream=None):
+    load()
+    E = cfg.num_exits
+    hid = (ctypes.c_void_p * E)(*[h.data_ptr() for h in hidden])
+    w = (ctypes.c_float * E)(*[float(a) for a in exit_weights])
+    ax = None
+    if aux is not None:
+        ax = (ee_step_aux * E)()
+        for i, d in enumerate(aux):
+            for k in ("lse", "loss_tok", "argmax", "conf"):
+                t = d.get(k)
+                setattr(ax[i], k, None if t is None else t.data_ptr())
+    n = targets.numel()
+    _check(_lib.ee_tune_step(ctypes.byref(cfg), hid, n, _ptr(targets), w, heads(params),
+                             heads(grads), int(bool(accumulate)), _ptr(loss_out), ax,
+                             _ptr(valid_count), _ptr(workspace), workspace.numel(),
+                             _stream(stream)))
+
+
+def ee_count_valid(targets, vocab, out, workspace, stream=None):
+    load()
+    _check(_lib.ee_count_valid(_ptr(targets), targets.numel(), int(vocab), _ptr(out),
+                               _ptr(workspace), workspace.numel(), _stream(stream)))
+
+
+def ee_adam_update(cfg, master, operand, grads, m, v, lr, step, beta1=0.9, beta2=0.95, eps=1e-5,
+                   weight_decay=0.0, grad_scale=1.0, stream=None):
+    load()
+    _check(_lib.ee_adam_update(ctypes.byref(cfg), heads(master), heads(operand), heads(grads),
+                               heads(m), heads(v), lr, beta1, beta2, eps, weight_decay,
+                               int(step), grad_scale, _stream(stream)))
+
+
+def ee_sgd_update(cfg, master, operand, grads, lr, momentum=0.0, momentum_buf=None,
+                  grad_scale=1.0, stream=None):
+    load()
+    buf = heads(momentum_buf) if momentum_buf is not None else None
+    _check(_lib.ee_sgd_update(ctypes.byref(cfg), heads(master), heads(operand), heads(grads), buf,
+                              lr, momentum, grad_scale, _stream(stream)))
+
+
+def ee_get_status(workspace, stream=None):
+    load()
+    code, idx = ctypes.c_int32(0), ctypes.c_int32(0)
+    _check(_lib.ee_get_status(_ptr(workspace), _stream(stream), ctypes.byref(code),
+                              ctypes.byref(idx)))
+    return code.value, idx.value
+
+
+def ee_lr_at(it, total, warmup_frac=0.01, lr_max=1e-4, lr_min=1e-5) -> float:
+    load()
+    return _lib.ee_lr_at(int(it), int(total), warmup_frac, lr_max, lr_min)
+
+
+def ee_version() -> str:
+    load()
+    return _lib.ee_version().decode()
+
+
+def ee_test_gemm(A, B, C, a_kmajor, b_kmajor, M, N, K, accumulate=False, stream=None):
+    load()
+    _check(_lib.ee_test_gemm(int(a_kmajor), int(b_kmajor), _ptr(A), _ptr(B), _ptr(C), M, N, K,
+                             int(bool(accumulate)), _stream(stream)))
+
+
+# ---------------------------------------------------------------------------
+# ExitHeads: parameter store + optimizer state + workspace (torch allocations)
+# ---------------------------------------------------------------------------
+
+def tensor_shapes(hidden, vocab, ffn, arch):
+    s = {"w_out": (vocab, hidden)}
+    if arch in ("norm", "mlp"):
+        s["g_f"] = (hidden,)
+    if arch == "mlp":
+        s.update(g_a=(hidden,), w_gate=(ffn, hidden), w_up=(ffn, hidden), w_down=(hidden, ffn))
+    return s
+
+
+@dataclass
+class HeadSpec:
+    hidden: int
+    vocab: int
+    ffn: int
+    num_exits: int
+    arch: str
+    norm_eps: float = 1e-5
+
+
+class ExitHeads:
+    """The exit-head parameter store of one EE-Tuning run on one GPU.
+
+    Holds, per exit, the fp32 master parameters, the bf16 operand copies of the
+    matrices, fp32 gradients and Adam moments (exits only), and the
+    step workspace.  All compute goes through the C-ABI above.
+    """
+
+    def __init__(self, spec: HeadSpec, max_tokens: int, device="cuda", adam=True):
+        load()
+        self.spec = spec
+        self.cfg = make_config(spec.hidden, spec.vocab, spec.ffn, spec.num_exits, spec.arch,
+                               spec.norm_eps)
+        shapes = tensor_shapes(spec.hidden, spec.vocab, spec.ffn, spec.arch)
+        dev = torch.device(device)
+        E = spec.num_exits
+
+        def alloc(dtype_for):
+            return [{k: torch.zeros(s, dtype=dtype_for(k), device=dev) for k, s in shapes.items()}
+                    for _ in range(E)]
+
+        f32 = lambda k: torch.float32
+        self.master = alloc(f32)
+        # operand copies: bf16 matrices; gains alias the fp32 masters
+        self.operand = [{k: (m[k] if k.startswith("g_") else
+                             torch.zeros(shapes[k], dtype=torch.bfloat16, device=dev))
+                         for k in shapes} for m in self.master]
+        self.grads = alloc(f32)
+        self.m = alloc(f32) if adam else None
+        self.v = alloc(f32) if adam else None
+        self.step_count = 0
+        self.max_tokens = int(max_tokens)
+        ws = ee_workspace_size(self.cfg, self.max_tokens)
+        self.workspace = torch.zeros(ws, dtype=torch.uint8, device=dev)
+        self.loss = torch.zeros(E, dtype=torch.float32, device=dev)
+
+    def init(self, mode="copy", copy_src=None, seed=0, std=0.02, src_dtype=torch.bfloat16):
+        ee_init_heads(self.cfg, mode, copy_src, self.master, self.operand, seed=seed, std=std,
+                      src_dtype=src_dtype)
+
+    def step(self, hidden, targets, exit_weights=None, accumulate=False, aux=None,
+             valid_count=None):
+        if targets.numel() > self.max_tokens:
+            raise ValueError("more tokens than the workspace was sized for")
+        w = exit_weights if exit_weights is not None else [1.0] * self.spec.num_exits
+        ee_tune_step(self.cfg, hidden, targets, w, self.operand, self.grads, self.loss,
+                     self.workspace, accumulate=accumulate, aux=aux, valid_count=valid_count)
+        return self.loss
+
+    def adam(self, lr, beta1=0.9, beta2=0.95, eps=1e-5, weight_decay=0.0, grad_scale=1.0):
+        self.step_count += 1
+        ee_adam_update(self.cfg, self.master, self.operand, self.grads, self.m, self.v, lr,
+                       self.step_count, beta1, beta2, eps, weight_decay, grad_scale)
+
+    def status(self):
+        return ee_get_status(self.workspace)

@@ -1,0 +1,577 @@
+// api.cu -- the C-ABI (include/ee.h): argument validation, workspace carving
+// and the per-exit kernel sequence of one EE-Tuning step.
+//
+// Per exit i, all on `stream`:
+//   MLP only   a1  u = RMSNorm_a(x)                      rmsnorm_fwd        (HBM)
+//              a2  [A|B] = u [W_gate|W_up]^T, M = silu(A)B  GEMM+SwiGLU    (tensor)
+//              a3  y = x + M W_down^T                    GEMM+residual      (tensor)
+//   Norm/MLP   a4  z = RMSNorm_f(y)                      rmsnorm_fwd        (HBM)
+//   all        a5  per-tile online-softmax stats of z W_out^T  GEMM+CE     (tensor)
+//              a6  lse, loss_t, argmax, conf, L_i        ce_finalize/reduce (HBM)
+//              a7  dS = coef (softmax - onehot), recomputed GEMM -> bf16    (tensor)
+//   Norm/MLP   a8  dz = dS W_out                         GEMM (B MN-major)  (tensor)
+//   all        a9  dW_out = dS^T z                       GEMM (A,B MN-major)(tensor)
+//   Norm/MLP   a10 dg_f, dy                              rmsnorm_bwd        (HBM)
+//   MLP only   a11 dW_down = dy^T M; dM = dy W_down -> dA, dB (SwiGLU bwd epilogue)
+//              a12 dW_gate|up = [dA|dB]^T u; du = [dA|dB] [W_gate;W_up]
+//              a13 dg_a = sum du * xhat                  gain_grad          (HBM)
+// The full [tokens x vocab] logit matrix is never written: a5 keeps only
+// per-tile (max, sum-exp, argmax) partials and a7 recomputes S tile by tile.
+#include <cuda_runtime.h>
+#include <cmath>
+#include <cstdio>
+#include <cstdarg>
+#include <cstring>
+#include <string>
+#include "../../include/ee.h"
+#include "internal.cuh"
+
+using namespace ee;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+ee_status fail(ee_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return s;
+}
+
+#define EE_CUDA(call)                                                                         \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(EE_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_),        \
+                  __FILE__, __LINE__);                                                        \
+  } while (0)
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+constexpr int NORM_RPB = 64;  // rows per block of the norm backward / gain-grad kernels
+
+ee_status check_cfg(const ee_head_config* c) {
+  if (!c) return fail(EE_ERR_ARG, "cfg is NULL");
+  if (c->arch < EE_ARCH_EMBEDDING || c->arch > EE_ARCH_MLP)
+    return fail(EE_ERR_ARG, "unknown arch %d", c->arch);
+  if (c->num_exits < 1) return fail(EE_ERR_ARG, "num_exits must be >= 1");
+  if (c->hidden < 64 || c->hidden > 8192 || c->hidden % 64 != 0)
+    return fail(EE_ERR_SHAPE, "hidden must be a multiple of 64 in [64, 8192], got %d", c->hidden);
+  if (c->vocab < 1) return fail(EE_ERR_SHAPE, "vocab must be >= 1");
+  if (c->vocab_begin != 0 || c->vocab_end != c->vocab)
+    return fail(EE_ERR_UNSUPPORTED, "vocab-parallel shards are not implemented in this build");
+  if ((c->vocab_end - c->vocab_begin) % 8 != 0)
+    return fail(EE_ERR_SHAPE, "local vocab size must be a multiple of 8");
+  if (c->arch == EE_ARCH_MLP && (c->ffn < 128 || c->ffn % 128 != 0))
+    return fail(EE_ERR_SHAPE, "ffn must be a positive multiple of 128 for MLP exits, got %d",
+                c->ffn);
+  if (!(c->norm_eps >= 0.f)) return fail(EE_ERR_ARG, "norm_eps must be >= 0");
+  return EE_OK;
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Layout {
+  size_t status, vcount, loss_part, lse, coef, tgt, pm, ps, pi, z, ds, dz, dgp, ry, u, rx, ab,
+      mact, y, dy, total;
+  int nb, nparts, nfin;
+};
+
+Layout make_layout(const ee_head_config* c, long long n) {
+  Layout L{};
+  const long long h = c->hidden, Vl = c->vocab_end - c->vocab_begin, F = c->ffn;
+  L.nb = (int)((Vl + GEMM_BN - 1) / GEMM_BN);
+  L.nparts = (int)((n + NORM_RPB - 1) / NORM_RPB);
+  L.nfin = (int)((n + FINALIZE_THREADS - 1) / FINALIZE_THREADS);
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t r = o;
+    o = align_up(o + bytes);
+    return r;
+  };
+  L.status = take(sizeof(DevStatus));
+  L.vcount = take(8);
+  L.loss_part = take(4 * (size_t)(L.nfin > 0 ? L.nfin : 1));
+  L.lse = take(4 * n);
+  L.coef = take(4 * n);
+  L.tgt = take(4 * n);
+  L.pm = take(4 * (size_t)L.nb * n);
+  L.ps = take(4 * (size_t)L.nb * n);
+  L.pi = take(4 * (size_t)L.nb * n);
+  L.ds = take(2 * (size_t)n * Vl);
+  L.z = L.dz = L.dgp = L.ry = L.u = L.rx = L.ab = L.mact = L.y = L.dy = 0;
+  if (c->arch != EE_ARCH_EMBEDDING) {
+    L.z = take(2 * (size_t)n * h);
+    L.dz = take(4 * (size_t)n * h);
+    L.dgp = take(4 * (size_t)(L.nparts > 0 ? L.nparts : 1) * h);
+    L.ry = take(4 * n);
+  }
+  if (c->arch == EE_ARCH_MLP) {
+    L.u = take(2 * (size_t)n * h);
+    L.rx = take(4 * n);
+    L.ab = take(2 * (size_t)n * 2 * F);
+    L.mact = take(2 * (size_t)n * F);
+    L.y = take(4 * (size_t)n * h);
+    L.dy = take(2 * (size_t)n * h);
+  }
+  L.total = o;
+  return L;
+}
+
+ee_status check_device() {
+  static int ok = -1;
+  if (ok < 0) {
+    int dev = 0;
+    cudaDeviceProp p;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaGetDeviceProperties(&p, dev) != cudaSuccess) {
+      cudaGetLastError();
+      ok = 0;
+    } else {
+      ok = (p.major == 10 && p.minor == 0) ? 1 : 0;
+    }
+  }
+  if (!ok) return fail(EE_ERR_UNSUPPORTED, "no sm_100 (B200) device is current");
+  return EE_OK;
+}
+
+ee_status check_arch_tensors(const ee_head_config* c, const ee_head_tensors& t, const char* what,
+                             int i) {
+  const bool mlp = c->arch == EE_ARCH_MLP, nrm = c->arch != EE_ARCH_EMBEDDING;
+  if (!t.w_out) return fail(EE_ERR_ARCH, "%s[%d].w_out is NULL", what, i);
+  if (nrm != (t.g_f != nullptr)) return fail(EE_ERR_ARCH, "%s[%d].g_f presence does not match arch", what, i);
+  if (mlp != (t.g_a != nullptr) || mlp != (t.w_gate != nullptr) || mlp != (t.w_up != nullptr) ||
+      mlp != (t.w_down != nullptr))
+    return fail(EE_ERR_ARCH, "%s[%d]: MLP tensors present/absent do not match arch", what, i);
+  const void* ps[6] = {t.g_a, t.w_gate, t.w_up, t.w_down, t.g_f, t.w_out};
+  for (const void* p : ps)
+    if (p && !aligned16(p)) return fail(EE_ERR_ALIGN, "%s[%d]: tensor not 16-byte aligned", what, i);
+  return EE_OK;
+}
+
+GemmArgs base_args(int M, int N, int K) {
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.m_split = M;
+  a.group_m = 16;
+  return a;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ee_last_error(void) { return g_last_error.c_str(); }
+const char* ee_version(void) { return "ee_b200 0.1.0 (sm_100a tcgen05)"; }
+
+double ee_lr_at(int64_t it, int64_t total, double warmup_frac, double lr_max, double lr_min) {
+  if (total < 1 || it < 0 || it > total) return NAN;
+  const int64_t w = (int64_t)std::ceil(warmup_frac * (double)total);
+  if (w > 0 && it <= w) return lr_max * (double)it / (double)w;
+  if (total == w) return lr_max;
+  return lr_max - (lr_max - lr_min) * (double)(it - w) / (double)(total - w);
+}
+
+ee_status ee_workspace_size(const ee_head_config* cfg, int64_t n_tokens, size_t* bytes) {
+  ee_status s = check_cfg(cfg);
+  if (s != EE_OK) return s;
+  if (!bytes || n_tokens < 0) return fail(EE_ERR_ARG, "bytes NULL or n_tokens < 0");
+  *bytes = make_layout(cfg, n_tokens).total;
+  return EE_OK;
+}
+
+ee_status ee_get_status(void* workspace, void* stream, int32_t* code, int32_t* exit_index) {
+  if (!workspace || !code || !exit_index) return fail(EE_ERR_ARG, "NULL argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  DevStatus h{};
+  EE_CUDA(cudaMemcpyAsync(&h, workspace, sizeof(h), cudaMemcpyDeviceToHost, st));
+  EE_CUDA(cudaStreamSynchronize(st));
+  *code = h.code;
+  *exit_index = h.code ? h.exit_index : -1;
+  if (h.code) {
+    EE_CUDA(cudaMemsetAsync(workspace, 0, sizeof(DevStatus), st));
+    EE_CUDA(cudaStreamSynchronize(st));
+  }
+  return EE_OK;
+}
+
+ee_status ee_count_valid(const int32_t* targets, int64_t n, int32_t vocab, int64_t* out,
+                         void* workspace, size_t ws_bytes, void* stream) {
+  if (!out || !workspace || (n > 0 && !targets)) return fail(EE_ERR_ARG, "NULL argument");
+  if (ws_bytes < sizeof(DevStatus)) return fail(EE_ERR_WORKSPACE, "workspace too small");
+  ee_status s = check_device();
+  if (s != EE_OK) return s;
+  EE_CUDA(launch_count_valid(targets, n, vocab, (long long*)out, (DevStatus*)workspace,
+                             (cudaStream_t)stream));
+  return EE_OK;
+}
+
+ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int64_t n_tokens,
+                       const int32_t* targets, const float* exit_weights,
+                       const ee_head_tensors* params, ee_head_tensors* grads, int32_t accumulate,
+                       float* loss_out, const ee_step_aux* aux, const int64_t* valid_count,
+                       void* workspace, size_t ws_bytes, void* stream) {
+  ee_status s = check_cfg(cfg);
+  if (s != EE_OK) return s;
+  const int E = cfg->num_exits;
+  if (!hidden || !exit_weights || !params || !grads || !loss_out || n_tokens < 0 ||
+      (n_tokens > 0 && !targets))
+    return fail(EE_ERR_ARG, "NULL argument or n_tokens < 0");
+  if (n_tokens > (1LL << 30)) return fail(EE_ERR_SHAPE, "n_tokens too large");
+  for (int i = 0; i < E; ++i) {
+    if ((s = check_arch_tensors(cfg, params[i], "params", i)) != EE_OK) return s;
+    if ((s = check_arch_tensors(cfg, grads[i], "grads", i)) != EE_OK) return s;
+    if (n_tokens > 0 && (!hidden[i] || !aligned16(hidden[i])))
+      return fail(hidden[i] ? EE_ERR_ALIGN : EE_ERR_ARG, "hidden[%d] NULL or misaligned", i);
+  }
+  if ((targets && !aligned16(targets)) || !aligned16(workspace))
+    return fail(EE_ERR_ALIGN, "targets/workspace not 16-byte aligned");
+  const long long n = n_tokens;
+  const Layout L = make_layout(cfg, n);
+  if (!workspace || ws_bytes < L.total)
+    return fail(EE_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", L.total, ws_bytes);
+  if ((s = check_device()) != EE_OK) return s;
+
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* ws = (uint8_t*)workspace;
+  DevStatus* status = (DevStatus*)(ws + L.status);
+  long long* vc_local = (long long*)(ws + L.vcount);
+  const int h = cfg->hidden, F = cfg->ffn, Vl = cfg->vocab_end - cfg->vocab_begin;
+  const bool mlp = cfg->arch == EE_ARCH_MLP, nrm = cfg->arch != EE_ARCH_EMBEDDING;
+
+  EE_CUDA(launch_count_valid(targets, n, cfg->vocab, vc_local, status, st));
+  const long long* vc = valid_count ? (const long long*)valid_count : vc_local;
+
+  if (n == 0) {
+    for (int i = 0; i < E; ++i) {
+      if (!accumulate) {
+        const long long sz[6] = {h, (long long)F * h, (long long)F * h, (long long)h * F, h,
+                                 (long long)Vl * h};
+        void* ptrs[6] = {grads[i].g_a, grads[i].w_gate, grads[i].w_up, grads[i].w_down,
+                         grads[i].g_f, grads[i].w_out};
+        for (int k = 0; k < 6; ++k)
+          if (ptrs[k]) EE_CUDA(cudaMemsetAsync(ptrs[k], 0, 4 * sz[k], st));
+      }
+    }
+    EE_CUDA(cudaMemsetAsync(loss_out, 0, sizeof(float) * E, st));
+    return EE_OK;
+  }
+
+  float* lse = (float*)(ws + L.lse);
+  float* coef = (float*)(ws + L.coef);
+  float* tgt = (float*)(ws + L.tgt);
+  float* pm = (float*)(ws + L.pm);
+  float* ps = (float*)(ws + L.ps);
+  int32_t* pi = (int32_t*)(ws + L.pi);
+  float* loss_part = (float*)(ws + L.loss_part);
+  __nv_bfloat16* ds = (__nv_bfloat16*)(ws + L.ds);
+  __nv_bfloat16* zbuf = nrm ? (__nv_bfloat16*)(ws + L.z) : nullptr;
+  float* dz = nrm ? (float*)(ws + L.dz) : nullptr;
+  float* dgp = nrm ? (float*)(ws + L.dgp) : nullptr;
+  float* ry = nrm ? (float*)(ws + L.ry) : nullptr;
+  __nv_bfloat16* u = mlp ? (__nv_bfloat16*)(ws + L.u) : nullptr;
+  float* rx = mlp ? (float*)(ws + L.rx) : nullptr;
+  __nv_bfloat16* ab = mlp ? (__nv_bfloat16*)(ws + L.ab) : nullptr;
+  __nv_bfloat16* mact = mlp ? (__nv_bfloat16*)(ws + L.mact) : nullptr;
+  float* y = mlp ? (float*)(ws + L.y) : nullptr;
+  __nv_bfloat16* dy = mlp ? (__nv_bfloat16*)(ws + L.dy) : nullptr;
+
+  for (int i = 0; i < E; ++i) {
+    const ee_head_tensors& P = params[i];
+    const ee_head_tensors& G = grads[i];
+    const __nv_bfloat16* x = (const __nv_bfloat16*)hidden[i];
+    const __nv_bfloat16* z = x;
+    const float alpha = exit_weights[i];
+
+    if (mlp) {
+      // a1: u = RMSNorm_a(x)
+      EE_CUDA(launch_rmsnorm_fwd(x, false, (const float*)P.g_a, cfg->norm_eps, u, rx, n, h, st));
+      // a2: [A|B] = u [W_gate|W_up]^T (paired B tiles), M = silu(A) * B
+      {
+        GemmArgs a = base_args((int)n, F, h);
+        a.ab = ab;
+        a.ld_ab = 2LL * F;
+        a.mact = mact;
+        a.ld_m = F;
+        a.ffn = F;
+        Mat A{u, n, h, h}, B0{P.w_gate, F, h, h}, B1{P.w_up, F, h, h};
+        EE_CUDA(gemm_run(EPI_SWIGLU_FWD, true, true, A, B0, &B1, B_PAIR, 0, a, st));
+      }
+      // a3: y = x + M W_down^T  (fp32 residual stream, A15)
+      {
+        GemmArgs a = base_args((int)n, h, F);
+        a.out0 = y;
+        a.ldo = h;
+        a.resid = x;
+        a.ld_resid = h;
+        Mat A{mact, n, F, F}, B{P.w_down, h, F, F};
+        EE_CUDA(gemm_run(EPI_RESID, true, true, A, B, nullptr, B_PLAIN, 0, a, st));
+      }
+      // a4: z = RMSNorm_f(y)
+      EE_CUDA(launch_rmsnorm_fwd(y, true, (const float*)P.g_f, cfg->norm_eps, zbuf, ry, n, h, st));
+      z = zbuf;
+    } else if (nrm) {
+      EE_CUDA(launch_rmsnorm_fwd(x, false, (const float*)P.g_f, cfg->norm_eps, zbuf, ry, n, h, st));
+      z = zbuf;
+    }
+
+    // a5: per-tile online-softmax statistics of S = z W_out^T (logits never stored)
+    {
+      GemmArgs a = base_args((int)n, Vl, h);
+      a.targets = targets;
+      a.vocab_begin = cfg->vocab_begin;
+      a.part_m = pm;
+      a.part_s = ps;
+      a.part_i = pi;
+      a.tgt_logit = tgt;
+      Mat A{z, n, h, h}, B{P.w_out, Vl, h, h};
+      EE_CUDA(gemm_run(EPI_CE_STATS, true, true, A, B, nullptr, B_PLAIN, 0, a, st));
+    }
+    // a6: lse, coef, per-token aux, L_i
+    {
+      const ee_step_aux* ax = aux ? &aux[i] : nullptr;
+      EE_CUDA(launch_ce_finalize(pm, ps, pi, tgt, targets, L.nb, n, vc, alpha, lse, coef,
+                                 ax ? ax->lse : nullptr, ax ? ax->loss_tok : nullptr,
+                                 ax ? ax->argmax : nullptr, ax ? ax->conf : nullptr, loss_part,
+                                 L.nfin, st));
+      EE_CUDA(launch_loss_reduce(loss_part, L.nfin, vc, loss_out + i, status, i, st));
+    }
+    // a7: dS = alpha w_t / W (softmax(S_t) - onehot(y_t)), S recomputed -> bf16
+    {
+      GemmArgs a = base_args((int)n, Vl, h);
+      a.targets = targets;
+      a.vocab_begin = cfg->vocab_begin;
+      a.lse = lse;
+      a.coef = coef;
+      a.ds = ds;
+      a.ld_ds = Vl;
+      Mat A{z, n, h, h}, B{P.w_out, Vl, h, h};
+      EE_CUDA(gemm_run(EPI_CE_DS, true, true, A, B, nullptr, B_PLAIN, 0, a, st));
+    }
+    // a8: dz = dS W_out  (W_out read MN-major in place)
+    if (nrm) {
+      GemmArgs a = base_args((int)n, h, Vl);
+      a.out0 = dz;
+      a.ldo = h;
+      Mat A{ds, n, Vl, Vl}, B{P.w_out, Vl, h, h};
+      EE_CUDA(gemm_run(EPI_F32, true, false, A, B, nullptr, B_PLAIN, 0, a, st));
+    }
+    // a9: dW_out = dS^T z  (both operands MN-major, K = tokens)
+    {
+      GemmArgs a = base_args(Vl, h, (int)n);
+      a.out0 = (float*)G.w_out;
+      a.ldo = h;
+      a.accumulate = accumulate;
+      Mat A{ds, n, Vl, Vl}, B{z, n, h, h};
+      EE_CUDA(gemm_run(EPI_F32, false, false, A, B, nullptr, B_PLAIN, 0, a, st));
+    }
+    // a10: final RMSNorm backward -> dg_f (and dy for MLP)
+    if (nrm) {
+      EE_CUDA(launch_rmsnorm_bwd(dz, mlp ? (const void*)y : (const void*)x, mlp, ry,
+                                 (const float*)P.g_f, mlp ? dy : nullptr, dgp, n, h, NORM_RPB,
+                                 st));
+      EE_CUDA(launch_reduce_cols(dgp, L.nparts, h, (float*)G.g_f, accumulate, st));
+    }
+    if (mlp) {
+      // a11: dW_down = dy^T M
+      {
+        GemmArgs a = base_args(h, F, (int)n);
+        a.out0 = (float*)G.w_down;
+        a.ldo = F;
+        a.accumulate = accumulate;
+        Mat A{dy, n, h, h}, B{mact, n, F, F};
+        EE_CUDA(gemm_run(EPI_F32, false, false, A, B, nullptr, B_PLAIN, 0, a, st));
+      }
+      // a11: dM = dy W_down; dA = dM B silu'(A), dB = dM silu(A), in place over [A|B]
+      {
+        GemmArgs a = base_args((int)n, F, h);
+        a.ab = ab;
+        a.ld_ab = 2LL * F;
+        a.ffn = F;
+        Mat A{dy, n, h, h}, B{P.w_down, h, F, F};
+        EE_CUDA(gemm_run(EPI_SWIGLU_BWD, true, false, A, B, nullptr, B_PLAIN, 0, a, st));
+      }
+      // a12: [dW_gate; dW_up] = [dA|dB]^T u  (rows split at F over two outputs)
+      {
+        GemmArgs a = base_args(2 * F, h, (int)n);
+        a.out0 = (float*)G.w_gate;
+        a.out1 = (float*)G.w_up;
+        a.m_split = F;
+        a.ldo = h;
+        a.accumulate = accumulate;
+        Mat A{ab, n, 2LL * F, 2LL * F}, B{u, n, h, h};
+        EE_CUDA(gemm_run(EPI_F32, false, false, A, B, nullptr, B_PLAIN, 0, a, st));
+      }
+      // a12: du = dA W_gate + dB W_up  (K concatenation over the two weights)
+      {
+        GemmArgs a = base_args((int)n, h, 2 * F);
+        a.out0 = dz;  // dz is dead after a10: reuse as du
+        a.ldo = h;
+        Mat A{ab, n, 2LL * F, 2LL * F}, B0{P.w_gate, F, h, h}, B1{P.w_up, F, h, h};
+        EE_CUDA(gemm_run(EPI_F32, true, false, A, B0, &B1, B_KSPLIT, F, a, st));
+      }
+      // a13: dg_a = sum_t du_t * xhat_t  (no dx: frozen backbone)
+      EE_CUDA(launch_gain_grad(dz, x, rx, dgp, n, h, NORM_RPB, st));
+      EE_CUDA(launch_reduce_cols(dgp, L.nparts, h, (float*)G.g_a, accumulate, st));
+    }
+  }
+  return EE_OK;
+}
+
+ee_status ee_init_heads(const ee_head_config* cfg, int32_t init, const ee_head_tensors* src,
+                        int32_t src_dtype, uint64_t seed, float stdv, ee_head_tensors* master,
+                        ee_head_tensors* op, void* stream) {
+  ee_status s = check_cfg(cfg);
+  if (s != EE_OK) return s;
+  if (!master || !op) return fail(EE_ERR_ARG, "master/operand NULL");
+  if (init != EE_INIT_COPY && init != EE_INIT_RANDOM) return fail(EE_ERR_ARG, "unknown init");
+  if (src_dtype != EE_DTYPE_BF16 && src_dtype != EE_DTYPE_F32)
+    return fail(EE_ERR_ARG, "unknown src_dtype");
+  if (init == EE_INIT_COPY && !src) return fail(EE_ERR_STRUCTURE, "Copy init without a source");
+  if ((s = check_device()) != EE_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long h = cfg->hidden, F = cfg->ffn, Vl = cfg->vocab_end - cfg->vocab_begin;
+  for (int i = 0; i < cfg->num_exits; ++i) {
+    if ((s = check_arch_tensors(cfg, master[i], "master", i)) != EE_OK) return s;
+    if ((s = check_arch_tensors(cfg, op[i], "operand", i)) != EE_OK) return s;
+    struct T {
+      const void* src;
+      float* m;
+      void* o;
+      long long n;
+      bool gain;
+      const char* name;
+    } ts[6] = {
+        {src ? src[i].g_a : nullptr, (float*)master[i].g_a, op[i].g_a, h, true, "g_a"},
+        {src ? src[i].w_gate : nullptr, (float*)master[i].w_gate, op[i].w_gate, F * h, false, "w_gate"},
+        {src ? src[i].w_up : nullptr, (float*)master[i].w_up, op[i].w_up, F * h, false, "w_up"},
+        {src ? src[i].w_down : nullptr, (float*)master[i].w_down, op[i].w_down, h * F, false, "w_down"},
+        {src ? src[i].g_f : nullptr, (float*)master[i].g_f, op[i].g_f, h, true, "g_f"},
+        {src ? src[i].w_out : nullptr, (float*)master[i].w_out, op[i].w_out, Vl * h, false, "w_out"},
+    };
+    for (int k = 0; k < 6; ++k) {
+      const T& t = ts[k];
+      if (!t.m) continue;
+      float* op_f32 = (t.gain && t.o != (void*)t.m) ? (float*)t.o : nullptr;
+      __nv_bfloat16* op_bf = t.gain ? nullptr : (__nv_bfloat16*)t.o;
+      if (init == EE_INIT_COPY) {
+        if (!t.src)
+          return fail(EE_ERR_STRUCTURE, "Copy init: source module %s of exit %d is missing",
+                      t.name, i);
+        if (!aligned16(t.src)) return fail(EE_ERR_ALIGN, "copy source not 16-byte aligned");
+        EE_CUDA(launch_copy_cast(t.src, src_dtype == EE_DTYPE_F32, t.m, op_bf, op_f32, t.n, st));
+      } else if (t.gain) {
+        EE_CUDA(launch_fill(t.m, op_f32, t.n, 1.0f, st));
+      } else {
+        EE_CUDA(launch_random_normal(seed, (uint64_t)i * 16 + k, stdv, t.m, op_bf, t.n, st));
+      }
+    }
+  }
+  return EE_OK;
+}
+
+static ee_status opt_common(const ee_head_config* cfg, ee_head_tensors* master,
+                            ee_head_tensors* op, const ee_head_tensors* grads) {
+  ee_status s = check_cfg(cfg);
+  if (s != EE_OK) return s;
+  if (!master || !op || !grads) return fail(EE_ERR_ARG, "NULL argument");
+  for (int i = 0; i < cfg->num_exits; ++i) {
+    if ((s = check_arch_tensors(cfg, master[i], "master", i)) != EE_OK) return s;
+    if ((s = check_arch_tensors(cfg, op[i], "operand", i)) != EE_OK) return s;
+    if ((s = check_arch_tensors(cfg, grads[i], "grads", i)) != EE_OK) return s;
+  }
+  return check_device();
+}
+
+ee_status ee_adam_update(const ee_head_config* cfg, ee_head_tensors* master, ee_head_tensors* op,
+                         const ee_head_tensors* grads, ee_head_tensors* m, ee_head_tensors* v,
+                         float lr, float beta1, float beta2, float eps, float wd, int64_t step,
+                         float grad_scale, void* stream) {
+  ee_status s = opt_common(cfg, master, op, grads);
+  if (s != EE_OK) return s;
+  if (!m || !v) return fail(EE_ERR_ARG, "moments NULL");
+  if (step < 1) return fail(EE_ERR_ARG, "step must be >= 1");
+  cudaStream_t st = (cudaStream_t)stream;
+  const float bc1 = (float)(1.0 - std::pow((double)beta1, (double)step));
+  const float bc2 = (float)(1.0 - std::pow((double)beta2, (double)step));
+  const long long h = cfg->hidden, F = cfg->ffn, Vl = cfg->vocab_end - cfg->vocab_begin;
+  for (int i = 0; i < cfg->num_exits; ++i) {
+    if ((s = check_arch_tensors(cfg, m[i], "m", i)) != EE_OK) return s;
+    if ((s = check_arch_tensors(cfg, v[i], "v", i)) != EE_OK) return s;
+    void* const mp[6] = {master[i].g_a, master[i].w_gate, master[i].w_up, master[i].w_down, master[i].g_f, master[i].w_out};
+    void* const opp[6] = {op[i].g_a, op[i].w_gate, op[i].w_up, op[i].w_down, op[i].g_f, op[i].w_out};
+    void* const gp[6] = {grads[i].g_a, grads[i].w_gate, grads[i].w_up, grads[i].w_down, grads[i].g_f, grads[i].w_out};
+    void* const m1[6] = {m[i].g_a, m[i].w_gate, m[i].w_up, m[i].w_down, m[i].g_f, m[i].w_out};
+    void* const v1[6] = {v[i].g_a, v[i].w_gate, v[i].w_up, v[i].w_down, v[i].g_f, v[i].w_out};
+    const long long ns[6] = {h, F * h, F * h, h * F, h, Vl * h};
+    const bool gain[6] = {true, false, false, false, true, false};
+    for (int k = 0; k < 6; ++k) {
+      if (!mp[k]) continue;
+      float* opf = (gain[k] && opp[k] != mp[k]) ? (float*)opp[k] : nullptr;
+      __nv_bfloat16* opb = gain[k] ? nullptr : (__nv_bfloat16*)opp[k];
+      EE_CUDA(launch_adam((float*)mp[k], opb, opf, (const float*)gp[k], (float*)m1[k],
+                          (float*)v1[k], ns[k], lr, beta1, beta2, eps, wd, bc1, bc2, grad_scale,
+                          st));
+    }
+  }
+  return EE_OK;
+}
+
+ee_status ee_sgd_update(const ee_head_config* cfg, ee_head_tensors* master, ee_head_tensors* op,
+                        const ee_head_tensors* grads, ee_head_tensors* buf, float lr,
+                        float momentum, float grad_scale, void* stream) {
+  ee_status s = opt_common(cfg, master, op, grads);
+  if (s != EE_OK) return s;
+  if (momentum != 0.f && !buf) return fail(EE_ERR_ARG, "momentum buffer required");
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long h = cfg->hidden, F = cfg->ffn, Vl = cfg->vocab_end - cfg->vocab_begin;
+  for (int i = 0; i < cfg->num_exits; ++i) {
+    void* const mp[6] = {master[i].g_a, master[i].w_gate, master[i].w_up, master[i].w_down, master[i].g_f, master[i].w_out};
+    void* const opp[6] = {op[i].g_a, op[i].w_gate, op[i].w_up, op[i].w_down, op[i].g_f, op[i].w_out};
+    void* const gp[6] = {grads[i].g_a, grads[i].w_gate, grads[i].w_up, grads[i].w_down, grads[i].g_f, grads[i].w_out};
+    void* b1[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    if (buf) {
+      b1[0] = buf[i].g_a; b1[1] = buf[i].w_gate; b1[2] = buf[i].w_up;
+      b1[3] = buf[i].w_down; b1[4] = buf[i].g_f; b1[5] = buf[i].w_out;
+    }
+    const long long ns[6] = {h, F * h, F * h, h * F, h, Vl * h};
+    const bool gain[6] = {true, false, false, false, true, false};
+    for (int k = 0; k < 6; ++k) {
+      if (!mp[k]) continue;
+      float* opf = (gain[k] && opp[k] != mp[k]) ? (float*)opp[k] : nullptr;
+      __nv_bfloat16* opb = gain[k] ? nullptr : (__nv_bfloat16*)opp[k];
+      EE_CUDA(launch_sgd((float*)mp[k], opb, opf, (const float*)gp[k],
+                         momentum != 0.f ? (float*)b1[k] : nullptr, ns[k], lr, momentum,
+                         grad_scale, st));
+    }
+  }
+  return EE_OK;
+}
+
+// Testing hook: C[M x N] (fp32, row-major) (+)= A B^T with A stored [M x K]
+// (a_kmajor) or [K x M], B stored [N x K] (b_kmajor) or [K x N]; bf16.
+ee_status ee_test_gemm(int32_t a_kmajor, int32_t b_kmajor, const void* A, const void* B, float* C,
+                       int32_t M, int32_t N, int32_t K, int32_t accumulate, void* stream) {
+  if (!A || !B || !C || M < 1 || N < 1 || K < 1) return fail(EE_ERR_ARG, "bad test_gemm args");
+  if (K % 8 || (!a_kmajor && M % 8) || (!b_kmajor && N % 8) || N % 4)
+    return fail(EE_ERR_SHAPE, "test_gemm: strides must be 16-byte multiples");
+  ee_status s = check_device();
+  if (s != EE_OK) return s;
+  GemmArgs a = base_args(M, N, K);
+  a.out0 = C;
+  a.ldo = N;
+  a.accumulate = accumulate;
+  Mat mA = a_kmajor ? Mat{A, M, K, K} : Mat{A, K, M, M};
+  Mat mB = b_kmajor ? Mat{B, N, K, K} : Mat{B, K, N, N};
+  EE_CUDA(gemm_run(EPI_F32, a_kmajor != 0, b_kmajor != 0, mA, mB, nullptr, B_PLAIN, 0, a,
+                   (cudaStream_t)stream));
+  return EE_OK;
+}
+
+}  // extern "C"

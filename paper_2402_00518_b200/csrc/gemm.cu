@@ -1,0 +1,107 @@
+// gemm.cu -- host side of the tcgen05 GEMM: TMA descriptors and dispatch.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <mutex>
+#include "internal.cuh"
+
+namespace ee {
+
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                      const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                      const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                      CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled_t encode_fn() {
+  static PFN_encodeTiled_t fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+  });
+  return fn;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// 2-D bf16 tensor map, 128B swizzle; inner = contiguous dim.
+static bool make_tmap(CUtensorMap* m, const Mat& t, uint32_t box_inner, uint32_t box_outer) {
+  PFN_encodeTiled_t enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)t.cols, (cuuint64_t)t.rows};
+  cuuint64_t strides[1] = {(cuuint64_t)t.ld * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(t.ptr), dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int EPI, bool A_MN, bool B_MN>
+static cudaError_t launch(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1,
+                          const GemmArgs& args, cudaStream_t st) {
+  auto kern = gemm_kernel<EPI, A_MN, B_MN>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int tiles = args.m_blocks * args.n_blocks;
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  kern<<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(a, b0, b1, args);
+  return cudaGetLastError();
+}
+
+cudaError_t gemm_run(int epi, bool a_kmajor, bool b_kmajor, const Mat& A, const Mat& B0,
+                     const Mat* B1, int b_mode, int b_ksplit, GemmArgs args, cudaStream_t st) {
+  CUtensorMap ta, tb0, tb1;
+  const bool a_mn = !a_kmajor, b_mn = !b_kmajor;
+  if (!make_tmap(&ta, A, 64, a_mn ? 64 : GEMM_BM)) return cudaErrorInvalidValue;
+  const uint32_t b_outer = b_mn ? 64 : (b_mode == B_PAIR ? GEMM_BN / 2 : GEMM_BN);
+  if (!make_tmap(&tb0, B0, 64, b_outer)) return cudaErrorInvalidValue;
+  if (b_mode != B_PLAIN) {
+    if (!B1 || !make_tmap(&tb1, *B1, 64, b_outer)) return cudaErrorInvalidValue;
+  } else {
+    tb1 = tb0;
+  }
+  args.b_mode = b_mode;
+  args.b_ksplit = b_ksplit;
+  args.m_blocks = (args.M + GEMM_BM - 1) / GEMM_BM;
+  const int bn = (b_mode == B_PAIR) ? GEMM_BN / 2 : GEMM_BN;
+  args.n_blocks = (args.N + bn - 1) / bn;
+  args.k_blocks = (args.K + GEMM_BK - 1) / GEMM_BK;
+  if (args.group_m <= 0) args.group_m = 16;
+  if (args.m_blocks == 0 || args.n_blocks == 0 || args.k_blocks == 0) return cudaSuccess;
+
+#define EE_GEMM_CASE(E, AM, BM)                                   \
+  if (epi == E && a_mn == AM && b_mn == BM) return launch<E, AM, BM>(ta, tb0, tb1, args, st);
+  // the (epilogue, A major, B major) combinations the step uses, plus the
+  // plain fp32 GEMM in all four majors (exported for the parity tests)
+  EE_GEMM_CASE(EPI_F32, false, false)
+  EE_GEMM_CASE(EPI_F32, false, true)
+  EE_GEMM_CASE(EPI_F32, true, false)
+  EE_GEMM_CASE(EPI_F32, true, true)
+  EE_GEMM_CASE(EPI_RESID, false, false)
+  EE_GEMM_CASE(EPI_SWIGLU_FWD, false, false)
+  EE_GEMM_CASE(EPI_SWIGLU_BWD, false, true)
+  EE_GEMM_CASE(EPI_CE_STATS, false, false)
+  EE_GEMM_CASE(EPI_CE_DS, false, false)
+#undef EE_GEMM_CASE
+  return cudaErrorNotSupported;
+}
+
+}  // namespace ee

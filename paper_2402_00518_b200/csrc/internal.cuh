@@ -1,0 +1,69 @@
+// internal.cuh -- declarations shared by the library's translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+#include "gemm.cuh"
+
+namespace ee {
+
+// Device status word at the head of the workspace (ee_get_status).
+struct DevStatus {
+  int32_t code;
+  int32_t exit_index;
+  int32_t pad[2];
+};
+__device__ __forceinline__ void set_status(DevStatus* st, int32_t code, int32_t exit_index) {
+  if (atomicCAS(&st->code, 0, code) == 0) st->exit_index = exit_index;
+}
+
+// ---- GEMM host launcher (gemm.cu) ------------------------------------------
+struct Mat {  // a row-major bf16 matrix in global memory
+  const void* ptr;
+  long long rows, cols, ld;  // ld in elements
+};
+// Operand description of one GEMM side.
+//   k_major = true : storage [MN rows x K cols]  (K contiguous)
+//   k_major = false: storage [K rows x MN cols]  (MN contiguous)
+cudaError_t gemm_run(int epi, bool a_kmajor, bool b_kmajor, const Mat& A, const Mat& B0,
+                     const Mat* B1, int b_mode, int b_ksplit, GemmArgs args, cudaStream_t st);
+int num_sms();
+
+// ---- bandwidth-bound kernels (kernels.cu) -----------------------------------
+cudaError_t launch_count_valid(const int32_t* targets, long long n, int vocab, long long* out,
+                               DevStatus* st, cudaStream_t s);
+// rmsnorm forward; in = bf16 or fp32 [n x h] -> out bf16 [n x h], r fp32 [n]
+cudaError_t launch_rmsnorm_fwd(const void* in, bool in_f32, const float* g, float eps,
+                               __nv_bfloat16* out, float* r, long long n, int h, cudaStream_t s);
+// rmsnorm backward: dz fp32, y (bf16/fp32), r, g -> dy bf16 (nullable), dg partials
+cudaError_t launch_rmsnorm_bwd(const float* dz, const void* y, bool y_f32, const float* r,
+                               const float* g, __nv_bfloat16* dy, float* dg_part, long long n,
+                               int h, int rows_per_block, cudaStream_t s);
+// gain grad: dg partials of sum_t du_t * x_t * r_t
+cudaError_t launch_gain_grad(const float* du, const __nv_bfloat16* x, const float* r,
+                             float* dg_part, long long n, int h, int rows_per_block,
+                             cudaStream_t s);
+cudaError_t launch_reduce_cols(const float* part, int nparts, int h, float* out, int accumulate,
+                               cudaStream_t s);
+cudaError_t launch_ce_finalize(const float* pm, const float* ps, const int32_t* pi,
+                               const float* tl, const int32_t* targets, int nb, long long n,
+                               const long long* valid_count, float alpha, float* lse, float* coef,
+                               float* aux_lse, float* aux_loss, int32_t* aux_argmax,
+                               float* aux_conf, float* loss_part, int nblocks, cudaStream_t s);
+cudaError_t launch_loss_reduce(const float* loss_part, int nparts, const long long* valid_count,
+                               float* loss_out, DevStatus* st, int exit_index, cudaStream_t s);
+constexpr int FINALIZE_THREADS = 256;
+
+// optimizer / init
+cudaError_t launch_adam(float* theta, __nv_bfloat16* op_bf16, float* op_f32, const float* grad,
+                        float* m, float* v, long long n, float lr, float b1, float b2, float eps,
+                        float wd, float bc1, float bc2, float gscale, cudaStream_t s);
+cudaError_t launch_sgd(float* theta, __nv_bfloat16* op_bf16, float* op_f32, const float* grad,
+                       float* buf, long long n, float lr, float mom, float gscale, cudaStream_t s);
+cudaError_t launch_copy_cast(const void* src, bool src_f32, float* master, __nv_bfloat16* op_bf16,
+                             float* op_f32, long long n, cudaStream_t s);
+cudaError_t launch_random_normal(uint64_t seed, uint64_t stream_id, float std, float* master,
+                                 __nv_bfloat16* op_bf16, long long n, cudaStream_t s);
+cudaError_t launch_fill(float* master, float* op_f32, long long n, float value, cudaStream_t s);
+
+}  // namespace ee

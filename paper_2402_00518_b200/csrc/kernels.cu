@@ -1,0 +1,543 @@
+// kernels.cu -- the bandwidth-bound kernels of the exit-head step:
+// RMSNorm forward/backward, gain gradients, cross-entropy
+// finalisation (merge of the per-tile online-softmax partials),
+// loss reduction, valid-token count, Adam/SGD and initialisers
+// (P:227-238).  All reductions are deterministic (fixed order, no float
+// atomics), so reruns are bitwise identical.
+#include <cfloat>
+#include <climits>
+#include "internal.cuh"
+
+namespace ee {
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&v)[8]) {
+  const uint4 q = *reinterpret_cast<const uint4*>(p);
+  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    v[2 * i] = bf16lo(w[i]);
+    v[2 * i + 1] = bf16hi(w[i]);
+  }
+}
+__device__ __forceinline__ void load8(const float* p, float (&v)[8]) {
+  const float4 a = *reinterpret_cast<const float4*>(p);
+  const float4 b = *reinterpret_cast<const float4*>(p + 4);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float (&v)[8]) {
+  uint4 q;
+  q.x = pack_bf16(v[0], v[1]);
+  q.y = pack_bf16(v[2], v[3]);
+  q.z = pack_bf16(v[4], v[5]);
+  q.w = pack_bf16(v[6], v[7]);
+  *reinterpret_cast<uint4*>(p) = q;
+}
+
+// Block-wide sum (deterministic: fixed shuffle tree, then warp 0 over warps).
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    T t = l < nw ? red[l] : T(0);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (l == 0) red[32] = t;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+// Each thread owns up to 2 chunks of 8 consecutive columns: h <= 16*blockDim.
+constexpr int NORM_CHUNKS = 2;
+static inline int norm_threads(int h) {
+  int t = (h / 8 + NORM_CHUNKS - 1) / NORM_CHUNKS;
+  return ((t + 31) / 32) * 32;
+}
+
+// ---------------------------------------------------------------- valid count
+__global__ void count_valid_kernel(const int32_t* __restrict__ y, long long n, int vocab,
+                                   long long* out, DevStatus* st) {
+  __shared__ long long red[33];
+  long long c = 0;
+  bool bad = false;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+    const int t = y[i];
+    c += (t != -1);
+    bad |= (t < -1 || t >= vocab);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) set_status(st, 4 /*EE_ERR_VOCAB*/, -1);
+  c = block_sum(c, red);
+  if (threadIdx.x == 0) out[0] = c;
+}
+
+cudaError_t launch_count_valid(const int32_t* targets, long long n, int vocab, long long* out,
+                               DevStatus* st, cudaStream_t s) {
+  count_valid_kernel<<<1, 1024, 0, s>>>(targets, n, vocab, out, st);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- RMSNorm fwd
+// out = g * x * r, r = rsqrt(mean x^2 + eps)   (A3)
+template <typename TIn>
+__global__ void rmsnorm_fwd_kernel(const TIn* __restrict__ in, const float* __restrict__ g,
+                                   float eps, __nv_bfloat16* __restrict__ out,
+                                   float* __restrict__ r, int h) {
+  __shared__ float red[33];
+  const long long row = blockIdx.x;
+  const int nchunk = h / 8;
+  float x[NORM_CHUNKS][8];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < NORM_CHUNKS; ++i) {
+    const int c = threadIdx.x + i * blockDim.x;
+    if (c < nchunk) {
+      load8(in + row * h + c * 8, x[i]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) ss += x[i][k] * x[i][k];
+    }
+  }
+  ss = block_sum(ss, red);
+  const float rr = 1.0f / sqrtf(ss / (float)h + eps);
+#pragma unroll
+  for (int i = 0; i < NORM_CHUNKS; ++i) {
+    const int c = threadIdx.x + i * blockDim.x;
+    if (c < nchunk) {
+      float gv[8], o[8];
+      load8(g + c * 8, gv);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) o[k] = gv[k] * (x[i][k] * rr);
+      store8(out + row * h + c * 8, o);
+    }
+  }
+  if (threadIdx.x == 0) r[row] = rr;
+}
+
+cudaError_t launch_rmsnorm_fwd(const void* in, bool in_f32, const float* g, float eps,
+                               __nv_bfloat16* out, float* r, long long n, int h, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const int t = norm_threads(h);
+  if (in_f32)
+    rmsnorm_fwd_kernel<float><<<(unsigned)n, t, 0, s>>>((const float*)in, g, eps, out, r, h);
+  else
+    rmsnorm_fwd_kernel<__nv_bfloat16>
+        <<<(unsigned)n, t, 0, s>>>((const __nv_bfloat16*)in, g, eps, out, r, h);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- RMSNorm bwd
+// yhat = y r; dg += dz * yhat; dy = r (g dz - yhat mean_j(g dz yhat))
+template <typename TY>
+__global__ void rmsnorm_bwd_kernel(const float* __restrict__ dz, const TY* __restrict__ y,
+                                   const float* __restrict__ r, const float* __restrict__ g,
+                                   __nv_bfloat16* __restrict__ dy, float* __restrict__ dg_part,
+                                   long long n, int h, int rpb) {
+  __shared__ float red[33];
+  const int nchunk = h / 8;
+  float gv[NORM_CHUNKS][8], acc[NORM_CHUNKS][8];
+#pragma unroll
+  for (int i = 0; i < NORM_CHUNKS; ++i) {
+    const int c = threadIdx.x + i * blockDim.x;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[i][k] = 0.f;
+    if (c < nchunk) load8(g + c * 8, gv[i]);
+  }
+  const long long r0 = (long long)blockIdx.x * rpb;
+  const long long r1 = min(n, r0 + rpb);
+  for (long long row = r0; row < r1; ++row) {
+    const float rr = r[row];
+    float d[NORM_CHUNKS][8], yh[NORM_CHUNKS][8];
+    float dot = 0.f;
+#pragma unroll
+    for (int i = 0; i < NORM_CHUNKS; ++i) {
+      const int c = threadIdx.x + i * blockDim.x;
+      if (c < nchunk) {
+        load8(dz + row * h + c * 8, d[i]);
+        load8(y + row * h + c * 8, yh[i]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          yh[i][k] *= rr;
+          dot += gv[i][k] * d[i][k] * yh[i][k];
+          acc[i][k] += d[i][k] * yh[i][k];
+        }
+      }
+    }
+    if (dy != nullptr) {
+      const float mean = block_sum(dot, red) / (float)h;
+#pragma unroll
+      for (int i = 0; i < NORM_CHUNKS; ++i) {
+        const int c = threadIdx.x + i * blockDim.x;
+        if (c < nchunk) {
+          float o[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) o[k] = rr * (gv[i][k] * d[i][k] - yh[i][k] * mean);
+          store8(dy + row * h + c * 8, o);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NORM_CHUNKS; ++i) {
+    const int c = threadIdx.x + i * blockDim.x;
+    if (c < nchunk) {
+      float* p = dg_part + (long long)blockIdx.x * h + c * 8;
+      *reinterpret_cast<float4*>(p) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+      *reinterpret_cast<float4*>(p + 4) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+    }
+  }
+}
+
+cudaError_t launch_rmsnorm_bwd(const float* dz, const void* y, bool y_f32, const float* r,
+                               const float* g, __nv_bfloat16* dy, float* dg_part, long long n,
+                               int h, int rpb, cudaStream_t s) {
+  const unsigned nb = (unsigned)((n + rpb - 1) / rpb);
+  if (nb == 0) return cudaSuccess;
+  const int t = norm_threads(h);
+  if (y_f32)
+    rmsnorm_bwd_kernel<float><<<nb, t, 0, s>>>(dz, (const float*)y, r, g, dy, dg_part, n, h, rpb);
+  else
+    rmsnorm_bwd_kernel<__nv_bfloat16>
+        <<<nb, t, 0, s>>>(dz, (const __nv_bfloat16*)y, r, g, dy, dg_part, n, h, rpb);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- gain grad
+// dg_a = sum_t du_t * (x_t r_t)   (no dx: the backbone is frozen)
+__global__ void gain_grad_kernel(const float* __restrict__ du, const __nv_bfloat16* __restrict__ x,
+                                 const float* __restrict__ r, float* __restrict__ dg_part,
+                                 long long n, int h, int rpb) {
+  const int nchunk = h / 8;
+  float acc[NORM_CHUNKS][8];
+#pragma unroll
+  for (int i = 0; i < NORM_CHUNKS; ++i)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[i][k] = 0.f;
+  const long long r0 = (long long)blockIdx.x * rpb;
+  const long long r1 = min(n, r0 + rpb);
+  for (long long row = r0; row < r1; ++row) {
+    const float rr = r[row];
+#pragma unroll
+    for (int i = 0; i < NORM_CHUNKS; ++i) {
+      const int c = threadIdx.x + i * blockDim.x;
+      if (c < nchunk) {
+        float d[8], xv[8];
+        load8(du + row * h + c * 8, d);
+        load8(x + row * h + c * 8, xv);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[i][k] += d[k] * (xv[k] * rr);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NORM_CHUNKS; ++i) {
+    const int c = threadIdx.x + i * blockDim.x;
+    if (c < nchunk) {
+      float* p = dg_part + (long long)blockIdx.x * h + c * 8;
+      *reinterpret_cast<float4*>(p) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+      *reinterpret_cast<float4*>(p + 4) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+    }
+  }
+}
+
+cudaError_t launch_gain_grad(const float* du, const __nv_bfloat16* x, const float* r,
+                             float* dg_part, long long n, int h, int rpb, cudaStream_t s) {
+  const unsigned nb = (unsigned)((n + rpb - 1) / rpb);
+  if (nb == 0) return cudaSuccess;
+  gain_grad_kernel<<<nb, norm_threads(h), 0, s>>>(du, x, r, dg_part, n, h, rpb);
+  return cudaGetLastError();
+}
+
+// Column sums of [nparts x h] partials in part order (deterministic).
+__global__ void reduce_cols_kernel(const float* __restrict__ part, int nparts, int h,
+                                   float* __restrict__ out, int accumulate) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= h) return;
+  float s = 0.f;
+  for (int p = 0; p < nparts; ++p) s += part[(long long)p * h + c];
+  out[c] = accumulate ? out[c] + s : s;
+}
+
+cudaError_t launch_reduce_cols(const float* part, int nparts, int h, float* out, int accumulate,
+                               cudaStream_t s) {
+  reduce_cols_kernel<<<(h + 255) / 256, 256, 0, s>>>(part, nparts, h, out, accumulate);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- CE finalize
+// Merge the per-V-tile (max, sum-exp, argmax) partials of each row:
+//   m = max_j m_j; s = sum_j s_j exp(m_j - m); lse = m + ln s;
+//   loss_t = lse - S[y_t]; conf_t = 1/s (max softmax prob);
+//   argmax = the argmax of the first tile attaining m (lowest index, A9);
+//   coef_t = alpha_i w_t / W (the dS scale).
+__global__ void ce_finalize_kernel(const float* __restrict__ pm, const float* __restrict__ ps,
+                                   const int32_t* __restrict__ pi, const float* __restrict__ tl,
+                                   const int32_t* __restrict__ targets, int nb, long long n,
+                                   const long long* __restrict__ valid_count, float alpha,
+                                   float* __restrict__ lse, float* __restrict__ coef,
+                                   float* aux_lse, float* aux_loss, int32_t* aux_argmax,
+                                   float* aux_conf, float* __restrict__ loss_part) {
+  __shared__ double red[33];
+  const long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  double lossv = 0.0;
+  if (row < n) {
+    float m = -INFINITY;
+    for (int j = 0; j < nb; ++j) m = fmaxf(m, pm[(long long)j * n + row]);
+    float s = 0.f;
+    int am = INT_MAX;
+    for (int j = 0; j < nb; ++j) {
+      const float mj = pm[(long long)j * n + row];
+      s += ps[(long long)j * n + row] * expf(mj - m);
+      if (mj == m && am == INT_MAX) am = pi[(long long)j * n + row];
+    }
+    const float l = m + logf(s);
+    const int y = targets[row];
+    const bool valid = y >= 0;
+    const float lt = valid ? l - tl[row] : 0.f;
+    const long long W = *valid_count;
+    lse[row] = l;
+    coef[row] = (valid && W > 0) ? alpha / (float)W : 0.f;
+    if (aux_lse) aux_lse[row] = l;
+    if (aux_loss) aux_loss[row] = lt;
+    if (aux_argmax) aux_argmax[row] = am;
+    if (aux_conf) aux_conf[row] = 1.0f / s;
+    lossv = (double)lt;
+  }
+  lossv = block_sum(lossv, red);
+  if (threadIdx.x == 0) loss_part[blockIdx.x] = (float)lossv;
+}
+
+cudaError_t launch_ce_finalize(const float* pm, const float* ps, const int32_t* pi,
+                               const float* tl, const int32_t* targets, int nb, long long n,
+                               const long long* valid_count, float alpha, float* lse, float* coef,
+                               float* aux_lse, float* aux_loss, int32_t* aux_argmax,
+                               float* aux_conf, float* loss_part, int nblocks, cudaStream_t s) {
+  if (nblocks == 0) return cudaSuccess;
+  ce_finalize_kernel<<<nblocks, FINALIZE_THREADS, 0, s>>>(pm, ps, pi, tl, targets, nb, n,
+                                                          valid_count, alpha, lse, coef, aux_lse,
+                                                          aux_loss, aux_argmax, aux_conf,
+                                                          loss_part);
+  return cudaGetLastError();
+}
+
+// L_i = sum_t w_t loss_t / W (A4, A16); non-finite -> EE_ERR_DIVERGED.
+__global__ void loss_reduce_kernel(const float* __restrict__ part, int nparts,
+                                   const long long* __restrict__ valid_count, float* loss_out,
+                                   DevStatus* st, int exit_index) {
+  __shared__ double red[33];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += (double)part[i];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) {
+    const long long W = *valid_count;
+    const float L = W > 0 ? (float)(s / (double)W) : 0.f;
+    *loss_out = L;
+    if (!isfinite(L)) set_status(st, 7 /*EE_ERR_DIVERGED*/, exit_index);
+  }
+}
+
+cudaError_t launch_loss_reduce(const float* loss_part, int nparts, const long long* valid_count,
+                               float* loss_out, DevStatus* st, int exit_index, cudaStream_t s) {
+  loss_reduce_kernel<<<1, 1024, 0, s>>>(loss_part, nparts, valid_count, loss_out, st, exit_index);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- optimizer
+static inline unsigned ew_blocks(long long n4) {
+  long long b = (n4 + 255) / 256;
+  const long long cap = (long long)num_sms() * 16;
+  return (unsigned)(b < cap ? (b > 0 ? b : 1) : cap);
+}
+
+// Adam (A14), 4 elements per thread-iteration.
+__global__ void adam_kernel(float* __restrict__ th, __nv_bfloat16* op_bf16, float* op_f32,
+                            const float* __restrict__ gr, float* __restrict__ m,
+                            float* __restrict__ v, long long n4, float lr, float b1, float b2,
+                            float eps, float wd, float bc1, float bc2, float gs) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    float4 t = reinterpret_cast<float4*>(th)[i];
+    const float4 g4 = reinterpret_cast<const float4*>(gr)[i];
+    float4 m4 = reinterpret_cast<float4*>(m)[i];
+    float4 v4 = reinterpret_cast<float4*>(v)[i];
+    float* tp = &t.x;
+    const float* gp = &g4.x;
+    float* mp = &m4.x;
+    float* vp = &v4.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float g = gs * gp[k];
+      mp[k] = b1 * mp[k] + (1.f - b1) * g;
+      vp[k] = b2 * vp[k] + (1.f - b2) * g * g;
+      const float upd = (mp[k] / bc1) / (sqrtf(vp[k] / bc2) + eps);
+      tp[k] = tp[k] - lr * upd - lr * wd * tp[k];
+    }
+    reinterpret_cast<float4*>(th)[i] = t;
+    reinterpret_cast<float4*>(m)[i] = m4;
+    reinterpret_cast<float4*>(v)[i] = v4;
+    if (op_bf16) {
+      uint2 q;
+      q.x = pack_bf16(t.x, t.y);
+      q.y = pack_bf16(t.z, t.w);
+      reinterpret_cast<uint2*>(op_bf16)[i] = q;
+    }
+    if (op_f32) reinterpret_cast<float4*>(op_f32)[i] = t;
+  }
+}
+
+cudaError_t launch_adam(float* theta, __nv_bfloat16* op_bf16, float* op_f32, const float* grad,
+                        float* m, float* v, long long n, float lr, float b1, float b2, float eps,
+                        float wd, float bc1, float bc2, float gscale, cudaStream_t s) {
+  const long long n4 = n / 4;
+  adam_kernel<<<ew_blocks(n4), 256, 0, s>>>(theta, op_bf16, op_f32, grad, m, v, n4, lr, b1, b2,
+                                            eps, wd, bc1, bc2, gscale);
+  return cudaGetLastError();
+}
+
+__global__ void sgd_kernel(float* __restrict__ th, __nv_bfloat16* op_bf16, float* op_f32,
+                           const float* __restrict__ gr, float* buf, long long n4, float lr,
+                           float mom, float gs) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    float4 t = reinterpret_cast<float4*>(th)[i];
+    float4 g4 = reinterpret_cast<const float4*>(gr)[i];
+    float* tp = &t.x;
+    float* gp = &g4.x;
+    if (buf) {
+      float4 b4 = reinterpret_cast<float4*>(buf)[i];
+      float* bp = &b4.x;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        bp[k] = mom * bp[k] + gs * gp[k];
+        gp[k] = bp[k];
+      }
+      reinterpret_cast<float4*>(buf)[i] = b4;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) gp[k] *= gs;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) tp[k] -= lr * gp[k];
+    reinterpret_cast<float4*>(th)[i] = t;
+    if (op_bf16) {
+      uint2 q;
+      q.x = pack_bf16(t.x, t.y);
+      q.y = pack_bf16(t.z, t.w);
+      reinterpret_cast<uint2*>(op_bf16)[i] = q;
+    }
+    if (op_f32) reinterpret_cast<float4*>(op_f32)[i] = t;
+  }
+}
+
+cudaError_t launch_sgd(float* theta, __nv_bfloat16* op_bf16, float* op_f32, const float* grad,
+                       float* buf, long long n, float lr, float mom, float gscale, cudaStream_t s) {
+  const long long n4 = n / 4;
+  sgd_kernel<<<ew_blocks(n4), 256, 0, s>>>(theta, op_bf16, op_f32, grad, buf, n4, lr, mom, gscale);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- initialisers
+// Copy: deep copy of the source module, widened to the fp32 master
+// and narrowed to the bf16 operand (exact when the source is bf16).
+template <typename TS>
+__global__ void copy_cast_kernel(const TS* __restrict__ src, float* master, __nv_bfloat16* op_bf16,
+                                 float* op_f32, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float v = (float)src[i];
+    if (master) master[i] = v;
+    if (op_bf16) op_bf16[i] = __float2bfloat16_rn(v);
+    if (op_f32) op_f32[i] = v;
+  }
+}
+
+cudaError_t launch_copy_cast(const void* src, bool src_f32, float* master, __nv_bfloat16* op_bf16,
+                             float* op_f32, long long n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  if (src_f32)
+    copy_cast_kernel<float><<<ew_blocks(n / 4 + 1), 256, 0, s>>>((const float*)src, master,
+                                                                  op_bf16, op_f32, n);
+  else
+    copy_cast_kernel<__nv_bfloat16><<<ew_blocks(n / 4 + 1), 256, 0, s>>>(
+        (const __nv_bfloat16*)src, master, op_bf16, op_f32, n);
+  return cudaGetLastError();
+}
+
+// Philox4x32-10 (Salmon et al. 2011), counter = (i, 0, stream lo, stream hi),
+// key = seed; Box-Muller on the 4 outputs -> 4 N(0,1) samples.
+__device__ __forceinline__ void philox4x32_10(uint32_t (&c)[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), lo0 = 0xD2511F53u * c[0];
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]), lo1 = 0xCD9E8D57u * c[2];
+    const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+__global__ void random_normal_kernel(uint64_t seed, uint64_t sid, float std, float* master,
+                                     __nv_bfloat16* op_bf16, long long n) {
+  const long long n4 = (n + 3) / 4;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    uint32_t c[4] = {(uint32_t)i, (uint32_t)(i >> 32), (uint32_t)sid, (uint32_t)(sid >> 32)};
+    philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+    float z[4];
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const float u1 = ((float)c[2 * p] + 1.0f) * 2.3283064365386963e-10f;  // (0, 1]
+      const float u2 = (float)c[2 * p + 1] * 2.3283064365386963e-10f;       // [0, 1)
+      const float rad = sqrtf(-2.0f * logf(u1));
+      float sn, cs;
+      sincospif(2.0f * u2, &sn, &cs);
+      z[2 * p] = rad * cs;
+      z[2 * p + 1] = rad * sn;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const long long j = i * 4 + k;
+      if (j < n) {
+        const float w = std * z[k];
+        const __nv_bfloat16 b = __float2bfloat16_rn(w);
+        // master on the bf16 grid so operand == master exactly at t = 0
+        if (master) master[j] = __bfloat162float(b);
+        if (op_bf16) op_bf16[j] = b;
+      }
+    }
+  }
+}
+
+cudaError_t launch_random_normal(uint64_t seed, uint64_t stream_id, float std, float* master,
+                                 __nv_bfloat16* op_bf16, long long n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  random_normal_kernel<<<ew_blocks(n / 4 + 1), 256, 0, s>>>(seed, stream_id, std, master, op_bf16,
+                                                            n);
+  return cudaGetLastError();
+}
+
+__global__ void fill_kernel(float* a, float* b, long long n, float v) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (a) a[i] = v;
+    if (b) b[i] = v;
+  }
+}
+
+cudaError_t launch_fill(float* master, float* op_f32, long long n, float value, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  fill_kernel<<<ew_blocks(n / 4 + 1), 256, 0, s>>>(master, op_f32, n, value);
+  return cudaGetLastError();
+}
+
+}  // namespace ee

@@ -1,0 +1,66 @@
+"""CPU-only checks of the C-ABI library: it loads without a GPU, exports every
+symbol include/ee.h declares, and its pure host functions / argument
+validation behave (no compute calls)."""
+
+import ctypes
+import math
+import os
+import re
+
+import pytest
+
+import paper_2402_00518_b200 as ee
+from oracle import ee_oracle as O
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "ee.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ee_[a-z_]+)\s*\(", src)))
+
+
+def test_library_loads_and_exports_header_symbols():
+    if not os.path.exists(ee.LIB_PATH):
+        from paper_2402_00518_b200 import build
+        build.build()
+    lib = ee.load()
+    names = _declared()
+    assert "ee_tune_step" in names and "ee_init_heads" in names and "ee_adam_update" in names
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(ee.EXPORTED) == set(names)
+
+
+def test_lr_schedule_host_function_matches_oracle_pins():
+    ee.load()
+    T = 40000
+    for it in (0, 1, 200, 400, 401, 20000, 39999, 40000):
+        assert ee.ee_lr_at(it, T) == pytest.approx(O.lr_at(it, T), rel=1e-12, abs=1e-18)
+    assert ee.ee_lr_at(400, T) == pytest.approx(1e-4)        # P:375 max
+    assert ee.ee_lr_at(T, T) == pytest.approx(1e-5)          # P:375 min
+    assert math.isnan(ee.ee_lr_at(T + 1, T))
+
+
+def test_workspace_size_and_shape_validation():
+    ee.load()
+    c = ee.make_config(8192, 32000, 28672, 4, "mlp")
+    ws = ee.ee_workspace_size(c, 65536)
+    assert 20e9 < ws < 30e9                                   # ~23 GB at the 70B shape
+    assert ee.ee_workspace_size(c, 0) < 1 << 20
+    for bad in (ee.make_config(100, 512, 0, 1, "norm"),      # h not multiple of 64
+                ee.make_config(128, 512, 100, 1, "mlp"),     # F not multiple of 128
+                ee.make_config(128, 510, 0, 1, "norm"),      # V not multiple of 8
+                ee.make_config(128, 512, 0, 0, "norm")):     # no exits
+        with pytest.raises(ee.EEError):
+            ee.ee_workspace_size(bad, 10)
+
+
+def test_null_arguments_rejected_before_any_device_work():
+    lib = ee.load()
+    c = ee.make_config(128, 512, 0, 1, "norm")
+    r = lib.ee_tune_step(ctypes.byref(c), None, 10, None, None, None, None, 0, None, None, None,
+                         None, 0, None)
+    assert r == 1                                             # EE_ERR_ARG
+    assert b"NULL" in lib.ee_last_error()

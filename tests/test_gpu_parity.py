@@ -1,0 +1,164 @@
+"""Parity of the CUDA exit-head step with the fp64 oracle (north_star tolerances).
+
+Sizes: the tiny config in full; small shapes spanning several tiles with
+ragged token/vocab tails; and the 7B / 13B / 70B head shapes (full h, V, F) on
+a token subsample the oracle finishes in seconds.  Full-size runs in the
+bench's launch configuration are in test_gpu_fullsize.py.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import eesynth as S
+from harness import compare_exit, gpu_step, oracle_exit
+from oracle import ee_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_and_compare(ee, cfg, n, weights, seed=0, params=None, ignore_frac=1 / 64):
+    hidden = S.hidden_states(cfg, n, seed=seed)
+    targets = S.targets(cfg, n, seed=seed, ignore_frac=ignore_frac)
+    if params is None:
+        params = S.head_params(cfg, seed=seed)
+    loss, grads, aux, status = gpu_step(ee, cfg, hidden, targets, params, weights)
+    assert status == (0, -1), status
+    errs = []
+    for i in range(cfg.exits):
+        res = oracle_exit(cfg.arch, params[i], hidden[i], targets, weights[i])
+        errs.append(compare_exit(cfg.arch, res, loss[i].item(), grads[i], aux[i], targets,
+                                 tag=f"{cfg.name}[{i}]"))
+    return errs
+
+
+def test_tiny_config_full(gpu_lib):
+    """BASELINE configs[0]: h 64, V 512, 2 Norm exits, 256 tokens."""
+    cfg = S.get_cfg("tiny")
+    _run_and_compare(gpu_lib, cfg, cfg.tokens, [1.0, 0.5])
+
+
+@pytest.mark.parametrize("arch,h,V,F,n", [
+    ("embedding", 192, 2056, 0, 77),
+    ("norm", 128, 1000, 0, 300),
+    ("mlp", 128, 1000, 384, 300),
+    ("mlp", 256, 4104, 512, 1000),
+])
+def test_small_ragged(gpu_lib, arch, h, V, F, n):
+    cfg = S.Cfg(name="small", hidden=h, vocab=V, ffn=F, arch=arch, tokens=n, layers=2,
+                after=[1, 2], init="random", seed=11)
+    _run_and_compare(gpu_lib, cfg, n, [1.0, 0.75])
+
+
+@pytest.mark.parametrize("name,n,exits", [("7b", 256, 2), ("13b", 192, 2), ("70b", 128, 1)])
+def test_llama_shapes_token_subsample(gpu_lib, name, n, exits):
+    cfg = S.get_cfg(name)
+    cfg.after = cfg.after[:exits]
+    cfg.exits = exits
+    errs = _run_and_compare(gpu_lib, cfg, n, [1.0] * exits)
+    print(name, errs)
+
+
+def test_zero_alpha_and_all_ignored(gpu_lib):
+    """alpha = 0 -> gradients exactly 0; all targets ignored -> loss 0, grads 0 (P12)."""
+    cfg = S.Cfg(name="small", hidden=128, vocab=512, ffn=256, arch="mlp", tokens=200, layers=2,
+                after=[1, 2], init="random", seed=5)
+    hidden = S.hidden_states(cfg, 200)
+    targets = S.targets(cfg, 200)
+    params = S.head_params(cfg)
+    loss, grads, aux, st = gpu_step(gpu_lib, cfg, hidden, targets, params, [0.0, 1.0])
+    assert st == (0, -1)
+    for k, g in grads[0].items():
+        assert torch.count_nonzero(g).item() == 0, k
+    assert loss[0].item() > 0
+    t2 = torch.full((200,), -1, dtype=torch.int32)
+    loss, grads, aux, st = gpu_step(gpu_lib, cfg, hidden, t2, params, [1.0, 1.0])
+    assert st == (0, -1)
+    assert torch.all(loss == 0)
+    for gd in grads:
+        for k, g in gd.items():
+            assert torch.count_nonzero(g).item() == 0, k
+
+
+def test_uniform_logits_closed_form(gpu_lib):
+    """W_out = 0 -> loss = ln V exactly-ish, conf = 1/V, dz = 0 so every MLP and
+    gain gradient is exactly zero on the GPU too (P3)."""
+    cfg = S.Cfg(name="small", hidden=128, vocab=1024, ffn=256, arch="mlp", tokens=256, layers=2,
+                after=[1], init="random", seed=6)
+    hidden = S.hidden_states(cfg, 256)
+    targets = S.targets(cfg, 256)
+    params = S.head_params(cfg)
+    params[0]["w_out"].zero_()
+    loss, grads, aux, st = gpu_step(gpu_lib, cfg, hidden, targets, params, [1.0])
+    assert abs(loss[0].item() - np.log(1024)) < 1e-5
+    assert torch.allclose(aux[0]["conf"], torch.full_like(aux[0]["conf"], 1 / 1024))
+    for k in ("g_a", "w_gate", "w_up", "w_down", "g_f"):
+        assert torch.count_nonzero(grads[0][k]).item() == 0, k
+
+
+def test_accumulate_and_determinism(gpu_lib):
+    cfg = S.Cfg(name="small", hidden=128, vocab=1000, ffn=256, arch="mlp", tokens=300, layers=2,
+                after=[1], init="random", seed=7)
+    hidden = S.hidden_states(cfg, 300)
+    targets = S.targets(cfg, 300)
+    params = S.head_params(cfg)
+    l1, g1, _, _ = gpu_step(gpu_lib, cfg, hidden, targets, params, [1.0])
+    l2, g2, _, _ = gpu_step(gpu_lib, cfg, hidden, targets, params, [1.0])
+    assert torch.equal(l1, l2)
+    for k in g1[0]:
+        assert torch.equal(g1[0][k], g2[0][k]), k                  # bitwise rerun
+    g3 = [{k: v.clone() for k, v in g1[0].items()}]
+    gpu_step(gpu_lib, cfg, hidden, targets, params, [1.0], accumulate=True, grads=g3)
+    for k in g1[0]:
+        torch.testing.assert_close(g3[0][k], 2 * g1[0][k], rtol=1e-6, atol=0)
+
+
+def test_exit_independence(gpu_lib):
+    """Exit A's loss and grads are bitwise the same with or without exit B (P11)."""
+    cfg = S.Cfg(name="small", hidden=128, vocab=1000, ffn=256, arch="mlp", tokens=300, layers=2,
+                after=[1, 2], init="random", seed=8)
+    hidden = S.hidden_states(cfg, 300)
+    targets = S.targets(cfg, 300)
+    params = S.head_params(cfg)
+    l2, g2, _, _ = gpu_step(gpu_lib, cfg, hidden, targets, params, [1.0, 1.0])
+    one = S.Cfg(name="small", hidden=128, vocab=1000, ffn=256, arch="mlp", tokens=300, layers=2,
+                after=[1], init="random", seed=8)
+    l1, g1, _, _ = gpu_step(gpu_lib, one, hidden[:1], targets, params[:1], [1.0])
+    assert torch.equal(l1[0], l2[0])
+    for k in g1[0]:
+        assert torch.equal(g1[0][k], g2[0][k]), k
+
+
+def test_inputs_unchanged(gpu_lib):
+    """Frozen backbone contract: hidden states and parameters are read-only."""
+    cfg = S.Cfg(name="small", hidden=128, vocab=1000, ffn=256, arch="mlp", tokens=300, layers=2,
+                after=[1], init="random", seed=9)
+    hidden = [h.cuda() for h in S.hidden_states(cfg, 300)]
+    h0 = [h.clone() for h in hidden]
+    targets = S.targets(cfg, 300)
+    params = [{k: v.cuda() for k, v in p.items()} for p in S.head_params(cfg)]
+    p0 = [{k: v.clone() for k, v in p.items()} for p in params]
+    gpu_step(gpu_lib, cfg, hidden, targets, params, [1.0])
+    assert all(torch.equal(a, b) for a, b in zip(hidden, h0))
+    for p, q in zip(params, p0):
+        for k in p:
+            assert torch.equal(p[k], q[k])
+
+
+def test_device_errors(gpu_lib):
+    ee = gpu_lib
+    cfg = S.Cfg(name="small", hidden=128, vocab=512, ffn=0, arch="norm", tokens=64, layers=2,
+                after=[1], init="random", seed=10)
+    hidden = S.hidden_states(cfg, 64)
+    params = S.head_params(cfg)
+    bad = S.targets(cfg, 64)
+    bad[5] = 512                                                    # == V: out of range
+    _, _, _, st = gpu_step(ee, cfg, hidden, bad, params, [1.0])
+    assert st[0] == 4                                               # EE_ERR_VOCAB
+    h_nan = [hidden[0].clone()]
+    h_nan[0][3, :] = float("inf")
+    _, _, _, st = gpu_step(ee, cfg, h_nan, S.targets(cfg, 64), params, [1.0])
+    assert st == (7, 0)                                             # EE_ERR_DIVERGED, exit 0
+    with pytest.raises(ee.EEError):
+        c = ee.make_config(100, 512, 0, 1, "norm")                  # h not a multiple of 64
+        ee.ee_workspace_size(c, 10)
