@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""bench.py -- EE-Tuning exit-head tuning step on B200 (BASELINE.json metric).
+
+One "step" = one pass of the whole hot path: for every
+exit, the exit-head forward, softmax cross-entropy, backward into the exit
+parameters (ee_tune_step), plus the Adam update of all exit parameters
+(ee_adam_update).  Default workload (N=1): the 70B-shaped head set of
+BASELINE.json configs[3] (h 8192, V 32000, F 28672, 4 MLP exits, 32 x 2048
+tokens), unsharded W_out; synthetic seeded inputs (eesynth), Copy init from a
+synthetic backbone.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun, one process per GPU): data parallel over tokens, 32 x 2048
+tokens per GPU (weak scaling); the global valid-token count and every exit's
+gradients are all-reduced over NCCL, each exit's all-reduce overlapping the
+next exit's compute.  Rank 0 prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+METRIC = "exit-head tuning tokens/s and % bf16 tensor-core peak at 1/2/4/8 B200"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]),
+                "bf16_tflops_sustained": float(d.get("bf16_tflops_sustained", d["bf16_tflops"])),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return dict(PEAKS_FALLBACK, source="fallback (B200_PROFILING.md)")
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms in a thread."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 7:
+                self.rows.append(f)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = self.rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[0]) for r in rows if num(r[0])]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[3:7]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": num(rows[0][1]), "samples": len(rows),
+                "power_w_max": max((num(r[2]) or 0) for r in rows), "reasons": reasons}
+
+
+def step_flops(cfg, n):
+    """Algorithmic FLOPs of one step: 6hV (+18hF for MLP) per
+    token per exit; Embedding exits have no dz GEMM (4hV)."""
+    h, V, F = cfg.hidden, cfg.vocab, cfg.ffn
+    per = (4 if cfg.arch == "embedding" else 6) * h * V + (18 * h * F if cfg.arch == "mlp" else 0)
+    return per * n * cfg.exits
+
+
+def cpu_oracle_sample(cfg, n_sub, seed):
+    """Times the fp64 oracle (as it stands) on a bounded sample of the workload:
+    the first exit on n_sub tokens at full h, V, F.  Returns (seconds, cores)."""
+    import numpy as np
+    import torch
+    import eesynth as S
+    from eesynth import to_f64
+    from oracle import ee_oracle as O
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] or [os.cpu_count()])
+    except Exception:
+        cores = os.cpu_count()
+    one = S.Cfg(name=cfg.name, hidden=cfg.hidden, vocab=cfg.vocab, ffn=cfg.ffn, arch=cfg.arch,
+                tokens=n_sub, layers=cfg.layers, after=cfg.after[:1], init=cfg.init, seed=cfg.seed)
+    p = S.head_params(one, seed=seed)[0]
+    p64 = {}
+    for k in list(p):
+        p64[k] = to_f64(p.pop(k))
+    x = to_f64(S.hidden_states(one, n_sub, seed=seed)[0])
+    y = S.targets(one, n_sub, seed=seed).numpy().astype(np.int64)
+    t0 = time.perf_counter()
+    O.exit_loss_and_grads(cfg.arch, p64, x, y, 1.0, 1e-5)
+    return time.perf_counter() - t0, cores
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the oracle on the host cores (bounded sample per step)."""
+    if rank != 0:
+        return
+    n_sub = args.cpu_tokens
+    times = []
+    cores = None
+    for i in range(args.warmup + args.steps):
+        t, cores = cpu_oracle_sample(cfg, n_sub, seed=cfg.seed)
+        if i >= args.warmup:
+            times.append(t)
+    t_step = statistics.mean(times) * cfg.exits       # all exits of the step
+    value = n_sub / t_step
+    sample = (f"fp64 oracle, exit 1 of {cfg.exits} on {n_sub} tokens at full h/V/F, "
+              f"scaled x{cfg.exits} exits; Adam not included")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(cfg, 1, args),
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores,
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(cfg, world, args):
+    return {"workload": f"{cfg.name}: h {cfg.hidden}, V {cfg.vocab}, F {cfg.ffn}, "
+                        f"{cfg.exits} {cfg.arch} exits, {cfg.tokens} tokens/GPU, "
+                        f"{cfg.init} init, W_out unsharded",
+            "global_batch": (cfg.tokens // 2048) * world, "seq_len": 2048,
+            "tokens_per_gpu": cfg.tokens, "exits": cfg.exits,
+            "parallelism": f"dp{world}",
+            "l2": "inputs larger than L2 (hidden states + exit weights per step >> 126 MB)",
+            "optimizer": "Adam (P:374-375), included in the step"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="70b")
+    ap.add_argument("--tokens", type=int, default=0, help="override tokens per GPU")
+    ap.add_argument("--cpu-tokens", type=int, default=32)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="ncu/profiling run: no extras")
+    args = ap.parse_args()
+
+    import torch
+    import torch.distributed as dist
+    import eesynth as S
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = S.get_cfg(args.config)
+    if args.tokens:
+        cfg.tokens = args.tokens
+    args.warmup = max(args.warmup, 3 if not args.quick else args.warmup)
+
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    import paper_2402_00518_b200 as ee
+    ee.load()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    dp = world > 1
+    n = cfg.tokens
+    E = cfg.exits
+
+    # ---- parameter store, Copy init from a synthetic backbone
+    heads = ee.ExitHeads(ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch), n, device=dev)
+    bb = S.backbone(cfg, device=dev)
+    src = []
+    for k in cfg.after:
+        d = {"w_out": bb["w_out"]}
+        if cfg.arch in ("norm", "mlp"):
+            d["g_f"] = bb["final_norm"]
+        if cfg.arch == "mlp":
+            L = bb["layers"][k]
+            d.update(g_a=L["mlp_norm"], w_gate=L["w_gate"], w_up=L["w_up"], w_down=L["w_down"])
+        src.append(d)
+    heads.init("copy", copy_src=src)
+    torch.cuda.synchronize()
+    del src, bb
+    torch.cuda.empty_cache()
+
+    hidden = S.hidden_states(cfg, n, seed=cfg.seed * 100 + rank, device=dev)
+    targets = S.targets(cfg, n, seed=cfg.seed * 100 + rank, device=dev)
+    vc = torch.zeros(1, dtype=torch.int64, device=dev)
+    total_iters = 40000
+    one_cfg = ee.make_config(cfg.hidden, cfg.vocab, cfg.ffn, 1, cfg.arch)
+
+    def step(it, hid=hidden, tg=targets):
+        lr = ee.ee_lr_at(min(it + 1, total_iters), total_iters)
+        if not dp:
+            heads.step(hid, tg)
+        else:
+            ee.ee_count_valid(tg, cfg.vocab, vc, heads.workspace)
+            dist.all_reduce(vc)                           # global W (A16)
+            handles = []
+            for i in range(E):                            # per exit: compute, then async all-reduce
+                ee.ee_tune_step(one_cfg, hid[i:i + 1], tg, [1.0], heads.operand[i:i + 1],
+                                heads.grads[i:i + 1], heads.loss[i:i + 1], heads.workspace,
+                                valid_count=vc)
+                for t in heads.grads[i].values():
+                    handles.append(dist.all_reduce(t, async_op=True))
+            handles.append(dist.all_reduce(heads.loss, async_op=True))
+            for hd in handles:
+                hd.wait()
+        heads.adam(lr)
+
+    for it in range(args.warmup):
+        step(it)
+    torch.cuda.synchronize()
+    if dp:
+        dist.barrier()
+
+    # ---- timed region (device time, CUDA events on the launching stream)
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    l0 = ee.ee_launch_count()
+    ee.ee_profile_start()
+    torch.cuda.synchronize()
+    if dp:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for it in range(args.steps):
+        step(args.warmup + it)
+    e1.record()
+    torch.cuda.synchronize()
+    if dp:
+        dist.barrier()
+    prof = ee.ee_profile_stop()
+    launches = ee.ee_launch_count() - l0
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], device=dev)
+    if dp:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.item()
+    code, idx = heads.status()
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e and not args.quick:
+        h_host = [h.cpu().pin_memory() for h in hidden]
+        t_host = targets.cpu().pin_memory()
+        loss_host = torch.empty(E, dtype=torch.float32).pin_memory()
+        torch.cuda.synchronize()
+        if dp:
+            dist.barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for it in range(args.steps):
+            for d_, h_ in zip(hidden, h_host):
+                d_.copy_(h_, non_blocking=True)
+            targets.copy_(t_host, non_blocking=True)
+            step(args.warmup + args.steps + it)
+            loss_host.copy_(heads.loss, non_blocking=True)
+        a1.record()
+        torch.cuda.synchronize()
+        te = torch.tensor([a0.elapsed_time(a1) / args.steps], device=dev)
+        if dp:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": n * world / (te.item() / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": sum(h.numel() * 2 for h in hidden) + targets.numel() * 4,
+               "d2h_bytes_per_step": E * 4, "ms_per_step": te.item()}
+        del h_host
+
+    if rank != 0:
+        if dp:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---- per-kernel breakdown of the timed region
+    peaks = load_peaks()
+    kern = {}
+    for name, kms, fe, fa, by in prof:
+        d = kern.setdefault(name, {"launches": 0, "ms": 0.0, "flops_exec": 0.0, "flops_alg": 0.0,
+                                   "bytes": 0.0})
+        d["launches"] += 1
+        d["ms"] += kms
+        d["flops_exec"] += fe
+        d["flops_alg"] += fa
+        d["bytes"] += by
+    step_ms_sum = sum(d["ms"] for d in kern.values())
+    kernels = {}
+    for name, d in sorted(kern.items(), key=lambda kv: -kv[1]["ms"]):
+        e = {"launches_per_step": d["launches"] / args.steps, "ms_per_launch": d["ms"] / d["launches"],
+             "share": d["ms"] / step_ms_sum if step_ms_sum else None}
+        if d["flops_exec"]:
+            e["tflops_exec"] = d["flops_exec"] / (d["ms"] / 1e3) / 1e12
+        if d["bytes"]:
+            e["gbs"] = d["bytes"] / (d["ms"] / 1e3) / 1e9
+        kernels[name] = e
+    gemms = {k: v for k, v in kern.items() if v["flops_alg"] > 0}
+    dom = max(gemms, key=lambda k: gemms[k]["ms"]) if gemms else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if dom and os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(dom)
+        except Exception:
+            traffic = None
+    roofline = None
+    if dom:
+        d = gemms[dom]
+        per_launch_flops = d["flops_alg"] / d["launches"]
+        ach = per_launch_flops / (d["ms"] / d["launches"] / 1e3) / 1e12
+        roofline = {"bound": "tensor", "kernel": dom, "achieved": ach,
+                    "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                    "frac": ach / peaks["bf16_tflops_sustained"], "traffic": traffic,
+                    "algorithmic_flops_per_launch": per_launch_flops,
+                    "peak_source": peaks["source"] + ", sustained (kernel timed inside a long step)"}
+
+    F_alg = step_flops(cfg, n)
+    tflops = F_alg / (ms / 1e3) / 1e12
+    value = n * world / (ms / 1e3)
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (seeded eesynth inputs, Copy init from a synthetic backbone)",
+        "config": workload_config(cfg, world, args),
+        "pct_peak": {"algorithmic_tflops_per_gpu": tflops,
+                     "of_burst": tflops / peaks["bf16_tflops"],
+                     "of_sustained": tflops / peaks["bf16_tflops_sustained"],
+                     "of_datasheet_2250": tflops / 2250.0,
+                     "step_flops_alg": F_alg},
+        "roofline": roofline,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "status": code,
+        "kernels": kernels,
+    }
+    if world == 1 and not args.no_cpu_baseline and not args.quick:
+        try:
+            t_or, cores = cpu_oracle_sample(cfg, args.cpu_tokens, seed=cfg.seed)
+            v = args.cpu_tokens / (t_or * E)
+            line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                                    "sample": f"fp64 oracle, exit 1 of {E} on {args.cpu_tokens} "
+                                              f"tokens at full h/V/F ({t_or:.1f} s), scaled "
+                                              f"x{E} exits"}
+        except Exception as ex:  # never let the baseline kill the GPU number
+            line["cpu_baseline"] = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(),
+                                    "kind": "oracle", "sample": f"failed: {ex!r}"}
+    print(json.dumps(line), flush=True)
+    if dp:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

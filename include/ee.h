@@ -203,6 +203,19 @@ const char* ee_last_error(void);
 /* Library version string. */
 const char* ee_version(void);
 
+/* ---- instrumentation (process-global; used by bench.py) ----
+ * Between ee_profile_start() and ee_profile_stop(), every kernel launch the
+ * library makes is bracketed by a CUDA event pair on its stream.
+ * ee_profile_record(i, ...) returns launch i's name (copied into name[0..len)),
+ * its device duration in ms (synchronises that event), and its executed FLOPs,
+ * algorithmic FLOPs (the recompute GEMM counts 0) and algorithmic HBM bytes.
+ * ee_launch_count() = total kernel launches made by the library so far. */
+ee_status ee_profile_start(void);
+ee_status ee_profile_stop(int32_t* count);
+ee_status ee_profile_record(int32_t i, char* name, int32_t name_len, float* ms, double* flops_exec,
+                            double* flops_alg, double* bytes);
+int64_t ee_launch_count(void);
+
 /* ---- testing hook (used by the GPU parity tests; not part of the step) ----
  * C[M x N] (fp32 row-major, device) = A B^T  (or += if accumulate), where the
  * bf16 device operands are stored A: [M x K] if a_kmajor else [K x M];

@@ -29,7 +29,8 @@ DTYPE = {torch.bfloat16: 0, torch.float32: 1}
 TENSOR_NAMES = ("g_a", "w_gate", "w_up", "w_down", "g_f", "w_out")
 EXPORTED = ("ee_workspace_size", "ee_init_heads", "ee_tune_step", "ee_count_valid",
             "ee_adam_update", "ee_sgd_update", "ee_get_status", "ee_lr_at", "ee_last_error",
-            "ee_version", "ee_test_gemm")
+            "ee_version", "ee_test_gemm", "ee_profile_start", "ee_profile_stop",
+            "ee_profile_record", "ee_launch_count")
 
 
 class EEError(RuntimeError):
@@ -84,6 +85,13 @@ def load(path: str = LIB_PATH):
         "ee_last_error": (ctypes.c_char_p, []),
         "ee_version": (ctypes.c_char_p, []),
         "ee_test_gemm": (I32, [I32, I32, P, P, P, I32, I32, I32, I32, P]),
+        "ee_profile_start": (I32, []),
+        "ee_profile_stop": (I32, [ctypes.POINTER(I32)]),
+        "ee_profile_record": (I32, [I32, ctypes.c_char_p, I32, ctypes.POINTER(F32),
+                                    ctypes.POINTER(ctypes.c_double),
+                                    ctypes.POINTER(ctypes.c_double),
+                                    ctypes.POINTER(ctypes.c_double)]),
+        "ee_launch_count": (I64, []),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -206,6 +214,32 @@ def ee_test_gemm(A, B, C, a_kmajor, b_kmajor, M, N, K, accumulate=False, stream=
     load()
     _check(_lib.ee_test_gemm(int(a_kmajor), int(b_kmajor), _ptr(A), _ptr(B), _ptr(C), M, N, K,
                              int(bool(accumulate)), _stream(stream)))
+
+
+def ee_profile_start():
+    load()
+    _check(_lib.ee_profile_start())
+
+
+def ee_profile_stop():
+    """Stop recording; returns [(name, ms, flops_exec, flops_alg, bytes)] per launch."""
+    load()
+    n = ctypes.c_int32(0)
+    _check(_lib.ee_profile_stop(ctypes.byref(n)))
+    out = []
+    buf = ctypes.create_string_buffer(64)
+    ms = ctypes.c_float(0)
+    fe, fa, by = ctypes.c_double(0), ctypes.c_double(0), ctypes.c_double(0)
+    for i in range(n.value):
+        _check(_lib.ee_profile_record(i, buf, 64, ctypes.byref(ms), ctypes.byref(fe),
+                                      ctypes.byref(fa), ctypes.byref(by)))
+        out.append((buf.value.decode(), ms.value, fe.value, fa.value, by.value))
+    return out
+
+
+def ee_launch_count() -> int:
+    load()
+    return int(_lib.ee_launch_count())
 
 
 # ---------------------------------------------------------------------------

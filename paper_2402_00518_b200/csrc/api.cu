@@ -23,6 +23,7 @@
 #include <cstdarg>
 #include <cstring>
 #include <string>
+#include <vector>
 #include "../../include/ee.h"
 #include "internal.cuh"
 
@@ -152,6 +153,49 @@ ee_status check_arch_tensors(const ee_head_config* c, const ee_head_tensors& t, 
   return EE_OK;
 }
 
+
+// ---------------------------------------------------------------- profiler
+// Optional per-launch CUDA-event timing (ee_profile_*): one event pair per
+// kernel launch, recorded on the launching stream, so bench.py can report the
+// duration and algorithmic FLOPs / bytes of each kernel inside its timed region.
+struct ProfRec {
+  const char* name;
+  cudaEvent_t a, b;
+  double flops_exec, flops_alg, bytes;
+};
+std::vector<ProfRec> g_prof;
+std::vector<cudaEvent_t> g_event_pool;
+bool g_prof_on = false;
+long long g_launches = 0;
+
+cudaEvent_t pool_event() {
+  if (!g_event_pool.empty()) {
+    cudaEvent_t e = g_event_pool.back();
+    g_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct Prof {
+  bool on;
+  size_t idx;
+  cudaStream_t st;
+  Prof(const char* name, cudaStream_t s, double fe, double fa, double by) : on(g_prof_on), st(s) {
+    ++g_launches;
+    if (!on) return;
+    ProfRec r{name, pool_event(), pool_event(), fe, fa, by};
+    cudaEventRecord(r.a, st);
+    idx = g_prof.size();
+    g_prof.push_back(r);
+  }
+  ~Prof() {
+    if (on) cudaEventRecord(g_prof[idx].b, st);
+  }
+};
+
 GemmArgs base_args(int M, int N, int K) {
   GemmArgs a;
   memset(&a, 0, sizeof(a));
@@ -245,7 +289,8 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
   const int h = cfg->hidden, F = cfg->ffn, Vl = cfg->vocab_end - cfg->vocab_begin;
   const bool mlp = cfg->arch == EE_ARCH_MLP, nrm = cfg->arch != EE_ARCH_EMBEDDING;
 
-  EE_CUDA(launch_count_valid(targets, n, cfg->vocab, vc_local, status, st));
+  { Prof p_("count_valid", st, 0, 0, 4.0 * n);
+  EE_CUDA(launch_count_valid(targets, n, cfg->vocab, vc_local, status, st)); }
   const long long* vc = valid_count ? (const long long*)valid_count : vc_local;
 
   if (n == 0) {
@@ -291,7 +336,8 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
 
     if (mlp) {
       // a1: u = RMSNorm_a(x)
-      EE_CUDA(launch_rmsnorm_fwd(x, false, (const float*)P.g_a, cfg->norm_eps, u, rx, n, h, st));
+      { Prof p_("a1_rmsnorm_fwd", st, 0, 0, 4.0 * n * h + 4.0 * n);
+      EE_CUDA(launch_rmsnorm_fwd(x, false, (const float*)P.g_a, cfg->norm_eps, u, rx, n, h, st)); }
       // a2: [A|B] = u [W_gate|W_up]^T (paired B tiles), M = silu(A) * B
       {
         GemmArgs a = base_args((int)n, F, h);
@@ -301,6 +347,7 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
         a.ld_m = F;
         a.ffn = F;
         Mat A{u, n, h, h}, B0{P.w_gate, F, h, h}, B1{P.w_up, F, h, h};
+        Prof p_("a2_gateup_swiglu", st, 4.0 * n * F * h, 4.0 * n * F * h, 0);
         EE_CUDA(gemm_run(EPI_SWIGLU_FWD, true, true, A, B0, &B1, B_PAIR, 0, a, st));
       }
       // a3: y = x + M W_down^T  (fp32 residual stream, A15)
@@ -311,13 +358,16 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
         a.resid = x;
         a.ld_resid = h;
         Mat A{mact, n, F, F}, B{P.w_down, h, F, F};
+        Prof p_("a3_down_resid", st, 2.0 * n * F * h, 2.0 * n * F * h, 0);
         EE_CUDA(gemm_run(EPI_RESID, true, true, A, B, nullptr, B_PLAIN, 0, a, st));
       }
       // a4: z = RMSNorm_f(y)
-      EE_CUDA(launch_rmsnorm_fwd(y, true, (const float*)P.g_f, cfg->norm_eps, zbuf, ry, n, h, st));
+      { Prof p_("a4_rmsnorm_fwd", st, 0, 0, 6.0 * n * h + 4.0 * n);
+      EE_CUDA(launch_rmsnorm_fwd(y, true, (const float*)P.g_f, cfg->norm_eps, zbuf, ry, n, h, st)); }
       z = zbuf;
     } else if (nrm) {
-      EE_CUDA(launch_rmsnorm_fwd(x, false, (const float*)P.g_f, cfg->norm_eps, zbuf, ry, n, h, st));
+      { Prof p_("a4_rmsnorm_fwd", st, 0, 0, 4.0 * n * h + 4.0 * n);
+      EE_CUDA(launch_rmsnorm_fwd(x, false, (const float*)P.g_f, cfg->norm_eps, zbuf, ry, n, h, st)); }
       z = zbuf;
     }
 
@@ -331,15 +381,18 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
       a.part_i = pi;
       a.tgt_logit = tgt;
       Mat A{z, n, h, h}, B{P.w_out, Vl, h, h};
+      Prof p_("a5_vocab_ce_stats", st, 2.0 * n * Vl * h, 2.0 * n * Vl * h, 0);
       EE_CUDA(gemm_run(EPI_CE_STATS, true, true, A, B, nullptr, B_PLAIN, 0, a, st));
     }
     // a6: lse, coef, per-token aux, L_i
     {
       const ee_step_aux* ax = aux ? &aux[i] : nullptr;
+      { Prof p_("a6_ce_finalize", st, 0, 0, 12.0 * L.nb * n + 24.0 * n);
       EE_CUDA(launch_ce_finalize(pm, ps, pi, tgt, targets, L.nb, n, vc, alpha, lse, coef,
                                  ax ? ax->lse : nullptr, ax ? ax->loss_tok : nullptr,
                                  ax ? ax->argmax : nullptr, ax ? ax->conf : nullptr, loss_part,
-                                 L.nfin, st));
+                                 L.nfin, st)); }
+      Prof p2_("a6_loss_reduce", st, 0, 0, 4.0 * L.nfin);
       EE_CUDA(launch_loss_reduce(loss_part, L.nfin, vc, loss_out + i, status, i, st));
     }
     // a7: dS = alpha w_t / W (softmax(S_t) - onehot(y_t)), S recomputed -> bf16
@@ -352,6 +405,7 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
       a.ds = ds;
       a.ld_ds = Vl;
       Mat A{z, n, h, h}, B{P.w_out, Vl, h, h};
+      Prof p_("a7_ds_recompute", st, 2.0 * n * Vl * h, 0, 0);
       EE_CUDA(gemm_run(EPI_CE_DS, true, true, A, B, nullptr, B_PLAIN, 0, a, st));
     }
     // a8: dz = dS W_out  (W_out read MN-major in place)
@@ -360,6 +414,7 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
       a.out0 = dz;
       a.ldo = h;
       Mat A{ds, n, Vl, Vl}, B{P.w_out, Vl, h, h};
+      Prof p_("a8_dz", st, 2.0 * n * Vl * h, 2.0 * n * Vl * h, 0);
       EE_CUDA(gemm_run(EPI_F32, true, false, A, B, nullptr, B_PLAIN, 0, a, st));
     }
     // a9: dW_out = dS^T z  (both operands MN-major, K = tokens)
@@ -369,14 +424,17 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
       a.ldo = h;
       a.accumulate = accumulate;
       Mat A{ds, n, Vl, Vl}, B{z, n, h, h};
+      Prof p_("a9_dw_out", st, 2.0 * n * Vl * h, 2.0 * n * Vl * h, 0);
       EE_CUDA(gemm_run(EPI_F32, false, false, A, B, nullptr, B_PLAIN, 0, a, st));
     }
     // a10: final RMSNorm backward -> dg_f (and dy for MLP)
     if (nrm) {
+      { Prof p_("a10_rmsnorm_bwd", st, 0, 0, (mlp ? 10.0 : 6.0) * n * h);
       EE_CUDA(launch_rmsnorm_bwd(dz, mlp ? (const void*)y : (const void*)x, mlp, ry,
                                  (const float*)P.g_f, mlp ? dy : nullptr, dgp, n, h, NORM_RPB,
-                                 st));
-      EE_CUDA(launch_reduce_cols(dgp, L.nparts, h, (float*)G.g_f, accumulate, st));
+                                 st)); }
+      { Prof p_("reduce_cols", st, 0, 0, 4.0 * L.nparts * h);
+      EE_CUDA(launch_reduce_cols(dgp, L.nparts, h, (float*)G.g_f, accumulate, st)); }
     }
     if (mlp) {
       // a11: dW_down = dy^T M
@@ -386,6 +444,7 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
         a.ldo = F;
         a.accumulate = accumulate;
         Mat A{dy, n, h, h}, B{mact, n, F, F};
+        Prof p_("a11_dw_down", st, 2.0 * n * F * h, 2.0 * n * F * h, 0);
         EE_CUDA(gemm_run(EPI_F32, false, false, A, B, nullptr, B_PLAIN, 0, a, st));
       }
       // a11: dM = dy W_down; dA = dM B silu'(A), dB = dM silu(A), in place over [A|B]
@@ -395,6 +454,7 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
         a.ld_ab = 2LL * F;
         a.ffn = F;
         Mat A{dy, n, h, h}, B{P.w_down, h, F, F};
+        Prof p_("a11_dm_swiglu_bwd", st, 2.0 * n * F * h, 2.0 * n * F * h, 0);
         EE_CUDA(gemm_run(EPI_SWIGLU_BWD, true, false, A, B, nullptr, B_PLAIN, 0, a, st));
       }
       // a12: [dW_gate; dW_up] = [dA|dB]^T u  (rows split at F over two outputs)
@@ -406,6 +466,7 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
         a.ldo = h;
         a.accumulate = accumulate;
         Mat A{ab, n, 2LL * F, 2LL * F}, B{u, n, h, h};
+        Prof p_("a12_dw_gateup", st, 4.0 * n * F * h, 4.0 * n * F * h, 0);
         EE_CUDA(gemm_run(EPI_F32, false, false, A, B, nullptr, B_PLAIN, 0, a, st));
       }
       // a12: du = dA W_gate + dB W_up  (K concatenation over the two weights)
@@ -414,11 +475,14 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
         a.out0 = dz;  // dz is dead after a10: reuse as du
         a.ldo = h;
         Mat A{ab, n, 2LL * F, 2LL * F}, B0{P.w_gate, F, h, h}, B1{P.w_up, F, h, h};
+        Prof p_("a12_du", st, 4.0 * n * F * h, 4.0 * n * F * h, 0);
         EE_CUDA(gemm_run(EPI_F32, true, false, A, B0, &B1, B_KSPLIT, F, a, st));
       }
       // a13: dg_a = sum_t du_t * xhat_t  (no dx: frozen backbone)
-      EE_CUDA(launch_gain_grad(dz, x, rx, dgp, n, h, NORM_RPB, st));
-      EE_CUDA(launch_reduce_cols(dgp, L.nparts, h, (float*)G.g_a, accumulate, st));
+      { Prof p_("a13_gain_grad", st, 0, 0, 6.0 * n * h);
+      EE_CUDA(launch_gain_grad(dz, x, rx, dgp, n, h, NORM_RPB, st)); }
+      { Prof p_("reduce_cols", st, 0, 0, 4.0 * L.nparts * h);
+      EE_CUDA(launch_reduce_cols(dgp, L.nparts, h, (float*)G.g_a, accumulate, st)); }
     }
   }
   return EE_OK;
@@ -465,10 +529,13 @@ ee_status ee_init_heads(const ee_head_config* cfg, int32_t init, const ee_head_t
           return fail(EE_ERR_STRUCTURE, "Copy init: source module %s of exit %d is missing",
                       t.name, i);
         if (!aligned16(t.src)) return fail(EE_ERR_ALIGN, "copy source not 16-byte aligned");
+        Prof p_("a0_init_copy", st, 0, 0, 8.0 * t.n);
         EE_CUDA(launch_copy_cast(t.src, src_dtype == EE_DTYPE_F32, t.m, op_bf, op_f32, t.n, st));
       } else if (t.gain) {
+        Prof p_("a0_init_fill", st, 0, 0, 8.0 * t.n);
         EE_CUDA(launch_fill(t.m, op_f32, t.n, 1.0f, st));
       } else {
+        Prof p_("a0_init_random", st, 0, 0, 6.0 * t.n);
         EE_CUDA(launch_random_normal(seed, (uint64_t)i * 16 + k, stdv, t.m, op_bf, t.n, st));
       }
     }
@@ -515,6 +582,7 @@ ee_status ee_adam_update(const ee_head_config* cfg, ee_head_tensors* master, ee_
       if (!mp[k]) continue;
       float* opf = (gain[k] && opp[k] != mp[k]) ? (float*)opp[k] : nullptr;
       __nv_bfloat16* opb = gain[k] ? nullptr : (__nv_bfloat16*)opp[k];
+      Prof p_("a15_adam", st, 0, 0, 30.0 * ns[k]);
       EE_CUDA(launch_adam((float*)mp[k], opb, opf, (const float*)gp[k], (float*)m1[k],
                           (float*)v1[k], ns[k], lr, beta1, beta2, eps, wd, bc1, bc2, grad_scale,
                           st));
@@ -546,6 +614,7 @@ ee_status ee_sgd_update(const ee_head_config* cfg, ee_head_tensors* master, ee_h
       if (!mp[k]) continue;
       float* opf = (gain[k] && opp[k] != mp[k]) ? (float*)opp[k] : nullptr;
       __nv_bfloat16* opb = gain[k] ? nullptr : (__nv_bfloat16*)opp[k];
+      Prof p_("a15_sgd", st, 0, 0, 14.0 * ns[k]);
       EE_CUDA(launch_sgd((float*)mp[k], opb, opf, (const float*)gp[k],
                          momentum != 0.f ? (float*)b1[k] : nullptr, ns[k], lr, momentum,
                          grad_scale, st));
@@ -553,6 +622,43 @@ ee_status ee_sgd_update(const ee_head_config* cfg, ee_head_tensors* master, ee_h
   }
   return EE_OK;
 }
+
+
+ee_status ee_profile_start(void) {
+  for (auto& r : g_prof) {
+    g_event_pool.push_back(r.a);
+    g_event_pool.push_back(r.b);
+  }
+  g_prof.clear();
+  g_prof_on = true;
+  return EE_OK;
+}
+
+ee_status ee_profile_stop(int32_t* count) {
+  g_prof_on = false;
+  if (count) *count = (int32_t)g_prof.size();
+  return EE_OK;
+}
+
+ee_status ee_profile_record(int32_t i, char* name, int32_t name_len, float* ms, double* flops_exec,
+                            double* flops_alg, double* bytes) {
+  if (i < 0 || i >= (int32_t)g_prof.size()) return fail(EE_ERR_ARG, "profile index out of range");
+  const ProfRec& r = g_prof[i];
+  EE_CUDA(cudaEventSynchronize(r.b));
+  float t = 0.f;
+  EE_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+  if (name && name_len > 0) {
+    strncpy(name, r.name, name_len - 1);
+    name[name_len - 1] = 0;
+  }
+  if (ms) *ms = t;
+  if (flops_exec) *flops_exec = r.flops_exec;
+  if (flops_alg) *flops_alg = r.flops_alg;
+  if (bytes) *bytes = r.bytes;
+  return EE_OK;
+}
+
+int64_t ee_launch_count(void) { return g_launches; }
 
 // Testing hook: C[M x N] (fp32, row-major) (+)= A B^T with A stored [M x K]
 // (a_kmajor) or [K x M], B stored [N x K] (b_kmajor) or [K x N]; bf16.
