@@ -235,23 +235,24 @@ def main():
     total_iters = 40000
     one_cfg = ee.make_config(cfg.hidden, cfg.vocab, cfg.ffn, 1, cfg.arch)
 
+    from paper_2402_00518_b200.parallel import data_parallel_step
+
     def step(it, hid=hidden, tg=targets):
         lr = ee.ee_lr_at(min(it + 1, total_iters), total_iters)
         if not dp:
             heads.step(hid, tg)
         else:
-            ee.ee_count_valid(tg, cfg.vocab, vc, heads.workspace)
-            dist.all_reduce(vc)                           # global W (A16)
-            handles = []
-            for i in range(E):                            # per exit: compute, then async all-reduce
+            def count_local():
+                ee.ee_count_valid(tg, cfg.vocab, vc, heads.workspace)
+                return vc
+
+            def run_exit(i, W):                           # exit i on this rank's tokens
                 ee.ee_tune_step(one_cfg, hid[i:i + 1], tg, [1.0], heads.operand[i:i + 1],
                                 heads.grads[i:i + 1], heads.loss[i:i + 1], heads.workspace,
-                                valid_count=vc)
-                for t in heads.grads[i].values():
-                    handles.append(dist.all_reduce(t, async_op=True))
-            handles.append(dist.all_reduce(heads.loss, async_op=True))
-            for hd in handles:
-                hd.wait()
+                                valid_count=W)
+
+            data_parallel_step(E, count_local, run_exit, lambda i: heads.grads[i].values(),
+                               heads.loss)
         heads.adam(lr)
 
     for it in range(args.warmup):
