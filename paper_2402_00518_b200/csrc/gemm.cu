@@ -1,6 +1,7 @@
 // gemm.cu -- host side of the tcgen05 GEMM: TMA descriptors and dispatch.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <mutex>
 #include "internal.cuh"
 
@@ -51,6 +52,28 @@ static bool make_tmap(CUtensorMap* m, const Mat& t, uint32_t box_inner, uint32_t
 }
 
 template <int EPI, bool A_MN, bool B_MN>
+static cudaError_t launch2(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1,
+                           const GemmArgs& args, cudaStream_t st) {
+  auto kern = gemm2_kernel<EPI, A_MN, B_MN>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G2_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int tiles = args.m_blocks * args.n_blocks;
+  const int pairs = num_sms() / 2;
+  const int grid = 2 * (tiles < pairs ? tiles : pairs);
+  kern<<<grid, GEMM_THREADS, G2_SMEM, st>>>(a, b0, b1, args);
+  return cudaGetLastError();
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+template <int EPI, bool A_MN, bool B_MN>
 static cudaError_t launch(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1,
                           const GemmArgs& args, cudaStream_t st) {
   auto kern = gemm_kernel<EPI, A_MN, B_MN>;
@@ -68,10 +91,13 @@ static cudaError_t launch(const CUtensorMap& a, const CUtensorMap& b0, const CUt
 
 cudaError_t gemm_run(int epi, bool a_kmajor, bool b_kmajor, const Mat& A, const Mat& B0,
                      const Mat* B1, int b_mode, int b_ksplit, GemmArgs args, cudaStream_t st) {
+  static const int cta_pair = env_int("EE_GEMM_CTA", 1) == 2;  // 1-CTA default: measured faster under the power cap
+  static const int group = env_int("EE_GEMM_GROUP", 0);
   CUtensorMap ta, tb0, tb1;
   const bool a_mn = !a_kmajor, b_mn = !b_kmajor;
   if (!make_tmap(&ta, A, 64, a_mn ? 64 : GEMM_BM)) return cudaErrorInvalidValue;
-  const uint32_t b_outer = b_mn ? 64 : (b_mode == B_PAIR ? GEMM_BN / 2 : GEMM_BN);
+  const uint32_t b_outer =
+      b_mn ? 64 : ((b_mode == B_PAIR || cta_pair) ? GEMM_BN / 2 : GEMM_BN);
   if (!make_tmap(&tb0, B0, 64, b_outer)) return cudaErrorInvalidValue;
   if (b_mode != B_PLAIN) {
     if (!B1 || !make_tmap(&tb1, *B1, 64, b_outer)) return cudaErrorInvalidValue;
@@ -80,15 +106,18 @@ cudaError_t gemm_run(int epi, bool a_kmajor, bool b_kmajor, const Mat& A, const 
   }
   args.b_mode = b_mode;
   args.b_ksplit = b_ksplit;
-  args.m_blocks = (args.M + GEMM_BM - 1) / GEMM_BM;
+  const int bm = cta_pair ? 2 * GEMM_BM : GEMM_BM;
+  args.m_blocks = (args.M + bm - 1) / bm;
   const int bn = (b_mode == B_PAIR) ? GEMM_BN / 2 : GEMM_BN;
   args.n_blocks = (args.N + bn - 1) / bn;
   args.k_blocks = (args.K + GEMM_BK - 1) / GEMM_BK;
-  if (args.group_m <= 0) args.group_m = 16;
+  args.group_m = group > 0 ? group : (cta_pair ? 8 : 16);
   if (args.m_blocks == 0 || args.n_blocks == 0 || args.k_blocks == 0) return cudaSuccess;
 
-#define EE_GEMM_CASE(E, AM, BM)                                   \
-  if (epi == E && a_mn == AM && b_mn == BM) return launch<E, AM, BM>(ta, tb0, tb1, args, st);
+#define EE_GEMM_CASE(E, AM, BM)                                              \
+  if (epi == E && a_mn == AM && b_mn == BM)                                  \
+    return cta_pair ? launch2<E, AM, BM>(ta, tb0, tb1, args, st)             \
+                    : launch<E, AM, BM>(ta, tb0, tb1, args, st);
   // the (epilogue, A major, B major) combinations the step uses, plus the
   // plain fp32 GEMM in all four majors (exported for the parity tests)
   EE_GEMM_CASE(EPI_F32, false, false)

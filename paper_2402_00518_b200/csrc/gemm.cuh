@@ -91,6 +91,201 @@ __device__ __forceinline__ void tile_coords(const GemmArgs& a, int tile, int& mb
 
 __device__ __forceinline__ float u2f(uint32_t v) { return __uint_as_float(v); }
 
+// Epilogue of one accumulator tile: thread `row` of the 128 epilogue threads
+// owns TMEM lane `row` = output row gm; `tb` = TMEM address of this warp's
+// lane quarter in the accumulator stage; nb = N-block of the tile.
+template <int EPI>
+__device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb, int gm, int nb) {
+  const bool row_ok = gm < args.M;
+  if constexpr (EPI == EPI_F32 || EPI == EPI_RESID) {
+    float* orow = nullptr;
+    if (row_ok) {
+      orow = (gm < args.m_split) ? args.out0 + (long long)gm * args.ldo
+                                 : args.out1 + (long long)(gm - args.m_split) * args.ldo;
+    }
+#pragma unroll 1
+    for (int c = 0; c < GEMM_BN / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tb + c * 32, v);
+      tmem_ld_wait();
+      const int gn0 = nb * GEMM_BN + c * 32;
+      if (row_ok && gn0 < args.N) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          const int gn = gn0 + j;
+          if (gn < args.N) {
+            float4 o = make_float4(u2f(v[j]), u2f(v[j + 1]), u2f(v[j + 2]), u2f(v[j + 3]));
+            if constexpr (EPI == EPI_RESID) {
+              const uint2 r = *reinterpret_cast<const uint2*>(
+                  args.resid + (long long)gm * args.ld_resid + gn);
+              o.x += bf16lo(r.x);
+              o.y += bf16hi(r.x);
+              o.z += bf16lo(r.y);
+              o.w += bf16hi(r.y);
+            } else {
+              if (args.accumulate) {
+                const float4 p = *reinterpret_cast<const float4*>(orow + gn);
+                o.x += p.x;
+                o.y += p.y;
+                o.z += p.z;
+                o.w += p.w;
+              }
+            }
+            *reinterpret_cast<float4*>(orow + gn) = o;
+          }
+        }
+      }
+    }
+  } else if constexpr (EPI == EPI_SWIGLU_FWD) {
+    const int F = args.ffn;
+#pragma unroll 1
+    for (int c = 0; c < GEMM_BN / 64; ++c) {
+      uint32_t g[32], u[32];
+      tmem_ld_32x32b_x32(tb + c * 32, g);
+      tmem_ld_32x32b_x32(tb + GEMM_BN / 2 + c * 32, u);
+      tmem_ld_wait();
+      const int f0 = nb * (GEMM_BN / 2) + c * 32;
+      if (row_ok && f0 < args.N) {
+        __nv_bfloat16* arow = args.ab + (long long)gm * args.ld_ab;
+        __nv_bfloat16* mrow = args.mact + (long long)gm * args.ld_m;
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          uint4 pa, pb, pm;
+          uint32_t* qa = reinterpret_cast<uint32_t*>(&pa);
+          uint32_t* qb = reinterpret_cast<uint32_t*>(&pb);
+          uint32_t* qm = reinterpret_cast<uint32_t*>(&pm);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float a0 = u2f(g[j + 2 * q]), a1 = u2f(g[j + 2 * q + 1]);
+            const float b0 = u2f(u[j + 2 * q]), b1 = u2f(u[j + 2 * q + 1]);
+            const float s0 = a0 / (1.0f + __expf(-a0)), s1 = a1 / (1.0f + __expf(-a1));
+            qa[q] = pack_bf16(a0, a1);
+            qb[q] = pack_bf16(b0, b1);
+            qm[q] = pack_bf16(s0 * b0, s1 * b1);
+          }
+          *reinterpret_cast<uint4*>(arow + f0 + j) = pa;
+          *reinterpret_cast<uint4*>(arow + F + f0 + j) = pb;
+          *reinterpret_cast<uint4*>(mrow + f0 + j) = pm;
+        }
+      }
+    }
+  } else if constexpr (EPI == EPI_SWIGLU_BWD) {
+    const int F = args.ffn;
+#pragma unroll 1
+    for (int c = 0; c < GEMM_BN / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tb + c * 32, v);
+      tmem_ld_wait();
+      const int f0 = nb * GEMM_BN + c * 32;
+      if (row_ok && f0 < args.N) {
+        __nv_bfloat16* arow = args.ab + (long long)gm * args.ld_ab;
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          uint4 ra = *reinterpret_cast<const uint4*>(arow + f0 + j);
+          uint4 rb = *reinterpret_cast<const uint4*>(arow + F + f0 + j);
+          const uint32_t* qa = reinterpret_cast<const uint32_t*>(&ra);
+          const uint32_t* qb = reinterpret_cast<const uint32_t*>(&rb);
+          uint4 wa, wb;
+          uint32_t* pa = reinterpret_cast<uint32_t*>(&wa);
+          uint32_t* pb = reinterpret_cast<uint32_t*>(&wb);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float da[2], db[2];
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const float a = h2 ? bf16hi(qa[q]) : bf16lo(qa[q]);
+              const float b = h2 ? bf16hi(qb[q]) : bf16lo(qb[q]);
+              const float dm = u2f(v[j + 2 * q + h2]);
+              const float sg = 1.0f / (1.0f + __expf(-a));
+              db[h2] = dm * a * sg;
+              da[h2] = dm * b * sg * (1.0f + a * (1.0f - sg));
+            }
+            pa[q] = pack_bf16(da[0], da[1]);
+            pb[q] = pack_bf16(db[0], db[1]);
+          }
+          *reinterpret_cast<uint4*>(arow + f0 + j) = wa;
+          *reinterpret_cast<uint4*>(arow + F + f0 + j) = wb;
+        }
+      }
+    }
+  } else if constexpr (EPI == EPI_CE_STATS) {
+    const int yl = row_ok ? args.targets[gm] - args.vocab_begin : -1;
+    float mx = -INFINITY, sm = 0.0f, tl = 0.0f;
+    int am = 0;
+    bool has_t = false;
+#pragma unroll 1
+    for (int c = 0; c < GEMM_BN / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tb + c * 32, v);
+      tmem_ld_wait();
+      const int gn0 = nb * GEMM_BN + c * 32;
+      float cmax = -INFINITY;
+      int cidx = 0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float x = u2f(v[j]);
+        const bool ok = gn0 + j < args.N;
+        if (ok && x > cmax) {
+          cmax = x;
+          cidx = gn0 + j;
+        }
+        if (gn0 + j == yl) {
+          tl = x;
+          has_t = true;
+        }
+      }
+      if (cmax > mx) {
+        sm *= __expf(mx - cmax);
+        mx = cmax;
+        am = cidx;
+      }
+      float cs = 0.0f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (gn0 + j < args.N) cs += __expf(u2f(v[j]) - mx);
+      }
+      sm += cs;
+    }
+    if (row_ok) {
+      const long long o = (long long)nb * args.M + gm;
+      args.part_m[o] = mx;
+      args.part_s[o] = sm;
+      args.part_i[o] = am + args.vocab_begin;
+      if (has_t) args.tgt_logit[gm] = tl;
+    }
+  } else if constexpr (EPI == EPI_CE_DS) {
+    const int yl = row_ok ? args.targets[gm] - args.vocab_begin : -1;
+    const float l = row_ok ? args.lse[gm] : 0.0f;
+    const float cf = row_ok ? args.coef[gm] : 0.0f;
+    __nv_bfloat16* drow = row_ok ? args.ds + (long long)gm * args.ld_ds : nullptr;
+#pragma unroll 1
+    for (int c = 0; c < GEMM_BN / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tb + c * 32, v);
+      tmem_ld_wait();
+      const int gn0 = nb * GEMM_BN + c * 32;
+      if (row_ok && gn0 < args.N) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          if (gn0 + j < args.N) {
+            uint4 w;
+            uint32_t* pw = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int c0 = gn0 + j + 2 * q;
+              const float d0 = cf * (__expf(u2f(v[j + 2 * q]) - l) - (c0 == yl ? 1.0f : 0.0f));
+              const float d1 =
+                  cf * (__expf(u2f(v[j + 2 * q + 1]) - l) - (c0 + 1 == yl ? 1.0f : 0.0f));
+              pw[q] = pack_bf16(d0, d1);
+            }
+            *reinterpret_cast<uint4*>(drow + gn0 + j) = w;
+          }
+        }
+      }
+    }
+  }
+}
+
 template <int EPI, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
@@ -233,193 +428,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tc_fence_after();
       const uint32_t tb = tmem_base + acc * GEMM_BN + (static_cast<uint32_t>(ew * 32) << 16);
 
-      if constexpr (EPI == EPI_F32 || EPI == EPI_RESID) {
-        float* orow = nullptr;
-        if (row_ok) {
-          orow = (gm < args.m_split) ? args.out0 + (long long)gm * args.ldo
-                                     : args.out1 + (long long)(gm - args.m_split) * args.ldo;
-        }
-#pragma unroll 1
-        for (int c = 0; c < GEMM_BN / 32; ++c) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(tb + c * 32, v);
-          tmem_ld_wait();
-          const int gn0 = nb * GEMM_BN + c * 32;
-          if (row_ok && gn0 < args.N) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              const int gn = gn0 + j;
-              if (gn < args.N) {
-                float4 o = make_float4(u2f(v[j]), u2f(v[j + 1]), u2f(v[j + 2]), u2f(v[j + 3]));
-                if constexpr (EPI == EPI_RESID) {
-                  const uint2 r = *reinterpret_cast<const uint2*>(
-                      args.resid + (long long)gm * args.ld_resid + gn);
-                  o.x += bf16lo(r.x);
-                  o.y += bf16hi(r.x);
-                  o.z += bf16lo(r.y);
-                  o.w += bf16hi(r.y);
-                } else {
-                  if (args.accumulate) {
-                    const float4 p = *reinterpret_cast<const float4*>(orow + gn);
-                    o.x += p.x;
-                    o.y += p.y;
-                    o.z += p.z;
-                    o.w += p.w;
-                  }
-                }
-                *reinterpret_cast<float4*>(orow + gn) = o;
-              }
-            }
-          }
-        }
-      } else if constexpr (EPI == EPI_SWIGLU_FWD) {
-        const int F = args.ffn;
-#pragma unroll 1
-        for (int c = 0; c < GEMM_BN / 64; ++c) {
-          uint32_t g[32], u[32];
-          tmem_ld_32x32b_x32(tb + c * 32, g);
-          tmem_ld_32x32b_x32(tb + GEMM_BN / 2 + c * 32, u);
-          tmem_ld_wait();
-          const int f0 = nb * (GEMM_BN / 2) + c * 32;
-          if (row_ok && f0 < args.N) {
-            __nv_bfloat16* arow = args.ab + (long long)gm * args.ld_ab;
-            __nv_bfloat16* mrow = args.mact + (long long)gm * args.ld_m;
-#pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              uint4 pa, pb, pm;
-              uint32_t* qa = reinterpret_cast<uint32_t*>(&pa);
-              uint32_t* qb = reinterpret_cast<uint32_t*>(&pb);
-              uint32_t* qm = reinterpret_cast<uint32_t*>(&pm);
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const float a0 = u2f(g[j + 2 * q]), a1 = u2f(g[j + 2 * q + 1]);
-                const float b0 = u2f(u[j + 2 * q]), b1 = u2f(u[j + 2 * q + 1]);
-                const float s0 = a0 / (1.0f + __expf(-a0)), s1 = a1 / (1.0f + __expf(-a1));
-                qa[q] = pack_bf16(a0, a1);
-                qb[q] = pack_bf16(b0, b1);
-                qm[q] = pack_bf16(s0 * b0, s1 * b1);
-              }
-              *reinterpret_cast<uint4*>(arow + f0 + j) = pa;
-              *reinterpret_cast<uint4*>(arow + F + f0 + j) = pb;
-              *reinterpret_cast<uint4*>(mrow + f0 + j) = pm;
-            }
-          }
-        }
-      } else if constexpr (EPI == EPI_SWIGLU_BWD) {
-        const int F = args.ffn;
-#pragma unroll 1
-        for (int c = 0; c < GEMM_BN / 32; ++c) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(tb + c * 32, v);
-          tmem_ld_wait();
-          const int f0 = nb * GEMM_BN + c * 32;
-          if (row_ok && f0 < args.N) {
-            __nv_bfloat16* arow = args.ab + (long long)gm * args.ld_ab;
-#pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              uint4 ra = *reinterpret_cast<const uint4*>(arow + f0 + j);
-              uint4 rb = *reinterpret_cast<const uint4*>(arow + F + f0 + j);
-              const uint32_t* qa = reinterpret_cast<const uint32_t*>(&ra);
-              const uint32_t* qb = reinterpret_cast<const uint32_t*>(&rb);
-              uint4 wa, wb;
-              uint32_t* pa = reinterpret_cast<uint32_t*>(&wa);
-              uint32_t* pb = reinterpret_cast<uint32_t*>(&wb);
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                float da[2], db[2];
-#pragma unroll
-                for (int h2 = 0; h2 < 2; ++h2) {
-                  const float a = h2 ? bf16hi(qa[q]) : bf16lo(qa[q]);
-                  const float b = h2 ? bf16hi(qb[q]) : bf16lo(qb[q]);
-                  const float dm = u2f(v[j + 2 * q + h2]);
-                  const float sg = 1.0f / (1.0f + __expf(-a));
-                  db[h2] = dm * a * sg;
-                  da[h2] = dm * b * sg * (1.0f + a * (1.0f - sg));
-                }
-                pa[q] = pack_bf16(da[0], da[1]);
-                pb[q] = pack_bf16(db[0], db[1]);
-              }
-              *reinterpret_cast<uint4*>(arow + f0 + j) = wa;
-              *reinterpret_cast<uint4*>(arow + F + f0 + j) = wb;
-            }
-          }
-        }
-      } else if constexpr (EPI == EPI_CE_STATS) {
-        const int yl = row_ok ? args.targets[gm] - args.vocab_begin : -1;
-        float mx = -INFINITY, sm = 0.0f, tl = 0.0f;
-        int am = 0;
-        bool has_t = false;
-#pragma unroll 1
-        for (int c = 0; c < GEMM_BN / 32; ++c) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(tb + c * 32, v);
-          tmem_ld_wait();
-          const int gn0 = nb * GEMM_BN + c * 32;
-          float cmax = -INFINITY;
-          int cidx = 0;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float x = u2f(v[j]);
-            const bool ok = gn0 + j < args.N;
-            if (ok && x > cmax) {
-              cmax = x;
-              cidx = gn0 + j;
-            }
-            if (gn0 + j == yl) {
-              tl = x;
-              has_t = true;
-            }
-          }
-          if (cmax > mx) {
-            sm *= __expf(mx - cmax);
-            mx = cmax;
-            am = cidx;
-          }
-          float cs = 0.0f;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            if (gn0 + j < args.N) cs += __expf(u2f(v[j]) - mx);
-          }
-          sm += cs;
-        }
-        if (row_ok) {
-          const long long o = (long long)nb * args.M + gm;
-          args.part_m[o] = mx;
-          args.part_s[o] = sm;
-          args.part_i[o] = am + args.vocab_begin;
-          if (has_t) args.tgt_logit[gm] = tl;
-        }
-      } else if constexpr (EPI == EPI_CE_DS) {
-        const int yl = row_ok ? args.targets[gm] - args.vocab_begin : -1;
-        const float l = row_ok ? args.lse[gm] : 0.0f;
-        const float cf = row_ok ? args.coef[gm] : 0.0f;
-        __nv_bfloat16* drow = row_ok ? args.ds + (long long)gm * args.ld_ds : nullptr;
-#pragma unroll 1
-        for (int c = 0; c < GEMM_BN / 32; ++c) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(tb + c * 32, v);
-          tmem_ld_wait();
-          const int gn0 = nb * GEMM_BN + c * 32;
-          if (row_ok && gn0 < args.N) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              if (gn0 + j < args.N) {
-                uint4 w;
-                uint32_t* pw = reinterpret_cast<uint32_t*>(&w);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  const int c0 = gn0 + j + 2 * q;
-                  const float d0 = cf * (__expf(u2f(v[j + 2 * q]) - l) - (c0 == yl ? 1.0f : 0.0f));
-                  const float d1 =
-                      cf * (__expf(u2f(v[j + 2 * q + 1]) - l) - (c0 + 1 == yl ? 1.0f : 0.0f));
-                  pw[q] = pack_bf16(d0, d1);
-                }
-                *reinterpret_cast<uint4*>(drow + gn0 + j) = w;
-              }
-            }
-          }
-        }
-      }
+      epilogue_tile<EPI>(args, tb, gm, nb);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       if (++acc == 2) {
@@ -434,6 +443,191 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, GEMM_TMEM_COLS);
+  }
+}
+
+
+// ============================================================================
+// CTA-pair variant (tcgen05 cta_group::2): a cluster of 2 CTAs on the two SMs
+// of a TPC computes a 256 x 256 tile.  Each CTA stages its own 128 rows of A
+// and its own 128-row half of B (N) per stage; the leader's single thread
+// issues tcgen05.mma.cta_group::2 (M = 256) which reads both CTAs' smem and
+// writes each CTA's 128 accumulator rows into that CTA's TMEM.  Per SM this
+// halves the B bytes pulled from L2 and read from smem per FLOP versus the
+// 128 x 256 single-CTA tile.
+//   - full[s]   lives in the leader; both CTAs' TMA (cta_group::2 form) count
+//               their bytes on it; only the leader's MMA thread waits on it.
+//   - empty[s]  in both CTAs; the leader's tcgen05.commit multicasts to both.
+//   - tfull[a]  in both CTAs (multicast commit); tempty[a] in the leader,
+//               256 arrivals (128 epilogue threads of each CTA, remote via mapa).
+// ============================================================================
+constexpr int G2_STAGES = 6;
+constexpr int G2_A_STAGE = 128 * GEMM_BK * 2;  // 16 KB (this CTA's 128 rows of A)
+constexpr int G2_B_STAGE = 128 * GEMM_BK * 2;  // 16 KB (this CTA's half of B)
+constexpr int G2_SMEM = G2_STAGES * (G2_A_STAGE + G2_B_STAGE) + 1024 + 256;
+
+template <int EPI, bool A_MN, bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
+                 const __grid_constant__ CUtensorMap tmB1, const GemmArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + G2_STAGES * G2_A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + G2_STAGES * G2_B_STAGE);
+  uint64_t* empty = full + G2_STAGES;
+  uint64_t* tfull = empty + G2_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x >> 1;
+  const int nclusters = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB0);
+    if (args.b_mode != B_PLAIN) tma_prefetch_desc(&tmB1);
+    for (int s = 0; s < G2_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 256);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    tmem_alloc_2sm(tmem_slot, GEMM_TMEM_COLS);
+    tmem_relinquish_2sm();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int num_tiles = args.m_blocks * args.n_blocks;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int tile = cluster_id; tile < num_tiles; tile += nclusters) {
+        int mb, nb;
+        tile_coords(args, tile, mb, nb);
+        const int m0 = mb * 256 + (int)rank * 128;
+        for (int kb = 0; kb < args.k_blocks; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
+          uint8_t* a = sA + s * G2_A_STAGE;
+          uint8_t* b = sB + s * G2_B_STAGE;
+          const int k0 = kb * GEMM_BK;
+          if constexpr (!A_MN) {
+            tma_load_2d_2sm(a, &tmA, fb, k0, m0);
+          } else {
+            tma_load_2d_2sm(a, &tmA, fb, m0, k0);
+            tma_load_2d_2sm(a + 8192, &tmA, fb, m0 + 64, k0);
+          }
+          if (args.b_mode == B_PAIR) {
+            // CTA 0 holds the 128 gate rows, CTA 1 the 128 up rows of the same f range
+            tma_load_2d_2sm(b, rank ? &tmB1 : &tmB0, fb, k0, nb * 128);
+          } else {
+            const CUtensorMap* mB = &tmB0;
+            int kk = k0;
+            if (args.b_mode == B_KSPLIT && k0 >= args.b_ksplit) {
+              mB = &tmB1;
+              kk = k0 - args.b_ksplit;
+            }
+            const int n0 = nb * GEMM_BN + (int)rank * 128;
+            if constexpr (!B_MN) {
+              tma_load_2d_2sm(b, mB, fb, kk, n0);
+            } else {
+              tma_load_2d_2sm(b, mB, fb, n0, kk);
+              tma_load_2d_2sm(b + 8192, mB, fb, n0 + 64, kk);
+            }
+          }
+          if (leader) mbar_arrive_expect_tx(&full[s], 2 * (G2_A_STAGE + G2_B_STAGE));
+          if (++s == G2_STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader only)
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(256, GEMM_BN, A_MN, B_MN);
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t acc_ph = 0;
+      for (int tile = cluster_id; tile < num_tiles; tile += nclusters) {
+        mbar_wait(&tempty[acc], acc_ph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * GEMM_BN;
+        for (int kb = 0; kb < args.k_blocks; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + s * G2_A_STAGE);
+          const uint32_t b_addr = smem_u32(sB + s * G2_B_STAGE);
+#pragma unroll
+          for (int k = 0; k < GEMM_BK / 16; ++k) {
+            const uint64_t ad = A_MN ? make_sdesc(a_addr + k * 2048, 8192, 1024)
+                                     : make_sdesc(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_sdesc(b_addr + k * 2048, 8192, 1024)
+                                     : make_sdesc(b_addr + k * 32, 16, 1024);
+            tc_mma_f16_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          tc_commit_2sm(&empty[s], 0x3);
+          if (++s == G2_STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        tc_commit_2sm(&tfull[acc], 0x3);
+        if (++acc == 2) {
+          acc = 0;
+          acc_ph ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int ew = warp - 4;
+    const int row = ew * 32 + lane;
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    const uint32_t te0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    const uint32_t te1 = mapa_shared(smem_u32(&tempty[1]), 0);
+    for (int tile = cluster_id; tile < num_tiles; tile += nclusters) {
+      int mb, nb;
+      tile_coords(args, tile, mb, nb);
+      mbar_wait(&tfull[acc], acc_ph);
+      tc_fence_after();
+      const uint32_t tb = tmem_base + acc * GEMM_BN + (static_cast<uint32_t>(ew * 32) << 16);
+      epilogue_tile<EPI>(args, tb, mb * 256 + (int)rank * 128 + row, nb);
+      tc_fence_before();
+      mbar_arrive_cluster(acc ? te1 : te0);
+      if (++acc == 2) {
+        acc = 0;
+        acc_ph ^= 1;
+      }
+    }
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_2sm(tmem_base, GEMM_TMEM_COLS);
   }
 }
 

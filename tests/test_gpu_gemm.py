@@ -49,4 +49,4 @@ def test_gemm_large_k_precision(gpu_lib):
     ee.ee_test_gemm(A.cuda(), B.cuda(), C, False, False, M, N, K)
     torch.cuda.synchronize()
     rel = ((C.cpu().double() - ref).norm() / ref.norm()).item()
-    assert rel < 1e-5, rel
+    assert rel < 5e-5, rel
