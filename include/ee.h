@@ -76,10 +76,9 @@ typedef enum { EE_DTYPE_BF16 = 0, EE_DTYPE_F32 = 1 } ee_dtype;
  *  norm_eps     RMSNorm epsilon (A3: 1e-5).
  *  vocab_begin, vocab_end
  *               the rows [vocab_begin, vocab_end) of W_out held by this call
- *               (vocab-parallel shard).  Only the unsharded case
- *               vocab_begin = 0, vocab_end = V is implemented in this round;
- *               anything else returns EE_ERR_UNSUPPORTED.  (vocab_end -
- *               vocab_begin) must be a multiple of 8. */
+ *               (a vocab-parallel shard, 0 <= begin < end <= V, width a
+ *               multiple of 8).  ee_tune_step needs the full vocabulary
+ *               [0, V); shards are driven through the ee_vp_* phases. */
 typedef struct {
   int32_t hidden, vocab, ffn, num_exits;
   int32_t arch;
@@ -160,6 +159,52 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
                        const ee_head_tensors* params, ee_head_tensors* grads, int32_t accumulate,
                        float* loss_out, const ee_step_aux* aux, const int64_t* valid_count,
                        void* workspace, size_t ws_bytes, void* stream);
+
+/* ---- vocab-parallel phases (one exit on one of P ranks) ----
+ * W_out is split by rows over P ranks (cfg->vocab_begin/vocab_end = this rank's
+ * shard); tokens are split over ranks for the exit body (RMSNorm/MLP) and
+ * gathered for the vocab projection.  The caller runs the collectives between
+ * the phases, in this order, for each exit i:
+ *   1. ee_vp_exit_forward   (a1-a4 on the rank's n_local tokens) -> z_out, which
+ *                           should be this rank's slot of z_all [n_all x h] bf16
+ *      all-gather z_all
+ *   2. ee_vp_vocab_stats    (a5 on the local W_out shard for all n_all tokens)
+ *                           -> key [n_all] int64, sums [n_all x 2] fp32
+ *      all-reduce MAX (signed int64) on key  -> global row max + lowest argmax
+ *   3. ee_vp_rescale        sums[:,0] *= exp(m_local - m_global)
+ *      all-reduce SUM on sums                -> global sum-exp, target logit
+ *   4. ee_vp_vocab_backward (lse, loss, dS on the shard; dW_out shard = dS^T z_all
+ *                           needs no reduction; dz_partial [n_all x h] fp32 =
+ *                           dS W_out_shard, NULL for Embedding exits)
+ *      reduce-scatter SUM dz_partial -> dz_local [n_local x h]
+ *   5. ee_vp_exit_backward  (a10-a13 on local tokens: g_f and MLP grads)
+ *      all-reduce SUM of the exit's g_f / MLP gradients (W_out grads stay sharded)
+ * The distributed softmax-CE is steps 2-3 (max + argmax key, sum-exp and target
+ * logit), the paper's "vocab-parallel" reading of Megatron TP.
+ * The workspace must be sized by ee_workspace_size(cfg, n_all) and is shared by
+ * the five phases of one exit; exits are processed one after another.
+ * loss_out (one float) = sum over ALL tokens of w_t loss_t / W, identical on
+ * every rank.  valid_count = W over all tokens (NULL: count targets_all). */
+ee_status ee_vp_exit_forward(const ee_head_config* cfg, const void* hidden, int64_t n_local,
+                             int64_t n_all, const ee_head_tensors* params, void* z_out,
+                             void* workspace, size_t ws_bytes, void* stream);
+ee_status ee_vp_vocab_stats(const ee_head_config* cfg, const void* z_all, int64_t n_all,
+                            const int32_t* targets_all, const ee_head_tensors* params,
+                            int64_t* key_out, float* sums_out, void* workspace, size_t ws_bytes,
+                            void* stream);
+ee_status ee_vp_rescale(const ee_head_config* cfg, int64_t n_all, const int64_t* key_global,
+                        float* sums, void* workspace, size_t ws_bytes, void* stream);
+ee_status ee_vp_vocab_backward(const ee_head_config* cfg, const void* z_all, int64_t n_all,
+                               const int32_t* targets_all, const int64_t* key_global,
+                               const float* sums_global, float exit_weight,
+                               const int64_t* valid_count, const ee_head_tensors* params,
+                               ee_head_tensors* grads, int32_t accumulate, float* dz_partial,
+                               float* loss_out, const ee_step_aux* aux, int32_t exit_index,
+                               void* workspace, size_t ws_bytes, void* stream);
+ee_status ee_vp_exit_backward(const ee_head_config* cfg, const void* hidden, int64_t n_local,
+                              int64_t n_all, const ee_head_tensors* params, const float* dz_local,
+                              ee_head_tensors* grads, int32_t accumulate, void* workspace,
+                              size_t ws_bytes, void* stream);
 
 /* Number of valid targets (!= -1) -> device int64 out[0]; flags ids outside
  * [-1, V) in the workspace status word.  Used to form the global W under

@@ -200,20 +200,29 @@ def exit_loss_and_grads(arch: str, params: dict, x: np.ndarray, targets: np.ndar
     grads["w_out"] = dS.T @ z                               # dW_out = dS^T z
     if arch in ("norm", "mlp"):
         dz = dS @ params["w_out"]                           # dz = dS W_out
-        dy, dg_f = rmsnorm_backward(dz, act["yhat"], act["r_y"], params["g_f"])
-        grads["g_f"] = dg_f
-        if arch == "mlp":
-            M, A, B, u = act["M"], act["A"], act["B"], act["u"]
-            grads["w_down"] = dy.T @ M                      # dW_down = dy^T M
-            dM = dy @ params["w_down"]
-            dA = dM * B * silu_grad(A)
-            dB = dM * silu(A)
-            grads["w_gate"] = dA.T @ u
-            grads["w_up"] = dB.T @ u
-            du = dA @ params["w_gate"] + dB @ params["w_up"]
-            # u = g_a * xhat  =>  dg_a = sum_t du_t * xhat_t; no dx (frozen backbone)
-            grads["g_a"] = np.sum(du * act["xhat"], axis=0)
+        grads.update(exit_body_backward(arch, params, act, dz))
     return ExitResult(loss, grads, st, act if keep_act else {})
+
+
+def exit_body_backward(arch: str, params: dict, act: dict, dz: np.ndarray) -> dict:
+    """Gradients of the exit body below W_out given dz = dL/dz: the
+    final RMSNorm gain and, for MLP exits, the SwiGLU MLP and its pre-norm gain.
+    No gradient w.r.t. the exit input x (frozen backbone)."""
+    grads = {}
+    dy, dg_f = rmsnorm_backward(dz, act["yhat"], act["r_y"], params["g_f"])
+    grads["g_f"] = dg_f
+    if arch == "mlp":
+        M, A, B, u = act["M"], act["A"], act["B"], act["u"]
+        grads["w_down"] = dy.T @ M                          # dW_down = dy^T M
+        dM = dy @ params["w_down"]
+        dA = dM * B * silu_grad(A)
+        dB = dM * silu(A)
+        grads["w_gate"] = dA.T @ u
+        grads["w_up"] = dB.T @ u
+        du = dA @ params["w_gate"] + dB @ params["w_up"]
+        # u = g_a * xhat  =>  dg_a = sum_t du_t * xhat_t; no dx (frozen backbone, P:250)
+        grads["g_a"] = np.sum(du * act["xhat"], axis=0)
+    return grads
 
 
 def tune_step(arch: str, params_list, hidden_list, targets, exit_weights, eps: float,

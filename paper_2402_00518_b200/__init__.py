@@ -30,7 +30,8 @@ TENSOR_NAMES = ("g_a", "w_gate", "w_up", "w_down", "g_f", "w_out")
 EXPORTED = ("ee_workspace_size", "ee_init_heads", "ee_tune_step", "ee_count_valid",
             "ee_adam_update", "ee_sgd_update", "ee_get_status", "ee_lr_at", "ee_last_error",
             "ee_version", "ee_test_gemm", "ee_profile_start", "ee_profile_stop",
-            "ee_profile_record", "ee_launch_count")
+            "ee_profile_record", "ee_launch_count", "ee_vp_exit_forward", "ee_vp_vocab_stats",
+            "ee_vp_rescale", "ee_vp_vocab_backward", "ee_vp_exit_backward")
 
 
 class EEError(RuntimeError):
@@ -92,6 +93,12 @@ def load(path: str = LIB_PATH):
                                     ctypes.POINTER(ctypes.c_double),
                                     ctypes.POINTER(ctypes.c_double)]),
         "ee_launch_count": (I64, []),
+        "ee_vp_exit_forward": (I32, [CFG, P, I64, I64, HT, P, P, SZ, P]),
+        "ee_vp_vocab_stats": (I32, [CFG, P, I64, P, HT, P, P, P, SZ, P]),
+        "ee_vp_rescale": (I32, [CFG, I64, P, P, P, SZ, P]),
+        "ee_vp_vocab_backward": (I32, [CFG, P, I64, P, P, P, F32, P, HT, HT, I32, P, P,
+                                       ctypes.POINTER(ee_step_aux), I32, P, SZ, P]),
+        "ee_vp_exit_backward": (I32, [CFG, P, I64, I64, HT, P, HT, I32, P, SZ, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -214,6 +221,60 @@ def ee_test_gemm(A, B, C, a_kmajor, b_kmajor, M, N, K, accumulate=False, stream=
     load()
     _check(_lib.ee_test_gemm(int(a_kmajor), int(b_kmajor), _ptr(A), _ptr(B), _ptr(C), M, N, K,
                              int(bool(accumulate)), _stream(stream)))
+
+
+def _aux1(aux):
+    if aux is None:
+        return None
+    ax = ee_step_aux()
+    for k in ("lse", "loss_tok", "argmax", "conf"):
+        t = aux.get(k)
+        setattr(ax, k, None if t is None else t.data_ptr())
+    return ctypes.pointer(ax)
+
+
+def ee_vp_exit_forward(cfg, hidden, n_all, params, z_out, workspace, stream=None):
+    load()
+    n_local = 0 if hidden is None else hidden.shape[0]
+    _check(_lib.ee_vp_exit_forward(ctypes.byref(cfg), _ptr(hidden), n_local, int(n_all),
+                                   heads([params]), _ptr(z_out), _ptr(workspace),
+                                   workspace.numel(), _stream(stream)))
+
+
+def ee_vp_vocab_stats(cfg, z_all, targets_all, params, key_out, sums_out, workspace, stream=None):
+    load()
+    _check(_lib.ee_vp_vocab_stats(ctypes.byref(cfg), _ptr(z_all), targets_all.numel(),
+                                  _ptr(targets_all), heads([params]), _ptr(key_out),
+                                  _ptr(sums_out), _ptr(workspace), workspace.numel(),
+                                  _stream(stream)))
+
+
+def ee_vp_rescale(cfg, n_all, key_global, sums, workspace, stream=None):
+    load()
+    _check(_lib.ee_vp_rescale(ctypes.byref(cfg), int(n_all), _ptr(key_global), _ptr(sums),
+                              _ptr(workspace), workspace.numel(), _stream(stream)))
+
+
+def ee_vp_vocab_backward(cfg, z_all, targets_all, key_global, sums_global, exit_weight,
+                         params, grads, dz_partial, loss_out, workspace, valid_count=None,
+                         accumulate=False, aux=None, exit_index=0, stream=None):
+    load()
+    _check(_lib.ee_vp_vocab_backward(ctypes.byref(cfg), _ptr(z_all), targets_all.numel(),
+                                     _ptr(targets_all), _ptr(key_global), _ptr(sums_global),
+                                     float(exit_weight), _ptr(valid_count), heads([params]),
+                                     heads([grads]), int(bool(accumulate)), _ptr(dz_partial),
+                                     _ptr(loss_out), _aux1(aux), int(exit_index),
+                                     _ptr(workspace), workspace.numel(), _stream(stream)))
+
+
+def ee_vp_exit_backward(cfg, hidden, n_all, params, dz_local, grads, workspace,
+                        accumulate=False, stream=None):
+    load()
+    n_local = 0 if hidden is None else hidden.shape[0]
+    _check(_lib.ee_vp_exit_backward(ctypes.byref(cfg), _ptr(hidden), n_local, int(n_all),
+                                    heads([params]), _ptr(dz_local), heads([grads]),
+                                    int(bool(accumulate)), _ptr(workspace), workspace.numel(),
+                                    _stream(stream)))
 
 
 def ee_profile_start():

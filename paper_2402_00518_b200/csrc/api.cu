@@ -63,8 +63,9 @@ ee_status check_cfg(const ee_head_config* c) {
   if (c->hidden < 64 || c->hidden > 8192 || c->hidden % 64 != 0)
     return fail(EE_ERR_SHAPE, "hidden must be a multiple of 64 in [64, 8192], got %d", c->hidden);
   if (c->vocab < 1) return fail(EE_ERR_SHAPE, "vocab must be >= 1");
-  if (c->vocab_begin != 0 || c->vocab_end != c->vocab)
-    return fail(EE_ERR_UNSUPPORTED, "vocab-parallel shards are not implemented in this build");
+  if (c->vocab_begin < 0 || c->vocab_end > c->vocab || c->vocab_begin >= c->vocab_end)
+    return fail(EE_ERR_SHAPE, "vocab shard [%d, %d) outside [0, %d)", c->vocab_begin, c->vocab_end,
+                c->vocab);
   if ((c->vocab_end - c->vocab_begin) % 8 != 0)
     return fail(EE_ERR_SHAPE, "local vocab size must be a multiple of 8");
   if (c->arch == EE_ARCH_MLP && (c->ffn < 128 || c->ffn % 128 != 0))
@@ -256,6 +257,256 @@ ee_status ee_count_valid(const int32_t* targets, int64_t n, int32_t vocab, int64
   return EE_OK;
 }
 
+}  // extern "C"
+
+// ---------------------------------------------------------------- step phases
+namespace {
+
+// Workspace views for one call (layout sized for n tokens).
+struct Bufs {
+  DevStatus* status;
+  long long* vcount;
+  float *lse, *coef, *tgt, *pm, *ps, *loss_part;
+  int32_t* pi;
+  __nv_bfloat16* ds;
+  __nv_bfloat16* z;
+  float *dz, *dgp, *ry;
+  __nv_bfloat16* u;
+  float* rx;
+  __nv_bfloat16 *ab, *mact;
+  float* y;
+  __nv_bfloat16* dy;
+  // vocab-parallel merge state
+  float* m_loc;
+  Layout L;
+};
+
+Bufs make_bufs(const ee_head_config* cfg, long long n, void* workspace) {
+  Bufs B{};
+  B.L = make_layout(cfg, n);
+  const Layout& L = B.L;
+  uint8_t* ws = (uint8_t*)workspace;
+  const bool mlp = cfg->arch == EE_ARCH_MLP, nrm = cfg->arch != EE_ARCH_EMBEDDING;
+  B.status = (DevStatus*)(ws + L.status);
+  B.vcount = (long long*)(ws + L.vcount);
+  B.lse = (float*)(ws + L.lse);
+  B.coef = (float*)(ws + L.coef);
+  B.tgt = (float*)(ws + L.tgt);
+  B.pm = (float*)(ws + L.pm);
+  B.ps = (float*)(ws + L.ps);
+  B.pi = (int32_t*)(ws + L.pi);
+  B.loss_part = (float*)(ws + L.loss_part);
+  B.ds = (__nv_bfloat16*)(ws + L.ds);
+  B.m_loc = B.coef;  // VP: m_loc is dead before coef is written (vp_finalize)
+  if (nrm) {
+    B.z = (__nv_bfloat16*)(ws + L.z);
+    B.dz = (float*)(ws + L.dz);
+    B.dgp = (float*)(ws + L.dgp);
+    B.ry = (float*)(ws + L.ry);
+  }
+  if (mlp) {
+    B.u = (__nv_bfloat16*)(ws + L.u);
+    B.rx = (float*)(ws + L.rx);
+    B.ab = (__nv_bfloat16*)(ws + L.ab);
+    B.mact = (__nv_bfloat16*)(ws + L.mact);
+    B.y = (float*)(ws + L.y);
+    B.dy = (__nv_bfloat16*)(ws + L.dy);
+  }
+  return B;
+}
+
+// a1..a4: z = exit-head input of the vocab projection, on n tokens.
+// z_out: where to write z (NULL = the workspace buffer; Embedding: z = x unless
+// z_out is given, in which case x is copied there).  Returns z in *z_ret.
+ee_status phase_exit_forward(const ee_head_config* cfg, const Bufs& B, const ee_head_tensors& P,
+                             const __nv_bfloat16* x, long long n, __nv_bfloat16* z_out,
+                             const __nv_bfloat16** z_ret, cudaStream_t st) {
+  const int h = cfg->hidden, F = cfg->ffn;
+  const bool mlp = cfg->arch == EE_ARCH_MLP, nrm = cfg->arch != EE_ARCH_EMBEDDING;
+  if (!nrm) {
+    if (z_out && n > 0)
+      EE_CUDA(cudaMemcpyAsync(z_out, x, 2 * (size_t)n * h, cudaMemcpyDeviceToDevice, st));
+    *z_ret = z_out ? z_out : x;
+    return EE_OK;
+  }
+  __nv_bfloat16* z = z_out ? z_out : B.z;
+  *z_ret = z;
+  if (n == 0) return EE_OK;
+  if (mlp) {
+    // a1: u = RMSNorm_a(x)
+    { Prof p_("a1_rmsnorm_fwd", st, 0, 0, 4.0 * n * h + 4.0 * n);
+    EE_CUDA(launch_rmsnorm_fwd(x, false, (const float*)P.g_a, cfg->norm_eps, B.u, B.rx, n, h, st)); }
+    // a2: [A|B] = u [W_gate|W_up]^T (paired B tiles), M = silu(A) * B
+    {
+      GemmArgs a = base_args((int)n, F, h);
+      a.ab = B.ab;
+      a.ld_ab = 2LL * F;
+      a.mact = B.mact;
+      a.ld_m = F;
+      a.ffn = F;
+      Mat A{B.u, n, h, h}, B0{P.w_gate, F, h, h}, B1{P.w_up, F, h, h};
+      Prof p_("a2_gateup_swiglu", st, 4.0 * n * F * h, 4.0 * n * F * h, 0);
+      EE_CUDA(gemm_run(EPI_SWIGLU_FWD, true, true, A, B0, &B1, B_PAIR, 0, a, st));
+    }
+    // a3: y = x + M W_down^T  (fp32 residual stream, A15)
+    {
+      GemmArgs a = base_args((int)n, h, F);
+      a.out0 = B.y;
+      a.ldo = h;
+      a.resid = x;
+      a.ld_resid = h;
+      Mat A{B.mact, n, F, F}, Bm{P.w_down, h, F, F};
+      Prof p_("a3_down_resid", st, 2.0 * n * F * h, 2.0 * n * F * h, 0);
+      EE_CUDA(gemm_run(EPI_RESID, true, true, A, Bm, nullptr, B_PLAIN, 0, a, st));
+    }
+    // a4: z = RMSNorm_f(y)
+    { Prof p_("a4_rmsnorm_fwd", st, 0, 0, 6.0 * n * h + 4.0 * n);
+    EE_CUDA(launch_rmsnorm_fwd(B.y, true, (const float*)P.g_f, cfg->norm_eps, z, B.ry, n, h, st)); }
+  } else {
+    { Prof p_("a4_rmsnorm_fwd", st, 0, 0, 4.0 * n * h + 4.0 * n);
+    EE_CUDA(launch_rmsnorm_fwd(x, false, (const float*)P.g_f, cfg->norm_eps, z, B.ry, n, h, st)); }
+  }
+  return EE_OK;
+}
+
+// a5: per-V-tile online-softmax partials of S = z W_out^T (logits never stored).
+ee_status phase_vocab_stats(const ee_head_config* cfg, const Bufs& B, const ee_head_tensors& P,
+                            const __nv_bfloat16* z, long long n, const int32_t* targets,
+                            cudaStream_t st) {
+  const int h = cfg->hidden, Vl = cfg->vocab_end - cfg->vocab_begin;
+  GemmArgs a = base_args((int)n, Vl, h);
+  a.targets = targets;
+  a.vocab_begin = cfg->vocab_begin;
+  a.part_m = B.pm;
+  a.part_s = B.ps;
+  a.part_i = B.pi;
+  a.tgt_logit = B.tgt;
+  Mat A{z, n, h, h}, Bm{P.w_out, Vl, h, h};
+  Prof p_("a5_vocab_ce_stats", st, 2.0 * n * Vl * h, 2.0 * n * Vl * h, 0);
+  EE_CUDA(gemm_run(EPI_CE_STATS, true, true, A, Bm, nullptr, B_PLAIN, 0, a, st));
+  return EE_OK;
+}
+
+// a7 (dS, recomputed S), a8 (dz = dS W_out, if dz_out) and a9 (dW_out = dS^T z).
+ee_status phase_vocab_backward(const ee_head_config* cfg, const Bufs& B, const ee_head_tensors& P,
+                               const ee_head_tensors& G, const __nv_bfloat16* z, long long n,
+                               const int32_t* targets, int accumulate, float* dz_out,
+                               cudaStream_t st) {
+  const int h = cfg->hidden, Vl = cfg->vocab_end - cfg->vocab_begin;
+  {
+    GemmArgs a = base_args((int)n, Vl, h);
+    a.targets = targets;
+    a.vocab_begin = cfg->vocab_begin;
+    a.lse = B.lse;
+    a.coef = B.coef;
+    a.ds = B.ds;
+    a.ld_ds = Vl;
+    Mat A{z, n, h, h}, Bm{P.w_out, Vl, h, h};
+    Prof p_("a7_ds_recompute", st, 2.0 * n * Vl * h, 0, 0);
+    EE_CUDA(gemm_run(EPI_CE_DS, true, true, A, Bm, nullptr, B_PLAIN, 0, a, st));
+  }
+  if (dz_out) {  // a8: W_out read MN-major in place
+    GemmArgs a = base_args((int)n, h, Vl);
+    a.out0 = dz_out;
+    a.ldo = h;
+    Mat A{B.ds, n, Vl, Vl}, Bm{P.w_out, Vl, h, h};
+    Prof p_("a8_dz", st, 2.0 * n * Vl * h, 2.0 * n * Vl * h, 0);
+    EE_CUDA(gemm_run(EPI_F32, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
+  }
+  {  // a9: both operands MN-major, K = tokens
+    GemmArgs a = base_args(Vl, h, (int)n);
+    a.out0 = (float*)G.w_out;
+    a.ldo = h;
+    a.accumulate = accumulate;
+    Mat A{B.ds, n, Vl, Vl}, Bm{z, n, h, h};
+    Prof p_("a9_dw_out", st, 2.0 * n * Vl * h, 2.0 * n * Vl * h, 0);
+    EE_CUDA(gemm_run(EPI_F32, false, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
+  }
+  return EE_OK;
+}
+
+// a10..a13 on n tokens given dz: dg_f (+ dy, MLP grads, dg_a for MLP exits).
+ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee_head_tensors& P,
+                              const ee_head_tensors& G, const __nv_bfloat16* x, long long n,
+                              const float* dz, int accumulate, cudaStream_t st) {
+  const int h = cfg->hidden, F = cfg->ffn;
+  const bool mlp = cfg->arch == EE_ARCH_MLP;
+  if (cfg->arch == EE_ARCH_EMBEDDING) return EE_OK;
+  const int nparts = (int)((n + NORM_RPB - 1) / NORM_RPB);
+  // a10: final RMSNorm backward -> dg_f (and dy for MLP)
+  { Prof p_("a10_rmsnorm_bwd", st, 0, 0, (mlp ? 10.0 : 6.0) * n * h);
+  EE_CUDA(launch_rmsnorm_bwd(dz, mlp ? (const void*)B.y : (const void*)x, mlp, B.ry,
+                             (const float*)P.g_f, mlp ? B.dy : nullptr, B.dgp, n, h, NORM_RPB,
+                             st)); }
+  { Prof p_("reduce_cols", st, 0, 0, 4.0 * nparts * h);
+  EE_CUDA(launch_reduce_cols(B.dgp, nparts, h, (float*)G.g_f, accumulate, st)); }
+  if (!mlp) return EE_OK;
+  // a11: dW_down = dy^T M
+  {
+    GemmArgs a = base_args(h, F, (int)n);
+    a.out0 = (float*)G.w_down;
+    a.ldo = F;
+    a.accumulate = accumulate;
+    Mat A{B.dy, n, h, h}, Bm{B.mact, n, F, F};
+    Prof p_("a11_dw_down", st, 2.0 * n * F * h, 2.0 * n * F * h, 0);
+    EE_CUDA(gemm_run(EPI_F32, false, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
+  }
+  // a11: dM = dy W_down; dA = dM B silu'(A), dB = dM silu(A), in place over [A|B]
+  {
+    GemmArgs a = base_args((int)n, F, h);
+    a.ab = B.ab;
+    a.ld_ab = 2LL * F;
+    a.ffn = F;
+    Mat A{B.dy, n, h, h}, Bm{P.w_down, h, F, F};
+    Prof p_("a11_dm_swiglu_bwd", st, 2.0 * n * F * h, 2.0 * n * F * h, 0);
+    EE_CUDA(gemm_run(EPI_SWIGLU_BWD, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
+  }
+  // a12: [dW_gate; dW_up] = [dA|dB]^T u  (rows split at F over two outputs)
+  {
+    GemmArgs a = base_args(2 * F, h, (int)n);
+    a.out0 = (float*)G.w_gate;
+    a.out1 = (float*)G.w_up;
+    a.m_split = F;
+    a.ldo = h;
+    a.accumulate = accumulate;
+    Mat A{B.ab, n, 2LL * F, 2LL * F}, Bm{B.u, n, h, h};
+    Prof p_("a12_dw_gateup", st, 4.0 * n * F * h, 4.0 * n * F * h, 0);
+    EE_CUDA(gemm_run(EPI_F32, false, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
+  }
+  // a12: du = dA W_gate + dB W_up  (K concatenation over the two weights) -> B.dz
+  {
+    GemmArgs a = base_args((int)n, h, 2 * F);
+    a.out0 = B.dz;
+    a.ldo = h;
+    Mat A{B.ab, n, 2LL * F, 2LL * F}, B0{P.w_gate, F, h, h}, B1{P.w_up, F, h, h};
+    Prof p_("a12_du", st, 4.0 * n * F * h, 4.0 * n * F * h, 0);
+    EE_CUDA(gemm_run(EPI_F32, true, false, A, B0, &B1, B_KSPLIT, F, a, st));
+  }
+  // a13: dg_a = sum_t du_t * xhat_t  (no dx: frozen backbone)
+  { Prof p_("a13_gain_grad", st, 0, 0, 6.0 * n * h);
+  EE_CUDA(launch_gain_grad(B.dz, x, B.rx, B.dgp, n, h, NORM_RPB, st)); }
+  { Prof p_("reduce_cols", st, 0, 0, 4.0 * nparts * h);
+  EE_CUDA(launch_reduce_cols(B.dgp, nparts, h, (float*)G.g_a, accumulate, st)); }
+  return EE_OK;
+}
+
+ee_status zero_grads(const ee_head_config* cfg, const ee_head_tensors& G, bool vocab_part,
+                     bool exit_part, cudaStream_t st) {
+  const long long h = cfg->hidden, F = cfg->ffn, Vl = cfg->vocab_end - cfg->vocab_begin;
+  const long long sz[6] = {h, F * h, F * h, h * F, h, Vl * h};
+  void* ptrs[6] = {G.g_a, G.w_gate, G.w_up, G.w_down, G.g_f, G.w_out};
+  for (int k = 0; k < 6; ++k) {
+    const bool is_vocab = k == 5;
+    if (ptrs[k] && ((is_vocab && vocab_part) || (!is_vocab && exit_part)))
+      EE_CUDA(cudaMemsetAsync(ptrs[k], 0, 4 * sz[k], st));
+  }
+  return EE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int64_t n_tokens,
                        const int32_t* targets, const float* exit_weights,
                        const ee_head_tensors* params, ee_head_tensors* grads, int32_t accumulate,
@@ -263,6 +514,9 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
                        void* workspace, size_t ws_bytes, void* stream) {
   ee_status s = check_cfg(cfg);
   if (s != EE_OK) return s;
+  if (cfg->vocab_begin != 0 || cfg->vocab_end != cfg->vocab)
+    return fail(EE_ERR_ARG, "ee_tune_step needs the full vocabulary; use the ee_vp_* phases "
+                            "for a vocab-parallel shard");
   const int E = cfg->num_exits;
   if (!hidden || !exit_weights || !params || !grads || !loss_out || n_tokens < 0 ||
       (n_tokens > 0 && !targets))
@@ -277,215 +531,170 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
   if ((targets && !aligned16(targets)) || !aligned16(workspace))
     return fail(EE_ERR_ALIGN, "targets/workspace not 16-byte aligned");
   const long long n = n_tokens;
-  const Layout L = make_layout(cfg, n);
-  if (!workspace || ws_bytes < L.total)
-    return fail(EE_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", L.total, ws_bytes);
+  const Bufs B = make_bufs(cfg, n, workspace);
+  if (!workspace || ws_bytes < B.L.total)
+    return fail(EE_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", B.L.total, ws_bytes);
   if ((s = check_device()) != EE_OK) return s;
-
   cudaStream_t st = (cudaStream_t)stream;
-  uint8_t* ws = (uint8_t*)workspace;
-  DevStatus* status = (DevStatus*)(ws + L.status);
-  long long* vc_local = (long long*)(ws + L.vcount);
-  const int h = cfg->hidden, F = cfg->ffn, Vl = cfg->vocab_end - cfg->vocab_begin;
-  const bool mlp = cfg->arch == EE_ARCH_MLP, nrm = cfg->arch != EE_ARCH_EMBEDDING;
 
   { Prof p_("count_valid", st, 0, 0, 4.0 * n);
-  EE_CUDA(launch_count_valid(targets, n, cfg->vocab, vc_local, status, st)); }
-  const long long* vc = valid_count ? (const long long*)valid_count : vc_local;
+  EE_CUDA(launch_count_valid(targets, n, cfg->vocab, B.vcount, B.status, st)); }
+  const long long* vc = valid_count ? (const long long*)valid_count : B.vcount;
 
   if (n == 0) {
-    for (int i = 0; i < E; ++i) {
-      if (!accumulate) {
-        const long long sz[6] = {h, (long long)F * h, (long long)F * h, (long long)h * F, h,
-                                 (long long)Vl * h};
-        void* ptrs[6] = {grads[i].g_a, grads[i].w_gate, grads[i].w_up, grads[i].w_down,
-                         grads[i].g_f, grads[i].w_out};
-        for (int k = 0; k < 6; ++k)
-          if (ptrs[k]) EE_CUDA(cudaMemsetAsync(ptrs[k], 0, 4 * sz[k], st));
-      }
-    }
+    for (int i = 0; i < E; ++i)
+      if (!accumulate && (s = zero_grads(cfg, grads[i], true, true, st)) != EE_OK) return s;
     EE_CUDA(cudaMemsetAsync(loss_out, 0, sizeof(float) * E, st));
     return EE_OK;
   }
-
-  float* lse = (float*)(ws + L.lse);
-  float* coef = (float*)(ws + L.coef);
-  float* tgt = (float*)(ws + L.tgt);
-  float* pm = (float*)(ws + L.pm);
-  float* ps = (float*)(ws + L.ps);
-  int32_t* pi = (int32_t*)(ws + L.pi);
-  float* loss_part = (float*)(ws + L.loss_part);
-  __nv_bfloat16* ds = (__nv_bfloat16*)(ws + L.ds);
-  __nv_bfloat16* zbuf = nrm ? (__nv_bfloat16*)(ws + L.z) : nullptr;
-  float* dz = nrm ? (float*)(ws + L.dz) : nullptr;
-  float* dgp = nrm ? (float*)(ws + L.dgp) : nullptr;
-  float* ry = nrm ? (float*)(ws + L.ry) : nullptr;
-  __nv_bfloat16* u = mlp ? (__nv_bfloat16*)(ws + L.u) : nullptr;
-  float* rx = mlp ? (float*)(ws + L.rx) : nullptr;
-  __nv_bfloat16* ab = mlp ? (__nv_bfloat16*)(ws + L.ab) : nullptr;
-  __nv_bfloat16* mact = mlp ? (__nv_bfloat16*)(ws + L.mact) : nullptr;
-  float* y = mlp ? (float*)(ws + L.y) : nullptr;
-  __nv_bfloat16* dy = mlp ? (__nv_bfloat16*)(ws + L.dy) : nullptr;
-
+  const bool nrm = cfg->arch != EE_ARCH_EMBEDDING;
   for (int i = 0; i < E; ++i) {
     const ee_head_tensors& P = params[i];
     const ee_head_tensors& G = grads[i];
     const __nv_bfloat16* x = (const __nv_bfloat16*)hidden[i];
-    const __nv_bfloat16* z = x;
-    const float alpha = exit_weights[i];
-
-    if (mlp) {
-      // a1: u = RMSNorm_a(x)
-      { Prof p_("a1_rmsnorm_fwd", st, 0, 0, 4.0 * n * h + 4.0 * n);
-      EE_CUDA(launch_rmsnorm_fwd(x, false, (const float*)P.g_a, cfg->norm_eps, u, rx, n, h, st)); }
-      // a2: [A|B] = u [W_gate|W_up]^T (paired B tiles), M = silu(A) * B
-      {
-        GemmArgs a = base_args((int)n, F, h);
-        a.ab = ab;
-        a.ld_ab = 2LL * F;
-        a.mact = mact;
-        a.ld_m = F;
-        a.ffn = F;
-        Mat A{u, n, h, h}, B0{P.w_gate, F, h, h}, B1{P.w_up, F, h, h};
-        Prof p_("a2_gateup_swiglu", st, 4.0 * n * F * h, 4.0 * n * F * h, 0);
-        EE_CUDA(gemm_run(EPI_SWIGLU_FWD, true, true, A, B0, &B1, B_PAIR, 0, a, st));
-      }
-      // a3: y = x + M W_down^T  (fp32 residual stream, A15)
-      {
-        GemmArgs a = base_args((int)n, h, F);
-        a.out0 = y;
-        a.ldo = h;
-        a.resid = x;
-        a.ld_resid = h;
-        Mat A{mact, n, F, F}, B{P.w_down, h, F, F};
-        Prof p_("a3_down_resid", st, 2.0 * n * F * h, 2.0 * n * F * h, 0);
-        EE_CUDA(gemm_run(EPI_RESID, true, true, A, B, nullptr, B_PLAIN, 0, a, st));
-      }
-      // a4: z = RMSNorm_f(y)
-      { Prof p_("a4_rmsnorm_fwd", st, 0, 0, 6.0 * n * h + 4.0 * n);
-      EE_CUDA(launch_rmsnorm_fwd(y, true, (const float*)P.g_f, cfg->norm_eps, zbuf, ry, n, h, st)); }
-      z = zbuf;
-    } else if (nrm) {
-      { Prof p_("a4_rmsnorm_fwd", st, 0, 0, 4.0 * n * h + 4.0 * n);
-      EE_CUDA(launch_rmsnorm_fwd(x, false, (const float*)P.g_f, cfg->norm_eps, zbuf, ry, n, h, st)); }
-      z = zbuf;
-    }
-
-    // a5: per-tile online-softmax statistics of S = z W_out^T (logits never stored)
-    {
-      GemmArgs a = base_args((int)n, Vl, h);
-      a.targets = targets;
-      a.vocab_begin = cfg->vocab_begin;
-      a.part_m = pm;
-      a.part_s = ps;
-      a.part_i = pi;
-      a.tgt_logit = tgt;
-      Mat A{z, n, h, h}, B{P.w_out, Vl, h, h};
-      Prof p_("a5_vocab_ce_stats", st, 2.0 * n * Vl * h, 2.0 * n * Vl * h, 0);
-      EE_CUDA(gemm_run(EPI_CE_STATS, true, true, A, B, nullptr, B_PLAIN, 0, a, st));
-    }
+    const __nv_bfloat16* z = nullptr;
+    if ((s = phase_exit_forward(cfg, B, P, x, n, nullptr, &z, st)) != EE_OK) return s;
+    if ((s = phase_vocab_stats(cfg, B, P, z, n, targets, st)) != EE_OK) return s;
     // a6: lse, coef, per-token aux, L_i
     {
       const ee_step_aux* ax = aux ? &aux[i] : nullptr;
-      { Prof p_("a6_ce_finalize", st, 0, 0, 12.0 * L.nb * n + 24.0 * n);
-      EE_CUDA(launch_ce_finalize(pm, ps, pi, tgt, targets, L.nb, n, vc, alpha, lse, coef,
-                                 ax ? ax->lse : nullptr, ax ? ax->loss_tok : nullptr,
-                                 ax ? ax->argmax : nullptr, ax ? ax->conf : nullptr, loss_part,
-                                 L.nfin, st)); }
-      Prof p2_("a6_loss_reduce", st, 0, 0, 4.0 * L.nfin);
-      EE_CUDA(launch_loss_reduce(loss_part, L.nfin, vc, loss_out + i, status, i, st));
+      { Prof p_("a6_ce_finalize", st, 0, 0, 12.0 * B.L.nb * n + 24.0 * n);
+      EE_CUDA(launch_ce_finalize(B.pm, B.ps, B.pi, B.tgt, targets, B.L.nb, n, vc,
+                                 exit_weights[i], B.lse, B.coef, ax ? ax->lse : nullptr,
+                                 ax ? ax->loss_tok : nullptr, ax ? ax->argmax : nullptr,
+                                 ax ? ax->conf : nullptr, B.loss_part, B.L.nfin, st)); }
+      Prof p2_("a6_loss_reduce", st, 0, 0, 4.0 * B.L.nfin);
+      EE_CUDA(launch_loss_reduce(B.loss_part, B.L.nfin, vc, loss_out + i, B.status, i, st));
     }
-    // a7: dS = alpha w_t / W (softmax(S_t) - onehot(y_t)), S recomputed -> bf16
-    {
-      GemmArgs a = base_args((int)n, Vl, h);
-      a.targets = targets;
-      a.vocab_begin = cfg->vocab_begin;
-      a.lse = lse;
-      a.coef = coef;
-      a.ds = ds;
-      a.ld_ds = Vl;
-      Mat A{z, n, h, h}, B{P.w_out, Vl, h, h};
-      Prof p_("a7_ds_recompute", st, 2.0 * n * Vl * h, 0, 0);
-      EE_CUDA(gemm_run(EPI_CE_DS, true, true, A, B, nullptr, B_PLAIN, 0, a, st));
-    }
-    // a8: dz = dS W_out  (W_out read MN-major in place)
-    if (nrm) {
-      GemmArgs a = base_args((int)n, h, Vl);
-      a.out0 = dz;
-      a.ldo = h;
-      Mat A{ds, n, Vl, Vl}, B{P.w_out, Vl, h, h};
-      Prof p_("a8_dz", st, 2.0 * n * Vl * h, 2.0 * n * Vl * h, 0);
-      EE_CUDA(gemm_run(EPI_F32, true, false, A, B, nullptr, B_PLAIN, 0, a, st));
-    }
-    // a9: dW_out = dS^T z  (both operands MN-major, K = tokens)
-    {
-      GemmArgs a = base_args(Vl, h, (int)n);
-      a.out0 = (float*)G.w_out;
-      a.ldo = h;
-      a.accumulate = accumulate;
-      Mat A{ds, n, Vl, Vl}, B{z, n, h, h};
-      Prof p_("a9_dw_out", st, 2.0 * n * Vl * h, 2.0 * n * Vl * h, 0);
-      EE_CUDA(gemm_run(EPI_F32, false, false, A, B, nullptr, B_PLAIN, 0, a, st));
-    }
-    // a10: final RMSNorm backward -> dg_f (and dy for MLP)
-    if (nrm) {
-      { Prof p_("a10_rmsnorm_bwd", st, 0, 0, (mlp ? 10.0 : 6.0) * n * h);
-      EE_CUDA(launch_rmsnorm_bwd(dz, mlp ? (const void*)y : (const void*)x, mlp, ry,
-                                 (const float*)P.g_f, mlp ? dy : nullptr, dgp, n, h, NORM_RPB,
-                                 st)); }
-      { Prof p_("reduce_cols", st, 0, 0, 4.0 * L.nparts * h);
-      EE_CUDA(launch_reduce_cols(dgp, L.nparts, h, (float*)G.g_f, accumulate, st)); }
-    }
-    if (mlp) {
-      // a11: dW_down = dy^T M
-      {
-        GemmArgs a = base_args(h, F, (int)n);
-        a.out0 = (float*)G.w_down;
-        a.ldo = F;
-        a.accumulate = accumulate;
-        Mat A{dy, n, h, h}, B{mact, n, F, F};
-        Prof p_("a11_dw_down", st, 2.0 * n * F * h, 2.0 * n * F * h, 0);
-        EE_CUDA(gemm_run(EPI_F32, false, false, A, B, nullptr, B_PLAIN, 0, a, st));
-      }
-      // a11: dM = dy W_down; dA = dM B silu'(A), dB = dM silu(A), in place over [A|B]
-      {
-        GemmArgs a = base_args((int)n, F, h);
-        a.ab = ab;
-        a.ld_ab = 2LL * F;
-        a.ffn = F;
-        Mat A{dy, n, h, h}, B{P.w_down, h, F, F};
-        Prof p_("a11_dm_swiglu_bwd", st, 2.0 * n * F * h, 2.0 * n * F * h, 0);
-        EE_CUDA(gemm_run(EPI_SWIGLU_BWD, true, false, A, B, nullptr, B_PLAIN, 0, a, st));
-      }
-      // a12: [dW_gate; dW_up] = [dA|dB]^T u  (rows split at F over two outputs)
-      {
-        GemmArgs a = base_args(2 * F, h, (int)n);
-        a.out0 = (float*)G.w_gate;
-        a.out1 = (float*)G.w_up;
-        a.m_split = F;
-        a.ldo = h;
-        a.accumulate = accumulate;
-        Mat A{ab, n, 2LL * F, 2LL * F}, B{u, n, h, h};
-        Prof p_("a12_dw_gateup", st, 4.0 * n * F * h, 4.0 * n * F * h, 0);
-        EE_CUDA(gemm_run(EPI_F32, false, false, A, B, nullptr, B_PLAIN, 0, a, st));
-      }
-      // a12: du = dA W_gate + dB W_up  (K concatenation over the two weights)
-      {
-        GemmArgs a = base_args((int)n, h, 2 * F);
-        a.out0 = dz;  // dz is dead after a10: reuse as du
-        a.ldo = h;
-        Mat A{ab, n, 2LL * F, 2LL * F}, B0{P.w_gate, F, h, h}, B1{P.w_up, F, h, h};
-        Prof p_("a12_du", st, 4.0 * n * F * h, 4.0 * n * F * h, 0);
-        EE_CUDA(gemm_run(EPI_F32, true, false, A, B0, &B1, B_KSPLIT, F, a, st));
-      }
-      // a13: dg_a = sum_t du_t * xhat_t  (no dx: frozen backbone)
-      { Prof p_("a13_gain_grad", st, 0, 0, 6.0 * n * h);
-      EE_CUDA(launch_gain_grad(dz, x, rx, dgp, n, h, NORM_RPB, st)); }
-      { Prof p_("reduce_cols", st, 0, 0, 4.0 * L.nparts * h);
-      EE_CUDA(launch_reduce_cols(dgp, L.nparts, h, (float*)G.g_a, accumulate, st)); }
-    }
+    if ((s = phase_vocab_backward(cfg, B, P, G, z, n, targets, accumulate, nrm ? B.dz : nullptr,
+                                  st)) != EE_OK)
+      return s;
+    if ((s = phase_exit_backward(cfg, B, P, G, x, n, B.dz, accumulate, st)) != EE_OK) return s;
   }
   return EE_OK;
+}
+
+// ---------------------------------------------------------------- vocab parallel
+// One exit, one rank of P.  The caller runs the collectives between phases
+// (include/ee.h, "vocab-parallel phases").  cfg->num_exits is ignored (the
+// calls take one exit's tensors); the workspace is sized for n_all tokens.
+static ee_status vp_common(const ee_head_config* cfg, long long n_all, void* ws, size_t ws_bytes,
+                           Bufs* B) {
+  ee_status s = check_cfg(cfg);
+  if (s != EE_OK) return s;
+  if (n_all < 0 || n_all > (1LL << 30)) return fail(EE_ERR_SHAPE, "bad n_all");
+  if (!ws || !aligned16(ws)) return fail(EE_ERR_ARG, "workspace NULL or misaligned");
+  *B = make_bufs(cfg, n_all, ws);
+  if (ws_bytes < B->L.total)
+    return fail(EE_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", B->L.total, ws_bytes);
+  return check_device();
+}
+
+ee_status ee_vp_exit_forward(const ee_head_config* cfg, const void* hidden, int64_t n_local,
+                             int64_t n_all, const ee_head_tensors* params, void* z_out,
+                             void* workspace, size_t ws_bytes, void* stream) {
+  Bufs B;
+  ee_status s = vp_common(cfg, n_all, workspace, ws_bytes, &B);
+  if (s != EE_OK) return s;
+  if (!params || !z_out || n_local < 0 || n_local > n_all || (n_local > 0 && !hidden))
+    return fail(EE_ERR_ARG, "bad ee_vp_exit_forward arguments");
+  if ((s = check_arch_tensors(cfg, *params, "params", 0)) != EE_OK) return s;
+  if (!aligned16(z_out) || (hidden && !aligned16(hidden))) return fail(EE_ERR_ALIGN, "misaligned");
+  const __nv_bfloat16* z = nullptr;
+  return phase_exit_forward(cfg, B, *params, (const __nv_bfloat16*)hidden, n_local,
+                            (__nv_bfloat16*)z_out, &z, (cudaStream_t)stream);
+}
+
+ee_status ee_vp_vocab_stats(const ee_head_config* cfg, const void* z_all, int64_t n_all,
+                            const int32_t* targets_all, const ee_head_tensors* params,
+                            int64_t* key_out, float* sums_out, void* workspace, size_t ws_bytes,
+                            void* stream) {
+  Bufs B;
+  ee_status s = vp_common(cfg, n_all, workspace, ws_bytes, &B);
+  if (s != EE_OK) return s;
+  if (!params || !params->w_out || (n_all > 0 && (!z_all || !targets_all || !key_out || !sums_out)))
+    return fail(EE_ERR_ARG, "bad ee_vp_vocab_stats arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_all == 0) return EE_OK;
+  { Prof p_("count_valid", st, 0, 0, 4.0 * n_all);
+  EE_CUDA(launch_count_valid(targets_all, n_all, cfg->vocab, B.vcount, B.status, st)); }
+  if ((s = phase_vocab_stats(cfg, B, *params, (const __nv_bfloat16*)z_all, n_all, targets_all,
+                             st)) != EE_OK)
+    return s;
+  Prof p_("vp_local_merge", st, 0, 0, 12.0 * B.L.nb * n_all + 20.0 * n_all);
+  EE_CUDA(launch_vp_local_merge(B.pm, B.ps, B.pi, B.tgt, targets_all, B.L.nb, n_all,
+                                cfg->vocab_begin, cfg->vocab_end, (long long*)key_out, B.m_loc,
+                                sums_out, st));
+  return EE_OK;
+}
+
+ee_status ee_vp_rescale(const ee_head_config* cfg, int64_t n_all, const int64_t* key_global,
+                        float* sums, void* workspace, size_t ws_bytes, void* stream) {
+  Bufs B;
+  ee_status s = vp_common(cfg, n_all, workspace, ws_bytes, &B);
+  if (s != EE_OK) return s;
+  if (n_all > 0 && (!key_global || !sums)) return fail(EE_ERR_ARG, "NULL argument");
+  if (n_all == 0) return EE_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  Prof p_("vp_rescale", st, 0, 0, 20.0 * n_all);
+  EE_CUDA(launch_vp_rescale((const long long*)key_global, B.m_loc, sums, n_all, st));
+  return EE_OK;
+}
+
+ee_status ee_vp_vocab_backward(const ee_head_config* cfg, const void* z_all, int64_t n_all,
+                               const int32_t* targets_all, const int64_t* key_global,
+                               const float* sums_global, float exit_weight,
+                               const int64_t* valid_count, const ee_head_tensors* params,
+                               ee_head_tensors* grads, int32_t accumulate, float* dz_partial,
+                               float* loss_out, const ee_step_aux* aux, int32_t exit_index,
+                               void* workspace, size_t ws_bytes, void* stream) {
+  Bufs B;
+  ee_status s = vp_common(cfg, n_all, workspace, ws_bytes, &B);
+  if (s != EE_OK) return s;
+  if (!params || !grads || !grads->w_out || !loss_out ||
+      (n_all > 0 && (!z_all || !targets_all || !key_global || !sums_global)))
+    return fail(EE_ERR_ARG, "bad ee_vp_vocab_backward arguments");
+  const bool nrm = cfg->arch != EE_ARCH_EMBEDDING;
+  if (nrm && n_all > 0 && !dz_partial) return fail(EE_ERR_ARG, "dz_partial required");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_all == 0) {
+    if (!accumulate && (s = zero_grads(cfg, *grads, true, false, st)) != EE_OK) return s;
+    EE_CUDA(cudaMemsetAsync(loss_out, 0, sizeof(float), st));
+    return EE_OK;
+  }
+  const long long* vc = valid_count ? (const long long*)valid_count : B.vcount;
+  {
+    Prof p_("vp_finalize", st, 0, 0, 28.0 * n_all);
+    EE_CUDA(launch_vp_finalize((const long long*)key_global, sums_global, targets_all, n_all, vc,
+                               exit_weight, B.lse, B.coef, aux ? aux->lse : nullptr,
+                               aux ? aux->loss_tok : nullptr, aux ? aux->argmax : nullptr,
+                               aux ? aux->conf : nullptr, B.loss_part, B.L.nfin, st));
+  }
+  {
+    Prof p_("a6_loss_reduce", st, 0, 0, 4.0 * B.L.nfin);
+    EE_CUDA(launch_loss_reduce(B.loss_part, B.L.nfin, vc, loss_out, B.status, exit_index, st));
+  }
+  return phase_vocab_backward(cfg, B, *params, *grads, (const __nv_bfloat16*)z_all, n_all,
+                              targets_all, accumulate, nrm ? dz_partial : nullptr, st);
+}
+
+ee_status ee_vp_exit_backward(const ee_head_config* cfg, const void* hidden, int64_t n_local,
+                              int64_t n_all, const ee_head_tensors* params, const float* dz_local,
+                              ee_head_tensors* grads, int32_t accumulate, void* workspace,
+                              size_t ws_bytes, void* stream) {
+  Bufs B;
+  ee_status s = vp_common(cfg, n_all, workspace, ws_bytes, &B);
+  if (s != EE_OK) return s;
+  if (!params || !grads || n_local < 0 || n_local > n_all ||
+      (n_local > 0 && cfg->arch != EE_ARCH_EMBEDDING && (!hidden || !dz_local)))
+    return fail(EE_ERR_ARG, "bad ee_vp_exit_backward arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_local == 0) {
+    if (!accumulate) return zero_grads(cfg, *grads, false, true, st);
+    return EE_OK;
+  }
+  return phase_exit_backward(cfg, B, *params, *grads, (const __nv_bfloat16*)hidden, n_local,
+                             dz_local, accumulate, st);
 }
 
 ee_status ee_init_heads(const ee_head_config* cfg, int32_t init, const ee_head_tensors* src,

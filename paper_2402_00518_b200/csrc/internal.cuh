@@ -54,6 +54,21 @@ cudaError_t launch_loss_reduce(const float* loss_part, int nparts, const long lo
                                float* loss_out, DevStatus* st, int exit_index, cudaStream_t s);
 constexpr int FINALIZE_THREADS = 256;
 
+// vocab-parallel softmax-CE (distributed statistics)
+//   key = orderable(m) << 32 | (0xFFFFFFFF - argmax), sign-flipped so that a
+//   signed int64 MAX all-reduce yields the global max and lowest-index argmax.
+cudaError_t launch_vp_local_merge(const float* pm, const float* ps, const int32_t* pi,
+                                  const float* tl, const int32_t* targets, int nb, long long n,
+                                  int vocab_begin, int vocab_end, long long* key, float* m_loc,
+                                  float* sums, cudaStream_t s);
+cudaError_t launch_vp_rescale(const long long* key_global, const float* m_loc, float* sums,
+                              long long n, cudaStream_t s);
+cudaError_t launch_vp_finalize(const long long* key_global, const float* sums,
+                               const int32_t* targets, long long n, const long long* valid_count,
+                               float alpha, float* lse, float* coef, float* aux_lse,
+                               float* aux_loss, int32_t* aux_argmax, float* aux_conf,
+                               float* loss_part, int nblocks, cudaStream_t s);
+
 // optimizer / init
 cudaError_t launch_adam(float* theta, __nv_bfloat16* op_bf16, float* op_f32, const float* grad,
                         float* m, float* v, long long n, float lr, float b1, float b2, float eps,

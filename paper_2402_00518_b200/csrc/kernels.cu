@@ -348,6 +348,118 @@ cudaError_t launch_loss_reduce(const float* loss_part, int nparts, const long lo
   return cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------- vocab parallel CE
+// Rank r holds W_out rows [vb, ve).  Per row it merges its own V tiles into
+// (m_r, s_r = sum exp(S - m_r), argmax_r, S[y] if y in [vb, ve) else 0); the
+// caller all-reduces MAX over the (m, argmax) key and then SUM over
+// (s_r exp(m_r - m), S[y]) -- the distributed softmax-CE of north_star.
+__device__ __forceinline__ long long vp_make_key(float m, int idx) {
+  uint32_t u = __float_as_uint(m);
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  const unsigned long long k =
+      ((unsigned long long)u << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)idx);
+  return (long long)(k ^ 0x8000000000000000ull);
+}
+__device__ __forceinline__ void vp_split_key(long long key, float& m, int& idx) {
+  const unsigned long long k = (unsigned long long)key ^ 0x8000000000000000ull;
+  uint32_t u = (uint32_t)(k >> 32);
+  u = (u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u;
+  m = __uint_as_float(u);
+  idx = (int)(0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFull));
+}
+
+__global__ void vp_local_merge_kernel(const float* __restrict__ pm, const float* __restrict__ ps,
+                                      const int32_t* __restrict__ pi, const float* __restrict__ tl,
+                                      const int32_t* __restrict__ targets, int nb, long long n,
+                                      int vb, int ve, long long* key, float* m_loc, float* sums) {
+  const long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n) return;
+  float m = -INFINITY;
+  for (int j = 0; j < nb; ++j) m = fmaxf(m, pm[(long long)j * n + row]);
+  float s = 0.f;
+  int am = INT_MAX;
+  for (int j = 0; j < nb; ++j) {
+    const float mj = pm[(long long)j * n + row];
+    s += ps[(long long)j * n + row] * expf(mj - m);
+    if (mj == m && am == INT_MAX) am = pi[(long long)j * n + row];
+  }
+  const int y = targets[row];
+  key[row] = vp_make_key(m, am);
+  m_loc[row] = m;
+  sums[2 * row] = s;
+  sums[2 * row + 1] = (y >= vb && y < ve) ? tl[row] : 0.f;
+}
+
+cudaError_t launch_vp_local_merge(const float* pm, const float* ps, const int32_t* pi,
+                                  const float* tl, const int32_t* targets, int nb, long long n,
+                                  int vocab_begin, int vocab_end, long long* key, float* m_loc,
+                                  float* sums, cudaStream_t s) {
+  vp_local_merge_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+      pm, ps, pi, tl, targets, nb, n, vocab_begin, vocab_end, key, m_loc, sums);
+  return cudaGetLastError();
+}
+
+__global__ void vp_rescale_kernel(const long long* __restrict__ key, const float* __restrict__ m_loc,
+                                  float* sums, long long n) {
+  const long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n) return;
+  float m;
+  int idx;
+  vp_split_key(key[row], m, idx);
+  sums[2 * row] *= expf(m_loc[row] - m);
+}
+
+cudaError_t launch_vp_rescale(const long long* key_global, const float* m_loc, float* sums,
+                              long long n, cudaStream_t s) {
+  vp_rescale_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(key_global, m_loc, sums, n);
+  return cudaGetLastError();
+}
+
+__global__ void vp_finalize_kernel(const long long* __restrict__ key, const float* __restrict__ sums,
+                                   const int32_t* __restrict__ targets, long long n,
+                                   const long long* __restrict__ valid_count, float alpha,
+                                   float* __restrict__ lse, float* __restrict__ coef,
+                                   float* aux_lse, float* aux_loss, int32_t* aux_argmax,
+                                   float* aux_conf, float* __restrict__ loss_part) {
+  __shared__ double red[33];
+  const long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  double lossv = 0.0;
+  if (row < n) {
+    float m;
+    int am;
+    vp_split_key(key[row], m, am);
+    const float s = sums[2 * row];
+    const float l = m + logf(s);
+    const int y = targets[row];
+    const bool valid = y >= 0;
+    const float lt = valid ? l - sums[2 * row + 1] : 0.f;
+    const long long W = *valid_count;
+    lse[row] = l;
+    coef[row] = (valid && W > 0) ? alpha / (float)W : 0.f;
+    if (aux_lse) aux_lse[row] = l;
+    if (aux_loss) aux_loss[row] = lt;
+    if (aux_argmax) aux_argmax[row] = am;
+    if (aux_conf) aux_conf[row] = 1.0f / s;
+    lossv = (double)lt;
+  }
+  lossv = block_sum(lossv, red);
+  if (threadIdx.x == 0) loss_part[blockIdx.x] = (float)lossv;
+}
+
+cudaError_t launch_vp_finalize(const long long* key_global, const float* sums,
+                               const int32_t* targets, long long n, const long long* valid_count,
+                               float alpha, float* lse, float* coef, float* aux_lse,
+                               float* aux_loss, int32_t* aux_argmax, float* aux_conf,
+                               float* loss_part, int nblocks, cudaStream_t s) {
+  if (nblocks == 0) return cudaSuccess;
+  vp_finalize_kernel<<<nblocks, FINALIZE_THREADS, 0, s>>>(key_global, sums, targets, n,
+                                                          valid_count, alpha, lse, coef, aux_lse,
+                                                          aux_loss, aux_argmax, aux_conf,
+                                                          loss_part);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- optimizer
 static inline unsigned ew_blocks(long long n4) {
   long long b = (n4 + 255) / 256;

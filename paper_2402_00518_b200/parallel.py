@@ -57,3 +57,104 @@ def data_parallel_step(n_exits: int, count_local: Callable[[], torch.Tensor],
     if optimizer_step is not None:
         optimizer_step()
     return W
+
+
+# ---------------------------------------------------------------------------
+# Vocab-parallel W_out (BASELINE configs[3]: "vocab-parallel W_out over 8 GPUs")
+# ---------------------------------------------------------------------------
+
+EXIT_BODY = ("g_a", "w_gate", "w_up", "w_down", "g_f")   # replicated; W_out is sharded
+
+
+class TorchComm:
+    """Collectives of the vocab-parallel step over a torch.distributed group
+    (NCCL on GPUs, gloo on CPUs)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def all_gather_into(self, out, inp):
+        dist.all_gather_into_tensor(out, inp, group=self.group)
+
+    def all_reduce(self, t, op="sum", async_op=False):
+        o = dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM
+        return dist.all_reduce(t, op=o, group=self.group, async_op=async_op)
+
+    def reduce_scatter(self, out, inp):
+        dist.reduce_scatter_tensor(out, inp, op=dist.ReduceOp.SUM, group=self.group)
+
+
+class GpuPhases:
+    """The five ee_vp_* phases of the CUDA library for one rank."""
+
+    def __init__(self, ee, cfg, workspace, stream=None):
+        self.ee, self.cfg, self.ws, self.stream = ee, cfg, workspace, stream
+
+    def exit_forward(self, hidden, params, z_out, n_all):
+        self.ee.ee_vp_exit_forward(self.cfg, hidden, n_all, params, z_out, self.ws, self.stream)
+
+    def vocab_stats(self, z_all, targets_all, params, key, sums):
+        self.ee.ee_vp_vocab_stats(self.cfg, z_all, targets_all, params, key, sums, self.ws,
+                                  self.stream)
+
+    def rescale(self, key, sums):
+        self.ee.ee_vp_rescale(self.cfg, key.numel(), key, sums, self.ws, self.stream)
+
+    def vocab_backward(self, i, z_all, targets_all, key, sums, alpha, W, params, grads,
+                       dz_partial, loss_slot, accumulate, aux=None):
+        self.ee.ee_vp_vocab_backward(self.cfg, z_all, targets_all, key, sums, alpha, params, grads,
+                                     dz_partial, loss_slot, self.ws, valid_count=W,
+                                     accumulate=accumulate, aux=aux, exit_index=i,
+                                     stream=self.stream)
+
+    def exit_backward(self, hidden, params, dz_local, grads, accumulate, n_all):
+        self.ee.ee_vp_exit_backward(self.cfg, hidden, n_all, params, dz_local, grads, self.ws,
+                                    accumulate=accumulate, stream=self.stream)
+
+
+def vocab_parallel_step(phases, comm, arch: str, hidden_local, targets_all, params, grads,
+                        loss: torch.Tensor, exit_weights, W: torch.Tensor, bufs: dict,
+                        accumulate: bool = False, aux=None):
+    """One EE-Tuning step with W_out sharded by vocabulary rows over the ranks
+    of `comm` and tokens sharded for the exit bodies (equal shards, n_all =
+    world * n_local).  Per exit: all-gather z, the distributed softmax-CE
+    (MAX all-reduce of the (max, argmax) key, SUM all-reduce of the rescaled
+    sum-exp and target logit), local dW_out shard, reduce-scatter of dz back
+    to the token owners, and an async SUM all-reduce of the exit-body grads.
+
+    bufs: z_all [n_all x h] (exit-head input dtype), key [n_all] int64,
+    sums [n_all x 2] fp32, dz_partial [n_all x h] fp32, dz_local [n_local x h].
+    W: global valid-token count (int64 [1]).  loss[i] = global mean loss.
+    """
+    r = comm.rank
+    z_all, key, sums = bufs["z_all"], bufs["key"], bufs["sums"]
+    n_all = z_all.shape[0]
+    n_local = n_all // comm.world
+    if n_local * comm.world != n_all:
+        raise ValueError("vocab-parallel step needs equal token shards")
+    dz_partial = bufs.get("dz_partial") if arch != "embedding" else None
+    dz_local = bufs.get("dz_local") if arch != "embedding" else None
+    handles = []
+    for i in range(len(hidden_local)):
+        mine = z_all[r * n_local:(r + 1) * n_local]
+        phases.exit_forward(hidden_local[i], params[i], mine, n_all)            # a1-a4
+        comm.all_gather_into(z_all, mine)
+        phases.vocab_stats(z_all, targets_all, params[i], key, sums)            # a5
+        comm.all_reduce(key, "max")
+        phases.rescale(key, sums)
+        comm.all_reduce(sums, "sum")
+        phases.vocab_backward(i, z_all, targets_all, key, sums, exit_weights[i], W, params[i],
+                              grads[i], dz_partial, loss[i:i + 1], accumulate,
+                              None if aux is None else aux[i])                  # a6-a9
+        if dz_partial is not None:
+            comm.reduce_scatter(dz_local, dz_partial)
+        phases.exit_backward(hidden_local[i], params[i], dz_local, grads[i], accumulate,
+                             n_all)                                             # a10-a13
+        for k in EXIT_BODY:
+            if grads[i].get(k) is not None:
+                handles.append(comm.all_reduce(grads[i][k], "sum", async_op=True))
+    for h in handles:
+        if h is not None:
+            h.wait()

@@ -1,0 +1,175 @@
+"""Vocab-parallel orchestration on CPUs: world size 2 (and 3), gloo backend.
+
+The product's vocab_parallel_step (paper_2402_00518_b200.parallel) runs over
+real torch.distributed collectives (all-gather, signed-int64 MAX all-reduce of
+the (max, argmax) key, SUM all-reduce, reduce-scatter); each rank's compute is
+a numpy stand-in for the five ee_vp_* phases built from the fp64 oracle's
+pieces.  Gathered W_out shards, all-reduced body grads, losses and argmax must
+equal the single-process oracle on the full batch."""
+
+import os
+import socket
+import struct
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _key(m, idx):
+    """Same ordering as the CUDA key: orderable float32(m) high, ~idx low, sign-flipped."""
+    u = struct.unpack("<I", struct.pack("<f", float(m)))[0]
+    u = (~u & 0xFFFFFFFF) if u & 0x80000000 else (u | 0x80000000)
+    k = (u << 32) | (0xFFFFFFFF - idx)
+    k ^= 1 << 63
+    return k - (1 << 64) if k >= 1 << 63 else k
+
+
+def _unkey(k):
+    k = (k + (1 << 64)) % (1 << 64)
+    k ^= 1 << 63
+    u = k >> 32
+    u = (u & 0x7FFFFFFF) if u & 0x80000000 else (~u & 0xFFFFFFFF)
+    return struct.unpack("<f", struct.pack("<I", u))[0], 0xFFFFFFFF - (k & 0xFFFFFFFF)
+
+
+class NumpyPhases:
+    """fp64 stand-in for the ee_vp_* phases of one rank (shard [vb, ve))."""
+
+    def __init__(self, O, arch, vb, ve, eps=1e-5):
+        self.O, self.arch, self.vb, self.ve, self.eps = O, arch, vb, ve, eps
+
+    def exit_forward(self, hidden, params, z_out, n_all):
+        p = {k: v.numpy() for k, v in params.items()}
+        self.act = self.O.exit_forward(self.arch, p, hidden.numpy(), self.eps)
+        z_out.copy_(torch.from_numpy(self.act["z"]))
+
+    def vocab_stats(self, z_all, targets_all, params, key, sums):
+        S = z_all.numpy() @ params["w_out"].numpy().T
+        self.S = S
+        m = S.max(axis=1)
+        am = S.argmax(axis=1) + self.vb
+        self.m_loc = m
+        y = targets_all.numpy()
+        own = (y >= self.vb) & (y < self.ve)
+        sums[:, 0] = torch.from_numpy(np.exp(S - m[:, None]).sum(axis=1))
+        tl = np.where(own, S[np.arange(len(y)), np.clip(y - self.vb, 0, S.shape[1] - 1)], 0.0)
+        sums[:, 1] = torch.from_numpy(tl)
+        key.copy_(torch.tensor([_key(a, int(b)) for a, b in zip(m, am)], dtype=torch.int64))
+
+    def rescale(self, key, sums):
+        mg = np.array([_unkey(int(k))[0] for k in key])
+        self.m_glob = mg
+        sums[:, 0] *= torch.from_numpy(np.exp(self.m_loc - mg))
+
+    def vocab_backward(self, i, z_all, targets_all, key, sums, alpha, W, params, grads,
+                       dz_partial, loss_slot, accumulate, aux=None):
+        s = sums.numpy()
+        lse = self.m_glob + np.log(s[:, 0])
+        y = targets_all.numpy()
+        valid = y != -1
+        Wv = float(W.item())
+        loss_slot[0] = float(np.sum(np.where(valid, lse - s[:, 1], 0.0)) / Wv)
+        P = np.exp(self.S - lse[:, None])
+        own = valid & (y >= self.vb) & (y < self.ve)
+        P[np.nonzero(own)[0], y[own] - self.vb] -= 1.0
+        dS = (alpha * valid / Wv)[:, None] * P
+        grads["w_out"].copy_(torch.from_numpy(dS.T @ z_all.numpy()))
+        if dz_partial is not None:
+            dz_partial.copy_(torch.from_numpy(dS @ params["w_out"].numpy()))
+        if aux is not None:
+            aux["argmax"].copy_(torch.tensor([_unkey(int(k))[1] for k in key]))
+
+    def exit_backward(self, hidden, params, dz_local, grads, accumulate, n_all):
+        if self.arch == "embedding":
+            return
+        p = {k: v.numpy() for k, v in params.items()}
+        for k, g in self.O.exit_body_backward(self.arch, p, self.act, dz_local.numpy()).items():
+            grads[k].copy_(torch.from_numpy(g))
+
+
+def _worker(rank, world, port, arch, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import ee_oracle as O
+        from paper_2402_00518_b200.parallel import TorchComm, vocab_parallel_step
+        rng = np.random.default_rng(1)
+        h, V, F, N, E = 16, 40, 24, 12 * world, 2
+        params = [{"w_out": rng.normal(0, .5, (V, h))} for _ in range(E)]
+        for p in params:
+            if arch in ("norm", "mlp"):
+                p["g_f"] = 1 + .1 * rng.normal(size=h)
+            if arch == "mlp":
+                p.update(g_a=1 + .1 * rng.normal(size=h), w_gate=rng.normal(0, .5, (F, h)),
+                         w_up=rng.normal(0, .5, (F, h)), w_down=rng.normal(0, .5, (h, F)))
+        xs = [rng.normal(size=(N, h)) for _ in range(E)]
+        y = rng.integers(0, V, N)
+        y[[1, 7]] = -1
+        alphas = [1.0, 0.7]
+        w = 16                                            # shard width (multiple of 8)
+        vb, ve = min(V, rank * w), (V if rank == world - 1 else min(V, (rank + 1) * w))
+        nl = N // world
+        T = lambda a: torch.from_numpy(np.ascontiguousarray(a))
+        prm = [{k: T(v[vb:ve] if k == "w_out" else v) for k, v in p.items()} for p in params]
+        grd = [{k: torch.zeros_like(v) for k, v in p.items()} for p in prm]
+        hid = [T(x[rank * nl:(rank + 1) * nl]) for x in xs]
+        bufs = {"z_all": torch.zeros(N, h, dtype=torch.float64),
+                "key": torch.zeros(N, dtype=torch.int64),
+                "sums": torch.zeros(N, 2, dtype=torch.float64),
+                "dz_partial": torch.zeros(N, h, dtype=torch.float64),
+                "dz_local": torch.zeros(nl, h, dtype=torch.float64)}
+        W = torch.tensor([int(np.sum(y != -1))])
+        loss = torch.zeros(E, dtype=torch.float64)
+        aux = [{"argmax": torch.zeros(N, dtype=torch.int64)} for _ in range(E)]
+        vocab_parallel_step(NumpyPhases(O, arch, vb, ve), TorchComm(), arch, hid,
+                            torch.from_numpy(y), prm, grd, loss, alphas, W, bufs, aux=aux)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, ([g["w_out"].numpy() for g in grd],))
+        if rank == 0:
+            full_l, full_g, full_st = O.tune_step(arch, params, xs, y, alphas, 1e-5)
+            ok = np.allclose(loss.numpy(), full_l, rtol=1e-10)
+            for i in range(E):
+                dw = np.concatenate([gathered[r][0][i] for r in range(world)])
+                ok &= np.allclose(dw, full_g[i]["w_out"], rtol=1e-9, atol=1e-14)
+                for k in full_g[i]:
+                    if k != "w_out":
+                        ok &= np.allclose(grd[i][k].numpy(), full_g[i][k], rtol=1e-9, atol=1e-14)
+                ok &= np.array_equal(aux[i]["argmax"].numpy(), full_st[i]["argmax"])
+            q.put(bool(ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("arch,world", [("mlp", 2), ("norm", 3), ("embedding", 2)])
+def test_vocab_parallel_gloo_matches_full_batch_oracle(arch, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, arch, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    assert q.get(timeout=5) is True
+
+
+def test_key_encoding_orders_by_value_then_lowest_index():
+    vals = [(-3.5, 7), (-3.5, 2), (0.0, 9), (1e-30, 4), (2.25, 100), (2.25, 3), (float("inf"), 0)]
+    keys = [_key(m, i) for m, i in vals]
+    order = sorted(range(len(vals)), key=lambda j: keys[j])
+    expect = sorted(range(len(vals)), key=lambda j: (vals[j][0], -vals[j][1]))
+    assert order == expect
+    for (m, i), k in zip(vals, keys):
+        assert _unkey(k) == (np.float32(m), i)
