@@ -162,12 +162,15 @@ def run_reference(args, cfg, rank, world):
 
 
 def workload_config(cfg, world, args):
+    vp = getattr(args, "parallel", "dp") == "vp"
+    tok = cfg.tokens // world if vp else cfg.tokens
     return {"workload": f"{cfg.name}: h {cfg.hidden}, V {cfg.vocab}, F {cfg.ffn}, "
-                        f"{cfg.exits} {cfg.arch} exits, {cfg.tokens} tokens/GPU, "
-                        f"{cfg.init} init, W_out unsharded",
-            "global_batch": (cfg.tokens // 2048) * world, "seq_len": 2048,
-            "tokens_per_gpu": cfg.tokens, "exits": cfg.exits,
-            "parallelism": f"dp{world}",
+                        f"{cfg.exits} {cfg.arch} exits, {tok} tokens/GPU, "
+                        f"{cfg.init} init, " + (f"W_out vocab-parallel over {world}" if vp
+                                                else "W_out unsharded"),
+            "global_batch": (cfg.tokens // 2048) * (1 if vp else world), "seq_len": 2048,
+            "tokens_per_gpu": tok, "exits": cfg.exits,
+            "parallelism": f"vp{world}" if vp else f"dp{world}",
             "l2": "inputs larger than L2 (hidden states + exit weights per step >> 126 MB)",
             "optimizer": "Adam (P:374-375), included in the step"}
 
@@ -184,6 +187,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quick", action="store_true", help="ncu/profiling run: no extras")
+    ap.add_argument("--parallel", default="dp", choices=["dp", "vp"],
+                    help="N>1: dp = data parallel over tokens (weak scaling); vp = W_out "
+                         "vocab-parallel with the distributed softmax-CE (strong scaling)")
     args = ap.parse_args()
 
     import torch
@@ -208,16 +214,24 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    dp = world > 1
-    n = cfg.tokens
+    multi = world > 1
+    vp = args.parallel == "vp"
+    dp = world > 1 and not vp
+    n = cfg.tokens // world if vp else cfg.tokens       # tokens of this rank's exit bodies
+    n_all = cfg.tokens if vp else n
     E = cfg.exits
+    from paper_2402_00518_b200.parallel import (GpuPhases, LocalComm, TorchComm,
+                                                data_parallel_step, vocab_parallel_step,
+                                                vocab_shard)
+    vb, ve = vocab_shard(cfg.vocab, world, rank) if vp else (0, cfg.vocab)
 
     # ---- parameter store, Copy init from a synthetic backbone
-    heads = ee.ExitHeads(ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch), n, device=dev)
+    heads = ee.ExitHeads(ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch,
+                                     vocab_begin=vb, vocab_end=ve), n_all, device=dev)
     bb = S.backbone(cfg, device=dev)
     src = []
     for k in cfg.after:
-        d = {"w_out": bb["w_out"]}
+        d = {"w_out": bb["w_out"][vb:ve]}
         if cfg.arch in ("norm", "mlp"):
             d["g_f"] = bb["final_norm"]
         if cfg.arch == "mlp":
@@ -229,17 +243,35 @@ def main():
     del src, bb
     torch.cuda.empty_cache()
 
-    hidden = S.hidden_states(cfg, n, seed=cfg.seed * 100 + rank, device=dev)
-    targets = S.targets(cfg, n, seed=cfg.seed * 100 + rank, device=dev)
+    if vp:
+        # every rank generates the same global batch and keeps its token shard
+        hidden = []
+        for x in S.hidden_states(cfg, n_all, seed=cfg.seed * 100, device=dev):
+            hidden.append(x[rank * n:(rank + 1) * n].contiguous())
+            del x
+        targets = S.targets(cfg, n_all, seed=cfg.seed * 100, device=dev)   # all tokens
+        bufs = {"z_all": torch.zeros(n_all, cfg.hidden, dtype=torch.bfloat16, device=dev),
+                "key": torch.zeros(n_all, dtype=torch.int64, device=dev),
+                "sums": torch.zeros(n_all, 2, device=dev),
+                "dz_partial": torch.zeros(n_all, cfg.hidden, device=dev),
+                "dz_local": torch.zeros(n, cfg.hidden, device=dev)}
+        comm = TorchComm() if world > 1 else LocalComm()
+        phases = GpuPhases(ee, heads.cfg, heads.workspace)
+    else:
+        hidden = S.hidden_states(cfg, n, seed=cfg.seed * 100 + rank, device=dev)
+        targets = S.targets(cfg, n, seed=cfg.seed * 100 + rank, device=dev)
     vc = torch.zeros(1, dtype=torch.int64, device=dev)
+    job_tokens = n_all if vp else n * world
     total_iters = 40000
     one_cfg = ee.make_config(cfg.hidden, cfg.vocab, cfg.ffn, 1, cfg.arch)
 
-    from paper_2402_00518_b200.parallel import data_parallel_step
-
     def step(it, hid=hidden, tg=targets):
         lr = ee.ee_lr_at(min(it + 1, total_iters), total_iters)
-        if not dp:
+        if vp:
+            ee.ee_count_valid(tg, cfg.vocab, vc, heads.workspace)   # W over all tokens
+            vocab_parallel_step(phases, comm, cfg.arch, hid, tg, heads.operand, heads.grads,
+                                heads.loss, [1.0] * E, vc, bufs)
+        elif not dp:
             heads.step(hid, tg)
         else:
             def count_local():
@@ -258,7 +290,7 @@ def main():
     for it in range(args.warmup):
         step(it)
     torch.cuda.synchronize()
-    if dp:
+    if multi:
         dist.barrier()
 
     # ---- timed region (device time, CUDA events on the launching stream)
@@ -268,7 +300,7 @@ def main():
     l0 = ee.ee_launch_count()
     ee.ee_profile_start()
     torch.cuda.synchronize()
-    if dp:
+    if multi:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -276,14 +308,14 @@ def main():
         step(args.warmup + it)
     e1.record()
     torch.cuda.synchronize()
-    if dp:
+    if multi:
         dist.barrier()
     prof = ee.ee_profile_stop()
     launches = ee.ee_launch_count() - l0
     clocks = sampler.stop()
     ms = e0.elapsed_time(e1) / args.steps
     t = torch.tensor([ms], device=dev)
-    if dp:
+    if multi:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = t.item()
     code, idx = heads.status()
@@ -295,7 +327,7 @@ def main():
         t_host = targets.cpu().pin_memory()
         loss_host = torch.empty(E, dtype=torch.float32).pin_memory()
         torch.cuda.synchronize()
-        if dp:
+        if multi:
             dist.barrier()
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record()
@@ -308,15 +340,15 @@ def main():
         a1.record()
         torch.cuda.synchronize()
         te = torch.tensor([a0.elapsed_time(a1) / args.steps], device=dev)
-        if dp:
+        if multi:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": n * world / (te.item() / 1e3), "unit": "tokens/s",
+        e2e = {"value": job_tokens / (te.item() / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": sum(h.numel() * 2 for h in hidden) + targets.numel() * 4,
                "d2h_bytes_per_step": E * 4, "ms_per_step": te.item()}
         del h_host
 
     if rank != 0:
-        if dp:
+        if multi:
             dist.barrier()
             dist.destroy_process_group()
         return
@@ -362,13 +394,13 @@ def main():
                     "algorithmic_flops_per_launch": per_launch_flops,
                     "peak_source": peaks["source"] + ", sustained (kernel timed inside a long step)"}
 
-    F_alg = step_flops(cfg, n)
-    tflops = F_alg / (ms / 1e3) / 1e12
-    value = n * world / (ms / 1e3)
+    F_alg = step_flops(cfg, n_all if vp else n)          # per GPU for dp, whole job for vp
+    tflops = F_alg / (ms / 1e3) / 1e12 / (world if vp else 1)
+    value = job_tokens / (ms / 1e3)
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if vp else "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (seeded eesynth inputs, Copy init from a synthetic backbone)",
         "config": workload_config(cfg, world, args),
         "pct_peak": {"algorithmic_tflops_per_gpu": tflops,
@@ -395,7 +427,7 @@ def main():
             line["cpu_baseline"] = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(),
                                     "kind": "oracle", "sample": f"failed: {ex!r}"}
     print(json.dumps(line), flush=True)
-    if dp:
+    if multi:
         dist.barrier()
         dist.destroy_process_group()
 

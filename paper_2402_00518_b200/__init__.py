@@ -308,6 +308,7 @@ def ee_launch_count() -> int:
 # ---------------------------------------------------------------------------
 
 def tensor_shapes(hidden, vocab, ffn, arch):
+    """Parameter shapes of one exit; `vocab` = rows of W_out held (a shard under VP)."""
     s = {"w_out": (vocab, hidden)}
     if arch in ("norm", "mlp"):
         s["g_f"] = (hidden,)
@@ -324,6 +325,8 @@ class HeadSpec:
     num_exits: int
     arch: str
     norm_eps: float = 1e-5
+    vocab_begin: int = 0          # vocab-parallel shard of W_out rows [begin, end)
+    vocab_end: int | None = None
 
 
 class ExitHeads:
@@ -337,9 +340,10 @@ class ExitHeads:
     def __init__(self, spec: HeadSpec, max_tokens: int, device="cuda", adam=True):
         load()
         self.spec = spec
+        ve = spec.vocab if spec.vocab_end is None else spec.vocab_end
         self.cfg = make_config(spec.hidden, spec.vocab, spec.ffn, spec.num_exits, spec.arch,
-                               spec.norm_eps)
-        shapes = tensor_shapes(spec.hidden, spec.vocab, spec.ffn, spec.arch)
+                               spec.norm_eps, spec.vocab_begin, ve)
+        shapes = tensor_shapes(spec.hidden, ve - spec.vocab_begin, spec.ffn, spec.arch)
         dev = torch.device(device)
         E = spec.num_exits
 

@@ -869,6 +869,14 @@ ee_status ee_profile_record(int32_t i, char* name, int32_t name_len, float* ms, 
 
 int64_t ee_launch_count(void) { return g_launches; }
 
+// Debug hook (not in ee.h's product surface): arm a per-tile timing trace of the
+// next GEMM launch, then read (globaltimer_ns << 8 | smid) per tile.
+void ee_debug_trace_arm(void) { debug_trace_arm(); }
+int32_t ee_debug_trace_read(uint64_t* host, int32_t max) {
+  cudaDeviceSynchronize();
+  return debug_trace_read((unsigned long long*)host, max);
+}
+
 // Testing hook: C[M x N] (fp32, row-major) (+)= A B^T with A stored [M x K]
 // (a_kmajor) or [K x M], B stored [N x K] (b_kmajor) or [K x N]; bf16.
 ee_status ee_test_gemm(int32_t a_kmajor, int32_t b_kmajor, const void* A, const void* B, float* C,

@@ -51,6 +51,19 @@ static bool make_tmap(CUtensorMap* m, const Mat& t, uint32_t box_inner, uint32_t
   return r == CUDA_SUCCESS;
 }
 
+// Per-launch tile counters of the dynamic schedule (CTA-pair kernel): slot k is
+// zeroed on the launch's stream right before the launch that uses it.
+constexpr int kTileCounters = 4096;
+__device__ int g_tile_ctr[kTileCounters];
+static int* tile_counter(cudaStream_t st) {
+  static int* base = nullptr;
+  static unsigned next = 0;
+  if (!base && cudaGetSymbolAddress((void**)&base, g_tile_ctr) != cudaSuccess) return nullptr;
+  int* c = base + (next++ % kTileCounters);
+  if (cudaMemsetAsync(c, 0, sizeof(int), st) != cudaSuccess) return nullptr;
+  return c;
+}
+
 template <int EPI, bool A_MN, bool B_MN>
 static cudaError_t launch2(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1,
                            const GemmArgs& args, cudaStream_t st) {
@@ -64,13 +77,39 @@ static cudaError_t launch2(const CUtensorMap& a, const CUtensorMap& b0, const CU
   const int tiles = args.m_blocks * args.n_blocks;
   const int pairs = num_sms() / 2;
   const int grid = 2 * (tiles < pairs ? tiles : pairs);
-  kern<<<grid, GEMM_THREADS, G2_SMEM, st>>>(a, b0, b1, args);
+  GemmArgs a2 = args;
+  static const int dyn = getenv("EE_GEMM_DYN") ? atoi(getenv("EE_GEMM_DYN")) : 1;
+  a2.tile_counter = dyn ? tile_counter(st) : nullptr;
+  kern<<<grid, GEMM_THREADS, G2_SMEM, st>>>(a, b0, b1, a2);
   return cudaGetLastError();
 }
 
 static int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
   return v ? atoi(v) : dflt;
+}
+
+// Debug tile trace (EE_GEMM_TRACE=1): the first GEMM launch after
+// ee_debug_trace_arm() records, per tile, when its accumulator became ready.
+static unsigned long long* g_trace = nullptr;
+static int g_trace_cap = 0, g_trace_n = 0;
+static bool g_trace_armed = false;
+unsigned long long* trace_buffer(int tiles) {
+  if (!g_trace_armed) return nullptr;
+  g_trace_armed = false;
+  if (tiles > g_trace_cap) {
+    if (g_trace) cudaFree(g_trace);
+    cudaMalloc(&g_trace, sizeof(unsigned long long) * tiles);
+    g_trace_cap = tiles;
+  }
+  g_trace_n = tiles;
+  return g_trace;
+}
+void debug_trace_arm() { g_trace_armed = true; }
+int debug_trace_read(unsigned long long* host, int max) {
+  const int n = g_trace_n < max ? g_trace_n : max;
+  if (g_trace && n > 0) cudaMemcpy(host, g_trace, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost);
+  return n;
 }
 
 template <int EPI, bool A_MN, bool B_MN>
@@ -85,14 +124,34 @@ static cudaError_t launch(const CUtensorMap& a, const CUtensorMap& b0, const CUt
   }
   const int tiles = args.m_blocks * args.n_blocks;
   const int grid = tiles < num_sms() ? tiles : num_sms();
+  static const int cluster = env_int("EE_GEMM_CLUSTER", 1);  // placement experiment only
+  if (cluster > 1 && grid % cluster == 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(GEMM_THREADS);
+    cfg.dynamicSmemBytes = GEMM_SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a, b0, b1, args);
+  }
   kern<<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(a, b0, b1, args);
   return cudaGetLastError();
 }
 
+unsigned long long* trace_buffer(int tiles);
 cudaError_t gemm_run(int epi, bool a_kmajor, bool b_kmajor, const Mat& A, const Mat& B0,
                      const Mat* B1, int b_mode, int b_ksplit, GemmArgs args, cudaStream_t st) {
-  static const int cta_pair = env_int("EE_GEMM_CTA", 1) == 2;  // 1-CTA default: measured faster under the power cap
+  static const int cta_pair = env_int("EE_GEMM_CTA", 2) == 2;  // CTA pair + dynamic schedule: measured fastest (profiles/r01_cta2_dyn.log)
   static const int group = env_int("EE_GEMM_GROUP", 0);
+  static const int hint_a = env_int("EE_GEMM_HINT_A", -1);
+  static const int hint_b = env_int("EE_GEMM_HINT_B", -1);
+  static const int epi_sleep = env_int("EE_GEMM_SLEEP", 1);
   CUtensorMap ta, tb0, tb1;
   const bool a_mn = !a_kmajor, b_mn = !b_kmajor;
   if (!make_tmap(&ta, A, 64, a_mn ? 64 : GEMM_BM)) return cudaErrorInvalidValue;
@@ -112,6 +171,10 @@ cudaError_t gemm_run(int epi, bool a_kmajor, bool b_kmajor, const Mat& A, const 
   args.n_blocks = (args.N + bn - 1) / bn;
   args.k_blocks = (args.K + GEMM_BK - 1) / GEMM_BK;
   args.group_m = group > 0 ? group : (cta_pair ? 8 : 16);
+  args.hint_a = hint_a;
+  args.hint_b = hint_b;
+  args.epi_sleep = epi_sleep;
+  args.trace = trace_buffer(args.m_blocks * args.n_blocks);
   if (args.m_blocks == 0 || args.n_blocks == 0 || args.k_blocks == 0) return cudaSuccess;
 
 #define EE_GEMM_CASE(E, AM, BM)                                              \

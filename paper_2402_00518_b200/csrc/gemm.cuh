@@ -52,6 +52,10 @@ struct GemmArgs {
   int M, N, K;  // N = logical output columns (B_PAIR: columns of each of the two halves)
   int m_blocks, n_blocks, k_blocks;
   int b_mode, b_ksplit, group_m;
+  int hint_a, hint_b;
+  int epi_sleep;  // epilogue waits with a suspend-time hint instead of spinning
+  int* tile_counter;  // CTA-pair kernel: dynamic tile schedule counter (zeroed per launch), or NULL
+  unsigned long long* trace;  // debug: per-tile (globaltimer << 8 | smid) at accumulator-ready, or NULL  // L2 policy of the A / B TMA loads: -1 none, 0 normal, 1 evict_last, 2 evict_first
   // EPI_F32 / EPI_RESID
   float* out0;
   float* out1;
@@ -90,6 +94,14 @@ __device__ __forceinline__ void tile_coords(const GemmArgs& a, int tile, int& mb
 }
 
 __device__ __forceinline__ float u2f(uint32_t v) { return __uint_as_float(v); }
+
+__device__ __forceinline__ unsigned long long trace_stamp() {
+  unsigned long long t;
+  uint32_t sm;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  return (t << 8) | (sm & 0xFF);
+}
 
 // Epilogue of one accumulator tile: thread `row` of the 128 epilogue threads
 // owns TMEM lane `row` = output row gm; `tb` = TMEM address of this warp's
@@ -331,6 +343,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
+      const uint64_t pa = l2_policy(args.hint_a), pb = l2_policy(args.hint_b);
+      const bool ha = args.hint_a >= 0, hb = args.hint_b >= 0;
+      auto lda = [&](void* d, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+        if (ha) tma_load_2d_hint(d, m, bar, c0, c1, pa); else tma_load_2d(d, m, bar, c0, c1);
+      };
+      auto ldb = [&](void* d, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+        if (hb) tma_load_2d_hint(d, m, bar, c0, c1, pb); else tma_load_2d(d, m, bar, c0, c1);
+      };
       int s = 0;
       uint32_t ph = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -343,15 +363,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           uint8_t* b = sB + s * GEMM_B_STAGE;
           const int k0 = kb * GEMM_BK;
           if constexpr (!A_MN) {
-            tma_load_2d(a, &tmA, &full[s], k0, m0);
+            lda(a, &tmA, &full[s], k0, m0);
           } else {
-            tma_load_2d(a, &tmA, &full[s], m0, k0);
-            tma_load_2d(a + 8192, &tmA, &full[s], m0 + 64, k0);
+            lda(a, &tmA, &full[s], m0, k0);
+            lda(a + 8192, &tmA, &full[s], m0 + 64, k0);
           }
           if (args.b_mode == B_PAIR) {
             const int n0 = nb * (GEMM_BN / 2);
-            tma_load_2d(b, &tmB0, &full[s], k0, n0);
-            tma_load_2d(b + GEMM_B_STAGE / 2, &tmB1, &full[s], k0, n0);
+            ldb(b, &tmB0, &full[s], k0, n0);
+            ldb(b + GEMM_B_STAGE / 2, &tmB1, &full[s], k0, n0);
           } else {
             const CUtensorMap* mB = &tmB0;
             int kk = k0;
@@ -361,10 +381,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
             const int n0 = nb * GEMM_BN;
             if constexpr (!B_MN) {
-              tma_load_2d(b, mB, &full[s], kk, n0);
+              ldb(b, mB, &full[s], kk, n0);
             } else {
 #pragma unroll
-              for (int j = 0; j < 4; ++j) tma_load_2d(b + j * 8192, mB, &full[s], n0 + 64 * j, kk);
+              for (int j = 0; j < 4; ++j) ldb(b + j * 8192, mB, &full[s], n0 + 64 * j, kk);
             }
           }
           mbar_arrive_expect_tx(&full[s], GEMM_A_STAGE + GEMM_B_STAGE);
@@ -424,10 +444,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tile_coords(args, tile, mb, nb);
       const int gm = mb * GEMM_BM + row;
       const bool row_ok = gm < args.M;
-      mbar_wait(&tfull[acc], acc_ph);
+      if (args.epi_sleep) mbar_wait_sleep(&tfull[acc], acc_ph); else mbar_wait(&tfull[acc], acc_ph);
       tc_fence_after();
       const uint32_t tb = tmem_base + acc * GEMM_BN + (static_cast<uint32_t>(ew * 32) << 16);
-
+      if (args.trace && threadIdx.x == 128) args.trace[tile] = trace_stamp();
+      (void)row_ok;
       epilogue_tile<EPI>(args, tb, gm, nb);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
@@ -464,6 +485,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 constexpr int G2_STAGES = 6;
 constexpr int G2_A_STAGE = 128 * GEMM_BK * 2;  // 16 KB (this CTA's 128 rows of A)
 constexpr int G2_B_STAGE = 128 * GEMM_BK * 2;  // 16 KB (this CTA's half of B)
+constexpr int G2_SQ = 4;  // depth of the tile-index ring (dynamic schedule)
 constexpr int G2_SMEM = G2_STAGES * (G2_A_STAGE + G2_B_STAGE) + 1024 + 256;
 
 template <int EPI, bool A_MN, bool B_MN>
@@ -479,7 +501,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   uint64_t* empty = full + G2_STAGES;
   uint64_t* tfull = empty + G2_STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* sfull = tempty + 2;        // tile ring: slot published (both CTAs)
+  uint64_t* sempty = sfull + G2_SQ;     // tile ring: slot consumed (leader, 10 arrivals)
+  int* ring = reinterpret_cast<int*>(sempty + G2_SQ);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + G2_SQ);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -500,6 +525,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 256);
     }
+    for (int s = 0; s < G2_SQ; ++s) {
+      mbar_init(&sfull[s], 1);
+      mbar_init(&sempty[s], 10);  // leader MMA + 4 epilogue warps of each CTA + peer producer
+    }
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -513,12 +542,68 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
   const int num_tiles = args.m_blocks * args.n_blocks;
 
+  // Tile schedule.  Static: cluster c takes tiles c, c+P, ...  Dynamic
+  // (args.tile_counter): the leader's producer claims the next tile with an
+  // atomicAdd and publishes it through a small smem ring in both CTAs; every
+  // consumer unit (leader MMA thread, 4 epilogue warps per CTA, peer producer)
+  // reads it and releases the slot.  Clusters then take tiles in global order
+  // as they free up, so the clusters sharing an operand block stay within a
+  // tile of each other instead of drifting apart over hundreds of tiles (the
+  // drift cost 3x DRAM traffic: profiles/r01_cta2_trace.log).
+  const bool dyn = args.tile_counter != nullptr;
+  int sj = 0;
+  uint32_t sph = 0;
+  auto take = [&]() -> int {  // one lane per consumer unit
+    mbar_wait_acq_cluster(&sfull[sj], sph);
+    const int t = ring[sj];
+    if (leader)
+      mbar_arrive(&sempty[sj]);
+    else
+      mbar_arrive_cluster(mapa_shared(smem_u32(&sempty[sj]), 0));
+    if (++sj == G2_SQ) {
+      sj = 0;
+      sph ^= 1;
+    }
+    return t;
+  };
+  auto publish = [&]() -> int {  // leader producer
+    mbar_wait(&sempty[sj], sph ^ 1);
+    int t = atomicAdd(args.tile_counter, 1);
+    if (t >= num_tiles) t = -1;
+    ring[sj] = t;
+    st_shared_cluster_u32(mapa_shared(smem_u32(&ring[sj]), 1), (uint32_t)t);
+    mbar_arrive(&sfull[sj]);
+    mbar_arrive_cluster(mapa_shared(smem_u32(&sfull[sj]), 1));
+    if (++sj == G2_SQ) {
+      sj = 0;
+      sph ^= 1;
+    }
+    return t;
+  };
+  auto first_tile = [&](bool producer) -> int {
+    if (!dyn) return cluster_id;
+    return producer ? (leader ? publish() : take()) : take();
+  };
+  auto next_tile = [&](int tile, bool producer) -> int {
+    if (!dyn) return tile + nclusters;
+    return producer ? (leader ? publish() : take()) : take();
+  };
+
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
+      const uint64_t pa = l2_policy(args.hint_a), pb = l2_policy(args.hint_b);
+      const bool ha = args.hint_a >= 0, hb = args.hint_b >= 0;
+      auto lda = [&](void* d, const CUtensorMap* m, uint32_t bar, int c0, int c1) {
+        if (ha) tma_load_2d_2sm_hint(d, m, bar, c0, c1, pa); else tma_load_2d_2sm(d, m, bar, c0, c1);
+      };
+      auto ldb = [&](void* d, const CUtensorMap* m, uint32_t bar, int c0, int c1) {
+        if (hb) tma_load_2d_2sm_hint(d, m, bar, c0, c1, pb); else tma_load_2d_2sm(d, m, bar, c0, c1);
+      };
       int s = 0;
       uint32_t ph = 0;
-      for (int tile = cluster_id; tile < num_tiles; tile += nclusters) {
+      for (int tile = first_tile(true); tile >= 0 && tile < num_tiles;
+           tile = next_tile(tile, true)) {
         int mb, nb;
         tile_coords(args, tile, mb, nb);
         const int m0 = mb * 256 + (int)rank * 128;
@@ -529,14 +614,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           uint8_t* b = sB + s * G2_B_STAGE;
           const int k0 = kb * GEMM_BK;
           if constexpr (!A_MN) {
-            tma_load_2d_2sm(a, &tmA, fb, k0, m0);
+            lda(a, &tmA, fb, k0, m0);
           } else {
-            tma_load_2d_2sm(a, &tmA, fb, m0, k0);
-            tma_load_2d_2sm(a + 8192, &tmA, fb, m0 + 64, k0);
+            lda(a, &tmA, fb, m0, k0);
+            lda(a + 8192, &tmA, fb, m0 + 64, k0);
           }
           if (args.b_mode == B_PAIR) {
             // CTA 0 holds the 128 gate rows, CTA 1 the 128 up rows of the same f range
-            tma_load_2d_2sm(b, rank ? &tmB1 : &tmB0, fb, k0, nb * 128);
+            ldb(b, rank ? &tmB1 : &tmB0, fb, k0, nb * 128);
           } else {
             const CUtensorMap* mB = &tmB0;
             int kk = k0;
@@ -546,10 +631,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
             }
             const int n0 = nb * GEMM_BN + (int)rank * 128;
             if constexpr (!B_MN) {
-              tma_load_2d_2sm(b, mB, fb, kk, n0);
+              ldb(b, mB, fb, kk, n0);
             } else {
-              tma_load_2d_2sm(b, mB, fb, n0, kk);
-              tma_load_2d_2sm(b + 8192, mB, fb, n0 + 64, kk);
+              ldb(b, mB, fb, n0, kk);
+              ldb(b + 8192, mB, fb, n0 + 64, kk);
             }
           }
           if (leader) mbar_arrive_expect_tx(&full[s], 2 * (G2_A_STAGE + G2_B_STAGE));
@@ -568,7 +653,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       uint32_t ph = 0;
       int acc = 0;
       uint32_t acc_ph = 0;
-      for (int tile = cluster_id; tile < num_tiles; tile += nclusters) {
+      for (int tile = first_tile(false); tile >= 0 && tile < num_tiles;
+           tile = next_tile(tile, false)) {
         mbar_wait(&tempty[acc], acc_ph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * GEMM_BN;
@@ -606,12 +692,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     uint32_t acc_ph = 0;
     const uint32_t te0 = mapa_shared(smem_u32(&tempty[0]), 0);
     const uint32_t te1 = mapa_shared(smem_u32(&tempty[1]), 0);
-    for (int tile = cluster_id; tile < num_tiles; tile += nclusters) {
+    auto warp_tile = [&](int prev, bool first) -> int {  // lane 0 consumes, broadcast
+      int t = 0;
+      if (lane == 0) t = first ? first_tile(false) : next_tile(prev, false);
+      return __shfl_sync(0xffffffffu, t, 0);
+    };
+    for (int tile = warp_tile(0, true); tile >= 0 && tile < num_tiles;
+         tile = warp_tile(tile, false)) {
       int mb, nb;
       tile_coords(args, tile, mb, nb);
-      mbar_wait(&tfull[acc], acc_ph);
+      if (args.epi_sleep) mbar_wait_sleep(&tfull[acc], acc_ph); else mbar_wait(&tfull[acc], acc_ph);
       tc_fence_after();
       const uint32_t tb = tmem_base + acc * GEMM_BN + (static_cast<uint32_t>(ew * 32) << 16);
+      if (args.trace && threadIdx.x == 128 && rank == 0) args.trace[tile] = trace_stamp();
       epilogue_tile<EPI>(args, tb, mb * 256 + (int)rank * 128 + row, nb);
       tc_fence_before();
       mbar_arrive_cluster(acc ? te1 : te0);

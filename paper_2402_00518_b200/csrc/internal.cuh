@@ -28,6 +28,8 @@ struct Mat {  // a row-major bf16 matrix in global memory
 cudaError_t gemm_run(int epi, bool a_kmajor, bool b_kmajor, const Mat& A, const Mat& B0,
                      const Mat* B1, int b_mode, int b_ksplit, GemmArgs args, cudaStream_t st);
 int num_sms();
+void debug_trace_arm();
+int debug_trace_read(unsigned long long* host, int max);
 
 // ---- bandwidth-bound kernels (kernels.cu) -----------------------------------
 cudaError_t launch_count_valid(const int32_t* targets, long long n, int vocab, long long* out,

@@ -86,6 +86,30 @@ class TorchComm:
         dist.reduce_scatter_tensor(out, inp, op=dist.ReduceOp.SUM, group=self.group)
 
 
+class LocalComm:
+    """World of one: every collective is the identity (P = 1)."""
+    rank, world = 0, 1
+
+    def all_gather_into(self, out, inp):
+        if inp.data_ptr() != out.data_ptr():
+            out[:inp.shape[0]].copy_(inp)
+
+    def all_reduce(self, t, op="sum", async_op=False):
+        return None
+
+    def reduce_scatter(self, out, inp):
+        out.copy_(inp[:out.shape[0]])
+
+
+def vocab_shard(V: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous W_out row shard of `rank`; widths are multiples of 8 (TMA row
+    stride rule), the last shard takes the remainder."""
+    w = ((V // world + 7) // 8) * 8
+    b = min(V, rank * w)
+    e = V if rank == world - 1 else min(V, (rank + 1) * w)
+    return b, e
+
+
 class GpuPhases:
     """The five ee_vp_* phases of the CUDA library for one rank."""
 
