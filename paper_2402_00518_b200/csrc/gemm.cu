@@ -78,8 +78,13 @@ static cudaError_t launch2(const CUtensorMap& a, const CUtensorMap& b0, const CU
   const int pairs = num_sms() / 2;
   const int grid = 2 * (tiles < pairs ? tiles : pairs);
   GemmArgs a2 = args;
+  // Schedule: K = h GEMMs (short mainloop) take tiles dynamically; long-K
+  // GEMMs use the static schedule with a per-wave soft barrier.
   static const int dyn = getenv("EE_GEMM_DYN") ? atoi(getenv("EE_GEMM_DYN")) : 1;
-  a2.tile_counter = dyn ? tile_counter(st) : nullptr;
+  static const int wsync = getenv("EE_GEMM_WAVESYNC") ? atoi(getenv("EE_GEMM_WAVESYNC")) : 1;
+  const bool long_k = args.K >= 16384;
+  a2.tile_counter = (dyn && !(wsync && long_k)) ? tile_counter(st) : nullptr;
+  a2.wave_counter = (wsync && long_k && a2.tile_counter == nullptr) ? tile_counter(st) : nullptr;
   kern<<<grid, GEMM_THREADS, G2_SMEM, st>>>(a, b0, b1, a2);
   return cudaGetLastError();
 }
@@ -170,7 +175,18 @@ cudaError_t gemm_run(int epi, bool a_kmajor, bool b_kmajor, const Mat& A, const 
   const int bn = (b_mode == B_PAIR) ? GEMM_BN / 2 : GEMM_BN;
   args.n_blocks = (args.N + bn - 1) / bn;
   args.k_blocks = (args.K + GEMM_BK - 1) / GEMM_BK;
-  args.group_m = group > 0 ? group : (cta_pair ? 8 : 16);
+  // Rasterisation group (M-blocks per group).  Long-K GEMMs (K >= 16384: the
+  // weight gradients over tokens, dz over V, du over 2F, down over F) want
+  // small groups, the K = h GEMMs 8 (measured DRAM traffic per launch,
+  // profiles/r01_dyn_group_sweep.log).
+  static const int g_long = env_int("EE_GEMM_GROUP_LONGK", 4);
+  static const int g_short = env_int("EE_GEMM_GROUP_SHORTK", 8);
+  if (group > 0)
+    args.group_m = group;
+  else if (cta_pair)
+    args.group_m = args.K >= 16384 ? g_long : g_short;
+  else
+    args.group_m = 16;
   args.hint_a = hint_a;
   args.hint_b = hint_b;
   args.epi_sleep = epi_sleep;

@@ -55,6 +55,7 @@ struct GemmArgs {
   int hint_a, hint_b;
   int epi_sleep;  // epilogue waits with a suspend-time hint instead of spinning
   int* tile_counter;  // CTA-pair kernel: dynamic tile schedule counter (zeroed per launch), or NULL
+  int* wave_counter;  // CTA-pair kernel, static schedule: per-wave soft barrier counter, or NULL
   unsigned long long* trace;  // debug: per-tile (globaltimer << 8 | smid) at accumulator-ready, or NULL  // L2 policy of the A / B TMA loads: -1 none, 0 normal, 1 evict_last, 2 evict_first
   // EPI_F32 / EPI_RESID
   float* out0;
@@ -602,8 +603,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       };
       int s = 0;
       uint32_t ph = 0;
+      int wave = 0;
       for (int tile = first_tile(true); tile >= 0 && tile < num_tiles;
-           tile = next_tile(tile, true)) {
+           tile = next_tile(tile, true), ++wave) {
+        if (args.wave_counter != nullptr && leader) {
+          // Soft wave barrier (static schedule): the leaders of all clusters
+          // start wave w together, so clusters sharing an operand stream the
+          // same K range at the same time and hit in L2 (long-K GEMMs).  The
+          // wait is bounded (50 us) so co-running kernels (NCCL) that keep a
+          // cluster off the GPU cannot deadlock it.
+          red_add_release_gpu(args.wave_counter, 1);
+          const int target = min(num_tiles, (wave + 1) * nclusters);
+          const unsigned long long t0 = globaltimer_ns();
+          while (ld_acquire_gpu(args.wave_counter) < target &&
+                 globaltimer_ns() - t0 < 50000ull) {
+          }
+        }
         int mb, nb;
         tile_coords(args, tile, mb, nb);
         const int m0 = mb * 256 + (int)rank * 128;

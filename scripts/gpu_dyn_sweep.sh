@@ -1,0 +1,10 @@
+M="--metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control base -k regex:gemm -s 0 -c 10"
+for g in 8 4 16; do
+echo "GROUP=$g"
+EE_GEMM_GROUP=$g ncu $M python bench.py --quick --steps 1 --warmup 0 2>&1 | grep -E "dram__bytes_read|duration" | awk '{printf "%s ", $3} END {print ""}'
+EE_GEMM_GROUP=$g timeout 900 python bench.py --steps 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); k=d.pop('kernels'); print('GROUP=$g', round(d['ms_per_step'],1), round(d['value']), round(d['pct_peak']['of_burst'],3), d['clocks']['sm_mhz'])"
+done
+echo "GROUP=8 HINT 1 1"
+EE_GEMM_HINT_A=1 EE_GEMM_HINT_B=1 timeout 900 python bench.py --steps 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); k=d.pop('kernels'); print('HINT', round(d['ms_per_step'],1), round(d['value']), round(d['pct_peak']['of_burst'],3), d['clocks']['sm_mhz'])"

@@ -1,0 +1,10 @@
+timeout 300 python -m pytest tests/test_gpu_gemm.py tests/test_gpu_parity.py -x -q 2>&1 | tail -2
+M="--metrics dram__bytes_read.sum,gpu__time_duration.sum --clock-control base -k regex:gemm -s 0 -c 10"
+for ws in 1 0; do
+echo "WAVESYNC=$ws"
+EE_GEMM_WAVESYNC=$ws ncu $M python bench.py --quick --steps 1 --warmup 0 2>&1 | grep -E "dram__bytes_read|duration" | awk '{printf "%s ", $3} END {print ""}'
+done
+for ws in 1 0 1 0; do
+EE_GEMM_WAVESYNC=$ws timeout 900 python bench.py --steps 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); k=d.pop('kernels'); print('WAVESYNC=$ws', round(d['ms_per_step'],1), round(d['value']), round(d['pct_peak']['of_burst'],3), d['clocks']['sm_mhz']); print({n: round(v['ms_per_launch'],1) for n,v in list(k.items())[:10]})"
+done
