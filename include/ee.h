@@ -64,6 +64,16 @@ typedef enum { EE_ARCH_EMBEDDING = 0, EE_ARCH_NORM = 1, EE_ARCH_MLP = 2 } ee_arc
 /* Initialisation of exit parameters. */
 typedef enum { EE_INIT_COPY = 0, EE_INIT_RANDOM = 1 } ee_init;
 
+/* Token weights of the exit loss.
+ * UNIFORM:    w_t = 1 for valid tokens; L_i = sum_t w_t loss_t / W  (A4).
+ * CONFIDENCE: dynamic token-wise weights (App. B.3):
+ *             w_t = c_t = max softmax probability of the exit at token t,
+ *             detached (a constant in the backward); L_i = sum_t c_t loss_t /
+ *             sum_t c_t (normalisation: DESIGN.md A17).  Needs all tokens of
+ *             the batch in one call (ee_tune_step without valid_count, or the
+ *             ee_vp_* phases); a DP shard returns EE_ERR_UNSUPPORTED. */
+typedef enum { EE_WEIGHT_UNIFORM = 0, EE_WEIGHT_CONFIDENCE = 1 } ee_token_weighting;
+
 /* Element type of Copy-init source tensors. */
 typedef enum { EE_DTYPE_BF16 = 0, EE_DTYPE_F32 = 1 } ee_dtype;
 
@@ -78,12 +88,14 @@ typedef enum { EE_DTYPE_BF16 = 0, EE_DTYPE_F32 = 1 } ee_dtype;
  *               the rows [vocab_begin, vocab_end) of W_out held by this call
  *               (a vocab-parallel shard, 0 <= begin < end <= V, width a
  *               multiple of 8).  ee_tune_step needs the full vocabulary
- *               [0, V); shards are driven through the ee_vp_* phases. */
+ *               [0, V); shards are driven through the ee_vp_* phases.
+ *  token_weighting  ee_token_weighting. */
 typedef struct {
   int32_t hidden, vocab, ffn, num_exits;
   int32_t arch;
   float norm_eps;
   int32_t vocab_begin, vocab_end;
+  int32_t token_weighting;
 } ee_head_config;
 
 /* Parameters (or gradients, or optimizer moments) of ONE exit.  Device

@@ -172,18 +172,33 @@ class ExitResult:
 
 def exit_loss_and_grads(arch: str, params: dict, x: np.ndarray, targets: np.ndarray,
                         alpha: float, eps: float, valid_count: int | None = None,
-                        keep_act: bool = False) -> ExitResult:
+                        keep_act: bool = False, weighting="uniform") -> ExitResult:
     """Loss and parameter gradients of one exit.
 
     ``valid_count`` is W, the normaliser of the mean over valid tokens; it
     defaults to the number of valid tokens in ``targets`` (single-GPU
     semantics) and is the *global* count under data parallelism (A16).
     The gradient is that of alpha * L_i (A5).
+
+    ``weighting``: "uniform" (w_t = 1 on valid tokens); "confidence" -- the
+    dynamic token-wise weights of P:326-336 / App. B.3: w_t = c_t,
+    the exit's maximum softmax probability at token t, "detached from the
+    computational graph and thus regarded as constants"; or an explicit array
+    of per-token constants.  Non-uniform weights are normalised by their sum
+    over valid tokens (A17); ``valid_count`` then does not apply.
     """
     act = exit_forward(arch, params, x, eps)
     st = lm_loss_stats(act["S"], targets)
     w = st["valid"].astype(np.float64)
-    W = float(np.sum(w)) if valid_count is None else float(valid_count)
+    if isinstance(weighting, str) and weighting == "uniform":
+        W = float(np.sum(w)) if valid_count is None else float(valid_count)
+    else:
+        c = st["conf"] if isinstance(weighting, str) and weighting == "confidence" \
+            else np.asarray(weighting, dtype=np.float64)
+        if isinstance(weighting, str) and weighting != "confidence":
+            raise ValueError(f"unknown weighting {weighting!r}")
+        w = w * c                                           # detached constants (P:896-899)
+        W = float(np.sum(w))
     z = act["z"]
     grads = {k: np.zeros_like(v) for k, v in params.items() if v is not None}
     if W == 0.0:

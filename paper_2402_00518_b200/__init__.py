@@ -44,7 +44,7 @@ class ee_head_config(ctypes.Structure):
     _fields_ = [("hidden", ctypes.c_int32), ("vocab", ctypes.c_int32), ("ffn", ctypes.c_int32),
                 ("num_exits", ctypes.c_int32), ("arch", ctypes.c_int32),
                 ("norm_eps", ctypes.c_float), ("vocab_begin", ctypes.c_int32),
-                ("vocab_end", ctypes.c_int32)]
+                ("vocab_end", ctypes.c_int32), ("token_weighting", ctypes.c_int32)]
 
 
 class ee_head_tensors(ctypes.Structure):
@@ -122,9 +122,15 @@ def _stream(stream=None):
     return ctypes.c_void_p(s.cuda_stream)
 
 
-def make_config(hidden, vocab, ffn, num_exits, arch, norm_eps=1e-5, vocab_begin=0, vocab_end=None):
+WEIGHTING = {"uniform": 0, "confidence": 1}
+
+
+def make_config(hidden, vocab, ffn, num_exits, arch, norm_eps=1e-5, vocab_begin=0, vocab_end=None,
+                token_weighting="uniform"):
     return ee_head_config(hidden, vocab, ffn, num_exits, ARCH[arch] if isinstance(arch, str) else arch,
-                          norm_eps, vocab_begin, vocab if vocab_end is None else vocab_end)
+                          norm_eps, vocab_begin, vocab if vocab_end is None else vocab_end,
+                          WEIGHTING[token_weighting] if isinstance(token_weighting, str)
+                          else token_weighting)
 
 
 def heads(list_of_dicts):
@@ -327,6 +333,7 @@ class HeadSpec:
     norm_eps: float = 1e-5
     vocab_begin: int = 0          # vocab-parallel shard of W_out rows [begin, end)
     vocab_end: int | None = None
+    token_weighting: str = "uniform"   # or "confidence"
 
 
 class ExitHeads:
@@ -342,7 +349,7 @@ class ExitHeads:
         self.spec = spec
         ve = spec.vocab if spec.vocab_end is None else spec.vocab_end
         self.cfg = make_config(spec.hidden, spec.vocab, spec.ffn, spec.num_exits, spec.arch,
-                               spec.norm_eps, spec.vocab_begin, ve)
+                               spec.norm_eps, spec.vocab_begin, ve, spec.token_weighting)
         shapes = tensor_shapes(spec.hidden, ve - spec.vocab_begin, spec.ffn, spec.arch)
         dev = torch.device(device)
         E = spec.num_exits

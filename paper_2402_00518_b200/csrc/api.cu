@@ -72,12 +72,15 @@ ee_status check_cfg(const ee_head_config* c) {
     return fail(EE_ERR_SHAPE, "ffn must be a positive multiple of 128 for MLP exits, got %d",
                 c->ffn);
   if (!(c->norm_eps >= 0.f)) return fail(EE_ERR_ARG, "norm_eps must be >= 0");
+  if (c->token_weighting != EE_WEIGHT_UNIFORM && c->token_weighting != EE_WEIGHT_CONFIDENCE)
+    return fail(EE_ERR_ARG, "unknown token_weighting %d", c->token_weighting);
   return EE_OK;
 }
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
+  size_t wsum_part, wsum;
   size_t status, vcount, loss_part, lse, coef, tgt, pm, ps, pi, z, ds, dz, dgp, ry, u, rx, ab,
       mact, y, dy, total;
   int nb, nparts, nfin;
@@ -98,6 +101,8 @@ Layout make_layout(const ee_head_config* c, long long n) {
   L.status = take(sizeof(DevStatus));
   L.vcount = take(8);
   L.loss_part = take(4 * (size_t)(L.nfin > 0 ? L.nfin : 1));
+  L.wsum_part = take(4 * (size_t)(L.nfin > 0 ? L.nfin : 1));
+  L.wsum = take(4);
   L.lse = take(4 * n);
   L.coef = take(4 * n);
   L.tgt = take(4 * n);
@@ -266,7 +271,7 @@ namespace {
 struct Bufs {
   DevStatus* status;
   long long* vcount;
-  float *lse, *coef, *tgt, *pm, *ps, *loss_part;
+  float *lse, *coef, *tgt, *pm, *ps, *loss_part, *wsum_part, *wsum;
   int32_t* pi;
   __nv_bfloat16* ds;
   __nv_bfloat16* z;
@@ -296,6 +301,8 @@ Bufs make_bufs(const ee_head_config* cfg, long long n, void* workspace) {
   B.ps = (float*)(ws + L.ps);
   B.pi = (int32_t*)(ws + L.pi);
   B.loss_part = (float*)(ws + L.loss_part);
+  B.wsum_part = (float*)(ws + L.wsum_part);
+  B.wsum = (float*)(ws + L.wsum);
   B.ds = (__nv_bfloat16*)(ws + L.ds);
   B.m_loc = B.coef;  // VP: m_loc is dead before coef is written (vp_finalize)
   if (nrm) {
@@ -522,6 +529,9 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
       (n_tokens > 0 && !targets))
     return fail(EE_ERR_ARG, "NULL argument or n_tokens < 0");
   if (n_tokens > (1LL << 30)) return fail(EE_ERR_SHAPE, "n_tokens too large");
+  if (valid_count && cfg->token_weighting == EE_WEIGHT_CONFIDENCE)
+    return fail(EE_ERR_UNSUPPORTED, "confidence weighting needs every token of the batch in one "
+                                    "call (single GPU or the ee_vp_* phases), not a DP shard");
   for (int i = 0; i < E; ++i) {
     if ((s = check_arch_tensors(cfg, params[i], "params", i)) != EE_OK) return s;
     if ((s = check_arch_tensors(cfg, grads[i], "grads", i)) != EE_OK) return s;
@@ -558,13 +568,20 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
     // a6: lse, coef, per-token aux, L_i
     {
       const ee_step_aux* ax = aux ? &aux[i] : nullptr;
+      const bool dynw = cfg->token_weighting == EE_WEIGHT_CONFIDENCE;
       { Prof p_("a6_ce_finalize", st, 0, 0, 12.0 * B.L.nb * n + 24.0 * n);
       EE_CUDA(launch_ce_finalize(B.pm, B.ps, B.pi, B.tgt, targets, B.L.nb, n, vc,
                                  exit_weights[i], B.lse, B.coef, ax ? ax->lse : nullptr,
                                  ax ? ax->loss_tok : nullptr, ax ? ax->argmax : nullptr,
-                                 ax ? ax->conf : nullptr, B.loss_part, B.L.nfin, st)); }
-      Prof p2_("a6_loss_reduce", st, 0, 0, 4.0 * B.L.nfin);
-      EE_CUDA(launch_loss_reduce(B.loss_part, B.L.nfin, vc, loss_out + i, B.status, i, st));
+                                 ax ? ax->conf : nullptr, B.loss_part,
+                                 dynw ? B.wsum_part : nullptr, B.L.nfin, st)); }
+      { Prof p2_("a6_loss_reduce", st, 0, 0, 4.0 * B.L.nfin);
+      EE_CUDA(launch_loss_reduce(B.loss_part, B.L.nfin, vc, dynw ? B.wsum_part : nullptr, B.wsum,
+                                 loss_out + i, B.status, i, st)); }
+      if (dynw) {
+        Prof p3_("a6_coef_scale", st, 0, 0, 8.0 * n);
+        EE_CUDA(launch_ce_coef_scale(B.coef, n, exit_weights[i], B.wsum, st));
+      }
     }
     if ((s = phase_vocab_backward(cfg, B, P, G, z, n, targets, accumulate, nrm ? B.dz : nullptr,
                                   st)) != EE_OK)
@@ -663,16 +680,23 @@ ee_status ee_vp_vocab_backward(const ee_head_config* cfg, const void* z_all, int
     return EE_OK;
   }
   const long long* vc = valid_count ? (const long long*)valid_count : B.vcount;
+  const bool dynw = cfg->token_weighting == EE_WEIGHT_CONFIDENCE;
   {
     Prof p_("vp_finalize", st, 0, 0, 28.0 * n_all);
     EE_CUDA(launch_vp_finalize((const long long*)key_global, sums_global, targets_all, n_all, vc,
                                exit_weight, B.lse, B.coef, aux ? aux->lse : nullptr,
                                aux ? aux->loss_tok : nullptr, aux ? aux->argmax : nullptr,
-                               aux ? aux->conf : nullptr, B.loss_part, B.L.nfin, st));
+                               aux ? aux->conf : nullptr, B.loss_part,
+                               dynw ? B.wsum_part : nullptr, B.L.nfin, st));
   }
   {
     Prof p_("a6_loss_reduce", st, 0, 0, 4.0 * B.L.nfin);
-    EE_CUDA(launch_loss_reduce(B.loss_part, B.L.nfin, vc, loss_out, B.status, exit_index, st));
+    EE_CUDA(launch_loss_reduce(B.loss_part, B.L.nfin, vc, dynw ? B.wsum_part : nullptr, B.wsum,
+                               loss_out, B.status, exit_index, st));
+  }
+  if (dynw) {
+    Prof p_("a6_coef_scale", st, 0, 0, 8.0 * n_all);
+    EE_CUDA(launch_ce_coef_scale(B.coef, n_all, exit_weight, B.wsum, st));
   }
   return phase_vocab_backward(cfg, B, *params, *grads, (const __nv_bfloat16*)z_all, n_all,
                               targets_all, accumulate, nrm ? dz_partial : nullptr, st);

@@ -82,7 +82,7 @@ static cudaError_t launch2(const CUtensorMap& a, const CUtensorMap& b0, const CU
   // GEMMs use the static schedule with a per-wave soft barrier.
   static const int dyn = getenv("EE_GEMM_DYN") ? atoi(getenv("EE_GEMM_DYN")) : 1;
   static const int wsync = getenv("EE_GEMM_WAVESYNC") ? atoi(getenv("EE_GEMM_WAVESYNC")) : 1;
-  const bool long_k = args.K >= 16384;
+  const bool long_k = args.K >= 16384 || wsync == 2;
   a2.tile_counter = (dyn && !(wsync && long_k)) ? tile_counter(st) : nullptr;
   a2.wave_counter = (wsync && long_k && a2.tile_counter == nullptr) ? tile_counter(st) : nullptr;
   kern<<<grid, GEMM_THREADS, G2_SMEM, st>>>(a, b0, b1, a2);

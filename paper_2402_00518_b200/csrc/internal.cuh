@@ -51,9 +51,14 @@ cudaError_t launch_ce_finalize(const float* pm, const float* ps, const int32_t* 
                                const float* tl, const int32_t* targets, int nb, long long n,
                                const long long* valid_count, float alpha, float* lse, float* coef,
                                float* aux_lse, float* aux_loss, int32_t* aux_argmax,
-                               float* aux_conf, float* loss_part, int nblocks, cudaStream_t s);
+                               float* aux_conf, float* loss_part, float* wsum_part, int nblocks,
+                               cudaStream_t s);
+// wsum_part != NULL: confidence weighting (L = sum w loss / sum w, written to wsum_out)
 cudaError_t launch_loss_reduce(const float* loss_part, int nparts, const long long* valid_count,
-                               float* loss_out, DevStatus* st, int exit_index, cudaStream_t s);
+                               const float* wsum_part, float* wsum_out, float* loss_out,
+                               DevStatus* st, int exit_index, cudaStream_t s);
+cudaError_t launch_ce_coef_scale(float* coef, long long n, float alpha, const float* wsum,
+                                 cudaStream_t s);
 constexpr int FINALIZE_THREADS = 256;
 
 // vocab-parallel softmax-CE (distributed statistics)
@@ -69,7 +74,7 @@ cudaError_t launch_vp_finalize(const long long* key_global, const float* sums,
                                const int32_t* targets, long long n, const long long* valid_count,
                                float alpha, float* lse, float* coef, float* aux_lse,
                                float* aux_loss, int32_t* aux_argmax, float* aux_conf,
-                               float* loss_part, int nblocks, cudaStream_t s);
+                               float* loss_part, float* wsum_part, int nblocks, cudaStream_t s);
 
 // optimizer / init
 cudaError_t launch_adam(float* theta, __nv_bfloat16* op_bf16, float* op_f32, const float* grad,

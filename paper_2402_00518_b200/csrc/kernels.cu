@@ -282,10 +282,11 @@ __global__ void ce_finalize_kernel(const float* __restrict__ pm, const float* __
                                    const long long* __restrict__ valid_count, float alpha,
                                    float* __restrict__ lse, float* __restrict__ coef,
                                    float* aux_lse, float* aux_loss, int32_t* aux_argmax,
-                                   float* aux_conf, float* __restrict__ loss_part) {
+                                   float* aux_conf, float* __restrict__ loss_part,
+                                   float* __restrict__ wsum_part) {
   __shared__ double red[33];
   const long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  double lossv = 0.0;
+  double lossv = 0.0, wsum = 0.0;
   if (row < n) {
     float m = -INFINITY;
     for (int j = 0; j < nb; ++j) m = fmaxf(m, pm[(long long)j * n + row]);
@@ -300,51 +301,86 @@ __global__ void ce_finalize_kernel(const float* __restrict__ pm, const float* __
     const int y = targets[row];
     const bool valid = y >= 0;
     const float lt = valid ? l - tl[row] : 0.f;
-    const long long W = *valid_count;
     lse[row] = l;
-    coef[row] = (valid && W > 0) ? alpha / (float)W : 0.f;
     if (aux_lse) aux_lse[row] = l;
     if (aux_loss) aux_loss[row] = lt;
     if (aux_argmax) aux_argmax[row] = am;
     if (aux_conf) aux_conf[row] = 1.0f / s;
-    lossv = (double)lt;
+    if (wsum_part) {  // confidence weights w_t = c_t = 1/s, detached
+      const float w = valid ? 1.0f / s : 0.f;
+      coef[row] = w;  // scaled by alpha / sum(w) in ce_coef_scale
+      lossv = (double)w * (double)lt;
+      wsum = (double)w;
+    } else {
+      const long long W = *valid_count;
+      coef[row] = (valid && W > 0) ? alpha / (float)W : 0.f;
+      lossv = (double)lt;
+    }
   }
   lossv = block_sum(lossv, red);
   if (threadIdx.x == 0) loss_part[blockIdx.x] = (float)lossv;
+  if (wsum_part) {
+    wsum = block_sum(wsum, red);
+    if (threadIdx.x == 0) wsum_part[blockIdx.x] = (float)wsum;
+  }
 }
 
 cudaError_t launch_ce_finalize(const float* pm, const float* ps, const int32_t* pi,
                                const float* tl, const int32_t* targets, int nb, long long n,
                                const long long* valid_count, float alpha, float* lse, float* coef,
                                float* aux_lse, float* aux_loss, int32_t* aux_argmax,
-                               float* aux_conf, float* loss_part, int nblocks, cudaStream_t s) {
+                               float* aux_conf, float* loss_part, float* wsum_part, int nblocks,
+                               cudaStream_t s) {
   if (nblocks == 0) return cudaSuccess;
   ce_finalize_kernel<<<nblocks, FINALIZE_THREADS, 0, s>>>(pm, ps, pi, tl, targets, nb, n,
                                                           valid_count, alpha, lse, coef, aux_lse,
                                                           aux_loss, aux_argmax, aux_conf,
-                                                          loss_part);
+                                                          loss_part, wsum_part);
   return cudaGetLastError();
 }
 
 // L_i = sum_t w_t loss_t / W (A4, A16); non-finite -> EE_ERR_DIVERGED.
 __global__ void loss_reduce_kernel(const float* __restrict__ part, int nparts,
-                                   const long long* __restrict__ valid_count, float* loss_out,
-                                   DevStatus* st, int exit_index) {
+                                   const long long* __restrict__ valid_count,
+                                   const float* __restrict__ wsum_part, float* wsum_out,
+                                   float* loss_out, DevStatus* st, int exit_index) {
   __shared__ double red[33];
-  double s = 0.0;
-  for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += (double)part[i];
+  double s = 0.0, ws = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
+    s += (double)part[i];
+    if (wsum_part) ws += (double)wsum_part[i];
+  }
   s = block_sum(s, red);
+  if (wsum_part) ws = block_sum(ws, red);
   if (threadIdx.x == 0) {
-    const long long W = *valid_count;
-    const float L = W > 0 ? (float)(s / (double)W) : 0.f;
+    const double W = wsum_part ? ws : (double)*valid_count;
+    const float L = W > 0 ? (float)(s / W) : 0.f;
     *loss_out = L;
+    if (wsum_out) *wsum_out = (float)W;
     if (!isfinite(L)) set_status(st, 7 /*EE_ERR_DIVERGED*/, exit_index);
   }
 }
 
 cudaError_t launch_loss_reduce(const float* loss_part, int nparts, const long long* valid_count,
-                               float* loss_out, DevStatus* st, int exit_index, cudaStream_t s) {
-  loss_reduce_kernel<<<1, 1024, 0, s>>>(loss_part, nparts, valid_count, loss_out, st, exit_index);
+                               const float* wsum_part, float* wsum_out, float* loss_out,
+                               DevStatus* st, int exit_index, cudaStream_t s) {
+  loss_reduce_kernel<<<1, 1024, 0, s>>>(loss_part, nparts, valid_count, wsum_part, wsum_out,
+                                        loss_out, st, exit_index);
+  return cudaGetLastError();
+}
+
+// coef_t = alpha * w_t / sum_t w_t  (confidence weighting; w_t stored in coef)
+__global__ void ce_coef_scale_kernel(float* coef, long long n, float alpha, const float* wsum) {
+  const long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n) return;
+  const float W = *wsum;
+  coef[row] = W > 0.f ? alpha * coef[row] / W : 0.f;
+}
+
+cudaError_t launch_ce_coef_scale(float* coef, long long n, float alpha, const float* wsum,
+                                 cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  ce_coef_scale_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(coef, n, alpha, wsum);
   return cudaGetLastError();
 }
 
@@ -421,10 +457,11 @@ __global__ void vp_finalize_kernel(const long long* __restrict__ key, const floa
                                    const long long* __restrict__ valid_count, float alpha,
                                    float* __restrict__ lse, float* __restrict__ coef,
                                    float* aux_lse, float* aux_loss, int32_t* aux_argmax,
-                                   float* aux_conf, float* __restrict__ loss_part) {
+                                   float* aux_conf, float* __restrict__ loss_part,
+                                   float* __restrict__ wsum_part) {
   __shared__ double red[33];
   const long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  double lossv = 0.0;
+  double lossv = 0.0, wsum = 0.0;
   if (row < n) {
     float m;
     int am;
@@ -434,29 +471,40 @@ __global__ void vp_finalize_kernel(const long long* __restrict__ key, const floa
     const int y = targets[row];
     const bool valid = y >= 0;
     const float lt = valid ? l - sums[2 * row + 1] : 0.f;
-    const long long W = *valid_count;
     lse[row] = l;
-    coef[row] = (valid && W > 0) ? alpha / (float)W : 0.f;
     if (aux_lse) aux_lse[row] = l;
     if (aux_loss) aux_loss[row] = lt;
     if (aux_argmax) aux_argmax[row] = am;
     if (aux_conf) aux_conf[row] = 1.0f / s;
-    lossv = (double)lt;
+    if (wsum_part) {
+      const float w = valid ? 1.0f / s : 0.f;
+      coef[row] = w;
+      lossv = (double)w * (double)lt;
+      wsum = (double)w;
+    } else {
+      const long long W = *valid_count;
+      coef[row] = (valid && W > 0) ? alpha / (float)W : 0.f;
+      lossv = (double)lt;
+    }
   }
   lossv = block_sum(lossv, red);
   if (threadIdx.x == 0) loss_part[blockIdx.x] = (float)lossv;
+  if (wsum_part) {
+    wsum = block_sum(wsum, red);
+    if (threadIdx.x == 0) wsum_part[blockIdx.x] = (float)wsum;
+  }
 }
 
 cudaError_t launch_vp_finalize(const long long* key_global, const float* sums,
                                const int32_t* targets, long long n, const long long* valid_count,
                                float alpha, float* lse, float* coef, float* aux_lse,
                                float* aux_loss, int32_t* aux_argmax, float* aux_conf,
-                               float* loss_part, int nblocks, cudaStream_t s) {
+                               float* loss_part, float* wsum_part, int nblocks, cudaStream_t s) {
   if (nblocks == 0) return cudaSuccess;
   vp_finalize_kernel<<<nblocks, FINALIZE_THREADS, 0, s>>>(key_global, sums, targets, n,
                                                           valid_count, alpha, lse, coef, aux_lse,
                                                           aux_loss, aux_argmax, aux_conf,
-                                                          loss_part);
+                                                          loss_part, wsum_part);
   return cudaGetLastError();
 }
 

@@ -43,7 +43,7 @@ def launches(path, out):
             continue
         ns = float(r["Metric Value"])
         k = short(r["Kernel Name"])
-        if k.startswith("gemm_kernel"):
+        if k.startswith(("gemm_kernel", "gemm2_kernel")):
             k = f"{k} [{MLP_GEMM_ORDER[gemm_idx % len(MLP_GEMM_ORDER)]}]"
             gemm_idx += 1
         ours = not k.startswith("at::") and "elementwise" not in k and "distribution" not in k
@@ -89,7 +89,7 @@ def full(path, out, traffic_out=None):
     for i, row in enumerate(rows[2:]):
         k = short(row[kcol])
         tag = ""
-        if k.startswith("gemm_kernel"):
+        if k.startswith(("gemm_kernel", "gemm2_kernel")):
             tag = MLP_GEMM_ORDER[gi % len(MLP_GEMM_ORDER)]
             gi += 1
 

@@ -24,13 +24,14 @@ TENSORS = ("g_a", "w_gate", "w_up", "w_down", "g_f", "w_out")
 
 
 def gpu_step(ee, cfg, hidden, targets, params, exit_weights, accumulate=False, grads=None,
-             eps=1e-5):
+             eps=1e-5, weighting="uniform"):
     """Run ee_tune_step on the GPU.  hidden: list of bf16 tensors (any device);
     params: list of dicts of fp32 tensors (matrices are cast to bf16 operands).
     Returns (loss[E] tensor, grads list of dicts (device fp32), aux list)."""
     E = len(hidden)
     n = targets.numel()
-    c = ee.make_config(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch, eps)
+    c = ee.make_config(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch, eps,
+                       token_weighting=weighting)
     hid = [h.cuda().contiguous() for h in hidden]
     tg = targets.cuda().to(torch.int32).contiguous()
     ops = [{k: (v.cuda().float().contiguous() if k.startswith("g_") else
@@ -49,11 +50,11 @@ def gpu_step(ee, cfg, hidden, targets, params, exit_weights, accumulate=False, g
     return loss, grads, aux, (code, idx)
 
 
-def oracle_exit(arch, params, hidden, targets, alpha, eps=1e-5):
+def oracle_exit(arch, params, hidden, targets, alpha, eps=1e-5, weighting="uniform"):
     """fp64 oracle on the same bytes (bf16/fp32 inputs widened exactly)."""
     p64 = {k: to_f64(v) for k, v in params.items()}
     return O.exit_loss_and_grads(arch, p64, to_f64(hidden), targets.cpu().numpy().astype(np.int64),
-                                 float(alpha), eps, keep_act=True)
+                                 float(alpha), eps, keep_act=True, weighting=weighting)
 
 
 def rel_fro(a, b):

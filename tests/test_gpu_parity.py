@@ -162,3 +162,36 @@ def test_device_errors(gpu_lib):
     with pytest.raises(ee.EEError):
         c = ee.make_config(100, 512, 0, 1, "norm")                  # h not a multiple of 64
         ee.ee_workspace_size(c, 10)
+
+
+@pytest.mark.parametrize("arch,h,V,F,n", [("mlp", 128, 1000, 384, 300), ("embedding", 192, 2056, 0, 77),
+                                          ("norm", 256, 4104, 0, 1000)])
+def test_confidence_token_weighting(gpu_lib, arch, h, V, F, n):
+    """Dynamic token-wise loss weights: w_t = c_t detached, sum-c
+    normalisation (A17); GPU vs the fp64 oracle's 'confidence' weighting."""
+    cfg = S.Cfg(name="small", hidden=h, vocab=V, ffn=F, arch=arch, tokens=n, layers=2,
+                after=[1, 2], init="random", seed=13)
+    hidden = S.hidden_states(cfg, n)
+    targets = S.targets(cfg, n)
+    params = S.head_params(cfg)
+    loss, grads, aux, st = gpu_step(gpu_lib, cfg, hidden, targets, params, [1.0, 0.5],
+                                    weighting="confidence")
+    assert st == (0, -1)
+    for i in range(2):
+        res = oracle_exit(arch, params[i], hidden[i], targets, [1.0, 0.5][i], weighting="confidence")
+        compare_exit(arch, res, loss[i].item(), grads[i], aux[i], targets, tag=f"conf[{i}]")
+
+
+def test_confidence_weighting_rejected_for_dp_shard(gpu_lib):
+    ee = gpu_lib
+    c = ee.make_config(128, 512, 0, 1, "norm", token_weighting="confidence")
+    ws = torch.zeros(ee.ee_workspace_size(c, 8), dtype=torch.uint8, device="cuda")
+    vc = torch.tensor([8], dtype=torch.int64, device="cuda")
+    p = [{"w_out": torch.zeros(512, 128, dtype=torch.bfloat16, device="cuda"),
+          "g_f": torch.ones(128, device="cuda")}]
+    g = [{"w_out": torch.zeros(512, 128, device="cuda"), "g_f": torch.zeros(128, device="cuda")}]
+    with pytest.raises(ee.EEError) as e:
+        ee.ee_tune_step(c, [torch.zeros(8, 128, dtype=torch.bfloat16, device="cuda")],
+                        torch.zeros(8, dtype=torch.int32, device="cuda"), [1.0], p, g,
+                        torch.zeros(1, device="cuda"), ws, valid_count=vc)
+    assert e.value.code == 11

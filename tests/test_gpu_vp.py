@@ -61,7 +61,7 @@ def _shards(V, P):
     return [(edges[r], edges[r + 1]) for r in range(P)]
 
 
-def run_vp(ee, cfg, P, hidden, targets, params, weights):
+def run_vp(ee, cfg, P, hidden, targets, params, weights, weighting="uniform"):
     from paper_2402_00518_b200.parallel import GpuPhases, vocab_parallel_step
     N, h, E = targets.numel(), cfg.hidden, cfg.exits
     nl = N // P
@@ -74,7 +74,8 @@ def run_vp(ee, cfg, P, hidden, targets, params, weights):
     def rank_fn(r):
         try:
             vb, ve = shards[r]
-            c = ee.make_config(h, cfg.vocab, cfg.ffn, E, cfg.arch, 1e-5, vb, ve)
+            c = ee.make_config(h, cfg.vocab, cfg.ffn, E, cfg.arch, 1e-5, vb, ve,
+                               token_weighting=weighting)
             ws = torch.zeros(ee.ee_workspace_size(c, N), dtype=torch.uint8, device="cuda")
             prm, grd = [], []
             for p in params:
@@ -157,3 +158,20 @@ def test_vocab_parallel_p1_equals_single_gpu_step(gpu_lib):
     assert out[0][0][0].item() == loss[0].item()
     for k, g in grads[0].items():
         assert torch.equal(out[0][1][0][k], g.cpu()), k
+
+
+def test_vocab_parallel_confidence_weighting(gpu_lib):
+    """Dynamic token weights under VP: every rank sees all tokens after the
+    stats all-reduce, so sum_t c_t is formed locally (no extra collective)."""
+    cfg = S.Cfg(name="small", hidden=128, vocab=1000, ffn=256, arch="mlp", tokens=256, layers=2,
+                after=[1], init="random", seed=23)
+    hidden = S.hidden_states(cfg, 256)
+    targets = S.targets(cfg, 256)
+    params = S.head_params(cfg)
+    out, shards = run_vp(gpu_lib, cfg, 4, hidden, targets, params, [1.0], weighting="confidence")
+    res = oracle_exit("mlp", params[0], hidden[0], targets, 1.0, weighting="confidence")
+    assert abs(out[0][0][0].item() - res.loss) / res.loss <= LOSS_RTOL
+    dw = torch.cat([out[r][1][0]["w_out"] for r in range(4)]).double().numpy()
+    assert rel_fro(dw, res.grads["w_out"]) <= GRAD_RTOL
+    for k in ("g_a", "w_gate", "w_up", "w_down", "g_f"):
+        assert rel_fro(out[0][1][0][k].double().numpy(), res.grads[k]) <= GRAD_RTOL, k

@@ -348,3 +348,56 @@ def test_bf16_widening_is_exact():
     t = torch.randn(1000).to(torch.bfloat16)
     bits = t.view(torch.int16).numpy().view(np.uint16)
     np.testing.assert_array_equal(O.bf16_bits_to_f64(bits), t.to(torch.float64).numpy())
+
+
+# --------------------------------------------------------------------------- A17 (NEXT #1)
+@pytest.mark.parametrize("arch", O.ARCHS)
+def test_confidence_weighting_detached_and_identity(arch):
+    """Dynamic token-wise weights: w_t = c_t = max
+    softmax prob, detached.  Pins: (i) explicit all-ones weights reproduce the
+    static loss and gradients bitwise; (ii) c_t is the max softmax probability
+    (scipy); (iii) the gradient equals central finite differences of
+    sum_t c_t loss_t(theta) / sum_t c_t with c held at its value at theta_0."""
+    rng = _rng(21)
+    h, V, F, N = 8, 16, 12, 6
+    p = _params(arch, h, V, F, rng)
+    x = rng.normal(size=(N, h))
+    y = np.array([3, -1, 15, 0, 7, 7])
+    alpha, eps = 0.9, 1e-5
+    r_u = O.exit_loss_and_grads(arch, p, x, y, alpha, eps)
+    r_1 = O.exit_loss_and_grads(arch, p, x, y, alpha, eps, weighting=np.ones(N))
+    assert r_1.loss == r_u.loss
+    for k in p:
+        assert np.array_equal(r_1.grads[k], r_u.grads[k]), k
+    r_c = O.exit_loss_and_grads(arch, p, x, y, alpha, eps, keep_act=True, weighting="confidence")
+    c = softmax(r_c.act["S"], axis=1).max(axis=1)
+    np.testing.assert_allclose(r_c.stats["conf"], c, rtol=1e-13)
+    valid = y != -1
+    L_expect = np.sum(c[valid] * r_c.stats["loss"][valid]) / np.sum(c[valid])
+    assert r_c.loss == pytest.approx(L_expect, rel=1e-13)
+
+    def f(pp):  # c held fixed (detached)
+        return alpha * O.exit_loss_and_grads(arch, pp, x, y, alpha, eps, weighting=c).loss
+
+    step = 1e-6
+    for name, val in p.items():
+        num = np.zeros_like(val)
+        it = np.nditer(val, flags=["multi_index"])
+        for _ in it:
+            idx = it.multi_index
+            q = {k: v.copy() for k, v in p.items()}
+            q[name][idx] += step
+            fp = f(q)
+            q[name][idx] -= 2 * step
+            num[idx] = (fp - f(q)) / (2 * step)
+        err = np.linalg.norm(num - r_c.grads[name]) / max(np.linalg.norm(r_c.grads[name]), 1e-30)
+        assert err <= 1e-6, (arch, name, err)
+
+
+def test_confidence_weighting_uniform_logits():
+    """W_out = 0: every c_t = 1/V, so confidence weighting = uniform: loss ln V."""
+    p = {"w_out": np.zeros((64, 8))}
+    x = _rng(0).normal(size=(5, 8))
+    r = O.exit_loss_and_grads("embedding", p, x, np.array([0, 1, 2, -1, 63]), 1.0, 0.0,
+                              weighting="confidence")
+    assert r.loss == pytest.approx(math.log(64), rel=1e-14)
