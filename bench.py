@@ -108,19 +108,12 @@ def step_flops(cfg, n):
     return per * n * cfg.exits
 
 
-def cpu_oracle_sample(cfg, n_sub, seed):
-    """Times the fp64 oracle (as it stands) on a bounded sample of the workload:
-    the first exit on n_sub tokens at full h, V, F.  Returns (seconds, cores)."""
+def cpu_oracle_inputs(cfg, n_sub, seed):
+    """Bounded sample of the workload for the fp64 oracle: the first exit's
+    parameters at full h, V, F and n_sub tokens (seeded eesynth draws)."""
     import numpy as np
-    import torch
     import eesynth as S
     from eesynth import to_f64
-    from oracle import ee_oracle as O
-    try:
-        from threadpoolctl import threadpool_info
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] or [os.cpu_count()])
-    except Exception:
-        cores = os.cpu_count()
     one = S.Cfg(name=cfg.name, hidden=cfg.hidden, vocab=cfg.vocab, ffn=cfg.ffn, arch=cfg.arch,
                 tokens=n_sub, layers=cfg.layers, after=cfg.after[:1], init=cfg.init, seed=cfg.seed)
     p = S.head_params(one, seed=seed)[0]
@@ -129,9 +122,26 @@ def cpu_oracle_sample(cfg, n_sub, seed):
         p64[k] = to_f64(p.pop(k))
     x = to_f64(S.hidden_states(one, n_sub, seed=seed)[0])
     y = S.targets(one, n_sub, seed=seed).numpy().astype(np.int64)
+    return p64, x, y
+
+
+def cpu_oracle_time(cfg, inputs):
+    """Times the fp64 oracle (as it stands) on one exit of the sample.
+    Returns (seconds, threads used)."""
+    from oracle import ee_oracle as O
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] or [os.cpu_count()])
+    except Exception:
+        cores = os.cpu_count()
+    p64, x, y = inputs
     t0 = time.perf_counter()
     O.exit_loss_and_grads(cfg.arch, p64, x, y, 1.0, 1e-5)
     return time.perf_counter() - t0, cores
+
+
+def cpu_oracle_sample(cfg, n_sub, seed):
+    return cpu_oracle_time(cfg, cpu_oracle_inputs(cfg, n_sub, seed))
 
 
 def run_reference(args, cfg, rank, world):
@@ -141,8 +151,9 @@ def run_reference(args, cfg, rank, world):
     n_sub = args.cpu_tokens
     times = []
     cores = None
+    inputs = cpu_oracle_inputs(cfg, n_sub, seed=cfg.seed)
     for i in range(args.warmup + args.steps):
-        t, cores = cpu_oracle_sample(cfg, n_sub, seed=cfg.seed)
+        t, cores = cpu_oracle_time(cfg, inputs)
         if i >= args.warmup:
             times.append(t)
     t_step = statistics.mean(times) * cfg.exits       # all exits of the step
