@@ -80,7 +80,8 @@ ee_status check_cfg(const ee_head_config* c) {
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t wsum_part, wsum;
+  size_t wsum_part, wsum, zT, uT, dyT;
+  long long ldT;  // leading dimension of the transposed [h x n] copies (n rounded up to 8)
   size_t status, vcount, loss_part, lse, coef, tgt, pm, ps, pi, z, ds, dz, dgp, ry, u, rx, ab,
       mact, y, dy, total;
   int nb, nparts, nfin;
@@ -110,6 +111,9 @@ Layout make_layout(const ee_head_config* c, long long n) {
   L.ps = take(4 * (size_t)L.nb * n);
   L.pi = take(4 * (size_t)L.nb * n);
   L.ds = take(2 * (size_t)n * Vl);
+  L.ldT = (n + 7) / 8 * 8;
+  L.zT = take(2 * (size_t)h * L.ldT);
+  L.uT = L.dyT = 0;
   L.z = L.dz = L.dgp = L.ry = L.u = L.rx = L.ab = L.mact = L.y = L.dy = 0;
   if (c->arch != EE_ARCH_EMBEDDING) {
     L.z = take(2 * (size_t)n * h);
@@ -124,6 +128,8 @@ Layout make_layout(const ee_head_config* c, long long n) {
     L.mact = take(2 * (size_t)n * F);
     L.y = take(4 * (size_t)n * h);
     L.dy = take(2 * (size_t)n * h);
+    L.uT = take(2 * (size_t)h * L.ldT);
+    L.dyT = take(2 * (size_t)h * L.ldT);
   }
   L.total = o;
   return L;
@@ -209,6 +215,7 @@ GemmArgs base_args(int M, int N, int K) {
   a.N = N;
   a.K = K;
   a.m_split = M;
+  a.n_split = N;
   a.group_m = 16;
   return a;
 }
@@ -281,6 +288,7 @@ struct Bufs {
   __nv_bfloat16 *ab, *mact;
   float* y;
   __nv_bfloat16* dy;
+  __nv_bfloat16 *zT, *uT, *dyT;  // K-major copies for the weight-gradient GEMMs
   // vocab-parallel merge state
   float* m_loc;
   Layout L;
@@ -305,6 +313,7 @@ Bufs make_bufs(const ee_head_config* cfg, long long n, void* workspace) {
   B.wsum = (float*)(ws + L.wsum);
   B.ds = (__nv_bfloat16*)(ws + L.ds);
   B.m_loc = B.coef;  // VP: m_loc is dead before coef is written (vp_finalize)
+  B.zT = (__nv_bfloat16*)(ws + L.zT);
   if (nrm) {
     B.z = (__nv_bfloat16*)(ws + L.z);
     B.dz = (float*)(ws + L.dz);
@@ -318,6 +327,8 @@ Bufs make_bufs(const ee_head_config* cfg, long long n, void* workspace) {
     B.mact = (__nv_bfloat16*)(ws + L.mact);
     B.y = (float*)(ws + L.y);
     B.dy = (__nv_bfloat16*)(ws + L.dy);
+    B.uT = (__nv_bfloat16*)(ws + L.uT);
+    B.dyT = (__nv_bfloat16*)(ws + L.dyT);
   }
   return B;
 }
@@ -420,14 +431,17 @@ ee_status phase_vocab_backward(const ee_head_config* cfg, const Bufs& B, const e
     Prof p_("a8_dz", st, 2.0 * n * Vl * h, 2.0 * n * Vl * h, 0);
     EE_CUDA(gemm_run(EPI_F32, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
   }
-  {  // a9: both operands MN-major, K = tokens
-    GemmArgs a = base_args(Vl, h, (int)n);
+  {  // a9: dW_out^T = z^T dS with z^T K-major (transposed copy), dS MN-major; stored transposed
+    { Prof p_("transpose_z", st, 0, 0, 4.0 * n * h);
+    EE_CUDA(launch_transpose_bf16(z, B.zT, n, h, B.L.ldT, st)); }
+    GemmArgs a = base_args(h, Vl, (int)n);
     a.out0 = (float*)G.w_out;
     a.ldo = h;
+    a.n_split = Vl;
     a.accumulate = accumulate;
-    Mat A{B.ds, n, Vl, Vl}, Bm{z, n, h, h};
+    Mat A{B.zT, h, n, B.L.ldT}, Bm{B.ds, n, Vl, Vl};
     Prof p_("a9_dw_out", st, 2.0 * n * Vl * h, 2.0 * n * Vl * h, 0);
-    EE_CUDA(gemm_run(EPI_F32, false, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
+    EE_CUDA(gemm_run(EPI_F32T, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
   }
   return EE_OK;
 }
@@ -448,15 +462,17 @@ ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee
   { Prof p_("reduce_cols", st, 0, 0, 4.0 * nparts * h);
   EE_CUDA(launch_reduce_cols(B.dgp, nparts, h, (float*)G.g_f, accumulate, st)); }
   if (!mlp) return EE_OK;
-  // a11: dW_down = dy^T M
+  // a11: dW_down = dy^T M  (A = dy^T K-major copy, B = M MN-major)
   {
+    { Prof p_("transpose_dy", st, 0, 0, 4.0 * n * h);
+    EE_CUDA(launch_transpose_bf16(B.dy, B.dyT, n, h, B.L.ldT, st)); }
     GemmArgs a = base_args(h, F, (int)n);
     a.out0 = (float*)G.w_down;
     a.ldo = F;
     a.accumulate = accumulate;
-    Mat A{B.dy, n, h, h}, Bm{B.mact, n, F, F};
+    Mat A{B.dyT, h, n, B.L.ldT}, Bm{B.mact, n, F, F};
     Prof p_("a11_dw_down", st, 2.0 * n * F * h, 2.0 * n * F * h, 0);
-    EE_CUDA(gemm_run(EPI_F32, false, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
+    EE_CUDA(gemm_run(EPI_F32, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
   }
   // a11: dM = dy W_down; dA = dM B silu'(A), dB = dM silu(A), in place over [A|B]
   {
@@ -468,17 +484,20 @@ ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee
     Prof p_("a11_dm_swiglu_bwd", st, 2.0 * n * F * h, 2.0 * n * F * h, 0);
     EE_CUDA(gemm_run(EPI_SWIGLU_BWD, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
   }
-  // a12: [dW_gate; dW_up] = [dA|dB]^T u  (rows split at F over two outputs)
+  // a12: [dW_gate; dW_up]^T = u^T [dA|dB]  (A = u^T K-major copy, B = [dA|dB]
+  // MN-major), stored transposed; output columns split at F over the two grads
   {
-    GemmArgs a = base_args(2 * F, h, (int)n);
+    { Prof p_("transpose_u", st, 0, 0, 4.0 * n * h);
+    EE_CUDA(launch_transpose_bf16(B.u, B.uT, n, h, B.L.ldT, st)); }
+    GemmArgs a = base_args(h, 2 * F, (int)n);
     a.out0 = (float*)G.w_gate;
     a.out1 = (float*)G.w_up;
-    a.m_split = F;
+    a.n_split = F;
     a.ldo = h;
     a.accumulate = accumulate;
-    Mat A{B.ab, n, 2LL * F, 2LL * F}, Bm{B.u, n, h, h};
+    Mat A{B.uT, h, n, B.L.ldT}, Bm{B.ab, n, 2LL * F, 2LL * F};
     Prof p_("a12_dw_gateup", st, 4.0 * n * F * h, 4.0 * n * F * h, 0);
-    EE_CUDA(gemm_run(EPI_F32, false, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
+    EE_CUDA(gemm_run(EPI_F32T, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
   }
   // a12: du = dA W_gate + dB W_up  (K concatenation over the two weights) -> B.dz
   {

@@ -40,6 +40,7 @@ enum EpiKind : int {
   EPI_SWIGLU_BWD = 3,  // acc = dM; dA = dM*B*silu'(A), dB = dM*silu(A) in place over A, B
   EPI_CE_STATS = 4,    // per-row (max, sum exp, argmax) of the tile + target logit
   EPI_CE_DS = 5,       // dS = coef * (exp(S - lse) - onehot(y)) -> bf16
+  EPI_F32T = 6,        // out^T: out[n][m] = acc (or +=), columns n >= n_split go to out1
 };
 
 enum BMode : int {
@@ -62,6 +63,7 @@ struct GemmArgs {
   float* out1;
   long long ldo;
   int m_split;
+  int n_split;  // EPI_F32T: output columns n >= n_split go to out1 (row n - n_split)
   int accumulate;
   const __nv_bfloat16* resid;
   long long ld_resid;
@@ -145,6 +147,31 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
               }
             }
             *reinterpret_cast<float4*>(orow + gn) = o;
+          }
+        }
+      }
+    }
+  } else if constexpr (EPI == EPI_F32T) {
+    // Transposed store: the tile is D' = A'B'^T computed with the operands
+    // swapped so that A' is K-major (the fast UMMA path); the caller's output
+    // is D'^T.  Thread `row` (m) writes out[n][m]: for each n the 32 threads of
+    // a warp store 32 consecutive floats (one 128-byte line).
+#pragma unroll 1
+    for (int c = 0; c < GEMM_BN / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tb + c * 32, v);
+      tmem_ld_wait();
+      const int gn0 = nb * GEMM_BN + c * 32;
+      if (row_ok && gn0 < args.N) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int gn = gn0 + j;
+          if (gn < args.N) {
+            float* o = (gn < args.n_split)
+                           ? args.out0 + (long long)gn * args.ldo + gm
+                           : args.out1 + (long long)(gn - args.n_split) * args.ldo + gm;
+            const float val = u2f(v[j]);
+            *o = args.accumulate ? *o + val : val;
           }
         }
       }

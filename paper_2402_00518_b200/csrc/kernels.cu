@@ -508,6 +508,46 @@ cudaError_t launch_vp_finalize(const long long* key_global, const float* sums,
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- transpose
+// dst[C x R] = src[R x C]^T (bf16), 64 x 64 tiles through shared memory:
+// 128-byte coalesced reads and writes.  Gives the weight-gradient GEMMs a
+// K-major copy of their token-major activation operand (u, z, dy), so their
+// A operand takes the K-major UMMA path.
+__global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ src,
+                                      __nv_bfloat16* __restrict__ dst, long long R, int C,
+                                      long long ldd) {
+  __shared__ __nv_bfloat16 tile[64][64 + 2];
+  const long long r0 = (long long)blockIdx.y * 64;
+  const int c0 = blockIdx.x * 64;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 256 threads: 32 x 8
+  for (int i = ty; i < 64; i += 8) {
+    const long long r = r0 + i;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int c = c0 + tx * 2 + k;
+      tile[i][tx * 2 + k] = (r < R && c < C) ? src[r * C + c] : __float2bfloat16_rn(0.f);
+    }
+  }
+  __syncthreads();
+  for (int i = ty; i < 64; i += 8) {
+    const int c = c0 + i;
+    if (c >= C) continue;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const long long r = r0 + tx * 2 + k;
+      if (r < R) dst[(long long)c * ldd + r] = tile[tx * 2 + k][i];
+    }
+  }
+}
+
+cudaError_t launch_transpose_bf16(const __nv_bfloat16* src, __nv_bfloat16* dst, long long R, int C,
+                                  long long ldd, cudaStream_t s) {
+  if (R == 0 || C == 0) return cudaSuccess;
+  dim3 grid((C + 63) / 64, (unsigned)((R + 63) / 64));
+  transpose_bf16_kernel<<<grid, 256, 0, s>>>(src, dst, R, C, ldd);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- optimizer
 static inline unsigned ew_blocks(long long n4) {
   long long b = (n4 + 255) / 256;
