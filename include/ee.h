@@ -218,6 +218,18 @@ ee_status ee_vp_exit_backward(const ee_head_config* cfg, const void* hidden, int
                               ee_head_tensors* grads, int32_t accumulate, void* workspace,
                               size_t ws_bytes, void* stream);
 
+/* Early-exit inference statistics (§3 "Inference"): for
+ * each exit i and token t, the exit's greedy next token argmax_out[i][t]
+ * (lowest index on ties) and its confidence conf_out[i][t] = max softmax
+ * probability; first_exit[t] (may be NULL) = the lowest exit index whose
+ * confidence reaches `threshold`, or -1 (threshold 1 disables early exits,
+ * P:385).  hidden[i]: device bf16 [n_tokens x h]; outputs device [n_tokens].
+ * Same kernels as the tuning step's forward (a1-a6); no loss, no gradients. */
+ee_status ee_exit_infer(const ee_head_config* cfg, const void* const* hidden, int64_t n_tokens,
+                        const ee_head_tensors* params, float threshold, int32_t* const* argmax_out,
+                        float* const* conf_out, int32_t* first_exit, void* workspace,
+                        size_t ws_bytes, void* stream);
+
 /* Number of valid targets (!= -1) -> device int64 out[0]; flags ids outside
  * [-1, V) in the workspace status word.  Used to form the global W under
  * data parallelism (the caller all-reduces out). */

@@ -259,6 +259,28 @@ def tune_step(arch: str, params_list, hidden_list, targets, exit_weights, eps: f
     return np.array(losses), grads, stats
 
 
+def exit_infer(arch: str, params_list, hidden_list, threshold: float, eps: float):
+    """Confidence-based early exit at inference (§3 "Inference"):
+    per exit the greedy token (argmax) and confidence (max softmax prob); a
+    token exits at the first exit whose confidence reaches the threshold
+    (threshold 1 disables early exits).  Returns (argmax [E,N],
+    conf [E,N], first_exit [N], -1 = no early exit)."""
+    am, cf = [], []
+    for p, x in zip(params_list, hidden_list):
+        S = exit_forward(arch, p, x, eps)["S"]
+        st = lm_loss_stats(S, np.full(S.shape[0], IGNORE_INDEX))
+        am.append(st["argmax"])
+        cf.append(st["conf"])
+    am, cf = np.array(am), np.array(cf)
+    first = np.full(cf.shape[1], -1, dtype=np.int64)
+    for t in range(cf.shape[1]):
+        for i in range(cf.shape[0]):
+            if cf[i, t] >= threshold:
+                first[t] = i
+                break
+    return am, cf, first
+
+
 # ----------------------------------------------------------------------------
 # optimizer (P:264: state for exits only; P:374-375: Adam constants)
 # ----------------------------------------------------------------------------

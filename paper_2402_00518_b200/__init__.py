@@ -31,7 +31,7 @@ EXPORTED = ("ee_workspace_size", "ee_init_heads", "ee_tune_step", "ee_count_vali
             "ee_adam_update", "ee_sgd_update", "ee_get_status", "ee_lr_at", "ee_last_error",
             "ee_version", "ee_test_gemm", "ee_profile_start", "ee_profile_stop",
             "ee_profile_record", "ee_launch_count", "ee_vp_exit_forward", "ee_vp_vocab_stats",
-            "ee_vp_rescale", "ee_vp_vocab_backward", "ee_vp_exit_backward")
+            "ee_vp_rescale", "ee_vp_vocab_backward", "ee_vp_exit_backward", "ee_exit_infer")
 
 
 class EEError(RuntimeError):
@@ -99,6 +99,8 @@ def load(path: str = LIB_PATH):
         "ee_vp_vocab_backward": (I32, [CFG, P, I64, P, P, P, F32, P, HT, HT, I32, P, P,
                                        ctypes.POINTER(ee_step_aux), I32, P, SZ, P]),
         "ee_vp_exit_backward": (I32, [CFG, P, I64, I64, HT, P, HT, I32, P, SZ, P]),
+        "ee_exit_infer": (I32, [CFG, ctypes.POINTER(P), I64, HT, F32, ctypes.POINTER(P),
+                                ctypes.POINTER(P), P, P, SZ, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -181,6 +183,21 @@ def ee_tune_step(cfg, hidden, targets, exit_weights, params, grads, loss_out, wo
                              heads(grads), int(bool(accumulate)), _ptr(loss_out), ax,
                              _ptr(valid_count), _ptr(workspace), workspace.numel(),
                              _stream(stream)))
+
+
+def ee_exit_infer(cfg, hidden, params, threshold, argmax_out, conf_out, workspace,
+                  first_exit=None, stream=None):
+    """Greedy token + confidence per exit and the first exit reaching
+    `threshold` (P:381-386)."""
+    load()
+    E = cfg.num_exits
+    n = hidden[0].shape[0] if E else 0
+    hid = (ctypes.c_void_p * E)(*[h.data_ptr() for h in hidden])
+    am = (ctypes.c_void_p * E)(*[a.data_ptr() for a in argmax_out])
+    cf = (ctypes.c_void_p * E)(*[c.data_ptr() for c in conf_out])
+    _check(_lib.ee_exit_infer(ctypes.byref(cfg), hid, n, heads(params), float(threshold), am, cf,
+                              _ptr(first_exit), _ptr(workspace), workspace.numel(),
+                              _stream(stream)))
 
 
 def ee_count_valid(targets, vocab, out, workspace, stream=None):
@@ -385,6 +402,17 @@ class ExitHeads:
         ee_tune_step(self.cfg, hidden, targets, w, self.operand, self.grads, self.loss,
                      self.workspace, accumulate=accumulate, aux=aux, valid_count=valid_count)
         return self.loss
+
+    def infer(self, hidden, threshold):
+        """Greedy token, confidence per exit and the first exit reaching
+        `threshold` (P:381-386).  Returns (argmax [E] list, conf [E] list, first)."""
+        n = hidden[0].shape[0]
+        dev = self.loss.device
+        am = [torch.empty(n, dtype=torch.int32, device=dev) for _ in range(self.spec.num_exits)]
+        cf = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(self.spec.num_exits)]
+        first = torch.empty(n, dtype=torch.int32, device=dev)
+        ee_exit_infer(self.cfg, hidden, self.operand, threshold, am, cf, self.workspace, first)
+        return am, cf, first
 
     def adam(self, lr, beta1=0.9, beta2=0.95, eps=1e-5, weight_decay=0.0, grad_scale=1.0):
         self.step_count += 1

@@ -610,6 +610,56 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
   return EE_OK;
 }
 
+// ---------------------------------------------------------------- early-exit inference
+// Confidence-based exit decision: per exit, the greedy token and
+// the max softmax probability; first_exit[t] = lowest exit with c >= tau.
+ee_status ee_exit_infer(const ee_head_config* cfg, const void* const* hidden, int64_t n_tokens,
+                        const ee_head_tensors* params, float threshold, int32_t* const* argmax_out,
+                        float* const* conf_out, int32_t* first_exit, void* workspace,
+                        size_t ws_bytes, void* stream) {
+  ee_status s = check_cfg(cfg);
+  if (s != EE_OK) return s;
+  if (cfg->vocab_begin != 0 || cfg->vocab_end != cfg->vocab)
+    return fail(EE_ERR_ARG, "ee_exit_infer needs the full vocabulary");
+  const int E = cfg->num_exits;
+  if (!hidden || !params || !argmax_out || !conf_out || n_tokens < 0)
+    return fail(EE_ERR_ARG, "NULL argument or n_tokens < 0");
+  if (E > 64) return fail(EE_ERR_SHAPE, "at most 64 exits");
+  for (int i = 0; i < E; ++i) {
+    if ((s = check_arch_tensors(cfg, params[i], "params", i)) != EE_OK) return s;
+    if (n_tokens > 0 && (!hidden[i] || !argmax_out[i] || !conf_out[i]))
+      return fail(EE_ERR_ARG, "exit %d: NULL hidden/output", i);
+  }
+  const long long n = n_tokens;
+  const Bufs B = make_bufs(cfg, n, workspace);
+  if (!workspace || !aligned16(workspace) || ws_bytes < B.L.total)
+    return fail(EE_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", B.L.total, ws_bytes);
+  if ((s = check_device()) != EE_OK) return s;
+  if (n == 0) return EE_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  // no targets at inference: every row "ignored" (the int32 -1 pattern)
+  int32_t* no_targets = (int32_t*)B.tgt;  // tgt (fp32 [n]) is free: no target logits needed
+  EE_CUDA(cudaMemsetAsync(no_targets, 0xFF, sizeof(int32_t) * n, st));
+  EE_CUDA(cudaMemsetAsync(B.vcount, 0, sizeof(long long), st));
+  for (int i = 0; i < E; ++i) {
+    const __nv_bfloat16* x = (const __nv_bfloat16*)hidden[i];
+    const __nv_bfloat16* z = nullptr;
+    if ((s = phase_exit_forward(cfg, B, params[i], x, n, nullptr, &z, st)) != EE_OK) return s;
+    if ((s = phase_vocab_stats(cfg, B, params[i], z, n, no_targets, st)) != EE_OK) return s;
+    Prof p_("infer_finalize", st, 0, 0, 12.0 * B.L.nb * n + 8.0 * n);
+    EE_CUDA(launch_ce_finalize(B.pm, B.ps, B.pi, nullptr, no_targets, B.L.nb, n, B.vcount, 0.f,
+                               B.lse, B.coef, nullptr, nullptr, argmax_out[i], conf_out[i],
+                               B.loss_part, nullptr, B.L.nfin, st));
+  }
+  if (first_exit) {
+    float* confs[64];
+    for (int i = 0; i < E; ++i) confs[i] = conf_out[i];
+    Prof p_("infer_first_exit", st, 0, 0, 4.0 * E * n + 4.0 * n);
+    EE_CUDA(launch_first_exit((const float* const*)confs, E, n, threshold, first_exit, st));
+  }
+  return EE_OK;
+}
+
 // ---------------------------------------------------------------- vocab parallel
 // One exit, one rank of P.  The caller runs the collectives between phases
 // (include/ee.h, "vocab-parallel phases").  cfg->num_exits is ignored (the

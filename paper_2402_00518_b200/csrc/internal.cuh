@@ -79,6 +79,9 @@ cudaError_t launch_vp_finalize(const long long* key_global, const float* sums,
 cudaError_t launch_transpose_bf16(const __nv_bfloat16* src, __nv_bfloat16* dst, long long R, int C,
                                   long long ldd, cudaStream_t s);
 
+cudaError_t launch_first_exit(const float* const* conf, int E, long long n, float tau,
+                              int32_t* out, cudaStream_t s);
+
 // optimizer / init
 cudaError_t launch_adam(float* theta, __nv_bfloat16* op_bf16, float* op_f32, const float* grad,
                         float* m, float* v, long long n, float lr, float b1, float b2, float eps,

@@ -300,7 +300,7 @@ __global__ void ce_finalize_kernel(const float* __restrict__ pm, const float* __
     const float l = m + logf(s);
     const int y = targets[row];
     const bool valid = y >= 0;
-    const float lt = valid ? l - tl[row] : 0.f;
+    const float lt = valid ? l - tl[row] : 0.f;  // tl never read for ignored rows
     lse[row] = l;
     if (aux_lse) aux_lse[row] = l;
     if (aux_loss) aux_loss[row] = lt;
@@ -505,6 +505,32 @@ cudaError_t launch_vp_finalize(const long long* key_global, const float* sums,
                                                           valid_count, alpha, lse, coef, aux_lse,
                                                           aux_loss, aux_argmax, aux_conf,
                                                           loss_part, wsum_part);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- early exit (inference)
+// first_exit[t] = lowest exit index i with conf_i[t] >= tau, else -1 (
+// tau = 1 disables early exits).
+struct ConfPtrs {
+  const float* p[64];
+};
+__global__ void first_exit_kernel(ConfPtrs c, int E, long long n, float tau, int32_t* out) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  int f = -1;
+  for (int i = 0; i < E; ++i)
+    if (c.p[i][t] >= tau) {
+      f = i;
+      break;
+    }
+  out[t] = f;
+}
+
+cudaError_t launch_first_exit(const float* const* conf, int E, long long n, float tau,
+                              int32_t* out, cudaStream_t s) {
+  ConfPtrs c;
+  for (int i = 0; i < E && i < 64; ++i) c.p[i] = conf[i];
+  first_exit_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c, E, n, tau, out);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,48 @@
+"""Confidence-based early-exit decision (NEXT #4) on the GPU vs the
+fp64 oracle: greedy token (argmax, gap rule A9), confidence, first exit."""
+
+import numpy as np
+import pytest
+import torch
+
+import eesynth as S
+from eesynth import to_f64
+from harness import check_argmax
+from oracle import ee_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("arch,h,V,F,n", [("mlp", 256, 4104, 512, 300), ("norm", 128, 1000, 0, 8),
+                                          ("embedding", 192, 2056, 0, 77)])
+def test_exit_infer_matches_oracle(gpu_lib, arch, h, V, F, n):
+    ee = gpu_lib
+    cfg = S.Cfg(name="small", hidden=h, vocab=V, ffn=F, arch=arch, tokens=n, layers=3,
+                after=[1, 2, 3], init="random", seed=31)
+    hidden = S.hidden_states(cfg, n)
+    params = S.head_params(cfg)
+    c = ee.make_config(h, V, F, 3, arch)
+    ops = [{k: (v.cuda().float() if k.startswith("g_") else v.cuda().to(torch.bfloat16))
+            for k, v in p.items()} for p in params]
+    am = [torch.zeros(n, dtype=torch.int32, device="cuda") for _ in range(3)]
+    cf = [torch.zeros(n, device="cuda") for _ in range(3)]
+    first = torch.zeros(n, dtype=torch.int32, device="cuda")
+    ws = torch.zeros(ee.ee_workspace_size(c, n), dtype=torch.uint8, device="cuda")
+    p64 = [{k: to_f64(v) for k, v in p.items()} for p in params]
+    _, cf_o, _ = O.exit_infer(arch, p64, [to_f64(x) for x in hidden], 1.0, 1e-5)
+    tau = float(np.median(cf_o))
+    ee.ee_exit_infer(c, [x.cuda() for x in hidden], ops, tau, am, cf, ws, first_exit=first)
+    torch.cuda.synchronize()
+    am_o, cf_o, first_o = O.exit_infer(arch, p64, [to_f64(x) for x in hidden], tau, 1e-5)
+    for i in range(3):
+        S_i = O.exit_forward(arch, p64[i], to_f64(hidden[i]), 1e-5)["S"]
+        check_argmax(am[i].cpu().numpy(), S_i)
+        assert np.max(np.abs(cf[i].cpu().numpy() - cf_o[i])) <= 2e-2
+    fg = first.cpu().numpy()
+    cfg_np = np.array([c_.cpu().numpy() for c_ in cf])
+    for t in range(n):   # exact except where an exit's confidence sits within 1e-3 of tau
+        near = np.any(np.abs(cf_o[:, t] - tau) < 1e-3)
+        if not near:
+            assert fg[t] == first_o[t], t
+        expect_gpu = next((i for i in range(3) if cfg_np[i, t] >= tau), -1)
+        assert fg[t] == expect_gpu

@@ -401,3 +401,28 @@ def test_confidence_weighting_uniform_logits():
     r = O.exit_loss_and_grads("embedding", p, x, np.array([0, 1, 2, -1, 63]), 1.0, 0.0,
                               weighting="confidence")
     assert r.loss == pytest.approx(math.log(64), rel=1e-14)
+
+
+def test_exit_infer_thresholds():
+    """Confidence-based early exit: threshold 1 disables exits
+    (P:385); threshold 0 exits every token at the first exit; with W_out = 0 the
+    confidence is exactly 1/V (uniform)."""
+    rng = _rng(30)
+    h, V, F, N = 8, 20, 12, 9
+    ps = [_params("mlp", h, V, F, rng) for _ in range(3)]
+    xs = [rng.normal(size=(N, h)) for _ in range(3)]
+    am, cf, first = O.exit_infer("mlp", ps, xs, 1.0, 1e-5)
+    assert np.all(first == -1) and np.all(cf < 1.0)
+    _, _, first0 = O.exit_infer("mlp", ps, xs, 0.0, 1e-5)
+    assert np.all(first0 == 0)
+    tau = float(np.median(cf[1]))
+    _, _, f = O.exit_infer("mlp", ps, xs, tau, 1e-5)
+    for t in range(N):
+        expect = next((i for i in range(3) if cf[i, t] >= tau), -1)
+        assert f[t] == expect
+    p0 = dict(ps[0], w_out=np.zeros((V, h)))
+    _, c0, _ = O.exit_infer("mlp", [p0], [xs[0]], 0.5, 1e-5)
+    np.testing.assert_allclose(c0, 1.0 / V, rtol=1e-14)
+    for i in range(3):
+        S = O.exit_forward("mlp", ps[i], xs[i], 1e-5)["S"]
+        np.testing.assert_array_equal(am[i], np.argmax(S, axis=1))
