@@ -182,6 +182,9 @@ def workload_config(cfg, world, args):
             "global_batch": (cfg.tokens // 2048) * (1 if vp else world), "seq_len": 2048,
             "tokens_per_gpu": tok, "exits": cfg.exits,
             "parallelism": f"vp{world}" if vp else f"dp{world}",
+            "collectives": ("none" if world == 1 else
+                            "gloo, ranks sharing one GPU (test mode)" if getattr(args, "shared_gpu", False)
+                            else "NCCL (torch.distributed)"),
             "l2": "inputs larger than L2 (hidden states + exit weights per step >> 126 MB)",
             "optimizer": "Adam (P:374-375), included in the step"}
 
@@ -221,10 +224,17 @@ def main():
 
     import paper_2402_00518_b200 as ee
     ee.load()
+    ndev = torch.cuda.device_count()
+    shared_gpu = world > ndev            # test mode: several ranks on one GPU (gloo)
+    args.shared_gpu = shared_gpu
+    local = local % ndev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     multi = world > 1
     vp = args.parallel == "vp"
     dp = world > 1 and not vp
@@ -424,6 +434,7 @@ def main():
         "gpu_launches": launches,
         "clocks": clocks,
         "status": code,
+        "loss_last_step": [round(float(v), 6) for v in heads.loss.tolist()],
         "kernels": kernels,
     }
     if world == 1 and not args.no_cpu_baseline and not args.quick:
