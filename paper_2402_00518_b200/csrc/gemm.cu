@@ -175,11 +175,10 @@ cudaError_t gemm_run(int epi, bool a_kmajor, bool b_kmajor, const Mat& A, const 
   const int bn = (b_mode == B_PAIR) ? GEMM_BN / 2 : GEMM_BN;
   args.n_blocks = (args.N + bn - 1) / bn;
   args.k_blocks = (args.K + GEMM_BK - 1) / GEMM_BK;
-  // Rasterisation group (M-blocks per group).  Long-K GEMMs (K >= 16384: the
-  // weight gradients over tokens, dz over V, du over 2F, down over F) want
-  // small groups, the K = h GEMMs 8 (measured DRAM traffic per launch,
-  // profiles/r01_dyn_group_sweep.log).
-  static const int g_long = env_int("EE_GEMM_GROUP_LONGK", 4);
+  // Rasterisation group (pair M-blocks per group): 8 for both schedules
+  // (profiles/r01_dyn_group_sweep.log, r01_longk2_group.log; with the dynamic
+  // schedule long-K GEMMs preferred 4, with the wave barrier 8).
+  static const int g_long = env_int("EE_GEMM_GROUP_LONGK", 8);
   static const int g_short = env_int("EE_GEMM_GROUP_SHORTK", 8);
   if (group > 0)
     args.group_m = group;
