@@ -186,7 +186,9 @@ def workload_config(cfg, world, args):
                             "gloo, ranks sharing one GPU (test mode)" if getattr(args, "shared_gpu", False)
                             else "NCCL (torch.distributed)"),
             "l2": "inputs larger than L2 (hidden states + exit weights per step >> 126 MB)",
-            "optimizer": "Adam (P:374-375), included in the step"}
+            "optimizer": "Adam (P:374-375), included in the step",
+            "update_schedule": ("per exit, shared gradient buffers (P:261)"
+                                if getattr(args, "per_exit", False) else "all exits, then Adam")}
 
 
 def main():
@@ -201,6 +203,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quick", action="store_true", help="ncu/profiling run: no extras")
+    ap.add_argument("--grad-buffers", type=int, default=-1,
+                    help="k < exits: exits share k gradient buffers and are updated one by one "
+                         "(P:261); default 2 when the config has more than 4 exits")
     ap.add_argument("--parallel", default="dp", choices=["dp", "vp"],
                     help="N>1: dp = data parallel over tokens (weak scaling); vp = W_out "
                          "vocab-parallel with the distributed softmax-CE (strong scaling)")
@@ -247,8 +252,14 @@ def main():
     vb, ve = vocab_shard(cfg.vocab, world, rank) if vp else (0, cfg.vocab)
 
     # ---- parameter store, Copy init from a synthetic backbone
+    gbuf = args.grad_buffers if args.grad_buffers >= 0 else (2 if E > 4 else 0)
+    if vp:
+        gbuf = 0
     heads = ee.ExitHeads(ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch,
-                                     vocab_begin=vb, vocab_end=ve), n_all, device=dev)
+                                     vocab_begin=vb, vocab_end=ve), n_all, device=dev,
+                         grad_buffers=gbuf if gbuf > 0 else None)
+    per_exit = heads.grad_buffers < E
+    args.per_exit = per_exit
     bb = S.backbone(cfg, device=dev)
     src = []
     for k in cfg.after:
@@ -288,6 +299,18 @@ def main():
 
     def step(it, hid=hidden, tg=targets):
         lr = ee.ee_lr_at(min(it + 1, total_iters), total_iters)
+        if per_exit:       # exit-by-exit update with shared gradient buffers
+            W = None
+            if dp:
+                ee.ee_count_valid(tg, cfg.vocab, vc, heads.workspace)
+                dist.all_reduce(vc)
+                W = vc
+            red = (lambda i: [dist.all_reduce(t, async_op=True) for t in heads.grads[i].values()]) \
+                if dp else None
+            heads.step_per_exit(hid, tg, lr, valid_count=W, reduce_grads=red)
+            if dp:
+                dist.all_reduce(heads.loss)
+            return
         if vp:
             ee.ee_count_valid(tg, cfg.vocab, vc, heads.workspace)   # W over all tokens
             vocab_parallel_step(phases, comm, cfg.arch, hid, tg, heads.operand, heads.grads,

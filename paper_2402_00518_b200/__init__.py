@@ -361,7 +361,13 @@ class ExitHeads:
     step workspace.  All compute goes through the C-ABI above.
     """
 
-    def __init__(self, spec: HeadSpec, max_tokens: int, device="cuda", adam=True):
+    def __init__(self, spec: HeadSpec, max_tokens: int, device="cuda", adam=True,
+                 grad_buffers: int | None = None):
+        """grad_buffers = k < num_exits: exits share k fp32 gradient buffers
+        (exit i uses buffer i % k), for the per-exit update schedule
+        (step_per_exit): "forward, backward, and parameter update for each
+        early-exit layer, without any dependency between early exits".
+        At the 70B shape with 8 exits this saves 27 GB."""
         load()
         self.spec = spec
         ve = spec.vocab if spec.vocab_end is None else spec.vocab_end
@@ -381,7 +387,13 @@ class ExitHeads:
         self.operand = [{k: (m[k] if k.startswith("g_") else
                              torch.zeros(shapes[k], dtype=torch.bfloat16, device=dev))
                          for k in shapes} for m in self.master]
-        self.grads = alloc(f32)
+        k = E if grad_buffers is None else max(1, min(int(grad_buffers), E))
+        pool = [{n: torch.zeros(sh, dtype=torch.float32, device=dev) for n, sh in shapes.items()}
+                for _ in range(k)]
+        self.grad_buffers = k
+        self.grads = [pool[i % k] for i in range(E)]
+        self.exit_cfg = make_config(spec.hidden, spec.vocab, spec.ffn, 1, spec.arch,
+                                    spec.norm_eps, spec.vocab_begin, ve, spec.token_weighting)
         self.m = alloc(f32) if adam else None
         self.v = alloc(f32) if adam else None
         self.step_count = 0
@@ -415,9 +427,47 @@ class ExitHeads:
         return am, cf, first
 
     def adam(self, lr, beta1=0.9, beta2=0.95, eps=1e-5, weight_decay=0.0, grad_scale=1.0):
+        if self.grad_buffers < self.spec.num_exits:
+            raise RuntimeError("shared gradient buffers: use step_per_exit()")
         self.step_count += 1
         ee_adam_update(self.cfg, self.master, self.operand, self.grads, self.m, self.v, lr,
                        self.step_count, beta1, beta2, eps, weight_decay, grad_scale)
+
+    def adam_exit(self, i, lr, step, beta1=0.9, beta2=0.95, eps=1e-5, weight_decay=0.0,
+                  grad_scale=1.0):
+        ee_adam_update(self.exit_cfg, self.master[i:i + 1], self.operand[i:i + 1],
+                       self.grads[i:i + 1], self.m[i:i + 1], self.v[i:i + 1], lr, step, beta1,
+                       beta2, eps, weight_decay, grad_scale)
+
+    def step_per_exit(self, hidden, targets, lr, exit_weights=None, valid_count=None,
+                      reduce_grads=None):
+        """One step exit by exit: tune exit i, (optionally) reduce its gradients,
+        Adam on exit i.  With k gradient buffers, exit i's update is
+        deferred until exit i + k - 1 has been launched, so a reduction issued
+        by reduce_grads(i) (returning async handles) overlaps the next exits'
+        compute.  Returns the per-exit losses."""
+        E = self.spec.num_exits
+        k = self.grad_buffers
+        w = exit_weights if exit_weights is not None else [1.0] * E
+        self.step_count += 1
+        pending = {}
+
+        def finish(j):
+            for h in pending.pop(j, []):
+                h.wait()
+            self.adam_exit(j, lr, self.step_count)
+
+        for i in range(E):
+            if i - k >= 0:
+                finish(i - k)
+            ee_tune_step(self.exit_cfg, hidden[i:i + 1], targets, w[i:i + 1],
+                         self.operand[i:i + 1], self.grads[i:i + 1], self.loss[i:i + 1],
+                         self.workspace, valid_count=valid_count)
+            if reduce_grads is not None:
+                pending[i] = reduce_grads(i) or []
+        for j in range(max(0, E - k), E):
+            finish(j)
+        return self.loss
 
     def status(self):
         return ee_get_status(self.workspace)

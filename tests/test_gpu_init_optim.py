@@ -167,3 +167,29 @@ def test_sgd_step_decreases_loss(gpu_lib):
     l1 = heads.step(hidden, targets).clone()
     torch.cuda.synchronize()
     assert torch.all(l1 < l0), (l0, l1)
+
+
+def test_per_exit_update_with_shared_grad_buffer_equals_full_step(gpu_lib):
+    """Exit-by-exit tune + Adam with one shared gradient buffer ("forward,
+    backward, and parameter update for each early-exit layer, without any
+    dependency between early exits") gives bitwise the same parameters as
+    tuning all exits and then updating them all."""
+    cfg = S.Cfg(name="small", hidden=128, vocab=1000, ffn=256, arch="mlp", tokens=300, layers=3,
+                after=[1, 2, 3], init="random", seed=41)
+    spec = gpu_lib.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, 3, cfg.arch)
+    a = gpu_lib.ExitHeads(spec, 300)
+    b = gpu_lib.ExitHeads(spec, 300, grad_buffers=1)
+    a.init("random", seed=5)
+    b.init("random", seed=5)
+    hidden = [h.cuda() for h in S.hidden_states(cfg, 300)]
+    targets = S.targets(cfg, 300).cuda()
+    for it in range(2):
+        la = a.step(hidden, targets).clone()
+        a.adam(1e-3)
+        lb = b.step_per_exit(hidden, targets, 1e-3).clone()
+        torch.cuda.synchronize()
+        assert torch.equal(la, lb)
+    for i in range(3):
+        for k in a.master[i]:
+            assert torch.equal(a.master[i][k], b.master[i][k]), (i, k)
+            assert torch.equal(a.m[i][k], b.m[i][k]), (i, k)
