@@ -64,13 +64,14 @@ static int* tile_counter(cudaStream_t st) {
   return c;
 }
 
-template <int EPI, bool A_MN, bool B_MN>
+template <int EPI, bool A_MN, bool B_MN, int NB2 = 1>
 static cudaError_t launch2(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1,
                            const GemmArgs& args, cudaStream_t st) {
-  auto kern = gemm2_kernel<EPI, A_MN, B_MN>;
+  auto kern = gemm2_kernel<EPI, A_MN, B_MN, NB2>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G2_SMEM);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         G2Cfg<NB2>::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -85,7 +86,7 @@ static cudaError_t launch2(const CUtensorMap& a, const CUtensorMap& b0, const CU
   const bool long_k = args.K >= 16384 || wsync == 2;
   a2.tile_counter = (dyn && !(wsync && long_k)) ? tile_counter(st) : nullptr;
   a2.wave_counter = (wsync && long_k && a2.tile_counter == nullptr) ? tile_counter(st) : nullptr;
-  kern<<<grid, GEMM_THREADS, G2_SMEM, st>>>(a, b0, b1, a2);
+  kern<<<grid, GEMM_THREADS, G2Cfg<NB2>::SMEM, st>>>(a, b0, b1, a2);
   return cudaGetLastError();
 }
 
@@ -172,7 +173,13 @@ cudaError_t gemm_run(int epi, bool a_kmajor, bool b_kmajor, const Mat& A, const 
   args.b_ksplit = b_ksplit;
   const int bm = cta_pair ? 2 * GEMM_BM : GEMM_BM;
   args.m_blocks = (args.M + bm - 1) / bm;
-  const int bn = (b_mode == B_PAIR) ? GEMM_BN / 2 : GEMM_BN;
+  // 256 x 512 pair tiles for the long-K GEMMs (EE_GEMM_WIDE=1): 25% fewer
+  // operand bytes per FLOP on paper, but measured 7% slower per step at the
+  // power cap (profiles/r01_wide_ab.log), so off by default
+  static const int wide_env = env_int("EE_GEMM_WIDE", 0);  // measured slower (profiles/r01_wide_ab.log)
+  const bool wide = cta_pair && wide_env && b_mode != B_PAIR && args.K >= 16384 &&
+                    (epi == EPI_F32 || epi == EPI_F32T || epi == EPI_RESID);
+  const int bn = (b_mode == B_PAIR) ? GEMM_BN / 2 : (wide ? 2 * GEMM_BN : GEMM_BN);
   args.n_blocks = (args.N + bn - 1) / bn;
   args.k_blocks = (args.K + GEMM_BK - 1) / GEMM_BK;
   // Rasterisation group (pair M-blocks per group): 8 for both schedules
@@ -196,6 +203,15 @@ cudaError_t gemm_run(int epi, bool a_kmajor, bool b_kmajor, const Mat& A, const 
   if (epi == E && a_mn == AM && b_mn == BM)                                  \
     return cta_pair ? launch2<E, AM, BM>(ta, tb0, tb1, args, st)             \
                     : launch<E, AM, BM>(ta, tb0, tb1, args, st);
+#define EE_GEMM_WIDE(E, AM, BM) \
+  if (wide && epi == E && a_mn == AM && b_mn == BM) return launch2<E, AM, BM, 2>(ta, tb0, tb1, args, st);
+  EE_GEMM_WIDE(EPI_F32, false, false)
+  EE_GEMM_WIDE(EPI_F32, false, true)
+  EE_GEMM_WIDE(EPI_F32, true, false)
+  EE_GEMM_WIDE(EPI_F32, true, true)
+  EE_GEMM_WIDE(EPI_F32T, false, true)
+  EE_GEMM_WIDE(EPI_RESID, false, false)
+#undef EE_GEMM_WIDE
   // the (epilogue, A major, B major) combinations the step uses, plus the
   // plain fp32 GEMM in all four majors (exported for the parity tests)
   EE_GEMM_CASE(EPI_F32, false, false)

@@ -510,19 +510,33 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 //   - tfull[a]  in both CTAs (multicast commit); tempty[a] in the leader,
 //               256 arrivals (128 epilogue threads of each CTA, remote via mapa).
 // ============================================================================
-constexpr int G2_STAGES = 6;
-constexpr int G2_A_STAGE = 128 * GEMM_BK * 2;  // 16 KB (this CTA's 128 rows of A)
-constexpr int G2_B_STAGE = 128 * GEMM_BK * 2;  // 16 KB (this CTA's half of B)
+// NB2 = 256-column accumulator halves per pair tile: 1 -> 256 x 256 tiles with a
+// double-buffered accumulator (2 x 256 TMEM columns); 2 -> 256 x 512 tiles, one
+// accumulator filling all 512 columns (no epilogue overlap, but 25% fewer
+// operand bytes per FLOP from L2 and DRAM: used for the long-K GEMMs).
+template <int NB2>
+struct G2Cfg {
+  static constexpr int STAGES = NB2 == 1 ? 6 : 4;
+  static constexpr int A_STAGE = 128 * GEMM_BK * 2;        // 16 KB: this CTA's 128 rows of A
+  static constexpr int B_STAGE = NB2 * 128 * GEMM_BK * 2;  // this CTA's NB2 x 128 rows of B
+  static constexpr int NACC = NB2 == 1 ? 2 : 1;            // accumulator buffers in TMEM
+  static constexpr int TILE_N = NB2 * GEMM_BN;
+  static constexpr int SMEM = STAGES * (A_STAGE + B_STAGE) + 1024 + 256;
+};
 constexpr int G2_SQ = 4;  // depth of the tile-index ring (dynamic schedule)
-constexpr int G2_SMEM = G2_STAGES * (G2_A_STAGE + G2_B_STAGE) + 1024 + 256;
+constexpr int G2_SMEM = G2Cfg<1>::SMEM;
 
-template <int EPI, bool A_MN, bool B_MN>
+template <int EPI, bool A_MN, bool B_MN, int NB2 = 1>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
                  const __grid_constant__ CUtensorMap tmB1, const GemmArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
+  using C = G2Cfg<NB2>;
+  constexpr int G2_STAGES = C::STAGES;
+  constexpr int G2_A_STAGE = C::A_STAGE;
+  constexpr int G2_B_STAGE = C::B_STAGE;
   uint8_t* sA = smem;
   uint8_t* sB = smem + G2_STAGES * G2_A_STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + G2_STAGES * G2_B_STAGE);
@@ -671,12 +685,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
               mB = &tmB1;
               kk = k0 - args.b_ksplit;
             }
-            const int n0 = nb * GEMM_BN + (int)rank * 128;
-            if constexpr (!B_MN) {
-              ldb(b, mB, fb, kk, n0);
-            } else {
-              ldb(b, mB, fb, n0, kk);
-              ldb(b + 8192, mB, fb, n0 + 64, kk);
+#pragma unroll
+            for (int hh = 0; hh < NB2; ++hh) {
+              // half hh of the pair tile: columns [n0h, n0h + 256), CTA r holds rows
+              // n0h + 128 r .. +128 in smem rows [128 hh, 128 hh + 128)
+              const int n0 = nb * C::TILE_N + hh * GEMM_BN + (int)rank * 128;
+              uint8_t* bh = b + hh * 16384;
+              if constexpr (!B_MN) {
+                ldb(bh, mB, fb, kk, n0);
+              } else {
+                ldb(bh, mB, fb, n0, kk);
+                ldb(bh + 8192, mB, fb, n0 + 64, kk);
+              }
             }
           }
           if (leader) mbar_arrive_expect_tx(&full[s], 2 * (G2_A_STAGE + G2_B_STAGE));
@@ -709,9 +729,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           for (int k = 0; k < GEMM_BK / 16; ++k) {
             const uint64_t ad = A_MN ? make_sdesc(a_addr + k * 2048, 8192, 1024)
                                      : make_sdesc(a_addr + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? make_sdesc(b_addr + k * 2048, 8192, 1024)
-                                     : make_sdesc(b_addr + k * 32, 16, 1024);
-            tc_mma_f16_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+#pragma unroll
+            for (int hh = 0; hh < NB2; ++hh) {
+              const uint32_t bh = b_addr + hh * 16384;
+              const uint64_t bd = B_MN ? make_sdesc(bh + k * 2048, 8192, 1024)
+                                       : make_sdesc(bh + k * 32, 16, 1024);
+              tc_mma_f16_2sm(d_tmem + hh * GEMM_BN, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            }
           }
           tc_commit_2sm(&empty[s], 0x3);
           if (++s == G2_STAGES) {
@@ -720,7 +744,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           }
         }
         tc_commit_2sm(&tfull[acc], 0x3);
-        if (++acc == 2) {
+        if (++acc == C::NACC) {
           acc = 0;
           acc_ph ^= 1;
         }
@@ -747,10 +771,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       tc_fence_after();
       const uint32_t tb = tmem_base + acc * GEMM_BN + (static_cast<uint32_t>(ew * 32) << 16);
       if (args.trace && threadIdx.x == 128 && rank == 0) args.trace[tile] = trace_stamp();
-      epilogue_tile<EPI>(args, tb, mb * 256 + (int)rank * 128 + row, nb);
+#pragma unroll 1
+      for (int hh = 0; hh < NB2; ++hh)
+        epilogue_tile<EPI>(args, tb + hh * GEMM_BN, mb * 256 + (int)rank * 128 + row,
+                           nb * NB2 + hh);
       tc_fence_before();
       mbar_arrive_cluster(acc ? te1 : te0);
-      if (++acc == 2) {
+      if (++acc == C::NACC) {
         acc = 0;
         acc_ph ^= 1;
       }
