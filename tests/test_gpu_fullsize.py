@@ -1,0 +1,115 @@
+"""Full-size parity in the launch configuration bench.py times (BASELINE.json
+configs at their full token counts, one exit = the same GEMM launches the
+bench repeats per exit).  The oracle cannot run the full batch (~1e14 fp64
+FLOPs), so these check (a) sampled rows the oracle computes one by one (lse,
+loss_t, confidence, argmax), and (b) properties that hold at any size:
+loss = mean of the per-token losses, softmax-CE gradient rows sum to zero
+(P4), bitwise rerun determinism, read-only inputs, and -- for the Embedding
+config, where z = x -- the uniform-logit closed form of dW_out (P3) on every
+element."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import eesynth as S
+from eesynth import to_f64
+from harness import check_argmax
+from oracle import ee_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _one_exit(name):
+    cfg = S.get_cfg(name)
+    cfg.after = cfg.after[:1]
+    cfg.exits = 1
+    return cfg
+
+
+def _run(ee, cfg, hidden, targets, params, aux=True):
+    n = targets.numel()
+    c = ee.make_config(cfg.hidden, cfg.vocab, cfg.ffn, 1, cfg.arch)
+    ops = [{k: (v.float().contiguous() if k.startswith("g_") else v.to(torch.bfloat16).contiguous())
+            for k, v in params[0].items()}]
+    grads = [{k: torch.empty(v.shape, device="cuda") for k, v in params[0].items()}]
+    ax = [{"lse": torch.zeros(n, device="cuda"), "loss_tok": torch.zeros(n, device="cuda"),
+           "argmax": torch.zeros(n, dtype=torch.int32, device="cuda"),
+           "conf": torch.zeros(n, device="cuda")}]
+    ws = torch.zeros(ee.ee_workspace_size(c, n), dtype=torch.uint8, device="cuda")
+    loss = torch.zeros(1, device="cuda")
+    ee.ee_tune_step(c, hidden, targets, [1.0], ops, grads, loss, ws, aux=ax)
+    torch.cuda.synchronize()
+    return loss, grads, ax, ee.ee_get_status(ws), ops
+
+
+@pytest.mark.parametrize("name", ["13b", "70b"])
+def test_full_size_sampled_rows_and_invariants(gpu_lib, name):
+    ee = gpu_lib
+    cfg = _one_exit(name)
+    n = cfg.tokens
+    hidden = [h.contiguous() for h in S.hidden_states(cfg, n, device="cuda")]
+    targets = S.targets(cfg, n, device="cuda")
+    params = S.head_params(cfg, device="cuda")
+    h0 = hidden[0].clone()
+    loss, grads, aux, st, ops = _run(ee, cfg, hidden, targets, params)
+    assert st == (0, -1)
+    assert torch.equal(hidden[0], h0)                                   # frozen input
+    # (a) sampled rows vs the oracle, row by row
+    tg = targets.cpu().numpy()
+    rows = np.unique(np.concatenate([[0, 1, n // 2, n - 1], np.nonzero(tg == -1)[0][:2],
+                                     np.random.default_rng(0).integers(0, n, 10)]))
+    p64 = {k: to_f64(v) for k, v in ops[0].items()}
+    act = O.exit_forward(cfg.arch, p64, to_f64(hidden[0][torch.as_tensor(rows, device="cuda")]),
+                         1e-5)
+    st_o = O.lm_loss_stats(act["S"], tg[rows])
+    lse = aux[0]["lse"].cpu().numpy()[rows]
+    assert np.max(np.abs(lse - st_o["lse"])) <= 5e-2
+    assert np.max(np.abs(aux[0]["conf"].cpu().numpy()[rows] - st_o["conf"])) <= 2e-2
+    lt = aux[0]["loss_tok"].cpu().numpy()[rows]
+    assert np.max(np.abs(lt - st_o["loss"])) <= 5e-2
+    assert np.all(lt[tg[rows] == -1] == 0.0)
+    check_argmax(aux[0]["argmax"].cpu().numpy()[rows], act["S"])
+    # (b) loss = mean of per-token losses over valid tokens
+    valid = tg != -1
+    lt_all = aux[0]["loss_tok"].double().cpu().numpy()
+    assert abs(loss.item() - lt_all[valid].mean()) <= 1e-5 * abs(loss.item())
+    # P4: sum_v dW_out[v, :] = 0 (dS rows sum to zero), against the no-cancellation scale
+    dw = grads[0]["w_out"].double()
+    colsum = dw.sum(dim=0).norm().item()
+    scale = dw.abs().sum(dim=0).norm().item()
+    assert colsum <= 1e-2 * scale, (colsum, scale)
+    for k, g in grads[0].items():
+        assert torch.isfinite(g).all(), k
+    # bitwise rerun determinism (no float atomics anywhere)
+    loss2, grads2, _, _, _ = _run(ee, cfg, hidden, targets, params)
+    assert torch.equal(loss, loss2)
+    for k in grads[0]:
+        assert torch.equal(grads[0][k], grads2[0][k]), k
+
+
+def test_full_size_embedding_uniform_logits_closed_form(gpu_lib):
+    """7B config (Embedding exit, z = x), W_out = 0: loss = ln V, conf = 1/V and
+    dW_out[v] = (1/W) sum_t w_t (1/V - 1[y_t = v]) x_t on every element (P3)."""
+    ee = gpu_lib
+    cfg = _one_exit("7b")
+    n, V = cfg.tokens, cfg.vocab
+    hidden = [h.contiguous() for h in S.hidden_states(cfg, n, device="cuda")]
+    targets = S.targets(cfg, n, device="cuda")
+    params = S.head_params(cfg, device="cuda")
+    params[0]["w_out"].zero_()
+    loss, grads, aux, st, _ = _run(ee, cfg, hidden, targets, params)
+    assert st == (0, -1)
+    assert abs(loss.item() - math.log(V)) <= 1e-5 * math.log(V)
+    assert torch.allclose(aux[0]["conf"], torch.full_like(aux[0]["conf"], 1.0 / V), rtol=1e-5)
+    x = to_f64(hidden[0])
+    y = targets.cpu().numpy()
+    w = (y != -1).astype(np.float64)
+    W = w.sum()
+    expect = np.tile((w @ x) / (V * W), (V, 1))
+    np.subtract.at(expect, y[w > 0], x[w > 0] / W)
+    got = grads[0]["w_out"].double().cpu().numpy()
+    rel = np.linalg.norm(got - expect) / np.linalg.norm(expect)
+    assert rel <= 2e-2, rel
