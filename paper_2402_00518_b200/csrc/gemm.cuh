@@ -126,27 +126,39 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
       const int gn0 = nb * GEMM_BN + c * 32;
       if (row_ok && gn0 < args.N) {
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
+        for (int j = 0; j < 32; j += 8) {
           const int gn = gn0 + j;
-          if (gn < args.N) {
-            float4 o = make_float4(u2f(v[j]), u2f(v[j + 1]), u2f(v[j + 2]), u2f(v[j + 3]));
-            if constexpr (EPI == EPI_RESID) {
-              const uint2 r = *reinterpret_cast<const uint2*>(
-                  args.resid + (long long)gm * args.ld_resid + gn);
-              o.x += bf16lo(r.x);
-              o.y += bf16hi(r.x);
-              o.z += bf16lo(r.y);
-              o.w += bf16hi(r.y);
-            } else {
-              if (args.accumulate) {
-                const float4 p = *reinterpret_cast<const float4*>(orow + gn);
-                o.x += p.x;
-                o.y += p.y;
-                o.z += p.z;
-                o.w += p.w;
+          if (gn >= args.N) continue;
+          float o[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) o[q] = u2f(v[j + q]);
+          const bool full8 = gn + 8 <= args.N;
+          if constexpr (EPI == EPI_RESID) {
+            const __nv_bfloat16* rp = args.resid + (long long)gm * args.ld_resid + gn;
+            const uint2 r0 = *reinterpret_cast<const uint2*>(rp);
+            o[0] += bf16lo(r0.x); o[1] += bf16hi(r0.x); o[2] += bf16lo(r0.y); o[3] += bf16hi(r0.y);
+            if (full8) {
+              const uint2 r1 = *reinterpret_cast<const uint2*>(rp + 4);
+              o[4] += bf16lo(r1.x); o[5] += bf16hi(r1.x); o[6] += bf16lo(r1.y); o[7] += bf16hi(r1.y);
+            }
+          } else {
+            if (args.accumulate) {
+              const float4 p0 = *reinterpret_cast<const float4*>(orow + gn);
+              o[0] += p0.x; o[1] += p0.y; o[2] += p0.z; o[3] += p0.w;
+              if (full8) {
+                const float4 p1 = *reinterpret_cast<const float4*>(orow + gn + 4);
+                o[4] += p1.x; o[5] += p1.y; o[6] += p1.z; o[7] += p1.w;
               }
             }
-            *reinterpret_cast<float4*>(orow + gn) = o;
+          }
+          if (full8 && aligned32(orow + gn)) {
+            uint32_t w[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) w[q] = __float_as_uint(o[q]);
+            st_global_v8(orow + gn, w);
+          } else {
+            *reinterpret_cast<float4*>(orow + gn) = make_float4(o[0], o[1], o[2], o[3]);
+            if (full8) *reinterpret_cast<float4*>(orow + gn + 4) = make_float4(o[4], o[5], o[6], o[7]);
           }
         }
       }
@@ -189,13 +201,10 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
         __nv_bfloat16* arow = args.ab + (long long)gm * args.ld_ab;
         __nv_bfloat16* mrow = args.mact + (long long)gm * args.ld_m;
 #pragma unroll
-        for (int j = 0; j < 32; j += 8) {
-          uint4 pa, pb, pm;
-          uint32_t* qa = reinterpret_cast<uint32_t*>(&pa);
-          uint32_t* qb = reinterpret_cast<uint32_t*>(&pb);
-          uint32_t* qm = reinterpret_cast<uint32_t*>(&pm);
+        for (int j = 0; j < 32; j += 16) {
+          uint32_t qa[8], qb[8], qm[8];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < 8; ++q) {
             const float a0 = u2f(g[j + 2 * q]), a1 = u2f(g[j + 2 * q + 1]);
             const float b0 = u2f(u[j + 2 * q]), b1 = u2f(u[j + 2 * q + 1]);
             const float s0 = a0 / (1.0f + __expf(-a0)), s1 = a1 / (1.0f + __expf(-a1));
@@ -203,9 +212,21 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
             qb[q] = pack_bf16(b0, b1);
             qm[q] = pack_bf16(s0 * b0, s1 * b1);
           }
-          *reinterpret_cast<uint4*>(arow + f0 + j) = pa;
-          *reinterpret_cast<uint4*>(arow + F + f0 + j) = pb;
-          *reinterpret_cast<uint4*>(mrow + f0 + j) = pm;
+          __nv_bfloat16* pa = arow + f0 + j;
+          __nv_bfloat16* pb = arow + F + f0 + j;
+          __nv_bfloat16* pm = mrow + f0 + j;
+          if (aligned32(pa) && aligned32(pb) && aligned32(pm)) {
+            st_global_v8(pa, qa);
+            st_global_v8(pb, qb);
+            st_global_v8(pm, qm);
+          } else {
+            *reinterpret_cast<uint4*>(pa) = make_uint4(qa[0], qa[1], qa[2], qa[3]);
+            *reinterpret_cast<uint4*>(pa + 8) = make_uint4(qa[4], qa[5], qa[6], qa[7]);
+            *reinterpret_cast<uint4*>(pb) = make_uint4(qb[0], qb[1], qb[2], qb[3]);
+            *reinterpret_cast<uint4*>(pb + 8) = make_uint4(qb[4], qb[5], qb[6], qb[7]);
+            *reinterpret_cast<uint4*>(pm) = make_uint4(qm[0], qm[1], qm[2], qm[3]);
+            *reinterpret_cast<uint4*>(pm + 8) = make_uint4(qm[4], qm[5], qm[6], qm[7]);
+          }
         }
       }
     }
@@ -220,16 +241,26 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
       if (row_ok && f0 < args.N) {
         __nv_bfloat16* arow = args.ab + (long long)gm * args.ld_ab;
 #pragma unroll
-        for (int j = 0; j < 32; j += 8) {
-          uint4 ra = *reinterpret_cast<const uint4*>(arow + f0 + j);
-          uint4 rb = *reinterpret_cast<const uint4*>(arow + F + f0 + j);
-          const uint32_t* qa = reinterpret_cast<const uint32_t*>(&ra);
-          const uint32_t* qb = reinterpret_cast<const uint32_t*>(&rb);
-          uint4 wa, wb;
-          uint32_t* pa = reinterpret_cast<uint32_t*>(&wa);
-          uint32_t* pb = reinterpret_cast<uint32_t*>(&wb);
+        for (int j = 0; j < 32; j += 16) {
+          __nv_bfloat16* pa_ = arow + f0 + j;
+          __nv_bfloat16* pb_ = arow + F + f0 + j;
+          const bool v8 = aligned32(pa_) && aligned32(pb_);
+          uint32_t qa[8], qb[8], wa[8], wb[8];
+          if (v8) {
+            ld_global_v8(pa_, qa);
+            ld_global_v8(pb_, qb);
+          } else {
+            const uint4 a0 = *reinterpret_cast<const uint4*>(pa_);
+            const uint4 a1 = *reinterpret_cast<const uint4*>(pa_ + 8);
+            const uint4 b0 = *reinterpret_cast<const uint4*>(pb_);
+            const uint4 b1 = *reinterpret_cast<const uint4*>(pb_ + 8);
+            qa[0] = a0.x; qa[1] = a0.y; qa[2] = a0.z; qa[3] = a0.w;
+            qa[4] = a1.x; qa[5] = a1.y; qa[6] = a1.z; qa[7] = a1.w;
+            qb[0] = b0.x; qb[1] = b0.y; qb[2] = b0.z; qb[3] = b0.w;
+            qb[4] = b1.x; qb[5] = b1.y; qb[6] = b1.z; qb[7] = b1.w;
+          }
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < 8; ++q) {
             float da[2], db[2];
 #pragma unroll
             for (int h2 = 0; h2 < 2; ++h2) {
@@ -240,11 +271,18 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
               db[h2] = dm * a * sg;
               da[h2] = dm * b * sg * (1.0f + a * (1.0f - sg));
             }
-            pa[q] = pack_bf16(da[0], da[1]);
-            pb[q] = pack_bf16(db[0], db[1]);
+            wa[q] = pack_bf16(da[0], da[1]);
+            wb[q] = pack_bf16(db[0], db[1]);
           }
-          *reinterpret_cast<uint4*>(arow + f0 + j) = wa;
-          *reinterpret_cast<uint4*>(arow + F + f0 + j) = wb;
+          if (v8) {
+            st_global_v8(pa_, wa);
+            st_global_v8(pb_, wb);
+          } else {
+            *reinterpret_cast<uint4*>(pa_) = make_uint4(wa[0], wa[1], wa[2], wa[3]);
+            *reinterpret_cast<uint4*>(pa_ + 8) = make_uint4(wa[4], wa[5], wa[6], wa[7]);
+            *reinterpret_cast<uint4*>(pb_) = make_uint4(wb[0], wb[1], wb[2], wb[3]);
+            *reinterpret_cast<uint4*>(pb_ + 8) = make_uint4(wb[4], wb[5], wb[6], wb[7]);
+          }
         }
       }
     }
@@ -306,19 +344,24 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
       const int gn0 = nb * GEMM_BN + c * 32;
       if (row_ok && gn0 < args.N) {
 #pragma unroll
-        for (int j = 0; j < 32; j += 8) {
-          if (gn0 + j < args.N) {
-            uint4 w;
-            uint32_t* pw = reinterpret_cast<uint32_t*>(&w);
+        for (int j = 0; j < 32; j += 16) {
+          if (gn0 + j >= args.N) continue;
+          uint32_t w[8];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int c0 = gn0 + j + 2 * q;
-              const float d0 = cf * (__expf(u2f(v[j + 2 * q]) - l) - (c0 == yl ? 1.0f : 0.0f));
-              const float d1 =
-                  cf * (__expf(u2f(v[j + 2 * q + 1]) - l) - (c0 + 1 == yl ? 1.0f : 0.0f));
-              pw[q] = pack_bf16(d0, d1);
-            }
-            *reinterpret_cast<uint4*>(drow + gn0 + j) = w;
+          for (int q = 0; q < 8; ++q) {
+            const int c0 = gn0 + j + 2 * q;
+            const float d0 = cf * (__expf(u2f(v[j + 2 * q]) - l) - (c0 == yl ? 1.0f : 0.0f));
+            const float d1 =
+                cf * (__expf(u2f(v[j + 2 * q + 1]) - l) - (c0 + 1 == yl ? 1.0f : 0.0f));
+            w[q] = pack_bf16(d0, d1);
+          }
+          __nv_bfloat16* pd = drow + gn0 + j;
+          if (gn0 + j + 16 <= args.N && aligned32(pd)) {
+            st_global_v8(pd, w);
+          } else {
+            *reinterpret_cast<uint4*>(pd) = make_uint4(w[0], w[1], w[2], w[3]);
+            if (gn0 + j + 8 < args.N)
+              *reinterpret_cast<uint4*>(pd + 8) = make_uint4(w[4], w[5], w[6], w[7]);
           }
         }
       }
