@@ -23,7 +23,13 @@
  *    and nothing is enqueued; errors only the device can see (target ids out
  *    of range, non-finite losses) are recorded in a status word inside the
  *    workspace and read with ee_get_status().
- *  - Thread safety: calls are re-entrant; ee_last_error() is thread-local.
+ *  - Workspace: caller-allocated device scratch of ee_workspace_size() bytes,
+ *    ZERO-INITIALISED ONCE before first use (its head holds the device status
+ *    word, cleared again by ee_get_status); one workspace per stream.
+ *  - Thread safety: calls are re-entrant (distinct workspaces); ee_last_error()
+ *    is thread-local; the ee_profile_* instrumentation is process-global.
+ *  - Device: the first call caches the current device's properties; use one
+ *    device per process (the torchrun model).
  *  - Requires an sm_100a GPU (B200); on anything else ee_tune_step returns
  *    EE_ERR_UNSUPPORTED.  There is no CPU fallback.
  */

@@ -23,6 +23,7 @@
 #include <cstdarg>
 #include <cstring>
 #include <string>
+#include <atomic>
 #include <vector>
 #include "../../include/ee.h"
 #include "internal.cuh"
@@ -178,7 +179,7 @@ struct ProfRec {
 std::vector<ProfRec> g_prof;
 std::vector<cudaEvent_t> g_event_pool;
 bool g_prof_on = false;
-long long g_launches = 0;
+std::atomic<long long> g_launches{0};
 
 cudaEvent_t pool_event() {
   if (!g_event_pool.empty()) {
@@ -960,7 +961,7 @@ ee_status ee_profile_record(int32_t i, char* name, int32_t name_len, float* ms, 
   return EE_OK;
 }
 
-int64_t ee_launch_count(void) { return g_launches; }
+int64_t ee_launch_count(void) { return g_launches.load(); }
 
 // Debug hook (not in ee.h's product surface): arm a per-tile timing trace of the
 // next GEMM launch, then read (globaltimer_ns << 8 | smid) per tile.
