@@ -375,11 +375,17 @@ def main():
             dist.barrier()
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record()
+        streamed = not multi and not per_exit and not vp
         for it in range(args.steps):
-            for d_, h_ in zip(hidden, h_host):
-                d_.copy_(h_, non_blocking=True)
-            targets.copy_(t_host, non_blocking=True)
-            step(args.warmup + args.steps + it)
+            if streamed:   # public API for host-resident hidden states: H2D overlapped per exit
+                heads.step_host(h_host, t_host)
+                heads.adam(ee.ee_lr_at(min(args.warmup + args.steps + it + 1, total_iters),
+                                       total_iters))
+            else:
+                for d_, h_ in zip(hidden, h_host):
+                    d_.copy_(h_, non_blocking=True)
+                targets.copy_(t_host, non_blocking=True)
+                step(args.warmup + args.steps + it)
             loss_host.copy_(heads.loss, non_blocking=True)
         a1.record()
         torch.cuda.synchronize()
@@ -388,7 +394,9 @@ def main():
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": job_tokens / (te.item() / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": sum(h.numel() * 2 for h in hidden) + targets.numel() * 4,
-               "d2h_bytes_per_step": E * 4, "ms_per_step": te.item()}
+               "d2h_bytes_per_step": E * 4, "ms_per_step": te.item(),
+               "api": ("ExitHeads.step_host (per-exit H2D overlapped with compute) + adam"
+                       if streamed else "H2D copies + step")}
         del h_host
 
     if rank != 0:

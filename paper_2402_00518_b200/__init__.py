@@ -439,6 +439,49 @@ class ExitHeads:
                        self.grads[i:i + 1], self.m[i:i + 1], self.v[i:i + 1], lr, step, beta1,
                        beta2, eps, weight_decay, grad_scale)
 
+    def step_host(self, hidden_host, targets_host, exit_weights=None):
+        """One tuning step with the cached hidden states in pinned HOST memory
+        (the usual place for them: 4.3 GB per step at the 70B shape).  Exit
+        i + 1's hidden states are copied host-to-device on a side stream while
+        exit i computes (two device staging buffers, event-ordered), so the
+        PCIe/C2C transfer hides under the exit's GEMMs.  Same results as
+        step() on device copies of the same bytes.  Returns the device losses."""
+        E = self.spec.num_exits
+        n, h = hidden_host[0].shape
+        if n > self.max_tokens:
+            raise ValueError("more tokens than the workspace was sized for")
+        dev = self.loss.device
+        st = torch.cuda.current_stream(dev)
+        if getattr(self, "_stage", None) is None or self._stage[0].shape[0] < n:
+            self._stage = [torch.empty(n, h, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+            self._stage_tg = torch.empty(n, dtype=torch.int32, device=dev)
+            self._copy_stream = torch.cuda.Stream(dev)
+            self._ev = [[torch.cuda.Event(), torch.cuda.Event()] for _ in range(2)]
+        bufs = [b[:n] for b in self._stage]
+        tg = self._stage_tg[:n]
+        cs = self._copy_stream
+        ev_copied, ev_free = self._ev[0], self._ev[1]
+        w = exit_weights if exit_weights is not None else [1.0] * E
+        tg.copy_(targets_host, non_blocking=True)
+        cs.wait_stream(st)                      # staging buffers free from the last call
+        with torch.cuda.stream(cs):
+            bufs[0].copy_(hidden_host[0], non_blocking=True)
+            ev_copied[0].record(cs)
+        for i in range(E):
+            b = i % 2
+            if i + 1 < E:
+                nb_ = (i + 1) % 2
+                with torch.cuda.stream(cs):
+                    if i >= 1:
+                        cs.wait_event(ev_free[nb_])     # exit i-1 done with this buffer
+                    bufs[nb_].copy_(hidden_host[i + 1], non_blocking=True)
+                    ev_copied[nb_].record(cs)
+            st.wait_event(ev_copied[b])
+            ee_tune_step(self.exit_cfg, [bufs[b]], tg, w[i:i + 1], self.operand[i:i + 1],
+                         self.grads[i:i + 1], self.loss[i:i + 1], self.workspace)
+            ev_free[b].record(st)
+        return self.loss
+
     def step_per_exit(self, hidden, targets, lr, exit_weights=None, valid_count=None,
                       reduce_grads=None):
         """One step exit by exit: tune exit i, (optionally) reduce its gradients,

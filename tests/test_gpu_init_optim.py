@@ -193,3 +193,23 @@ def test_per_exit_update_with_shared_grad_buffer_equals_full_step(gpu_lib):
         for k in a.master[i]:
             assert torch.equal(a.master[i][k], b.master[i][k]), (i, k)
             assert torch.equal(a.m[i][k], b.m[i][k]), (i, k)
+
+
+def test_step_host_streaming_equals_device_step(gpu_lib):
+    """Host-resident hidden states streamed per exit (H2D overlapped with the
+    previous exit's compute) give bitwise the same losses and gradients."""
+    cfg = S.Cfg(name="small", hidden=128, vocab=1000, ffn=256, arch="mlp", tokens=300, layers=3,
+                after=[1, 2, 3], init="random", seed=42)
+    spec = gpu_lib.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, 3, cfg.arch)
+    a = gpu_lib.ExitHeads(spec, 300)
+    a.init("random", seed=9)
+    hidden = S.hidden_states(cfg, 300)
+    targets = S.targets(cfg, 300)
+    la = a.step([h.cuda() for h in hidden], targets.cuda()).clone()
+    ga = [{k: v.clone() for k, v in g.items()} for g in a.grads]
+    lb = a.step_host([h.pin_memory() for h in hidden], targets.pin_memory()).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(la, lb)
+    for i in range(3):
+        for k in ga[i]:
+            assert torch.equal(ga[i][k], a.grads[i][k]), (i, k)
