@@ -367,3 +367,78 @@ def original_final_logits(backbone: dict, h_last: np.ndarray, eps: float) -> np.
     g = backbone["final_norm"]
     r = 1.0 / np.sqrt(np.mean(h_last * h_last, axis=-1) + eps)
     return (g[None, :] * (h_last * r[:, None])) @ backbone["w_out"].T
+
+
+# ----------------------------------------------------------------------------
+# Frozen backbone partial forward (NEXT #3; §2.2 "Computational
+# efficiency": "the partial forward pass of the Transformer backbone up to the
+# hidden states connected to the last early exit")
+# ----------------------------------------------------------------------------
+
+def rope(x: np.ndarray, positions: np.ndarray, theta: float = 10000.0) -> np.ndarray:
+    """Rotary position embedding, Llama "rotate-half" convention, applied to
+    x [N, heads, d]: for i < d/2, angle_i(t) = t * theta^(-2i/d);
+    out_i = x_i cos - x_{i+d/2} sin, out_{i+d/2} = x_{i+d/2} cos + x_i sin."""
+    d = x.shape[-1]
+    half = d // 2
+    inv = theta ** (-np.arange(half, dtype=np.float64) * 2.0 / d)
+    ang = positions.astype(np.float64)[:, None] * inv[None, :]          # [N, d/2]
+    c, s = np.cos(ang)[:, None, :], np.sin(ang)[:, None, :]
+    x1, x2 = x[..., :half], x[..., half:]
+    return np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], axis=-1)
+
+
+def causal_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, seq_len: int) -> np.ndarray:
+    """softmax(q k^T / sqrt(d) + causal mask) v within each sequence of
+    seq_len consecutive rows; GQA: query head j uses kv head j // (Hq/Hkv).
+    q [N, Hq, d], k, v [N, Hkv, d] -> [N, Hq, d]."""
+    N, Hq, d = q.shape
+    Hkv = k.shape[1]
+    g = Hq // Hkv
+    out = np.zeros_like(q)
+    mask = np.triu(np.ones((seq_len, seq_len), dtype=bool), 1)
+    for b in range(N // seq_len):
+        rs = slice(b * seq_len, (b + 1) * seq_len)
+        for j in range(Hq):
+            S = q[rs, j, :] @ k[rs, j // g, :].T / math.sqrt(d)
+            S = np.where(mask, -np.inf, S)
+            S = S - S.max(axis=1, keepdims=True)
+            P = np.exp(S)
+            P /= P.sum(axis=1, keepdims=True)
+            out[rs, j, :] = P @ v[rs, j // g, :]
+    return out
+
+
+def llama_layer_forward(layer: dict, x: np.ndarray, seq_len: int, n_heads: int, n_kv: int,
+                        eps: float, theta: float = 10000.0) -> np.ndarray:
+    """One pre-norm Llama-2 decoder layer (the backbone the paper tunes on,
+    P:356-358; "residual structure with pre-normalization", P:165-166):
+    x += Wo attn(RoPE(Wq u), RoPE(Wk u), Wv u), u = RMSNorm(x; g_att);
+    x += W_down(silu(W_gate u') * W_up u'), u' = RMSNorm(x; g_mlp)."""
+    N, h = x.shape
+    d = h // n_heads
+    pos = np.arange(N) % seq_len
+    u, _, _ = rmsnorm(x, layer["g_att"], eps)
+    q = (u @ layer["w_q"].T).reshape(N, n_heads, d)
+    k = (u @ layer["w_k"].T).reshape(N, n_kv, d)
+    v = (u @ layer["w_v"].T).reshape(N, n_kv, d)
+    q, k = rope(q, pos, theta), rope(k, pos, theta)
+    o = causal_attention(q, k, v, seq_len).reshape(N, n_heads * d)
+    x = x + o @ layer["w_o"].T
+    u2, _, _ = rmsnorm(x, layer["g_mlp"], eps)
+    x = x + (silu(u2 @ layer["w_gate"].T) * (u2 @ layer["w_up"].T)) @ layer["w_down"].T
+    return x
+
+
+def backbone_forward(layers, x0: np.ndarray, seq_len: int, n_heads: int, n_kv: int,
+                     exit_after, eps: float, theta: float = 10000.0):
+    """Runs layers 1..max(exit_after) only (the partial forward of P:260) and
+    returns the hidden state after each requested layer (the exits' inputs)."""
+    outs = {}
+    x = x0
+    last = max(exit_after)
+    for l in range(1, last + 1):
+        x = llama_layer_forward(layers[l - 1], x, seq_len, n_heads, n_kv, eps, theta)
+        if l in exit_after:
+            outs[l] = x.copy()
+    return [outs[l] for l in exit_after]

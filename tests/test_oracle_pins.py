@@ -426,3 +426,85 @@ def test_exit_infer_thresholds():
     for i in range(3):
         S = O.exit_forward("mlp", ps[i], xs[i], 1e-5)["S"]
         np.testing.assert_array_equal(am[i], np.argmax(S, axis=1))
+
+
+# --------------------------------------------------------------------------- NEXT #3
+def _layer(rng, h, nh, nkv, F, std=0.3):
+    d = h // nh
+    return {"g_att": 1 + 0.1 * rng.normal(size=h), "w_q": rng.normal(0, std, (nh * d, h)),
+            "w_k": rng.normal(0, std, (nkv * d, h)), "w_v": rng.normal(0, std, (nkv * d, h)),
+            "w_o": rng.normal(0, std, (h, nh * d)), "g_mlp": 1 + 0.1 * rng.normal(size=h),
+            "w_gate": rng.normal(0, std, (F, h)), "w_up": rng.normal(0, std, (F, h)),
+            "w_down": rng.normal(0, std, (h, F))}
+
+
+def test_rope_is_a_relative_rotation():
+    """RoPE preserves norms and q_m . k_n depends only on m - n."""
+    rng = _rng(40)
+    d = 16
+    q = rng.normal(size=(1, 1, d))
+    k = rng.normal(size=(1, 1, d))
+    for m in (0, 3, 100):
+        np.testing.assert_allclose(np.linalg.norm(O.rope(q, np.array([m]))), np.linalg.norm(q),
+                                   rtol=1e-13)
+    dot = lambda m, n: float(np.sum(O.rope(q, np.array([m])) * O.rope(k, np.array([n]))))
+    assert dot(7, 3) == pytest.approx(dot(104, 100), rel=1e-11)
+    assert dot(0, 0) == pytest.approx(float(np.sum(q * k)), rel=1e-13)
+
+
+@pytest.mark.parametrize("nh,nkv", [(4, 4), (4, 2)])
+def test_llama_layer_matches_torch_sdpa(nh, nkv):
+    """One layer vs a composition of torch library routines in fp64:
+    F.rms_norm, F.scaled_dot_product_attention(is_causal, GQA), F.silu; RoPE
+    written out (rotate-half) and pinned separately above."""
+    rng = _rng(41)
+    h, F, T, B = 32, 24, 6, 2
+    L = _layer(rng, h, nh, nkv, F)
+    x = rng.normal(size=(B * T, h))
+    got = O.llama_layer_forward(L, x, T, nh, nkv, 1e-5)
+    t = {k: torch.tensor(v) for k, v in L.items()}
+    X = torch.tensor(x)
+    d = h // nh
+    u = Fn.rms_norm(X, (h,), t["g_att"], 1e-5)
+    pos = torch.arange(B * T) % T
+    inv = 10000.0 ** (-torch.arange(d // 2, dtype=torch.float64) * 2 / d)
+    ang = pos[:, None].double() * inv[None]
+
+    def rot(z):
+        z1, z2 = z[..., :d // 2], z[..., d // 2:]
+        c, s = torch.cos(ang)[:, None], torch.sin(ang)[:, None]
+        return torch.cat([z1 * c - z2 * s, z2 * c + z1 * s], -1)
+    q = rot(Fn.linear(u, t["w_q"]).view(B * T, nh, d)).view(B, T, nh, d).transpose(1, 2)
+    k = rot(Fn.linear(u, t["w_k"]).view(B * T, nkv, d)).view(B, T, nkv, d).transpose(1, 2)
+    v = Fn.linear(u, t["w_v"]).view(B, T, nkv, d).transpose(1, 2)
+    o = Fn.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=nkv != nh)
+    X = X + Fn.linear(o.transpose(1, 2).reshape(B * T, nh * d), t["w_o"])
+    u2 = Fn.rms_norm(X, (h,), t["g_mlp"], 1e-5)
+    X = X + Fn.linear(Fn.silu(Fn.linear(u2, t["w_gate"])) * Fn.linear(u2, t["w_up"]), t["w_down"])
+    np.testing.assert_allclose(got, X.numpy(), rtol=1e-11, atol=1e-12)
+
+
+def test_backbone_partial_forward_structure():
+    """Zero output projections make a layer the identity (pure residual);
+    the partial forward stops at the last exit layer and returns the
+    states after the requested layers; sequences do not attend across each
+    other (causal within each seq_len block)."""
+    rng = _rng(42)
+    h, nh, nkv, F, T = 16, 2, 1, 12, 5
+    layers = [_layer(rng, h, nh, nkv, F) for _ in range(4)]
+    x0 = rng.normal(size=(2 * T, h))
+    z = dict(layers[0], w_o=np.zeros((h, h)), w_down=np.zeros((h, F)))
+    np.testing.assert_array_equal(O.llama_layer_forward(z, x0, T, nh, nkv, 1e-5), x0)
+    outs = O.backbone_forward(layers, x0, T, nh, nkv, [1, 3], 1e-5)
+    x1 = O.llama_layer_forward(layers[0], x0, T, nh, nkv, 1e-5)
+    x3 = O.llama_layer_forward(layers[2], O.llama_layer_forward(layers[1], x1, T, nh, nkv, 1e-5),
+                               T, nh, nkv, 1e-5)
+    np.testing.assert_array_equal(outs[0], x1)
+    np.testing.assert_array_equal(outs[1], x3)
+    x_mod = x0.copy()
+    x_mod[T:] += 1.0                                                  # change sequence 2 only
+    np.testing.assert_array_equal(O.llama_layer_forward(layers[0], x_mod, T, nh, nkv, 1e-5)[:T], x1[:T])
+    x_fut = x0.copy()
+    x_fut[T - 1] += 1.0                                               # change the last token
+    np.testing.assert_array_equal(O.llama_layer_forward(layers[0], x_fut, T, nh, nkv, 1e-5)[:T - 1],
+                                  x1[:T - 1])
