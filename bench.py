@@ -191,6 +191,51 @@ def workload_config(cfg, world, args):
                                 if getattr(args, "per_exit", False) else "all exits, then Adam")}
 
 
+LLAMA2 = {4096: (32, 32), 5120: (40, 40), 8192: (64, 8)}   # hidden -> (heads, kv heads) [ext]
+
+
+def bench_backbone(ee, torch, cfg, args, dev):
+    """Frozen backbone partial forward (ee_backbone_forward) over
+    args.backbone_layers Llama-2 layers at the config's shape, on the same
+    token batch; CUDA-event timed (3 warm-ups)."""
+    h, F, T = cfg.hidden, cfg.ffn, 2048
+    nh, nkv = LLAMA2[h]
+    n = cfg.tokens
+    L = args.backbone_layers
+    g = torch.Generator(device=dev).manual_seed(11)
+
+    def r(*shape):
+        return (torch.randn(*shape, generator=g, device=dev) * 0.02).to(torch.bfloat16)
+    layers = [{"g_att": torch.ones(h, device=dev), "w_q": r(h, h), "w_k": r(128 * nkv, h),
+               "w_v": r(128 * nkv, h), "w_o": r(h, h), "g_mlp": torch.ones(h, device=dev),
+               "w_gate": r(F, h), "w_up": r(F, h), "w_down": r(h, F)} for _ in range(L)]
+    x0 = torch.randn(n, h, generator=g, device=dev).to(torch.bfloat16)
+    bc = ee.make_backbone_config(h, nh, nkv, F, T)
+    ws = torch.empty(ee.ee_backbone_workspace_size(bc, n), dtype=torch.uint8, device=dev)
+    out = [torch.empty(n, h, dtype=torch.bfloat16, device=dev)]
+    for _ in range(3):
+        ee.ee_backbone_forward(bc, layers, x0, [L], out, ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ee.ee_profile_start()
+    e0.record()
+    steps = max(1, args.steps // 2)
+    for _ in range(steps):
+        ee.ee_backbone_forward(bc, layers, x0, [L], out, ws)
+    e1.record()
+    torch.cuda.synchronize()
+    prof = ee.ee_profile_stop()
+    ms = e0.elapsed_time(e1) / steps
+    flops = sum(p[3] for p in prof) / steps
+    peaks = load_peaks()
+    att = sum(p[1] for p in prof if p[0] == "bb_attention") / steps
+    return {"layers": L, "shape": f"h {h}, heads {nh}/{nkv} kv, F {F}, seq 2048",
+            "tokens": n, "ms": ms, "tokens_per_s": n / (ms / 1e3),
+            "tflops": flops / (ms / 1e3) / 1e12,
+            "pct_burst_peak": flops / (ms / 1e3) / 1e12 / peaks["bf16_tflops"],
+            "attention_share": att / ms}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -203,6 +248,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quick", action="store_true", help="ncu/profiling run: no extras")
+    ap.add_argument("--backbone-layers", type=int, default=0,
+                    help="also time the frozen backbone partial forward (NEXT #3, P:260) over "
+                         "this many Llama-2 layers of the config's shape (70b: 20 = 1/4 depth)")
     ap.add_argument("--grad-buffers", type=int, default=-1,
                     help="k < exits: exits share k gradient buffers and are updated one by one "
                          "(P:261); default 2 when the config has more than 4 exits")
@@ -468,6 +516,8 @@ def main():
         "loss_last_step": [round(float(v), 6) for v in heads.loss.tolist()],
         "kernels": kernels,
     }
+    if args.backbone_layers > 0 and world == 1:
+        line["backbone_forward"] = bench_backbone(ee, torch, cfg, args, dev)
     if world == 1 and not args.no_cpu_baseline and not args.quick:
         try:
             t_or, cores = cpu_oracle_sample(cfg, args.cpu_tokens, seed=cfg.seed)

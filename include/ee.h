@@ -236,6 +236,35 @@ ee_status ee_exit_infer(const ee_head_config* cfg, const void* const* hidden, in
                         float* const* conf_out, int32_t* first_exit, void* workspace,
                         size_t ws_bytes, void* stream);
 
+/* ---- frozen backbone partial forward (NEXT #3) ----
+ * "the partial forward pass of the Transformer backbone up to the hidden
+ * states connected to the last early exit": Llama-2 pre-norm decoder
+ * layers (residual + pre-normalisation), RoPE
+ * (rotate-half, base rope_theta), causal GQA attention within sequences of
+ * seq_len rows, SwiGLU MLP.  Produces the exits' cached hidden states.
+ *  hidden      h = n_heads * 128 (head dim 128, as in every Llama-2 size)
+ *  n_kv_heads  divides n_heads (GQA; = n_heads for MHA)
+ *  ffn         multiple of 128;  seq_len multiple of 64;  n_tokens multiple
+ *              of seq_len (row = sequence * seq_len + position).
+ * Layer tensors: gains fp32 [h]; w_q [h x h], w_k, w_v [n_kv*128 x h],
+ * w_o [h x h], w_gate, w_up [F x h], w_down [h x F] bf16, row-major.
+ * The residual stream is kept in fp32; hidden_out[i] (bf16 [n_tokens x h])
+ * receives it after layer exit_after[i] (1-based, ascending); only layers
+ * 1..exit_after[num_exits-1] run.  x0: bf16 [n_tokens x h] (the embeddings). */
+typedef struct {
+  int32_t hidden, n_heads, n_kv_heads, ffn, seq_len;
+  float norm_eps, rope_theta;
+} ee_backbone_config;
+typedef struct {
+  void *g_att, *w_q, *w_k, *w_v, *w_o, *g_mlp, *w_gate, *w_up, *w_down;
+} ee_layer_tensors;
+ee_status ee_backbone_workspace_size(const ee_backbone_config* cfg, int64_t n_tokens, size_t* bytes);
+ee_status ee_backbone_forward(const ee_backbone_config* cfg, const ee_layer_tensors* layers,
+                              int32_t n_layers, const void* x0, int64_t n_tokens,
+                              const int32_t* exit_after, int32_t num_exits,
+                              void* const* hidden_out, void* workspace, size_t ws_bytes,
+                              void* stream);
+
 /* Number of valid targets (!= -1) -> device int64 out[0]; flags ids outside
  * [-1, V) in the workspace status word.  Used to form the global W under
  * data parallelism (the caller all-reduces out). */

@@ -31,7 +31,8 @@ EXPORTED = ("ee_workspace_size", "ee_init_heads", "ee_tune_step", "ee_count_vali
             "ee_adam_update", "ee_sgd_update", "ee_get_status", "ee_lr_at", "ee_last_error",
             "ee_version", "ee_test_gemm", "ee_profile_start", "ee_profile_stop",
             "ee_profile_record", "ee_launch_count", "ee_vp_exit_forward", "ee_vp_vocab_stats",
-            "ee_vp_rescale", "ee_vp_vocab_backward", "ee_vp_exit_backward", "ee_exit_infer")
+            "ee_vp_rescale", "ee_vp_vocab_backward", "ee_vp_exit_backward", "ee_exit_infer",
+            "ee_backbone_workspace_size", "ee_backbone_forward")
 
 
 class EEError(RuntimeError):
@@ -49,6 +50,20 @@ class ee_head_config(ctypes.Structure):
 
 class ee_head_tensors(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in TENSOR_NAMES]
+
+
+class ee_backbone_config(ctypes.Structure):
+    _fields_ = [("hidden", ctypes.c_int32), ("n_heads", ctypes.c_int32),
+                ("n_kv_heads", ctypes.c_int32), ("ffn", ctypes.c_int32),
+                ("seq_len", ctypes.c_int32), ("norm_eps", ctypes.c_float),
+                ("rope_theta", ctypes.c_float)]
+
+
+LAYER_NAMES = ("g_att", "w_q", "w_k", "w_v", "w_o", "g_mlp", "w_gate", "w_up", "w_down")
+
+
+class ee_layer_tensors(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in LAYER_NAMES]
 
 
 class ee_step_aux(ctypes.Structure):
@@ -101,6 +116,11 @@ def load(path: str = LIB_PATH):
         "ee_vp_exit_backward": (I32, [CFG, P, I64, I64, HT, P, HT, I32, P, SZ, P]),
         "ee_exit_infer": (I32, [CFG, ctypes.POINTER(P), I64, HT, F32, ctypes.POINTER(P),
                                 ctypes.POINTER(P), P, P, SZ, P]),
+        "ee_backbone_workspace_size": (I32, [ctypes.POINTER(ee_backbone_config), I64,
+                                             ctypes.POINTER(SZ)]),
+        "ee_backbone_forward": (I32, [ctypes.POINTER(ee_backbone_config),
+                                      ctypes.POINTER(ee_layer_tensors), I32, P, I64,
+                                      ctypes.POINTER(I32), I32, ctypes.POINTER(P), P, SZ, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -198,6 +218,33 @@ def ee_exit_infer(cfg, hidden, params, threshold, argmax_out, conf_out, workspac
     _check(_lib.ee_exit_infer(ctypes.byref(cfg), hid, n, heads(params), float(threshold), am, cf,
                               _ptr(first_exit), _ptr(workspace), workspace.numel(),
                               _stream(stream)))
+
+
+def make_backbone_config(hidden, n_heads, n_kv_heads, ffn, seq_len, norm_eps=1e-5,
+                         rope_theta=10000.0):
+    return ee_backbone_config(hidden, n_heads, n_kv_heads, ffn, seq_len, norm_eps, rope_theta)
+
+
+def ee_backbone_workspace_size(cfg, n_tokens) -> int:
+    load()
+    out = ctypes.c_size_t(0)
+    _check(_lib.ee_backbone_workspace_size(ctypes.byref(cfg), int(n_tokens), ctypes.byref(out)))
+    return out.value
+
+
+def ee_backbone_forward(cfg, layers, x0, exit_after, hidden_out, workspace, stream=None):
+    """Frozen backbone partial forward: runs layers 1..max(exit_after)
+    on x0 [n x h] bf16 and writes the state after each exit layer."""
+    load()
+    L = (ee_layer_tensors * len(layers))()
+    for i, d in enumerate(layers):
+        for n in LAYER_NAMES:
+            setattr(L[i], n, d[n].data_ptr())
+    E = len(exit_after)
+    ex = (ctypes.c_int32 * E)(*[int(e) for e in exit_after])
+    ho = (ctypes.c_void_p * E)(*[t.data_ptr() for t in hidden_out])
+    _check(_lib.ee_backbone_forward(ctypes.byref(cfg), L, len(layers), _ptr(x0), x0.shape[0], ex,
+                                    E, ho, _ptr(workspace), workspace.numel(), _stream(stream)))
 
 
 def ee_count_valid(targets, vocab, out, workspace, stream=None):

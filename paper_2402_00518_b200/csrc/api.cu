@@ -611,6 +611,163 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
   return EE_OK;
 }
 
+// ---------------------------------------------------------------- backbone partial forward
+static ee_status check_backbone(const ee_backbone_config* c) {
+  if (!c) return fail(EE_ERR_ARG, "backbone cfg is NULL");
+  if (c->n_heads < 1 || c->n_kv_heads < 1 || c->n_heads % c->n_kv_heads != 0)
+    return fail(EE_ERR_SHAPE, "n_kv_heads must divide n_heads");
+  if (c->hidden != c->n_heads * 128 || c->hidden > 16384)
+    return fail(EE_ERR_SHAPE, "hidden must be n_heads * 128 (head dim 128)");
+  if (c->ffn < 128 || c->ffn % 128 != 0) return fail(EE_ERR_SHAPE, "ffn must be a multiple of 128");
+  if (c->seq_len < 64 || c->seq_len % 64 != 0)
+    return fail(EE_ERR_SHAPE, "seq_len must be a positive multiple of 64");
+  if (!(c->norm_eps >= 0.f) || !(c->rope_theta > 0.f)) return fail(EE_ERR_ARG, "bad eps/theta");
+  return EE_OK;
+}
+
+struct BbLayout {
+  size_t x, u, q, k, v, o, ab, m, r, total;
+};
+static BbLayout bb_layout(const ee_backbone_config* c, long long n) {
+  BbLayout L{};
+  const long long h = c->hidden, hkv = 128LL * c->n_kv_heads, F = c->ffn;
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    size_t r = off;
+    off = align_up(off + b);
+    return r;
+  };
+  L.x = take(4 * (size_t)n * h);
+  L.u = take(2 * (size_t)n * h);
+  L.q = take(2 * (size_t)n * h);
+  L.k = take(2 * (size_t)n * hkv);
+  L.v = take(2 * (size_t)n * hkv);
+  L.o = take(2 * (size_t)n * h);
+  L.ab = take(2 * (size_t)n * 2 * F);
+  L.m = take(2 * (size_t)n * F);
+  L.r = take(4 * (size_t)(n > 0 ? n : 1));
+  L.total = off;
+  return L;
+}
+
+ee_status ee_backbone_workspace_size(const ee_backbone_config* cfg, int64_t n_tokens,
+                                     size_t* bytes) {
+  ee_status s = check_backbone(cfg);
+  if (s != EE_OK) return s;
+  if (!bytes || n_tokens < 0) return fail(EE_ERR_ARG, "bytes NULL or n_tokens < 0");
+  *bytes = bb_layout(cfg, n_tokens).total;
+  return EE_OK;
+}
+
+ee_status ee_backbone_forward(const ee_backbone_config* cfg, const ee_layer_tensors* layers,
+                              int32_t n_layers, const void* x0, int64_t n_tokens,
+                              const int32_t* exit_after, int32_t num_exits,
+                              void* const* hidden_out, void* workspace, size_t ws_bytes,
+                              void* stream) {
+  ee_status s = check_backbone(cfg);
+  if (s != EE_OK) return s;
+  if (!layers || !x0 || !exit_after || !hidden_out || num_exits < 1 || n_tokens < 0)
+    return fail(EE_ERR_ARG, "NULL argument");
+  if (n_tokens % cfg->seq_len != 0)
+    return fail(EE_ERR_SHAPE, "n_tokens must be a multiple of seq_len");
+  for (int i = 0; i < num_exits; ++i) {
+    if (exit_after[i] < 1 || exit_after[i] > n_layers || (i && exit_after[i] <= exit_after[i - 1]))
+      return fail(EE_ERR_ARG, "exit_after must be ascending in [1, n_layers]");
+    if (!hidden_out[i]) return fail(EE_ERR_ARG, "hidden_out[%d] is NULL", i);
+  }
+  const int last = exit_after[num_exits - 1];
+  for (int l = 0; l < last; ++l) {
+    const ee_layer_tensors& t = layers[l];
+    const void* ps[9] = {t.g_att, t.w_q, t.w_k, t.w_v, t.w_o, t.g_mlp, t.w_gate, t.w_up, t.w_down};
+    for (const void* p : ps)
+      if (!p || !aligned16(p)) return fail(EE_ERR_ARG, "layer %d: tensor NULL or misaligned", l + 1);
+  }
+  const long long n = n_tokens;
+  const BbLayout L = bb_layout(cfg, n);
+  if (!workspace || !aligned16(workspace) || ws_bytes < L.total)
+    return fail(EE_ERR_WORKSPACE, "workspace needs %zu bytes, got %zu", L.total, ws_bytes);
+  if ((s = check_device()) != EE_OK) return s;
+  if (n == 0) return EE_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* ws = (uint8_t*)workspace;
+  float* x = (float*)(ws + L.x);
+  __nv_bfloat16* u = (__nv_bfloat16*)(ws + L.u);
+  __nv_bfloat16* q = (__nv_bfloat16*)(ws + L.q);
+  __nv_bfloat16* k = (__nv_bfloat16*)(ws + L.k);
+  __nv_bfloat16* v = (__nv_bfloat16*)(ws + L.v);
+  __nv_bfloat16* o = (__nv_bfloat16*)(ws + L.o);
+  __nv_bfloat16* ab = (__nv_bfloat16*)(ws + L.ab);
+  __nv_bfloat16* mact = (__nv_bfloat16*)(ws + L.m);
+  float* r = (float*)(ws + L.r);
+  const int h = cfg->hidden, Hq = cfg->n_heads, Hkv = cfg->n_kv_heads, F = cfg->ffn;
+  const int hkv = 128 * Hkv;
+  { Prof p_("bb_cast_in", st, 0, 0, 6.0 * n * h);
+  EE_CUDA(launch_cast_bf16_f32((const __nv_bfloat16*)x0, x, n * h, st)); }
+  int next_exit = 0;
+  for (int l = 0; l < last; ++l) {
+    const ee_layer_tensors& t = layers[l];
+    { Prof p_("bb_rmsnorm_att", st, 0, 0, 6.0 * n * h);
+    EE_CUDA(launch_rmsnorm_fwd(x, true, (const float*)t.g_att, cfg->norm_eps, u, r, n, h, st)); }
+    struct Proj {
+      const void* w;
+      __nv_bfloat16* out;
+      int N;
+      const char* name;
+    } projs[3] = {{t.w_q, q, h, "bb_q_proj"}, {t.w_k, k, hkv, "bb_k_proj"}, {t.w_v, v, hkv, "bb_v_proj"}};
+    for (const Proj& pj : projs) {
+      GemmArgs a = base_args((int)n, pj.N, h);
+      a.outb = pj.out;
+      a.ldo = pj.N;
+      Mat A{u, n, h, h}, B{pj.w, pj.N, h, h};
+      Prof p_(pj.name, st, 2.0 * n * pj.N * h, 2.0 * n * pj.N * h, 0);
+      EE_CUDA(gemm_run(EPI_BF16, true, true, A, B, nullptr, B_PLAIN, 0, a, st));
+    }
+    { Prof p_("bb_rope", st, 0, 0, 4.0 * n * (h + hkv));
+    EE_CUDA(launch_rope(q, n, Hq, cfg->seq_len, cfg->rope_theta, st));
+    EE_CUDA(launch_rope(k, n, Hkv, cfg->seq_len, cfg->rope_theta, st)); }
+    { const double fl = 2.0 * 2.0 * (double)n * (cfg->seq_len + 64) / 2.0 * h;  // causal
+      Prof p_("bb_attention", st, fl, fl, 0);
+      EE_CUDA(launch_attn_fwd(q, k, v, o, n, cfg->seq_len, Hq, Hkv, st)); }
+    {  // x += o W_o^T
+      GemmArgs a = base_args((int)n, h, h);
+      a.out0 = x;
+      a.ldo = h;
+      a.accumulate = 1;
+      Mat A{o, n, h, h}, B{t.w_o, h, h, h};
+      Prof p_("bb_o_proj", st, 2.0 * n * h * h, 2.0 * n * h * h, 0);
+      EE_CUDA(gemm_run(EPI_F32, true, true, A, B, nullptr, B_PLAIN, 0, a, st));
+    }
+    { Prof p_("bb_rmsnorm_mlp", st, 0, 0, 6.0 * n * h);
+    EE_CUDA(launch_rmsnorm_fwd(x, true, (const float*)t.g_mlp, cfg->norm_eps, u, r, n, h, st)); }
+    {
+      GemmArgs a = base_args((int)n, F, h);
+      a.ab = ab;
+      a.ld_ab = 2LL * F;
+      a.mact = mact;
+      a.ld_m = F;
+      a.ffn = F;
+      Mat A{u, n, h, h}, B0{t.w_gate, F, h, h}, B1{t.w_up, F, h, h};
+      Prof p_("bb_gateup_swiglu", st, 4.0 * n * F * h, 4.0 * n * F * h, 0);
+      EE_CUDA(gemm_run(EPI_SWIGLU_FWD, true, true, A, B0, &B1, B_PAIR, 0, a, st));
+    }
+    {  // x += M W_down^T
+      GemmArgs a = base_args((int)n, h, F);
+      a.out0 = x;
+      a.ldo = h;
+      a.accumulate = 1;
+      Mat A{mact, n, F, F}, B{t.w_down, h, F, F};
+      Prof p_("bb_down", st, 2.0 * n * F * h, 2.0 * n * F * h, 0);
+      EE_CUDA(gemm_run(EPI_F32, true, true, A, B, nullptr, B_PLAIN, 0, a, st));
+    }
+    if (l + 1 == exit_after[next_exit]) {
+      Prof p_("bb_cast_out", st, 0, 0, 6.0 * n * h);
+      EE_CUDA(launch_cast_f32_bf16(x, (__nv_bfloat16*)hidden_out[next_exit], n * h, st));
+      ++next_exit;
+    }
+  }
+  return EE_OK;
+}
+
 // ---------------------------------------------------------------- early-exit inference
 // Confidence-based exit decision: per exit, the greedy token and
 // the max softmax probability; first_exit[t] = lowest exit with c >= tau.

@@ -1,0 +1,238 @@
+// backbone.cu -- the frozen backbone's partial forward (NEXT #3; P:258-260,
+// PAPER.md §2.2 "Computational efficiency": "the partial forward pass of the
+// Transformer backbone up to the hidden states connected to the last early
+// exit").  Llama-2 pre-norm decoder layers:
+//   x += W_o attn(RoPE(W_q u), RoPE(W_k u), W_v u),   u  = RMSNorm(x; g_att)
+//   x += W_down(silu(W_gate u') * W_up u'),           u' = RMSNorm(x; g_mlp)
+// The projections and the MLP run on the tcgen05 GEMM (gemm.cuh); this file
+// holds RoPE, causal flash attention (forward only) and the residual casts.
+//
+// Attention is ~2% of a Llama-2 layer's FLOPs at T = 2048 (4 T h / 2 vs
+// 2 (2 h^2 + 2 h h_kv + 3 h F) per token), so it uses warp-level mma.sync
+// (m16n8k16 bf16, fp32 accumulate) in the FlashAttention-2 register layout:
+// one CTA per (64-query tile, head, sequence), 4 warps x 16 query rows, K/V
+// tiles of 64 keys staged in shared memory, online softmax in registers, P
+// reused as the A fragments of P V.
+#include <cmath>
+#include "internal.cuh"
+
+namespace ee {
+
+// ---------------------------------------------------------------- RoPE
+// In place on x [N x H x 128] bf16 (Llama rotate-half): for i < 64,
+// angle = (row % T) * theta^(-2i/128);  (x_i, x_{i+64}) -> rotated.
+__global__ void rope_kernel(__nv_bfloat16* __restrict__ x, long long N, int H, int T, float theta) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // (row, head, i)
+  const long long total = N * H * 64;
+  if (idx >= total) return;
+  const int i = (int)(idx & 63);
+  const long long rh = idx >> 6;
+  const long long row = rh / H;
+  const int pos = (int)(row % T);
+  __nv_bfloat16* p = x + rh * 128;
+  const float inv = powf(theta, -2.0f * (float)i / 128.0f);
+  float s, c;
+  sincosf((float)pos * inv, &s, &c);
+  const float a = __bfloat162float(p[i]), b = __bfloat162float(p[i + 64]);
+  p[i] = __float2bfloat16_rn(a * c - b * s);
+  p[i + 64] = __float2bfloat16_rn(b * c + a * s);
+}
+
+cudaError_t launch_rope(__nv_bfloat16* x, long long N, int H, int T, float theta, cudaStream_t s) {
+  const long long total = N * H * 64;
+  if (total == 0) return cudaSuccess;
+  rope_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(x, N, H, T, theta);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- casts
+__global__ void cast_bf16_f32_kernel(const __nv_bfloat16* __restrict__ a, float* __restrict__ b,
+                                     long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    b[i] = __bfloat162float(a[i]);
+}
+__global__ void cast_f32_bf16_kernel(const float* __restrict__ a, __nv_bfloat16* __restrict__ b,
+                                     long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    b[i] = __float2bfloat16_rn(a[i]);
+}
+cudaError_t launch_cast_bf16_f32(const __nv_bfloat16* a, float* b, long long n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  cast_bf16_f32_kernel<<<(unsigned)min((n + 255) / 256, 65535LL * 16), 256, 0, s>>>(a, b, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_cast_f32_bf16(const float* a, __nv_bfloat16* b, long long n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  cast_f32_bf16_kernel<<<(unsigned)min((n + 255) / 256, 65535LL * 16), 256, 0, s>>>(a, b, n);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- attention
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
+                                               uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldmatrix_x4_trans(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+
+constexpr int ATT_D = 128;   // head dim (Llama-2: 128 at every size)
+constexpr int ATT_BQ = 64;   // query rows per CTA (4 warps x 16)
+constexpr int ATT_BK = 64;   // keys per tile
+constexpr int ATT_PAD = 8;
+
+// o = softmax(q k^T / sqrt(d) + causal) v for each (sequence b, query head hq);
+// k/v head = hq / (Hq / Hkv) (GQA).  q [N x Hq*128], k, v [N x Hkv*128],
+// o [N x Hq*128], bf16; row = b * T + t.
+__global__ void __launch_bounds__(128) attn_fwd_kernel(const __nv_bfloat16* __restrict__ q,
+                                                       const __nv_bfloat16* __restrict__ k,
+                                                       const __nv_bfloat16* __restrict__ v,
+                                                       __nv_bfloat16* __restrict__ o, int T,
+                                                       int Hq, int Hkv, float scale_log2) {
+  __shared__ __align__(16) __nv_bfloat16 Ks[ATT_BK][ATT_D + ATT_PAD];
+  __shared__ __align__(16) __nv_bfloat16 Vs[ATT_BK][ATT_D + ATT_PAD];
+  const int qt = blockIdx.x, hq = blockIdx.y, b = blockIdx.z;
+  const int hk = hq / (Hq / Hkv);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, c = lane & 3;
+  const long long ldq = (long long)Hq * ATT_D, ldk = (long long)Hkv * ATT_D;
+  const long long qrow0 = (long long)b * T + (long long)qt * ATT_BQ + warp * 16;
+  const int qpos0 = qt * ATT_BQ + warp * 16 + g;  // position of row g (row g+8: +8)
+
+  uint32_t qa[ATT_D / 16][4];
+#pragma unroll
+  for (int ks = 0; ks < ATT_D / 16; ++ks) {
+    const __nv_bfloat16* q0 = q + (qrow0 + g) * ldq + hq * ATT_D + ks * 16 + 2 * c;
+    const __nv_bfloat16* q1 = q0 + 8 * ldq;
+    qa[ks][0] = *reinterpret_cast<const uint32_t*>(q0);
+    qa[ks][1] = *reinterpret_cast<const uint32_t*>(q1);
+    qa[ks][2] = *reinterpret_cast<const uint32_t*>(q0 + 8);
+    qa[ks][3] = *reinterpret_cast<const uint32_t*>(q1 + 8);
+  }
+  float oacc[ATT_D / 8][4];
+#pragma unroll
+  for (int nb = 0; nb < ATT_D / 8; ++nb)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) oacc[nb][e] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+
+  const int nkt = qt + 1;  // causal: key tiles 0..qt (tile sizes equal)
+  for (int kt = 0; kt < nkt; ++kt) {
+    __syncthreads();
+    const long long krow0 = (long long)b * T + (long long)kt * ATT_BK;
+    for (int i = threadIdx.x; i < ATT_BK * (ATT_D / 8); i += blockDim.x) {
+      const int key = i / (ATT_D / 8), ch = i % (ATT_D / 8);
+      const long long off = (krow0 + key) * ldk + hk * ATT_D + ch * 8;
+      *reinterpret_cast<uint4*>(&Ks[key][ch * 8]) = *reinterpret_cast<const uint4*>(k + off);
+      *reinterpret_cast<uint4*>(&Vs[key][ch * 8]) = *reinterpret_cast<const uint4*>(v + off);
+    }
+    __syncthreads();
+    // S = Q K^T (16 x 64 per warp)
+    float sacc[ATT_BK / 8][4];
+#pragma unroll
+    for (int nb = 0; nb < ATT_BK / 8; ++nb) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sacc[nb][e] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < ATT_D / 16; ++ks) {
+        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&Ks[nb * 8 + g][ks * 16 + 2 * c]);
+        const uint32_t b1 =
+            *reinterpret_cast<const uint32_t*>(&Ks[nb * 8 + g][ks * 16 + 8 + 2 * c]);
+        mma_bf16_16816(sacc[nb], qa[ks], b0, b1);
+      }
+    }
+    // scale (log2 domain), causal mask on the diagonal tile, online softmax
+    float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+    for (int nb = 0; nb < ATT_BK / 8; ++nb) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int kpos = kt * ATT_BK + nb * 8 + 2 * c + (e & 1);
+        const int qpos = qpos0 + (e >= 2 ? 8 : 0);
+        float x = sacc[nb][e] * scale_log2;
+        if (kt == qt && kpos > qpos) x = -INFINITY;
+        sacc[nb][e] = x;
+      }
+      mx0 = fmaxf(mx0, fmaxf(sacc[nb][0], sacc[nb][1]));
+      mx1 = fmaxf(mx1, fmaxf(sacc[nb][2], sacc[nb][3]));
+    }
+#pragma unroll
+    for (int sh = 1; sh <= 2; sh <<= 1) {
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, sh));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, sh));
+    }
+    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);  // finite: diagonal always valid
+    const float al0 = exp2f(m0 - mn0), al1 = exp2f(m1 - mn1);
+    m0 = mn0;
+    m1 = mn1;
+    l0 *= al0;
+    l1 *= al1;
+#pragma unroll
+    for (int nb = 0; nb < ATT_D / 8; ++nb) {
+      oacc[nb][0] *= al0;
+      oacc[nb][1] *= al0;
+      oacc[nb][2] *= al1;
+      oacc[nb][3] *= al1;
+    }
+    uint32_t pa[ATT_BK / 16][4];
+#pragma unroll
+    for (int nb = 0; nb < ATT_BK / 8; ++nb) {
+      const float p0 = exp2f(sacc[nb][0] - m0), p1 = exp2f(sacc[nb][1] - m0);
+      const float p2 = exp2f(sacc[nb][2] - m1), p3 = exp2f(sacc[nb][3] - m1);
+      l0 += p0 + p1;
+      l1 += p2 + p3;
+      const int kk = nb >> 1, hi = nb & 1;
+      pa[kk][hi ? 2 : 0] = pack_bf16(p0, p1);
+      pa[kk][hi ? 3 : 1] = pack_bf16(p2, p3);
+    }
+    // O += P V: B fragments of V (k = key, n = d) via ldmatrix.trans
+#pragma unroll
+    for (int kk = 0; kk < ATT_BK / 16; ++kk) {
+#pragma unroll
+      for (int nb = 0; nb < ATT_D / 8; nb += 2) {
+        // matrices: (keys kk*16+0..7, d nb*8..), (keys +8..15, d nb*8..),
+        //           (keys kk*16+0..7, d (nb+1)*8..), (keys +8..15, d (nb+1)*8..)
+        const int mi = lane >> 3, r = lane & 7;
+        const int key = kk * 16 + (mi & 1) * 8 + r;
+        const int dcol = (nb + (mi >> 1)) * 8;
+        uint32_t bv[4];
+        ldmatrix_x4_trans(bv, &Vs[key][dcol]);
+        mma_bf16_16816(oacc[nb], pa[kk], bv[0], bv[1]);
+        mma_bf16_16816(oacc[nb + 1], pa[kk], bv[2], bv[3]);
+      }
+    }
+  }
+#pragma unroll
+  for (int sh = 1; sh <= 2; sh <<= 1) {
+    l0 += __shfl_xor_sync(0xffffffffu, l0, sh);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, sh);
+  }
+  const float i0 = 1.0f / l0, i1 = 1.0f / l1;
+  __nv_bfloat16* o0 = o + (qrow0 + g) * ldq + hq * ATT_D + 2 * c;
+  __nv_bfloat16* o1 = o0 + 8 * ldq;
+#pragma unroll
+  for (int nb = 0; nb < ATT_D / 8; ++nb) {
+    *reinterpret_cast<uint32_t*>(o0 + nb * 8) = pack_bf16(oacc[nb][0] * i0, oacc[nb][1] * i0);
+    *reinterpret_cast<uint32_t*>(o1 + nb * 8) = pack_bf16(oacc[nb][2] * i1, oacc[nb][3] * i1);
+  }
+}
+
+cudaError_t launch_attn_fwd(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
+                            __nv_bfloat16* o, long long N, int T, int Hq, int Hkv,
+                            cudaStream_t s) {
+  if (N == 0) return cudaSuccess;
+  const float scale_log2 = 1.4426950408889634f / sqrtf((float)ATT_D);
+  dim3 grid(T / ATT_BQ, Hq, (unsigned)(N / T));
+  attn_fwd_kernel<<<grid, 128, 0, s>>>(q, k, v, o, T, Hq, Hkv, scale_log2);
+  return cudaGetLastError();
+}
+
+}  // namespace ee

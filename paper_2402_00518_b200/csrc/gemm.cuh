@@ -41,6 +41,7 @@ enum EpiKind : int {
   EPI_CE_STATS = 4,    // per-row (max, sum exp, argmax) of the tile + target logit
   EPI_CE_DS = 5,       // dS = coef * (exp(S - lse) - onehot(y)) -> bf16
   EPI_F32T = 6,        // out^T: out[n][m] = acc (or +=), columns n >= n_split go to out1
+  EPI_BF16 = 7,        // outb[m][n] = bf16(acc)   (backbone projections)
 };
 
 enum BMode : int {
@@ -67,6 +68,7 @@ struct GemmArgs {
   int accumulate;
   const __nv_bfloat16* resid;
   long long ld_resid;
+  __nv_bfloat16* outb;  // EPI_BF16 output (ldo)
   // SwiGLU
   __nv_bfloat16* ab;  // [M x 2F]: A in columns [0,F), B in [F,2F)
   long long ld_ab;
@@ -159,6 +161,32 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
           } else {
             *reinterpret_cast<float4*>(orow + gn) = make_float4(o[0], o[1], o[2], o[3]);
             if (full8) *reinterpret_cast<float4*>(orow + gn + 4) = make_float4(o[4], o[5], o[6], o[7]);
+          }
+        }
+      }
+    }
+  } else if constexpr (EPI == EPI_BF16) {
+    __nv_bfloat16* orow = row_ok ? args.outb + (long long)gm * args.ldo : nullptr;
+#pragma unroll 1
+    for (int c = 0; c < GEMM_BN / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tb + c * 32, v);
+      tmem_ld_wait();
+      const int gn0 = nb * GEMM_BN + c * 32;
+      if (row_ok && gn0 < args.N) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 16) {
+          if (gn0 + j >= args.N) continue;
+          uint32_t w[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) w[q] = pack_bf16(u2f(v[j + 2 * q]), u2f(v[j + 2 * q + 1]));
+          __nv_bfloat16* p = orow + gn0 + j;
+          if (gn0 + j + 16 <= args.N && aligned32(p)) {
+            st_global_v8(p, w);
+          } else {
+            *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+            if (gn0 + j + 8 < args.N)
+              *reinterpret_cast<uint4*>(p + 8) = make_uint4(w[4], w[5], w[6], w[7]);
           }
         }
       }

@@ -82,6 +82,13 @@ cudaError_t launch_transpose_bf16(const __nv_bfloat16* src, __nv_bfloat16* dst, 
 cudaError_t launch_first_exit(const float* const* conf, int E, long long n, float tau,
                               int32_t* out, cudaStream_t s);
 
+// backbone partial forward (backbone.cu)
+cudaError_t launch_rope(__nv_bfloat16* x, long long N, int H, int T, float theta, cudaStream_t s);
+cudaError_t launch_attn_fwd(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
+                            __nv_bfloat16* o, long long N, int T, int Hq, int Hkv, cudaStream_t s);
+cudaError_t launch_cast_bf16_f32(const __nv_bfloat16* a, float* b, long long n, cudaStream_t s);
+cudaError_t launch_cast_f32_bf16(const float* a, __nv_bfloat16* b, long long n, cudaStream_t s);
+
 // optimizer / init
 cudaError_t launch_adam(float* theta, __nv_bfloat16* op_bf16, float* op_f32, const float* grad,
                         float* m, float* v, long long n, float lr, float b1, float b2, float eps,
