@@ -329,6 +329,18 @@ int64_t ee_launch_count(void);
 ee_status ee_test_gemm(int32_t a_kmajor, int32_t b_kmajor, const void* A, const void* B, float* C,
                        int32_t M, int32_t N, int32_t K, int32_t accumulate, void* stream);
 
+/* ---- testing hook: the causal GQA attention kernels of the backbone / the
+ * Layer exit (Llama-2 attention; head dim 128).  q [n x Hq*128],
+ * k, v [n x Hkv*128], o [n x Hq*128] bf16 row-major (row = sequence * T + t,
+ * no RoPE applied here); lse2 [n x Hq] fp32 out = log2-domain row statistics
+ * (max + log2 sum of 2^(s/sqrt(d) * log2 e)).  If dout != NULL the backward
+ * also runs: dq, dk, dv (shapes of q, k, v, bf16) and scratch fp32 [n x Hq].
+ * seq_len a multiple of 64 dividing n; n_heads a multiple of n_kv_heads. */
+ee_status ee_test_attention(const void* q, const void* k, const void* v, void* o, float* lse2,
+                            const void* dout, void* dq, void* dk, void* dv, float* scratch,
+                            int64_t n_tokens, int32_t seq_len, int32_t n_heads, int32_t n_kv_heads,
+                            void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -32,7 +32,7 @@ EXPORTED = ("ee_workspace_size", "ee_init_heads", "ee_tune_step", "ee_count_vali
             "ee_version", "ee_test_gemm", "ee_profile_start", "ee_profile_stop",
             "ee_profile_record", "ee_launch_count", "ee_vp_exit_forward", "ee_vp_vocab_stats",
             "ee_vp_rescale", "ee_vp_vocab_backward", "ee_vp_exit_backward", "ee_exit_infer",
-            "ee_backbone_workspace_size", "ee_backbone_forward")
+            "ee_backbone_workspace_size", "ee_backbone_forward", "ee_test_attention")
 
 
 class EEError(RuntimeError):
@@ -101,6 +101,7 @@ def load(path: str = LIB_PATH):
         "ee_last_error": (ctypes.c_char_p, []),
         "ee_version": (ctypes.c_char_p, []),
         "ee_test_gemm": (I32, [I32, I32, P, P, P, I32, I32, I32, I32, P]),
+        "ee_test_attention": (I32, [P, P, P, P, P, P, P, P, P, P, I64, I32, I32, I32, P]),
         "ee_profile_start": (I32, []),
         "ee_profile_stop": (I32, [ctypes.POINTER(I32)]),
         "ee_profile_record": (I32, [I32, ctypes.c_char_p, I32, ctypes.POINTER(F32),
@@ -291,6 +292,14 @@ def ee_test_gemm(A, B, C, a_kmajor, b_kmajor, M, N, K, accumulate=False, stream=
     load()
     _check(_lib.ee_test_gemm(int(a_kmajor), int(b_kmajor), _ptr(A), _ptr(B), _ptr(C), M, N, K,
                              int(bool(accumulate)), _stream(stream)))
+
+
+def ee_test_attention(q, k, v, o, lse2, seq_len, n_heads, n_kv_heads, dout=None, dq=None,
+                      dk=None, dv=None, scratch=None, stream=None):
+    load()
+    _check(_lib.ee_test_attention(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse2), _ptr(dout),
+                                  _ptr(dq), _ptr(dk), _ptr(dv), _ptr(scratch), q.shape[0],
+                                  seq_len, n_heads, n_kv_heads, _stream(stream)))
 
 
 def _aux1(aux):

@@ -727,7 +727,7 @@ ee_status ee_backbone_forward(const ee_backbone_config* cfg, const ee_layer_tens
     EE_CUDA(launch_rope(k, n, Hkv, cfg->seq_len, cfg->rope_theta, st)); }
     { const double fl = 2.0 * 2.0 * (double)n * (cfg->seq_len + 64) / 2.0 * h;  // causal
       Prof p_("bb_attention", st, fl, fl, 0);
-      EE_CUDA(launch_attn_fwd(q, k, v, o, n, cfg->seq_len, Hq, Hkv, st)); }
+      EE_CUDA(launch_attn_fwd(q, k, v, o, n, cfg->seq_len, Hq, Hkv, nullptr, st)); }
     {  // x += o W_o^T
       GemmArgs a = base_args((int)n, h, h);
       a.out0 = x;
@@ -1126,6 +1126,33 @@ void ee_debug_trace_arm(void) { debug_trace_arm(); }
 int32_t ee_debug_trace_read(uint64_t* host, int32_t max) {
   cudaDeviceSynchronize();
   return debug_trace_read((unsigned long long*)host, max);
+}
+
+// Testing hook: causal GQA attention forward (o, lse2) and backward (dq, dk, dv)
+// on q [N x Hq*128], k, v [N x Hkv*128] bf16 (RoPE not applied).  dout may be
+// NULL (forward only).  scratch: fp32 [N*Hq] for rowsum(dO*O).
+ee_status ee_test_attention(const void* q, const void* k, const void* v, void* o, float* lse2,
+                            const void* dout, void* dq, void* dk, void* dv, float* scratch,
+                            int64_t n_tokens, int32_t seq_len, int32_t n_heads, int32_t n_kv_heads,
+                            void* stream) {
+  if (!q || !k || !v || !o || !lse2 || n_tokens < 0 || seq_len < 64 || seq_len % 64 ||
+      n_tokens % seq_len || n_heads < 1 || n_kv_heads < 1 || n_heads % n_kv_heads)
+    return fail(EE_ERR_ARG, "bad ee_test_attention arguments");
+  ee_status s = check_device();
+  if (s != EE_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  EE_CUDA(launch_attn_fwd((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
+                          (const __nv_bfloat16*)v, (__nv_bfloat16*)o, n_tokens, seq_len, n_heads,
+                          n_kv_heads, lse2, st));
+  if (dout) {
+    if (!dq || !dk || !dv || !scratch) return fail(EE_ERR_ARG, "backward outputs NULL");
+    EE_CUDA(launch_attn_bwd((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
+                            (const __nv_bfloat16*)v, (const __nv_bfloat16*)o,
+                            (const __nv_bfloat16*)dout, lse2, scratch, (__nv_bfloat16*)dq,
+                            (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, n_tokens, seq_len, n_heads,
+                            n_kv_heads, st));
+  }
+  return EE_OK;
 }
 
 // Testing hook: C[M x N] (fp32, row-major) (+)= A B^T with A stored [M x K]

@@ -85,7 +85,14 @@ cudaError_t launch_first_exit(const float* const* conf, int E, long long n, floa
 // backbone partial forward (backbone.cu)
 cudaError_t launch_rope(__nv_bfloat16* x, long long N, int H, int T, float theta, cudaStream_t s);
 cudaError_t launch_attn_fwd(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
-                            __nv_bfloat16* o, long long N, int T, int Hq, int Hkv, cudaStream_t s);
+                            __nv_bfloat16* o, long long N, int T, int Hq, int Hkv, float* lse2,
+                            cudaStream_t s);
+cudaError_t launch_attn_bwd(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
+                            const __nv_bfloat16* o, const __nv_bfloat16* dout, const float* lse2,
+                            float* Dv, __nv_bfloat16* dq, __nv_bfloat16* dk, __nv_bfloat16* dv,
+                            long long N, int T, int Hq, int Hkv, cudaStream_t s);
+cudaError_t launch_rope_bwd(__nv_bfloat16* x, long long N, int H, int T, float theta,
+                            cudaStream_t s);
 cudaError_t launch_cast_bf16_f32(const __nv_bfloat16* a, float* b, long long n, cudaStream_t s);
 cudaError_t launch_cast_f32_bf16(const float* a, __nv_bfloat16* b, long long n, cudaStream_t s);
 
