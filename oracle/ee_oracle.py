@@ -13,6 +13,11 @@ section they fall in; "A<n>" are the readings listed in DESIGN.md §3):
   ``norm``:      z = RMSNorm_f(x) (P:207-208; RMSNorm used in experiments P:464);
   ``mlp``:       y = x + MLP(RMSNorm_a(x)), z = RMSNorm_f(y) (P:209, pre-norm
                  residual structure P:165-166; SwiGLU MLP as in Llama-2, A2).
+  ``layer``:     "a complete Transformer layer, with the same structure as those
+                 on the backbone, ... in front of the Norm architecture":
+                 x1 = x + W_o attn(RoPE(W_q u1), RoPE(W_k u1), W_v u1),
+                 u1 = RMSNorm_att(x); then the MLP exit on x1 (Llama-2 layer,
+                 P:356-358; causal attention within each sequence of T tokens).
 * loss: next-token negative log-likelihood (§2 "Preliminaries"),
   averaged over valid tokens (A4), ignore_index -1 (A6).
 * exits are independent; the backbone is frozen, so gradients flow into the
@@ -39,7 +44,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-ARCHS = ("embedding", "norm", "mlp")
+ARCHS = ("embedding", "norm", "mlp", "layer")
+MLP_BODY = ("mlp", "layer")
 IGNORE_INDEX = -1
 
 
@@ -101,27 +107,35 @@ def _need(params: dict, names, arch):
             raise ValueError(f"arch {arch!r} requires parameter {n!r}")
 
 
-def exit_forward(arch: str, params: dict, x: np.ndarray, eps: float) -> dict:
+def exit_forward(arch: str, params: dict, x: np.ndarray, eps: float, attn: dict | None = None) -> dict:
     """Forward of one exit head up to the logits S = z W_out^T.
 
-    params (fp64 numpy): w_out [V,h]; norm/mlp: g_f [h];
-    mlp: g_a [h], w_gate [F,h], w_up [F,h], w_down [h,F].
+    params (fp64 numpy): w_out [V,h]; norm/mlp/layer: g_f [h];
+    mlp/layer: g_a [h], w_gate [F,h], w_up [F,h], w_down [h,F];
+    layer: g_att [h], w_q [Hq d, h], w_k, w_v [Hkv d, h], w_o [h, Hq d].
+    attn (layer only): seq_len T, n_heads Hq, n_kv Hkv, theta (RoPE base).
     """
     if arch not in ARCHS:
         raise ValueError(f"unknown arch {arch!r}")
     _need(params, ["w_out"], arch)
     act = {"x": x}
-    y = x
-    if arch == "mlp":
+    xin = x
+    if arch == "layer":
+        _need(params, ["g_att", "w_q", "w_k", "w_v", "w_o"], arch)
+        if attn is None:
+            raise ValueError("arch 'layer' needs attn = {seq_len, n_heads, n_kv, theta}")
+        xin = _attention_block_forward(params, x, eps, attn, act)
+    y = xin
+    if arch in MLP_BODY:
         _need(params, ["g_a", "w_gate", "w_up", "w_down"], arch)
-        u, r_x, xhat = rmsnorm(x, params["g_a"], eps)       # pre-norm (P:166)
+        u, r_x, xhat = rmsnorm(xin, params["g_a"], eps)     # pre-norm (P:166)
         A = u @ params["w_gate"].T
         B = u @ params["w_up"].T
         M = silu(A) * B                                     # SwiGLU (A2)
-        y = x + M @ params["w_down"].T                      # residual (P:166)
+        y = xin + M @ params["w_down"].T                    # residual (P:166)
         act.update(u=u, r_x=r_x, xhat=xhat, A=A, B=B, M=M)
     act["y"] = y
-    if arch in ("norm", "mlp"):
+    if arch != "embedding":
         _need(params, ["g_f"], arch)
         z, r_y, yhat = rmsnorm(y, params["g_f"], eps)       # Norm exit (P:207)
         act.update(r_y=r_y, yhat=yhat)
@@ -130,6 +144,74 @@ def exit_forward(arch: str, params: dict, x: np.ndarray, eps: float) -> dict:
     act["z"] = z
     act["S"] = z @ params["w_out"].T                        # output embedding
     return act
+
+
+def _attention_block_forward(params: dict, x: np.ndarray, eps: float, attn: dict,
+                             act: dict) -> np.ndarray:
+    """Attention half of the Layer exit (Llama-2 layer P:356-358):
+    x1 = x + W_o softmax(q k^T / sqrt(d) + causal) v with q, k rotated by RoPE at
+    the token's position within its sequence (row % T).  Keeps q, k (rotated),
+    v, the attention probabilities P and o for the backward."""
+    T, Hq, Hkv = int(attn["seq_len"]), int(attn["n_heads"]), int(attn["n_kv"])
+    theta = float(attn.get("theta", 10000.0))
+    N, h = x.shape
+    if N % T:
+        raise ValueError("Layer exit: tokens must be whole sequences of seq_len")
+    d = params["w_q"].shape[0] // Hq
+    pos = np.arange(N) % T
+    u1, r1, xh1 = rmsnorm(x, params["g_att"], eps)
+    q = rope((u1 @ params["w_q"].T).reshape(N, Hq, d), pos, theta)
+    k = rope((u1 @ params["w_k"].T).reshape(N, Hkv, d), pos, theta)
+    v = (u1 @ params["w_v"].T).reshape(N, Hkv, d)
+    P = attention_probs(q, k, T)                                    # [B, Hq, T, T]
+    g = Hq // Hkv
+    o = np.zeros((N, Hq, d))
+    for b in range(N // T):
+        rs = slice(b * T, (b + 1) * T)
+        for j in range(Hq):
+            o[rs, j, :] = P[b, j] @ v[rs, j // g, :]
+    o = o.reshape(N, Hq * d)
+    x1 = x + o @ params["w_o"].T                                    # residual (P:166)
+    act.update(u1=u1, r1=r1, xh1=xh1, q=q, k=k, v=v, P=P, o=o, x1=x1, pos=pos, theta=theta,
+               T=T)
+    return x1
+
+
+def attention_probs(q: np.ndarray, k: np.ndarray, T: int) -> np.ndarray:
+    """P[b, j] = softmax over keys s <= t of q_t . k_s / sqrt(d) (causal), per
+    sequence b and query head j (GQA: kv head j // (Hq / Hkv))."""
+    N, Hq, d = q.shape
+    g = Hq // k.shape[1]
+    P = np.zeros((N // T, Hq, T, T))
+    mask = np.triu(np.ones((T, T), dtype=bool), 1)
+    for b in range(N // T):
+        rs = slice(b * T, (b + 1) * T)
+        for j in range(Hq):
+            S = q[rs, j, :] @ k[rs, j // g, :].T / math.sqrt(d)
+            S = np.where(mask, -np.inf, S)
+            E = np.exp(S - S.max(axis=1, keepdims=True))
+            P[b, j] = E / E.sum(axis=1, keepdims=True)
+    return P
+
+
+def attention_backward(q, k, v, P, do, T):
+    """Backward of o = P v with P = softmax(q k^T / sqrt(d) + causal):
+    dv = P^T do;  dP = do v^T;  dS = P * (dP - rowsum(dP * P));
+    dq = dS k / sqrt(d);  dk = dS^T q / sqrt(d)  (summed over a GQA group)."""
+    N, Hq, d = q.shape
+    g = Hq // k.shape[1]
+    dq, dk, dv = np.zeros_like(q), np.zeros_like(k), np.zeros_like(v)
+    c = 1.0 / math.sqrt(d)
+    for b in range(N // T):
+        rs = slice(b * T, (b + 1) * T)
+        for j in range(Hq):
+            Pj = P[b, j]
+            dv[rs, j // g, :] += Pj.T @ do[rs, j, :]
+            dP = do[rs, j, :] @ v[rs, j // g, :].T
+            dS = Pj * (dP - np.sum(dP * Pj, axis=1, keepdims=True))
+            dq[rs, j, :] = c * (dS @ k[rs, j // g, :])
+            dk[rs, j // g, :] += c * (dS.T @ q[rs, j, :])
+    return dq, dk, dv
 
 
 # ----------------------------------------------------------------------------
@@ -172,7 +254,8 @@ class ExitResult:
 
 def exit_loss_and_grads(arch: str, params: dict, x: np.ndarray, targets: np.ndarray,
                         alpha: float, eps: float, valid_count: int | None = None,
-                        keep_act: bool = False, weighting="uniform") -> ExitResult:
+                        keep_act: bool = False, weighting="uniform",
+                        attn: dict | None = None) -> ExitResult:
     """Loss and parameter gradients of one exit.
 
     ``valid_count`` is W, the normaliser of the mean over valid tokens; it
@@ -187,7 +270,7 @@ def exit_loss_and_grads(arch: str, params: dict, x: np.ndarray, targets: np.ndar
     of per-token constants.  Non-uniform weights are normalised by their sum
     over valid tokens (A17); ``valid_count`` then does not apply.
     """
-    act = exit_forward(arch, params, x, eps)
+    act = exit_forward(arch, params, x, eps, attn)
     st = lm_loss_stats(act["S"], targets)
     w = st["valid"].astype(np.float64)
     if isinstance(weighting, str) and weighting == "uniform":
@@ -213,7 +296,7 @@ def exit_loss_and_grads(arch: str, params: dict, x: np.ndarray, targets: np.ndar
     dS = (alpha * w / W)[:, None] * (P - onehot)
 
     grads["w_out"] = dS.T @ z                               # dW_out = dS^T z
-    if arch in ("norm", "mlp"):
+    if arch != "embedding":
         dz = dS @ params["w_out"]                           # dz = dS W_out
         grads.update(exit_body_backward(arch, params, act, dz))
     return ExitResult(loss, grads, st, act if keep_act else {})
@@ -221,12 +304,13 @@ def exit_loss_and_grads(arch: str, params: dict, x: np.ndarray, targets: np.ndar
 
 def exit_body_backward(arch: str, params: dict, act: dict, dz: np.ndarray) -> dict:
     """Gradients of the exit body below W_out given dz = dL/dz: the
-    final RMSNorm gain and, for MLP exits, the SwiGLU MLP and its pre-norm gain.
-    No gradient w.r.t. the exit input x (frozen backbone)."""
+    final RMSNorm gain and, for MLP exits, the SwiGLU MLP and its pre-norm gain;
+    for Layer exits also the attention block.  No gradient w.r.t. the exit input
+    x (frozen backbone)."""
     grads = {}
     dy, dg_f = rmsnorm_backward(dz, act["yhat"], act["r_y"], params["g_f"])
     grads["g_f"] = dg_f
-    if arch == "mlp":
+    if arch in MLP_BODY:
         M, A, B, u = act["M"], act["A"], act["B"], act["u"]
         grads["w_down"] = dy.T @ M                          # dW_down = dy^T M
         dM = dy @ params["w_down"]
@@ -237,11 +321,37 @@ def exit_body_backward(arch: str, params: dict, act: dict, dz: np.ndarray) -> di
         du = dA @ params["w_gate"] + dB @ params["w_up"]
         # u = g_a * xhat  =>  dg_a = sum_t du_t * xhat_t; no dx (frozen backbone)
         grads["g_a"] = np.sum(du * act["xhat"], axis=0)
+    if arch == "layer":
+        # through the MLP's pre-norm and residual into x1, then the attention block
+        dxn, _ = rmsnorm_backward(du, act["xhat"], act["r_x"], params["g_a"])
+        dx1 = dy + dxn
+        grads.update(_attention_block_backward(params, act, dx1))
+    return grads
+
+
+def _attention_block_backward(params: dict, act: dict, dx1: np.ndarray) -> dict:
+    """Gradients of x1 = x + W_o attn(...) w.r.t. g_att, W_q, W_k, W_v, W_o
+    given dx1 (no gradient w.r.t. x: frozen backbone)."""
+    N = dx1.shape[0]
+    q, k, v = act["q"], act["k"], act["v"]
+    grads = {"w_o": dx1.T @ act["o"]}                               # dW_o = dx1^T o
+    do = (dx1 @ params["w_o"]).reshape(q.shape)
+    dq, dk, dv = attention_backward(q, k, v, act["P"], do, act["T"])
+    # RoPE is a rotation: its backward rotates by the opposite angle
+    dq = rope(dq, -act["pos"], act["theta"]).reshape(N, -1)
+    dk = rope(dk, -act["pos"], act["theta"]).reshape(N, -1)
+    dv = dv.reshape(N, -1)
+    u1 = act["u1"]
+    grads["w_q"] = dq.T @ u1
+    grads["w_k"] = dk.T @ u1
+    grads["w_v"] = dv.T @ u1
+    du1 = dq @ params["w_q"] + dk @ params["w_k"] + dv @ params["w_v"]
+    grads["g_att"] = np.sum(du1 * act["xh1"], axis=0)
     return grads
 
 
 def tune_step(arch: str, params_list, hidden_list, targets, exit_weights, eps: float,
-              valid_count: int | None = None):
+              valid_count: int | None = None, attn: dict | None = None):
     """All exits of one step: exits are independent.
 
     Returns (losses [E] (unweighted L_i), grads list, stats list).
@@ -252,14 +362,15 @@ def tune_step(arch: str, params_list, hidden_list, targets, exit_weights, eps: f
     losses, grads, stats = [], [], []
     for i in range(E):
         r = exit_loss_and_grads(arch, params_list[i], hidden_list[i], targets,
-                                float(exit_weights[i]), eps, valid_count)
+                                float(exit_weights[i]), eps, valid_count, attn=attn)
         losses.append(r.loss)
         grads.append(r.grads)
         stats.append(r.stats)
     return np.array(losses), grads, stats
 
 
-def exit_infer(arch: str, params_list, hidden_list, threshold: float, eps: float):
+def exit_infer(arch: str, params_list, hidden_list, threshold: float, eps: float,
+               attn: dict | None = None):
     """Confidence-based early exit at inference (§3 "Inference"):
     per exit the greedy token (argmax) and confidence (max softmax prob); a
     token exits at the first exit whose confidence reaches the threshold
@@ -267,7 +378,7 @@ def exit_infer(arch: str, params_list, hidden_list, threshold: float, eps: float
     conf [E,N], first_exit [N], -1 = no early exit)."""
     am, cf = [], []
     for p, x in zip(params_list, hidden_list):
-        S = exit_forward(arch, p, x, eps)["S"]
+        S = exit_forward(arch, p, x, eps, attn)["S"]
         st = lm_loss_stats(S, np.full(S.shape[0], IGNORE_INDEX))
         am.append(st["argmax"])
         cf.append(st["conf"])
@@ -336,14 +447,17 @@ def init_copy(arch: str, backbone: dict, after_layer: int) -> dict:
     backbone: ``final_norm`` [h], ``w_out`` [V,h], ``layers``: list of dicts with
     ``mlp_norm`` [h] (pre-MLP norm gain), ``w_gate``, ``w_up``, ``w_down``.
     Embedding/Norm copy the final-exit layer's modules; MLP copies the
-    MLP of the same layer plus its pre-MLP norm gain (A10).
+    MLP of the same layer plus its pre-MLP norm gain (A10); Layer copies
+    "the last Transformer layer of the original LLM" whatever the exit's
+    position -- its attention (``g_att``, ``w_q``, ``w_k``, ``w_v``, ``w_o``)
+    and MLP (``mlp_norm`` -> g_a, ``w_gate``, ``w_up``, ``w_down``).
     """
     if arch not in ARCHS:
         raise ValueError(f"unknown arch {arch!r}")
     if backbone.get("w_out") is None:
         raise LookupError("structure error: backbone has no output embedding")
     p = {"w_out": np.array(backbone["w_out"], copy=True)}
-    if arch in ("norm", "mlp"):
+    if arch != "embedding":
         if backbone.get("final_norm") is None:
             raise LookupError("structure error: backbone has no final norm")
         p["g_f"] = np.array(backbone["final_norm"], copy=True)
@@ -356,6 +470,17 @@ def init_copy(arch: str, backbone: dict, after_layer: int) -> dict:
                              ("w_up", "w_up"), ("w_down", "w_down")):
             if L.get(k_bb) is None:
                 raise LookupError(f"structure error: layer {after_layer} has no {k_bb}")
+            p[k_exit] = np.array(L[k_bb], copy=True)
+    if arch == "layer":
+        layers = backbone.get("layers") or []
+        if not layers or layers[-1] is None:
+            raise LookupError("structure error: backbone has no last layer to copy")
+        L = layers[-1]
+        for k_exit, k_bb in (("g_att", "g_att"), ("w_q", "w_q"), ("w_k", "w_k"), ("w_v", "w_v"),
+                             ("w_o", "w_o"), ("g_a", "mlp_norm"), ("w_gate", "w_gate"),
+                             ("w_up", "w_up"), ("w_down", "w_down")):
+            if L.get(k_bb) is None:
+                raise LookupError(f"structure error: last layer has no {k_bb}")
             p[k_exit] = np.array(L[k_bb], copy=True)
     return p
 

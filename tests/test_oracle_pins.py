@@ -28,14 +28,33 @@ def _rng(seed):
 
 def _params(arch, h, V, F, rng, w_std=0.5):
     p = {"w_out": rng.normal(0, w_std, (V, h))}
-    if arch in ("norm", "mlp"):
+    if arch != "embedding":
         p["g_f"] = 1.0 + 0.1 * rng.normal(size=h)
-    if arch == "mlp":
+    if arch in ("mlp", "layer"):
         p["g_a"] = 1.0 + 0.1 * rng.normal(size=h)
         p["w_gate"] = rng.normal(0, w_std, (F, h))
         p["w_up"] = rng.normal(0, w_std, (F, h))
         p["w_down"] = rng.normal(0, w_std, (h, F))
+    if arch == "layer":   # 2 query heads sharing 1 kv head (GQA), d = h / 2
+        p["g_att"] = 1.0 + 0.1 * rng.normal(size=h)
+        p["w_q"] = rng.normal(0, w_std, (h, h))
+        p["w_k"] = rng.normal(0, w_std, (h // 2, h))
+        p["w_v"] = rng.normal(0, w_std, (h // 2, h))
+        p["w_o"] = rng.normal(0, w_std, (h, h))
     return p
+
+
+def _attn(arch, N, T=None):
+    """Attention geometry of the test Layer exits: 2 heads, 1 kv head, and
+    sequences of T tokens (default: two sequences when N is even)."""
+    if arch != "layer":
+        return None
+    T = T or (N // 2 if N % 2 == 0 else N)
+    return {"seq_len": T, "n_heads": 2, "n_kv": 1, "theta": 10000.0}
+
+
+def _elg(arch, p, x, y, alpha, eps, **kw):
+    return O.exit_loss_and_grads(arch, p, x, y, alpha, eps, attn=_attn(arch, x.shape[0]), **kw)
 
 
 # --------------------------------------------------------------------------- P1, P2
@@ -81,7 +100,7 @@ def test_P3_uniform_logits_closed_form(arch):
     y = rng.integers(0, V, N)
     y[3] = -1
     alpha = 0.7
-    r = O.exit_loss_and_grads(arch, p, x, y, alpha, 1e-5, keep_act=True)
+    r = _elg(arch, p, x, y, alpha, 1e-5, keep_act=True)
     assert r.loss == pytest.approx(math.log(512), rel=1e-15)       # ln V
     assert math.log(512) == pytest.approx(6.238324625039508, rel=1e-15)
     np.testing.assert_allclose(r.stats["conf"], 1.0 / V, rtol=1e-14)
@@ -93,7 +112,7 @@ def test_P3_uniform_logits_closed_form(arch):
     expect = alpha / W * ((w[:, None] * (1.0 / V - onehot)).T @ r.act["z"])
     np.testing.assert_allclose(r.grads["w_out"], expect, rtol=1e-12, atol=1e-15)
     # dz = dS W_out = 0 exactly, so every gradient below W_out is exactly zero.
-    for k in ("g_f", "g_a", "w_gate", "w_up", "w_down"):
+    for k in ("g_f", "g_a", "w_gate", "w_up", "w_down", "g_att", "w_q", "w_k", "w_v", "w_o"):
         if k in r.grads:
             assert np.all(r.grads[k] == 0.0), k
 
@@ -113,7 +132,7 @@ def test_P4_softmax_ce_gradient_rows_sum_to_zero(arch):
     p = _params(arch, h, V, F, rng)
     x = rng.normal(size=(N, h))
     y = rng.integers(0, V, N)
-    r = O.exit_loss_and_grads(arch, p, x, y, 1.3, 1e-5)
+    r = _elg(arch, p, x, y, 1.3, 1e-5)
     col = r.grads["w_out"].sum(axis=0)
     assert np.max(np.abs(col)) <= 1e-13 * np.max(np.abs(r.grads["w_out"])) * V
 
@@ -141,10 +160,10 @@ def test_P6_central_finite_differences(arch):
     x = rng.normal(size=(N, h))
     y = np.array([3, -1, 15, 0])
     alpha, eps = 0.8, 1e-5
-    r = O.exit_loss_and_grads(arch, p, x, y, alpha, eps)
+    r = _elg(arch, p, x, y, alpha, eps)
 
     def f(pp):
-        return alpha * O.exit_loss_and_grads(arch, pp, x, y, alpha, eps).loss
+        return alpha * _elg(arch, pp, x, y, alpha, eps).loss
 
     step = 1e-6
     for name, val in p.items():
@@ -225,16 +244,33 @@ def test_P8_P9_against_torch_library_and_autograd(arch):
     y = rng.integers(0, V, N)
     y[[2, 11]] = -1
     alpha, eps = 1.7, 1e-5
-    r = O.exit_loss_and_grads(arch, p, x, y, alpha, eps, keep_act=True)
+    r = _elg(arch, p, x, y, alpha, eps, keep_act=True)
 
     tp = {k: torch.tensor(v, requires_grad=True) for k, v in p.items()}
     tx = torch.tensor(x)
     t = tx
-    if arch == "mlp":
+    if arch == "layer":  # F.scaled_dot_product_attention (causal, GQA); RoPE rotate-half
+        T, d = N // 2, h // 2
+        u = Fn.rms_norm(tx, (h,), tp["g_att"], eps)
+        pos = torch.arange(N) % T
+        inv = 10000.0 ** (-torch.arange(d // 2, dtype=torch.float64) * 2 / d)
+        ang = pos[:, None].double() * inv[None]
+
+        def rot(zz):
+            z1, z2 = zz[..., :d // 2], zz[..., d // 2:]
+            c, s_ = torch.cos(ang)[:, None], torch.sin(ang)[:, None]
+            return torch.cat([z1 * c - z2 * s_, z2 * c + z1 * s_], -1)
+        q = rot(Fn.linear(u, tp["w_q"]).view(N, 2, d)).view(2, T, 2, d).transpose(1, 2)
+        k = rot(Fn.linear(u, tp["w_k"]).view(N, 1, d)).view(2, T, 1, d).transpose(1, 2)
+        v = Fn.linear(u, tp["w_v"]).view(2, T, 1, d).transpose(1, 2)
+        o = Fn.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
+        tx = tx + Fn.linear(o.transpose(1, 2).reshape(N, h), tp["w_o"])
+        t = tx
+    if arch in ("mlp", "layer"):
         u = Fn.rms_norm(tx, (h,), tp["g_a"], eps)
         m = Fn.silu(Fn.linear(u, tp["w_gate"])) * Fn.linear(u, tp["w_up"])
         t = tx + Fn.linear(m, tp["w_down"])
-    if arch in ("norm", "mlp"):
+    if arch != "embedding":
         t = Fn.rms_norm(t, (h,), tp["g_f"], eps)
     logits = Fn.linear(t, tp["w_out"])
     loss = Fn.cross_entropy(logits, torch.tensor(y, dtype=torch.long), ignore_index=-1)
@@ -364,12 +400,12 @@ def test_confidence_weighting_detached_and_identity(arch):
     x = rng.normal(size=(N, h))
     y = np.array([3, -1, 15, 0, 7, 7])
     alpha, eps = 0.9, 1e-5
-    r_u = O.exit_loss_and_grads(arch, p, x, y, alpha, eps)
-    r_1 = O.exit_loss_and_grads(arch, p, x, y, alpha, eps, weighting=np.ones(N))
+    r_u = _elg(arch, p, x, y, alpha, eps)
+    r_1 = _elg(arch, p, x, y, alpha, eps, weighting=np.ones(N))
     assert r_1.loss == r_u.loss
     for k in p:
         assert np.array_equal(r_1.grads[k], r_u.grads[k]), k
-    r_c = O.exit_loss_and_grads(arch, p, x, y, alpha, eps, keep_act=True, weighting="confidence")
+    r_c = _elg(arch, p, x, y, alpha, eps, keep_act=True, weighting="confidence")
     c = softmax(r_c.act["S"], axis=1).max(axis=1)
     np.testing.assert_allclose(r_c.stats["conf"], c, rtol=1e-13)
     valid = y != -1
@@ -377,7 +413,7 @@ def test_confidence_weighting_detached_and_identity(arch):
     assert r_c.loss == pytest.approx(L_expect, rel=1e-13)
 
     def f(pp):  # c held fixed (detached)
-        return alpha * O.exit_loss_and_grads(arch, pp, x, y, alpha, eps, weighting=c).loss
+        return alpha * _elg(arch, pp, x, y, alpha, eps, weighting=c).loss
 
     step = 1e-6
     for name, val in p.items():
@@ -508,3 +544,80 @@ def test_backbone_partial_forward_structure():
     x_fut[T - 1] += 1.0                                               # change the last token
     np.testing.assert_array_equal(O.llama_layer_forward(layers[0], x_fut, T, nh, nkv, 1e-5)[:T - 1],
                                   x1[:T - 1])
+
+
+# --------------------------------------------------------------------------- NEXT #2: Layer exit
+def test_P10_layer_data_parallel_over_whole_sequences():
+    """Layer exits couple tokens within a sequence, so DP shards are whole
+    sequences; with the global W the shard gradients sum to the full batch's."""
+    rng = _rng(50)
+    h, V, F, T = 8, 30, 12, 5
+    N = 4 * T
+    p = _params("layer", h, V, F, rng)
+    x = rng.normal(size=(N, h))
+    y = rng.integers(0, V, N)
+    y[[0, 7, 13]] = -1
+    at = _attn("layer", N, T)
+    full = O.exit_loss_and_grads("layer", p, x, y, 0.9, 1e-5, attn=at)
+    W = int(np.sum(y != -1))
+    shards = [O.exit_loss_and_grads("layer", p, x[s], y[s], 0.9, 1e-5, valid_count=W, attn=at)
+              for s in (slice(0, T), slice(T, 3 * T), slice(3 * T, N))]
+    assert sum(s.loss for s in shards) == pytest.approx(full.loss, rel=1e-13)
+    for k in p:
+        np.testing.assert_allclose(sum(s.grads[k] for s in shards), full.grads[k], rtol=1e-10,
+                                   atol=1e-14, err_msg=k)
+
+
+def test_layer_exit_uniform_attention_closed_form():
+    """W_q = W_k = 0: every score is 0, so token t attends uniformly to the
+    t+1 positions s <= t of its own sequence: x1_t = x_t + W_o (mean_{s<=t} v_s)
+    per query head (GQA: both heads read kv head 0)."""
+    rng = _rng(51)
+    h, V, F, T = 8, 16, 12, 6
+    N = 2 * T
+    p = _params("layer", h, V, F, rng)
+    p["w_q"][:] = 0.0
+    p["w_k"][:] = 0.0
+    x = rng.normal(size=(N, h))
+    act = O.exit_forward("layer", p, x, 1e-5, _attn("layer", N, T))
+    u1 = O.rmsnorm(x, p["g_att"], 1e-5)[0]
+    v = u1 @ p["w_v"].T                                              # [N, d], one kv head
+    o = np.zeros((N, h))
+    for b in range(2):
+        for t in range(T):
+            m = v[b * T:b * T + t + 1].mean(axis=0)
+            o[b * T + t] = np.concatenate([m, m])                    # both query heads
+    np.testing.assert_allclose(act["x1"], x + o @ p["w_o"].T, rtol=1e-13, atol=1e-14)
+    np.testing.assert_allclose(act["x1"][0], x[0] + np.concatenate([v[0], v[0]]) @ p["w_o"].T,
+                               rtol=1e-13)                           # t = 0 sees only itself
+
+
+def test_layer_exit_copy_of_last_layer_skips_one_layer():
+    """P:237 + P:242: a Layer exit after layer L-1, initialised as a copy of the
+    last layer L (plus final norm and W_out), reproduces the original model's
+    output on the same input: the exit *is* layer L followed by the final head.
+    Cross-checks the exit's forward against llama_layer_forward (independent
+    code, pinned to torch SDPA above)."""
+    rng = _rng(52)
+    h, nh, nkv, F, T, V, Lyr = 16, 2, 1, 12, 5, 40, 3
+    layers = [_layer(rng, h, nh, nkv, F) for _ in range(Lyr)]
+    for L in layers:
+        L["mlp_norm"] = L["g_mlp"]
+    bb = {"final_norm": 1 + 0.1 * rng.normal(size=h), "w_out": rng.normal(0, 0.3, (V, h)),
+          "layers": layers}
+    x0 = rng.normal(size=(2 * T, h))
+    h_prev, h_last = O.backbone_forward(layers, x0, T, nh, nkv, [Lyr - 1, Lyr], 1e-5)
+    p = O.init_copy("layer", bb, after_layer=Lyr - 1)
+    assert np.array_equal(p["w_q"], layers[-1]["w_q"]) and not np.shares_memory(p["w_q"], layers[-1]["w_q"])
+    assert np.array_equal(p["g_a"], layers[-1]["g_mlp"])
+    at = {"seq_len": T, "n_heads": nh, "n_kv": nkv, "theta": 10000.0}
+    S_exit = O.exit_forward("layer", p, h_prev, 1e-5, at)["S"]
+    S_orig = O.original_final_logits(bb, h_last, 1e-5)
+    np.testing.assert_allclose(S_exit, S_orig, rtol=1e-12, atol=1e-12)
+    # copying is position-independent (always the LAST layer, P:237)
+    p1 = O.init_copy("layer", bb, after_layer=1)
+    assert all(np.array_equal(p1[k], p[k]) for k in p)
+    with pytest.raises(LookupError):
+        O.init_copy("layer", dict(bb, layers=[{k: v for k, v in layers[0].items() if k != "w_o"}]), 1)
+    with pytest.raises(ValueError):                                  # tokens not whole sequences
+        O.exit_forward("layer", p, h_prev[:7], 1e-5, at)
