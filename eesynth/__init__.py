@@ -30,6 +30,15 @@ CONFIGS = {
                 layers=80, after=[20, 40, 60, 80], init="copy", seed=3),
     "70b_dp": dict(hidden=8192, vocab=32000, ffn=28672, arch="mlp", tokens=32 * 2048,
                    layers=80, after=[10, 20, 30, 40, 50, 60, 70, 80], init="copy", seed=4),
+    # Layer exits (NEXT #2): a full Llama-2 layer per exit; tokens are
+    # whole sequences (causal attention within each).
+    "tiny_layer": dict(hidden=256, vocab=1000, ffn=384, arch="layer", tokens=2 * 128, layers=2,
+                       after=[1, 2], init="copy", seed=5, n_heads=2, n_kv_heads=1, seq_len=128),
+    # the paper's architecture comparison: 13B with 8 exits at 1/8 .. 8/8 depth
+    # (P:465), batch 16 x 2048
+    "13b_layer": dict(hidden=5120, vocab=32000, ffn=13824, arch="layer", tokens=16 * 2048,
+                      layers=40, after=[5, 10, 15, 20, 25, 30, 35, 40], init="copy", seed=6,
+                      n_heads=40, n_kv_heads=40, seq_len=2048),
 }
 
 MATRIX_STD = 0.02          # N(0, 0.02^2) weights (A12)
@@ -50,6 +59,9 @@ class Cfg:
     after: list
     init: str
     seed: int
+    n_heads: int = 0          # Layer exits: attention geometry (head dim 128)
+    n_kv_heads: int = 0
+    seq_len: int = 0
     exits: int = field(init=False)
 
     def __post_init__(self):
@@ -125,27 +137,55 @@ def head_params(cfg: Cfg, seed: int | None = None, device="cpu", w_out_std: floa
     h, V, F = cfg.hidden, cfg.vocab, cfg.ffn
     if w_out_std is None:
         w_out_std = (1.0 / h) ** 0.5 if cfg.name == "tiny" else MATRIX_STD
+    tiny = cfg.name.startswith("tiny")
+    mstd = (1.0 / h) ** 0.5 if tiny else MATRIX_STD
     res = []
     for i in range(cfg.exits):
         g = _gen(s * 1000 + 500 + i, device)
         p = {"w_out": _randn((V, h), g, device, std=w_out_std)}
-        if cfg.arch in ("norm", "mlp"):
+        if cfg.arch != "embedding":
             p["g_f"] = _randn((h,), g, device, std=GAIN_JITTER, mean=1.0)
-        if cfg.arch == "mlp":
+        if cfg.arch in ("mlp", "layer"):
             p["g_a"] = _randn((h,), g, device, std=GAIN_JITTER, mean=1.0)
-            p["w_gate"] = _randn((F, h), g, device, std=MATRIX_STD)
-            p["w_up"] = _randn((F, h), g, device, std=MATRIX_STD)
-            p["w_down"] = _randn((h, F), g, device, std=MATRIX_STD)
+            p["w_gate"] = _randn((F, h), g, device, std=mstd)
+            p["w_up"] = _randn((F, h), g, device, std=mstd)
+            p["w_down"] = _randn((h, F), g, device, std=mstd)
+        if cfg.arch == "layer":
+            p.update(_attn_params(cfg, g, device))
         for k in list(p):
             p[k] = p[k].to(torch.bfloat16).to(torch.float32)   # on the bf16 grid
         res.append(p)
     return res
 
 
+def _attn_params(cfg: Cfg, g, device):
+    """Attention tensors of a Layer exit / backbone layer.  tiny: W_q, W_k with
+    std 2/sqrt(h) (attention scores of std ~4: peaked, so the softmax backward
+    is exercised), W_v, W_o 1/sqrt(h); Llama-shaped: N(0, 0.02^2) (score std
+    ~2 at h = 5120)."""
+    h = cfg.hidden
+    hkv = 128 * (cfg.n_kv_heads or cfg.n_heads)
+    tiny = cfg.name.startswith("tiny")
+    sqk = 2.0 * (1.0 / h) ** 0.5 if tiny else MATRIX_STD
+    svo = (1.0 / h) ** 0.5 if tiny else MATRIX_STD
+    return {"g_att": _randn((h,), g, device, std=GAIN_JITTER, mean=1.0),
+            "w_q": _randn((h, h), g, device, std=sqk), "w_k": _randn((hkv, h), g, device, std=sqk),
+            "w_v": _randn((hkv, h), g, device, std=svo), "w_o": _randn((h, h), g, device, std=svo)}
+
+
+def attn_geometry(cfg: Cfg) -> dict | None:
+    """The oracle's `attn` argument for Layer exits (None otherwise)."""
+    if cfg.arch != "layer":
+        return None
+    return {"seq_len": cfg.seq_len, "n_heads": cfg.n_heads,
+            "n_kv": cfg.n_kv_heads or cfg.n_heads, "theta": 10000.0}
+
+
 def backbone(cfg: Cfg, seed: int | None = None, device="cpu"):
     """Synthetic frozen backbone views needed by Copy init (D8): the final norm
     gain, the final output embedding and, for each exit layer, that layer's MLP
-    and pre-MLP norm gain.  bf16 tensors (a Llama checkpoint is bf16)."""
+    and pre-MLP norm gain (Layer exits: the last layer, attention included).
+    bf16 tensors (a Llama checkpoint is bf16)."""
     s = cfg.seed if seed is None else seed
     h, V, F = cfg.hidden, cfg.vocab, cfg.ffn
     g = _gen(s * 1000 + 300, device)
@@ -164,6 +204,15 @@ def backbone(cfg: Cfg, seed: int | None = None, device="cpu"):
                 "w_up": _randn((F, h), gl, device, std=MATRIX_STD).to(torch.bfloat16),
                 "w_down": _randn((h, F), gl, device, std=MATRIX_STD).to(torch.bfloat16),
             }
+    if cfg.arch == "layer":
+        gl = _gen(s * 1000 + 400 + cfg.layers, device)
+        mstd = (1.0 / h) ** 0.5 if cfg.name.startswith("tiny") else MATRIX_STD
+        L = {"mlp_norm": _randn((h,), gl, device, std=GAIN_JITTER, mean=1.0),
+             "w_gate": _randn((F, h), gl, device, std=mstd),
+             "w_up": _randn((F, h), gl, device, std=mstd),
+             "w_down": _randn((h, F), gl, device, std=mstd)}
+        L.update(_attn_params(cfg, gl, device))
+        bb["layers"][cfg.layers] = {k: v.to(torch.bfloat16) for k, v in L.items()}
     return bb
 
 

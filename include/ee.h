@@ -64,8 +64,18 @@ typedef enum {
  * MLP:       y = x + W_down(silu(W_gate u) * W_up u), u = RMSNorm_a(x);
  *            logits = RMSNorm_f(y) W_out^T   (pre-norm residual P:165-166;
  *            SwiGLU as in the Llama-2 backbone, reading A2)
- * The `Layer` architecture is not implemented. */
-typedef enum { EE_ARCH_EMBEDDING = 0, EE_ARCH_NORM = 1, EE_ARCH_MLP = 2 } ee_arch;
+ * LAYER:     "a complete Transformer layer, with the same structure as those
+ *            on the backbone" in front of NORM: the Llama-2 layer
+ *            x1 = x + W_o attn(RoPE(W_q u1), RoPE(W_k u1), W_v u1),
+ *            u1 = RMSNorm_att(x), causal GQA attention within each sequence of
+ *            seq_len tokens (head dim 128), then the MLP exit on x1.  Tokens
+ *            couple within a sequence: n_tokens must be whole sequences. */
+typedef enum {
+  EE_ARCH_EMBEDDING = 0,
+  EE_ARCH_NORM = 1,
+  EE_ARCH_MLP = 2,
+  EE_ARCH_LAYER = 3
+} ee_arch;
 
 /* Initialisation of exit parameters. */
 typedef enum { EE_INIT_COPY = 0, EE_INIT_RANDOM = 1 } ee_init;
@@ -95,29 +105,42 @@ typedef enum { EE_DTYPE_BF16 = 0, EE_DTYPE_F32 = 1 } ee_dtype;
  *               (a vocab-parallel shard, 0 <= begin < end <= V, width a
  *               multiple of 8).  ee_tune_step needs the full vocabulary
  *               [0, V); shards are driven through the ee_vp_* phases.
- *  token_weighting  ee_token_weighting. */
+ *  token_weighting  ee_token_weighting.
+ *  n_heads, n_kv_heads, seq_len, rope_theta
+ *               LAYER only (ignored otherwise): query heads (hidden =
+ *               n_heads * 128), key/value heads (divides n_heads; GQA),
+ *               sequence length T (multiple of 64; token t of row r sits at
+ *               position r % T), RoPE base (Llama-2: 10000). */
 typedef struct {
   int32_t hidden, vocab, ffn, num_exits;
   int32_t arch;
   float norm_eps;
   int32_t vocab_begin, vocab_end;
   int32_t token_weighting;
+  int32_t n_heads, n_kv_heads, seq_len;
+  float rope_theta;
 } ee_head_config;
 
 /* Parameters (or gradients, or optimizer moments) of ONE exit.  Device
  * pointers, NULL when the arch has no such tensor.
- *   g_a    [h]     pre-MLP RMSNorm gain       (MLP)
- *   w_gate [F x h] SwiGLU gate projection     (MLP)
- *   w_up   [F x h] SwiGLU up projection       (MLP)
- *   w_down [h x F] down projection            (MLP)
- *   g_f    [h]     final RMSNorm gain         (NORM, MLP)
+ *   g_a    [h]     pre-MLP RMSNorm gain       (MLP, LAYER)
+ *   w_gate [F x h] SwiGLU gate projection     (MLP, LAYER)
+ *   w_up   [F x h] SwiGLU up projection       (MLP, LAYER)
+ *   w_down [h x F] down projection            (MLP, LAYER)
+ *   g_f    [h]     final RMSNorm gain         (NORM, MLP, LAYER)
  *   w_out  [Vl x h] output embedding, Vl = vocab_end - vocab_begin (all archs);
  *                  the paper's "h x V" matrix stored transposed (A7).
+ *   g_att  [h]       pre-attention RMSNorm gain   (LAYER)
+ *   w_q    [h x h]   query projection             (LAYER)
+ *   w_k    [hkv x h] key projection, hkv = 128 n_kv_heads (LAYER)
+ *   w_v    [hkv x h] value projection             (LAYER)
+ *   w_o    [h x h]   attention output projection  (LAYER)
  * Element types depend on the role of the struct:
  *   "operand" params: matrices bf16, gains fp32;
  *   master params, grads, Adam m/v: everything fp32. */
 typedef struct {
   void *g_a, *w_gate, *w_up, *w_down, *g_f, *w_out;
+  void *g_att, *w_q, *w_k, *w_v, *w_o;
 } ee_head_tensors;
 
 /* Optional per-token outputs of one exit (device, [n_tokens] each; any may be
@@ -140,7 +163,9 @@ ee_status ee_workspace_size(const ee_head_config* cfg, int64_t n_tokens, size_t*
  *     (element type src_dtype, device): Embedding/Norm -> the final-exit
  *     layer's W_out (and final norm gain g_f); MLP -> the MLP of the
  *     layer the exit is attached to, and that layer's pre-MLP norm gain as g_a
- *     (A10), plus the final g_f and W_out.  A NULL source tensor that
+ *     (A10), plus the final g_f and W_out; LAYER -> "the last Transformer
+ *     layer of the original LLM" for every exit (attention tensors
+ *     and MLP, its pre-MLP gain as g_a), plus g_f and W_out.  A NULL source tensor that
  *     the arch needs -> EE_ERR_STRUCTURE.  Copies are deep.
  *   init = EE_INIT_RANDOM: matrices ~ N(0, std^2) from a counter-based Philox
  *     stream keyed by (seed, exit, tensor); gains = 1 (A12).
@@ -158,7 +183,8 @@ ee_status ee_init_heads(const ee_head_config* cfg, int32_t init, const ee_head_t
  * backbone is frozen: no gradient w.r.t. hidden).  Exits are
  * independent.
  *   hidden[i]      device bf16 [n_tokens x h], read-only.
- *   n_tokens       tokens on this rank (N = batch * seq flattened), >= 0.
+ *   n_tokens       tokens on this rank (N = batch * seq flattened), >= 0;
+ *                  LAYER: a multiple of seq_len (whole sequences).
  *   targets        device int32 [n_tokens], next-token ids; -1 = ignore.
  *   exit_weights   host float [E], alpha_i (A5).
  *   params[i]      operand parameters (matrices bf16, gains fp32), read-only.

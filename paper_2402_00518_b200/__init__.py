@@ -23,10 +23,11 @@ STATUS_NAMES = {0: "EE_OK", 1: "EE_ERR_ARG", 2: "EE_ERR_SHAPE", 3: "EE_ERR_ALIGN
                 4: "EE_ERR_VOCAB", 5: "EE_ERR_ARCH", 6: "EE_ERR_STRUCTURE",
                 7: "EE_ERR_DIVERGED", 8: "EE_ERR_WORKSPACE", 9: "EE_ERR_CUDA",
                 10: "EE_ERR_NCCL", 11: "EE_ERR_UNSUPPORTED"}
-ARCH = {"embedding": 0, "norm": 1, "mlp": 2}
+ARCH = {"embedding": 0, "norm": 1, "mlp": 2, "layer": 3}
 INIT = {"copy": 0, "random": 1}
 DTYPE = {torch.bfloat16: 0, torch.float32: 1}
-TENSOR_NAMES = ("g_a", "w_gate", "w_up", "w_down", "g_f", "w_out")
+TENSOR_NAMES = ("g_a", "w_gate", "w_up", "w_down", "g_f", "w_out", "g_att", "w_q", "w_k", "w_v",
+                "w_o")
 EXPORTED = ("ee_workspace_size", "ee_init_heads", "ee_tune_step", "ee_count_valid",
             "ee_adam_update", "ee_sgd_update", "ee_get_status", "ee_lr_at", "ee_last_error",
             "ee_version", "ee_test_gemm", "ee_profile_start", "ee_profile_stop",
@@ -45,7 +46,9 @@ class ee_head_config(ctypes.Structure):
     _fields_ = [("hidden", ctypes.c_int32), ("vocab", ctypes.c_int32), ("ffn", ctypes.c_int32),
                 ("num_exits", ctypes.c_int32), ("arch", ctypes.c_int32),
                 ("norm_eps", ctypes.c_float), ("vocab_begin", ctypes.c_int32),
-                ("vocab_end", ctypes.c_int32), ("token_weighting", ctypes.c_int32)]
+                ("vocab_end", ctypes.c_int32), ("token_weighting", ctypes.c_int32),
+                ("n_heads", ctypes.c_int32), ("n_kv_heads", ctypes.c_int32),
+                ("seq_len", ctypes.c_int32), ("rope_theta", ctypes.c_float)]
 
 
 class ee_head_tensors(ctypes.Structure):
@@ -149,11 +152,18 @@ WEIGHTING = {"uniform": 0, "confidence": 1}
 
 
 def make_config(hidden, vocab, ffn, num_exits, arch, norm_eps=1e-5, vocab_begin=0, vocab_end=None,
-                token_weighting="uniform"):
-    return ee_head_config(hidden, vocab, ffn, num_exits, ARCH[arch] if isinstance(arch, str) else arch,
-                          norm_eps, vocab_begin, vocab if vocab_end is None else vocab_end,
+                token_weighting="uniform", n_heads=0, n_kv_heads=0, seq_len=0, rope_theta=10000.0):
+    """ee_head_config; n_heads / n_kv_heads / seq_len / rope_theta are the Layer
+    exit's attention geometry (n_heads defaults to hidden / 128)."""
+    a = ARCH[arch] if isinstance(arch, str) else arch
+    if a == ARCH["layer"] and not n_heads:
+        n_heads = hidden // 128
+    if a == ARCH["layer"] and not n_kv_heads:
+        n_kv_heads = n_heads
+    return ee_head_config(hidden, vocab, ffn, num_exits, a, norm_eps, vocab_begin,
+                          vocab if vocab_end is None else vocab_end,
                           WEIGHTING[token_weighting] if isinstance(token_weighting, str)
-                          else token_weighting)
+                          else token_weighting, n_heads, n_kv_heads, seq_len, rope_theta)
 
 
 def heads(list_of_dicts):
@@ -386,13 +396,17 @@ def ee_launch_count() -> int:
 # ExitHeads: parameter store + optimizer state + workspace (torch allocations)
 # ---------------------------------------------------------------------------
 
-def tensor_shapes(hidden, vocab, ffn, arch):
+def tensor_shapes(hidden, vocab, ffn, arch, n_kv_heads=0):
     """Parameter shapes of one exit; `vocab` = rows of W_out held (a shard under VP)."""
     s = {"w_out": (vocab, hidden)}
-    if arch in ("norm", "mlp"):
+    if arch != "embedding":
         s["g_f"] = (hidden,)
-    if arch == "mlp":
+    if arch in ("mlp", "layer"):
         s.update(g_a=(hidden,), w_gate=(ffn, hidden), w_up=(ffn, hidden), w_down=(hidden, ffn))
+    if arch == "layer":
+        hkv = 128 * (n_kv_heads or hidden // 128)
+        s.update(g_att=(hidden,), w_q=(hidden, hidden), w_k=(hkv, hidden), w_v=(hkv, hidden),
+                 w_o=(hidden, hidden))
     return s
 
 
@@ -407,6 +421,14 @@ class HeadSpec:
     vocab_begin: int = 0          # vocab-parallel shard of W_out rows [begin, end)
     vocab_end: int | None = None
     token_weighting: str = "uniform"   # or "confidence"
+    n_heads: int = 0              # Layer exits: attention geometry (default hidden / 128)
+    n_kv_heads: int = 0           # (default n_heads: no GQA)
+    seq_len: int = 0
+    rope_theta: float = 10000.0
+
+    def attn_kwargs(self):
+        return dict(n_heads=self.n_heads, n_kv_heads=self.n_kv_heads, seq_len=self.seq_len,
+                    rope_theta=self.rope_theta)
 
 
 class ExitHeads:
@@ -428,8 +450,10 @@ class ExitHeads:
         self.spec = spec
         ve = spec.vocab if spec.vocab_end is None else spec.vocab_end
         self.cfg = make_config(spec.hidden, spec.vocab, spec.ffn, spec.num_exits, spec.arch,
-                               spec.norm_eps, spec.vocab_begin, ve, spec.token_weighting)
-        shapes = tensor_shapes(spec.hidden, ve - spec.vocab_begin, spec.ffn, spec.arch)
+                               spec.norm_eps, spec.vocab_begin, ve, spec.token_weighting,
+                               **spec.attn_kwargs())
+        shapes = tensor_shapes(spec.hidden, ve - spec.vocab_begin, spec.ffn, spec.arch,
+                               self.cfg.n_kv_heads)
         dev = torch.device(device)
         E = spec.num_exits
 
@@ -449,7 +473,8 @@ class ExitHeads:
         self.grad_buffers = k
         self.grads = [pool[i % k] for i in range(E)]
         self.exit_cfg = make_config(spec.hidden, spec.vocab, spec.ffn, 1, spec.arch,
-                                    spec.norm_eps, spec.vocab_begin, ve, spec.token_weighting)
+                                    spec.norm_eps, spec.vocab_begin, ve, spec.token_weighting,
+                                    **spec.attn_kwargs())
         self.m = alloc(f32) if adam else None
         self.v = alloc(f32) if adam else None
         self.step_count = 0

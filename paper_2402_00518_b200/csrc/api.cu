@@ -58,7 +58,7 @@ constexpr int NORM_RPB = 64;  // rows per block of the norm backward / gain-grad
 
 ee_status check_cfg(const ee_head_config* c) {
   if (!c) return fail(EE_ERR_ARG, "cfg is NULL");
-  if (c->arch < EE_ARCH_EMBEDDING || c->arch > EE_ARCH_MLP)
+  if (c->arch < EE_ARCH_EMBEDDING || c->arch > EE_ARCH_LAYER)
     return fail(EE_ERR_ARG, "unknown arch %d", c->arch);
   if (c->num_exits < 1) return fail(EE_ERR_ARG, "num_exits must be >= 1");
   if (c->hidden < 64 || c->hidden > 8192 || c->hidden % 64 != 0)
@@ -69,9 +69,19 @@ ee_status check_cfg(const ee_head_config* c) {
                 c->vocab);
   if ((c->vocab_end - c->vocab_begin) % 8 != 0)
     return fail(EE_ERR_SHAPE, "local vocab size must be a multiple of 8");
-  if (c->arch == EE_ARCH_MLP && (c->ffn < 128 || c->ffn % 128 != 0))
-    return fail(EE_ERR_SHAPE, "ffn must be a positive multiple of 128 for MLP exits, got %d",
+  if (c->arch >= EE_ARCH_MLP && (c->ffn < 128 || c->ffn % 128 != 0))
+    return fail(EE_ERR_SHAPE, "ffn must be a positive multiple of 128 for MLP/Layer exits, got %d",
                 c->ffn);
+  if (c->arch == EE_ARCH_LAYER) {
+    if (c->n_heads < 1 || c->n_kv_heads < 1 || c->n_heads % c->n_kv_heads != 0)
+      return fail(EE_ERR_SHAPE, "Layer exit: n_kv_heads must divide n_heads (%d, %d)", c->n_heads,
+                  c->n_kv_heads);
+    if (c->hidden != 128 * c->n_heads)
+      return fail(EE_ERR_SHAPE, "Layer exit: hidden must be n_heads * 128 (head dim 128)");
+    if (c->seq_len < 64 || c->seq_len % 64 != 0)
+      return fail(EE_ERR_SHAPE, "Layer exit: seq_len must be a positive multiple of 64");
+    if (!(c->rope_theta > 0.f)) return fail(EE_ERR_ARG, "Layer exit: rope_theta must be > 0");
+  }
   if (!(c->norm_eps >= 0.f)) return fail(EE_ERR_ARG, "norm_eps must be >= 0");
   if (c->token_weighting != EE_WEIGHT_UNIFORM && c->token_weighting != EE_WEIGHT_CONFIDENCE)
     return fail(EE_ERR_ARG, "unknown token_weighting %d", c->token_weighting);
@@ -80,11 +90,56 @@ ee_status check_cfg(const ee_head_config* c) {
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
+// Layer exits couple the tokens of a sequence: a call must hold whole sequences.
+ee_status check_tokens(const ee_head_config* c, long long n) {
+  if (c->arch == EE_ARCH_LAYER && n % c->seq_len != 0)
+    return fail(EE_ERR_SHAPE, "Layer exit: n_tokens (%lld) must be a multiple of seq_len (%d)", n,
+                c->seq_len);
+  return EE_OK;
+}
+
+// The exit tensors in ee_head_tensors order; Random-init streams are keyed by
+// this index (exit * 16 + k).
+constexpr int NTENS = 11;
+struct TInfo {
+  void* ee_head_tensors::*f;
+  const char* name;
+  bool gain, vocab;
+};
+const TInfo kTens[NTENS] = {
+    {&ee_head_tensors::g_a, "g_a", true, false},       {&ee_head_tensors::w_gate, "w_gate", false, false},
+    {&ee_head_tensors::w_up, "w_up", false, false},    {&ee_head_tensors::w_down, "w_down", false, false},
+    {&ee_head_tensors::g_f, "g_f", true, false},       {&ee_head_tensors::w_out, "w_out", false, true},
+    {&ee_head_tensors::g_att, "g_att", true, false},   {&ee_head_tensors::w_q, "w_q", false, false},
+    {&ee_head_tensors::w_k, "w_k", false, false},      {&ee_head_tensors::w_v, "w_v", false, false},
+    {&ee_head_tensors::w_o, "w_o", false, false}};
+
+bool tensor_needed(const ee_head_config* c, int k) {
+  if (k == 5) return true;                          // w_out
+  if (k == 4) return c->arch != EE_ARCH_EMBEDDING;  // g_f
+  if (k < 4) return c->arch >= EE_ARCH_MLP;         // MLP body
+  return c->arch == EE_ARCH_LAYER;                  // attention block
+}
+
+long long tensor_numel(const ee_head_config* c, int k) {
+  const long long h = c->hidden, F = c->ffn, Vl = c->vocab_end - c->vocab_begin;
+  const long long hkv = 128LL * c->n_kv_heads;
+  switch (k) {
+    case 0: case 4: case 6: return h;
+    case 1: case 2: case 3: return F * h;
+    case 5: return Vl * h;
+    case 7: case 10: return h * h;
+    default: return hkv * h;  // w_k, w_v
+  }
+}
+
 struct Layout {
   size_t wsum_part, wsum, zT, uT, dyT;
   long long ldT;  // leading dimension of the transposed [h x n] copies (n rounded up to 8)
   size_t status, vcount, loss_part, lse, coef, tgt, pm, ps, pi, z, ds, dz, dgp, ry, u, rx, ab,
       mact, y, dy, total;
+  // Layer exits: attention block activations / gradients
+  size_t u1, r1, q, k, v, o, lse2, x1, da, dq, dk, dv, dvec;
   int nb, nparts, nfin;
 };
 
@@ -122,7 +177,8 @@ Layout make_layout(const ee_head_config* c, long long n) {
     L.dgp = take(4 * (size_t)(L.nparts > 0 ? L.nparts : 1) * h);
     L.ry = take(4 * n);
   }
-  if (c->arch == EE_ARCH_MLP) {
+  L.u1 = L.r1 = L.q = L.k = L.v = L.o = L.lse2 = L.x1 = L.da = L.dq = L.dk = L.dv = L.dvec = 0;
+  if (c->arch >= EE_ARCH_MLP) {
     L.u = take(2 * (size_t)n * h);
     L.rx = take(4 * n);
     L.ab = take(2 * (size_t)n * 2 * F);
@@ -131,6 +187,22 @@ Layout make_layout(const ee_head_config* c, long long n) {
     L.dy = take(2 * (size_t)n * h);
     L.uT = take(2 * (size_t)h * L.ldT);
     L.dyT = take(2 * (size_t)h * L.ldT);
+  }
+  if (c->arch == EE_ARCH_LAYER) {
+    const long long hkv = 128LL * c->n_kv_heads, Hq = c->n_heads;
+    L.u1 = take(2 * (size_t)n * h);
+    L.r1 = take(4 * n);
+    L.q = take(2 * (size_t)n * h);
+    L.k = take(2 * (size_t)n * hkv);
+    L.v = take(2 * (size_t)n * hkv);
+    L.o = take(2 * (size_t)n * h);
+    L.lse2 = take(4 * (size_t)n * Hq);
+    L.x1 = take(4 * (size_t)n * h);
+    L.da = take(2 * (size_t)n * h);
+    L.dq = take(2 * (size_t)n * h);
+    L.dk = take(2 * (size_t)n * hkv);
+    L.dv = take(2 * (size_t)n * hkv);
+    L.dvec = take(4 * (size_t)n * Hq);
   }
   L.total = o;
   return L;
@@ -154,15 +226,14 @@ ee_status check_device() {
 
 ee_status check_arch_tensors(const ee_head_config* c, const ee_head_tensors& t, const char* what,
                              int i) {
-  const bool mlp = c->arch == EE_ARCH_MLP, nrm = c->arch != EE_ARCH_EMBEDDING;
-  if (!t.w_out) return fail(EE_ERR_ARCH, "%s[%d].w_out is NULL", what, i);
-  if (nrm != (t.g_f != nullptr)) return fail(EE_ERR_ARCH, "%s[%d].g_f presence does not match arch", what, i);
-  if (mlp != (t.g_a != nullptr) || mlp != (t.w_gate != nullptr) || mlp != (t.w_up != nullptr) ||
-      mlp != (t.w_down != nullptr))
-    return fail(EE_ERR_ARCH, "%s[%d]: MLP tensors present/absent do not match arch", what, i);
-  const void* ps[6] = {t.g_a, t.w_gate, t.w_up, t.w_down, t.g_f, t.w_out};
-  for (const void* p : ps)
-    if (p && !aligned16(p)) return fail(EE_ERR_ALIGN, "%s[%d]: tensor not 16-byte aligned", what, i);
+  for (int k = 0; k < NTENS; ++k) {
+    const void* p = t.*(kTens[k].f);
+    if (tensor_needed(c, k) != (p != nullptr))
+      return fail(EE_ERR_ARCH, "%s[%d].%s is %s for arch %d", what, i, kTens[k].name,
+                  p ? "set but unused" : "NULL but required", c->arch);
+    if (p && !aligned16(p)) return fail(EE_ERR_ALIGN, "%s[%d].%s not 16-byte aligned", what, i,
+                                        kTens[k].name);
+  }
   return EE_OK;
 }
 
@@ -290,6 +361,9 @@ struct Bufs {
   float* y;
   __nv_bfloat16* dy;
   __nv_bfloat16 *zT, *uT, *dyT;  // K-major copies for the weight-gradient GEMMs
+  // Layer exits
+  __nv_bfloat16 *u1, *q, *k, *v, *o, *da, *dq, *dk, *dv;
+  float *r1, *lse2, *x1, *dvec;
   // vocab-parallel merge state
   float* m_loc;
   Layout L;
@@ -300,7 +374,7 @@ Bufs make_bufs(const ee_head_config* cfg, long long n, void* workspace) {
   B.L = make_layout(cfg, n);
   const Layout& L = B.L;
   uint8_t* ws = (uint8_t*)workspace;
-  const bool mlp = cfg->arch == EE_ARCH_MLP, nrm = cfg->arch != EE_ARCH_EMBEDDING;
+  const bool mlp = cfg->arch >= EE_ARCH_MLP, nrm = cfg->arch != EE_ARCH_EMBEDDING;
   B.status = (DevStatus*)(ws + L.status);
   B.vcount = (long long*)(ws + L.vcount);
   B.lse = (float*)(ws + L.lse);
@@ -331,7 +405,139 @@ Bufs make_bufs(const ee_head_config* cfg, long long n, void* workspace) {
     B.uT = (__nv_bfloat16*)(ws + L.uT);
     B.dyT = (__nv_bfloat16*)(ws + L.dyT);
   }
+  if (cfg->arch == EE_ARCH_LAYER) {
+    B.u1 = (__nv_bfloat16*)(ws + L.u1);
+    B.r1 = (float*)(ws + L.r1);
+    B.q = (__nv_bfloat16*)(ws + L.q);
+    B.k = (__nv_bfloat16*)(ws + L.k);
+    B.v = (__nv_bfloat16*)(ws + L.v);
+    B.o = (__nv_bfloat16*)(ws + L.o);
+    B.lse2 = (float*)(ws + L.lse2);
+    B.x1 = (float*)(ws + L.x1);
+    B.da = (__nv_bfloat16*)(ws + L.da);
+    B.dq = (__nv_bfloat16*)(ws + L.dq);
+    B.dk = (__nv_bfloat16*)(ws + L.dk);
+    B.dv = (__nv_bfloat16*)(ws + L.dv);
+    B.dvec = (float*)(ws + L.dvec);
+  }
   return B;
+}
+
+// ---- Layer exit, attention block (Llama-2 layer P:356-358) ----
+// L1 u1 = RMSNorm_att(x); L2 q|k|v = u1 W^T with L3 RoPE(q, k) fused into the
+// projection epilogues; L4 causal GQA flash
+// attention (o, lse2); L5 x1 = x + o W_o^T (fp32 residual stream, A15).
+ee_status layer_attn_forward(const ee_head_config* cfg, const Bufs& B, const ee_head_tensors& P,
+                             const __nv_bfloat16* x, long long n, cudaStream_t st) {
+  const int h = cfg->hidden, Hq = cfg->n_heads, Hkv = cfg->n_kv_heads, hkv = 128 * Hkv;
+  { Prof p_("L1_rmsnorm_att", st, 0, 0, 4.0 * n * h + 4.0 * n);
+  EE_CUDA(launch_rmsnorm_fwd(x, false, (const float*)P.g_att, cfg->norm_eps, B.u1, B.r1, n, h, st)); }
+  struct Proj {
+    const void* w;
+    __nv_bfloat16* out;
+    int N;
+    const char* name;
+  } projs[3] = {{P.w_q, B.q, h, "L2_q_proj"}, {P.w_k, B.k, hkv, "L2_k_proj"},
+                {P.w_v, B.v, hkv, "L2_v_proj"}};
+  for (int j = 0; j < 3; ++j) {  // L3: RoPE fused into the q / k epilogues (fp32, one rounding)
+    const Proj& pj = projs[j];
+    GemmArgs a = base_args((int)n, pj.N, h);
+    a.outb = pj.out;
+    a.ldo = pj.N;
+    if (j < 2) {
+      a.rope_seq = cfg->seq_len;
+      a.rope_theta = cfg->rope_theta;
+    }
+    Mat A{B.u1, n, h, h}, Bm{pj.w, pj.N, h, h};
+    Prof p_(pj.name, st, 2.0 * n * pj.N * h, 2.0 * n * pj.N * h, 0);
+    EE_CUDA(gemm_run(EPI_BF16, true, true, A, Bm, nullptr, B_PLAIN, 0, a, st));
+  }
+  { const double fl = 2.0 * (double)n * h * (cfg->seq_len + 1);  // causal: 2 GEMMs x T/2 keys
+    Prof p_("L4_attn_fwd", st, 2.0 * (double)n * h * (cfg->seq_len + 64), fl, 0);
+    EE_CUDA(launch_attn_fwd(B.q, B.k, B.v, B.o, n, cfg->seq_len, Hq, Hkv, B.lse2, st)); }
+  {
+    GemmArgs a = base_args((int)n, h, h);
+    a.out0 = B.x1;
+    a.ldo = h;
+    a.resid = x;
+    a.ld_resid = h;
+    Mat A{B.o, n, h, h}, Bm{P.w_o, h, h, h};
+    Prof p_("L5_o_proj_resid", st, 2.0 * n * h * h, 2.0 * n * h * h, 0);
+    EE_CUDA(gemm_run(EPI_RESID, true, true, A, Bm, nullptr, B_PLAIN, 0, a, st));
+  }
+  return EE_OK;
+}
+
+// Backward of the attention block given dx1 (bf16, in B.dy): L6 dW_o = dx1^T o;
+// L7 da = dx1 W_o; L8 flash-attention backward (dq, dk, dv) with L9 RoPE^T
+// fused into its dq / dk stores;
+// L10 dW_{q,k,v} = d{q,k,v}^T u1; L11 du1 = dq W_q + dk W_k + dv W_v;
+// L12 dg_att = sum du1 * xhat1 (no dx: frozen backbone).
+ee_status layer_attn_backward(const ee_head_config* cfg, const Bufs& B, const ee_head_tensors& P,
+                              const ee_head_tensors& G, const __nv_bfloat16* x, long long n,
+                              int accumulate, cudaStream_t st) {
+  const int h = cfg->hidden, Hq = cfg->n_heads, Hkv = cfg->n_kv_heads, hkv = 128 * Hkv;
+  const int nparts = (int)((n + NORM_RPB - 1) / NORM_RPB);
+  {  // L6: dW_o = dx1^T o  (A = dx1^T K-major copy, B = o MN-major)
+    { Prof p_("transpose_dx1", st, 0, 0, 4.0 * n * h);
+    EE_CUDA(launch_transpose_bf16(B.dy, B.dyT, n, h, B.L.ldT, st)); }
+    GemmArgs a = base_args(h, h, (int)n);
+    a.out0 = (float*)G.w_o;
+    a.ldo = h;
+    a.accumulate = accumulate;
+    Mat A{B.dyT, h, n, B.L.ldT}, Bm{B.o, n, h, h};
+    Prof p_("L6_dw_o", st, 2.0 * n * h * h, 2.0 * n * h * h, 0);
+    EE_CUDA(gemm_run(EPI_F32, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
+  }
+  {  // L7: da = dx1 W_o  (W_o read MN-major in place)
+    GemmArgs a = base_args((int)n, h, h);
+    a.outb = B.da;
+    a.ldo = h;
+    Mat A{B.dy, n, h, h}, Bm{P.w_o, h, h, h};
+    Prof p_("L7_da", st, 2.0 * n * h * h, 2.0 * n * h * h, 0);
+    EE_CUDA(gemm_run(EPI_BF16, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
+  }
+  { const double fa = 4.0 * (double)n * h * (cfg->seq_len + 1);    // dV, dP, dQ, dK
+    const double fe = 7.0 * (double)n * h * (cfg->seq_len + 64);   // + S twice, dP twice
+    Prof p_("L8_attn_bwd", st, fe, fa, 0);
+    EE_CUDA(launch_attn_bwd(B.q, B.k, B.v, B.o, B.da, B.lse2, B.dvec, B.dq, B.dk, B.dv, n,
+                            cfg->seq_len, Hq, Hkv, cfg->rope_theta, st)); }  // + L9 RoPE^T fused
+  { Prof p_("transpose_u1", st, 0, 0, 4.0 * n * h);
+  EE_CUDA(launch_transpose_bf16(B.u1, B.uT, n, h, B.L.ldT, st)); }
+  struct WG {
+    const __nv_bfloat16* d;
+    void* g;
+    const void* w;
+    int N;
+    const char *name, *dname;
+  } wg[3] = {{B.dq, G.w_q, P.w_q, h, "L10_dw_q", "L11_du1_q"},
+             {B.dk, G.w_k, P.w_k, hkv, "L10_dw_k", "L11_du1_k"},
+             {B.dv, G.w_v, P.w_v, hkv, "L10_dw_v", "L11_du1_v"}};
+  for (const WG& w : wg) {  // L10: dW^T = u1^T d (A = u1^T K-major, B = d MN-major), stored transposed
+    GemmArgs a = base_args(h, w.N, (int)n);
+    a.out0 = (float*)w.g;
+    a.ldo = h;
+    a.n_split = w.N;
+    a.accumulate = accumulate;
+    Mat A{B.uT, h, n, B.L.ldT}, Bm{w.d, n, w.N, w.N};
+    Prof p_(w.name, st, 2.0 * n * w.N * h, 2.0 * n * w.N * h, 0);
+    EE_CUDA(gemm_run(EPI_F32T, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
+  }
+  for (int j = 0; j < 3; ++j) {  // L11: du1 (+)= d W  (W read MN-major in place) -> B.dz
+    const WG& w = wg[j];
+    GemmArgs a = base_args((int)n, h, w.N);
+    a.out0 = B.dz;
+    a.ldo = h;
+    a.accumulate = j > 0;
+    Mat A{w.d, n, w.N, w.N}, Bm{w.w, w.N, h, h};
+    Prof p_(w.dname, st, 2.0 * n * w.N * h, 2.0 * n * w.N * h, 0);
+    EE_CUDA(gemm_run(EPI_F32, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
+  }
+  { Prof p_("L12_gain_grad", st, 0, 0, 6.0 * n * h);
+  EE_CUDA(launch_gain_grad(B.dz, x, B.r1, B.dgp, n, h, NORM_RPB, st)); }
+  { Prof p_("reduce_cols", st, 0, 0, 4.0 * nparts * h);
+  EE_CUDA(launch_reduce_cols(B.dgp, nparts, h, (float*)G.g_att, accumulate, st)); }
+  return EE_OK;
 }
 
 // a1..a4: z = exit-head input of the vocab projection, on n tokens.
@@ -341,7 +547,8 @@ ee_status phase_exit_forward(const ee_head_config* cfg, const Bufs& B, const ee_
                              const __nv_bfloat16* x, long long n, __nv_bfloat16* z_out,
                              const __nv_bfloat16** z_ret, cudaStream_t st) {
   const int h = cfg->hidden, F = cfg->ffn;
-  const bool mlp = cfg->arch == EE_ARCH_MLP, nrm = cfg->arch != EE_ARCH_EMBEDDING;
+  const bool mlp = cfg->arch >= EE_ARCH_MLP, nrm = cfg->arch != EE_ARCH_EMBEDDING;
+  const bool layer = cfg->arch == EE_ARCH_LAYER;
   if (!nrm) {
     if (z_out && n > 0)
       EE_CUDA(cudaMemcpyAsync(z_out, x, 2 * (size_t)n * h, cudaMemcpyDeviceToDevice, st));
@@ -352,9 +559,15 @@ ee_status phase_exit_forward(const ee_head_config* cfg, const Bufs& B, const ee_
   *z_ret = z;
   if (n == 0) return EE_OK;
   if (mlp) {
+    // Layer: the attention block first; the MLP body then runs on x1 (fp32)
+    if (layer) {
+      ee_status s = layer_attn_forward(cfg, B, P, x, n, st);
+      if (s != EE_OK) return s;
+    }
+    const void* xin = layer ? (const void*)B.x1 : (const void*)x;
     // a1: u = RMSNorm_a(x)
-    { Prof p_("a1_rmsnorm_fwd", st, 0, 0, 4.0 * n * h + 4.0 * n);
-    EE_CUDA(launch_rmsnorm_fwd(x, false, (const float*)P.g_a, cfg->norm_eps, B.u, B.rx, n, h, st)); }
+    { Prof p_("a1_rmsnorm_fwd", st, 0, 0, (layer ? 6.0 : 4.0) * n * h + 4.0 * n);
+    EE_CUDA(launch_rmsnorm_fwd(xin, layer, (const float*)P.g_a, cfg->norm_eps, B.u, B.rx, n, h, st)); }
     // a2: [A|B] = u [W_gate|W_up]^T (paired B tiles), M = silu(A) * B
     {
       GemmArgs a = base_args((int)n, F, h);
@@ -367,16 +580,21 @@ ee_status phase_exit_forward(const ee_head_config* cfg, const Bufs& B, const ee_
       Prof p_("a2_gateup_swiglu", st, 4.0 * n * F * h, 4.0 * n * F * h, 0);
       EE_CUDA(gemm_run(EPI_SWIGLU_FWD, true, true, A, B0, &B1, B_PAIR, 0, a, st));
     }
-    // a3: y = x + M W_down^T  (fp32 residual stream, A15)
+    // a3: y = x + M W_down^T  (fp32 residual stream, A15; Layer: y = x1 + ...)
     {
       GemmArgs a = base_args((int)n, h, F);
       a.out0 = B.y;
       a.ldo = h;
-      a.resid = x;
-      a.ld_resid = h;
+      if (layer) {  // fp32 residual: y <- x1, then accumulate
+        EE_CUDA(cudaMemcpyAsync(B.y, B.x1, 4 * (size_t)n * h, cudaMemcpyDeviceToDevice, st));
+        a.accumulate = 1;
+      } else {
+        a.resid = x;
+        a.ld_resid = h;
+      }
       Mat A{B.mact, n, F, F}, Bm{P.w_down, h, F, F};
       Prof p_("a3_down_resid", st, 2.0 * n * F * h, 2.0 * n * F * h, 0);
-      EE_CUDA(gemm_run(EPI_RESID, true, true, A, Bm, nullptr, B_PLAIN, 0, a, st));
+      EE_CUDA(gemm_run(layer ? EPI_F32 : EPI_RESID, true, true, A, Bm, nullptr, B_PLAIN, 0, a, st));
     }
     // a4: z = RMSNorm_f(y)
     { Prof p_("a4_rmsnorm_fwd", st, 0, 0, 6.0 * n * h + 4.0 * n);
@@ -452,7 +670,7 @@ ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee
                               const ee_head_tensors& G, const __nv_bfloat16* x, long long n,
                               const float* dz, int accumulate, cudaStream_t st) {
   const int h = cfg->hidden, F = cfg->ffn;
-  const bool mlp = cfg->arch == EE_ARCH_MLP;
+  const bool mlp = cfg->arch >= EE_ARCH_MLP, layer = cfg->arch == EE_ARCH_LAYER;
   if (cfg->arch == EE_ARCH_EMBEDDING) return EE_OK;
   const int nparts = (int)((n + NORM_RPB - 1) / NORM_RPB);
   // a10: final RMSNorm backward -> dg_f (and dy for MLP)
@@ -509,23 +727,29 @@ ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee
     Prof p_("a12_du", st, 4.0 * n * F * h, 4.0 * n * F * h, 0);
     EE_CUDA(gemm_run(EPI_F32, true, false, A, B0, &B1, B_KSPLIT, F, a, st));
   }
-  // a13: dg_a = sum_t du_t * xhat_t  (no dx: frozen backbone)
-  { Prof p_("a13_gain_grad", st, 0, 0, 6.0 * n * h);
-  EE_CUDA(launch_gain_grad(B.dz, x, B.rx, B.dgp, n, h, NORM_RPB, st)); }
+  if (!layer) {
+    // a13: dg_a = sum_t du_t * xhat_t  (no dx: frozen backbone)
+    { Prof p_("a13_gain_grad", st, 0, 0, 6.0 * n * h);
+    EE_CUDA(launch_gain_grad(B.dz, x, B.rx, B.dgp, n, h, NORM_RPB, st)); }
+  } else {
+    // a13 (Layer): dg_a and dx1 = dy + RMSNorm_a^T(du), written over dy in place
+    Prof p_("a13_rmsnorm_bwd_resid", st, 0, 0, 14.0 * n * h);
+    EE_CUDA(launch_rmsnorm_bwd(B.dz, B.x1, true, B.rx, (const float*)P.g_a, B.dy, B.dgp, n, h,
+                               NORM_RPB, st, B.dy));
+  }
   { Prof p_("reduce_cols", st, 0, 0, 4.0 * nparts * h);
   EE_CUDA(launch_reduce_cols(B.dgp, nparts, h, (float*)G.g_a, accumulate, st)); }
+  if (layer) return layer_attn_backward(cfg, B, P, G, x, n, accumulate, st);
   return EE_OK;
 }
 
 ee_status zero_grads(const ee_head_config* cfg, const ee_head_tensors& G, bool vocab_part,
                      bool exit_part, cudaStream_t st) {
-  const long long h = cfg->hidden, F = cfg->ffn, Vl = cfg->vocab_end - cfg->vocab_begin;
-  const long long sz[6] = {h, F * h, F * h, h * F, h, Vl * h};
-  void* ptrs[6] = {G.g_a, G.w_gate, G.w_up, G.w_down, G.g_f, G.w_out};
-  for (int k = 0; k < 6; ++k) {
-    const bool is_vocab = k == 5;
-    if (ptrs[k] && ((is_vocab && vocab_part) || (!is_vocab && exit_part)))
-      EE_CUDA(cudaMemsetAsync(ptrs[k], 0, 4 * sz[k], st));
+  for (int k = 0; k < NTENS; ++k) {
+    void* p = G.*(kTens[k].f);
+    const bool is_vocab = kTens[k].vocab;
+    if (p && ((is_vocab && vocab_part) || (!is_vocab && exit_part)))
+      EE_CUDA(cudaMemsetAsync(p, 0, 4 * (size_t)tensor_numel(cfg, k), st));
   }
   return EE_OK;
 }
@@ -549,6 +773,7 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
       (n_tokens > 0 && !targets))
     return fail(EE_ERR_ARG, "NULL argument or n_tokens < 0");
   if (n_tokens > (1LL << 30)) return fail(EE_ERR_SHAPE, "n_tokens too large");
+  if ((s = check_tokens(cfg, n_tokens)) != EE_OK) return s;
   if (valid_count && cfg->token_weighting == EE_WEIGHT_CONFIDENCE)
     return fail(EE_ERR_UNSUPPORTED, "confidence weighting needs every token of the batch in one "
                                     "call (single GPU or the ee_vp_* phases), not a DP shard");
@@ -714,17 +939,19 @@ ee_status ee_backbone_forward(const ee_backbone_config* cfg, const ee_layer_tens
       int N;
       const char* name;
     } projs[3] = {{t.w_q, q, h, "bb_q_proj"}, {t.w_k, k, hkv, "bb_k_proj"}, {t.w_v, v, hkv, "bb_v_proj"}};
-    for (const Proj& pj : projs) {
+    for (int j = 0; j < 3; ++j) {  // RoPE fused into the q / k epilogues
+      const Proj& pj = projs[j];
       GemmArgs a = base_args((int)n, pj.N, h);
       a.outb = pj.out;
       a.ldo = pj.N;
+      if (j < 2) {
+        a.rope_seq = cfg->seq_len;
+        a.rope_theta = cfg->rope_theta;
+      }
       Mat A{u, n, h, h}, B{pj.w, pj.N, h, h};
       Prof p_(pj.name, st, 2.0 * n * pj.N * h, 2.0 * n * pj.N * h, 0);
       EE_CUDA(gemm_run(EPI_BF16, true, true, A, B, nullptr, B_PLAIN, 0, a, st));
     }
-    { Prof p_("bb_rope", st, 0, 0, 4.0 * n * (h + hkv));
-    EE_CUDA(launch_rope(q, n, Hq, cfg->seq_len, cfg->rope_theta, st));
-    EE_CUDA(launch_rope(k, n, Hkv, cfg->seq_len, cfg->rope_theta, st)); }
     { const double fl = 2.0 * 2.0 * (double)n * (cfg->seq_len + 64) / 2.0 * h;  // causal
       Prof p_("bb_attention", st, fl, fl, 0);
       EE_CUDA(launch_attn_fwd(q, k, v, o, n, cfg->seq_len, Hq, Hkv, nullptr, st)); }
@@ -783,6 +1010,7 @@ ee_status ee_exit_infer(const ee_head_config* cfg, const void* const* hidden, in
   if (!hidden || !params || !argmax_out || !conf_out || n_tokens < 0)
     return fail(EE_ERR_ARG, "NULL argument or n_tokens < 0");
   if (E > 64) return fail(EE_ERR_SHAPE, "at most 64 exits");
+  if ((s = check_tokens(cfg, n_tokens)) != EE_OK) return s;
   for (int i = 0; i < E; ++i) {
     if ((s = check_arch_tensors(cfg, params[i], "params", i)) != EE_OK) return s;
     if (n_tokens > 0 && (!hidden[i] || !argmax_out[i] || !conf_out[i]))
@@ -842,6 +1070,7 @@ ee_status ee_vp_exit_forward(const ee_head_config* cfg, const void* hidden, int6
   if (s != EE_OK) return s;
   if (!params || !z_out || n_local < 0 || n_local > n_all || (n_local > 0 && !hidden))
     return fail(EE_ERR_ARG, "bad ee_vp_exit_forward arguments");
+  if (ee_status s2 = check_tokens(cfg, n_local); s2 != EE_OK) return s2;
   if ((s = check_arch_tensors(cfg, *params, "params", 0)) != EE_OK) return s;
   if (!aligned16(z_out) || (hidden && !aligned16(hidden))) return fail(EE_ERR_ALIGN, "misaligned");
   const __nv_bfloat16* z = nullptr;
@@ -939,6 +1168,7 @@ ee_status ee_vp_exit_backward(const ee_head_config* cfg, const void* hidden, int
   if (!params || !grads || n_local < 0 || n_local > n_all ||
       (n_local > 0 && cfg->arch != EE_ARCH_EMBEDDING && (!hidden || !dz_local)))
     return fail(EE_ERR_ARG, "bad ee_vp_exit_backward arguments");
+  if (ee_status s2 = check_tokens(cfg, n_local); s2 != EE_OK) return s2;
   cudaStream_t st = (cudaStream_t)stream;
   if (n_local == 0) {
     if (!accumulate) return zero_grads(cfg, *grads, false, true, st);
@@ -960,43 +1190,31 @@ ee_status ee_init_heads(const ee_head_config* cfg, int32_t init, const ee_head_t
   if (init == EE_INIT_COPY && !src) return fail(EE_ERR_STRUCTURE, "Copy init without a source");
   if ((s = check_device()) != EE_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
-  const long long h = cfg->hidden, F = cfg->ffn, Vl = cfg->vocab_end - cfg->vocab_begin;
   for (int i = 0; i < cfg->num_exits; ++i) {
     if ((s = check_arch_tensors(cfg, master[i], "master", i)) != EE_OK) return s;
     if ((s = check_arch_tensors(cfg, op[i], "operand", i)) != EE_OK) return s;
-    struct T {
-      const void* src;
-      float* m;
-      void* o;
-      long long n;
-      bool gain;
-      const char* name;
-    } ts[6] = {
-        {src ? src[i].g_a : nullptr, (float*)master[i].g_a, op[i].g_a, h, true, "g_a"},
-        {src ? src[i].w_gate : nullptr, (float*)master[i].w_gate, op[i].w_gate, F * h, false, "w_gate"},
-        {src ? src[i].w_up : nullptr, (float*)master[i].w_up, op[i].w_up, F * h, false, "w_up"},
-        {src ? src[i].w_down : nullptr, (float*)master[i].w_down, op[i].w_down, h * F, false, "w_down"},
-        {src ? src[i].g_f : nullptr, (float*)master[i].g_f, op[i].g_f, h, true, "g_f"},
-        {src ? src[i].w_out : nullptr, (float*)master[i].w_out, op[i].w_out, Vl * h, false, "w_out"},
-    };
-    for (int k = 0; k < 6; ++k) {
-      const T& t = ts[k];
-      if (!t.m) continue;
-      float* op_f32 = (t.gain && t.o != (void*)t.m) ? (float*)t.o : nullptr;
-      __nv_bfloat16* op_bf = t.gain ? nullptr : (__nv_bfloat16*)t.o;
+    for (int k = 0; k < NTENS; ++k) {
+      const TInfo& ti = kTens[k];
+      float* m = (float*)(master[i].*(ti.f));
+      void* o = op[i].*(ti.f);
+      const void* sp = src ? src[i].*(ti.f) : nullptr;
+      if (!m) continue;
+      const long long nel = tensor_numel(cfg, k);
+      float* op_f32 = (ti.gain && o != (void*)m) ? (float*)o : nullptr;
+      __nv_bfloat16* op_bf = ti.gain ? nullptr : (__nv_bfloat16*)o;
       if (init == EE_INIT_COPY) {
-        if (!t.src)
+        if (!sp)
           return fail(EE_ERR_STRUCTURE, "Copy init: source module %s of exit %d is missing",
-                      t.name, i);
-        if (!aligned16(t.src)) return fail(EE_ERR_ALIGN, "copy source not 16-byte aligned");
-        Prof p_("a0_init_copy", st, 0, 0, 8.0 * t.n);
-        EE_CUDA(launch_copy_cast(t.src, src_dtype == EE_DTYPE_F32, t.m, op_bf, op_f32, t.n, st));
-      } else if (t.gain) {
-        Prof p_("a0_init_fill", st, 0, 0, 8.0 * t.n);
-        EE_CUDA(launch_fill(t.m, op_f32, t.n, 1.0f, st));
+                      ti.name, i);
+        if (!aligned16(sp)) return fail(EE_ERR_ALIGN, "copy source not 16-byte aligned");
+        Prof p_("a0_init_copy", st, 0, 0, 8.0 * nel);
+        EE_CUDA(launch_copy_cast(sp, src_dtype == EE_DTYPE_F32, m, op_bf, op_f32, nel, st));
+      } else if (ti.gain) {
+        Prof p_("a0_init_fill", st, 0, 0, 8.0 * nel);
+        EE_CUDA(launch_fill(m, op_f32, nel, 1.0f, st));
       } else {
-        Prof p_("a0_init_random", st, 0, 0, 6.0 * t.n);
-        EE_CUDA(launch_random_normal(seed, (uint64_t)i * 16 + k, stdv, t.m, op_bf, t.n, st));
+        Prof p_("a0_init_random", st, 0, 0, 6.0 * nel);
+        EE_CUDA(launch_random_normal(seed, (uint64_t)i * 16 + k, stdv, m, op_bf, nel, st));
       }
     }
   }
@@ -1027,25 +1245,21 @@ ee_status ee_adam_update(const ee_head_config* cfg, ee_head_tensors* master, ee_
   cudaStream_t st = (cudaStream_t)stream;
   const float bc1 = (float)(1.0 - std::pow((double)beta1, (double)step));
   const float bc2 = (float)(1.0 - std::pow((double)beta2, (double)step));
-  const long long h = cfg->hidden, F = cfg->ffn, Vl = cfg->vocab_end - cfg->vocab_begin;
   for (int i = 0; i < cfg->num_exits; ++i) {
     if ((s = check_arch_tensors(cfg, m[i], "m", i)) != EE_OK) return s;
     if ((s = check_arch_tensors(cfg, v[i], "v", i)) != EE_OK) return s;
-    void* const mp[6] = {master[i].g_a, master[i].w_gate, master[i].w_up, master[i].w_down, master[i].g_f, master[i].w_out};
-    void* const opp[6] = {op[i].g_a, op[i].w_gate, op[i].w_up, op[i].w_down, op[i].g_f, op[i].w_out};
-    void* const gp[6] = {grads[i].g_a, grads[i].w_gate, grads[i].w_up, grads[i].w_down, grads[i].g_f, grads[i].w_out};
-    void* const m1[6] = {m[i].g_a, m[i].w_gate, m[i].w_up, m[i].w_down, m[i].g_f, m[i].w_out};
-    void* const v1[6] = {v[i].g_a, v[i].w_gate, v[i].w_up, v[i].w_down, v[i].g_f, v[i].w_out};
-    const long long ns[6] = {h, F * h, F * h, h * F, h, Vl * h};
-    const bool gain[6] = {true, false, false, false, true, false};
-    for (int k = 0; k < 6; ++k) {
-      if (!mp[k]) continue;
-      float* opf = (gain[k] && opp[k] != mp[k]) ? (float*)opp[k] : nullptr;
-      __nv_bfloat16* opb = gain[k] ? nullptr : (__nv_bfloat16*)opp[k];
-      Prof p_("a15_adam", st, 0, 0, 30.0 * ns[k]);
-      EE_CUDA(launch_adam((float*)mp[k], opb, opf, (const float*)gp[k], (float*)m1[k],
-                          (float*)v1[k], ns[k], lr, beta1, beta2, eps, wd, bc1, bc2, grad_scale,
-                          st));
+    for (int k = 0; k < NTENS; ++k) {
+      const TInfo& ti = kTens[k];
+      float* mp = (float*)(master[i].*(ti.f));
+      if (!mp) continue;
+      void* opp = op[i].*(ti.f);
+      float* opf = (ti.gain && opp != (void*)mp) ? (float*)opp : nullptr;
+      __nv_bfloat16* opb = ti.gain ? nullptr : (__nv_bfloat16*)opp;
+      const long long nel = tensor_numel(cfg, k);
+      Prof p_("a15_adam", st, 0, 0, 30.0 * nel);
+      EE_CUDA(launch_adam(mp, opb, opf, (const float*)(grads[i].*(ti.f)), (float*)(m[i].*(ti.f)),
+                          (float*)(v[i].*(ti.f)), nel, lr, beta1, beta2, eps, wd, bc1, bc2,
+                          grad_scale, st));
     }
   }
   return EE_OK;
@@ -1058,25 +1272,18 @@ ee_status ee_sgd_update(const ee_head_config* cfg, ee_head_tensors* master, ee_h
   if (s != EE_OK) return s;
   if (momentum != 0.f && !buf) return fail(EE_ERR_ARG, "momentum buffer required");
   cudaStream_t st = (cudaStream_t)stream;
-  const long long h = cfg->hidden, F = cfg->ffn, Vl = cfg->vocab_end - cfg->vocab_begin;
   for (int i = 0; i < cfg->num_exits; ++i) {
-    void* const mp[6] = {master[i].g_a, master[i].w_gate, master[i].w_up, master[i].w_down, master[i].g_f, master[i].w_out};
-    void* const opp[6] = {op[i].g_a, op[i].w_gate, op[i].w_up, op[i].w_down, op[i].g_f, op[i].w_out};
-    void* const gp[6] = {grads[i].g_a, grads[i].w_gate, grads[i].w_up, grads[i].w_down, grads[i].g_f, grads[i].w_out};
-    void* b1[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-    if (buf) {
-      b1[0] = buf[i].g_a; b1[1] = buf[i].w_gate; b1[2] = buf[i].w_up;
-      b1[3] = buf[i].w_down; b1[4] = buf[i].g_f; b1[5] = buf[i].w_out;
-    }
-    const long long ns[6] = {h, F * h, F * h, h * F, h, Vl * h};
-    const bool gain[6] = {true, false, false, false, true, false};
-    for (int k = 0; k < 6; ++k) {
-      if (!mp[k]) continue;
-      float* opf = (gain[k] && opp[k] != mp[k]) ? (float*)opp[k] : nullptr;
-      __nv_bfloat16* opb = gain[k] ? nullptr : (__nv_bfloat16*)opp[k];
-      Prof p_("a15_sgd", st, 0, 0, 14.0 * ns[k]);
-      EE_CUDA(launch_sgd((float*)mp[k], opb, opf, (const float*)gp[k],
-                         momentum != 0.f ? (float*)b1[k] : nullptr, ns[k], lr, momentum,
+    for (int k = 0; k < NTENS; ++k) {
+      const TInfo& ti = kTens[k];
+      float* mp = (float*)(master[i].*(ti.f));
+      if (!mp) continue;
+      void* opp = op[i].*(ti.f);
+      float* opf = (ti.gain && opp != (void*)mp) ? (float*)opp : nullptr;
+      __nv_bfloat16* opb = ti.gain ? nullptr : (__nv_bfloat16*)opp;
+      float* bk = (buf && momentum != 0.f) ? (float*)(buf[i].*(ti.f)) : nullptr;
+      const long long nel = tensor_numel(cfg, k);
+      Prof p_("a15_sgd", st, 0, 0, 14.0 * nel);
+      EE_CUDA(launch_sgd(mp, opb, opf, (const float*)(grads[i].*(ti.f)), bk, nel, lr, momentum,
                          grad_scale, st));
     }
   }
@@ -1150,7 +1357,7 @@ ee_status ee_test_attention(const void* q, const void* k, const void* v, void* o
                             (const __nv_bfloat16*)v, (const __nv_bfloat16*)o,
                             (const __nv_bfloat16*)dout, lse2, scratch, (__nv_bfloat16*)dq,
                             (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, n_tokens, seq_len, n_heads,
-                            n_kv_heads, st));
+                            n_kv_heads, 0.f, st));
   }
   return EE_OK;
 }

@@ -5,7 +5,9 @@
 //   x += W_o attn(RoPE(W_q u), RoPE(W_k u), W_v u),   u  = RMSNorm(x; g_att)
 //   x += W_down(silu(W_gate u') * W_up u'),           u' = RMSNorm(x; g_mlp)
 // The projections and the MLP run on the tcgen05 GEMM (gemm.cuh); this file
-// holds RoPE, causal flash attention (forward only) and the residual casts.
+// holds the causal flash attention (forward and backward) and the residual
+// casts; RoPE is fused into the q/k projection epilogues (gemm.cuh) and, as
+// RoPE^T, into the attention backward's dq/dk stores.
 //
 // Attention is ~2% of a Llama-2 layer's FLOPs at T = 2048 (4 T h / 2 vs
 // 2 (2 h^2 + 2 h h_kv + 3 h F) per token), so it uses warp-level mma.sync
@@ -17,33 +19,6 @@
 #include "internal.cuh"
 
 namespace ee {
-
-// ---------------------------------------------------------------- RoPE
-// In place on x [N x H x 128] bf16 (Llama rotate-half): for i < 64,
-// angle = (row % T) * theta^(-2i/128);  (x_i, x_{i+64}) -> rotated.
-__global__ void rope_kernel(__nv_bfloat16* __restrict__ x, long long N, int H, int T, float theta) {
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // (row, head, i)
-  const long long total = N * H * 64;
-  if (idx >= total) return;
-  const int i = (int)(idx & 63);
-  const long long rh = idx >> 6;
-  const long long row = rh / H;
-  const int pos = (int)(row % T);
-  __nv_bfloat16* p = x + rh * 128;
-  const float inv = powf(theta, -2.0f * (float)i / 128.0f);
-  float s, c;
-  sincosf((float)pos * inv, &s, &c);
-  const float a = __bfloat162float(p[i]), b = __bfloat162float(p[i + 64]);
-  p[i] = __float2bfloat16_rn(a * c - b * s);
-  p[i + 64] = __float2bfloat16_rn(b * c + a * s);
-}
-
-cudaError_t launch_rope(__nv_bfloat16* x, long long N, int H, int T, float theta, cudaStream_t s) {
-  const long long total = N * H * 64;
-  if (total == 0) return cudaSuccess;
-  rope_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(x, N, H, T, theta);
-  return cudaGetLastError();
-}
 
 // ---------------------------------------------------------------- casts
 __global__ void cast_bf16_f32_kernel(const __nv_bfloat16* __restrict__ a, float* __restrict__ b,
@@ -266,6 +241,27 @@ __global__ void attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ o,
   if (lane == 0) Dv[w] = acc;
 }
 
+// RoPE^T (rotation by -angle) applied in fp32 to an accumulator fragment
+// acc[nb][e] = row (pos0 + (e >= 2 ? 8 : 0)), column nb * 8 + 2c + (e & 1) of a
+// 128-wide head: column i (nb < 8) pairs with i + 64 (nb + 8) in this thread.
+__device__ __forceinline__ void rope_t_frag(float (&acc)[ATT_D / 8][4], int pos0, int c,
+                                            float theta) {
+#pragma unroll
+  for (int nb = 0; nb < ATT_D / 16; ++nb) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int i = nb * 8 + 2 * c + (e & 1);
+      const float pos = (float)(pos0 + (e >= 2 ? 8 : 0));
+      const float inv = powf(theta, -2.0f * (float)i / 128.0f);
+      float sn, cs;
+      sincosf(pos * inv, &sn, &cs);
+      const float a = acc[nb][e], b = acc[nb + 8][e];
+      acc[nb][e] = a * cs + b * sn;
+      acc[nb + 8][e] = b * cs - a * sn;
+    }
+  }
+}
+
 __device__ __forceinline__ void ldmatrix_x4(uint32_t (&r)[4], const void* p) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -276,7 +272,8 @@ __global__ void __launch_bounds__(128) attn_bwd_dkdv_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
     const __nv_bfloat16* __restrict__ v, const __nv_bfloat16* __restrict__ dout,
     const float* __restrict__ lse2, const float* __restrict__ Dv, __nv_bfloat16* __restrict__ dk,
-    __nv_bfloat16* __restrict__ dv, int T, int Hq, int Hkv, float scale_log2, float scale) {
+    __nv_bfloat16* __restrict__ dv, int T, int Hq, int Hkv, float scale_log2, float scale,
+    float rope_theta) {
   __shared__ __align__(16) __nv_bfloat16 Qs[ATT_BQ][ATT_D + ATT_PAD];
   __shared__ __align__(16) __nv_bfloat16 Os[ATT_BQ][ATT_D + ATT_PAD];  // dO tile
   __shared__ float Ls[ATT_BQ], Ds[ATT_BQ];
@@ -384,6 +381,7 @@ __global__ void __launch_bounds__(128) attn_bwd_dkdv_kernel(
       }
     }
   }
+  if (rope_theta > 0.f) rope_t_frag(dka, kpos0, c, rope_theta);
   __nv_bfloat16* k0 = dk + (krow0 + g) * ldk + hk * ATT_D + 2 * c;
   __nv_bfloat16* v0 = dv + (krow0 + g) * ldk + hk * ATT_D + 2 * c;
 #pragma unroll
@@ -400,7 +398,7 @@ __global__ void __launch_bounds__(128) attn_bwd_dq_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
     const __nv_bfloat16* __restrict__ v, const __nv_bfloat16* __restrict__ dout,
     const float* __restrict__ lse2, const float* __restrict__ Dv, __nv_bfloat16* __restrict__ dq,
-    int T, int Hq, int Hkv, float scale_log2, float scale) {
+    int T, int Hq, int Hkv, float scale_log2, float scale, float rope_theta) {
   __shared__ __align__(16) __nv_bfloat16 Ks[ATT_BK][ATT_D + ATT_PAD];
   __shared__ __align__(16) __nv_bfloat16 Vs[ATT_BK][ATT_D + ATT_PAD];
   const int qt = blockIdx.x, hq = blockIdx.y, b = blockIdx.z;
@@ -489,6 +487,7 @@ __global__ void __launch_bounds__(128) attn_bwd_dq_kernel(
       }
     }
   }
+  if (rope_theta > 0.f) rope_t_frag(dqa, qpos0, c, rope_theta);
   __nv_bfloat16* q0 = dq + (qrow0 + g) * ldq + hq * ATT_D + 2 * c;
 #pragma unroll
   for (int nb = 0; nb < ATT_D / 8; ++nb) {
@@ -501,7 +500,8 @@ __global__ void __launch_bounds__(128) attn_bwd_dq_kernel(
 cudaError_t launch_attn_bwd(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                             const __nv_bfloat16* o, const __nv_bfloat16* dout, const float* lse2,
                             float* Dv, __nv_bfloat16* dq, __nv_bfloat16* dk, __nv_bfloat16* dv,
-                            long long N, int T, int Hq, int Hkv, cudaStream_t s) {
+                            long long N, int T, int Hq, int Hkv, float rope_theta,
+                            cudaStream_t s) {
   if (N == 0) return cudaSuccess;
   const float scale = 1.0f / sqrtf((float)ATT_D);
   const float scale_log2 = 1.4426950408889634f * scale;
@@ -511,39 +511,14 @@ cudaError_t launch_attn_bwd(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
   if (e != cudaSuccess) return e;
   dim3 g1(T / ATT_BK, Hkv, (unsigned)(N / T));
   attn_bwd_dkdv_kernel<<<g1, 128, 0, s>>>(q, k, v, dout, lse2, Dv, dk, dv, T, Hq, Hkv, scale_log2,
-                                          scale);
+                                          scale, rope_theta);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   dim3 g2(T / ATT_BQ, Hq, (unsigned)(N / T));
-  attn_bwd_dq_kernel<<<g2, 128, 0, s>>>(q, k, v, dout, lse2, Dv, dq, T, Hq, Hkv, scale_log2, scale);
+  attn_bwd_dq_kernel<<<g2, 128, 0, s>>>(q, k, v, dout, lse2, Dv, dq, T, Hq, Hkv, scale_log2, scale,
+                                        rope_theta);
   return cudaGetLastError();
 }
 
-// RoPE backward: rotate by -angle (the rotation is orthogonal).
-__global__ void rope_bwd_kernel(__nv_bfloat16* __restrict__ x, long long N, int H, int T,
-                                float theta) {
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long total = N * H * 64;
-  if (idx >= total) return;
-  const int i = (int)(idx & 63);
-  const long long rh = idx >> 6;
-  const long long row = rh / H;
-  const int pos = (int)(row % T);
-  __nv_bfloat16* p = x + rh * 128;
-  const float inv = powf(theta, -2.0f * (float)i / 128.0f);
-  float s, c;
-  sincosf((float)pos * inv, &s, &c);
-  const float a = __bfloat162float(p[i]), b = __bfloat162float(p[i + 64]);
-  p[i] = __float2bfloat16_rn(a * c + b * s);
-  p[i + 64] = __float2bfloat16_rn(b * c - a * s);
-}
-
-cudaError_t launch_rope_bwd(__nv_bfloat16* x, long long N, int H, int T, float theta,
-                            cudaStream_t s) {
-  const long long total = N * H * 64;
-  if (total == 0) return cudaSuccess;
-  rope_bwd_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(x, N, H, T, theta);
-  return cudaGetLastError();
-}
 
 }  // namespace ee

@@ -225,6 +225,7 @@ cudaError_t gemm_run(int epi, bool a_kmajor, bool b_kmajor, const Mat& A, const 
   EE_GEMM_CASE(EPI_CE_DS, false, false)
   EE_GEMM_CASE(EPI_F32T, false, true)
   EE_GEMM_CASE(EPI_BF16, false, false)
+  EE_GEMM_CASE(EPI_BF16, false, true)
 #undef EE_GEMM_CASE
   return cudaErrorNotSupported;
 }

@@ -69,6 +69,8 @@ struct GemmArgs {
   const __nv_bfloat16* resid;
   long long ld_resid;
   __nv_bfloat16* outb;  // EPI_BF16 output (ldo)
+  int rope_seq;         // EPI_BF16: > 0 = apply RoPE (rotate-half, head dim 128; N % 128 == 0)
+  float rope_theta;     //   at position row % rope_seq before the bf16 rounding
   // SwiGLU
   __nv_bfloat16* ab;  // [M x 2F]: A in columns [0,F), B in [F,2F)
   long long ld_ab;
@@ -106,6 +108,16 @@ __device__ __forceinline__ unsigned long long trace_stamp() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
   return (t << 8) | (sm & 0xFF);
+}
+
+// 16 bf16 (32 bytes): one 256-bit store when aligned, else two 128-bit stores.
+__device__ __forceinline__ void store16_bf16(__nv_bfloat16* p, const uint32_t (&w)[8]) {
+  if (aligned32(p)) {
+    st_global_v8(p, w);
+  } else {
+    *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+    *reinterpret_cast<uint4*>(p + 8) = make_uint4(w[4], w[5], w[6], w[7]);
+  }
 }
 
 // Epilogue of one accumulator tile: thread `row` of the 128 epilogue threads
@@ -167,6 +179,47 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
     }
   } else if constexpr (EPI == EPI_BF16) {
     __nv_bfloat16* orow = row_ok ? args.outb + (long long)gm * args.ldo : nullptr;
+    if (args.rope_seq > 0) {
+      // Fused RoPE (Llama rotate-half): the N-tile holds GEMM_BN / 128 whole
+      // heads, and this thread holds both x_i and x_{i+64} of each for its row;
+      // rotate in fp32 by angle pos * theta^(-2i/128), then round to bf16 once.
+      const float pos = (float)(gm % args.rope_seq);
+#pragma unroll 1
+      for (int hc = 0; hc < (GEMM_BN / 128) * 2; ++hc) {
+        const int hd = hc >> 1, c = hc & 1;  // head within the tile, 32-column chunk
+        if (nb * GEMM_BN + hd * 128 >= args.N) break;
+        // one load per wait: the asm outputs are only valid after wait::ld
+        uint32_t v0[32], v1[32];
+        tmem_ld_32x32b_x32(tb + hd * 128 + c * 32, v0);
+        tmem_ld_wait();
+        tmem_ld_32x32b_x32(tb + hd * 128 + (c + 2) * 32, v1);
+        tmem_ld_wait();
+        if (!row_ok) continue;
+        uint32_t w0[2][8], w1[2][8];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          float ra[2], rb[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int i = c * 32 + 2 * q + e;
+            const float inv = powf(args.rope_theta, -2.0f * (float)i / 128.0f);
+            float sn, cs;
+            sincosf(pos * inv, &sn, &cs);
+            const float a = u2f(v0[2 * q + e]), b = u2f(v1[2 * q + e]);
+            ra[e] = a * cs - b * sn;
+            rb[e] = b * cs + a * sn;
+          }
+          w0[q >> 3][q & 7] = pack_bf16(ra[0], ra[1]);
+          w1[q >> 3][q & 7] = pack_bf16(rb[0], rb[1]);
+        }
+        __nv_bfloat16* p0 = orow + nb * GEMM_BN + hd * 128 + c * 32;
+        store16_bf16(p0, w0[0]);
+        store16_bf16(p0 + 16, w0[1]);
+        store16_bf16(p0 + 64, w1[0]);
+        store16_bf16(p0 + 80, w1[1]);
+      }
+      return;
+    }
 #pragma unroll 1
     for (int c = 0; c < GEMM_BN / 32; ++c) {
       uint32_t v[32];

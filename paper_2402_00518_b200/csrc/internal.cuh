@@ -40,7 +40,8 @@ cudaError_t launch_rmsnorm_fwd(const void* in, bool in_f32, const float* g, floa
 // rmsnorm backward: dz fp32, y (bf16/fp32), r, g -> dy bf16 (nullable), dg partials
 cudaError_t launch_rmsnorm_bwd(const float* dz, const void* y, bool y_f32, const float* r,
                                const float* g, __nv_bfloat16* dy, float* dg_part, long long n,
-                               int h, int rows_per_block, cudaStream_t s);
+                               int h, int rows_per_block, cudaStream_t s,
+                               const __nv_bfloat16* add = nullptr);  // dy = add + dx
 // gain grad: dg partials of sum_t du_t * x_t * r_t
 cudaError_t launch_gain_grad(const float* du, const __nv_bfloat16* x, const float* r,
                              float* dg_part, long long n, int h, int rows_per_block,
@@ -83,16 +84,14 @@ cudaError_t launch_first_exit(const float* const* conf, int E, long long n, floa
                               int32_t* out, cudaStream_t s);
 
 // backbone partial forward (backbone.cu)
-cudaError_t launch_rope(__nv_bfloat16* x, long long N, int H, int T, float theta, cudaStream_t s);
 cudaError_t launch_attn_fwd(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                             __nv_bfloat16* o, long long N, int T, int Hq, int Hkv, float* lse2,
                             cudaStream_t s);
 cudaError_t launch_attn_bwd(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                             const __nv_bfloat16* o, const __nv_bfloat16* dout, const float* lse2,
                             float* Dv, __nv_bfloat16* dq, __nv_bfloat16* dk, __nv_bfloat16* dv,
-                            long long N, int T, int Hq, int Hkv, cudaStream_t s);
-cudaError_t launch_rope_bwd(__nv_bfloat16* x, long long N, int H, int T, float theta,
-                            cudaStream_t s);
+                            long long N, int T, int Hq, int Hkv, float rope_theta,
+                            cudaStream_t s);  // rope_theta > 0: fused RoPE^T on dq, dk
 cudaError_t launch_cast_bf16_f32(const __nv_bfloat16* a, float* b, long long n, cudaStream_t s);
 cudaError_t launch_cast_f32_bf16(const float* a, __nv_bfloat16* b, long long n, cudaStream_t s);
 

@@ -137,8 +137,8 @@ cudaError_t launch_rmsnorm_fwd(const void* in, bool in_f32, const float* g, floa
 template <typename TY>
 __global__ void rmsnorm_bwd_kernel(const float* __restrict__ dz, const TY* __restrict__ y,
                                    const float* __restrict__ r, const float* __restrict__ g,
-                                   __nv_bfloat16* __restrict__ dy, float* __restrict__ dg_part,
-                                   long long n, int h, int rpb) {
+                                   __nv_bfloat16* dy, const __nv_bfloat16* add,
+                                   float* __restrict__ dg_part, long long n, int h, int rpb) {
   __shared__ float red[33];
   const int nchunk = h / 8;
   float gv[NORM_CHUNKS][8], acc[NORM_CHUNKS][8];
@@ -178,6 +178,12 @@ __global__ void rmsnorm_bwd_kernel(const float* __restrict__ dz, const TY* __res
           float o[8];
 #pragma unroll
           for (int k = 0; k < 8; ++k) o[k] = rr * (gv[i][k] * d[i][k] - yh[i][k] * mean);
+          if (add != nullptr) {  // residual branch (may alias dy: same thread, read first)
+            float a8[8];
+            load8(add + row * h + c * 8, a8);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) o[k] += a8[k];
+          }
           store8(dy + row * h + c * 8, o);
         }
       }
@@ -196,15 +202,16 @@ __global__ void rmsnorm_bwd_kernel(const float* __restrict__ dz, const TY* __res
 
 cudaError_t launch_rmsnorm_bwd(const float* dz, const void* y, bool y_f32, const float* r,
                                const float* g, __nv_bfloat16* dy, float* dg_part, long long n,
-                               int h, int rpb, cudaStream_t s) {
+                               int h, int rpb, cudaStream_t s, const __nv_bfloat16* add) {
   const unsigned nb = (unsigned)((n + rpb - 1) / rpb);
   if (nb == 0) return cudaSuccess;
   const int t = norm_threads(h);
   if (y_f32)
-    rmsnorm_bwd_kernel<float><<<nb, t, 0, s>>>(dz, (const float*)y, r, g, dy, dg_part, n, h, rpb);
+    rmsnorm_bwd_kernel<float>
+        <<<nb, t, 0, s>>>(dz, (const float*)y, r, g, dy, add, dg_part, n, h, rpb);
   else
     rmsnorm_bwd_kernel<__nv_bfloat16>
-        <<<nb, t, 0, s>>>(dz, (const __nv_bfloat16*)y, r, g, dy, dg_part, n, h, rpb);
+        <<<nb, t, 0, s>>>(dz, (const __nv_bfloat16*)y, r, g, dy, add, dg_part, n, h, rpb);
   return cudaGetLastError();
 }
 

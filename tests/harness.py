@@ -20,7 +20,15 @@ from oracle import ee_oracle as O
 
 LOSS_RTOL = 1e-3
 GRAD_RTOL = 2e-2
-TENSORS = ("g_a", "w_gate", "w_up", "w_down", "g_f", "w_out")
+TENSORS = ("g_a", "w_gate", "w_up", "w_down", "g_f", "w_out", "g_att", "w_q", "w_k", "w_v", "w_o")
+
+
+def attn_kwargs(cfg):
+    """make_config keywords for the Layer exit's attention geometry."""
+    if cfg.arch != "layer":
+        return {}
+    return dict(n_heads=cfg.n_heads, n_kv_heads=cfg.n_kv_heads or cfg.n_heads,
+                seq_len=cfg.seq_len)
 
 
 def gpu_step(ee, cfg, hidden, targets, params, exit_weights, accumulate=False, grads=None,
@@ -31,7 +39,7 @@ def gpu_step(ee, cfg, hidden, targets, params, exit_weights, accumulate=False, g
     E = len(hidden)
     n = targets.numel()
     c = ee.make_config(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch, eps,
-                       token_weighting=weighting)
+                       token_weighting=weighting, **attn_kwargs(cfg))
     hid = [h.cuda().contiguous() for h in hidden]
     tg = targets.cuda().to(torch.int32).contiguous()
     ops = [{k: (v.cuda().float().contiguous() if k.startswith("g_") else
@@ -50,11 +58,11 @@ def gpu_step(ee, cfg, hidden, targets, params, exit_weights, accumulate=False, g
     return loss, grads, aux, (code, idx)
 
 
-def oracle_exit(arch, params, hidden, targets, alpha, eps=1e-5, weighting="uniform"):
+def oracle_exit(arch, params, hidden, targets, alpha, eps=1e-5, weighting="uniform", attn=None):
     """fp64 oracle on the same bytes (bf16/fp32 inputs widened exactly)."""
     p64 = {k: to_f64(v) for k, v in params.items()}
     return O.exit_loss_and_grads(arch, p64, to_f64(hidden), targets.cpu().numpy().astype(np.int64),
-                                 float(alpha), eps, keep_act=True, weighting=weighting)
+                                 float(alpha), eps, keep_act=True, weighting=weighting, attn=attn)
 
 
 def rel_fro(a, b):
