@@ -102,10 +102,26 @@ class ClockSampler:
 
 def step_flops(cfg, n):
     """Algorithmic FLOPs of one step: 6hV (+18hF for MLP) per
-    token per exit; Embedding exits have no dz GEMM (4hV)."""
+    token per exit; Embedding exits have no dz GEMM (4hV).  Layer exits add
+    the attention projections, 6 (2h^2 + 2h hkv), and the causal attention
+    core, 6h(T+1)/... = 2h(T+1) forward + 4h(T+1) backward (dV, dP, dQ, dK;
+    the recomputed S and dP are not counted)."""
     h, V, F = cfg.hidden, cfg.vocab, cfg.ffn
-    per = (4 if cfg.arch == "embedding" else 6) * h * V + (18 * h * F if cfg.arch == "mlp" else 0)
+    per = (4 if cfg.arch == "embedding" else 6) * h * V
+    if cfg.arch in ("mlp", "layer"):
+        per += 18 * h * F
+    if cfg.arch == "layer":
+        hkv = 128 * (cfg.n_kv_heads or cfg.n_heads)
+        per += 12 * h * h + 12 * h * hkv + 6 * h * (cfg.seq_len + 1)
     return per * n * cfg.exits
+
+
+def attn_kw(cfg):
+    """make_config / HeadSpec keywords of a Layer exit's attention geometry."""
+    if cfg.arch != "layer":
+        return {}
+    return dict(n_heads=cfg.n_heads, n_kv_heads=cfg.n_kv_heads or cfg.n_heads,
+                seq_len=cfg.seq_len)
 
 
 def cpu_oracle_inputs(cfg, n_sub, seed):
@@ -115,7 +131,9 @@ def cpu_oracle_inputs(cfg, n_sub, seed):
     import eesynth as S
     from eesynth import to_f64
     one = S.Cfg(name=cfg.name, hidden=cfg.hidden, vocab=cfg.vocab, ffn=cfg.ffn, arch=cfg.arch,
-                tokens=n_sub, layers=cfg.layers, after=cfg.after[:1], init=cfg.init, seed=cfg.seed)
+                tokens=n_sub, layers=cfg.layers, after=cfg.after[:1], init=cfg.init, seed=cfg.seed,
+                n_heads=cfg.n_heads, n_kv_heads=cfg.n_kv_heads,
+                seq_len=min(cfg.seq_len, n_sub) if cfg.arch == "layer" else 0)
     p = S.head_params(one, seed=seed)[0]
     p64 = {}
     for k in list(p):
@@ -134,9 +152,13 @@ def cpu_oracle_time(cfg, inputs):
         cores = max([i.get("num_threads", 1) for i in threadpool_info()] or [os.cpu_count()])
     except Exception:
         cores = os.cpu_count()
+    import eesynth as S
     p64, x, y = inputs
+    at = None
+    if cfg.arch == "layer":     # the sample is one sequence of len(x) tokens
+        at = dict(S.attn_geometry(cfg), seq_len=x.shape[0])
     t0 = time.perf_counter()
-    O.exit_loss_and_grads(cfg.arch, p64, x, y, 1.0, 1e-5)
+    O.exit_loss_and_grads(cfg.arch, p64, x, y, 1.0, 1e-5, attn=at)
     return time.perf_counter() - t0, cores
 
 
@@ -159,7 +181,9 @@ def run_reference(args, cfg, rank, world):
     t_step = statistics.mean(times) * cfg.exits       # all exits of the step
     value = n_sub / t_step
     sample = (f"fp64 oracle, exit 1 of {cfg.exits} on {n_sub} tokens at full h/V/F, "
-              f"scaled x{cfg.exits} exits; Adam not included")
+              f"scaled x{cfg.exits} exits; Adam not included"
+              + ("; Layer exit: one sequence of that many tokens (the T-dependent attention "
+                 "core is ~2% of the per-token work at T = 2048)" if cfg.arch == "layer" else ""))
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
@@ -304,19 +328,22 @@ def main():
     if vp:
         gbuf = 0
     heads = ee.ExitHeads(ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch,
-                                     vocab_begin=vb, vocab_end=ve), n_all, device=dev,
-                         grad_buffers=gbuf if gbuf > 0 else None)
+                                     vocab_begin=vb, vocab_end=ve, **attn_kw(cfg)), n_all,
+                         device=dev, grad_buffers=gbuf if gbuf > 0 else None)
     per_exit = heads.grad_buffers < E
     args.per_exit = per_exit
     bb = S.backbone(cfg, device=dev)
     src = []
     for k in cfg.after:
         d = {"w_out": bb["w_out"][vb:ve]}
-        if cfg.arch in ("norm", "mlp"):
+        if cfg.arch != "embedding":
             d["g_f"] = bb["final_norm"]
-        if cfg.arch == "mlp":
-            L = bb["layers"][k]
+        if cfg.arch in ("mlp", "layer"):
+            # MLP: the same layer's MLP; Layer: the last layer
+            L = bb["layers"][k if cfg.arch == "mlp" else cfg.layers]
             d.update(g_a=L["mlp_norm"], w_gate=L["w_gate"], w_up=L["w_up"], w_down=L["w_down"])
+            if cfg.arch == "layer":
+                d.update({t: L[t] for t in ("g_att", "w_q", "w_k", "w_v", "w_o")})
         src.append(d)
     heads.init("copy", copy_src=src)
     torch.cuda.synchronize()
@@ -343,7 +370,7 @@ def main():
     vc = torch.zeros(1, dtype=torch.int64, device=dev)
     job_tokens = n_all if vp else n * world
     total_iters = 40000
-    one_cfg = ee.make_config(cfg.hidden, cfg.vocab, cfg.ffn, 1, cfg.arch)
+    one_cfg = ee.make_config(cfg.hidden, cfg.vocab, cfg.ffn, 1, cfg.arch, **attn_kw(cfg))
 
     def step(it, hid=hidden, tg=targets):
         lr = ee.ee_lr_at(min(it + 1, total_iters), total_iters)
