@@ -104,7 +104,7 @@ def load(path: str = LIB_PATH):
         "ee_last_error": (ctypes.c_char_p, []),
         "ee_version": (ctypes.c_char_p, []),
         "ee_test_gemm": (I32, [I32, I32, P, P, P, I32, I32, I32, I32, P]),
-        "ee_test_attention": (I32, [P, P, P, P, P, P, P, P, P, P, I64, I32, I32, I32, P]),
+        "ee_test_attention": (I32, [P, P, P, P, P, P, P, P, P, P, I64, I32, I32, I32, I32, P]),
         "ee_profile_start": (I32, []),
         "ee_profile_stop": (I32, [ctypes.POINTER(I32)]),
         "ee_profile_record": (I32, [I32, ctypes.c_char_p, I32, ctypes.POINTER(F32),
@@ -305,11 +305,11 @@ def ee_test_gemm(A, B, C, a_kmajor, b_kmajor, M, N, K, accumulate=False, stream=
 
 
 def ee_test_attention(q, k, v, o, lse2, seq_len, n_heads, n_kv_heads, dout=None, dq=None,
-                      dk=None, dv=None, scratch=None, stream=None):
+                      dk=None, dv=None, scratch=None, impl=1, stream=None):
     load()
     _check(_lib.ee_test_attention(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse2), _ptr(dout),
                                   _ptr(dq), _ptr(dk), _ptr(dv), _ptr(scratch), q.shape[0],
-                                  seq_len, n_heads, n_kv_heads, _stream(stream)))
+                                  seq_len, n_heads, n_kv_heads, int(impl), _stream(stream)))
 
 
 def _aux1(aux):

@@ -280,6 +280,19 @@ struct Prof {
   }
 };
 
+// Attention forward: the tcgen05 kernel (attn_tc.cu) unless EE_ATTN_TC=0 selects
+// the mma.sync kernel (A/B measurements).
+cudaError_t attn_forward(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
+                         __nv_bfloat16* o, long long n, int T, int Hq, int Hkv, float* lse2,
+                         cudaStream_t st) {
+  static const int tc = [] {
+    const char* e = getenv("EE_ATTN_TC");
+    return e ? atoi(e) : 1;
+  }();
+  return tc ? launch_attn_fwd_tc(q, k, v, o, n, T, Hq, Hkv, lse2, st)
+            : launch_attn_fwd(q, k, v, o, n, T, Hq, Hkv, lse2, st);
+}
+
 GemmArgs base_args(int M, int N, int K) {
   GemmArgs a;
   memset(&a, 0, sizeof(a));
@@ -454,7 +467,7 @@ ee_status layer_attn_forward(const ee_head_config* cfg, const Bufs& B, const ee_
   }
   { const double fl = 2.0 * (double)n * h * (cfg->seq_len + 1);  // causal: 2 GEMMs x T/2 keys
     Prof p_("L4_attn_fwd", st, 2.0 * (double)n * h * (cfg->seq_len + 64), fl, 0);
-    EE_CUDA(launch_attn_fwd(B.q, B.k, B.v, B.o, n, cfg->seq_len, Hq, Hkv, B.lse2, st)); }
+    EE_CUDA(attn_forward(B.q, B.k, B.v, B.o, n, cfg->seq_len, Hq, Hkv, B.lse2, st)); }
   {
     GemmArgs a = base_args((int)n, h, h);
     a.out0 = B.x1;
@@ -954,7 +967,7 @@ ee_status ee_backbone_forward(const ee_backbone_config* cfg, const ee_layer_tens
     }
     { const double fl = 2.0 * 2.0 * (double)n * (cfg->seq_len + 64) / 2.0 * h;  // causal
       Prof p_("bb_attention", st, fl, fl, 0);
-      EE_CUDA(launch_attn_fwd(q, k, v, o, n, cfg->seq_len, Hq, Hkv, nullptr, st)); }
+      EE_CUDA(attn_forward(q, k, v, o, n, cfg->seq_len, Hq, Hkv, nullptr, st)); }
     {  // x += o W_o^T
       GemmArgs a = base_args((int)n, h, h);
       a.out0 = x;
@@ -1341,16 +1354,21 @@ int32_t ee_debug_trace_read(uint64_t* host, int32_t max) {
 ee_status ee_test_attention(const void* q, const void* k, const void* v, void* o, float* lse2,
                             const void* dout, void* dq, void* dk, void* dv, float* scratch,
                             int64_t n_tokens, int32_t seq_len, int32_t n_heads, int32_t n_kv_heads,
-                            void* stream) {
+                            int32_t impl, void* stream) {
   if (!q || !k || !v || !o || !lse2 || n_tokens < 0 || seq_len < 64 || seq_len % 64 ||
       n_tokens % seq_len || n_heads < 1 || n_kv_heads < 1 || n_heads % n_kv_heads)
     return fail(EE_ERR_ARG, "bad ee_test_attention arguments");
   ee_status s = check_device();
   if (s != EE_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
-  EE_CUDA(launch_attn_fwd((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
-                          (const __nv_bfloat16*)v, (__nv_bfloat16*)o, n_tokens, seq_len, n_heads,
-                          n_kv_heads, lse2, st));
+  if (impl == 1)
+    EE_CUDA(launch_attn_fwd_tc((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
+                               (const __nv_bfloat16*)v, (__nv_bfloat16*)o, n_tokens, seq_len,
+                               n_heads, n_kv_heads, lse2, st));
+  else
+    EE_CUDA(launch_attn_fwd((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
+                            (const __nv_bfloat16*)v, (__nv_bfloat16*)o, n_tokens, seq_len, n_heads,
+                            n_kv_heads, lse2, st));
   if (dout) {
     if (!dq || !dk || !dv || !scratch) return fail(EE_ERR_ARG, "backward outputs NULL");
     EE_CUDA(launch_attn_bwd((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,

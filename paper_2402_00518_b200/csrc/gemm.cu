@@ -38,7 +38,7 @@ int num_sms() {
 }
 
 // 2-D bf16 tensor map, 128B swizzle; inner = contiguous dim.
-static bool make_tmap(CUtensorMap* m, const Mat& t, uint32_t box_inner, uint32_t box_outer) {
+bool make_tmap(CUtensorMap* m, const Mat& t, uint32_t box_inner, uint32_t box_outer) {
   PFN_encodeTiled_t enc = encode_fn();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)t.cols, (cuuint64_t)t.rows};

@@ -22,6 +22,8 @@ struct Mat {  // a row-major bf16 matrix in global memory
   const void* ptr;
   long long rows, cols, ld;  // ld in elements
 };
+// 2-D TMA descriptor of a bf16 matrix, SWIZZLE_128B, box [box_outer rows x box_inner cols].
+bool make_tmap(CUtensorMap* m, const Mat& t, uint32_t box_inner, uint32_t box_outer);
 // Operand description of one GEMM side.
 //   k_major = true : storage [MN rows x K cols]  (K contiguous)
 //   k_major = false: storage [K rows x MN cols]  (MN contiguous)
@@ -87,6 +89,11 @@ cudaError_t launch_first_exit(const float* const* conf, int E, long long n, floa
 cudaError_t launch_attn_fwd(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                             __nv_bfloat16* o, long long N, int T, int Hq, int Hkv, float* lse2,
                             cudaStream_t s);
+// tcgen05 flash-attention forward (attn_tc.cu): same contract as launch_attn_fwd,
+// seq_len a multiple of 64, lse2 required.
+cudaError_t launch_attn_fwd_tc(const __nv_bfloat16* q, const __nv_bfloat16* k,
+                               const __nv_bfloat16* v, __nv_bfloat16* o, long long N, int T,
+                               int Hq, int Hkv, float* lse2, cudaStream_t s);
 cudaError_t launch_attn_bwd(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                             const __nv_bfloat16* o, const __nv_bfloat16* dout, const float* lse2,
                             float* Dv, __nv_bfloat16* dq, __nv_bfloat16* dk, __nv_bfloat16* dv,

@@ -34,9 +34,10 @@ def _rel(a, b):
     return ((a.float() - b.float()).norm() / b.float().norm()).item()
 
 
+@pytest.mark.parametrize("impl", [0, 1], ids=["mma_sync", "tcgen05"])
 @pytest.mark.parametrize("B,T,Hq,Hkv", [(2, 128, 4, 2), (1, 256, 2, 2), (3, 64, 8, 1),
-                                        (1, 512, 4, 1)])
-def test_attention_fwd_bwd_vs_fp32_autograd(gpu_lib, B, T, Hq, Hkv):
+                                        (1, 512, 4, 1), (2, 192, 2, 1), (1, 2048, 1, 1)])
+def test_attention_fwd_bwd_vs_fp32_autograd(gpu_lib, B, T, Hq, Hkv, impl):
     ee = gpu_lib
     g = torch.Generator(device="cuda").manual_seed(B * 1000 + T + Hq)
     n = B * T
@@ -48,7 +49,8 @@ def test_attention_fwd_bwd_vs_fp32_autograd(gpu_lib, B, T, Hq, Hkv):
     lse2 = torch.empty(n, Hq, device="cuda")
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     scr = torch.empty(n, Hq, device="cuda")
-    ee.ee_test_attention(q, k, v, o, lse2, T, Hq, Hkv, dout=do, dq=dq, dk=dk, dv=dv, scratch=scr)
+    ee.ee_test_attention(q, k, v, o, lse2, T, Hq, Hkv, dout=do, dq=dq, dk=dk, dv=dv, scratch=scr,
+                         impl=impl)
     torch.cuda.synchronize()
     o_r, lse_r, dq_r, dk_r, dv_r = _ref(q, k, v, do, T, Hq, Hkv)
     assert _rel(o, o_r) <= 1e-2
@@ -62,12 +64,13 @@ def test_attention_fwd_bwd_vs_fp32_autograd(gpu_lib, B, T, Hq, Hkv):
     # deterministic (no atomics)
     dq2, dk2, dv2 = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     ee.ee_test_attention(q, k, v, o, lse2, T, Hq, Hkv, dout=do, dq=dq2, dk=dk2, dv=dv2,
-                         scratch=scr)
+                         scratch=scr, impl=impl)
     torch.cuda.synchronize()
     assert torch.equal(dq, dq2) and torch.equal(dk, dk2) and torch.equal(dv, dv2)
 
 
-def test_attention_first_token_attends_only_to_itself(gpu_lib):
+@pytest.mark.parametrize("impl", [0, 1], ids=["mma_sync", "tcgen05"])
+def test_attention_first_token_attends_only_to_itself(gpu_lib, impl):
     """Causal special case: row t = 0 of every sequence has o = v_0 exactly (up to
     the bf16 output rounding), lse = s_00, and dK/dV rows of the last key only
     receive gradient from the last query."""
@@ -80,7 +83,7 @@ def test_attention_first_token_attends_only_to_itself(gpu_lib):
     v = torch.randn(n, Hkv * 128, device="cuda", generator=g).bfloat16()
     o = torch.empty_like(q)
     lse2 = torch.empty(n, Hq, device="cuda")
-    ee.ee_test_attention(q, k, v, o, lse2, T, Hq, Hkv)
+    ee.ee_test_attention(q, k, v, o, lse2, T, Hq, Hkv, impl=impl)
     torch.cuda.synchronize()
     for b in range(B):
         r = b * T
