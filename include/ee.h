@@ -362,8 +362,8 @@ ee_status ee_test_gemm(int32_t a_kmajor, int32_t b_kmajor, const void* A, const 
  * (max + log2 sum of 2^(s/sqrt(d) * log2 e)).  If dout != NULL the backward
  * also runs: dq, dk, dv (shapes of q, k, v, bf16) and scratch fp32 [n x Hq].
  * seq_len a multiple of 64 dividing n; n_heads a multiple of n_kv_heads.
- * impl selects the forward kernel: 0 = warp-level mma.sync, 1 = tcgen05/TMEM
- * (the step's default). */
+ * impl selects the forward and backward kernels: 0 = warp-level mma.sync,
+ * 1 = tcgen05/TMEM (the step's default). */
 ee_status ee_test_attention(const void* q, const void* k, const void* v, void* o, float* lse2,
                             const void* dout, void* dq, void* dk, void* dv, float* scratch,
                             int64_t n_tokens, int32_t seq_len, int32_t n_heads, int32_t n_kv_heads,

@@ -282,15 +282,18 @@ struct Prof {
 
 // Attention forward: the tcgen05 kernel (attn_tc.cu) unless EE_ATTN_TC=0 selects
 // the mma.sync kernel (A/B measurements).
-cudaError_t attn_forward(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
-                         __nv_bfloat16* o, long long n, int T, int Hq, int Hkv, float* lse2,
-                         cudaStream_t st) {
+int attn_tc_mode() {
   static const int tc = [] {
     const char* e = getenv("EE_ATTN_TC");
     return e ? atoi(e) : 1;
   }();
-  return tc ? launch_attn_fwd_tc(q, k, v, o, n, T, Hq, Hkv, lse2, st)
-            : launch_attn_fwd(q, k, v, o, n, T, Hq, Hkv, lse2, st);
+  return tc;
+}
+cudaError_t attn_forward(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
+                         __nv_bfloat16* o, long long n, int T, int Hq, int Hkv, float* lse2,
+                         cudaStream_t st) {
+  return attn_tc_mode() ? launch_attn_fwd_tc(q, k, v, o, n, T, Hq, Hkv, lse2, st)
+                        : launch_attn_fwd(q, k, v, o, n, T, Hq, Hkv, lse2, st);
 }
 
 GemmArgs base_args(int M, int N, int K) {
@@ -514,7 +517,8 @@ ee_status layer_attn_backward(const ee_head_config* cfg, const Bufs& B, const ee
     const double fe = 7.0 * (double)n * h * (cfg->seq_len + 64);   // + S twice, dP twice
     Prof p_("L8_attn_bwd", st, fe, fa, 0);
     EE_CUDA(launch_attn_bwd(B.q, B.k, B.v, B.o, B.da, B.lse2, B.dvec, B.dq, B.dk, B.dv, n,
-                            cfg->seq_len, Hq, Hkv, cfg->rope_theta, st)); }  // + L9 RoPE^T fused
+                            cfg->seq_len, Hq, Hkv, cfg->rope_theta, st,
+                            attn_tc_mode() != 0)); }  // + L9 RoPE^T fused
   { Prof p_("transpose_u1", st, 0, 0, 4.0 * n * h);
   EE_CUDA(launch_transpose_bf16(B.u1, B.uT, n, h, B.L.ldT, st)); }
   struct WG {
@@ -1375,7 +1379,7 @@ ee_status ee_test_attention(const void* q, const void* k, const void* v, void* o
                             (const __nv_bfloat16*)v, (const __nv_bfloat16*)o,
                             (const __nv_bfloat16*)dout, lse2, scratch, (__nv_bfloat16*)dq,
                             (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, n_tokens, seq_len, n_heads,
-                            n_kv_heads, 0.f, st));
+                            n_kv_heads, 0.f, st, impl == 1));
   }
   return EE_OK;
 }

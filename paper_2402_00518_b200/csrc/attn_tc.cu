@@ -279,4 +279,491 @@ cudaError_t launch_attn_fwd_tc(const __nv_bfloat16* q, const __nv_bfloat16* k,
   return cudaGetLastError();
 }
 
+// ============================================================================
+// Backward (FlashAttention-2 split, deterministic: no float atomics).  With
+// lse2 from the forward and Dv = rowsum(dO * O) (attn_bwd_dot_kernel):
+//   P = 2^(s S - lse2), dP = dO V^T, dS = P (dP - Dv),
+//   dQ = c dS K, dK = c dS^T Q, dV = P^T dO   (c = 1/sqrt(d), s = c log2 e)
+// and RoPE^T applied to dQ, dK in fp32 before their single bf16 rounding.
+// ============================================================================
+namespace {
+constexpr int FB_BQ = 64;                       // queries per step of the dK/dV kernel
+constexpr int FB_QT = FB_BQ * FA_D * 2;         // 16 KB: two 8 KB SW128 atoms
+constexpr int FB_SMEM_KV = 1024 + 2 * FA_TILE + 2 * 2 * FB_QT + 2 * (FA_BN * FB_BQ * 2) +
+                           2 * 2 * FB_BQ * 4 + 256;
+constexpr int FB_SMEM_Q = 1024 + 2 * FA_TILE + 2 * 2 * FA_TILE + FA_TILE + 256;
+
+// RoPE^T (rotation by -angle) of 32 columns [c0, c0 + 32) (c0 < 64) paired
+// with [c0 + 64, c0 + 96) of one row at position pos.
+__device__ __forceinline__ void rope_t_32(float* a, float* b, int c0, float pos, float theta) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const float inv = powf(theta, -2.0f * (float)(c0 + i) / 128.0f);
+    float sn, cs;
+    sincosf(pos * inv, &sn, &cs);
+    const float x = a[i], y = b[i];
+    a[i] = x * cs + y * sn;
+    b[i] = y * cs - x * sn;
+  }
+}
+
+// Row r of a [rows x 128] fp32 TMEM accumulator -> scale, optional RoPE^T at
+// `pos`, bf16, 256 bytes at dst.
+__device__ __forceinline__ void store_row_bf16(uint32_t tacc, __nv_bfloat16* dst, bool ok,
+                                               float scale, float pos, float theta) {
+#pragma unroll 1
+  for (int c = 0; c < 2; ++c) {
+    uint32_t va[32], vb[32];
+    tmem_ld_32x32b_x32(tacc + c * 32, va);
+    tmem_ld_wait();
+    tmem_ld_32x32b_x32(tacc + 64 + c * 32, vb);
+    tmem_ld_wait();
+    float a[32], b[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      a[i] = __uint_as_float(va[i]) * scale;
+      b[i] = __uint_as_float(vb[i]) * scale;
+    }
+    if (theta > 0.f) rope_t_32(a, b, c * 32, pos, theta);
+    if (ok) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t wa[8], wb[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          wa[q] = pack_bf16(a[h * 16 + 2 * q], a[h * 16 + 2 * q + 1]);
+          wb[q] = pack_bf16(b[h * 16 + 2 * q], b[h * 16 + 2 * q + 1]);
+        }
+        __nv_bfloat16* pa = dst + c * 32 + h * 16;
+        __nv_bfloat16* pb = pa + 64;
+        if (aligned32(pa) && aligned32(pb)) {
+          st_global_v8(pa, wa);
+          st_global_v8(pb, wb);
+        } else {
+          *reinterpret_cast<uint4*>(pa) = make_uint4(wa[0], wa[1], wa[2], wa[3]);
+          *reinterpret_cast<uint4*>(pa + 8) = make_uint4(wa[4], wa[5], wa[6], wa[7]);
+          *reinterpret_cast<uint4*>(pb) = make_uint4(wb[0], wb[1], wb[2], wb[3]);
+          *reinterpret_cast<uint4*>(pb + 8) = make_uint4(wb[4], wb[5], wb[6], wb[7]);
+        }
+      }
+    }
+  }
+}
+}  // namespace
+
+// dK, dV: one CTA per (128-key tile, kv head, sequence); loops over the query
+// heads of the GQA group and the 64-query tiles at or after the key tile.
+//   warp 0 TMA (K, V once; Q_i, dO_i double-buffered), warp 1 MMA,
+//   warps 4..7 one thread per key row (TMEM lane).
+// TMEM: S^T [128 x 64] | dP^T [128 x 64] | dK [128 x 128] | dV [128 x 128].
+__global__ void __launch_bounds__(256, 1)
+    attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
+                            const __grid_constant__ CUtensorMap tmK,
+                            const __grid_constant__ CUtensorMap tmV,
+                            const __grid_constant__ CUtensorMap tmDO,
+                            const float* __restrict__ lse2, const float* __restrict__ Dv,
+                            __nv_bfloat16* __restrict__ dk, __nv_bfloat16* __restrict__ dv,
+                            int T, int Hq, int Hkv, float scale_log2, float scale,
+                            float rope_theta) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + FA_TILE;
+  uint8_t* sQ = sV + FA_TILE;          // [2] x 16 KB
+  uint8_t* sDO = sQ + 2 * FB_QT;       // [2] x 16 KB
+  uint8_t* sPt = sDO + 2 * FB_QT;      // [128 keys x 64 q] bf16, one 16 KB atom
+  uint8_t* sDSt = sPt + FA_BN * FB_BQ * 2;
+  float* sL = reinterpret_cast<float*>(sDSt + FA_BN * FB_BQ * 2);  // [2][64]
+  float* sD = sL + 2 * FB_BQ;                                       // [2][64]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 2 * FB_BQ);
+  uint64_t* kv_full = bars;
+  uint64_t* qd_full = bars + 1;   // [2]
+  uint64_t* qd_empty = bars + 3;  // [2]
+  uint64_t* sdp_full = bars + 5;
+  uint64_t* pds_full = bars + 6;
+  uint64_t* acc_done = bars + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kt = blockIdx.x, hk = blockIdx.y, b = blockIdx.z;
+  const int grp = Hq / Hkv;
+  const int nq64 = (T + FB_BQ - 1) / FB_BQ;
+  const int q64_0 = kt * (FA_BN / FB_BQ);           // first 64-query tile touching this key tile
+  const int per_head = nq64 - q64_0;
+  const int n_it = grp * per_head;
+  const int k_row0 = b * T + kt * FA_BN;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    tma_prefetch_desc(&tmDO);
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&qd_full[s], 1);
+      mbar_init(&qd_empty[s], 1);
+    }
+    mbar_init(sdp_full, 1);
+    mbar_init(pds_full, 128);
+    mbar_init(acc_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tS = tmem_base, tDP = tmem_base + 64, tDK = tmem_base + 128,
+                 tDV = tmem_base + 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_load_2d(sK, &tmK, kv_full, hk * FA_D, k_row0);
+      tma_load_2d(sK + FA_ATOM, &tmK, kv_full, hk * FA_D + 64, k_row0);
+      tma_load_2d(sV, &tmV, kv_full, hk * FA_D, k_row0);
+      tma_load_2d(sV + FA_ATOM, &tmV, kv_full, hk * FA_D + 64, k_row0);
+      mbar_arrive_expect_tx(kv_full, 2 * FA_TILE);
+      for (int it = 0; it < n_it; ++it) {
+        const int s = it & 1;
+        const int hq = hk * grp + it / per_head;
+        const int q_row0 = b * T + (q64_0 + it % per_head) * FB_BQ;
+        mbar_wait(&qd_empty[s], ((it >> 1) & 1) ^ 1);
+        uint8_t* q = sQ + s * FB_QT;
+        uint8_t* d = sDO + s * FB_QT;
+        tma_load_2d(q, &tmQ, &qd_full[s], hq * FA_D, q_row0);
+        tma_load_2d(q + FB_QT / 2, &tmQ, &qd_full[s], hq * FA_D + 64, q_row0);
+        tma_load_2d(d, &tmDO, &qd_full[s], hq * FA_D, q_row0);
+        tma_load_2d(d + FB_QT / 2, &tmDO, &qd_full[s], hq * FA_D + 64, q_row0);
+        mbar_arrive_expect_tx(&qd_full[s], 2 * FB_QT);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = make_idesc_bf16(FA_BN, FB_BQ, false, false);   // 128 x 64
+      constexpr uint32_t idesc_acc = make_idesc_bf16(FA_BN, FA_D, false, true);   // 128 x 128
+      const uint32_t ak = smem_u32(sK), av = smem_u32(sV);
+      const uint32_t apt = smem_u32(sPt), ads = smem_u32(sDSt);
+      mbar_wait(kv_full, 0);
+      tc_fence_after();
+      for (int it = 0; it < n_it; ++it) {
+        const int s = it & 1;
+        mbar_wait(&qd_full[s], (it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t bq = smem_u32(sQ + s * FB_QT), bd = smem_u32(sDO + s * FB_QT);
+#pragma unroll
+        for (int k = 0; k < FA_D / 16; ++k) {  // S^T = K Q^T, dP^T = V dO^T (K-major, K = d)
+          const uint32_t offa = (k >> 2) * FA_ATOM + (k & 3) * 32;
+          const uint32_t offb = (k >> 2) * (FB_QT / 2) + (k & 3) * 32;
+          tc_mma_f16(tS, make_sdesc(ak + offa, 16, 1024), make_sdesc(bq + offb, 16, 1024), idesc_s,
+                     k != 0 ? 1u : 0u);
+          tc_mma_f16(tDP, make_sdesc(av + offa, 16, 1024), make_sdesc(bd + offb, 16, 1024),
+                     idesc_s, k != 0 ? 1u : 0u);
+        }
+        tc_commit(sdp_full);
+        mbar_wait(pds_full, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < FB_BQ / 16; ++k) {  // dV += P^T dO, dK += dS^T Q (B MN-major, K = q)
+          const uint32_t offa = k * 32;
+          const uint32_t offb = k * 2048;
+          tc_mma_f16(tDV, make_sdesc(apt + offa, 16, 1024), make_sdesc(bd + offb, FB_QT / 2, 1024),
+                     idesc_acc, (it | k) != 0 ? 1u : 0u);
+          tc_mma_f16(tDK, make_sdesc(ads + offa, 16, 1024), make_sdesc(bq + offb, FB_QT / 2, 1024),
+                     idesc_acc, (it | k) != 0 ? 1u : 0u);
+        }
+        tc_commit(&qd_empty[s]);
+      }
+      tc_commit(acc_done);
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    const int kr = ew * 32 + lane;  // key row = TMEM lane
+    const int kpos = kt * FA_BN + kr;
+    const uint32_t lane_off = static_cast<uint32_t>(ew * 32) << 16;
+    const int tid = threadIdx.x - 128;
+    uint8_t* pt_row = sPt + kr * 128;
+    uint8_t* ds_row = sDSt + kr * 128;
+    for (int it = 0; it < n_it; ++it) {
+      const int hq = hk * grp + it / per_head;
+      const int qpos0 = (q64_0 + it % per_head) * FB_BQ;
+      const int q_row0 = b * T + qpos0;
+      float* L = sL + (it & 1) * FB_BQ;
+      float* D = sD + (it & 1) * FB_BQ;
+      if (tid < FB_BQ) {
+        const bool in = qpos0 + tid < T;
+        L[tid] = in ? lse2[(long long)(q_row0 + tid) * Hq + hq] : 0.f;
+      } else {
+        const int t2 = tid - FB_BQ;
+        const bool in = qpos0 + t2 < T;
+        D[t2] = in ? Dv[(long long)(q_row0 + t2) * Hq + hq] : 0.f;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      mbar_wait(sdp_full, it & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < FB_BQ / 32; ++c) {
+        uint32_t vs[32], vp[32];
+        tmem_ld_32x32b_x32(tS + lane_off + c * 32, vs);
+        tmem_ld_wait();
+        tmem_ld_32x32b_x32(tDP + lane_off + c * 32, vp);
+        tmem_ld_wait();
+        uint32_t wp[16], wd[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          float p2[2], d2[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int col = c * 32 + 2 * q + e;
+            const int qpos = qpos0 + col;
+            float p = ex2_approx(__uint_as_float(vs[2 * q + e]) * scale_log2 - L[col]);
+            if (qpos < kpos || qpos >= T) p = 0.f;
+            p2[e] = p;
+            d2[e] = p * (__uint_as_float(vp[2 * q + e]) - D[col]);
+          }
+          wp[q] = pack_bf16(p2[0], p2[1]);
+          wd[q] = pack_bf16(d2[0], d2[1]);
+        }
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {  // 4 x 16-byte chunks of this 32-column slab
+          const int cc = c * 4 + h;
+          const int off = (cc ^ (kr & 7)) << 4;
+          *reinterpret_cast<uint4*>(pt_row + off) =
+              make_uint4(wp[4 * h], wp[4 * h + 1], wp[4 * h + 2], wp[4 * h + 3]);
+          *reinterpret_cast<uint4*>(ds_row + off) =
+              make_uint4(wd[4 * h], wd[4 * h + 1], wd[4 * h + 2], wd[4 * h + 3]);
+        }
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(pds_full);
+    }
+    mbar_wait(acc_done, 0);
+    tc_fence_after();
+    const bool ok = kpos < T;
+    const long long ldk = (long long)Hkv * FA_D;
+    store_row_bf16(tDK + lane_off, dk + (long long)(k_row0 + kr) * ldk + hk * FA_D, ok, scale,
+                   (float)kpos, rope_theta);
+    store_row_bf16(tDV + lane_off, dv + (long long)(k_row0 + kr) * ldk + hk * FA_D, ok, 1.0f,
+                   0.f, 0.f);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+// dQ: one CTA per (128-query tile, query head, sequence); loops over the key
+// tiles at or before the query tile.  TMEM: S | dP | dQ (128 columns each).
+__global__ void __launch_bounds__(256, 1)
+    attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
+                          const __grid_constant__ CUtensorMap tmK,
+                          const __grid_constant__ CUtensorMap tmV,
+                          const __grid_constant__ CUtensorMap tmDO,
+                          const float* __restrict__ lse2, const float* __restrict__ Dv,
+                          __nv_bfloat16* __restrict__ dq, int T, int Hq, int Hkv, float scale_log2,
+                          float scale, float rope_theta) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sDO = sQ + FA_TILE;
+  uint8_t* sK = sDO + FA_TILE;            // [2]
+  uint8_t* sV = sK + 2 * FA_TILE;         // [2]
+  uint8_t* sDS = sV + 2 * FA_TILE;        // [128 q x 128 keys] bf16, two atoms
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sDS + FA_TILE);
+  uint64_t* qo_full = bars;
+  uint64_t* kv_full = bars + 1;   // [2]
+  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* sdp_full = bars + 5;
+  uint64_t* ds_full = bars + 6;
+  uint64_t* acc_done = bars + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqt = (T + FA_BM - 1) / FA_BM;
+  const int qt = nqt - 1 - (int)blockIdx.x;
+  const int hq = blockIdx.y, b = blockIdx.z;
+  const int hk = hq / (Hq / Hkv);
+  const int q_row0 = b * T + qt * FA_BM;
+  const int n_kt = qt + 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    tma_prefetch_desc(&tmDO);
+    mbar_init(qo_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    mbar_init(sdp_full, 1);
+    mbar_init(ds_full, 128);
+    mbar_init(acc_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tS = tmem_base, tDP = tmem_base + 128, tDQ = tmem_base + 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_load_2d(sQ, &tmQ, qo_full, hq * FA_D, q_row0);
+      tma_load_2d(sQ + FA_ATOM, &tmQ, qo_full, hq * FA_D + 64, q_row0);
+      tma_load_2d(sDO, &tmDO, qo_full, hq * FA_D, q_row0);
+      tma_load_2d(sDO + FA_ATOM, &tmDO, qo_full, hq * FA_D + 64, q_row0);
+      mbar_arrive_expect_tx(qo_full, 2 * FA_TILE);
+      for (int j = 0; j < n_kt; ++j) {
+        const int s = j & 1;
+        mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
+        const int k_row0 = b * T + j * FA_BN;
+        uint8_t* k = sK + s * FA_TILE;
+        uint8_t* v = sV + s * FA_TILE;
+        tma_load_2d(k, &tmK, &kv_full[s], hk * FA_D, k_row0);
+        tma_load_2d(k + FA_ATOM, &tmK, &kv_full[s], hk * FA_D + 64, k_row0);
+        tma_load_2d(v, &tmV, &kv_full[s], hk * FA_D, k_row0);
+        tma_load_2d(v + FA_ATOM, &tmV, &kv_full[s], hk * FA_D + 64, k_row0);
+        mbar_arrive_expect_tx(&kv_full[s], 2 * FA_TILE);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = make_idesc_bf16(FA_BM, FA_BN, false, false);
+      constexpr uint32_t idesc_dq = make_idesc_bf16(FA_BM, FA_D, false, true);
+      const uint32_t aq = smem_u32(sQ), ado = smem_u32(sDO), ads = smem_u32(sDS);
+      mbar_wait(qo_full, 0);
+      for (int j = 0; j < n_kt; ++j) {
+        const int s = j & 1;
+        mbar_wait(&kv_full[s], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t bk = smem_u32(sK + s * FA_TILE), bv = smem_u32(sV + s * FA_TILE);
+#pragma unroll
+        for (int k = 0; k < FA_D / 16; ++k) {  // S = Q K^T, dP = dO V^T
+          const uint32_t off = (k >> 2) * FA_ATOM + (k & 3) * 32;
+          tc_mma_f16(tS, make_sdesc(aq + off, 16, 1024), make_sdesc(bk + off, 16, 1024), idesc_s,
+                     k != 0 ? 1u : 0u);
+          tc_mma_f16(tDP, make_sdesc(ado + off, 16, 1024), make_sdesc(bv + off, 16, 1024),
+                     idesc_s, k != 0 ? 1u : 0u);
+        }
+        tc_commit(sdp_full);
+        mbar_wait(ds_full, j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < FA_BN / 16; ++k) {  // dQ += dS K  (K MN-major: keys x d)
+          const uint32_t offa = (k >> 2) * FA_ATOM + (k & 3) * 32;
+          tc_mma_f16(tDQ, make_sdesc(ads + offa, 16, 1024), make_sdesc(bk + k * 2048, FA_ATOM, 1024),
+                     idesc_dq, (j | k) != 0 ? 1u : 0u);
+        }
+        tc_commit(&kv_empty[s]);
+      }
+      tc_commit(acc_done);
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    const int r = ew * 32 + lane;
+    const int pos = qt * FA_BM + r;
+    const uint32_t lane_off = static_cast<uint32_t>(ew * 32) << 16;
+    const bool ok = pos < T;
+    const float Lr = ok ? lse2[(long long)(q_row0 + r) * Hq + hq] : 0.f;
+    const float Dr = ok ? Dv[(long long)(q_row0 + r) * Hq + hq] : 0.f;
+    uint8_t* ds_row = sDS + r * 128;
+    for (int j = 0; j < n_kt; ++j) {
+      mbar_wait(sdp_full, j & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < FA_BN / 32; ++c) {
+        uint32_t vs[32], vp[32];
+        tmem_ld_32x32b_x32(tS + lane_off + c * 32, vs);
+        tmem_ld_wait();
+        tmem_ld_32x32b_x32(tDP + lane_off + c * 32, vp);
+        tmem_ld_wait();
+        uint32_t wd[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          float d2[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int kpos = j * FA_BN + c * 32 + 2 * q + e;
+            float p = ex2_approx(__uint_as_float(vs[2 * q + e]) * scale_log2 - Lr);
+            if (kpos > pos || !ok) p = 0.f;
+            d2[e] = p * (__uint_as_float(vp[2 * q + e]) - Dr);
+          }
+          wd[q] = pack_bf16(d2[0], d2[1]);
+        }
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int c8 = c * 4 + h;  // 16-byte chunk index over 128 keys
+          const int cc = c8 & 7;
+          *reinterpret_cast<uint4*>(ds_row + (c8 >> 3) * FA_ATOM + ((cc ^ (r & 7)) << 4)) =
+              make_uint4(wd[4 * h], wd[4 * h + 1], wd[4 * h + 2], wd[4 * h + 3]);
+        }
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(ds_full);
+    }
+    mbar_wait(acc_done, 0);
+    tc_fence_after();
+    store_row_bf16(tDQ + lane_off, dq + (long long)(q_row0 + r) * Hq * FA_D + hq * FA_D, ok, scale,
+                   (float)pos, rope_theta);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+cudaError_t launch_attn_bwd_tc(const __nv_bfloat16* q, const __nv_bfloat16* k,
+                               const __nv_bfloat16* v, const __nv_bfloat16* dout,
+                               const float* lse2, const float* Dv, __nv_bfloat16* dq,
+                               __nv_bfloat16* dk, __nv_bfloat16* dv, long long N, int T, int Hq,
+                               int Hkv, float rope_theta, cudaStream_t s) {
+  if (N == 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_dkdv_tc_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, FB_SMEM_KV);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(attn_bwd_dq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             FB_SMEM_Q);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const Mat Q{q, N, (long long)Hq * FA_D, (long long)Hq * FA_D};
+  const Mat DO{dout, N, (long long)Hq * FA_D, (long long)Hq * FA_D};
+  const Mat K{k, N, (long long)Hkv * FA_D, (long long)Hkv * FA_D};
+  const Mat V{v, N, (long long)Hkv * FA_D, (long long)Hkv * FA_D};
+  CUtensorMap tq64, tdo64, tq128, tdo128, tk, tv;
+  if (!make_tmap(&tq64, Q, 64, FB_BQ) || !make_tmap(&tdo64, DO, 64, FB_BQ) ||
+      !make_tmap(&tq128, Q, 64, FA_BM) || !make_tmap(&tdo128, DO, 64, FA_BM) ||
+      !make_tmap(&tk, K, 64, FA_BN) || !make_tmap(&tv, V, 64, FA_BN))
+    return cudaErrorInvalidValue;
+  const float scale = 1.0f / sqrtf((float)FA_D);
+  const float scale_log2 = 1.4426950408889634f * scale;
+  const unsigned B = (unsigned)(N / T);
+  dim3 g1((T + FA_BN - 1) / FA_BN, Hkv, B);
+  attn_bwd_dkdv_tc_kernel<<<g1, 256, FB_SMEM_KV, s>>>(tq64, tk, tv, tdo64, lse2, Dv, dk, dv, T, Hq,
+                                                      Hkv, scale_log2, scale, rope_theta);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  dim3 g2((T + FA_BM - 1) / FA_BM, Hq, B);
+  attn_bwd_dq_tc_kernel<<<g2, 256, FB_SMEM_Q, s>>>(tq128, tk, tv, tdo128, lse2, Dv, dq, T, Hq, Hkv,
+                                                   scale_log2, scale, rope_theta);
+  return cudaGetLastError();
+}
+
 }  // namespace ee

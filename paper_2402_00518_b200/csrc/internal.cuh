@@ -98,7 +98,13 @@ cudaError_t launch_attn_bwd(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
                             const __nv_bfloat16* o, const __nv_bfloat16* dout, const float* lse2,
                             float* Dv, __nv_bfloat16* dq, __nv_bfloat16* dk, __nv_bfloat16* dv,
                             long long N, int T, int Hq, int Hkv, float rope_theta,
-                            cudaStream_t s);  // rope_theta > 0: fused RoPE^T on dq, dk
+                            cudaStream_t s, bool tc = false);  // rope_theta > 0: fused RoPE^T
+// tcgen05 backward kernels (attn_tc.cu); Dv = rowsum(dO * O) precomputed.
+cudaError_t launch_attn_bwd_tc(const __nv_bfloat16* q, const __nv_bfloat16* k,
+                               const __nv_bfloat16* v, const __nv_bfloat16* dout,
+                               const float* lse2, const float* Dv, __nv_bfloat16* dq,
+                               __nv_bfloat16* dk, __nv_bfloat16* dv, long long N, int T, int Hq,
+                               int Hkv, float rope_theta, cudaStream_t s);
 cudaError_t launch_cast_bf16_f32(const __nv_bfloat16* a, float* b, long long n, cudaStream_t s);
 cudaError_t launch_cast_f32_bf16(const float* a, __nv_bfloat16* b, long long n, cudaStream_t s);
 
