@@ -24,11 +24,15 @@ import torch
 import torch.distributed as dist
 
 
-def shard_range(n_global: int, rank: int, world: int) -> tuple[int, int]:
-    """Contiguous token shard of `rank` (sizes differ by at most one)."""
-    base, rem = divmod(n_global, world)
+def shard_range(n_global: int, rank: int, world: int, align: int = 1) -> tuple[int, int]:
+    """Contiguous token shard of `rank`, in units of `align` tokens (sizes differ
+    by at most one unit).  Layer exits couple the tokens of a sequence, so their
+    shards are whole sequences: align = seq_len (n_global a multiple of it)."""
+    if n_global % align:
+        raise ValueError("n_global must be a multiple of align")
+    base, rem = divmod(n_global // align, world)
     start = rank * base + min(rank, rem)
-    return start, start + base + (1 if rank < rem else 0)
+    return start * align, (start + base + (1 if rank < rem else 0)) * align
 
 
 def data_parallel_step(n_exits: int, count_local: Callable[[], torch.Tensor],
@@ -63,7 +67,8 @@ def data_parallel_step(n_exits: int, count_local: Callable[[], torch.Tensor],
 # Vocab-parallel W_out (BASELINE configs[3]: "vocab-parallel W_out over 8 GPUs")
 # ---------------------------------------------------------------------------
 
-EXIT_BODY = ("g_a", "w_gate", "w_up", "w_down", "g_f")   # replicated; W_out is sharded
+EXIT_BODY = ("g_a", "w_gate", "w_up", "w_down", "g_f",    # replicated; W_out is sharded
+             "g_att", "w_q", "w_k", "w_v", "w_o")
 
 
 class TorchComm:

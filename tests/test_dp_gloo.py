@@ -23,7 +23,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, arch="mlp"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -31,15 +31,25 @@ def _worker(rank, world, port, q):
         from paper_2402_00518_b200.parallel import data_parallel_step, shard_range
         rng = np.random.default_rng(0)
         h, V, F, N, E = 16, 40, 24, 37, 2
+        T, align, at = 1, 1, None
+        if arch == "layer":      # 7 sequences of 5 tokens, sharded as whole sequences
+            T, N = 5, 35
+            align = T
+            at = {"seq_len": T, "n_heads": 2, "n_kv": 1, "theta": 10000.0}
         params = [{"w_out": rng.normal(0, .5, (V, h)), "g_f": 1 + .1 * rng.normal(size=h),
                    "g_a": 1 + .1 * rng.normal(size=h), "w_gate": rng.normal(0, .5, (F, h)),
                    "w_up": rng.normal(0, .5, (F, h)), "w_down": rng.normal(0, .5, (h, F))}
                   for _ in range(E)]
+        if arch == "layer":
+            for p in params:
+                p.update(g_att=1 + .1 * rng.normal(size=h), w_q=rng.normal(0, .5, (h, h)),
+                         w_k=rng.normal(0, .5, (h // 2, h)), w_v=rng.normal(0, .5, (h // 2, h)),
+                         w_o=rng.normal(0, .5, (h, h)))
         xs = [rng.normal(size=(N, h)) for _ in range(E)]
         y = rng.integers(0, V, N)
         y[[1, 8, 30]] = -1
         alphas = [1.0, 0.6]
-        s, e = shard_range(N, rank, world)
+        s, e = shard_range(N, rank, world, align)
         grads = [{k: torch.zeros(v.shape, dtype=torch.float64) for k, v in p.items()} for p in params]
         loss = torch.zeros(E, dtype=torch.float64)
 
@@ -47,15 +57,15 @@ def _worker(rank, world, port, q):
             return torch.tensor([int(np.sum(y[s:e] != -1))], dtype=torch.int64)
 
         def run_exit(i, W):
-            r = O.exit_loss_and_grads("mlp", params[i], xs[i][s:e], y[s:e], alphas[i], 1e-5,
-                                      valid_count=int(W.item()))
+            r = O.exit_loss_and_grads(arch, params[i], xs[i][s:e], y[s:e], alphas[i], 1e-5,
+                                      valid_count=int(W.item()), attn=at)
             loss[i] = r.loss
             for k, g in r.grads.items():
                 grads[i][k].copy_(torch.from_numpy(g))
 
         W = data_parallel_step(E, count_local, run_exit, lambda i: grads[i].values(), loss)
         if rank == 0:
-            full_l, full_g, _ = O.tune_step("mlp", params, xs, y, alphas, 1e-5)
+            full_l, full_g, _ = O.tune_step(arch, params, xs, y, alphas, 1e-5, attn=at)
             ok = int(W.item()) == int(np.sum(y != -1))
             ok &= np.allclose(loss.numpy(), full_l, rtol=1e-12)
             for i in range(E):
@@ -66,11 +76,12 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_data_parallel_world2_matches_full_batch_oracle():
+@pytest.mark.parametrize("arch", ["mlp", "layer"])
+def test_data_parallel_world2_matches_full_batch_oracle(arch):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, arch)) for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:
@@ -87,3 +98,8 @@ def test_shard_range_covers_tokens():
             assert spans[0][0] == 0 and spans[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
             assert max(b - a for a, b in spans) - min(b - a for a, b in spans) <= 1
+    for w in (1, 2, 3):                                 # whole sequences (Layer exits)
+        spans = [shard_range(7 * 2048, r, w, 2048) for r in range(w)]
+        assert spans[-1][1] == 7 * 2048 and all(a % 2048 == 0 and b % 2048 == 0 for a, b in spans)
+    with pytest.raises(ValueError):
+        shard_range(100, 0, 2, 64)

@@ -13,7 +13,7 @@ import pytest
 import torch
 
 import eesynth as S
-from harness import GRAD_RTOL, LOSS_RTOL, check_argmax, oracle_exit, rel_fro
+from harness import GRAD_RTOL, LOSS_RTOL, attn_kwargs, check_argmax, oracle_exit, rel_fro
 
 pytestmark = pytest.mark.gpu
 
@@ -75,7 +75,7 @@ def run_vp(ee, cfg, P, hidden, targets, params, weights, weighting="uniform"):
         try:
             vb, ve = shards[r]
             c = ee.make_config(h, cfg.vocab, cfg.ffn, E, cfg.arch, 1e-5, vb, ve,
-                               token_weighting=weighting)
+                               token_weighting=weighting, **attn_kwargs(cfg))
             ws = torch.zeros(ee.ee_workspace_size(c, N), dtype=torch.uint8, device="cuda")
             prm, grd = [], []
             for p in params:
@@ -115,10 +115,13 @@ def run_vp(ee, cfg, P, hidden, targets, params, weights, weighting="uniform"):
     return out, shards
 
 
-@pytest.mark.parametrize("arch,P", [("mlp", 2), ("mlp", 4), ("norm", 4), ("embedding", 2)])
+@pytest.mark.parametrize("arch,P", [("mlp", 2), ("mlp", 4), ("norm", 4), ("embedding", 2),
+                                    ("layer", 2)])
 def test_vocab_parallel_matches_oracle(gpu_lib, arch, P):
     cfg = S.Cfg(name="small", hidden=128, vocab=1000, ffn=256 if arch == "mlp" else 0,
                 arch=arch, tokens=256, layers=2, after=[1, 2], init="random", seed=21)
+    if arch == "layer":     # 2 sequences of 128: one per rank
+        cfg = S.get_cfg("tiny_layer", seed=21)
     hidden = S.hidden_states(cfg, 256)
     targets = S.targets(cfg, 256)
     params = S.head_params(cfg)
@@ -127,7 +130,8 @@ def test_vocab_parallel_matches_oracle(gpu_lib, arch, P):
     for r in range(P):
         assert out[r][3] == (0, -1)
     for i in range(cfg.exits):
-        res = oracle_exit(arch, params[i], hidden[i], targets, weights[i])
+        res = oracle_exit(arch, params[i], hidden[i], targets, weights[i],
+                          attn=S.attn_geometry(cfg))
         for r in range(P):                                     # loss identical on every rank
             L = out[r][0][i].item()
             assert abs(L - res.loss) / res.loss <= LOSS_RTOL

@@ -46,12 +46,13 @@ def _unkey(k):
 class NumpyPhases:
     """fp64 stand-in for the ee_vp_* phases of one rank (shard [vb, ve))."""
 
-    def __init__(self, O, arch, vb, ve, eps=1e-5):
+    def __init__(self, O, arch, vb, ve, eps=1e-5, attn=None):
         self.O, self.arch, self.vb, self.ve, self.eps = O, arch, vb, ve, eps
+        self.attn = attn
 
     def exit_forward(self, hidden, params, z_out, n_all):
         p = {k: v.numpy() for k, v in params.items()}
-        self.act = self.O.exit_forward(self.arch, p, hidden.numpy(), self.eps)
+        self.act = self.O.exit_forward(self.arch, p, hidden.numpy(), self.eps, self.attn)
         z_out.copy_(torch.from_numpy(self.act["z"]))
 
     def vocab_stats(self, z_all, targets_all, params, key, sums):
@@ -106,13 +107,18 @@ def _worker(rank, world, port, arch, q):
         from paper_2402_00518_b200.parallel import TorchComm, vocab_parallel_step
         rng = np.random.default_rng(1)
         h, V, F, N, E = 16, 40, 24, 12 * world, 2
+        at = {"seq_len": 6, "n_heads": 2, "n_kv": 1, "theta": 10000.0} if arch == "layer" else None
         params = [{"w_out": rng.normal(0, .5, (V, h))} for _ in range(E)]
         for p in params:
-            if arch in ("norm", "mlp"):
+            if arch != "embedding":
                 p["g_f"] = 1 + .1 * rng.normal(size=h)
-            if arch == "mlp":
+            if arch in ("mlp", "layer"):
                 p.update(g_a=1 + .1 * rng.normal(size=h), w_gate=rng.normal(0, .5, (F, h)),
                          w_up=rng.normal(0, .5, (F, h)), w_down=rng.normal(0, .5, (h, F)))
+            if arch == "layer":
+                p.update(g_att=1 + .1 * rng.normal(size=h), w_q=rng.normal(0, .5, (h, h)),
+                         w_k=rng.normal(0, .5, (h // 2, h)), w_v=rng.normal(0, .5, (h // 2, h)),
+                         w_o=rng.normal(0, .5, (h, h)))
         xs = [rng.normal(size=(N, h)) for _ in range(E)]
         y = rng.integers(0, V, N)
         y[[1, 7]] = -1
@@ -132,12 +138,12 @@ def _worker(rank, world, port, arch, q):
         W = torch.tensor([int(np.sum(y != -1))])
         loss = torch.zeros(E, dtype=torch.float64)
         aux = [{"argmax": torch.zeros(N, dtype=torch.int64)} for _ in range(E)]
-        vocab_parallel_step(NumpyPhases(O, arch, vb, ve), TorchComm(), arch, hid,
+        vocab_parallel_step(NumpyPhases(O, arch, vb, ve, attn=at), TorchComm(), arch, hid,
                             torch.from_numpy(y), prm, grd, loss, alphas, W, bufs, aux=aux)
         gathered = [None] * world
         dist.all_gather_object(gathered, ([g["w_out"].numpy() for g in grd],))
         if rank == 0:
-            full_l, full_g, full_st = O.tune_step(arch, params, xs, y, alphas, 1e-5)
+            full_l, full_g, full_st = O.tune_step(arch, params, xs, y, alphas, 1e-5, attn=at)
             ok = np.allclose(loss.numpy(), full_l, rtol=1e-10)
             for i in range(E):
                 dw = np.concatenate([gathered[r][0][i] for r in range(world)])
@@ -151,7 +157,7 @@ def _worker(rank, world, port, arch, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("arch,world", [("mlp", 2), ("norm", 3), ("embedding", 2)])
+@pytest.mark.parametrize("arch,world", [("mlp", 2), ("norm", 3), ("embedding", 2), ("layer", 2)])
 def test_vocab_parallel_gloo_matches_full_batch_oracle(arch, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
