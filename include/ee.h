@@ -87,8 +87,17 @@ typedef enum { EE_INIT_COPY = 0, EE_INIT_RANDOM = 1 } ee_init;
  *             detached (a constant in the backward); L_i = sum_t c_t loss_t /
  *             sum_t c_t (normalisation: DESIGN.md A17).  Needs all tokens of
  *             the batch in one call (ee_tune_step without valid_count, or the
- *             ee_vp_* phases); a DP shard returns EE_ERR_UNSUPPORTED. */
-typedef enum { EE_WEIGHT_UNIFORM = 0, EE_WEIGHT_CONFIDENCE = 1 } ee_token_weighting;
+ *             ee_vp_* phases); a DP shard returns EE_ERR_UNSUPPORTED.
+ * CONFIDENCE_SUM: the same weights, normaliser left to the caller (data
+ *             parallelism: sum_t c_t spans every rank's tokens): loss_out =
+ *             sum_t c_t loss_t, grads = gradient of alpha sum_t c_t loss_t,
+ *             ee_step_aux.weight_sum = sum_t c_t of this call.  The caller sums
+ *             the three over ranks and calls ee_normalize_exit. */
+typedef enum {
+  EE_WEIGHT_UNIFORM = 0,
+  EE_WEIGHT_CONFIDENCE = 1,
+  EE_WEIGHT_CONFIDENCE_SUM = 2
+} ee_token_weighting;
 
 /* Element type of Copy-init source tensors. */
 typedef enum { EE_DTYPE_BF16 = 0, EE_DTYPE_F32 = 1 } ee_dtype;
@@ -146,12 +155,15 @@ typedef struct {
 /* Optional per-token outputs of one exit (device, [n_tokens] each; any may be
  * NULL).  lse = log-sum-exp of the logits; loss_tok = lse - logit[target]
  * (0 for ignored tokens); argmax = lowest index of the max logit (A9);
- * conf = max softmax probability = 1/sum exp(S - max). */
+ * conf = max softmax probability = 1/sum exp(S - max).
+ * weight_sum (device float [1]) = the loss normaliser of this call: the valid
+ * count W (UNIFORM) or sum_t c_t over valid tokens (CONFIDENCE*). */
 typedef struct {
   float* lse;
   float* loss_tok;
   int32_t* argmax;
   float* conf;
+  float* weight_sum;
 } ee_step_aux;
 
 /* Bytes of workspace ee_tune_step needs for n_tokens tokens with this config.
@@ -203,6 +215,13 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
                        const ee_head_tensors* params, ee_head_tensors* grads, int32_t accumulate,
                        float* loss_out, const ee_step_aux* aux, const int64_t* valid_count,
                        void* workspace, size_t ws_bytes, void* stream);
+
+/* Data-parallel confidence weighting (EE_WEIGHT_CONFIDENCE_SUM): after the
+ * caller has summed one exit's grads, its loss and weight_sum over the ranks,
+ * divide the exit's fp32 gradients (grads: ONE exit) and *loss (device, may be
+ * NULL) by *weight_sum (device scalar; <= 0 -> zeros).  P:326-336, A17. */
+ee_status ee_normalize_exit(const ee_head_config* cfg, ee_head_tensors* grads, float* loss,
+                            const float* weight_sum, void* stream);
 
 /* ---- vocab-parallel phases (one exit on one of P ranks) ----
  * W_out is split by rows over P ranks (cfg->vocab_begin/vocab_end = this rank's

@@ -33,7 +33,8 @@ EXPORTED = ("ee_workspace_size", "ee_init_heads", "ee_tune_step", "ee_count_vali
             "ee_version", "ee_test_gemm", "ee_profile_start", "ee_profile_stop",
             "ee_profile_record", "ee_launch_count", "ee_vp_exit_forward", "ee_vp_vocab_stats",
             "ee_vp_rescale", "ee_vp_vocab_backward", "ee_vp_exit_backward", "ee_exit_infer",
-            "ee_backbone_workspace_size", "ee_backbone_forward", "ee_test_attention")
+            "ee_backbone_workspace_size", "ee_backbone_forward", "ee_test_attention",
+            "ee_normalize_exit")
 
 
 class EEError(RuntimeError):
@@ -69,9 +70,11 @@ class ee_layer_tensors(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in LAYER_NAMES]
 
 
+AUX_NAMES = ("lse", "loss_tok", "argmax", "conf", "weight_sum")
+
+
 class ee_step_aux(ctypes.Structure):
-    _fields_ = [("lse", ctypes.c_void_p), ("loss_tok", ctypes.c_void_p),
-                ("argmax", ctypes.c_void_p), ("conf", ctypes.c_void_p)]
+    _fields_ = [(n, ctypes.c_void_p) for n in AUX_NAMES]
 
 
 _lib = None
@@ -104,6 +107,7 @@ def load(path: str = LIB_PATH):
         "ee_last_error": (ctypes.c_char_p, []),
         "ee_version": (ctypes.c_char_p, []),
         "ee_test_gemm": (I32, [I32, I32, P, P, P, I32, I32, I32, I32, P]),
+        "ee_normalize_exit": (I32, [CFG, HT, P, P, P]),
         "ee_test_attention": (I32, [P, P, P, P, P, P, P, P, P, P, I64, I32, I32, I32, I32, P]),
         "ee_profile_start": (I32, []),
         "ee_profile_stop": (I32, [ctypes.POINTER(I32)]),
@@ -148,7 +152,7 @@ def _stream(stream=None):
     return ctypes.c_void_p(s.cuda_stream)
 
 
-WEIGHTING = {"uniform": 0, "confidence": 1}
+WEIGHTING = {"uniform": 0, "confidence": 1, "confidence_sum": 2}
 
 
 def make_config(hidden, vocab, ffn, num_exits, arch, norm_eps=1e-5, vocab_begin=0, vocab_end=None,
@@ -206,7 +210,7 @@ def ee_tune_step(cfg, hidden, targets, exit_weights, params, grads, loss_out, wo
     if aux is not None:
         ax = (ee_step_aux * E)()
         for i, d in enumerate(aux):
-            for k in ("lse", "loss_tok", "argmax", "conf"):
+            for k in AUX_NAMES:
                 t = d.get(k)
                 setattr(ax[i], k, None if t is None else t.data_ptr())
     n = targets.numel()
@@ -312,11 +316,19 @@ def ee_test_attention(q, k, v, o, lse2, seq_len, n_heads, n_kv_heads, dout=None,
                                   seq_len, n_heads, n_kv_heads, int(impl), _stream(stream)))
 
 
+def ee_normalize_exit(cfg, grads, loss, weight_sum, stream=None):
+    """Divide one exit's gradients (dict) and loss (device [1] or None) by the
+    device scalar weight_sum (data-parallel confidence weighting)."""
+    load()
+    _check(_lib.ee_normalize_exit(ctypes.byref(cfg), heads([grads]), _ptr(loss), _ptr(weight_sum),
+                                  _stream(stream)))
+
+
 def _aux1(aux):
     if aux is None:
         return None
     ax = ee_step_aux()
-    for k in ("lse", "loss_tok", "argmax", "conf"):
+    for k in AUX_NAMES:
         t = aux.get(k)
         setattr(ax, k, None if t is None else t.data_ptr())
     return ctypes.pointer(ax)

@@ -83,7 +83,8 @@ ee_status check_cfg(const ee_head_config* c) {
     if (!(c->rope_theta > 0.f)) return fail(EE_ERR_ARG, "Layer exit: rope_theta must be > 0");
   }
   if (!(c->norm_eps >= 0.f)) return fail(EE_ERR_ARG, "norm_eps must be >= 0");
-  if (c->token_weighting != EE_WEIGHT_UNIFORM && c->token_weighting != EE_WEIGHT_CONFIDENCE)
+  if (c->token_weighting != EE_WEIGHT_UNIFORM && c->token_weighting != EE_WEIGHT_CONFIDENCE &&
+      c->token_weighting != EE_WEIGHT_CONFIDENCE_SUM)
     return fail(EE_ERR_ARG, "unknown token_weighting %d", c->token_weighting);
   return EE_OK;
 }
@@ -793,7 +794,8 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
   if ((s = check_tokens(cfg, n_tokens)) != EE_OK) return s;
   if (valid_count && cfg->token_weighting == EE_WEIGHT_CONFIDENCE)
     return fail(EE_ERR_UNSUPPORTED, "confidence weighting needs every token of the batch in one "
-                                    "call (single GPU or the ee_vp_* phases), not a DP shard");
+                                    "call; a DP shard uses EE_WEIGHT_CONFIDENCE_SUM + "
+                                    "ee_normalize_exit");
   for (int i = 0; i < E; ++i) {
     if ((s = check_arch_tensors(cfg, params[i], "params", i)) != EE_OK) return s;
     if ((s = check_arch_tensors(cfg, grads[i], "grads", i)) != EE_OK) return s;
@@ -830,7 +832,8 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
     // a6: lse, coef, per-token aux, L_i
     {
       const ee_step_aux* ax = aux ? &aux[i] : nullptr;
-      const bool dynw = cfg->token_weighting == EE_WEIGHT_CONFIDENCE;
+      const bool dynw = cfg->token_weighting != EE_WEIGHT_UNIFORM;
+      const bool norm = cfg->token_weighting != EE_WEIGHT_CONFIDENCE_SUM;
       { Prof p_("a6_ce_finalize", st, 0, 0, 12.0 * B.L.nb * n + 24.0 * n);
       EE_CUDA(launch_ce_finalize(B.pm, B.ps, B.pi, B.tgt, targets, B.L.nb, n, vc,
                                  exit_weights[i], B.lse, B.coef, ax ? ax->lse : nullptr,
@@ -839,11 +842,13 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
                                  dynw ? B.wsum_part : nullptr, B.L.nfin, st)); }
       { Prof p2_("a6_loss_reduce", st, 0, 0, 4.0 * B.L.nfin);
       EE_CUDA(launch_loss_reduce(B.loss_part, B.L.nfin, vc, dynw ? B.wsum_part : nullptr, B.wsum,
-                                 loss_out + i, B.status, i, st)); }
+                                 loss_out + i, B.status, i, st, norm)); }
       if (dynw) {
         Prof p3_("a6_coef_scale", st, 0, 0, 8.0 * n);
-        EE_CUDA(launch_ce_coef_scale(B.coef, n, exit_weights[i], B.wsum, st));
+        EE_CUDA(launch_ce_coef_scale(B.coef, n, exit_weights[i], norm ? B.wsum : nullptr, st));
       }
+      if (ax && ax->weight_sum)
+        EE_CUDA(cudaMemcpyAsync(ax->weight_sum, B.wsum, sizeof(float), cudaMemcpyDeviceToDevice, st));
     }
     if ((s = phase_vocab_backward(cfg, B, P, G, z, n, targets, accumulate, nrm ? B.dz : nullptr,
                                   st)) != EE_OK)
@@ -1153,7 +1158,8 @@ ee_status ee_vp_vocab_backward(const ee_head_config* cfg, const void* z_all, int
     return EE_OK;
   }
   const long long* vc = valid_count ? (const long long*)valid_count : B.vcount;
-  const bool dynw = cfg->token_weighting == EE_WEIGHT_CONFIDENCE;
+  const bool dynw = cfg->token_weighting != EE_WEIGHT_UNIFORM;
+  const bool norm = cfg->token_weighting != EE_WEIGHT_CONFIDENCE_SUM;
   {
     Prof p_("vp_finalize", st, 0, 0, 28.0 * n_all);
     EE_CUDA(launch_vp_finalize((const long long*)key_global, sums_global, targets_all, n_all, vc,
@@ -1165,12 +1171,14 @@ ee_status ee_vp_vocab_backward(const ee_head_config* cfg, const void* z_all, int
   {
     Prof p_("a6_loss_reduce", st, 0, 0, 4.0 * B.L.nfin);
     EE_CUDA(launch_loss_reduce(B.loss_part, B.L.nfin, vc, dynw ? B.wsum_part : nullptr, B.wsum,
-                               loss_out, B.status, exit_index, st));
+                               loss_out, B.status, exit_index, st, norm));
   }
   if (dynw) {
     Prof p_("a6_coef_scale", st, 0, 0, 8.0 * n_all);
-    EE_CUDA(launch_ce_coef_scale(B.coef, n_all, exit_weight, B.wsum, st));
+    EE_CUDA(launch_ce_coef_scale(B.coef, n_all, exit_weight, norm ? B.wsum : nullptr, st));
   }
+  if (aux && aux->weight_sum)
+    EE_CUDA(cudaMemcpyAsync(aux->weight_sum, B.wsum, sizeof(float), cudaMemcpyDeviceToDevice, st));
   return phase_vocab_backward(cfg, B, *params, *grads, (const __nv_bfloat16*)z_all, n_all,
                               targets_all, accumulate, nrm ? dz_partial : nullptr, st);
 }
@@ -1193,6 +1201,24 @@ ee_status ee_vp_exit_backward(const ee_head_config* cfg, const void* hidden, int
   }
   return phase_exit_backward(cfg, B, *params, *grads, (const __nv_bfloat16*)hidden, n_local,
                              dz_local, accumulate, st);
+}
+
+ee_status ee_normalize_exit(const ee_head_config* cfg, ee_head_tensors* grads, float* loss,
+                            const float* weight_sum, void* stream) {
+  ee_status s = check_cfg(cfg);
+  if (s != EE_OK) return s;
+  if (!grads || !weight_sum) return fail(EE_ERR_ARG, "grads/weight_sum NULL");
+  if ((s = check_arch_tensors(cfg, *grads, "grads", 0)) != EE_OK) return s;
+  if ((s = check_device()) != EE_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int k = 0; k < NTENS; ++k) {
+    float* g = (float*)(grads->*(kTens[k].f));
+    if (!g) continue;
+    Prof p_("normalize_exit", st, 0, 0, 8.0 * tensor_numel(cfg, k));
+    EE_CUDA(launch_scale_by_inv(g, tensor_numel(cfg, k), weight_sum, st));
+  }
+  if (loss) EE_CUDA(launch_scale_by_inv(loss, 1, weight_sum, st));
+  return EE_OK;
 }
 
 ee_status ee_init_heads(const ee_head_config* cfg, int32_t init, const ee_head_tensors* src,

@@ -57,11 +57,14 @@ cudaError_t launch_ce_finalize(const float* pm, const float* ps, const int32_t* 
                                float* aux_conf, float* loss_part, float* wsum_part, int nblocks,
                                cudaStream_t s);
 // wsum_part != NULL: confidence weighting (L = sum w loss / sum w, written to wsum_out)
+// normalize = false: L = sum w loss (the normaliser is applied by the caller later)
 cudaError_t launch_loss_reduce(const float* loss_part, int nparts, const long long* valid_count,
                                const float* wsum_part, float* wsum_out, float* loss_out,
-                               DevStatus* st, int exit_index, cudaStream_t s);
+                               DevStatus* st, int exit_index, cudaStream_t s,
+                               bool normalize = true);
 cudaError_t launch_ce_coef_scale(float* coef, long long n, float alpha, const float* wsum,
                                  cudaStream_t s);
+cudaError_t launch_scale_by_inv(float* x, long long n, const float* den, cudaStream_t s);
 constexpr int FINALIZE_THREADS = 256;
 
 // vocab-parallel softmax-CE (distributed statistics)

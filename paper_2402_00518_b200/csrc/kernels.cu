@@ -4,6 +4,7 @@
 // loss reduction, valid-token count, Adam/SGD and initialisers
 // (P:227-238).  All reductions are deterministic (fixed order, no float
 // atomics), so reruns are bitwise identical.
+#include <algorithm>
 #include <cfloat>
 #include <climits>
 #include "internal.cuh"
@@ -350,7 +351,7 @@ cudaError_t launch_ce_finalize(const float* pm, const float* ps, const int32_t* 
 __global__ void loss_reduce_kernel(const float* __restrict__ part, int nparts,
                                    const long long* __restrict__ valid_count,
                                    const float* __restrict__ wsum_part, float* wsum_out,
-                                   float* loss_out, DevStatus* st, int exit_index) {
+                                   float* loss_out, DevStatus* st, int exit_index, int normalize) {
   __shared__ double red[33];
   double s = 0.0, ws = 0.0;
   for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
@@ -361,7 +362,7 @@ __global__ void loss_reduce_kernel(const float* __restrict__ part, int nparts,
   if (wsum_part) ws = block_sum(ws, red);
   if (threadIdx.x == 0) {
     const double W = wsum_part ? ws : (double)*valid_count;
-    const float L = W > 0 ? (float)(s / W) : 0.f;
+    const float L = !normalize ? (float)s : (W > 0 ? (float)(s / W) : 0.f);
     *loss_out = L;
     if (wsum_out) *wsum_out = (float)W;
     if (!isfinite(L)) set_status(st, 7 /*EE_ERR_DIVERGED*/, exit_index);
@@ -370,16 +371,21 @@ __global__ void loss_reduce_kernel(const float* __restrict__ part, int nparts,
 
 cudaError_t launch_loss_reduce(const float* loss_part, int nparts, const long long* valid_count,
                                const float* wsum_part, float* wsum_out, float* loss_out,
-                               DevStatus* st, int exit_index, cudaStream_t s) {
+                               DevStatus* st, int exit_index, cudaStream_t s, bool normalize) {
   loss_reduce_kernel<<<1, 1024, 0, s>>>(loss_part, nparts, valid_count, wsum_part, wsum_out,
-                                        loss_out, st, exit_index);
+                                        loss_out, st, exit_index, normalize ? 1 : 0);
   return cudaGetLastError();
 }
 
-// coef_t = alpha * w_t / sum_t w_t  (confidence weighting; w_t stored in coef)
+// coef_t = alpha * w_t / sum_t w_t  (confidence weighting; w_t stored in coef);
+// wsum == NULL: alpha * w_t (the normaliser is applied later, ee_normalize_exit)
 __global__ void ce_coef_scale_kernel(float* coef, long long n, float alpha, const float* wsum) {
   const long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= n) return;
+  if (wsum == nullptr) {
+    coef[row] = alpha * coef[row];
+    return;
+  }
   const float W = *wsum;
   coef[row] = W > 0.f ? alpha * coef[row] / W : 0.f;
 }
@@ -388,6 +394,22 @@ cudaError_t launch_ce_coef_scale(float* coef, long long n, float alpha, const fl
                                  cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   ce_coef_scale_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(coef, n, alpha, wsum);
+  return cudaGetLastError();
+}
+
+// x[i] *= 1 / *den  (den a device scalar; 0 -> x = 0)
+__global__ void scale_by_inv_kernel(float* __restrict__ x, long long n, const float* __restrict__ den) {
+  const float d = *den;
+  const float f = d > 0.f ? 1.0f / d : 0.f;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    x[i] *= f;
+}
+
+cudaError_t launch_scale_by_inv(float* x, long long n, const float* den, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const unsigned nb = (unsigned)std::min<long long>((n + 255) / 256, 148LL * 16);
+  scale_by_inv_kernel<<<nb, 256, 0, s>>>(x, n, den);
   return cudaGetLastError();
 }
 

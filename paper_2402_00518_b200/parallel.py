@@ -35,32 +35,46 @@ def shard_range(n_global: int, rank: int, world: int, align: int = 1) -> tuple[i
     return start * align, (start + base + (1 if rank < rem else 0)) * align
 
 
-def data_parallel_step(n_exits: int, count_local: Callable[[], torch.Tensor],
-                       run_exit: Callable[[int, torch.Tensor], None],
+def data_parallel_step(n_exits: int, count_local: Callable[[], torch.Tensor] | None,
+                       run_exit: Callable[[int, torch.Tensor | None], None],
                        grads_of: Callable[[int], Iterable[torch.Tensor]],
                        loss: torch.Tensor, optimizer_step: Callable[[], None] | None = None,
-                       group=None) -> torch.Tensor:
+                       group=None, weight_sums: torch.Tensor | None = None,
+                       normalize: Callable[[int], None] | None = None) -> torch.Tensor:
     """One data-parallel EE-Tuning step.
 
-    count_local() -> int64 tensor [1] with the local valid-token count;
-    run_exit(i, W) computes exit i's loss (into loss[i]) and gradients on the
-    local tokens, normalised by the global count W; grads_of(i) yields exit i's
-    gradient tensors; optimizer_step() applies the update after all reductions.
-    Returns the global count W.
+    Uniform token weights: count_local() -> int64 tensor [1] with the local
+    valid-token count; run_exit(i, W) computes exit i's loss (into loss[i]) and
+    gradients on the local tokens, normalised by the global count W (A16).
+    Confidence weights (weight_sums = float tensor [E]): run_exit(i,
+    None) computes the UNNORMALISED sum_t c_t loss_t, its gradient and
+    weight_sums[i] = sum_t c_t on the local tokens (EE_WEIGHT_CONFIDENCE_SUM);
+    after the SUM all-reduces, normalize(i) divides exit i by the global
+    sum_t c_t (ee_normalize_exit).  grads_of(i) yields exit i's gradient
+    tensors; optimizer_step() applies the update after all reductions.
+    Returns W (uniform) or the global weight sums (confidence).
     """
-    W = count_local()
-    dist.all_reduce(W, group=group)
+    conf = weight_sums is not None
+    W = None
+    if not conf:
+        W = count_local()
+        dist.all_reduce(W, group=group)
     handles = []
     for i in range(n_exits):
         run_exit(i, W)
         for t in grads_of(i):
             handles.append(dist.all_reduce(t, group=group, async_op=True))
     handles.append(dist.all_reduce(loss, group=group, async_op=True))
+    if conf:
+        handles.append(dist.all_reduce(weight_sums, group=group, async_op=True))
     for h in handles:
         h.wait()
+    if conf:
+        for i in range(n_exits):
+            normalize(i)
     if optimizer_step is not None:
         optimizer_step()
-    return W
+    return weight_sums if conf else W
 
 
 # ---------------------------------------------------------------------------

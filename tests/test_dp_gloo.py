@@ -23,7 +23,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q, arch="mlp"):
+def _worker(rank, world, port, q, arch="mlp", weighting="uniform"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -56,17 +56,48 @@ def _worker(rank, world, port, q, arch="mlp"):
         def count_local():
             return torch.tensor([int(np.sum(y[s:e] != -1))], dtype=torch.int64)
 
-        def run_exit(i, W):
-            r = O.exit_loss_and_grads(arch, params[i], xs[i][s:e], y[s:e], alphas[i], 1e-5,
-                                      valid_count=int(W.item()), attn=at)
-            loss[i] = r.loss
-            for k, g in r.grads.items():
-                grads[i][k].copy_(torch.from_numpy(g))
+        conf = weighting == "confidence"
+        wsums = torch.zeros(E, dtype=torch.float64) if conf else None
 
-        W = data_parallel_step(E, count_local, run_exit, lambda i: grads[i].values(), loss)
+        def run_exit(i, W):
+            if not conf:
+                r = O.exit_loss_and_grads(arch, params[i], xs[i][s:e], y[s:e], alphas[i], 1e-5,
+                                          valid_count=int(W.item()), attn=at)
+                loss[i] = r.loss
+                for k, g in r.grads.items():
+                    grads[i][k].copy_(torch.from_numpy(g))
+                return
+            # stand-in for EE_WEIGHT_CONFIDENCE_SUM: the locally normalised oracle
+            # times the local sum of c_t (detached confidences of valid tokens)
+            r = O.exit_loss_and_grads(arch, params[i], xs[i][s:e], y[s:e], alphas[i], 1e-5,
+                                      weighting="confidence", attn=at)
+            C = float(np.sum(r.stats["conf"][r.stats["valid"]]))
+            wsums[i] = C
+            loss[i] = r.loss * C
+            for k, g in r.grads.items():
+                grads[i][k].copy_(torch.from_numpy(g * C))
+
+        def normalize(i):
+            loss[i] /= wsums[i]
+            for g in grads[i].values():
+                g /= wsums[i]
+
+        W = data_parallel_step(E, None if conf else count_local, run_exit,
+                               lambda i: grads[i].values(), loss, weight_sums=wsums,
+                               normalize=normalize)
         if rank == 0:
-            full_l, full_g, _ = O.tune_step(arch, params, xs, y, alphas, 1e-5, attn=at)
-            ok = int(W.item()) == int(np.sum(y != -1))
+            if conf:
+                full_l, full_g = [], []
+                for i in range(E):
+                    r = O.exit_loss_and_grads(arch, params[i], xs[i], y, alphas[i], 1e-5,
+                                              weighting="confidence", attn=at)
+                    full_l.append(r.loss)
+                    full_g.append(r.grads)
+                full_l = np.array(full_l)
+                ok = True
+            else:
+                full_l, full_g, _ = O.tune_step(arch, params, xs, y, alphas, 1e-5, attn=at)
+                ok = int(W.item()) == int(np.sum(y != -1))
             ok &= np.allclose(loss.numpy(), full_l, rtol=1e-12)
             for i in range(E):
                 for k in params[i]:
@@ -76,12 +107,13 @@ def _worker(rank, world, port, q, arch="mlp"):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("arch", ["mlp", "layer"])
-def test_data_parallel_world2_matches_full_batch_oracle(arch):
+@pytest.mark.parametrize("arch,weighting", [("mlp", "uniform"), ("layer", "uniform"),
+                                            ("mlp", "confidence")])
+def test_data_parallel_world2_matches_full_batch_oracle(arch, weighting):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, arch)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, arch, weighting)) for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:

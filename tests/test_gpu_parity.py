@@ -195,3 +195,54 @@ def test_confidence_weighting_rejected_for_dp_shard(gpu_lib):
                         torch.zeros(8, dtype=torch.int32, device="cuda"), [1.0], p, g,
                         torch.zeros(1, device="cuda"), ws, valid_count=vc)
     assert e.value.code == 11
+
+
+@pytest.mark.parametrize("arch", ["mlp", "layer"])
+def test_confidence_weighting_data_parallel_shards(gpu_lib, arch):
+    """DP confidence weighting (NEXT #1 under DP): two token shards
+    run EE_WEIGHT_CONFIDENCE_SUM (unnormalised sum_t c_t loss_t, its gradient,
+    weight_sum = sum_t c_t); their sums, normalised by ee_normalize_exit,
+    equal the oracle's full-batch confidence-weighted loss and gradients."""
+    from harness import attn_kwargs
+    ee = gpu_lib
+    if arch == "layer":
+        cfg = S.get_cfg("tiny_layer", seed=33)
+    else:
+        cfg = S.Cfg(name="small", hidden=128, vocab=1000, ffn=256, arch="mlp", tokens=256,
+                    layers=2, after=[1, 2], init="random", seed=33)
+    n = cfg.tokens
+    hidden = S.hidden_states(cfg, n)
+    targets = S.targets(cfg, n)
+    params = S.head_params(cfg)
+    c = ee.make_config(cfg.hidden, cfg.vocab, cfg.ffn, 1, arch, token_weighting="confidence_sum",
+                       **attn_kwargs(cfg))
+    ops = {k: (v.cuda().float().contiguous() if k.startswith("g_") else
+               v.cuda().to(torch.bfloat16).contiguous()) for k, v in params[0].items()}
+    half = n // 2
+    tot_g = {k: torch.zeros(v.shape, device="cuda") for k, v in params[0].items()}
+    tot_l = torch.zeros(1, device="cuda")
+    tot_w = torch.zeros(1, device="cuda")
+    for r in range(2):                                   # the two ranks, one after the other
+        sl = slice(r * half, (r + 1) * half)
+        g = {k: torch.zeros(v.shape, device="cuda") for k, v in params[0].items()}
+        l = torch.zeros(1, device="cuda")
+        w = torch.zeros(1, device="cuda")
+        ws = torch.zeros(ee.ee_workspace_size(c, half), dtype=torch.uint8, device="cuda")
+        ee.ee_tune_step(c, [hidden[0][sl].cuda().contiguous()],
+                        targets[sl].cuda().to(torch.int32).contiguous(), [0.8], [ops], [g], l, ws,
+                        aux=[{"weight_sum": w}])
+        for k in g:                                      # the SUM all-reduce
+            tot_g[k] += g[k]
+        tot_l += l
+        tot_w += w
+    ee.ee_normalize_exit(c, tot_g, tot_l, tot_w)
+    torch.cuda.synchronize()
+    res = oracle_exit(arch, params[0], hidden[0], targets, 0.8, weighting="confidence",
+                      attn=S.attn_geometry(cfg))
+    valid = targets.numpy() != -1
+    C = float(np.sum(res.stats["conf"][valid]))
+    assert abs(tot_w.item() - C) <= 1e-3 * C
+    assert abs(tot_l.item() - res.loss) <= 1e-3 * abs(res.loss)
+    from harness import rel_fro
+    for k, gk in res.grads.items():
+        assert rel_fro(tot_g[k].double().cpu().numpy(), gk) <= 2e-2, k
