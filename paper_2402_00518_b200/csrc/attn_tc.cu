@@ -3,7 +3,9 @@
 // (Llama-2 attention; Layer exit P:210).
 //
 // One CTA per (128-query tile, query head, sequence); head dim 128.
-//   warp 0      TMA producer: Q once, then K_j / V_j (128 keys) into a 2-stage ring
+//   warp 0      TMA producer of Q and K_j (128 keys, 2-stage ring; a stage is
+//               released as soon as its QK MMA completes)
+//   warp 3      TMA producer of V_j (3-stage ring, released after its PV MMA)
 //   warp 1      MMA issuer (one thread): S_j = Q K_j^T into one of two TMEM
 //               S buffers, then O (+)= P_j V_j into the TMEM O accumulator
 //   warps 4..7  softmax, one thread per query row (= TMEM lane): reads S_j,
@@ -29,8 +31,9 @@ constexpr int FA_BN = 128;                        // keys per tile
 constexpr int FA_D = 128;                         // head dim
 constexpr int FA_TILE = FA_BM * FA_D * 2;         // 32 KB: two 16 KB SW128 atoms
 constexpr int FA_ATOM = 16384;
-constexpr int FA_STAGES = 2;
-constexpr int FA_SMEM = 1024 + FA_TILE * (2 + 2 * FA_STAGES) + 256;
+constexpr int FA_KST = 2;                         // K ring stages
+constexpr int FA_VST = 3;                         // V ring stages
+constexpr int FA_SMEM = 1024 + FA_TILE * (2 + FA_KST + FA_VST) + 256;
 constexpr float FA_RESCALE = 8.0f;                // log2 headroom before O is rescaled
 }  // namespace
 
@@ -43,16 +46,18 @@ __global__ void __launch_bounds__(256, 1)
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + FA_TILE;
-  uint8_t* sV = sK + FA_STAGES * FA_TILE;
-  uint8_t* sP = sV + FA_STAGES * FA_TILE;
+  uint8_t* sV = sK + FA_KST * FA_TILE;
+  uint8_t* sP = sV + FA_VST * FA_TILE;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sP + FA_TILE);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;    // [2]
-  uint64_t* p_full = bars + 7;
-  uint64_t* o_done = bars + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+  uint64_t* k_full = bars + 1;               // [KST]
+  uint64_t* k_empty = k_full + FA_KST;       // [KST]
+  uint64_t* v_full = k_empty + FA_KST;       // [VST]
+  uint64_t* v_empty = v_full + FA_VST;       // [VST]
+  uint64_t* s_full = v_empty + FA_VST;       // [2]
+  uint64_t* p_full = s_full + 2;
+  uint64_t* o_done = p_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqt = (T + FA_BM - 1) / FA_BM;
@@ -67,11 +72,16 @@ __global__ void __launch_bounds__(256, 1)
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
     mbar_init(q_full, 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
-      mbar_init(&s_full[s], 1);
+    for (int s = 0; s < FA_KST; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
     }
+    for (int s = 0; s < FA_VST; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    mbar_init(&s_full[0], 1);
+    mbar_init(&s_full[1], 1);
     mbar_init(p_full, 128);
     mbar_init(o_done, 1);
     fence_barrier_init();
@@ -87,22 +97,32 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t tS0 = tmem_base, tO = tmem_base + 2 * FA_BN;
 
   if (warp == 0) {
-    // ---------------------------------------------------------------- TMA producer
+    // ---------------------------------------------------------------- TMA: Q, K
     if (lane == 0) {
       tma_load_2d(sQ, &tmQ, q_full, hq * FA_D, q_row0);
       tma_load_2d(sQ + FA_ATOM, &tmQ, q_full, hq * FA_D + 64, q_row0);
       mbar_arrive_expect_tx(q_full, FA_TILE);
       for (int j = 0; j < n_kt; ++j) {
-        const int s = j & 1;
-        mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
-        const int k_row0 = b * T + j * FA_BN;
+        const int s = j % FA_KST;
+        mbar_wait(&k_empty[s], ((j / FA_KST) & 1) ^ 1);
         uint8_t* k = sK + s * FA_TILE;
+        const int k_row0 = b * T + j * FA_BN;
+        tma_load_2d(k, &tmK, &k_full[s], hk * FA_D, k_row0);
+        tma_load_2d(k + FA_ATOM, &tmK, &k_full[s], hk * FA_D + 64, k_row0);
+        mbar_arrive_expect_tx(&k_full[s], FA_TILE);
+      }
+    }
+  } else if (warp == 3) {
+    // ---------------------------------------------------------------- TMA: V
+    if (lane == 0) {
+      for (int j = 0; j < n_kt; ++j) {
+        const int s = j % FA_VST;
+        mbar_wait(&v_empty[s], ((j / FA_VST) & 1) ^ 1);
         uint8_t* v = sV + s * FA_TILE;
-        tma_load_2d(k, &tmK, &kv_full[s], hk * FA_D, k_row0);
-        tma_load_2d(k + FA_ATOM, &tmK, &kv_full[s], hk * FA_D + 64, k_row0);
-        tma_load_2d(v, &tmV, &kv_full[s], hk * FA_D, k_row0);
-        tma_load_2d(v + FA_ATOM, &tmV, &kv_full[s], hk * FA_D + 64, k_row0);
-        mbar_arrive_expect_tx(&kv_full[s], 2 * FA_TILE);
+        const int k_row0 = b * T + j * FA_BN;
+        tma_load_2d(v, &tmV, &v_full[s], hk * FA_D, k_row0);
+        tma_load_2d(v + FA_ATOM, &tmV, &v_full[s], hk * FA_D + 64, k_row0);
+        mbar_arrive_expect_tx(&v_full[s], FA_TILE);
       }
     }
   } else if (warp == 1) {
@@ -113,24 +133,27 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t aq = smem_u32(sQ), ap = smem_u32(sP);
       mbar_wait(q_full, 0);
       auto issue_qk = [&](int j) {
-        const int s = j & 1;
-        mbar_wait(&kv_full[s], (j >> 1) & 1);
+        const int s = j % FA_KST;
+        mbar_wait(&k_full[s], (j / FA_KST) & 1);
         tc_fence_after();
         const uint32_t bk = smem_u32(sK + s * FA_TILE);
 #pragma unroll
         for (int k = 0; k < FA_D / 16; ++k) {  // K-major A and B: 4 k-steps per 64-wide atom
           const uint32_t off = (k >> 2) * FA_ATOM + (k & 3) * 32;
-          tc_mma_f16(tS0 + s * FA_BN, make_sdesc(aq + off, 16, 1024), make_sdesc(bk + off, 16, 1024),
-                     idesc_qk, k != 0 ? 1u : 0u);
+          tc_mma_f16(tS0 + (j & 1) * FA_BN, make_sdesc(aq + off, 16, 1024),
+                     make_sdesc(bk + off, 16, 1024), idesc_qk, k != 0 ? 1u : 0u);
         }
-        tc_commit(&s_full[s]);
+        tc_commit(&s_full[j & 1]);
+        tc_commit(&k_empty[s]);  // K_j is free once S_j is computed
       };
       issue_qk(0);
       for (int j = 0; j < n_kt; ++j) {
         if (j + 1 < n_kt) issue_qk(j + 1);
+        const int sv = j % FA_VST;
+        mbar_wait(&v_full[sv], (j / FA_VST) & 1);
         mbar_wait(p_full, j & 1);
         tc_fence_after();
-        const uint32_t bv = smem_u32(sV + (j & 1) * FA_TILE);
+        const uint32_t bv = smem_u32(sV + sv * FA_TILE);
 #pragma unroll
         for (int k = 0; k < FA_BN / 16; ++k) {  // A = P (K-major), B = V (MN-major: keys x d)
           const uint32_t offa = (k >> 2) * FA_ATOM + (k & 3) * 32;
@@ -138,7 +161,7 @@ __global__ void __launch_bounds__(256, 1)
                      idesc_pv, (j | k) != 0 ? 1u : 0u);
         }
         tc_commit(o_done);
-        tc_commit(&kv_empty[j & 1]);
+        tc_commit(&v_empty[sv]);
       }
     }
   } else if (warp >= 4) {
@@ -147,70 +170,89 @@ __global__ void __launch_bounds__(256, 1)
     const int r = ew * 32 + lane;  // query row within the tile = TMEM lane
     const uint32_t lane_off = static_cast<uint32_t>(ew * 32) << 16;
     float m_ref = -INFINITY, l = 0.f;
-    uint8_t* prow = sP + r * 128;
+    const uint32_t prow = smem_u32(sP) + r * 128;
     for (int j = 0; j < n_kt; ++j) {
       mbar_wait(&s_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
-      float sv[FA_BN];
+      // all four 32-column TMEM loads in flight, one wait (outputs are only
+      // read after tcgen05.wait::ld)
+      uint32_t sr[FA_BN];
       const uint32_t ts = tS0 + (j & 1) * FA_BN + lane_off;
+      tmem_ld_32x32b_x32(ts, *reinterpret_cast<uint32_t(*)[32]>(sr));
+      tmem_ld_32x32b_x32(ts + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+      tmem_ld_32x32b_x32(ts + 64, *reinterpret_cast<uint32_t(*)[32]>(sr + 64));
+      tmem_ld_32x32b_x32(ts + 96, *reinterpret_cast<uint32_t(*)[32]>(sr + 96));
+      tmem_ld_wait();
+      float sv[FA_BN];
 #pragma unroll
-      for (int c = 0; c < FA_BN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(ts + c * 32, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(v[i]) * scale_log2;
-      }
+      for (int i = 0; i < FA_BN; ++i) sv[i] = __uint_as_float(sr[i]);
       if (j == qt) {  // diagonal tile: key column > query row is in the future
 #pragma unroll
         for (int i = 0; i < FA_BN; ++i)
           if (i > r) sv[i] = -INFINITY;
       }
-      float mx = sv[0];
+      // row max with 8 independent chains (latency, not throughput, bound)
+      float m8[8];
 #pragma unroll
-      for (int i = 1; i < FA_BN; ++i) mx = fmaxf(mx, sv[i]);
+      for (int e = 0; e < 8; ++e) m8[e] = sv[e];
+#pragma unroll
+      for (int i = 8; i < FA_BN; i += 8)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) m8[e] = fmaxf(m8[e], sv[i + e]);
+      float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                       fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+      mx *= scale_log2;
+      // reference max: set on the first tile, raised only past the 2^8 headroom
+      // (warp-uniform, since the O rescale below is a warp-collective TMEM op)
+      bool grow = false;
+      float alpha = 1.0f;
+      if (j == 0) {
+        m_ref = mx;
+      } else {
+        grow = mx > m_ref + FA_RESCALE;
+        if (grow) {
+          alpha = ex2_approx(m_ref - mx);
+          l *= alpha;
+          m_ref = mx;
+        }
+      }
+      const bool any_grow = __any_sync(0xffffffffu, grow);
+      // P = 2^(s * scale - m_ref): computed BEFORE waiting for PV_{j-1}, so the
+      // exp2 work overlaps the tensor core (one FFMA + one MUFU per element)
+      uint32_t pk[FA_BN / 2];
+      float l8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int i = 0; i < FA_BN / 2; ++i) {
+        const float p0 = ex2_approx(fmaf(sv[2 * i], scale_log2, -m_ref));
+        const float p1 = ex2_approx(fmaf(sv[2 * i + 1], scale_log2, -m_ref));
+        l8[(2 * i) & 7] += p0;
+        l8[(2 * i + 1) & 7] += p1;
+        pk[i] = pack_bf16(p0, p1);
+      }
+      l += ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
       if (j > 0) {
         mbar_wait(o_done, (j - 1) & 1);  // PV_{j-1} done: O stable, P buffer free
         tc_fence_after();
       }
-      if (j == 0) {
-        m_ref = mx;
-      } else {
-        // tcgen05.ld/st are warp-collective: the rescale decision is per warp
-        // (rows that did not grow past the headroom use alpha = 1)
-        const bool grow = mx > m_ref + FA_RESCALE;
-        if (__any_sync(0xffffffffu, grow)) {
-          const float alpha = grow ? ex2_approx(m_ref - mx) : 1.0f;
-          if (grow) {
-            l *= alpha;
-            m_ref = mx;
-          }
+      if (any_grow) {
 #pragma unroll 1
-          for (int c = 0; c < FA_D / 32; ++c) {
-            uint32_t v[32];
-            tmem_ld_32x32b_x32(tO + lane_off + c * 32, v);
-            tmem_ld_wait();
+        for (int c = 0; c < FA_D / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(tO + lane_off + c * 32, v);
+          tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-            tmem_st_32x32b_x32(tO + lane_off + c * 32, v);
-          }
-          tmem_st_wait();
+          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+          tmem_st_32x32b_x32(tO + lane_off + c * 32, v);
         }
+        tmem_st_wait();
       }
-      // P = 2^(s - m_ref) -> bf16, K-major SWIZZLE_128B: 16-byte chunk cc of
-      // row r sits at chunk (cc ^ (r & 7)) of the row's 128-byte line
+      // P -> smem, K-major SWIZZLE_128B: 16-byte chunk cc of row r sits at
+      // chunk (cc ^ (r & 7)) of the row's 128-byte line
 #pragma unroll
       for (int c8 = 0; c8 < FA_BN / 8; ++c8) {
-        float p[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          p[e] = ex2_approx(sv[c8 * 8 + e] - m_ref);
-          l += p[e];
-        }
-        const uint4 w = make_uint4(pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]),
-                                   pack_bf16(p[4], p[5]), pack_bf16(p[6], p[7]));
         const int cc = c8 & 7;
-        *reinterpret_cast<uint4*>(prow + (c8 >> 3) * FA_ATOM + ((cc ^ (r & 7)) << 4)) = w;
+        st_shared_v4(prow + (c8 >> 3) * FA_ATOM + ((cc ^ (r & 7)) << 4), pk[4 * c8],
+                     pk[4 * c8 + 1], pk[4 * c8 + 2], pk[4 * c8 + 3]);
       }
       fence_proxy_async_smem();
       tc_fence_before();
@@ -289,9 +331,14 @@ cudaError_t launch_attn_fwd_tc(const __nv_bfloat16* q, const __nv_bfloat16* k,
 namespace {
 constexpr int FB_BQ = 64;                       // queries per step of the dK/dV kernel
 constexpr int FB_QT = FB_BQ * FA_D * 2;         // 16 KB: two 8 KB SW128 atoms
-constexpr int FB_SMEM_KV = 1024 + 2 * FA_TILE + 2 * 2 * FB_QT + 2 * (FA_BN * FB_BQ * 2) +
+constexpr int FB_PT = FA_BN * FB_BQ * 2;       // one [128 x 64] bf16 operand (16 KB)
+constexpr int FB_SMEM_KV = 1024 + 2 * FA_TILE + 2 * 2 * FB_QT + 2 * 2 * FB_PT +
                            2 * 2 * FB_BQ * 4 + 256;
-constexpr int FB_SMEM_Q = 1024 + 2 * FA_TILE + 2 * 2 * FA_TILE + FA_TILE + 256;
+constexpr int FQ_BK = 64;                       // keys per step of the dQ kernel
+constexpr int FQ_KT = FQ_BK * FA_D * 2;         // 16 KB K or V tile
+constexpr int FQ_STAGES = 4;
+constexpr int FQ_DS = FA_BM * FQ_BK * 2;        // 16 KB dS tile
+constexpr int FB_SMEM_Q = 1024 + 2 * FA_TILE + FQ_STAGES * 2 * FQ_KT + 2 * FQ_DS + 256;
 
 // RoPE^T (rotation by -angle) of 32 columns [c0, c0 + 32) (c0 < 64) paired
 // with [c0 + 64, c0 + 96) of one row at position pos.
@@ -372,18 +419,18 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* sV = sK + FA_TILE;
   uint8_t* sQ = sV + FA_TILE;          // [2] x 16 KB
   uint8_t* sDO = sQ + 2 * FB_QT;       // [2] x 16 KB
-  uint8_t* sPt = sDO + 2 * FB_QT;      // [128 keys x 64 q] bf16, one 16 KB atom
-  uint8_t* sDSt = sPt + FA_BN * FB_BQ * 2;
-  float* sL = reinterpret_cast<float*>(sDSt + FA_BN * FB_BQ * 2);  // [2][64]
-  float* sD = sL + 2 * FB_BQ;                                       // [2][64]
+  uint8_t* sPt = sDO + 2 * FB_QT;      // [2] x [128 keys x 64 q] bf16 (one 16 KB atom each)
+  uint8_t* sDSt = sPt + 2 * FB_PT;     // [2]
+  float* sL = reinterpret_cast<float*>(sDSt + 2 * FB_PT);  // [2][64]
+  float* sD = sL + 2 * FB_BQ;                              // [2][64]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 2 * FB_BQ);
   uint64_t* kv_full = bars;
   uint64_t* qd_full = bars + 1;   // [2]
   uint64_t* qd_empty = bars + 3;  // [2]
-  uint64_t* sdp_full = bars + 5;
-  uint64_t* pds_full = bars + 6;
-  uint64_t* acc_done = bars + 7;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  uint64_t* sdp_full = bars + 5;  // [2]
+  uint64_t* pds_full = bars + 7;
+  uint64_t* acc_done = bars + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kt = blockIdx.x, hk = blockIdx.y, b = blockIdx.z;
@@ -404,7 +451,8 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&qd_full[s], 1);
       mbar_init(&qd_empty[s], 1);
     }
-    mbar_init(sdp_full, 1);
+    mbar_init(&sdp_full[0], 1);
+    mbar_init(&sdp_full[1], 1);
     mbar_init(pds_full, 128);
     mbar_init(acc_done, 1);
     fence_barrier_init();
@@ -417,8 +465,8 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const uint32_t tS = tmem_base, tDP = tmem_base + 64, tDK = tmem_base + 128,
-                 tDV = tmem_base + 256;
+  // S^T[b] at b*128, dP^T[b] at b*128 + 64 (b = step parity); dK, dV after
+  const uint32_t tDK = tmem_base + 256, tDV = tmem_base + 384;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -446,14 +494,16 @@ __global__ void __launch_bounds__(256, 1)
       constexpr uint32_t idesc_s = make_idesc_bf16(FA_BN, FB_BQ, false, false);   // 128 x 64
       constexpr uint32_t idesc_acc = make_idesc_bf16(FA_BN, FA_D, false, true);   // 128 x 128
       const uint32_t ak = smem_u32(sK), av = smem_u32(sV);
-      const uint32_t apt = smem_u32(sPt), ads = smem_u32(sDSt);
       mbar_wait(kv_full, 0);
       tc_fence_after();
-      for (int it = 0; it < n_it; ++it) {
+      // S^T / dP^T of step `it` into TMEM buffer it & 1, issued one step ahead
+      // so the tensor core works while the softmax threads process the last one
+      auto issue_sdp = [&](int it) {
         const int s = it & 1;
         mbar_wait(&qd_full[s], (it >> 1) & 1);
         tc_fence_after();
         const uint32_t bq = smem_u32(sQ + s * FB_QT), bd = smem_u32(sDO + s * FB_QT);
+        const uint32_t tS = tmem_base + s * 128, tDP = tS + 64;
 #pragma unroll
         for (int k = 0; k < FA_D / 16; ++k) {  // S^T = K Q^T, dP^T = V dO^T (K-major, K = d)
           const uint32_t offa = (k >> 2) * FA_ATOM + (k & 3) * 32;
@@ -463,9 +513,16 @@ __global__ void __launch_bounds__(256, 1)
           tc_mma_f16(tDP, make_sdesc(av + offa, 16, 1024), make_sdesc(bd + offb, 16, 1024),
                      idesc_s, k != 0 ? 1u : 0u);
         }
-        tc_commit(sdp_full);
+        tc_commit(&sdp_full[s]);
+      };
+      if (n_it > 0) issue_sdp(0);
+      for (int it = 0; it < n_it; ++it) {
+        const int s = it & 1;
+        if (it + 1 < n_it) issue_sdp(it + 1);
         mbar_wait(pds_full, it & 1);
         tc_fence_after();
+        const uint32_t bq = smem_u32(sQ + s * FB_QT), bd = smem_u32(sDO + s * FB_QT);
+        const uint32_t apt = smem_u32(sPt + s * FB_PT), ads = smem_u32(sDSt + s * FB_PT);
 #pragma unroll
         for (int k = 0; k < FB_BQ / 16; ++k) {  // dV += P^T dO, dK += dS^T Q (B MN-major, K = q)
           const uint32_t offa = k * 32;
@@ -485,9 +542,12 @@ __global__ void __launch_bounds__(256, 1)
     const int kpos = kt * FA_BN + kr;
     const uint32_t lane_off = static_cast<uint32_t>(ew * 32) << 16;
     const int tid = threadIdx.x - 128;
-    uint8_t* pt_row = sPt + kr * 128;
-    uint8_t* ds_row = sDSt + kr * 128;
     for (int it = 0; it < n_it; ++it) {
+      // P^T / dS^T go to smem buffer it & 1: the dV/dK MMAs of step it-2 that
+      // read it were issued before S^T(it), so sdp_full[it & 1] covers them
+      const uint32_t pt_row = smem_u32(sPt) + (it & 1) * FB_PT + kr * 128;
+      const uint32_t ds_row = smem_u32(sDSt) + (it & 1) * FB_PT + kr * 128;
+      const uint32_t tS = tmem_base + (it & 1) * 128, tDP = tS + 64;
       const int hq = hk * grp + it / per_head;
       const int qpos0 = (q64_0 + it % per_head) * FB_BQ;
       const int q_row0 = b * T + qpos0;
@@ -502,13 +562,12 @@ __global__ void __launch_bounds__(256, 1)
         D[t2] = in ? Dv[(long long)(q_row0 + t2) * Hq + hq] : 0.f;
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      mbar_wait(sdp_full, it & 1);
+      mbar_wait(&sdp_full[it & 1], (it >> 1) & 1);
       tc_fence_after();
 #pragma unroll 1
       for (int c = 0; c < FB_BQ / 32; ++c) {
         uint32_t vs[32], vp[32];
         tmem_ld_32x32b_x32(tS + lane_off + c * 32, vs);
-        tmem_ld_wait();
         tmem_ld_32x32b_x32(tDP + lane_off + c * 32, vp);
         tmem_ld_wait();
         uint32_t wp[16], wd[16];
@@ -531,10 +590,8 @@ __global__ void __launch_bounds__(256, 1)
         for (int h = 0; h < 4; ++h) {  // 4 x 16-byte chunks of this 32-column slab
           const int cc = c * 4 + h;
           const int off = (cc ^ (kr & 7)) << 4;
-          *reinterpret_cast<uint4*>(pt_row + off) =
-              make_uint4(wp[4 * h], wp[4 * h + 1], wp[4 * h + 2], wp[4 * h + 3]);
-          *reinterpret_cast<uint4*>(ds_row + off) =
-              make_uint4(wd[4 * h], wd[4 * h + 1], wd[4 * h + 2], wd[4 * h + 3]);
+          st_shared_v4(pt_row + off, wp[4 * h], wp[4 * h + 1], wp[4 * h + 2], wp[4 * h + 3]);
+          st_shared_v4(ds_row + off, wd[4 * h], wd[4 * h + 1], wd[4 * h + 2], wd[4 * h + 3]);
         }
       }
       fence_proxy_async_smem();
@@ -558,8 +615,11 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
-// dQ: one CTA per (128-query tile, query head, sequence); loops over the key
-// tiles at or before the query tile.  TMEM: S | dP | dQ (128 columns each).
+// dQ: one CTA per (128-query tile, query head, sequence); loops over the
+// 64-key tiles at or before the query tile (4-stage K/V ring).  TMEM: S[2] |
+// dP[2] (64 columns each, double-buffered so S/dP of step j+1 are computed
+// while the softmax threads form dS_j) | dQ (128 columns).  dS in smem is
+// double-buffered for the same reason.
 __global__ void __launch_bounds__(256, 1)
     attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
                           const __grid_constant__ CUtensorMap tmK,
@@ -573,17 +633,17 @@ __global__ void __launch_bounds__(256, 1)
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sQ = smem;
   uint8_t* sDO = sQ + FA_TILE;
-  uint8_t* sK = sDO + FA_TILE;            // [2]
-  uint8_t* sV = sK + 2 * FA_TILE;         // [2]
-  uint8_t* sDS = sV + 2 * FA_TILE;        // [128 q x 128 keys] bf16, two atoms
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sDS + FA_TILE);
+  uint8_t* sK = sDO + FA_TILE;                  // [STAGES] x 16 KB (64 keys x 128 d)
+  uint8_t* sV = sK + FQ_STAGES * FQ_KT;         // [STAGES]
+  uint8_t* sDS = sV + FQ_STAGES * FQ_KT;        // [2] x [128 q x 64 keys] bf16, one atom each
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sDS + 2 * FQ_DS);
   uint64_t* qo_full = bars;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* sdp_full = bars + 5;
-  uint64_t* ds_full = bars + 6;
-  uint64_t* acc_done = bars + 7;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  uint64_t* kv_full = bars + 1;                 // [STAGES]
+  uint64_t* kv_empty = kv_full + FQ_STAGES;     // [STAGES]
+  uint64_t* sdp_full = kv_empty + FQ_STAGES;    // [2]
+  uint64_t* ds_full = sdp_full + 2;
+  uint64_t* acc_done = ds_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqt = (T + FA_BM - 1) / FA_BM;
@@ -591,7 +651,7 @@ __global__ void __launch_bounds__(256, 1)
   const int hq = blockIdx.y, b = blockIdx.z;
   const int hk = hq / (Hq / Hkv);
   const int q_row0 = b * T + qt * FA_BM;
-  const int n_kt = qt + 1;
+  const int n_kt = (qt + 1) * (FA_BM / FQ_BK);   // 64-key tiles up to the diagonal
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
@@ -599,11 +659,12 @@ __global__ void __launch_bounds__(256, 1)
     tma_prefetch_desc(&tmV);
     tma_prefetch_desc(&tmDO);
     mbar_init(qo_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < FQ_STAGES; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
-    mbar_init(sdp_full, 1);
+    mbar_init(&sdp_full[0], 1);
+    mbar_init(&sdp_full[1], 1);
     mbar_init(ds_full, 128);
     mbar_init(acc_done, 1);
     fence_barrier_init();
@@ -616,7 +677,7 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const uint32_t tS = tmem_base, tDP = tmem_base + 128, tDQ = tmem_base + 256;
+  const uint32_t tDQ = tmem_base + 256;          // S[b] at b*128, dP[b] at b*128 + 64
 
   if (warp == 0) {
     if (lane == 0) {
@@ -626,46 +687,52 @@ __global__ void __launch_bounds__(256, 1)
       tma_load_2d(sDO + FA_ATOM, &tmDO, qo_full, hq * FA_D + 64, q_row0);
       mbar_arrive_expect_tx(qo_full, 2 * FA_TILE);
       for (int j = 0; j < n_kt; ++j) {
-        const int s = j & 1;
-        mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
-        const int k_row0 = b * T + j * FA_BN;
-        uint8_t* k = sK + s * FA_TILE;
-        uint8_t* v = sV + s * FA_TILE;
+        const int s = j % FQ_STAGES;
+        mbar_wait(&kv_empty[s], ((j / FQ_STAGES) & 1) ^ 1);
+        const int k_row0 = b * T + j * FQ_BK;
+        uint8_t* k = sK + s * FQ_KT;
+        uint8_t* v = sV + s * FQ_KT;
         tma_load_2d(k, &tmK, &kv_full[s], hk * FA_D, k_row0);
-        tma_load_2d(k + FA_ATOM, &tmK, &kv_full[s], hk * FA_D + 64, k_row0);
+        tma_load_2d(k + FQ_KT / 2, &tmK, &kv_full[s], hk * FA_D + 64, k_row0);
         tma_load_2d(v, &tmV, &kv_full[s], hk * FA_D, k_row0);
-        tma_load_2d(v + FA_ATOM, &tmV, &kv_full[s], hk * FA_D + 64, k_row0);
-        mbar_arrive_expect_tx(&kv_full[s], 2 * FA_TILE);
+        tma_load_2d(v + FQ_KT / 2, &tmV, &kv_full[s], hk * FA_D + 64, k_row0);
+        mbar_arrive_expect_tx(&kv_full[s], 2 * FQ_KT);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc_s = make_idesc_bf16(FA_BM, FA_BN, false, false);
-      constexpr uint32_t idesc_dq = make_idesc_bf16(FA_BM, FA_D, false, true);
-      const uint32_t aq = smem_u32(sQ), ado = smem_u32(sDO), ads = smem_u32(sDS);
+      constexpr uint32_t idesc_s = make_idesc_bf16(FA_BM, FQ_BK, false, false);   // 128 x 64
+      constexpr uint32_t idesc_dq = make_idesc_bf16(FA_BM, FA_D, false, true);    // 128 x 128
+      const uint32_t aq = smem_u32(sQ), ado = smem_u32(sDO);
       mbar_wait(qo_full, 0);
-      for (int j = 0; j < n_kt; ++j) {
-        const int s = j & 1;
-        mbar_wait(&kv_full[s], (j >> 1) & 1);
+      auto issue_sdp = [&](int j) {
+        const int s = j % FQ_STAGES;
+        mbar_wait(&kv_full[s], (j / FQ_STAGES) & 1);
         tc_fence_after();
-        const uint32_t bk = smem_u32(sK + s * FA_TILE), bv = smem_u32(sV + s * FA_TILE);
+        const uint32_t bk = smem_u32(sK + s * FQ_KT), bv = smem_u32(sV + s * FQ_KT);
+        const uint32_t tS = tmem_base + (j & 1) * 128, tDP = tS + 64;
 #pragma unroll
-        for (int k = 0; k < FA_D / 16; ++k) {  // S = Q K^T, dP = dO V^T
-          const uint32_t off = (k >> 2) * FA_ATOM + (k & 3) * 32;
-          tc_mma_f16(tS, make_sdesc(aq + off, 16, 1024), make_sdesc(bk + off, 16, 1024), idesc_s,
+        for (int k = 0; k < FA_D / 16; ++k) {  // S = Q K^T, dP = dO V^T  (K = d)
+          const uint32_t offa = (k >> 2) * FA_ATOM + (k & 3) * 32;
+          const uint32_t offb = (k >> 2) * (FQ_KT / 2) + (k & 3) * 32;
+          tc_mma_f16(tS, make_sdesc(aq + offa, 16, 1024), make_sdesc(bk + offb, 16, 1024), idesc_s,
                      k != 0 ? 1u : 0u);
-          tc_mma_f16(tDP, make_sdesc(ado + off, 16, 1024), make_sdesc(bv + off, 16, 1024),
+          tc_mma_f16(tDP, make_sdesc(ado + offa, 16, 1024), make_sdesc(bv + offb, 16, 1024),
                      idesc_s, k != 0 ? 1u : 0u);
         }
-        tc_commit(sdp_full);
+        tc_commit(&sdp_full[j & 1]);
+      };
+      issue_sdp(0);
+      for (int j = 0; j < n_kt; ++j) {
+        if (j + 1 < n_kt) issue_sdp(j + 1);
         mbar_wait(ds_full, j & 1);
         tc_fence_after();
+        const int s = j % FQ_STAGES;
+        const uint32_t bk = smem_u32(sK + s * FQ_KT), ads = smem_u32(sDS + (j & 1) * FQ_DS);
 #pragma unroll
-        for (int k = 0; k < FA_BN / 16; ++k) {  // dQ += dS K  (K MN-major: keys x d)
-          const uint32_t offa = (k >> 2) * FA_ATOM + (k & 3) * 32;
-          tc_mma_f16(tDQ, make_sdesc(ads + offa, 16, 1024), make_sdesc(bk + k * 2048, FA_ATOM, 1024),
-                     idesc_dq, (j | k) != 0 ? 1u : 0u);
-        }
+        for (int k = 0; k < FQ_BK / 16; ++k)  // dQ += dS K  (K MN-major: keys x d, LBO 8 KB)
+          tc_mma_f16(tDQ, make_sdesc(ads + k * 32, 16, 1024),
+                     make_sdesc(bk + k * 2048, FQ_KT / 2, 1024), idesc_dq, (j | k) != 0 ? 1u : 0u);
         tc_commit(&kv_empty[s]);
       }
       tc_commit(acc_done);
@@ -678,16 +745,16 @@ __global__ void __launch_bounds__(256, 1)
     const bool ok = pos < T;
     const float Lr = ok ? lse2[(long long)(q_row0 + r) * Hq + hq] : 0.f;
     const float Dr = ok ? Dv[(long long)(q_row0 + r) * Hq + hq] : 0.f;
-    uint8_t* ds_row = sDS + r * 128;
     for (int j = 0; j < n_kt; ++j) {
-      mbar_wait(sdp_full, j & 1);
+      mbar_wait(&sdp_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
+      const uint32_t tS = tmem_base + (j & 1) * 128 + lane_off, tDP = tS + 64;
+      const uint32_t ds_row = smem_u32(sDS) + (j & 1) * FQ_DS + r * 128;
 #pragma unroll 1
-      for (int c = 0; c < FA_BN / 32; ++c) {
+      for (int c = 0; c < FQ_BK / 32; ++c) {
         uint32_t vs[32], vp[32];
-        tmem_ld_32x32b_x32(tS + lane_off + c * 32, vs);
-        tmem_ld_wait();
-        tmem_ld_32x32b_x32(tDP + lane_off + c * 32, vp);
+        tmem_ld_32x32b_x32(tS + c * 32, vs);
+        tmem_ld_32x32b_x32(tDP + c * 32, vp);
         tmem_ld_wait();
         uint32_t wd[16];
 #pragma unroll
@@ -695,8 +762,8 @@ __global__ void __launch_bounds__(256, 1)
           float d2[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int kpos = j * FA_BN + c * 32 + 2 * q + e;
-            float p = ex2_approx(__uint_as_float(vs[2 * q + e]) * scale_log2 - Lr);
+            const int kpos = j * FQ_BK + c * 32 + 2 * q + e;
+            float p = ex2_approx(fmaf(__uint_as_float(vs[2 * q + e]), scale_log2, -Lr));
             if (kpos > pos || !ok) p = 0.f;
             d2[e] = p * (__uint_as_float(vp[2 * q + e]) - Dr);
           }
@@ -704,10 +771,9 @@ __global__ void __launch_bounds__(256, 1)
         }
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
-          const int c8 = c * 4 + h;  // 16-byte chunk index over 128 keys
-          const int cc = c8 & 7;
-          *reinterpret_cast<uint4*>(ds_row + (c8 >> 3) * FA_ATOM + ((cc ^ (r & 7)) << 4)) =
-              make_uint4(wd[4 * h], wd[4 * h + 1], wd[4 * h + 2], wd[4 * h + 3]);
+          const int cc = c * 4 + h;  // 16-byte chunk within the 128-byte row
+          st_shared_v4(ds_row + ((cc ^ (r & 7)) << 4), wd[4 * h], wd[4 * h + 1], wd[4 * h + 2],
+                       wd[4 * h + 3]);
         }
       }
       fence_proxy_async_smem();
@@ -747,10 +813,11 @@ cudaError_t launch_attn_bwd_tc(const __nv_bfloat16* q, const __nv_bfloat16* k,
   const Mat DO{dout, N, (long long)Hq * FA_D, (long long)Hq * FA_D};
   const Mat K{k, N, (long long)Hkv * FA_D, (long long)Hkv * FA_D};
   const Mat V{v, N, (long long)Hkv * FA_D, (long long)Hkv * FA_D};
-  CUtensorMap tq64, tdo64, tq128, tdo128, tk, tv;
+  CUtensorMap tq64, tdo64, tq128, tdo128, tk, tv, tk64, tv64;
   if (!make_tmap(&tq64, Q, 64, FB_BQ) || !make_tmap(&tdo64, DO, 64, FB_BQ) ||
       !make_tmap(&tq128, Q, 64, FA_BM) || !make_tmap(&tdo128, DO, 64, FA_BM) ||
-      !make_tmap(&tk, K, 64, FA_BN) || !make_tmap(&tv, V, 64, FA_BN))
+      !make_tmap(&tk, K, 64, FA_BN) || !make_tmap(&tv, V, 64, FA_BN) ||
+      !make_tmap(&tk64, K, 64, FQ_BK) || !make_tmap(&tv64, V, 64, FQ_BK))
     return cudaErrorInvalidValue;
   const float scale = 1.0f / sqrtf((float)FA_D);
   const float scale_log2 = 1.4426950408889634f * scale;
@@ -761,8 +828,8 @@ cudaError_t launch_attn_bwd_tc(const __nv_bfloat16* q, const __nv_bfloat16* k,
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   dim3 g2((T + FA_BM - 1) / FA_BM, Hq, B);
-  attn_bwd_dq_tc_kernel<<<g2, 256, FB_SMEM_Q, s>>>(tq128, tk, tv, tdo128, lse2, Dv, dq, T, Hq, Hkv,
-                                                   scale_log2, scale, rope_theta);
+  attn_bwd_dq_tc_kernel<<<g2, 256, FB_SMEM_Q, s>>>(tq128, tk64, tv64, tdo128, lse2, Dv, dq, T, Hq,
+                                                   Hkv, scale_log2, scale, rope_theta);
   return cudaGetLastError();
 }
 
