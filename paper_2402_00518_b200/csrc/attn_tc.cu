@@ -428,9 +428,9 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* qd_full = bars + 1;   // [2]
   uint64_t* qd_empty = bars + 3;  // [2]
   uint64_t* sdp_full = bars + 5;  // [2]
-  uint64_t* pds_full = bars + 7;
-  uint64_t* acc_done = bars + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+  uint64_t* pds_full = bars + 7;  // [2], per P^T/dS^T buffer (see attn_bwd_dq_tc_kernel)
+  uint64_t* acc_done = bars + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kt = blockIdx.x, hk = blockIdx.y, b = blockIdx.z;
@@ -453,7 +453,8 @@ __global__ void __launch_bounds__(256, 1)
     }
     mbar_init(&sdp_full[0], 1);
     mbar_init(&sdp_full[1], 1);
-    mbar_init(pds_full, 128);
+    mbar_init(&pds_full[0], 128);
+    mbar_init(&pds_full[1], 128);
     mbar_init(acc_done, 1);
     fence_barrier_init();
   }
@@ -519,7 +520,7 @@ __global__ void __launch_bounds__(256, 1)
       for (int it = 0; it < n_it; ++it) {
         const int s = it & 1;
         if (it + 1 < n_it) issue_sdp(it + 1);
-        mbar_wait(pds_full, it & 1);
+        mbar_wait(&pds_full[s], (it >> 1) & 1);
         tc_fence_after();
         const uint32_t bq = smem_u32(sQ + s * FB_QT), bd = smem_u32(sDO + s * FB_QT);
         const uint32_t apt = smem_u32(sPt + s * FB_PT), ads = smem_u32(sDSt + s * FB_PT);
@@ -542,25 +543,28 @@ __global__ void __launch_bounds__(256, 1)
     const int kpos = kt * FA_BN + kr;
     const uint32_t lane_off = static_cast<uint32_t>(ew * 32) << 16;
     const int tid = threadIdx.x - 128;
+    // thread tid < 64 stages lse2 of query tid of the step, tid >= 64 stages Dv;
+    // the global load for step it + 1 is issued during step it
+    auto stat_of = [&](int it) -> float {
+      const int hq = hk * grp + it / per_head;
+      const int qpos0 = (q64_0 + it % per_head) * FB_BQ;
+      const int t = tid & (FB_BQ - 1);
+      if (qpos0 + t >= T) return 0.f;
+      const long long idx = (long long)(b * T + qpos0 + t) * Hq + hq;
+      return tid < FB_BQ ? lse2[idx] : Dv[idx];
+    };
+    float stat_next = n_it > 0 ? stat_of(0) : 0.f;
     for (int it = 0; it < n_it; ++it) {
       // P^T / dS^T go to smem buffer it & 1: the dV/dK MMAs of step it-2 that
       // read it were issued before S^T(it), so sdp_full[it & 1] covers them
       const uint32_t pt_row = smem_u32(sPt) + (it & 1) * FB_PT + kr * 128;
       const uint32_t ds_row = smem_u32(sDSt) + (it & 1) * FB_PT + kr * 128;
       const uint32_t tS = tmem_base + (it & 1) * 128, tDP = tS + 64;
-      const int hq = hk * grp + it / per_head;
       const int qpos0 = (q64_0 + it % per_head) * FB_BQ;
-      const int q_row0 = b * T + qpos0;
       float* L = sL + (it & 1) * FB_BQ;
       float* D = sD + (it & 1) * FB_BQ;
-      if (tid < FB_BQ) {
-        const bool in = qpos0 + tid < T;
-        L[tid] = in ? lse2[(long long)(q_row0 + tid) * Hq + hq] : 0.f;
-      } else {
-        const int t2 = tid - FB_BQ;
-        const bool in = qpos0 + t2 < T;
-        D[t2] = in ? Dv[(long long)(q_row0 + t2) * Hq + hq] : 0.f;
-      }
+      (tid < FB_BQ ? L : D)[tid & (FB_BQ - 1)] = stat_next;
+      if (it + 1 < n_it) stat_next = stat_of(it + 1);
       asm volatile("bar.sync 1, 128;" ::: "memory");
       mbar_wait(&sdp_full[it & 1], (it >> 1) & 1);
       tc_fence_after();
@@ -596,7 +600,7 @@ __global__ void __launch_bounds__(256, 1)
       }
       fence_proxy_async_smem();
       tc_fence_before();
-      mbar_arrive(pds_full);
+      mbar_arrive(&pds_full[it & 1]);
     }
     mbar_wait(acc_done, 0);
     tc_fence_after();
@@ -616,10 +620,10 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 // dQ: one CTA per (128-query tile, query head, sequence); loops over the
-// 64-key tiles at or before the query tile (4-stage K/V ring).  TMEM: S[2] |
-// dP[2] (64 columns each, double-buffered so S/dP of step j+1 are computed
-// while the softmax threads form dS_j) | dQ (128 columns).  dS in smem is
-// double-buffered for the same reason.
+// 64-key tiles at or before the query tile (4-stage K/V ring).  TMEM: three
+// [S | dP] buffers of 128 columns (S/dP of steps j+1 and j+2 are queued on
+// the tensor core while the softmax threads form dS_j) and dQ (128 columns).
+// dS in smem is double-buffered.
 __global__ void __launch_bounds__(256, 1)
     attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
                           const __grid_constant__ CUtensorMap tmK,
@@ -640,9 +644,13 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* qo_full = bars;
   uint64_t* kv_full = bars + 1;                 // [STAGES]
   uint64_t* kv_empty = kv_full + FQ_STAGES;     // [STAGES]
-  uint64_t* sdp_full = kv_empty + FQ_STAGES;    // [2]
-  uint64_t* ds_full = sdp_full + 2;
-  uint64_t* acc_done = ds_full + 1;
+  uint64_t* sdp_full = kv_empty + FQ_STAGES;    // [3]
+  // ds_full[b] / ds_free[b] per dS buffer: one barrier per buffer so the
+  // softmax can never complete two phases of one barrier before the MMA
+  // thread observes the first (it runs up to two steps ahead of the MMA)
+  uint64_t* ds_full = sdp_full + 3;             // [2]
+  uint64_t* ds_free = ds_full + 2;              // [2]: dQ(j) done reading dS buffer j & 1
+  uint64_t* acc_done = ds_free + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -663,9 +671,11 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
-    mbar_init(&sdp_full[0], 1);
-    mbar_init(&sdp_full[1], 1);
-    mbar_init(ds_full, 128);
+    for (int bb = 0; bb < 3; ++bb) mbar_init(&sdp_full[bb], 1);
+    for (int bb = 0; bb < 2; ++bb) {
+      mbar_init(&ds_free[bb], 1);
+      mbar_init(&ds_full[bb], 128);
+    }
     mbar_init(acc_done, 1);
     fence_barrier_init();
   }
@@ -677,7 +687,7 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const uint32_t tDQ = tmem_base + 256;          // S[b] at b*128, dP[b] at b*128 + 64
+  const uint32_t tDQ = tmem_base + 384;          // S[b] at b*128, dP[b] at b*128 + 64, b < 3
 
   if (warp == 0) {
     if (lane == 0) {
@@ -710,7 +720,7 @@ __global__ void __launch_bounds__(256, 1)
         mbar_wait(&kv_full[s], (j / FQ_STAGES) & 1);
         tc_fence_after();
         const uint32_t bk = smem_u32(sK + s * FQ_KT), bv = smem_u32(sV + s * FQ_KT);
-        const uint32_t tS = tmem_base + (j & 1) * 128, tDP = tS + 64;
+        const uint32_t tS = tmem_base + (j % 3) * 128, tDP = tS + 64;
 #pragma unroll
         for (int k = 0; k < FA_D / 16; ++k) {  // S = Q K^T, dP = dO V^T  (K = d)
           const uint32_t offa = (k >> 2) * FA_ATOM + (k & 3) * 32;
@@ -720,12 +730,15 @@ __global__ void __launch_bounds__(256, 1)
           tc_mma_f16(tDP, make_sdesc(ado + offa, 16, 1024), make_sdesc(bv + offb, 16, 1024),
                      idesc_s, k != 0 ? 1u : 0u);
         }
-        tc_commit(&sdp_full[j & 1]);
+        tc_commit(&sdp_full[j % 3]);
       };
       issue_sdp(0);
+      if (n_kt > 1) issue_sdp(1);
       for (int j = 0; j < n_kt; ++j) {
-        if (j + 1 < n_kt) issue_sdp(j + 1);
-        mbar_wait(ds_full, j & 1);
+        // buffer (j + 2) % 3 held S/dP of step j - 1, whose dS the softmax has
+        // published (ds_full(j - 1) waited in the previous iteration)
+        if (j + 2 < n_kt) issue_sdp(j + 2);
+        mbar_wait(&ds_full[j & 1], (j >> 1) & 1);
         tc_fence_after();
         const int s = j % FQ_STAGES;
         const uint32_t bk = smem_u32(sK + s * FQ_KT), ads = smem_u32(sDS + (j & 1) * FQ_DS);
@@ -734,6 +747,7 @@ __global__ void __launch_bounds__(256, 1)
           tc_mma_f16(tDQ, make_sdesc(ads + k * 32, 16, 1024),
                      make_sdesc(bk + k * 2048, FQ_KT / 2, 1024), idesc_dq, (j | k) != 0 ? 1u : 0u);
         tc_commit(&kv_empty[s]);
+        tc_commit(&ds_free[j & 1]);
       }
       tc_commit(acc_done);
     }
@@ -746,10 +760,11 @@ __global__ void __launch_bounds__(256, 1)
     const float Lr = ok ? lse2[(long long)(q_row0 + r) * Hq + hq] : 0.f;
     const float Dr = ok ? Dv[(long long)(q_row0 + r) * Hq + hq] : 0.f;
     for (int j = 0; j < n_kt; ++j) {
-      mbar_wait(&sdp_full[j & 1], (j >> 1) & 1);
+      mbar_wait(&sdp_full[j % 3], (j / 3) & 1);
       tc_fence_after();
-      const uint32_t tS = tmem_base + (j & 1) * 128 + lane_off, tDP = tS + 64;
+      const uint32_t tS = tmem_base + (j % 3) * 128 + lane_off, tDP = tS + 64;
       const uint32_t ds_row = smem_u32(sDS) + (j & 1) * FQ_DS + r * 128;
+      if (j >= 2) mbar_wait(&ds_free[j & 1], ((j - 2) >> 1) & 1);  // dQ(j-2) has read it
 #pragma unroll 1
       for (int c = 0; c < FQ_BK / 32; ++c) {
         uint32_t vs[32], vp[32];
@@ -778,7 +793,7 @@ __global__ void __launch_bounds__(256, 1)
       }
       fence_proxy_async_smem();
       tc_fence_before();
-      mbar_arrive(ds_full);
+      mbar_arrive(&ds_full[j & 1]);
     }
     mbar_wait(acc_done, 0);
     tc_fence_after();
