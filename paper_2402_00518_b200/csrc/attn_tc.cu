@@ -357,9 +357,10 @@ __device__ __forceinline__ void rope_t_32(float* a, float* b, int c0, float pos,
 // Row r of a [rows x 128] fp32 TMEM accumulator -> scale, optional RoPE^T at
 // `pos`, bf16, 256 bytes at dst.
 __device__ __forceinline__ void store_row_bf16(uint32_t tacc, __nv_bfloat16* dst, bool ok,
-                                               float scale, float pos, float theta) {
+                                               float scale, float pos, float theta, int c0 = 0,
+                                               int c1 = 2) {
 #pragma unroll 1
-  for (int c = 0; c < 2; ++c) {
+  for (int c = c0; c < c1; ++c) {
     uint32_t va[32], vb[32];
     tmem_ld_32x32b_x32(tacc + c * 32, va);
     tmem_ld_wait();
@@ -403,7 +404,7 @@ __device__ __forceinline__ void store_row_bf16(uint32_t tacc, __nv_bfloat16* dst
 //   warp 0 TMA (K, V once; Q_i, dO_i double-buffered), warp 1 MMA,
 //   warps 4..7 one thread per key row (TMEM lane).
 // TMEM: S^T [128 x 64] | dP^T [128 x 64] | dK [128 x 128] | dV [128 x 128].
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
                             const __grid_constant__ CUtensorMap tmK,
                             const __grid_constant__ CUtensorMap tmV,
@@ -453,8 +454,8 @@ __global__ void __launch_bounds__(256, 1)
     }
     mbar_init(&sdp_full[0], 1);
     mbar_init(&sdp_full[1], 1);
-    mbar_init(&pds_full[0], 128);
-    mbar_init(&pds_full[1], 128);
+    mbar_init(&pds_full[0], 256);
+    mbar_init(&pds_full[1], 256);
     mbar_init(acc_done, 1);
     fence_barrier_init();
   }
@@ -538,7 +539,9 @@ __global__ void __launch_bounds__(256, 1)
       tc_commit(acc_done);
     }
   } else if (warp >= 4) {
-    const int ew = warp - 4;
+    // two softmax warpgroups: warps w and w + 4 share TMEM lanes 32 (w % 4) ..
+    // and take query columns [0, 32) and [32, 64) of every step
+    const int ew = (warp - 4) & 3, half = (warp - 4) >> 2;
     const int kr = ew * 32 + lane;  // key row = TMEM lane
     const int kpos = kt * FA_BN + kr;
     const uint32_t lane_off = static_cast<uint32_t>(ew * 32) << 16;
@@ -553,7 +556,7 @@ __global__ void __launch_bounds__(256, 1)
       const long long idx = (long long)(b * T + qpos0 + t) * Hq + hq;
       return tid < FB_BQ ? lse2[idx] : Dv[idx];
     };
-    float stat_next = n_it > 0 ? stat_of(0) : 0.f;
+    float stat_next = (n_it > 0 && tid < 2 * FB_BQ) ? stat_of(0) : 0.f;
     for (int it = 0; it < n_it; ++it) {
       // P^T / dS^T go to smem buffer it & 1: the dV/dK MMAs of step it-2 that
       // read it were issued before S^T(it), so sdp_full[it & 1] covers them
@@ -563,13 +566,15 @@ __global__ void __launch_bounds__(256, 1)
       const int qpos0 = (q64_0 + it % per_head) * FB_BQ;
       float* L = sL + (it & 1) * FB_BQ;
       float* D = sD + (it & 1) * FB_BQ;
-      (tid < FB_BQ ? L : D)[tid & (FB_BQ - 1)] = stat_next;
-      if (it + 1 < n_it) stat_next = stat_of(it + 1);
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (tid < 2 * FB_BQ) {
+        (tid < FB_BQ ? L : D)[tid & (FB_BQ - 1)] = stat_next;
+        if (it + 1 < n_it) stat_next = stat_of(it + 1);
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
       mbar_wait(&sdp_full[it & 1], (it >> 1) & 1);
       tc_fence_after();
-#pragma unroll 1
-      for (int c = 0; c < FB_BQ / 32; ++c) {
+      {
+        const int c = half;
         uint32_t vs[32], vp[32];
         tmem_ld_32x32b_x32(tS + lane_off + c * 32, vs);
         tmem_ld_32x32b_x32(tDP + lane_off + c * 32, vp);
@@ -606,10 +611,12 @@ __global__ void __launch_bounds__(256, 1)
     tc_fence_after();
     const bool ok = kpos < T;
     const long long ldk = (long long)Hkv * FA_D;
-    store_row_bf16(tDK + lane_off, dk + (long long)(k_row0 + kr) * ldk + hk * FA_D, ok, scale,
-                   (float)kpos, rope_theta);
-    store_row_bf16(tDV + lane_off, dv + (long long)(k_row0 + kr) * ldk + hk * FA_D, ok, 1.0f,
-                   0.f, 0.f);
+    if (half == 0)
+      store_row_bf16(tDK + lane_off, dk + (long long)(k_row0 + kr) * ldk + hk * FA_D, ok, scale,
+                     (float)kpos, rope_theta);
+    else
+      store_row_bf16(tDV + lane_off, dv + (long long)(k_row0 + kr) * ldk + hk * FA_D, ok, 1.0f,
+                     0.f, 0.f);
   }
   tc_fence_before();
   __syncthreads();
@@ -624,7 +631,7 @@ __global__ void __launch_bounds__(256, 1)
 // [S | dP] buffers of 128 columns (S/dP of steps j+1 and j+2 are queued on
 // the tensor core while the softmax threads form dS_j) and dQ (128 columns).
 // dS in smem is double-buffered.
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
                           const __grid_constant__ CUtensorMap tmK,
                           const __grid_constant__ CUtensorMap tmV,
@@ -674,7 +681,7 @@ __global__ void __launch_bounds__(256, 1)
     for (int bb = 0; bb < 3; ++bb) mbar_init(&sdp_full[bb], 1);
     for (int bb = 0; bb < 2; ++bb) {
       mbar_init(&ds_free[bb], 1);
-      mbar_init(&ds_full[bb], 128);
+      mbar_init(&ds_full[bb], 256);
     }
     mbar_init(acc_done, 1);
     fence_barrier_init();
@@ -752,7 +759,8 @@ __global__ void __launch_bounds__(256, 1)
       tc_commit(acc_done);
     }
   } else if (warp >= 4) {
-    const int ew = warp - 4;
+    // two softmax warpgroups: key columns [0, 32) and [32, 64) of every step
+    const int ew = (warp - 4) & 3, half = (warp - 4) >> 2;
     const int r = ew * 32 + lane;
     const int pos = qt * FA_BM + r;
     const uint32_t lane_off = static_cast<uint32_t>(ew * 32) << 16;
@@ -765,8 +773,8 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t tS = tmem_base + (j % 3) * 128 + lane_off, tDP = tS + 64;
       const uint32_t ds_row = smem_u32(sDS) + (j & 1) * FQ_DS + r * 128;
       if (j >= 2) mbar_wait(&ds_free[j & 1], ((j - 2) >> 1) & 1);  // dQ(j-2) has read it
-#pragma unroll 1
-      for (int c = 0; c < FQ_BK / 32; ++c) {
+      {
+        const int c = half;
         uint32_t vs[32], vp[32];
         tmem_ld_32x32b_x32(tS + c * 32, vs);
         tmem_ld_32x32b_x32(tDP + c * 32, vp);
@@ -798,7 +806,7 @@ __global__ void __launch_bounds__(256, 1)
     mbar_wait(acc_done, 0);
     tc_fence_after();
     store_row_bf16(tDQ + lane_off, dq + (long long)(q_row0 + r) * Hq * FA_D + hq * FA_D, ok, scale,
-                   (float)pos, rope_theta);
+                   (float)pos, rope_theta, half, half + 1);
   }
   tc_fence_before();
   __syncthreads();
@@ -838,12 +846,12 @@ cudaError_t launch_attn_bwd_tc(const __nv_bfloat16* q, const __nv_bfloat16* k,
   const float scale_log2 = 1.4426950408889634f * scale;
   const unsigned B = (unsigned)(N / T);
   dim3 g1((T + FA_BN - 1) / FA_BN, Hkv, B);
-  attn_bwd_dkdv_tc_kernel<<<g1, 256, FB_SMEM_KV, s>>>(tq64, tk, tv, tdo64, lse2, Dv, dk, dv, T, Hq,
+  attn_bwd_dkdv_tc_kernel<<<g1, 384, FB_SMEM_KV, s>>>(tq64, tk, tv, tdo64, lse2, Dv, dk, dv, T, Hq,
                                                       Hkv, scale_log2, scale, rope_theta);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   dim3 g2((T + FA_BM - 1) / FA_BM, Hq, B);
-  attn_bwd_dq_tc_kernel<<<g2, 256, FB_SMEM_Q, s>>>(tq128, tk64, tv64, tdo128, lse2, Dv, dq, T, Hq,
+  attn_bwd_dq_tc_kernel<<<g2, 384, FB_SMEM_Q, s>>>(tq128, tk64, tv64, tdo128, lse2, Dv, dq, T, Hq,
                                                    Hkv, scale_log2, scale, rope_theta);
   return cudaGetLastError();
 }
