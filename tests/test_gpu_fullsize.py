@@ -113,3 +113,60 @@ def test_full_size_embedding_uniform_logits_closed_form(gpu_lib):
     got = grads[0]["w_out"].double().cpu().numpy()
     rel = np.linalg.norm(got - expect) / np.linalg.norm(expect)
     assert rel <= 2e-2, rel
+
+
+def test_full_size_layer_exit_one_sequence_vs_oracle(gpu_lib):
+    """13b_layer (Llama-2 13B Layer exit: 40 heads, F 13824, V 32000) at the
+    bench's full 16 x 2048 tokens, one exit = the launches bench.py repeats
+    per exit.  The oracle runs the exit forward on one whole sequence (the
+    last, 2048 tokens: attention couples a sequence's rows) and every row of it
+    is compared (lse, loss_t, confidence, argmax under A9); loss = mean of the
+    per-token losses; P4 on dW_out; finite gradients; bitwise determinism."""
+    from harness import attn_kwargs
+    ee = gpu_lib
+    cfg = _one_exit("13b_layer")
+    n, T = cfg.tokens, cfg.seq_len
+    hidden = [h.contiguous() for h in S.hidden_states(cfg, n, device="cuda")]
+    targets = S.targets(cfg, n, device="cuda")
+    params = S.head_params(cfg, device="cuda")
+    c = ee.make_config(cfg.hidden, cfg.vocab, cfg.ffn, 1, "layer", **attn_kwargs(cfg))
+    ops = [{k: (v.float().contiguous() if k.startswith("g_") else v.to(torch.bfloat16).contiguous())
+            for k, v in params[0].items()}]
+
+    def run():
+        grads = [{k: torch.empty(v.shape, device="cuda") for k, v in params[0].items()}]
+        ax = [{"lse": torch.zeros(n, device="cuda"), "loss_tok": torch.zeros(n, device="cuda"),
+               "argmax": torch.zeros(n, dtype=torch.int32, device="cuda"),
+               "conf": torch.zeros(n, device="cuda")}]
+        ws = torch.zeros(ee.ee_workspace_size(c, n), dtype=torch.uint8, device="cuda")
+        loss = torch.zeros(1, device="cuda")
+        ee.ee_tune_step(c, hidden, targets, [1.0], ops, grads, loss, ws, aux=ax)
+        torch.cuda.synchronize()
+        return loss, grads, ax, ee.ee_get_status(ws)
+
+    loss, grads, aux, st = run()
+    assert st == (0, -1)
+    seq = slice(n - T, n)
+    p64 = {k: to_f64(v) for k, v in ops[0].items()}
+    act = O.exit_forward("layer", p64, to_f64(hidden[0][seq]), 1e-5, S.attn_geometry(cfg))
+    tg = targets.cpu().numpy()
+    st_o = O.lm_loss_stats(act["S"], tg[seq])
+    lse = aux[0]["lse"].cpu().numpy()[seq]
+    assert np.max(np.abs(lse - st_o["lse"])) <= 5e-2
+    assert np.max(np.abs(aux[0]["conf"].cpu().numpy()[seq] - st_o["conf"])) <= 2e-2
+    lt = aux[0]["loss_tok"].cpu().numpy()[seq]
+    assert np.max(np.abs(lt - st_o["loss"])) <= 5e-2
+    assert abs(lt.mean() - st_o["loss"].mean()) <= 1e-3 * st_o["loss"].mean()
+    check_argmax(aux[0]["argmax"].cpu().numpy()[seq], act["S"])
+    valid = tg != -1
+    lt_all = aux[0]["loss_tok"].double().cpu().numpy()
+    assert abs(loss.item() - lt_all[valid].mean()) <= 1e-5 * abs(loss.item())
+    dw = grads[0]["w_out"].double()
+    assert dw.sum(dim=0).norm().item() <= 1e-2 * dw.abs().sum(dim=0).norm().item()
+    for k, g in grads[0].items():
+        assert torch.isfinite(g).all(), k
+        assert g.abs().sum().item() > 0, k
+    loss2, grads2, _, _ = run()
+    assert torch.equal(loss, loss2)
+    for k in grads[0]:
+        assert torch.equal(grads[0][k], grads2[0][k]), k
