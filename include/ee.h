@@ -275,7 +275,12 @@ ee_status ee_vp_exit_backward(const ee_head_config* cfg, const void* hidden, int
  * probability; first_exit[t] (may be NULL) = the lowest exit index whose
  * confidence reaches `threshold`, or -1 (threshold 1 disables early exits,
  * P:385).  hidden[i]: device bf16 [n_tokens x h]; outputs device [n_tokens].
- * Same kernels as the tuning step's forward (a1-a6); no loss, no gradients. */
+ * n_tokens > 16 (or Layer exits): the tuning step's forward kernels (a1-a6).
+ * n_tokens <= 16 (decode): weight-streaming "skinny" kernels (warp-level bf16
+ * MMA over 128-bit streaming loads, fused SwiGLU / residual / per-block
+ * online-softmax statistics) and a wide finalize; same results up to fp32
+ * summation order.  No loss, no gradients.  Env EE_INFER_SKINNY=0 forces the
+ * GEMM path. */
 ee_status ee_exit_infer(const ee_head_config* cfg, const void* const* hidden, int64_t n_tokens,
                         const ee_head_tensors* params, float threshold, int32_t* const* argmax_out,
                         float* const* conf_out, int32_t* first_exit, void* workspace,

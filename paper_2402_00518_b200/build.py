@@ -8,7 +8,7 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = [os.path.join(HERE, "csrc", f) for f in ("api.cu", "gemm.cu", "kernels.cu", "backbone.cu",
-                                                   "attn_tc.cu")]
+                                                   "attn_tc.cu", "skinny.cu")]
 HDR = [os.path.join(HERE, "csrc", f) for f in ("ptx.cuh", "gemm.cuh", "internal.cuh")] + [
     os.path.join(HERE, "..", "include", "ee.h")]
 OUT = os.path.join(HERE, "libee_b200.so")

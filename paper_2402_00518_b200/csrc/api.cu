@@ -1018,6 +1018,50 @@ ee_status ee_backbone_forward(const ee_backbone_config* cfg, const ee_layer_tens
 }
 
 // ---------------------------------------------------------------- early-exit inference
+// Decode shapes (n <= SKINNY_MAX_M tokens): the exit head streams its weights
+// through the skinny kernels (skinny.cu); the CE partials of the 32-column
+// vocab blocks go to the dS region of the workspace (unused at inference).
+static ee_status infer_decode_exit(const ee_head_config* cfg, const Bufs& B,
+                                   const ee_head_tensors& P, const __nv_bfloat16* x, long long n,
+                                   float* pm, float* ps, int32_t* pi, cudaStream_t st) {
+  const int h = cfg->hidden, F = cfg->ffn, Vl = cfg->vocab_end - cfg->vocab_begin;
+  const int M = (int)n;
+  const __nv_bfloat16* z = x;
+  if (cfg->arch != EE_ARCH_EMBEDDING) {
+    const void* yin = x;
+    bool yf32 = false;
+    if (cfg->arch == EE_ARCH_MLP) {
+      { Prof p_("dec_rmsnorm_a", st, 0, 0, 4.0 * n * h + 4.0 * h);
+      EE_CUDA(launch_rmsnorm_fwd(x, false, (const float*)P.g_a, cfg->norm_eps, B.u, B.rx, n, h, st)); }
+      {
+        SkinnyArgs a{};
+        a.x = B.u; a.ldx = h; a.W0 = (const __nv_bfloat16*)P.w_gate;
+        a.W1 = (const __nv_bfloat16*)P.w_up; a.K = h; a.N = F; a.outb = B.mact; a.ldo = F;
+        Prof p_("dec_gateup_swiglu", st, 4.0 * n * F * h, 4.0 * n * F * h, 4.0 * F * h);
+        EE_CUDA(launch_skinny(SK_SWIGLU, a, M, st));
+      }
+      {
+        SkinnyArgs a{};
+        a.x = B.mact; a.ldx = F; a.W0 = (const __nv_bfloat16*)P.w_down; a.K = F; a.N = h;
+        a.out = B.y; a.ldo = h; a.resid = x; a.ldr = h;
+        Prof p_("dec_down_resid", st, 2.0 * n * F * h, 2.0 * n * F * h, 2.0 * F * h);
+        EE_CUDA(launch_skinny(SK_RESID, a, M, st));
+      }
+      yin = B.y;
+      yf32 = true;
+    }
+    { Prof p_("dec_rmsnorm_f", st, 0, 0, 4.0 * n * h + 4.0 * h);
+    EE_CUDA(launch_rmsnorm_fwd(yin, yf32, (const float*)P.g_f, cfg->norm_eps, B.z, B.ry, n, h, st)); }
+    z = B.z;
+  }
+  SkinnyArgs a{};
+  a.x = z; a.ldx = h; a.W0 = (const __nv_bfloat16*)P.w_out; a.K = h; a.N = Vl;
+  a.pm = pm; a.ps = ps; a.pi = pi; a.vocab_begin = cfg->vocab_begin;
+  Prof p_("dec_vocab_ce", st, 2.0 * n * Vl * h, 2.0 * n * Vl * h, 2.0 * Vl * h);
+  EE_CUDA(launch_skinny(SK_CE, a, M, st));
+  return EE_OK;
+}
+
 // Confidence-based exit decision: per exit, the greedy token and
 // the max softmax probability; first_exit[t] = lowest exit with c >= tau.
 ee_status ee_exit_infer(const ee_head_config* cfg, const void* const* hidden, int64_t n_tokens,
@@ -1049,8 +1093,24 @@ ee_status ee_exit_infer(const ee_head_config* cfg, const void* const* hidden, in
   int32_t* no_targets = (int32_t*)B.tgt;  // tgt (fp32 [n]) is free: no target logits needed
   EE_CUDA(cudaMemsetAsync(no_targets, 0xFF, sizeof(int32_t) * n, st));
   EE_CUDA(cudaMemsetAsync(B.vcount, 0, sizeof(long long), st));
+  static const int skinny_env = [] {
+    const char* e = getenv("EE_INFER_SKINNY");
+    return e ? atoi(e) : 1;
+  }();
+  const bool decode = skinny_env && n <= SKINNY_MAX_M && cfg->arch != EE_ARCH_LAYER;
   for (int i = 0; i < E; ++i) {
     const __nv_bfloat16* x = (const __nv_bfloat16*)hidden[i];
+    if (decode) {
+      const int nbd = skinny_blocks(cfg->vocab_end - cfg->vocab_begin);
+      float* pm = (float*)B.ds;
+      float* ps = pm + (size_t)nbd * n;
+      int32_t* pi = (int32_t*)(ps + (size_t)nbd * n);
+      if ((s = infer_decode_exit(cfg, B, params[i], x, n, pm, ps, pi, st)) != EE_OK) return s;
+      Prof p_("infer_finalize", st, 0, 0, 12.0 * nbd * n + 8.0 * n);
+      EE_CUDA(launch_infer_finalize_wide(pm, ps, pi, nbd, (int)n, B.lse, argmax_out[i],
+                                         conf_out[i], st));
+      continue;
+    }
     const __nv_bfloat16* z = nullptr;
     if ((s = phase_exit_forward(cfg, B, params[i], x, n, nullptr, &z, st)) != EE_OK) return s;
     if ((s = phase_vocab_stats(cfg, B, params[i], z, n, no_targets, st)) != EE_OK) return s;

@@ -92,6 +92,29 @@ cudaError_t launch_first_exit(const float* const* conf, int E, long long n, floa
 cudaError_t launch_attn_fwd(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                             __nv_bfloat16* o, long long N, int T, int Hq, int Hkv, float* lse2,
                             cudaStream_t s);
+// Decode-shape exit heads (skinny.cu): M <= SKINNY_MAX_M tokens.
+constexpr int SKINNY_MAX_M = 16;
+enum SkinnyMode { SK_F32 = 0, SK_RESID = 1, SK_SWIGLU = 2, SK_CE = 3 };
+struct SkinnyArgs {
+  const __nv_bfloat16* x;  // [M x K], row stride ldx
+  long long ldx;
+  const __nv_bfloat16* W0;  // [N x K] row-major (SWIGLU: gate)
+  const __nv_bfloat16* W1;  // SWIGLU: up
+  int K, N;
+  float* out;               // F32 / RESID: [M x ldo] fp32
+  __nv_bfloat16* outb;      // SWIGLU: [M x ldo] bf16 = silu(x W0^T) * (x W1^T)
+  long long ldo;
+  const __nv_bfloat16* resid;  // RESID: [M x ldr] bf16
+  long long ldr;
+  float *pm, *ps;           // CE: [blocks x M] partial max / sum-exp
+  int32_t* pi;              //     partial argmax (global vocab index)
+  int vocab_begin;
+};
+cudaError_t launch_skinny(int mode, const SkinnyArgs& a, int M, cudaStream_t s);
+int skinny_blocks(int N);
+cudaError_t launch_infer_finalize_wide(const float* pm, const float* ps, const int32_t* pi, int nb,
+                                       int M, float* lse, int32_t* argmax, float* conf,
+                                       cudaStream_t s);
 // tcgen05 flash-attention forward (attn_tc.cu): same contract as launch_attn_fwd,
 // seq_len a multiple of 64, lse2 required.
 cudaError_t launch_attn_fwd_tc(const __nv_bfloat16* q, const __nv_bfloat16* k,

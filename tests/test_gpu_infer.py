@@ -14,7 +14,11 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("arch,h,V,F,n", [("mlp", 256, 4104, 512, 300), ("norm", 128, 1000, 0, 8),
-                                          ("embedding", 192, 2056, 0, 77)])
+                                          ("embedding", 192, 2056, 0, 77),
+                                          # decode shapes (n <= 16): the skinny weight-streaming path
+                                          ("mlp", 256, 4104, 512, 1), ("mlp", 384, 1000, 640, 8),
+                                          ("mlp", 256, 2056, 384, 13), ("norm", 128, 1000, 0, 16),
+                                          ("embedding", 192, 2056, 0, 3), ("norm", 128, 1000, 0, 5)])
 def test_exit_infer_matches_oracle(gpu_lib, arch, h, V, F, n):
     ee = gpu_lib
     cfg = S.Cfg(name="small", hidden=h, vocab=V, ffn=F, arch=arch, tokens=n, layers=3,
