@@ -201,3 +201,58 @@ def vocab_parallel_step(phases, comm, arch: str, hidden_local, targets_all, para
     for h in handles:
         if h is not None:
             h.wait()
+
+
+# ---------------------------------------------------------------------------
+# Forward-communication-only pipeline schedule (Fig. 3; NEXT #3)
+# ---------------------------------------------------------------------------
+
+def pipeline_forward_only_step(stage: int, n_stages: int, n_micro: int,
+                               run_stage_forward: Callable[[int, torch.Tensor | None], torch.Tensor],
+                               run_stage_exits: Callable[[int], None],
+                               send: Callable[[int, torch.Tensor], object] | None,
+                               recv: Callable[[int], torch.Tensor] | None,
+                               optimizer_step: Callable[[], None] | None = None) -> None:
+    """One EE-Tuning iteration of the paper's customised pipeline schedule
+    "with forward communication only": the backbone is split into
+    n_stages consecutive layer ranges; for each microbatch m, stage s receives
+    the activation from stage s-1 (stage 0 reads its input), runs its backbone
+    layers forward (run_stage_forward -> the activation for stage s+1; it also
+    keeps the hidden states at this stage's exits), sends it on, and then --
+    "as soon as the forward pass of the Transformer backbone within that stage
+    is completed" -- runs forward, loss and backward of its own exits
+    (run_stage_exits, gradients accumulated over microbatches).  No backbone
+    activations are kept and nothing is sent backward.  optimizer_step()
+    updates this stage's exits after the last microbatch.
+
+    send(m, t) may return a handle with .wait() (isend); recv(m) returns the
+    received activation.  Sends are waited for at the end of the iteration so
+    stage s's exit work overlaps the transfer to stage s+1."""
+    pending = []
+    for m in range(n_micro):
+        x_in = recv(m) if stage > 0 else None
+        x_out = run_stage_forward(m, x_in)
+        if stage + 1 < n_stages:
+            pending.append(send(m, x_out))
+        run_stage_exits(m)
+    for h in pending:
+        if h is not None and hasattr(h, "wait"):
+            h.wait()
+    if optimizer_step is not None:
+        optimizer_step()
+
+
+class TorchP2P:
+    """Point-to-point transport of the forward-only pipeline over a
+    torch.distributed group (NCCL on GPUs, gloo in the CPU tests)."""
+
+    def __init__(self, stage: int, shape, dtype, device, group=None):
+        self.stage, self.shape, self.dtype, self.device, self.group = stage, shape, dtype, device, group
+
+    def send(self, m: int, t: torch.Tensor):
+        return dist.isend(t.contiguous(), dst=self.stage + 1, group=self.group)
+
+    def recv(self, m: int) -> torch.Tensor:
+        buf = torch.empty(self.shape, dtype=self.dtype, device=self.device)
+        dist.recv(buf, src=self.stage - 1, group=self.group)
+        return buf
