@@ -35,6 +35,9 @@ constexpr int FA_KST = 2;                         // K ring stages
 constexpr int FA_VST = 3;                         // V ring stages
 constexpr int FA_SMEM = 1024 + FA_TILE * (2 + FA_KST + FA_VST) + 256;
 constexpr float FA_RESCALE = 8.0f;                // log2 headroom before O is rescaled
+#ifndef EE_FA_P_TMEM
+#define EE_FA_P_TMEM 1                            // P as a TMEM A operand (else swizzled smem)
+#endif
 }  // namespace
 
 __global__ void __launch_bounds__(256, 1)
@@ -155,10 +158,15 @@ __global__ void __launch_bounds__(256, 1)
         tc_fence_after();
         const uint32_t bv = smem_u32(sV + sv * FA_TILE);
 #pragma unroll
-        for (int k = 0; k < FA_BN / 16; ++k) {  // A = P (K-major), B = V (MN-major: keys x d)
+        for (int k = 0; k < FA_BN / 16; ++k) {  // A = P, B = V (MN-major: keys x d)
+#if EE_FA_P_TMEM
+          tc_mma_f16_ts(tO, tS0 + (j & 1) * FA_BN + k * 8, make_sdesc(bv + k * 2048, FA_ATOM, 1024),
+                        idesc_pv, (j | k) != 0 ? 1u : 0u);
+#else
           const uint32_t offa = (k >> 2) * FA_ATOM + (k & 3) * 32;
           tc_mma_f16(tO, make_sdesc(ap + offa, 16, 1024), make_sdesc(bv + k * 2048, FA_ATOM, 1024),
                      idesc_pv, (j | k) != 0 ? 1u : 0u);
+#endif
         }
         tc_commit(o_done);
         tc_commit(&v_empty[sv]);
@@ -246,6 +254,13 @@ __global__ void __launch_bounds__(256, 1)
         }
         tmem_st_wait();
       }
+#if EE_FA_P_TMEM
+      // P -> TMEM over the first 64 columns of S_j's own buffer (S_j is in
+      // registers now; S_{j+2} reuses the buffer only after PV_j, in issue order)
+      tmem_st_32x32b_x32(ts, *reinterpret_cast<const uint32_t(*)[32]>(pk));
+      tmem_st_32x32b_x32(ts + 32, *reinterpret_cast<const uint32_t(*)[32]>(pk + 32));
+      tmem_st_wait();
+#else
       // P -> smem, K-major SWIZZLE_128B: 16-byte chunk cc of row r sits at
       // chunk (cc ^ (r & 7)) of the row's 128-byte line
 #pragma unroll
@@ -255,6 +270,7 @@ __global__ void __launch_bounds__(256, 1)
                      pk[4 * c8 + 1], pk[4 * c8 + 2], pk[4 * c8 + 3]);
       }
       fence_proxy_async_smem();
+#endif
       tc_fence_before();
       mbar_arrive(p_full);
     }
@@ -331,14 +347,11 @@ cudaError_t launch_attn_fwd_tc(const __nv_bfloat16* q, const __nv_bfloat16* k,
 namespace {
 constexpr int FB_BQ = 64;                       // queries per step of the dK/dV kernel
 constexpr int FB_QT = FB_BQ * FA_D * 2;         // 16 KB: two 8 KB SW128 atoms
-constexpr int FB_PT = FA_BN * FB_BQ * 2;       // one [128 x 64] bf16 operand (16 KB)
-constexpr int FB_SMEM_KV = 1024 + 2 * FA_TILE + 2 * 2 * FB_QT + 2 * 2 * FB_PT +
-                           2 * 2 * FB_BQ * 4 + 256;
+constexpr int FB_SMEM_KV = 1024 + 2 * FA_TILE + 2 * 2 * FB_QT + 2 * 2 * FB_BQ * 4 + 256;
 constexpr int FQ_BK = 64;                       // keys per step of the dQ kernel
 constexpr int FQ_KT = FQ_BK * FA_D * 2;         // 16 KB K or V tile
 constexpr int FQ_STAGES = 4;
-constexpr int FQ_DS = FA_BM * FQ_BK * 2;        // 16 KB dS tile
-constexpr int FB_SMEM_Q = 1024 + 2 * FA_TILE + FQ_STAGES * 2 * FQ_KT + 2 * FQ_DS + 256;
+constexpr int FB_SMEM_Q = 1024 + 2 * FA_TILE + FQ_STAGES * 2 * FQ_KT + 256;
 
 // RoPE^T (rotation by -angle) of 32 columns [c0, c0 + 32) (c0 < 64) paired
 // with [c0 + 64, c0 + 96) of one row at position pos.
@@ -420,9 +433,7 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sV = sK + FA_TILE;
   uint8_t* sQ = sV + FA_TILE;          // [2] x 16 KB
   uint8_t* sDO = sQ + 2 * FB_QT;       // [2] x 16 KB
-  uint8_t* sPt = sDO + 2 * FB_QT;      // [2] x [128 keys x 64 q] bf16 (one 16 KB atom each)
-  uint8_t* sDSt = sPt + 2 * FB_PT;     // [2]
-  float* sL = reinterpret_cast<float*>(sDSt + 2 * FB_PT);  // [2][64]
+  float* sL = reinterpret_cast<float*>(sDO + 2 * FB_QT);  // [2][64]
   float* sD = sL + 2 * FB_BQ;                              // [2][64]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 2 * FB_BQ);
   uint64_t* kv_full = bars;
@@ -524,15 +535,16 @@ __global__ void __launch_bounds__(384, 1)
         mbar_wait(&pds_full[s], (it >> 1) & 1);
         tc_fence_after();
         const uint32_t bq = smem_u32(sQ + s * FB_QT), bd = smem_u32(sDO + s * FB_QT);
-        const uint32_t apt = smem_u32(sPt + s * FB_PT), ads = smem_u32(sDSt + s * FB_PT);
+        const uint32_t tPt = tmem_base + s * 128, tDSt = tPt + 64;
 #pragma unroll
-        for (int k = 0; k < FB_BQ / 16; ++k) {  // dV += P^T dO, dK += dS^T Q (B MN-major, K = q)
-          const uint32_t offa = k * 32;
+        for (int k = 0; k < FB_BQ / 16; ++k) {  // dV += P^T dO, dK += dS^T Q (A in TMEM, K = q)
+          // queries 16k.. sit at column 32*(k/2) + 8*(k%2) (each warpgroup's slab)
+          const uint32_t offa = (k >> 1) * 32 + (k & 1) * 8;
           const uint32_t offb = k * 2048;
-          tc_mma_f16(tDV, make_sdesc(apt + offa, 16, 1024), make_sdesc(bd + offb, FB_QT / 2, 1024),
-                     idesc_acc, (it | k) != 0 ? 1u : 0u);
-          tc_mma_f16(tDK, make_sdesc(ads + offa, 16, 1024), make_sdesc(bq + offb, FB_QT / 2, 1024),
-                     idesc_acc, (it | k) != 0 ? 1u : 0u);
+          tc_mma_f16_ts(tDV, tPt + offa, make_sdesc(bd + offb, FB_QT / 2, 1024), idesc_acc,
+                        (it | k) != 0 ? 1u : 0u);
+          tc_mma_f16_ts(tDK, tDSt + offa, make_sdesc(bq + offb, FB_QT / 2, 1024), idesc_acc,
+                        (it | k) != 0 ? 1u : 0u);
         }
         tc_commit(&qd_empty[s]);
       }
@@ -558,10 +570,8 @@ __global__ void __launch_bounds__(384, 1)
     };
     float stat_next = (n_it > 0 && tid < 2 * FB_BQ) ? stat_of(0) : 0.f;
     for (int it = 0; it < n_it; ++it) {
-      // P^T / dS^T go to smem buffer it & 1: the dV/dK MMAs of step it-2 that
-      // read it were issued before S^T(it), so sdp_full[it & 1] covers them
-      const uint32_t pt_row = smem_u32(sPt) + (it & 1) * FB_PT + kr * 128;
-      const uint32_t ds_row = smem_u32(sDSt) + (it & 1) * FB_PT + kr * 128;
+      // P^T / dS^T overwrite S^T / dP^T of buffer it & 1 once read; S^T(it+2)
+      // reuses the buffer only after dV/dK(it) (tensor-pipe issue order)
       const uint32_t tS = tmem_base + (it & 1) * 128, tDP = tS + 64;
       const int qpos0 = (q64_0 + it % per_head) * FB_BQ;
       float* L = sL + (it & 1) * FB_BQ;
@@ -595,15 +605,13 @@ __global__ void __launch_bounds__(384, 1)
           wp[q] = pack_bf16(p2[0], p2[1]);
           wd[q] = pack_bf16(d2[0], d2[1]);
         }
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {  // 4 x 16-byte chunks of this 32-column slab
-          const int cc = c * 4 + h;
-          const int off = (cc ^ (kr & 7)) << 4;
-          st_shared_v4(pt_row + off, wp[4 * h], wp[4 * h + 1], wp[4 * h + 2], wp[4 * h + 3]);
-          st_shared_v4(ds_row + off, wd[4 * h], wd[4 * h + 1], wd[4 * h + 2], wd[4 * h + 3]);
-        }
+        // P^T and dS^T as TMEM A operands: this warpgroup's 32 query columns,
+        // packed bf16x2, over the first 16 columns of its own fp32 slab of the
+        // S^T / dP^T buffers (already read into registers above)
+        tmem_st_32x32b_x16(tS + lane_off + c * 32, wp);
+        tmem_st_32x32b_x16(tDP + lane_off + c * 32, wd);
+        tmem_st_wait();
       }
-      fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(&pds_full[it & 1]);
     }
@@ -646,18 +654,17 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sDO = sQ + FA_TILE;
   uint8_t* sK = sDO + FA_TILE;                  // [STAGES] x 16 KB (64 keys x 128 d)
   uint8_t* sV = sK + FQ_STAGES * FQ_KT;         // [STAGES]
-  uint8_t* sDS = sV + FQ_STAGES * FQ_KT;        // [2] x [128 q x 64 keys] bf16, one atom each
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sDS + 2 * FQ_DS);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + FQ_STAGES * FQ_KT);
   uint64_t* qo_full = bars;
   uint64_t* kv_full = bars + 1;                 // [STAGES]
   uint64_t* kv_empty = kv_full + FQ_STAGES;     // [STAGES]
   uint64_t* sdp_full = kv_empty + FQ_STAGES;    // [3]
-  // ds_full[b] / ds_free[b] per dS buffer: one barrier per buffer so the
-  // softmax can never complete two phases of one barrier before the MMA
-  // thread observes the first (it runs up to two steps ahead of the MMA)
-  uint64_t* ds_full = sdp_full + 3;             // [2]
-  uint64_t* ds_free = ds_full + 2;              // [2]: dQ(j) done reading dS buffer j & 1
-  uint64_t* acc_done = ds_free + 2;
+  // ds_full[j % 3]: dS of step j written (into S buffer j % 3).  One barrier
+  // per buffer: step j + 3 needs S/dP(j + 3), issued only after the MMA
+  // thread has observed ds_full(j), so no barrier can run two phases ahead
+  // of its waiter
+  uint64_t* ds_full = sdp_full + 3;             // [3]
+  uint64_t* acc_done = ds_full + 3;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -679,10 +686,7 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(&kv_empty[s], 1);
     }
     for (int bb = 0; bb < 3; ++bb) mbar_init(&sdp_full[bb], 1);
-    for (int bb = 0; bb < 2; ++bb) {
-      mbar_init(&ds_free[bb], 1);
-      mbar_init(&ds_full[bb], 256);
-    }
+    for (int bb = 0; bb < 3; ++bb) mbar_init(&ds_full[bb], 256);
     mbar_init(acc_done, 1);
     fence_barrier_init();
   }
@@ -745,16 +749,16 @@ __global__ void __launch_bounds__(384, 1)
         // buffer (j + 2) % 3 held S/dP of step j - 1, whose dS the softmax has
         // published (ds_full(j - 1) waited in the previous iteration)
         if (j + 2 < n_kt) issue_sdp(j + 2);
-        mbar_wait(&ds_full[j & 1], (j >> 1) & 1);
+        mbar_wait(&ds_full[j % 3], (j / 3) & 1);
         tc_fence_after();
         const int s = j % FQ_STAGES;
-        const uint32_t bk = smem_u32(sK + s * FQ_KT), ads = smem_u32(sDS + (j & 1) * FQ_DS);
+        const uint32_t bk = smem_u32(sK + s * FQ_KT), tDS = tmem_base + (j % 3) * 128;
 #pragma unroll
-        for (int k = 0; k < FQ_BK / 16; ++k)  // dQ += dS K  (K MN-major: keys x d, LBO 8 KB)
-          tc_mma_f16(tDQ, make_sdesc(ads + k * 32, 16, 1024),
-                     make_sdesc(bk + k * 2048, FQ_KT / 2, 1024), idesc_dq, (j | k) != 0 ? 1u : 0u);
+        for (int k = 0; k < FQ_BK / 16; ++k)  // dQ += dS K  (dS in TMEM; K MN-major, LBO 8 KB)
+          tc_mma_f16_ts(tDQ, tDS + (k >> 1) * 32 + (k & 1) * 8,
+                        make_sdesc(bk + k * 2048, FQ_KT / 2, 1024), idesc_dq,
+                        (j | k) != 0 ? 1u : 0u);
         tc_commit(&kv_empty[s]);
-        tc_commit(&ds_free[j & 1]);
       }
       tc_commit(acc_done);
     }
@@ -771,8 +775,6 @@ __global__ void __launch_bounds__(384, 1)
       mbar_wait(&sdp_full[j % 3], (j / 3) & 1);
       tc_fence_after();
       const uint32_t tS = tmem_base + (j % 3) * 128 + lane_off, tDP = tS + 64;
-      const uint32_t ds_row = smem_u32(sDS) + (j & 1) * FQ_DS + r * 128;
-      if (j >= 2) mbar_wait(&ds_free[j & 1], ((j - 2) >> 1) & 1);  // dQ(j-2) has read it
       {
         const int c = half;
         uint32_t vs[32], vp[32];
@@ -792,16 +794,13 @@ __global__ void __launch_bounds__(384, 1)
           }
           wd[q] = pack_bf16(d2[0], d2[1]);
         }
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const int cc = c * 4 + h;  // 16-byte chunk within the 128-byte row
-          st_shared_v4(ds_row + ((cc ^ (r & 7)) << 4), wd[4 * h], wd[4 * h + 1], wd[4 * h + 2],
-                       wd[4 * h + 3]);
-        }
+        // dS as a TMEM A operand: packed into the first 16 columns of this
+        // warpgroup's fp32 slab of the S buffer (read above)
+        tmem_st_32x32b_x16(tS + c * 32, wd);
+        tmem_st_wait();
       }
-      fence_proxy_async_smem();
       tc_fence_before();
-      mbar_arrive(&ds_full[j & 1]);
+      mbar_arrive(&ds_full[j % 3]);
     }
     mbar_wait(acc_done, 0);
     tc_fence_after();
