@@ -196,6 +196,16 @@ def run_reference(args, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def vp_comm_desc(args, vp, world):
+    if not vp or world == 1:
+        return {}
+    base = "gloo" if getattr(args, "shared_gpu", False) else "NCCL"
+    if getattr(args, "vp_comm", "nccl") == "fused":
+        return {"vp_comm": "z all-gather (a4) and dz reduce-scatter (a8) fused into the kernels "
+                           f"over CUDA-IPC peer memory + peer barriers; CE stats, body grads: {base}"}
+    return {"vp_comm": f"{base} all-gather / reduce-scatter"}
+
+
 def workload_config(cfg, world, args):
     vp = getattr(args, "parallel", "dp") == "vp"
     tok = cfg.tokens // world if vp else cfg.tokens
@@ -209,6 +219,7 @@ def workload_config(cfg, world, args):
             "collectives": ("none" if world == 1 else
                             "gloo, ranks sharing one GPU (test mode)" if getattr(args, "shared_gpu", False)
                             else "NCCL (torch.distributed)"),
+            **vp_comm_desc(args, vp, world),
             "l2": "inputs larger than L2 (hidden states + exit weights per step >> 126 MB)",
             "optimizer": "Adam (P:374-375), included in the step",
             "update_schedule": ("per exit, shared gradient buffers (P:261)"
@@ -278,6 +289,9 @@ def main():
     ap.add_argument("--grad-buffers", type=int, default=-1,
                     help="k < exits: exits share k gradient buffers and are updated one by one "
                          "(P:261); default 2 when the config has more than 4 exits")
+    ap.add_argument("--vp-comm", default="fused", choices=["fused", "nccl"],
+                    help="vp: fused = z all-gather / dz reduce-scatter inside the a4 / a8 "
+                         "kernels over CUDA-IPC peer memory; nccl = NCCL collectives")
     ap.add_argument("--parallel", default="dp", choices=["dp", "vp"],
                     help="N>1: dp = data parallel over tokens (weak scaling); vp = W_out "
                          "vocab-parallel with the distributed softmax-CE (strong scaling)")
@@ -318,9 +332,9 @@ def main():
     n = cfg.tokens // world if vp else cfg.tokens       # tokens of this rank's exit bodies
     n_all = cfg.tokens if vp else n
     E = cfg.exits
-    from paper_2402_00518_b200.parallel import (GpuPhases, LocalComm, TorchComm,
+    from paper_2402_00518_b200.parallel import (GpuPhases, LocalComm, PeerBuffers, TorchComm,
                                                 data_parallel_step, vocab_parallel_step,
-                                                vocab_shard)
+                                                vocab_parallel_step_fused, vocab_shard)
     vb, ve = vocab_shard(cfg.vocab, world, rank) if vp else (0, cfg.vocab)
 
     # ---- parameter store, Copy init from a synthetic backbone
@@ -357,11 +371,20 @@ def main():
             hidden.append(x[rank * n:(rank + 1) * n].contiguous())
             del x
         targets = S.targets(cfg, n_all, seed=cfg.seed * 100, device=dev)   # all tokens
-        bufs = {"z_all": torch.zeros(n_all, cfg.hidden, dtype=torch.bfloat16, device=dev),
-                "key": torch.zeros(n_all, dtype=torch.int64, device=dev),
-                "sums": torch.zeros(n_all, 2, device=dev),
-                "dz_partial": torch.zeros(n_all, cfg.hidden, device=dev),
-                "dz_local": torch.zeros(n, cfg.hidden, device=dev)}
+        bufs = {"key": torch.zeros(n_all, dtype=torch.int64, device=dev),
+                "sums": torch.zeros(n_all, 2, device=dev)}
+        peer = None
+        if args.vp_comm == "fused":
+            peer = PeerBuffers(rank, world, n_all, cfg.hidden, device=dev)
+            torch.cuda.synchronize()
+            if world > 1:
+                peer.connect_ipc()
+            else:
+                peer.connect_local([peer])
+        else:
+            bufs.update({"z_all": torch.zeros(n_all, cfg.hidden, dtype=torch.bfloat16, device=dev),
+                         "dz_partial": torch.zeros(n_all, cfg.hidden, device=dev),
+                         "dz_local": torch.zeros(n, cfg.hidden, device=dev)})
         comm = TorchComm() if world > 1 else LocalComm()
         phases = GpuPhases(ee, heads.cfg, heads.workspace)
     else:
@@ -388,8 +411,12 @@ def main():
             return
         if vp:
             ee.ee_count_valid(tg, cfg.vocab, vc, heads.workspace)   # W over all tokens
-            vocab_parallel_step(phases, comm, cfg.arch, hid, tg, heads.operand, heads.grads,
-                                heads.loss, [1.0] * E, vc, bufs)
+            if peer is not None:
+                vocab_parallel_step_fused(phases, comm, peer, cfg.arch, hid, tg, heads.operand,
+                                          heads.grads, heads.loss, [1.0] * E, vc, bufs)
+            else:
+                vocab_parallel_step(phases, comm, cfg.arch, hid, tg, heads.operand, heads.grads,
+                                    heads.loss, [1.0] * E, vc, bufs)
         elif not dp:
             heads.step(hid, tg)
         else:

@@ -55,7 +55,8 @@ typedef enum {
   EE_ERR_WORKSPACE = 8,   /* workspace NULL or smaller than ee_workspace_size()   */
   EE_ERR_CUDA = 9,        /* a CUDA runtime/driver call failed                    */
   EE_ERR_NCCL = 10,       /* reserved for the in-library collectives              */
-  EE_ERR_UNSUPPORTED = 11 /* no sm_100 device                                     */
+  EE_ERR_UNSUPPORTED = 11,/* no sm_100 device                                     */
+  EE_ERR_PEER = 12        /* a peer rank did not reach ee_peer_barrier (device)    */
 } ee_status;
 
 /* Exit architectures (§2.1 "Architectures of early exits").
@@ -268,6 +269,70 @@ ee_status ee_vp_exit_backward(const ee_head_config* cfg, const void* hidden, int
                               int64_t n_all, const ee_head_tensors* params, const float* dz_local,
                               ee_head_tensors* grads, int32_t accumulate, void* workspace,
                               size_t ws_bytes, void* stream);
+
+/* ---- fused vocab-parallel collectives over peer memory ("fused
+ * variants") ----
+ * The all-gather of z (after step 1) and the reduce-scatter of dz (after step
+ * 4) above move 0.94 GB and 1.88 GB per exit at the 70B shape.  These calls do
+ * both inside the producing kernels over NVLink peer memory instead:
+ *  - ee_vp_exit_forward_ag: the a4 RMSNorm kernel stores each z row into EVERY
+ *    rank's z_all (row rank*n_local + t) -- the all-gather is the kernel's own
+ *    stores (Embedding exits: z = x, copied to every rank).
+ *  - ee_vp_vocab_backward_rs: as ee_vp_vocab_backward, but the a8 GEMM epilogue
+ *    routes row m of this rank's dz partial to the token owner q = m / n_local,
+ *    into q's slot buffer at [rank][m - q*n_local][0..h) (no dz_partial).
+ *  - ee_vp_exit_backward_slots: as ee_vp_exit_backward with dz_local replaced
+ *    by the rank's own slot buffer [n_slots][n_local][h] fp32; the a10 kernel
+ *    sums the slots in rank order 0..n_slots-1 (deterministic reduce, fused
+ *    into its loads).
+ *  - ee_peer_barrier: stream-ordered barrier over all ranks through a signal
+ *    array (int32 [EE_MAX_PEERS] per rank): rank r stores `epoch` into slot r
+ *    of every rank's array (st.release.sys) and waits until its own array
+ *    holds >= epoch in all `world` slots (ld.acquire.sys).  epoch must grow by
+ *    one per call.  Required: after each fused all-gather (before step 2),
+ *    after each fused reduce-scatter (before step 5), and once per step before
+ *    the first exit (the previous step's readers of z_all / slots).  A peer
+ *    that does not arrive within ~20 s sets the status word to EE_ERR_PEER
+ *    (read it with ee_get_status) instead of hanging.
+ * Equal token shards are required (n_all = world * n_local).  Peer pointers
+ * (ee_peer_set.ptr[q] = rank q's buffer, mapped into this process; ptr[rank]
+ * is the local buffer) come from ee_ipc_get_handle / ee_ipc_open (CUDA IPC,
+ * one process per GPU) or, in single-process tests, are plain device
+ * buffers.  Results equal the NCCL path's bit for bit except the order of the
+ * dz sum (rank order here). */
+#define EE_MAX_PEERS 8
+typedef struct {
+  int32_t rank, world;            /* this rank; number of ranks (1..EE_MAX_PEERS) */
+  void* ptr[EE_MAX_PEERS];        /* device pointers valid in this process */
+} ee_peer_set;
+
+ee_status ee_vp_exit_forward_ag(const ee_head_config* cfg, const void* hidden, int64_t n_local,
+                                int64_t n_all, const ee_head_tensors* params,
+                                const ee_peer_set* z_all, void* workspace, size_t ws_bytes,
+                                void* stream);
+ee_status ee_vp_vocab_backward_rs(const ee_head_config* cfg, const void* z_all, int64_t n_all,
+                                  const int32_t* targets_all, const int64_t* key_global,
+                                  const float* sums_global, float exit_weight,
+                                  const int64_t* valid_count, const ee_head_tensors* params,
+                                  ee_head_tensors* grads, int32_t accumulate,
+                                  const ee_peer_set* dz_slots, float* loss_out,
+                                  const ee_step_aux* aux, int32_t exit_index, void* workspace,
+                                  size_t ws_bytes, void* stream);
+ee_status ee_vp_exit_backward_slots(const ee_head_config* cfg, const void* hidden,
+                                    int64_t n_local, int64_t n_all,
+                                    const ee_head_tensors* params, const float* dz_slots,
+                                    int32_t n_slots, ee_head_tensors* grads, int32_t accumulate,
+                                    void* workspace, size_t ws_bytes, void* stream);
+ee_status ee_peer_barrier(const ee_peer_set* signals, uint32_t epoch, void* workspace,
+                          void* stream);
+/* CUDA IPC plumbing for ee_peer_set (host calls, not stream-ordered).
+ * ee_ipc_get_handle: 64-byte handle of the allocation containing dev_ptr and
+ * the byte offset of dev_ptr inside it.  ee_ipc_open (in another process on
+ * any GPU of the node with peer access): maps the allocation and returns
+ * base + offset.  ee_ipc_close: unmaps a pointer returned by ee_ipc_open. */
+ee_status ee_ipc_get_handle(const void* dev_ptr, void* handle64, uint64_t* offset);
+ee_status ee_ipc_open(const void* handle64, uint64_t offset, void** dev_ptr);
+ee_status ee_ipc_close(void* dev_ptr, uint64_t offset);
 
 /* Early-exit inference statistics (§3 "Inference"): for
  * each exit i and token t, the exit's greedy next token argmax_out[i][t]

@@ -22,7 +22,7 @@ EE_OK = 0
 STATUS_NAMES = {0: "EE_OK", 1: "EE_ERR_ARG", 2: "EE_ERR_SHAPE", 3: "EE_ERR_ALIGN",
                 4: "EE_ERR_VOCAB", 5: "EE_ERR_ARCH", 6: "EE_ERR_STRUCTURE",
                 7: "EE_ERR_DIVERGED", 8: "EE_ERR_WORKSPACE", 9: "EE_ERR_CUDA",
-                10: "EE_ERR_NCCL", 11: "EE_ERR_UNSUPPORTED"}
+                10: "EE_ERR_NCCL", 11: "EE_ERR_UNSUPPORTED", 12: "EE_ERR_PEER"}
 ARCH = {"embedding": 0, "norm": 1, "mlp": 2, "layer": 3}
 INIT = {"copy": 0, "random": 1}
 DTYPE = {torch.bfloat16: 0, torch.float32: 1}
@@ -34,7 +34,10 @@ EXPORTED = ("ee_workspace_size", "ee_init_heads", "ee_tune_step", "ee_count_vali
             "ee_profile_record", "ee_launch_count", "ee_vp_exit_forward", "ee_vp_vocab_stats",
             "ee_vp_rescale", "ee_vp_vocab_backward", "ee_vp_exit_backward", "ee_exit_infer",
             "ee_backbone_workspace_size", "ee_backbone_forward", "ee_test_attention",
-            "ee_normalize_exit")
+            "ee_normalize_exit", "ee_vp_exit_forward_ag", "ee_vp_vocab_backward_rs",
+            "ee_vp_exit_backward_slots", "ee_peer_barrier", "ee_ipc_get_handle", "ee_ipc_open",
+            "ee_ipc_close")
+MAX_PEERS = 8
 
 
 class EEError(RuntimeError):
@@ -75,6 +78,11 @@ AUX_NAMES = ("lse", "loss_tok", "argmax", "conf", "weight_sum")
 
 class ee_step_aux(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in AUX_NAMES]
+
+
+class ee_peer_set(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("ptr", ctypes.c_void_p * MAX_PEERS)]
 
 
 _lib = None
@@ -122,6 +130,16 @@ def load(path: str = LIB_PATH):
         "ee_vp_vocab_backward": (I32, [CFG, P, I64, P, P, P, F32, P, HT, HT, I32, P, P,
                                        ctypes.POINTER(ee_step_aux), I32, P, SZ, P]),
         "ee_vp_exit_backward": (I32, [CFG, P, I64, I64, HT, P, HT, I32, P, SZ, P]),
+        "ee_vp_exit_forward_ag": (I32, [CFG, P, I64, I64, HT, ctypes.POINTER(ee_peer_set), P, SZ,
+                                        P]),
+        "ee_vp_vocab_backward_rs": (I32, [CFG, P, I64, P, P, P, F32, P, HT, HT, I32,
+                                          ctypes.POINTER(ee_peer_set), P,
+                                          ctypes.POINTER(ee_step_aux), I32, P, SZ, P]),
+        "ee_vp_exit_backward_slots": (I32, [CFG, P, I64, I64, HT, P, I32, HT, I32, P, SZ, P]),
+        "ee_peer_barrier": (I32, [ctypes.POINTER(ee_peer_set), ctypes.c_uint32, P, P]),
+        "ee_ipc_get_handle": (I32, [P, P, ctypes.POINTER(ctypes.c_uint64)]),
+        "ee_ipc_open": (I32, [P, ctypes.c_uint64, ctypes.POINTER(P)]),
+        "ee_ipc_close": (I32, [P, ctypes.c_uint64]),
         "ee_exit_infer": (I32, [CFG, ctypes.POINTER(P), I64, HT, F32, ctypes.POINTER(P),
                                 ctypes.POINTER(P), P, P, SZ, P]),
         "ee_backbone_workspace_size": (I32, [ctypes.POINTER(ee_backbone_config), I64,
@@ -376,6 +394,83 @@ def ee_vp_exit_backward(cfg, hidden, n_all, params, dz_local, grads, workspace,
                                     heads([params]), _ptr(dz_local), heads([grads]),
                                     int(bool(accumulate)), _ptr(workspace), workspace.numel(),
                                     _stream(stream)))
+
+
+def peer_set(rank: int, ptrs) -> ee_peer_set:
+    """ee_peer_set from per-rank device pointers (ints or tensors; entry `rank`
+    is this process's own buffer)."""
+    ptrs = list(ptrs)
+    if not 1 <= len(ptrs) <= MAX_PEERS or not 0 <= rank < len(ptrs):
+        raise ValueError("bad peer set")
+    ps = ee_peer_set()
+    ps.rank, ps.world = rank, len(ptrs)
+    for q, p in enumerate(ptrs):
+        ps.ptr[q] = p.data_ptr() if isinstance(p, torch.Tensor) else int(p)
+    return ps
+
+
+def ee_vp_exit_forward_ag(cfg, hidden, n_all, params, z_peers: ee_peer_set, workspace,
+                          stream=None):
+    """a1-a4 with the all-gather of z fused into the a4 stores (include/ee.h)."""
+    load()
+    n_local = 0 if hidden is None else hidden.shape[0]
+    _check(_lib.ee_vp_exit_forward_ag(ctypes.byref(cfg), _ptr(hidden), n_local, int(n_all),
+                                      heads([params]), ctypes.byref(z_peers), _ptr(workspace),
+                                      workspace.numel(), _stream(stream)))
+
+
+def ee_vp_vocab_backward_rs(cfg, z_all, targets_all, key_global, sums_global, exit_weight,
+                            params, grads, dz_slots: ee_peer_set, loss_out, workspace,
+                            valid_count=None, accumulate=False, aux=None, exit_index=0,
+                            stream=None):
+    """a6-a9 with the reduce-scatter of dz fused into the a8 epilogue stores."""
+    load()
+    _check(_lib.ee_vp_vocab_backward_rs(ctypes.byref(cfg), _ptr(z_all), targets_all.numel(),
+                                        _ptr(targets_all), _ptr(key_global), _ptr(sums_global),
+                                        float(exit_weight), _ptr(valid_count), heads([params]),
+                                        heads([grads]), int(bool(accumulate)),
+                                        ctypes.byref(dz_slots), _ptr(loss_out), _aux1(aux),
+                                        int(exit_index), _ptr(workspace), workspace.numel(),
+                                        _stream(stream)))
+
+
+def ee_vp_exit_backward_slots(cfg, hidden, n_all, params, dz_slots, n_slots, grads, workspace,
+                              accumulate=False, stream=None):
+    """a10-a13 with dz = the rank-ordered sum of this rank's n_slots slots."""
+    load()
+    n_local = 0 if hidden is None else hidden.shape[0]
+    _check(_lib.ee_vp_exit_backward_slots(ctypes.byref(cfg), _ptr(hidden), n_local, int(n_all),
+                                          heads([params]), _ptr(dz_slots), int(n_slots),
+                                          heads([grads]), int(bool(accumulate)), _ptr(workspace),
+                                          workspace.numel(), _stream(stream)))
+
+
+def ee_peer_barrier(signals: ee_peer_set, epoch: int, workspace, stream=None):
+    load()
+    _check(_lib.ee_peer_barrier(ctypes.byref(signals), ctypes.c_uint32(epoch & 0xFFFFFFFF),
+                                _ptr(workspace), _stream(stream)))
+
+
+def ee_ipc_get_handle(t: torch.Tensor) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of t's allocation, byte offset of t inside it)."""
+    load()
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_uint64()
+    _check(_lib.ee_ipc_get_handle(ctypes.c_void_p(t.data_ptr()), h, ctypes.byref(off)))
+    return h.raw, off.value
+
+
+def ee_ipc_open(handle: bytes, offset: int) -> int:
+    load()
+    p = ctypes.c_void_p()
+    _check(_lib.ee_ipc_open(ctypes.create_string_buffer(handle, 64), ctypes.c_uint64(offset),
+                            ctypes.byref(p)))
+    return p.value
+
+
+def ee_ipc_close(ptr: int, offset: int):
+    load()
+    _check(_lib.ee_ipc_close(ctypes.c_void_p(ptr), ctypes.c_uint64(offset)))
 
 
 def ee_profile_start():

@@ -17,6 +17,7 @@
 //              a13 dg_a = sum du * xhat                  gain_grad          (HBM)
 // The full [tokens x vocab] logit matrix is never written: a5 keeps only
 // per-tile (max, sum-exp, argmax) partials and a7 recomputes S tile by tile.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cmath>
 #include <cstdio>
@@ -563,11 +564,19 @@ ee_status layer_attn_backward(const ee_head_config* cfg, const Bufs& B, const ee
 // z_out is given, in which case x is copied there).  Returns z in *z_ret.
 ee_status phase_exit_forward(const ee_head_config* cfg, const Bufs& B, const ee_head_tensors& P,
                              const __nv_bfloat16* x, long long n, __nv_bfloat16* z_out,
-                             const __nv_bfloat16** z_ret, cudaStream_t st) {
+                             const __nv_bfloat16** z_ret, cudaStream_t st,
+                             const PeerRows* ag = nullptr) {
   const int h = cfg->hidden, F = cfg->ffn;
   const bool mlp = cfg->arch >= EE_ARCH_MLP, nrm = cfg->arch != EE_ARCH_EMBEDDING;
   const bool layer = cfg->arch == EE_ARCH_LAYER;
   if (!nrm) {
+    if (ag) {  // fused all-gather of z = x: one copy into every rank's z_all
+      for (int q = 0; q < ag->n && n > 0; ++q)
+        EE_CUDA(cudaMemcpyAsync(ag->p[q] + ag->row_off * h, x, 2 * (size_t)n * h,
+                                cudaMemcpyDefault, st));
+      *z_ret = nullptr;
+      return EE_OK;
+    }
     if (z_out && n > 0)
       EE_CUDA(cudaMemcpyAsync(z_out, x, 2 * (size_t)n * h, cudaMemcpyDeviceToDevice, st));
     *z_ret = z_out ? z_out : x;
@@ -616,10 +625,12 @@ ee_status phase_exit_forward(const ee_head_config* cfg, const Bufs& B, const ee_
     }
     // a4: z = RMSNorm_f(y)
     { Prof p_("a4_rmsnorm_fwd", st, 0, 0, 6.0 * n * h + 4.0 * n);
-    EE_CUDA(launch_rmsnorm_fwd(B.y, true, (const float*)P.g_f, cfg->norm_eps, z, B.ry, n, h, st)); }
+    EE_CUDA(launch_rmsnorm_fwd(B.y, true, (const float*)P.g_f, cfg->norm_eps, z, B.ry, n, h, st,
+                               ag)); }
   } else {
     { Prof p_("a4_rmsnorm_fwd", st, 0, 0, 4.0 * n * h + 4.0 * n);
-    EE_CUDA(launch_rmsnorm_fwd(x, false, (const float*)P.g_f, cfg->norm_eps, z, B.ry, n, h, st)); }
+    EE_CUDA(launch_rmsnorm_fwd(x, false, (const float*)P.g_f, cfg->norm_eps, z, B.ry, n, h, st,
+                               ag)); }
   }
   return EE_OK;
 }
@@ -646,7 +657,7 @@ ee_status phase_vocab_stats(const ee_head_config* cfg, const Bufs& B, const ee_h
 ee_status phase_vocab_backward(const ee_head_config* cfg, const Bufs& B, const ee_head_tensors& P,
                                const ee_head_tensors& G, const __nv_bfloat16* z, long long n,
                                const int32_t* targets, int accumulate, float* dz_out,
-                               cudaStream_t st) {
+                               cudaStream_t st, const ee_peer_set* rs = nullptr) {
   const int h = cfg->hidden, Vl = cfg->vocab_end - cfg->vocab_begin;
   {
     GemmArgs a = base_args((int)n, Vl, h);
@@ -660,10 +671,15 @@ ee_status phase_vocab_backward(const ee_head_config* cfg, const Bufs& B, const e
     Prof p_("a7_ds_recompute", st, 2.0 * n * Vl * h, 0, 0);
     EE_CUDA(gemm_run(EPI_CE_DS, true, true, A, Bm, nullptr, B_PLAIN, 0, a, st));
   }
-  if (dz_out) {  // a8: W_out read MN-major in place
+  if (dz_out || rs) {  // a8: W_out read MN-major in place
     GemmArgs a = base_args((int)n, h, Vl);
     a.out0 = dz_out;
     a.ldo = h;
+    if (rs) {  // fused reduce-scatter: rows to their owners' slot [rank] (include/ee.h)
+      a.scat_rows = (int)(n / rs->world);
+      a.scat_off = (long long)rs->rank * a.scat_rows * h;
+      for (int q = 0; q < rs->world; ++q) a.scat[q] = (float*)rs->ptr[q];
+    }
     Mat A{B.ds, n, Vl, Vl}, Bm{P.w_out, Vl, h, h};
     Prof p_("a8_dz", st, 2.0 * n * Vl * h, 2.0 * n * Vl * h, 0);
     EE_CUDA(gemm_run(EPI_F32, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
@@ -686,7 +702,8 @@ ee_status phase_vocab_backward(const ee_head_config* cfg, const Bufs& B, const e
 // a10..a13 on n tokens given dz: dg_f (+ dy, MLP grads, dg_a for MLP exits).
 ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee_head_tensors& P,
                               const ee_head_tensors& G, const __nv_bfloat16* x, long long n,
-                              const float* dz, int accumulate, cudaStream_t st) {
+                              const float* dz, int accumulate, cudaStream_t st,
+                              int nslots = 1) {
   const int h = cfg->hidden, F = cfg->ffn;
   const bool mlp = cfg->arch >= EE_ARCH_MLP, layer = cfg->arch == EE_ARCH_LAYER;
   if (cfg->arch == EE_ARCH_EMBEDDING) return EE_OK;
@@ -695,7 +712,7 @@ ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee
   { Prof p_("a10_rmsnorm_bwd", st, 0, 0, (mlp ? 10.0 : 6.0) * n * h);
   EE_CUDA(launch_rmsnorm_bwd(dz, mlp ? (const void*)B.y : (const void*)x, mlp, B.ry,
                              (const float*)P.g_f, mlp ? B.dy : nullptr, B.dgp, n, h, NORM_RPB,
-                             st)); }
+                             st, nullptr, nslots, (long long)n * h)); }
   { Prof p_("reduce_cols", st, 0, 0, 4.0 * nparts * h);
   EE_CUDA(launch_reduce_cols(B.dgp, nparts, h, (float*)G.g_f, accumulate, st)); }
   if (!mlp) return EE_OK;
@@ -1196,13 +1213,25 @@ ee_status ee_vp_rescale(const ee_head_config* cfg, int64_t n_all, const int64_t*
   return EE_OK;
 }
 
-ee_status ee_vp_vocab_backward(const ee_head_config* cfg, const void* z_all, int64_t n_all,
-                               const int32_t* targets_all, const int64_t* key_global,
-                               const float* sums_global, float exit_weight,
-                               const int64_t* valid_count, const ee_head_tensors* params,
-                               ee_head_tensors* grads, int32_t accumulate, float* dz_partial,
-                               float* loss_out, const ee_step_aux* aux, int32_t exit_index,
-                               void* workspace, size_t ws_bytes, void* stream) {
+static ee_status check_peer_set(const ee_peer_set* p, long long n_all, const char* what) {
+  if (!p || p->world < 1 || p->world > EE_MAX_PEERS || p->rank < 0 || p->rank >= p->world)
+    return fail(EE_ERR_ARG, "%s: bad ee_peer_set (rank/world)", what);
+  for (int q = 0; q < p->world; ++q)
+    if (!p->ptr[q] || !aligned16(p->ptr[q]))
+      return fail(EE_ERR_ALIGN, "%s: peer pointer %d NULL or misaligned", what, q);
+  if (n_all % p->world) return fail(EE_ERR_SHAPE, "%s: n_all not a multiple of world", what);
+  return EE_OK;
+}
+
+static ee_status vp_vocab_backward_impl(const ee_head_config* cfg, const void* z_all,
+                                        int64_t n_all, const int32_t* targets_all,
+                                        const int64_t* key_global, const float* sums_global,
+                                        float exit_weight, const int64_t* valid_count,
+                                        const ee_head_tensors* params, ee_head_tensors* grads,
+                                        int32_t accumulate, float* dz_partial,
+                                        const ee_peer_set* rs, float* loss_out,
+                                        const ee_step_aux* aux, int32_t exit_index,
+                                        void* workspace, size_t ws_bytes, void* stream) {
   Bufs B;
   ee_status s = vp_common(cfg, n_all, workspace, ws_bytes, &B);
   if (s != EE_OK) return s;
@@ -1210,7 +1239,8 @@ ee_status ee_vp_vocab_backward(const ee_head_config* cfg, const void* z_all, int
       (n_all > 0 && (!z_all || !targets_all || !key_global || !sums_global)))
     return fail(EE_ERR_ARG, "bad ee_vp_vocab_backward arguments");
   const bool nrm = cfg->arch != EE_ARCH_EMBEDDING;
-  if (nrm && n_all > 0 && !dz_partial) return fail(EE_ERR_ARG, "dz_partial required");
+  if (nrm && n_all > 0 && !dz_partial && !rs) return fail(EE_ERR_ARG, "dz_partial required");
+  if (rs && (s = check_peer_set(rs, n_all, "dz_slots")) != EE_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
   if (n_all == 0) {
     if (!accumulate && (s = zero_grads(cfg, *grads, true, false, st)) != EE_OK) return s;
@@ -1240,7 +1270,34 @@ ee_status ee_vp_vocab_backward(const ee_head_config* cfg, const void* z_all, int
   if (aux && aux->weight_sum)
     EE_CUDA(cudaMemcpyAsync(aux->weight_sum, B.wsum, sizeof(float), cudaMemcpyDeviceToDevice, st));
   return phase_vocab_backward(cfg, B, *params, *grads, (const __nv_bfloat16*)z_all, n_all,
-                              targets_all, accumulate, nrm ? dz_partial : nullptr, st);
+                              targets_all, accumulate, nrm ? dz_partial : nullptr, st,
+                              nrm ? rs : nullptr);
+}
+
+ee_status ee_vp_vocab_backward(const ee_head_config* cfg, const void* z_all, int64_t n_all,
+                               const int32_t* targets_all, const int64_t* key_global,
+                               const float* sums_global, float exit_weight,
+                               const int64_t* valid_count, const ee_head_tensors* params,
+                               ee_head_tensors* grads, int32_t accumulate, float* dz_partial,
+                               float* loss_out, const ee_step_aux* aux, int32_t exit_index,
+                               void* workspace, size_t ws_bytes, void* stream) {
+  return vp_vocab_backward_impl(cfg, z_all, n_all, targets_all, key_global, sums_global,
+                                exit_weight, valid_count, params, grads, accumulate, dz_partial,
+                                nullptr, loss_out, aux, exit_index, workspace, ws_bytes, stream);
+}
+
+ee_status ee_vp_vocab_backward_rs(const ee_head_config* cfg, const void* z_all, int64_t n_all,
+                                  const int32_t* targets_all, const int64_t* key_global,
+                                  const float* sums_global, float exit_weight,
+                                  const int64_t* valid_count, const ee_head_tensors* params,
+                                  ee_head_tensors* grads, int32_t accumulate,
+                                  const ee_peer_set* dz_slots, float* loss_out,
+                                  const ee_step_aux* aux, int32_t exit_index, void* workspace,
+                                  size_t ws_bytes, void* stream) {
+  if (!dz_slots) return fail(EE_ERR_ARG, "dz_slots required");
+  return vp_vocab_backward_impl(cfg, z_all, n_all, targets_all, key_global, sums_global,
+                                exit_weight, valid_count, params, grads, accumulate, nullptr,
+                                dz_slots, loss_out, aux, exit_index, workspace, ws_bytes, stream);
 }
 
 ee_status ee_vp_exit_backward(const ee_head_config* cfg, const void* hidden, int64_t n_local,
@@ -1261,6 +1318,110 @@ ee_status ee_vp_exit_backward(const ee_head_config* cfg, const void* hidden, int
   }
   return phase_exit_backward(cfg, B, *params, *grads, (const __nv_bfloat16*)hidden, n_local,
                              dz_local, accumulate, st);
+}
+
+ee_status ee_vp_exit_forward_ag(const ee_head_config* cfg, const void* hidden, int64_t n_local,
+                                int64_t n_all, const ee_head_tensors* params,
+                                const ee_peer_set* z_all, void* workspace, size_t ws_bytes,
+                                void* stream) {
+  Bufs B;
+  ee_status s = vp_common(cfg, n_all, workspace, ws_bytes, &B);
+  if (s != EE_OK) return s;
+  if (!params || n_local < 0 || (n_local > 0 && !hidden))
+    return fail(EE_ERR_ARG, "bad ee_vp_exit_forward_ag arguments");
+  if ((s = check_peer_set(z_all, n_all, "z_all")) != EE_OK) return s;
+  if (n_local * z_all->world != n_all) return fail(EE_ERR_SHAPE, "n_all != world * n_local");
+  if (ee_status s2 = check_tokens(cfg, n_local); s2 != EE_OK) return s2;
+  if ((s = check_arch_tensors(cfg, *params, "params", 0)) != EE_OK) return s;
+  if (hidden && !aligned16(hidden)) return fail(EE_ERR_ALIGN, "misaligned");
+  PeerRows ag{};
+  ag.n = z_all->world;
+  ag.row_off = (long long)z_all->rank * n_local;
+  for (int q = 0; q < z_all->world; ++q) ag.p[q] = (__nv_bfloat16*)z_all->ptr[q];
+  const __nv_bfloat16* z = nullptr;
+  return phase_exit_forward(cfg, B, *params, (const __nv_bfloat16*)hidden, n_local, nullptr, &z,
+                            (cudaStream_t)stream, &ag);
+}
+
+ee_status ee_vp_exit_backward_slots(const ee_head_config* cfg, const void* hidden,
+                                    int64_t n_local, int64_t n_all,
+                                    const ee_head_tensors* params, const float* dz_slots,
+                                    int32_t n_slots, ee_head_tensors* grads, int32_t accumulate,
+                                    void* workspace, size_t ws_bytes, void* stream) {
+  if (n_slots < 1 || n_slots > EE_MAX_PEERS) return fail(EE_ERR_ARG, "n_slots out of range");
+  if (dz_slots && !aligned16(dz_slots)) return fail(EE_ERR_ALIGN, "dz_slots misaligned");
+  Bufs B;
+  ee_status s = vp_common(cfg, n_all, workspace, ws_bytes, &B);
+  if (s != EE_OK) return s;
+  if (!params || !grads || n_local < 0 || n_local > n_all ||
+      (n_local > 0 && cfg->arch != EE_ARCH_EMBEDDING && (!hidden || !dz_slots)))
+    return fail(EE_ERR_ARG, "bad ee_vp_exit_backward_slots arguments");
+  if (ee_status s2 = check_tokens(cfg, n_local); s2 != EE_OK) return s2;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_local == 0) {
+    if (!accumulate) return zero_grads(cfg, *grads, false, true, st);
+    return EE_OK;
+  }
+  return phase_exit_backward(cfg, B, *params, *grads, (const __nv_bfloat16*)hidden, n_local,
+                             dz_slots, accumulate, st, n_slots);
+}
+
+ee_status ee_peer_barrier(const ee_peer_set* signals, uint32_t epoch, void* workspace,
+                          void* stream) {
+  if (!workspace || !aligned16(workspace)) return fail(EE_ERR_ARG, "workspace NULL or misaligned");
+  if (!signals || signals->world < 1 || signals->world > EE_MAX_PEERS || signals->rank < 0 ||
+      signals->rank >= signals->world)
+    return fail(EE_ERR_ARG, "bad ee_peer_set");
+  for (int q = 0; q < signals->world; ++q)
+    if (!signals->ptr[q]) return fail(EE_ERR_ARG, "signal pointer %d NULL", q);
+  if (ee_status s = check_device(); s != EE_OK) return s;
+  EE_CUDA(launch_peer_barrier((int* const*)signals->ptr, signals->rank, signals->world, epoch,
+                              (DevStatus*)workspace, (cudaStream_t)stream));
+  return EE_OK;
+}
+
+static CUresult (*get_addr_range())(CUdeviceptr*, size_t*, CUdeviceptr) {
+  static CUresult (*fn)(CUdeviceptr*, size_t*, CUdeviceptr) = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      fn = (CUresult(*)(CUdeviceptr*, size_t*, CUdeviceptr))p;
+  }
+  return fn;
+}
+
+ee_status ee_ipc_get_handle(const void* dev_ptr, void* handle64, uint64_t* offset) {
+  if (!dev_ptr || !handle64 || !offset) return fail(EE_ERR_ARG, "NULL argument");
+  auto range = get_addr_range();
+  if (!range) return fail(EE_ERR_CUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (CUdeviceptr)dev_ptr) != CUDA_SUCCESS)
+    return fail(EE_ERR_CUDA, "cuMemGetAddressRange failed (not device memory?)");
+  cudaIpcMemHandle_t h;
+  EE_CUDA(cudaIpcGetMemHandle(&h, (void*)base));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(handle64, &h, sizeof(h));
+  *offset = (uint64_t)((CUdeviceptr)dev_ptr - base);
+  return EE_OK;
+}
+
+ee_status ee_ipc_open(const void* handle64, uint64_t offset, void** dev_ptr) {
+  if (!handle64 || !dev_ptr) return fail(EE_ERR_ARG, "NULL argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  void* base = nullptr;
+  EE_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  *dev_ptr = (char*)base + offset;
+  return EE_OK;
+}
+
+ee_status ee_ipc_close(void* dev_ptr, uint64_t offset) {
+  if (!dev_ptr) return fail(EE_ERR_ARG, "NULL argument");
+  EE_CUDA(cudaIpcCloseMemHandle((char*)dev_ptr - offset));
+  return EE_OK;
 }
 
 ee_status ee_normalize_exit(const ee_head_config* cfg, ee_head_tensors* grads, float* loss,

@@ -66,6 +66,12 @@ struct GemmArgs {
   int m_split;
   int n_split;  // EPI_F32T: output columns n >= n_split go to out1 (row n - n_split)
   int accumulate;
+  // EPI_F32 fused reduce-scatter (scat_rows > 0): output row m goes to
+  // scat[m / scat_rows] + scat_off + (m % scat_rows) * ldo (the token owner's
+  // slot for this rank, include/ee.h ee_vp_vocab_backward_rs); out0/out1 unused
+  float* scat[8];
+  int scat_rows;
+  long long scat_off;
   const __nv_bfloat16* resid;
   long long ld_resid;
   __nv_bfloat16* outb;  // EPI_BF16 output (ldo)
@@ -129,8 +135,13 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
   if constexpr (EPI == EPI_F32 || EPI == EPI_RESID) {
     float* orow = nullptr;
     if (row_ok) {
-      orow = (gm < args.m_split) ? args.out0 + (long long)gm * args.ldo
-                                 : args.out1 + (long long)(gm - args.m_split) * args.ldo;
+      if (EPI == EPI_F32 && args.scat_rows > 0) {
+        const int q = gm / args.scat_rows;
+        orow = args.scat[q] + args.scat_off + (long long)(gm - q * args.scat_rows) * args.ldo;
+      } else {
+        orow = (gm < args.m_split) ? args.out0 + (long long)gm * args.ldo
+                                   : args.out1 + (long long)(gm - args.m_split) * args.ldo;
+      }
     }
 #pragma unroll 1
     for (int c = 0; c < GEMM_BN / 32; ++c) {

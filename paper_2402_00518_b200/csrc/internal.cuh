@@ -36,14 +36,33 @@ int debug_trace_read(unsigned long long* host, int max);
 // ---- bandwidth-bound kernels (kernels.cu) -----------------------------------
 cudaError_t launch_count_valid(const int32_t* targets, long long n, int vocab, long long* out,
                                DevStatus* st, cudaStream_t s);
+// Fused all-gather target of a row-producing kernel: row t is stored into
+// each of the n buffers at row row_off + t (peer pointers, include/ee.h).
+constexpr int MAX_PEERS = 8;
+struct PeerRows {
+  __nv_bfloat16* p[MAX_PEERS];
+  int n;
+  long long row_off;
+};
+struct PeerSig {
+  int* p[MAX_PEERS];
+};
 // rmsnorm forward; in = bf16 or fp32 [n x h] -> out bf16 [n x h], r fp32 [n]
+// (ag != NULL: out is ignored and each z row goes to every ag->p[q])
 cudaError_t launch_rmsnorm_fwd(const void* in, bool in_f32, const float* g, float eps,
-                               __nv_bfloat16* out, float* r, long long n, int h, cudaStream_t s);
-// rmsnorm backward: dz fp32, y (bf16/fp32), r, g -> dy bf16 (nullable), dg partials
+                               __nv_bfloat16* out, float* r, long long n, int h, cudaStream_t s,
+                               const PeerRows* ag = nullptr);
+// rmsnorm backward: dz fp32, y (bf16/fp32), r, g -> dy bf16 (nullable), dg partials.
+// dz = sum over nslots slabs dz + k*slot_stride, k = 0..nslots-1 in order
+// (the fused reduce-scatter's owner-side sum).
 cudaError_t launch_rmsnorm_bwd(const float* dz, const void* y, bool y_f32, const float* r,
                                const float* g, __nv_bfloat16* dy, float* dg_part, long long n,
                                int h, int rows_per_block, cudaStream_t s,
-                               const __nv_bfloat16* add = nullptr);  // dy = add + dx
+                               const __nv_bfloat16* add = nullptr,  // dy = add + dx
+                               int nslots = 1, long long slot_stride = 0);
+// stream-ordered barrier over peer signal arrays (int32 [MAX_PEERS] per rank)
+cudaError_t launch_peer_barrier(int* const* sig, int rank, int world, unsigned epoch,
+                                DevStatus* st, cudaStream_t s);
 // gain grad: dg partials of sum_t du_t * x_t * r_t
 cudaError_t launch_gain_grad(const float* du, const __nv_bfloat16* x, const float* r,
                              float* dg_part, long long n, int h, int rows_per_block,

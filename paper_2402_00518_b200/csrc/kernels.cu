@@ -90,7 +90,7 @@ cudaError_t launch_count_valid(const int32_t* targets, long long n, int vocab, l
 template <typename TIn>
 __global__ void rmsnorm_fwd_kernel(const TIn* __restrict__ in, const float* __restrict__ g,
                                    float eps, __nv_bfloat16* __restrict__ out,
-                                   float* __restrict__ r, int h) {
+                                   float* __restrict__ r, int h, PeerRows ag) {
   __shared__ float red[33];
   const long long row = blockIdx.x;
   const int nchunk = h / 8;
@@ -115,21 +115,28 @@ __global__ void rmsnorm_fwd_kernel(const TIn* __restrict__ in, const float* __re
       load8(g + c * 8, gv);
 #pragma unroll
       for (int k = 0; k < 8; ++k) o[k] = gv[k] * (x[i][k] * rr);
-      store8(out + row * h + c * 8, o);
+      if (ag.n == 0) {
+        store8(out + row * h + c * 8, o);
+      } else {  // fused all-gather: the same 16 bytes to every rank's z_all (NVLink stores)
+        for (int q = 0; q < ag.n; ++q) store8(ag.p[q] + (ag.row_off + row) * h + c * 8, o);
+      }
     }
   }
   if (threadIdx.x == 0) r[row] = rr;
 }
 
 cudaError_t launch_rmsnorm_fwd(const void* in, bool in_f32, const float* g, float eps,
-                               __nv_bfloat16* out, float* r, long long n, int h, cudaStream_t s) {
+                               __nv_bfloat16* out, float* r, long long n, int h, cudaStream_t s,
+                               const PeerRows* ag) {
   if (n == 0) return cudaSuccess;
   const int t = norm_threads(h);
+  PeerRows pr{};
+  if (ag) pr = *ag;
   if (in_f32)
-    rmsnorm_fwd_kernel<float><<<(unsigned)n, t, 0, s>>>((const float*)in, g, eps, out, r, h);
+    rmsnorm_fwd_kernel<float><<<(unsigned)n, t, 0, s>>>((const float*)in, g, eps, out, r, h, pr);
   else
     rmsnorm_fwd_kernel<__nv_bfloat16>
-        <<<(unsigned)n, t, 0, s>>>((const __nv_bfloat16*)in, g, eps, out, r, h);
+        <<<(unsigned)n, t, 0, s>>>((const __nv_bfloat16*)in, g, eps, out, r, h, pr);
   return cudaGetLastError();
 }
 
@@ -139,7 +146,8 @@ template <typename TY>
 __global__ void rmsnorm_bwd_kernel(const float* __restrict__ dz, const TY* __restrict__ y,
                                    const float* __restrict__ r, const float* __restrict__ g,
                                    __nv_bfloat16* dy, const __nv_bfloat16* add,
-                                   float* __restrict__ dg_part, long long n, int h, int rpb) {
+                                   float* __restrict__ dg_part, long long n, int h, int rpb,
+                                   int nslots, long long slot_stride) {
   __shared__ float red[33];
   const int nchunk = h / 8;
   float gv[NORM_CHUNKS][8], acc[NORM_CHUNKS][8];
@@ -161,6 +169,12 @@ __global__ void rmsnorm_bwd_kernel(const float* __restrict__ dz, const TY* __res
       const int c = threadIdx.x + i * blockDim.x;
       if (c < nchunk) {
         load8(dz + row * h + c * 8, d[i]);
+        for (int q = 1; q < nslots; ++q) {  // owner-side sum of the fused reduce-scatter
+          float e[8];
+          load8(dz + q * slot_stride + row * h + c * 8, e);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) d[i][k] += e[k];
+        }
         load8(y + row * h + c * 8, yh[i]);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -203,16 +217,56 @@ __global__ void rmsnorm_bwd_kernel(const float* __restrict__ dz, const TY* __res
 
 cudaError_t launch_rmsnorm_bwd(const float* dz, const void* y, bool y_f32, const float* r,
                                const float* g, __nv_bfloat16* dy, float* dg_part, long long n,
-                               int h, int rpb, cudaStream_t s, const __nv_bfloat16* add) {
+                               int h, int rpb, cudaStream_t s, const __nv_bfloat16* add,
+                               int nslots, long long slot_stride) {
   const unsigned nb = (unsigned)((n + rpb - 1) / rpb);
   if (nb == 0) return cudaSuccess;
   const int t = norm_threads(h);
   if (y_f32)
     rmsnorm_bwd_kernel<float>
-        <<<nb, t, 0, s>>>(dz, (const float*)y, r, g, dy, add, dg_part, n, h, rpb);
+        <<<nb, t, 0, s>>>(dz, (const float*)y, r, g, dy, add, dg_part, n, h, rpb, nslots,
+                          slot_stride);
   else
     rmsnorm_bwd_kernel<__nv_bfloat16>
-        <<<nb, t, 0, s>>>(dz, (const __nv_bfloat16*)y, r, g, dy, add, dg_part, n, h, rpb);
+        <<<nb, t, 0, s>>>(dz, (const __nv_bfloat16*)y, r, g, dy, add, dg_part, n, h, rpb,
+                          nslots, slot_stride);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- peer barrier
+// Rank `rank` publishes `epoch` into slot `rank` of every rank's signal array
+// (release at system scope: this stream's earlier kernels, including their
+// NVLink stores into peer buffers, are complete and visible first), then waits
+// until its own array holds >= epoch in all `world` slots (acquire).  Thread q
+// handles peer q.  A peer missing for ~20 s sets EE_ERR_PEER instead of hanging.
+__global__ void peer_barrier_kernel(PeerSig sig, int rank, int world, unsigned epoch,
+                                    DevStatus* st) {
+  const int q = threadIdx.x;
+  if (q >= world) return;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(sig.p[q] + rank), "r"(epoch) : "memory");
+  const int* mine = sig.p[rank] + q;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (true) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
+    if ((int)(v - epoch) >= 0) break;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 20000000000ull) {
+      set_status(st, 12 /* EE_ERR_PEER */, q);
+      break;
+    }
+    __nanosleep(256);
+  }
+}
+
+cudaError_t launch_peer_barrier(int* const* sig, int rank, int world, unsigned epoch,
+                                DevStatus* st, cudaStream_t s) {
+  PeerSig ps{};
+  for (int q = 0; q < world && q < MAX_PEERS; ++q) ps.p[q] = sig[q];
+  peer_barrier_kernel<<<1, 32, 0, s>>>(ps, rank, world, epoch, st);
   return cudaGetLastError();
 }
 

@@ -156,6 +156,27 @@ class GpuPhases:
         self.ee.ee_vp_exit_backward(self.cfg, hidden, n_all, params, dz_local, grads, self.ws,
                                     accumulate=accumulate, stream=self.stream)
 
+    # fused peer-memory variants (vocab_parallel_step_fused)
+    def exit_forward_ag(self, hidden, params, peer, n_all):
+        self.ee.ee_vp_exit_forward_ag(self.cfg, hidden, n_all, params, peer.z_set, self.ws,
+                                      self.stream)
+
+    def vocab_backward_rs(self, i, z_all, targets_all, key, sums, alpha, W, params, grads, peer,
+                          loss_slot, accumulate, aux=None):
+        self.ee.ee_vp_vocab_backward_rs(self.cfg, z_all, targets_all, key, sums, alpha, params,
+                                        grads, peer.slot_set, loss_slot, self.ws, valid_count=W,
+                                        accumulate=accumulate, aux=aux, exit_index=i,
+                                        stream=self.stream)
+
+    def exit_backward_slots(self, hidden, params, peer, grads, accumulate, n_all):
+        self.ee.ee_vp_exit_backward_slots(self.cfg, hidden, n_all, params, peer.slots,
+                                          peer.world, grads, self.ws, accumulate=accumulate,
+                                          stream=self.stream)
+
+    def barrier(self, peer):
+        peer.epoch += 1
+        self.ee.ee_peer_barrier(peer.sig_set, peer.epoch, self.ws, self.stream)
+
 
 def vocab_parallel_step(phases, comm, arch: str, hidden_local, targets_all, params, grads,
                         loss: torch.Tensor, exit_weights, W: torch.Tensor, bufs: dict,
@@ -195,6 +216,101 @@ def vocab_parallel_step(phases, comm, arch: str, hidden_local, targets_all, para
             comm.reduce_scatter(dz_local, dz_partial)
         phases.exit_backward(hidden_local[i], params[i], dz_local, grads[i], accumulate,
                              n_all)                                             # a10-a13
+        for k in EXIT_BODY:
+            if grads[i].get(k) is not None:
+                handles.append(comm.all_reduce(grads[i][k], "sum", async_op=True))
+    for h in handles:
+        if h is not None:
+            h.wait()
+
+
+# ---------------------------------------------------------------------------
+# Vocab-parallel step with the z all-gather and the dz reduce-scatter fused
+# into the producing kernels over peer memory (SURVEY §8(e) "fused variants")
+# ---------------------------------------------------------------------------
+
+class PeerBuffers:
+    """The symmetric buffers of the fused vocab-parallel collectives on one
+    rank: z_all [n_all x h] bf16 (every rank's a4 kernel stores its z rows
+    here), dz slots [world x n_local x h] fp32 (every rank's a8 epilogue stores
+    its dz partial rows for this rank's tokens into slot [its rank]) and the
+    int32 signal array of ee_peer_barrier.  ptr tables: connect_ipc (one
+    process per GPU, CUDA IPC handles exchanged over the process group) or
+    connect_local (ranks emulated inside one process)."""
+
+    def __init__(self, rank: int, world: int, n_all: int, h: int, device="cuda",
+                 z_dtype=torch.bfloat16):
+        if n_all % world:
+            raise ValueError("fused vocab-parallel step needs equal token shards")
+        self.rank, self.world, self.n_all, self.n_local = rank, world, n_all, n_all // world
+        self.z_all = torch.zeros(n_all, h, dtype=z_dtype, device=device)
+        self.slots = torch.zeros(world, self.n_local, h, dtype=torch.float32, device=device)
+        self.sig = torch.zeros(8, dtype=torch.int32, device=device)
+        self.epoch = 0
+        self._opened = []
+        self.z_set = self.slot_set = self.sig_set = None
+
+    def _tables(self, z, sl, sg):
+        from paper_2402_00518_b200 import peer_set
+        self.z_set, self.slot_set, self.sig_set = (peer_set(self.rank, z), peer_set(self.rank, sl),
+                                                   peer_set(self.rank, sg))
+
+    def connect_local(self, ranks: list["PeerBuffers"]):
+        self._tables([b.z_all for b in ranks], [b.slots for b in ranks], [b.sig for b in ranks])
+
+    def connect_ipc(self, group=None):
+        import paper_2402_00518_b200 as ee
+        mine = [ee.ee_ipc_get_handle(t) for t in (self.z_all, self.slots, self.sig)]
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=group)
+        tabs = [[], [], []]
+        for q in range(self.world):
+            for j, t in enumerate((self.z_all, self.slots, self.sig)):
+                if q == self.rank:
+                    tabs[j].append(t.data_ptr())
+                else:
+                    p = ee.ee_ipc_open(*allh[q][j])
+                    self._opened.append((p, allh[q][j][1]))
+                    tabs[j].append(p)
+        self._tables(*tabs)
+
+    def close(self):
+        import paper_2402_00518_b200 as ee
+        for p, off in self._opened:
+            ee.ee_ipc_close(p, off)
+        self._opened = []
+
+
+def vocab_parallel_step_fused(phases, comm, peer: PeerBuffers, arch: str, hidden_local,
+                              targets_all, params, grads, loss: torch.Tensor, exit_weights,
+                              W: torch.Tensor, bufs: dict, accumulate: bool = False, aux=None):
+    """vocab_parallel_step with the two bulk exchanges inside the kernels:
+    a4 stores z into every rank's z_all (all-gather), the a8 epilogue stores
+    dz rows into their owners' slots (reduce-scatter; the owner's a10 kernel
+    sums the slots in rank order).  Peer barriers (ee_peer_barrier) order the
+    stores against the readers: once before the first exit (the previous
+    step's readers), after each all-gather and after each reduce-scatter.  The
+    CE statistics (8 B + 8 B per token) stay on `comm`, as do the exit-body
+    gradient all-reduces (async).  bufs: key [n_all] int64, sums [n_all x 2]."""
+    key, sums = bufs["key"], bufs["sums"]
+    n_all = peer.n_all
+    body = arch != "embedding"
+    handles = []
+    phases.barrier(peer)
+    for i in range(len(hidden_local)):
+        phases.exit_forward_ag(hidden_local[i], params[i], peer, n_all)         # a1-a4 + AG
+        phases.barrier(peer)
+        phases.vocab_stats(peer.z_all, targets_all, params[i], key, sums)       # a5
+        comm.all_reduce(key, "max")
+        phases.rescale(key, sums)
+        comm.all_reduce(sums, "sum")
+        phases.vocab_backward_rs(i, peer.z_all, targets_all, key, sums, exit_weights[i], W,
+                                 params[i], grads[i], peer, loss[i:i + 1], accumulate,
+                                 None if aux is None else aux[i])               # a6-a9 + RS
+        phases.barrier(peer)
+        if body:
+            phases.exit_backward_slots(hidden_local[i], params[i], peer, grads[i], accumulate,
+                                       n_all)                                   # a10-a13
         for k in EXIT_BODY:
             if grads[i].get(k) is not None:
                 handles.append(comm.all_reduce(grads[i][k], "sum", async_op=True))
