@@ -197,6 +197,14 @@ def run_reference(args, cfg, rank, world):
 
 
 def vp_comm_desc(args, vp, world):
+    if getattr(args, "dp_fused", False):
+        base = "gloo" if getattr(args, "shared_gpu", False) else "NCCL"
+        return {"dp_comm": "gradient reduce-scatter fused into the weight-gradient GEMM epilogues "
+                           "(rows stored into their owners' arenas over CUDA-IPC peer memory), "
+                           "sharded Adam storing the new operands into every rank (ZeRO-1), "
+                           f"peer barriers; valid count and losses: {base}"}
+    if not vp and world > 1:
+        return {"dp_comm": "NCCL all-reduce of fp32 gradients (async, overlapped) + Adam per rank"}
     if not vp or world == 1:
         return {}
     base = "gloo" if getattr(args, "shared_gpu", False) else "NCCL"
@@ -223,7 +231,9 @@ def workload_config(cfg, world, args):
             "l2": "inputs larger than L2 (hidden states + exit weights per step >> 126 MB)",
             "optimizer": "Adam (P:374-375), included in the step",
             "update_schedule": ("per exit, shared gradient buffers (P:261)"
-                                if getattr(args, "per_exit", False) else "all exits, then Adam")}
+                                if getattr(args, "per_exit", False) else
+                                "per exit: tune, barrier, sharded Adam (P:261)"
+                                if getattr(args, "dp_fused", False) else "all exits, then Adam")}
 
 
 LLAMA2 = {4096: (32, 32), 5120: (40, 40), 8192: (64, 8)}   # hidden -> (heads, kv heads) [ext]
@@ -289,6 +299,12 @@ def main():
     ap.add_argument("--grad-buffers", type=int, default=-1,
                     help="k < exits: exits share k gradient buffers and are updated one by one "
                          "(P:261); default 2 when the config has more than 4 exits")
+    ap.add_argument("--dp-comm", default="fused", choices=["fused", "nccl"],
+                    help="dp, N>1: fused = gradient reduce-scatter in the weight-gradient GEMM "
+                         "epilogues + sharded Adam storing the operands to every rank (CUDA-IPC "
+                         "peer memory, ZeRO-1); nccl = NCCL all-reduce + full Adam per rank")
+    ap.add_argument("--force-dp-fused", action="store_true",
+                    help="run the fused DP path at N=1 as well (A/B against the plain step)")
     ap.add_argument("--vp-comm", default="fused", choices=["fused", "nccl"],
                     help="vp: fused = z all-gather / dz reduce-scatter inside the a4 / a8 "
                          "kernels over CUDA-IPC peer memory; nccl = NCCL collectives")
@@ -332,7 +348,8 @@ def main():
     n = cfg.tokens // world if vp else cfg.tokens       # tokens of this rank's exit bodies
     n_all = cfg.tokens if vp else n
     E = cfg.exits
-    from paper_2402_00518_b200.parallel import (GpuPhases, LocalComm, PeerBuffers, TorchComm,
+    from paper_2402_00518_b200.parallel import (GpuPhases, LocalComm, PeerBuffers,
+                                                ShardedDPHeads, TorchComm,
                                                 data_parallel_step, vocab_parallel_step,
                                                 vocab_parallel_step_fused, vocab_shard)
     vb, ve = vocab_shard(cfg.vocab, world, rank) if vp else (0, cfg.vocab)
@@ -341,10 +358,34 @@ def main():
     gbuf = args.grad_buffers if args.grad_buffers >= 0 else (2 if E > 4 else 0)
     if vp:
         gbuf = 0
-    heads = ee.ExitHeads(ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch,
-                                     vocab_begin=vb, vocab_end=ve, **attn_kw(cfg)), n_all,
-                         device=dev, grad_buffers=gbuf if gbuf > 0 else None)
-    per_exit = heads.grad_buffers < E
+    dp_fused = cfg.arch != "layer" and not vp and (
+        (dp and args.dp_comm == "fused") or args.force_dp_fused)
+    heads = None
+    if dp_fused:     # gradient reduce-scatter in the GEMM epilogues + sharded Adam (ZeRO-1)
+        heads = ShardedDPHeads(ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch), n,
+                               rank, world, device=dev)
+        err = None
+        try:
+            if world > 1:
+                heads.connect_ipc()
+            else:
+                heads.connect_local([heads])
+        except Exception as e:       # agree on the fallback on every rank
+            err = e
+        ok = torch.tensor([0 if err else 1], device=dev)
+        if multi:
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if not ok.item():
+            print(f"[bench] fused DP unavailable ({err}); using NCCL all-reduce", file=sys.stderr)
+            heads.close()
+            heads, dp_fused = None, False
+            torch.cuda.empty_cache()
+    args.dp_fused = dp_fused
+    if heads is None:
+        heads = ee.ExitHeads(ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch,
+                                         vocab_begin=vb, vocab_end=ve, **attn_kw(cfg)), n_all,
+                             device=dev, grad_buffers=gbuf if gbuf > 0 else None)
+    per_exit = (not dp_fused) and heads.grad_buffers < E
     args.per_exit = per_exit
     bb = S.backbone(cfg, device=dev)
     src = []
@@ -397,6 +438,9 @@ def main():
 
     def step(it, hid=hidden, tg=targets):
         lr = ee.ee_lr_at(min(it + 1, total_iters), total_iters)
+        if dp_fused:       # exit by exit: tune -> peer barrier -> sharded Adam
+            heads.step(hid, tg, lr, all_reduce=dist.all_reduce if multi else None)
+            return
         if per_exit:       # exit-by-exit update with shared gradient buffers
             W = None
             if dp:
@@ -477,7 +521,7 @@ def main():
             dist.barrier()
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record()
-        streamed = not multi and not per_exit and not vp
+        streamed = not multi and not per_exit and not vp and not dp_fused
         for it in range(args.steps):
             if streamed:   # public API for host-resident hidden states: H2D overlapped per exit
                 heads.step_host(h_host, t_host)

@@ -330,6 +330,50 @@ ee_status ee_peer_barrier(const ee_peer_set* signals, uint32_t epoch, void* work
  * the byte offset of dev_ptr inside it.  ee_ipc_open (in another process on
  * any GPU of the node with peer access): maps the allocation and returns
  * base + offset.  ee_ipc_close: unmaps a pointer returned by ee_ipc_open. */
+/* ---- data parallel over tokens with the gradient reduce-scatter fused into
+ * the weight-gradient GEMMs and a sharded Adam (ZeRO-1) ----
+ * The exits' gradients are summed over the P ranks' token shards (the
+ * loss is a sum over independent tokens; A16: normalised by the global W).
+ * Instead of an all-reduce of full fp32 gradients followed by Adam on every
+ * rank, each tensor is split into row blocks of chunk = ceil(R/P) rows (R =
+ * rows of the [R x C] tensor; gains are one row of h, owned by rank 0), and
+ *  - ee_tune_step_rs: as ee_tune_step (accumulate = 0), but the weight-gradient
+ *    GEMM epilogues (a9 dW_out, a11 dW_down, a12 dW_gate|up) and the gain
+ *    reductions store each gradient row into its OWNER's arena, slot [rank]
+ *    (NVLink stores), instead of a local gradient tensor;
+ *  - ee_adam_update_sharded: on each rank, for the rows it owns: g = sum of
+ *    the P slots in rank order, Adam on the fp32 master / moment shards, and
+ *    the new bf16 operand rows (fp32 for gains) stored into EVERY rank's
+ *    operand tensor (the all-gather).
+ * Arena of rank q (fp32, one per exit in flight): for each tensor k needed by
+ * the arch, in ee_head_tensors order, a block [P][rows_q(k) x C_k] (slot r =
+ * rank r's partial); ee_dp_shard_layout gives row_begin / rows of rank's shard
+ * of tensor k, the float offset of its block and the arena's total floats.
+ * grad_arenas[i] (ee_tune_step_rs): every rank's arena for exit i;
+ * grad_arenas[i] (ee_adam_update_sharded): this rank's arena (device ptr);
+ * operands[i * 11 + k]: every rank's operand tensor k of exit i (world
+ * entries; ignored for tensors the arch lacks).  Barriers (ee_peer_barrier):
+ * after the last ee_tune_step_rs writing an arena and before the Adam reading
+ * it; before a step's first forward (operand all-gather of the previous
+ * update complete); and before an arena is written again (2 arenas
+ * alternating exits need no extra barrier).  Results are bitwise equal to
+ * ee_tune_step + a rank-ordered fp32 all-reduce + ee_adam_update.
+ * Uniform token weights, Embedding/Norm/MLP exits (Layer: EE_ERR_UNSUPPORTED). */
+ee_status ee_dp_shard_layout(const ee_head_config* cfg, int32_t world, int32_t rank,
+                             int32_t tensor, int64_t* row_begin, int64_t* rows,
+                             int64_t* arena_offset_floats, int64_t* arena_total_floats);
+ee_status ee_tune_step_rs(const ee_head_config* cfg, const void* const* hidden, int64_t n_tokens,
+                          const int32_t* targets, const float* exit_weights,
+                          const ee_head_tensors* params, const ee_peer_set* grad_arenas,
+                          float* loss_out, const ee_step_aux* aux, const int64_t* valid_count,
+                          void* workspace, size_t ws_bytes, void* stream);
+ee_status ee_adam_update_sharded(const ee_head_config* cfg, int32_t world, int32_t rank,
+                                 const void* const* grad_arenas, ee_head_tensors* master_shard,
+                                 ee_head_tensors* m_shard, ee_head_tensors* v_shard,
+                                 const ee_peer_set* operands, float lr, float beta1, float beta2,
+                                 float eps, float weight_decay, int64_t step, float grad_scale,
+                                 void* stream);
+
 ee_status ee_ipc_get_handle(const void* dev_ptr, void* handle64, uint64_t* offset);
 ee_status ee_ipc_open(const void* handle64, uint64_t offset, void** dev_ptr);
 ee_status ee_ipc_close(void* dev_ptr, uint64_t offset);

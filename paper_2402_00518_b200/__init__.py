@@ -36,7 +36,7 @@ EXPORTED = ("ee_workspace_size", "ee_init_heads", "ee_tune_step", "ee_count_vali
             "ee_backbone_workspace_size", "ee_backbone_forward", "ee_test_attention",
             "ee_normalize_exit", "ee_vp_exit_forward_ag", "ee_vp_vocab_backward_rs",
             "ee_vp_exit_backward_slots", "ee_peer_barrier", "ee_ipc_get_handle", "ee_ipc_open",
-            "ee_ipc_close")
+            "ee_ipc_close", "ee_dp_shard_layout", "ee_tune_step_rs", "ee_adam_update_sharded")
 MAX_PEERS = 8
 
 
@@ -137,6 +137,15 @@ def load(path: str = LIB_PATH):
                                           ctypes.POINTER(ee_step_aux), I32, P, SZ, P]),
         "ee_vp_exit_backward_slots": (I32, [CFG, P, I64, I64, HT, P, I32, HT, I32, P, SZ, P]),
         "ee_peer_barrier": (I32, [ctypes.POINTER(ee_peer_set), ctypes.c_uint32, P, P]),
+        "ee_dp_shard_layout": (I32, [CFG, I32, I32, I32, ctypes.POINTER(I64),
+                                     ctypes.POINTER(I64), ctypes.POINTER(I64),
+                                     ctypes.POINTER(I64)]),
+        "ee_tune_step_rs": (I32, [CFG, ctypes.POINTER(P), I64, P, ctypes.POINTER(F32), HT,
+                                  ctypes.POINTER(ee_peer_set), P, ctypes.POINTER(ee_step_aux), P,
+                                  P, SZ, P]),
+        "ee_adam_update_sharded": (I32, [CFG, I32, I32, ctypes.POINTER(P), HT, HT, HT,
+                                         ctypes.POINTER(ee_peer_set), F32, F32, F32, F32, F32,
+                                         I64, F32, P]),
         "ee_ipc_get_handle": (I32, [P, P, ctypes.POINTER(ctypes.c_uint64)]),
         "ee_ipc_open": (I32, [P, ctypes.c_uint64, ctypes.POINTER(P)]),
         "ee_ipc_close": (I32, [P, ctypes.c_uint64]),
@@ -449,6 +458,55 @@ def ee_peer_barrier(signals: ee_peer_set, epoch: int, workspace, stream=None):
     load()
     _check(_lib.ee_peer_barrier(ctypes.byref(signals), ctypes.c_uint32(epoch & 0xFFFFFFFF),
                                 _ptr(workspace), _stream(stream)))
+
+
+def ee_dp_shard_layout(cfg, world: int, rank: int, tensor: str):
+    """(row_begin, rows, arena offset in floats, arena total floats) of `rank`'s
+    shard of `tensor` (a TENSOR_NAMES entry) under the fused DP path."""
+    load()
+    out = [ctypes.c_int64() for _ in range(4)]
+    _check(_lib.ee_dp_shard_layout(ctypes.byref(cfg), int(world), int(rank),
+                                   TENSOR_NAMES.index(tensor), *[ctypes.byref(o) for o in out]))
+    return tuple(o.value for o in out)
+
+
+def ee_tune_step_rs(cfg, hidden, targets, exit_weights, params, arenas, loss_out, workspace,
+                    aux=None, valid_count=None, stream=None):
+    """ee_tune_step with every gradient row stored into its owner's arena
+    (arenas: one ee_peer_set per exit)."""
+    load()
+    E = cfg.num_exits
+    hid = (ctypes.c_void_p * E)(*[h.data_ptr() for h in hidden])
+    w = (ctypes.c_float * E)(*[float(a) for a in exit_weights])
+    ar = (ee_peer_set * E)(*arenas)
+    ax = None
+    if aux is not None:
+        ax = (ee_step_aux * E)()
+        for i, d in enumerate(aux):
+            for k in AUX_NAMES:
+                t = d.get(k)
+                setattr(ax[i], k, None if t is None else t.data_ptr())
+    _check(_lib.ee_tune_step_rs(ctypes.byref(cfg), hid, targets.numel(), _ptr(targets), w,
+                                heads(params), ar, _ptr(loss_out), ax, _ptr(valid_count),
+                                _ptr(workspace), workspace.numel(), _stream(stream)))
+
+
+def ee_adam_update_sharded(cfg, world, rank, arenas_local, master_shard, m_shard, v_shard,
+                           operand_sets, lr, step, beta1=0.9, beta2=0.95, eps=1e-5,
+                           weight_decay=0.0, grad_scale=1.0, stream=None):
+    """Sharded Adam + operand all-gather; operand_sets: per exit a dict
+    {name: ee_peer_set of every rank's operand tensor}."""
+    load()
+    E = cfg.num_exits
+    ar = (ctypes.c_void_p * E)(*[a.data_ptr() for a in arenas_local])
+    ops = (ee_peer_set * (E * len(TENSOR_NAMES)))()
+    for i, d in enumerate(operand_sets):
+        for k, ps in d.items():
+            ops[i * len(TENSOR_NAMES) + TENSOR_NAMES.index(k)] = ps
+    _check(_lib.ee_adam_update_sharded(ctypes.byref(cfg), int(world), int(rank), ar,
+                                       heads(master_shard), heads(m_shard), heads(v_shard), ops,
+                                       lr, beta1, beta2, eps, weight_decay, int(step), grad_scale,
+                                       _stream(stream)))
 
 
 def ee_ipc_get_handle(t: torch.Tensor) -> tuple[bytes, int]:

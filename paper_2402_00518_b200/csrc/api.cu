@@ -19,6 +19,7 @@
 // per-tile (max, sum-exp, argmax) partials and a7 recomputes S tile by tile.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdarg>
@@ -115,6 +116,39 @@ const TInfo kTens[NTENS] = {
     {&ee_head_tensors::g_att, "g_att", true, false},   {&ee_head_tensors::w_q, "w_q", false, false},
     {&ee_head_tensors::w_k, "w_k", false, false},      {&ee_head_tensors::w_v, "w_v", false, false},
     {&ee_head_tensors::w_o, "w_o", false, false}};
+
+// Row geometry of tensor k as a [R x C] matrix (gains: one row) and its
+// row-block sharding over P ranks for the fused data-parallel path (ZeRO-1):
+// chunk = ceil(R / P) rows per owner, owner q holds rows [q*chunk, ...).
+void tensor_rc(const ee_head_config* c, int k, long long* R, long long* C) {
+  const long long h = c->hidden, F = c->ffn, Vl = c->vocab_end - c->vocab_begin;
+  const long long hkv = 128LL * c->n_kv_heads;
+  switch (k) {
+    case 0: case 4: case 6: *R = 1; *C = h; return;
+    case 1: case 2: *R = F; *C = h; return;
+    case 3: *R = h; *C = F; return;
+    case 5: *R = Vl; *C = h; return;
+    case 7: case 10: *R = h; *C = h; return;
+    default: *R = hkv; *C = h; return;
+  }
+}
+long long shard_chunk(long long R, int P) { return (R + P - 1) / P; }
+long long shard_rows(long long R, int P, int q) {
+  const long long ch = shard_chunk(R, P), b = q * ch;
+  return b >= R ? 0 : (R - b < ch ? R - b : ch);
+}
+bool tensor_needed(const ee_head_config* c, int k);
+// float offset of tensor k's slot block [P][rows_q x C] in rank q's arena; k = NTENS: total
+long long arena_offset(const ee_head_config* c, int P, int q, int k) {
+  long long off = 0;
+  for (int j = 0; j < k; ++j) {
+    if (!tensor_needed(c, j)) continue;
+    long long R, C;
+    tensor_rc(c, j, &R, &C);
+    off += (long long)P * shard_rows(R, P, q) * C;
+  }
+  return off;
+}
 
 bool tensor_needed(const ee_head_config* c, int k) {
   if (k == 5) return true;                          // w_out
@@ -559,6 +593,38 @@ ee_status layer_attn_backward(const ee_head_config* cfg, const Bufs& B, const ee
   return EE_OK;
 }
 
+// Fused data-parallel gradient routing (ee_tune_step_rs): p[k][q] = where
+// this rank's partial of tensor k's rows owned by rank q go (owner q's arena,
+// slot [rank]); chunk[k] = rows per owner.  Gains: one row, owner 0.
+struct GradScatter {
+  float* p[NTENS][MAX_PEERS];
+  int chunk[NTENS];
+};
+
+static GradScatter make_scatter(const ee_head_config* c, const ee_peer_set& arenas) {
+  GradScatter g;
+  memset(&g, 0, sizeof(g));
+  const int P = arenas.world;
+  for (int k = 0; k < NTENS; ++k) {
+    if (!tensor_needed(c, k)) continue;
+    long long R, C;
+    tensor_rc(c, k, &R, &C);
+    g.chunk[k] = (int)shard_chunk(R, P);
+    for (int q = 0; q < P; ++q)
+      g.p[k][q] = (float*)arenas.ptr[q] + arena_offset(c, P, q, k) +
+                  (long long)arenas.rank * shard_rows(R, P, q) * C;
+  }
+  return g;
+}
+
+static void set_scatter(GemmArgs& a, const GradScatter* gs, int k, int k1 = -1) {
+  a.scat_rows = gs->chunk[k];
+  for (int q = 0; q < MAX_PEERS; ++q) {
+    a.scat[q] = gs->p[k][q];
+    a.scat1[q] = k1 >= 0 ? gs->p[k1][q] : nullptr;
+  }
+}
+
 // a1..a4: z = exit-head input of the vocab projection, on n tokens.
 // z_out: where to write z (NULL = the workspace buffer; Embedding: z = x unless
 // z_out is given, in which case x is copied there).  Returns z in *z_ret.
@@ -657,7 +723,8 @@ ee_status phase_vocab_stats(const ee_head_config* cfg, const Bufs& B, const ee_h
 ee_status phase_vocab_backward(const ee_head_config* cfg, const Bufs& B, const ee_head_tensors& P,
                                const ee_head_tensors& G, const __nv_bfloat16* z, long long n,
                                const int32_t* targets, int accumulate, float* dz_out,
-                               cudaStream_t st, const ee_peer_set* rs = nullptr) {
+                               cudaStream_t st, const ee_peer_set* rs = nullptr,
+                               const GradScatter* gs = nullptr) {
   const int h = cfg->hidden, Vl = cfg->vocab_end - cfg->vocab_begin;
   {
     GemmArgs a = base_args((int)n, Vl, h);
@@ -677,8 +744,8 @@ ee_status phase_vocab_backward(const ee_head_config* cfg, const Bufs& B, const e
     a.ldo = h;
     if (rs) {  // fused reduce-scatter: rows to their owners' slot [rank] (include/ee.h)
       a.scat_rows = (int)(n / rs->world);
-      a.scat_off = (long long)rs->rank * a.scat_rows * h;
-      for (int q = 0; q < rs->world; ++q) a.scat[q] = (float*)rs->ptr[q];
+      for (int q = 0; q < rs->world; ++q)
+        a.scat[q] = (float*)rs->ptr[q] + (long long)rs->rank * a.scat_rows * h;
     }
     Mat A{B.ds, n, Vl, Vl}, Bm{P.w_out, Vl, h, h};
     Prof p_("a8_dz", st, 2.0 * n * Vl * h, 2.0 * n * Vl * h, 0);
@@ -692,6 +759,7 @@ ee_status phase_vocab_backward(const ee_head_config* cfg, const Bufs& B, const e
     a.ldo = h;
     a.n_split = Vl;
     a.accumulate = accumulate;
+    if (gs) set_scatter(a, gs, 5);
     Mat A{B.zT, h, n, B.L.ldT}, Bm{B.ds, n, Vl, Vl};
     Prof p_("a9_dw_out", st, 2.0 * n * Vl * h, 2.0 * n * Vl * h, 0);
     EE_CUDA(gemm_run(EPI_F32T, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
@@ -703,7 +771,7 @@ ee_status phase_vocab_backward(const ee_head_config* cfg, const Bufs& B, const e
 ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee_head_tensors& P,
                               const ee_head_tensors& G, const __nv_bfloat16* x, long long n,
                               const float* dz, int accumulate, cudaStream_t st,
-                              int nslots = 1) {
+                              int nslots = 1, const GradScatter* gs = nullptr) {
   const int h = cfg->hidden, F = cfg->ffn;
   const bool mlp = cfg->arch >= EE_ARCH_MLP, layer = cfg->arch == EE_ARCH_LAYER;
   if (cfg->arch == EE_ARCH_EMBEDDING) return EE_OK;
@@ -714,7 +782,8 @@ ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee
                              (const float*)P.g_f, mlp ? B.dy : nullptr, B.dgp, n, h, NORM_RPB,
                              st, nullptr, nslots, (long long)n * h)); }
   { Prof p_("reduce_cols", st, 0, 0, 4.0 * nparts * h);
-  EE_CUDA(launch_reduce_cols(B.dgp, nparts, h, (float*)G.g_f, accumulate, st)); }
+  EE_CUDA(launch_reduce_cols(B.dgp, nparts, h, gs ? gs->p[4][0] : (float*)G.g_f, accumulate,
+                             st)); }
   if (!mlp) return EE_OK;
   // a11: dW_down = dy^T M  (A = dy^T K-major copy, B = M MN-major)
   {
@@ -724,6 +793,7 @@ ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee
     a.out0 = (float*)G.w_down;
     a.ldo = F;
     a.accumulate = accumulate;
+    if (gs) set_scatter(a, gs, 3);
     Mat A{B.dyT, h, n, B.L.ldT}, Bm{B.mact, n, F, F};
     Prof p_("a11_dw_down", st, 2.0 * n * F * h, 2.0 * n * F * h, 0);
     EE_CUDA(gemm_run(EPI_F32, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
@@ -749,6 +819,7 @@ ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee
     a.n_split = F;
     a.ldo = h;
     a.accumulate = accumulate;
+    if (gs) set_scatter(a, gs, 1, 2);
     Mat A{B.uT, h, n, B.L.ldT}, Bm{B.ab, n, 2LL * F, 2LL * F};
     Prof p_("a12_dw_gateup", st, 4.0 * n * F * h, 4.0 * n * F * h, 0);
     EE_CUDA(gemm_run(EPI_F32T, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
@@ -773,7 +844,8 @@ ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee
                                NORM_RPB, st, B.dy));
   }
   { Prof p_("reduce_cols", st, 0, 0, 4.0 * nparts * h);
-  EE_CUDA(launch_reduce_cols(B.dgp, nparts, h, (float*)G.g_a, accumulate, st)); }
+  EE_CUDA(launch_reduce_cols(B.dgp, nparts, h, gs ? gs->p[0][0] : (float*)G.g_a, accumulate,
+                             st)); }
   if (layer) return layer_attn_backward(cfg, B, P, G, x, n, accumulate, st);
   return EE_OK;
 }
@@ -793,18 +865,20 @@ ee_status zero_grads(const ee_head_config* cfg, const ee_head_tensors& G, bool v
 
 extern "C" {
 
-ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int64_t n_tokens,
-                       const int32_t* targets, const float* exit_weights,
-                       const ee_head_tensors* params, ee_head_tensors* grads, int32_t accumulate,
-                       float* loss_out, const ee_step_aux* aux, const int64_t* valid_count,
-                       void* workspace, size_t ws_bytes, void* stream) {
+static ee_status tune_step_impl(const ee_head_config* cfg, const void* const* hidden,
+                                int64_t n_tokens, const int32_t* targets,
+                                const float* exit_weights, const ee_head_tensors* params,
+                                ee_head_tensors* grads, const ee_peer_set* arenas,
+                                int32_t accumulate, float* loss_out, const ee_step_aux* aux,
+                                const int64_t* valid_count, void* workspace, size_t ws_bytes,
+                                void* stream) {
   ee_status s = check_cfg(cfg);
   if (s != EE_OK) return s;
   if (cfg->vocab_begin != 0 || cfg->vocab_end != cfg->vocab)
     return fail(EE_ERR_ARG, "ee_tune_step needs the full vocabulary; use the ee_vp_* phases "
                             "for a vocab-parallel shard");
   const int E = cfg->num_exits;
-  if (!hidden || !exit_weights || !params || !grads || !loss_out || n_tokens < 0 ||
+  if (!hidden || !exit_weights || !params || (!grads && !arenas) || !loss_out || n_tokens < 0 ||
       (n_tokens > 0 && !targets))
     return fail(EE_ERR_ARG, "NULL argument or n_tokens < 0");
   if (n_tokens > (1LL << 30)) return fail(EE_ERR_SHAPE, "n_tokens too large");
@@ -815,7 +889,15 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
                                     "ee_normalize_exit");
   for (int i = 0; i < E; ++i) {
     if ((s = check_arch_tensors(cfg, params[i], "params", i)) != EE_OK) return s;
-    if ((s = check_arch_tensors(cfg, grads[i], "grads", i)) != EE_OK) return s;
+    if (!arenas && (s = check_arch_tensors(cfg, grads[i], "grads", i)) != EE_OK) return s;
+    if (arenas) {
+      const ee_peer_set& a = arenas[i];
+      if (a.world < 1 || a.world > EE_MAX_PEERS || a.rank < 0 || a.rank >= a.world)
+        return fail(EE_ERR_ARG, "grad_arenas[%d]: bad rank/world", i);
+      for (int q = 0; q < a.world; ++q)
+        if (!a.ptr[q] || !aligned16(a.ptr[q]))
+          return fail(EE_ERR_ALIGN, "grad_arenas[%d].ptr[%d] NULL or misaligned", i, q);
+    }
     if (n_tokens > 0 && (!hidden[i] || !aligned16(hidden[i])))
       return fail(hidden[i] ? EE_ERR_ALIGN : EE_ERR_ARG, "hidden[%d] NULL or misaligned", i);
   }
@@ -833,15 +915,36 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
   const long long* vc = valid_count ? (const long long*)valid_count : B.vcount;
 
   if (n == 0) {
-    for (int i = 0; i < E; ++i)
-      if (!accumulate && (s = zero_grads(cfg, grads[i], true, true, st)) != EE_OK) return s;
+    for (int i = 0; i < E && !accumulate; ++i) {
+      if (!arenas) {
+        if ((s = zero_grads(cfg, grads[i], true, true, st)) != EE_OK) return s;
+        continue;
+      }
+      const GradScatter gs = make_scatter(cfg, arenas[i]);   // zero this rank's slots
+      for (int k = 0; k < NTENS; ++k) {
+        if (!tensor_needed(cfg, k)) continue;
+        long long R, C;
+        tensor_rc(cfg, k, &R, &C);
+        for (int q = 0; q < arenas[i].world; ++q)
+          if (shard_rows(R, arenas[i].world, q) > 0)
+            EE_CUDA(cudaMemsetAsync(gs.p[k][q], 0, 4 * shard_rows(R, arenas[i].world, q) * C, st));
+      }
+    }
     EE_CUDA(cudaMemsetAsync(loss_out, 0, sizeof(float) * E, st));
     return EE_OK;
   }
   const bool nrm = cfg->arch != EE_ARCH_EMBEDDING;
   for (int i = 0; i < E; ++i) {
     const ee_head_tensors& P = params[i];
-    const ee_head_tensors& G = grads[i];
+    ee_head_tensors G0;
+    memset(&G0, 0, sizeof(G0));
+    const ee_head_tensors& G = arenas ? G0 : grads[i];
+    GradScatter gsv;
+    const GradScatter* gs = nullptr;
+    if (arenas) {
+      gsv = make_scatter(cfg, arenas[i]);
+      gs = &gsv;
+    }
     const __nv_bfloat16* x = (const __nv_bfloat16*)hidden[i];
     const __nv_bfloat16* z = nullptr;
     if ((s = phase_exit_forward(cfg, B, P, x, n, nullptr, &z, st)) != EE_OK) return s;
@@ -868,10 +971,52 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
         EE_CUDA(cudaMemcpyAsync(ax->weight_sum, B.wsum, sizeof(float), cudaMemcpyDeviceToDevice, st));
     }
     if ((s = phase_vocab_backward(cfg, B, P, G, z, n, targets, accumulate, nrm ? B.dz : nullptr,
-                                  st)) != EE_OK)
+                                  st, nullptr, gs)) != EE_OK)
       return s;
-    if ((s = phase_exit_backward(cfg, B, P, G, x, n, B.dz, accumulate, st)) != EE_OK) return s;
+    if ((s = phase_exit_backward(cfg, B, P, G, x, n, B.dz, accumulate, st, 1, gs)) != EE_OK)
+      return s;
   }
+  return EE_OK;
+}
+
+ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int64_t n_tokens,
+                       const int32_t* targets, const float* exit_weights,
+                       const ee_head_tensors* params, ee_head_tensors* grads, int32_t accumulate,
+                       float* loss_out, const ee_step_aux* aux, const int64_t* valid_count,
+                       void* workspace, size_t ws_bytes, void* stream) {
+  return tune_step_impl(cfg, hidden, n_tokens, targets, exit_weights, params, grads, nullptr,
+                        accumulate, loss_out, aux, valid_count, workspace, ws_bytes, stream);
+}
+
+ee_status ee_tune_step_rs(const ee_head_config* cfg, const void* const* hidden, int64_t n_tokens,
+                          const int32_t* targets, const float* exit_weights,
+                          const ee_head_tensors* params, const ee_peer_set* grad_arenas,
+                          float* loss_out, const ee_step_aux* aux, const int64_t* valid_count,
+                          void* workspace, size_t ws_bytes, void* stream) {
+  if (!grad_arenas) return fail(EE_ERR_ARG, "grad_arenas required");
+  if (cfg && cfg->arch == EE_ARCH_LAYER)
+    return fail(EE_ERR_UNSUPPORTED, "ee_tune_step_rs: Layer exits use ee_tune_step + all-reduce");
+  if (cfg && cfg->token_weighting != EE_WEIGHT_UNIFORM)
+    return fail(EE_ERR_UNSUPPORTED, "ee_tune_step_rs: uniform token weights only");
+  return tune_step_impl(cfg, hidden, n_tokens, targets, exit_weights, params, nullptr,
+                        grad_arenas, 0, loss_out, aux, valid_count, workspace, ws_bytes, stream);
+}
+
+ee_status ee_dp_shard_layout(const ee_head_config* cfg, int32_t world, int32_t rank,
+                             int32_t tensor, int64_t* row_begin, int64_t* rows,
+                             int64_t* arena_offset_floats, int64_t* arena_total_floats) {
+  ee_status s = check_cfg(cfg);
+  if (s != EE_OK) return s;
+  if (world < 1 || world > EE_MAX_PEERS || rank < 0 || rank >= world || tensor < 0 ||
+      tensor >= NTENS || !row_begin || !rows || !arena_offset_floats || !arena_total_floats)
+    return fail(EE_ERR_ARG, "bad ee_dp_shard_layout arguments");
+  long long R, C;
+  tensor_rc(cfg, tensor, &R, &C);
+  const bool need = tensor_needed(cfg, tensor);
+  *row_begin = need ? std::min<long long>(R, (long long)rank * shard_chunk(R, world)) : 0;
+  *rows = need ? shard_rows(R, world, rank) : 0;
+  *arena_offset_floats = arena_offset(cfg, world, rank, tensor);
+  *arena_total_floats = arena_offset(cfg, world, rank, NTENS);
   return EE_OK;
 }
 
@@ -1524,6 +1669,59 @@ ee_status ee_adam_update(const ee_head_config* cfg, ee_head_tensors* master, ee_
       EE_CUDA(launch_adam(mp, opb, opf, (const float*)(grads[i].*(ti.f)), (float*)(m[i].*(ti.f)),
                           (float*)(v[i].*(ti.f)), nel, lr, beta1, beta2, eps, wd, bc1, bc2,
                           grad_scale, st));
+    }
+  }
+  return EE_OK;
+}
+
+ee_status ee_adam_update_sharded(const ee_head_config* cfg, int32_t world, int32_t rank,
+                                const void* const* grad_arenas, ee_head_tensors* master_shard,
+                                ee_head_tensors* m_shard, ee_head_tensors* v_shard,
+                                const ee_peer_set* operands, float lr, float beta1, float beta2,
+                                float eps, float wd, int64_t step, float grad_scale,
+                                void* stream) {
+  ee_status s = check_cfg(cfg);
+  if (s != EE_OK) return s;
+  if (world < 1 || world > EE_MAX_PEERS || rank < 0 || rank >= world || !grad_arenas ||
+      !master_shard || !m_shard || !v_shard || !operands)
+    return fail(EE_ERR_ARG, "bad ee_adam_update_sharded arguments");
+  if (step < 1) return fail(EE_ERR_ARG, "step must be >= 1");
+  if ((s = check_device()) != EE_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  const float bc1 = (float)(1.0 - std::pow((double)beta1, (double)step));
+  const float bc2 = (float)(1.0 - std::pow((double)beta2, (double)step));
+  for (int i = 0; i < cfg->num_exits; ++i) {
+    if (!grad_arenas[i] || !aligned16(grad_arenas[i]))
+      return fail(EE_ERR_ALIGN, "grad_arenas[%d] NULL or misaligned", i);
+    for (int k = 0; k < NTENS; ++k) {
+      if (!tensor_needed(cfg, k)) continue;
+      long long R, C;
+      tensor_rc(cfg, k, &R, &C);
+      const long long rows = shard_rows(R, world, rank);
+      if (rows == 0) continue;
+      const TInfo& ti = kTens[k];
+      float* th = (float*)(master_shard[i].*(ti.f));
+      float* mm = (float*)(m_shard[i].*(ti.f));
+      float* vv = (float*)(v_shard[i].*(ti.f));
+      const ee_peer_set& op = operands[i * NTENS + k];
+      if (!th || !mm || !vv || !aligned16(th) || !aligned16(mm) || !aligned16(vv))
+        return fail(EE_ERR_ARG, "exit %d %s: shard tensors NULL or misaligned", i, ti.name);
+      if (op.world != world || op.rank != rank)
+        return fail(EE_ERR_ARG, "exit %d %s: operand peer set has wrong rank/world", i, ti.name);
+      OpPeers pp{};
+      pp.n = world;
+      pp.f32 = ti.gain ? 1 : 0;
+      for (int q = 0; q < world; ++q) {
+        if (!op.ptr[q] || !aligned16(op.ptr[q]))
+          return fail(EE_ERR_ALIGN, "exit %d %s: operand %d NULL or misaligned", i, ti.name, q);
+        pp.p[q] = op.ptr[q];
+      }
+      const float* slots = (const float*)grad_arenas[i] + arena_offset(cfg, world, rank, k);
+      const long long nel = rows * C;
+      Prof p_("a15_adam_sharded", st, 0, 0, (4.0 * world + 24.0 + 2.0 * world) * nel);
+      EE_CUDA(launch_adam_sharded(th, slots, world, mm, vv, nel, pp,
+                                  (long long)rank * shard_chunk(R, world) * C, lr, beta1, beta2,
+                                  eps, wd, bc1, bc2, grad_scale, st));
     }
   }
   return EE_OK;

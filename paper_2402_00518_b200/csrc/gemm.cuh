@@ -66,12 +66,16 @@ struct GemmArgs {
   int m_split;
   int n_split;  // EPI_F32T: output columns n >= n_split go to out1 (row n - n_split)
   int accumulate;
-  // EPI_F32 fused reduce-scatter (scat_rows > 0): output row m goes to
-  // scat[m / scat_rows] + scat_off + (m % scat_rows) * ldo (the token owner's
-  // slot for this rank, include/ee.h ee_vp_vocab_backward_rs); out0/out1 unused
+  // Fused reduce-scatter (scat_rows > 0; out0/out1 unused): stored row r of
+  // the output goes to the owner q = r / scat_rows of that row block, at
+  // scat[q] + (r - q * scat_rows) * ldo (scat1 for EPI_F32T rows >= n_split).
+  // The host folds this rank's slot offset into each pointer (include/ee.h
+  // ee_vp_vocab_backward_rs: dz rows to token owners; ee_tune_step_rs:
+  // gradient rows to parameter-shard owners).  EPI_F32: stored row = m;
+  // EPI_F32T: stored row = n.
   float* scat[8];
+  float* scat1[8];
   int scat_rows;
-  long long scat_off;
   const __nv_bfloat16* resid;
   long long ld_resid;
   __nv_bfloat16* outb;  // EPI_BF16 output (ldo)
@@ -137,7 +141,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
     if (row_ok) {
       if (EPI == EPI_F32 && args.scat_rows > 0) {
         const int q = gm / args.scat_rows;
-        orow = args.scat[q] + args.scat_off + (long long)(gm - q * args.scat_rows) * args.ldo;
+        orow = args.scat[q] + (long long)(gm - q * args.scat_rows) * args.ldo;
       } else {
         orow = (gm < args.m_split) ? args.out0 + (long long)gm * args.ldo
                                    : args.out1 + (long long)(gm - args.m_split) * args.ldo;
@@ -271,9 +275,16 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
         for (int j = 0; j < 32; ++j) {
           const int gn = gn0 + j;
           if (gn < args.N) {
-            float* o = (gn < args.n_split)
-                           ? args.out0 + (long long)gn * args.ldo + gm
-                           : args.out1 + (long long)(gn - args.n_split) * args.ldo + gm;
+            float* o;
+            if (args.scat_rows > 0) {  // fused reduce-scatter to the row-block owner
+              const bool hi = gn >= args.n_split;
+              const int r = hi ? gn - args.n_split : gn;
+              const int q = r / args.scat_rows;
+              o = (hi ? args.scat1[q] : args.scat[q]) + (long long)(r - q * args.scat_rows) * args.ldo + gm;
+            } else {
+              o = (gn < args.n_split) ? args.out0 + (long long)gn * args.ldo + gm
+                                      : args.out1 + (long long)(gn - args.n_split) * args.ldo + gm;
+            }
             const float val = u2f(v[j]);
             *o = args.accumulate ? *o + val : val;
           }

@@ -154,6 +154,16 @@ cudaError_t launch_cast_bf16_f32(const __nv_bfloat16* a, float* b, long long n, 
 cudaError_t launch_cast_f32_bf16(const float* a, __nv_bfloat16* b, long long n, cudaStream_t s);
 
 // optimizer / init
+struct OpPeers {  // every rank's operand tensor of one parameter (bf16, or fp32 if f32)
+  void* p[MAX_PEERS];
+  int n;
+  int f32;
+};
+// sharded Adam: grad = rank-ordered sum of P slots [P][n]; operand rows to all ranks
+cudaError_t launch_adam_sharded(float* theta, const float* slots, int P, float* m, float* v,
+                                long long n, const OpPeers& op, long long off, float lr, float b1,
+                                float b2, float eps, float wd, float bc1, float bc2, float gs,
+                                cudaStream_t s);
 cudaError_t launch_adam(float* theta, __nv_bfloat16* op_bf16, float* op_f32, const float* grad,
                         float* m, float* v, long long n, float lr, float b1, float b2, float eps,
                         float wd, float bc1, float bc2, float gscale, cudaStream_t s);

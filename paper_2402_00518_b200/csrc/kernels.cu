@@ -700,6 +700,65 @@ __global__ void adam_kernel(float* __restrict__ th, __nv_bfloat16* op_bf16, floa
   }
 }
 
+// Sharded Adam of the fused data-parallel path (ZeRO-1; include/ee.h
+// ee_adam_update_sharded): this rank owns n4*4 elements of one tensor.  Its
+// gradient is the rank-ordered sum of the P slots [P][n] that every rank's
+// backward stored here (the reduce-scatter's owner-side sum), the update is
+// adam_kernel's arithmetic, and the new operand values (bf16 matrices / fp32
+// gains) are stored into every rank's operand tensor at element offset off4*4
+// (the all-gather, as NVLink stores).
+__global__ void adam_sharded_kernel(float* __restrict__ th, const float* __restrict__ slots,
+                                    int P, float* __restrict__ m, float* __restrict__ v,
+                                    long long n4, OpPeers op, long long off4, float lr, float b1,
+                                    float b2, float eps, float wd, float bc1, float bc2,
+                                    float gs) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    float4 t = reinterpret_cast<float4*>(th)[i];
+    float4 g4 = reinterpret_cast<const float4*>(slots)[i];
+    for (int r = 1; r < P; ++r) {
+      const float4 e = reinterpret_cast<const float4*>(slots)[(long long)r * n4 + i];
+      g4.x += e.x; g4.y += e.y; g4.z += e.z; g4.w += e.w;
+    }
+    float4 m4 = reinterpret_cast<float4*>(m)[i];
+    float4 v4 = reinterpret_cast<float4*>(v)[i];
+    float* tp = &t.x;
+    const float* gp = &g4.x;
+    float* mp = &m4.x;
+    float* vp = &v4.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float g = gs * gp[k];
+      mp[k] = b1 * mp[k] + (1.f - b1) * g;
+      vp[k] = b2 * vp[k] + (1.f - b2) * g * g;
+      const float upd = (mp[k] / bc1) / (sqrtf(vp[k] / bc2) + eps);
+      tp[k] = tp[k] - lr * upd - lr * wd * tp[k];
+    }
+    reinterpret_cast<float4*>(th)[i] = t;
+    reinterpret_cast<float4*>(m)[i] = m4;
+    reinterpret_cast<float4*>(v)[i] = v4;
+    if (op.f32) {
+      for (int q = 0; q < op.n; ++q) reinterpret_cast<float4*>(op.p[q])[off4 + i] = t;
+    } else {
+      uint2 w;
+      w.x = pack_bf16(t.x, t.y);
+      w.y = pack_bf16(t.z, t.w);
+      for (int q = 0; q < op.n; ++q) reinterpret_cast<uint2*>(op.p[q])[off4 + i] = w;
+    }
+  }
+}
+
+cudaError_t launch_adam_sharded(float* theta, const float* slots, int P, float* m, float* v,
+                                long long n, const OpPeers& op, long long off, float lr, float b1,
+                                float b2, float eps, float wd, float bc1, float bc2, float gs,
+                                cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const long long n4 = n / 4;
+  adam_sharded_kernel<<<ew_blocks(n4), 256, 0, s>>>(theta, slots, P, m, v, n4, op, off / 4, lr,
+                                                    b1, b2, eps, wd, bc1, bc2, gs);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_adam(float* theta, __nv_bfloat16* op_bf16, float* op_f32, const float* grad,
                         float* m, float* v, long long n, float lr, float b1, float b2, float eps,
                         float wd, float bc1, float bc2, float gscale, cudaStream_t s) {

@@ -78,6 +78,191 @@ def data_parallel_step(n_exits: int, count_local: Callable[[], torch.Tensor] | N
 
 
 # ---------------------------------------------------------------------------
+# Data parallel with the gradient reduce-scatter fused into the weight-gradient
+# GEMMs and a sharded Adam whose operand stores are the all-gather (ZeRO-1)
+# ---------------------------------------------------------------------------
+
+def _peer_tables(rank, local_tensors, group=None, ranks=None):
+    """Per-tensor peer pointer lists: from the other ranks' objects (ranks, one
+    process) or by exchanging CUDA IPC handles over the process group.
+    Returns (tables, opened) with tables[j] = [ptr of rank q's tensor j]."""
+    import paper_2402_00518_b200 as ee
+    if ranks is not None:
+        return [[r_tensors[j].data_ptr() for r_tensors in ranks]
+                for j in range(len(local_tensors))], []
+    world = dist.get_world_size(group)
+    mine = [ee.ee_ipc_get_handle(t) for t in local_tensors]
+    allh = [None] * world
+    dist.all_gather_object(allh, mine, group=group)
+    tabs, opened = [], []
+    for j, t in enumerate(local_tensors):
+        row = []
+        for q in range(world):
+            if q == rank:
+                row.append(t.data_ptr())
+            else:
+                p = ee.ee_ipc_open(*allh[q][j])
+                opened.append((p, allh[q][j][1]))
+                row.append(p)
+        tabs.append(row)
+    return tabs, opened
+
+
+class ShardedDPHeads:
+    """Exit heads of one rank under the fused data-parallel path
+    (include/ee.h ee_tune_step_rs / ee_adam_update_sharded).
+
+    Every rank holds the full bf16 operands (fp32 gains) of every exit, but
+    only its row shard of the fp32 masters and Adam moments (1/P of the
+    optimizer state), and `n_arenas` gradient arenas in which the other ranks'
+    weight-gradient GEMMs deposit their partials of this rank's rows.  step():
+    exit by exit, tune with the gradient rows routed to their owners,
+    peer barrier, sharded Adam that stores the new operand rows into every
+    rank -- no NCCL on the bulk path; only the valid-token count and the
+    per-exit losses (8 B each) use `comm_all_reduce`."""
+
+    def __init__(self, spec, max_tokens: int, rank: int, world: int, device="cuda",
+                 n_arenas: int = 2):
+        import paper_2402_00518_b200 as ee
+        self.ee, self.spec, self.rank, self.world = ee, spec, rank, world
+        self.cfg = ee.make_config(spec.hidden, spec.vocab, spec.ffn, spec.num_exits, spec.arch,
+                                  spec.norm_eps)
+        self.exit_cfg = ee.make_config(spec.hidden, spec.vocab, spec.ffn, 1, spec.arch,
+                                       spec.norm_eps)
+        shapes = ee.tensor_shapes(spec.hidden, spec.vocab, spec.ffn, spec.arch)
+        self.names = [k for k in ee.TENSOR_NAMES if k in shapes]
+        self.shapes = shapes
+        dev = torch.device(device)
+        E = spec.num_exits
+        self.layout = {k: ee.ee_dp_shard_layout(self.exit_cfg, world, rank, k)
+                       for k in self.names}
+        total = self.layout[self.names[0]][3]
+
+        def shard(k):
+            rows = self.layout[k][1]
+            C = shapes[k][-1]
+            return torch.zeros(rows, C, dtype=torch.float32, device=dev)
+
+        self.operand = [{k: torch.zeros(shapes[k], device=dev,
+                                        dtype=torch.float32 if k.startswith("g_")
+                                        else torch.bfloat16) for k in self.names}
+                        for _ in range(E)]
+        self.master = [{k: shard(k) for k in self.names} for _ in range(E)]
+        self.m = [{k: shard(k) for k in self.names} for _ in range(E)]
+        self.v = [{k: shard(k) for k in self.names} for _ in range(E)]
+        self.n_arenas = max(1, min(int(n_arenas), E))
+        self.arenas = [torch.zeros(total, dtype=torch.float32, device=dev)
+                       for _ in range(self.n_arenas)]
+        self.sig = torch.zeros(8, dtype=torch.int32, device=dev)
+        self.epoch = 0
+        self.workspace = torch.zeros(ee.ee_workspace_size(self.cfg, max_tokens),
+                                     dtype=torch.uint8, device=dev)
+        self.loss = torch.zeros(E, dtype=torch.float32, device=dev)
+        self.step_count = 0
+        self._opened = []
+
+    def _locals(self):
+        ts = list(self.arenas) + [self.sig]
+        for d in self.operand:
+            ts += [d[k] for k in self.names]
+        return ts
+
+    def _set_tables(self, tabs):
+        ee = self.ee
+        na = self.n_arenas
+        self.arena_sets = [ee.peer_set(self.rank, tabs[j]) for j in range(na)]
+        self.sig_set = ee.peer_set(self.rank, tabs[na])
+        nt = len(self.names)
+        self.operand_sets = [{k: ee.peer_set(self.rank, tabs[na + 1 + i * nt + j])
+                              for j, k in enumerate(self.names)}
+                             for i in range(self.spec.num_exits)]
+
+    def connect_local(self, ranks: list["ShardedDPHeads"]):
+        tabs, _ = _peer_tables(self.rank, self._locals(), ranks=[r._locals() for r in ranks])
+        self._set_tables(tabs)
+
+    def connect_ipc(self, group=None):
+        tabs, self._opened = _peer_tables(self.rank, self._locals(), group=group)
+        self._set_tables(tabs)
+
+    def close(self):
+        for p, off in self._opened:
+            self.ee.ee_ipc_close(p, off)
+        self._opened = []
+
+    def init(self, mode="copy", copy_src=None, seed=0, std=0.02, src_dtype=torch.bfloat16):
+        """Initialise through full-size fp32 staging masters (Copy and Random
+        are deterministic, so every rank builds the same operands) and keep
+        this rank's rows.  Copy stages one exit at a time; Random stages all
+        exits at once (its streams are keyed by exit index)."""
+        ee = self.ee
+        dev = self.loss.device
+        E = self.spec.num_exits
+
+        def staging():
+            return {k: torch.zeros(self.shapes[k], dtype=torch.float32, device=dev)
+                    for k in self.names}
+
+        def keep(i, full):
+            for k in self.names:
+                b, rows = self.layout[k][0], self.layout[k][1]
+                if rows:
+                    self.master[i][k].copy_(full[k].reshape(-1, self.shapes[k][-1])[b:b + rows])
+                if k.startswith("g_"):
+                    self.operand[i][k].copy_(full[k])
+
+        if mode == "random":
+            full = [staging() for _ in range(E)]
+            ee.ee_init_heads(self.cfg, "random", None, full, self.operand, seed=seed, std=std)
+            for i in range(E):
+                keep(i, full[i])
+            return
+        for i in range(E):
+            full = staging()
+            ee.ee_init_heads(self.exit_cfg, mode, copy_src[i:i + 1], [full],
+                             self.operand[i:i + 1], src_dtype=src_dtype)
+            keep(i, full)
+            del full
+
+    def barrier(self, stream=None):
+        self.epoch += 1
+        self.ee.ee_peer_barrier(self.sig_set, self.epoch, self.workspace, stream)
+
+    def status(self):
+        return self.ee.ee_get_status(self.workspace)
+
+    def step(self, hidden, targets, lr, all_reduce=None, exit_weights=None, beta1=0.9,
+             beta2=0.95, eps=1e-5, weight_decay=0.0):
+        """One tuning step + Adam on this rank's tokens.  all_reduce(t) sums a
+        small tensor over the ranks in place (the valid-token count before the
+        step, the per-exit losses after); None = one rank."""
+        ee = self.ee
+        E = self.spec.num_exits
+        w = exit_weights if exit_weights is not None else [1.0] * E
+        W = torch.zeros(1, dtype=torch.int64, device=self.loss.device)
+        ee.ee_count_valid(targets, self.spec.vocab, W, self.workspace)
+        if all_reduce is not None:
+            all_reduce(W)
+        self.step_count += 1
+        self.barrier()                       # previous update's operand stores are complete
+        for i in range(E):
+            j = i % self.n_arenas
+            ee.ee_tune_step_rs(self.exit_cfg, hidden[i:i + 1], targets, w[i:i + 1],
+                               self.operand[i:i + 1], [self.arena_sets[j]],
+                               self.loss[i:i + 1], self.workspace, valid_count=W)
+            self.barrier()                   # every rank's partials of exit i have landed
+            ee.ee_adam_update_sharded(self.exit_cfg, self.world, self.rank, [self.arenas[j]],
+                                      self.master[i:i + 1], self.m[i:i + 1], self.v[i:i + 1],
+                                      self.operand_sets[i:i + 1], lr, self.step_count, beta1,
+                                      beta2, eps, weight_decay)
+            if self.n_arenas == 1 and i + 1 < E:
+                self.barrier()               # arena read by every owner before it is rewritten
+        if all_reduce is not None:
+            all_reduce(self.loss)
+        return self.loss
+
+
+# ---------------------------------------------------------------------------
 # Vocab-parallel W_out (BASELINE configs[3]: "vocab-parallel W_out over 8 GPUs")
 # ---------------------------------------------------------------------------
 
