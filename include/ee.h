@@ -358,7 +358,11 @@ ee_status ee_peer_barrier(const ee_peer_set* signals, uint32_t epoch, void* work
  * update complete); and before an arena is written again (2 arenas
  * alternating exits need no extra barrier).  Results are bitwise equal to
  * ee_tune_step + a rank-ordered fp32 all-reduce + ee_adam_update.
- * Uniform token weights, Embedding/Norm/MLP exits (Layer: EE_ERR_UNSUPPORTED). */
+ * Uniform token weights, Embedding/Norm/MLP exits (Layer: EE_ERR_UNSUPPORTED).
+ * Ranks sharing one process (tests): CUDA loads kernels lazily and a load
+ * waits for the context's running kernels, so one rank's first launch of a
+ * kernel can wait on another rank's spinning barrier; run one world-1 step
+ * first (or CUDA_MODULE_LOADING=EAGER).  One process per GPU is unaffected. */
 ee_status ee_dp_shard_layout(const ee_head_config* cfg, int32_t world, int32_t rank,
                              int32_t tensor, int64_t* row_begin, int64_t* rows,
                              int64_t* arena_offset_floats, int64_t* arena_total_floats);

@@ -1,4 +1,5 @@
 // gemm.cu -- host side of the tcgen05 GEMM: TMA descriptors and dispatch.
+#include <atomic>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdlib>
@@ -55,11 +56,17 @@ bool make_tmap(CUtensorMap* m, const Mat& t, uint32_t box_inner, uint32_t box_ou
 // zeroed on the launch's stream right before the launch that uses it.
 constexpr int kTileCounters = 4096;
 __device__ int g_tile_ctr[kTileCounters];
+// Thread-safe: several host threads (ranks sharing a process, or one stream
+// per thread) may launch concurrently; a slot is reused only after 4096 launches.
 static int* tile_counter(cudaStream_t st) {
-  static int* base = nullptr;
-  static unsigned next = 0;
-  if (!base && cudaGetSymbolAddress((void**)&base, g_tile_ctr) != cudaSuccess) return nullptr;
-  int* c = base + (next++ % kTileCounters);
+  static std::atomic<int*> base{nullptr};
+  static std::atomic<unsigned> next{0};
+  int* b = base.load();
+  if (!b) {
+    if (cudaGetSymbolAddress((void**)&b, g_tile_ctr) != cudaSuccess) return nullptr;
+    base.store(b);
+  }
+  int* c = b + (next.fetch_add(1) % kTileCounters);
   if (cudaMemsetAsync(c, 0, sizeof(int), st) != cudaSuccess) return nullptr;
   return c;
 }

@@ -103,6 +103,15 @@ def run_threads(ee, cfg, P, hidden, targets, params, fused, steps=2, n_arenas=2)
     return out
 
 
+def _warm(ee, cfg, hidden, targets, params):
+    """One world-1 fused step first.  CUDA loads kernels lazily, and loading
+    a kernel waits for the context's running kernels: with all emulated ranks
+    in ONE context, a rank's first launch of a kernel would wait for another
+    rank's spinning peer barrier, which waits for that first rank (deadlock
+    until the barrier's timeout).  One process per GPU has no such cycle."""
+    run_threads(ee, cfg, 1, hidden, targets, params, fused=True, steps=1)
+
+
 @pytest.mark.parametrize("arch,P,n_arenas", [("mlp", 2, 2), ("mlp", 4, 2), ("norm", 4, 2),
                                              ("embedding", 2, 2), ("mlp", 1, 2), ("mlp", 3, 1),
                                              ("mlp", 8, 2)])
@@ -114,6 +123,7 @@ def test_fused_dp_bitwise_equals_allreduce_path(gpu_lib, arch, P, n_arenas):
     targets = S.targets(cfg, N)
     params = S.head_params(cfg)
     ref = run_threads(ee, cfg, P, hidden, targets, params, fused=False)
+    _warm(ee, cfg, hidden, targets, params)
     fus = run_threads(ee, cfg, P, hidden, targets, params, fused=True, n_arenas=n_arenas)
     for r in range(P):
         assert fus[r][4] == (0, -1), fus[r][4]
