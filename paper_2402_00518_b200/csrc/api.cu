@@ -702,9 +702,17 @@ ee_status phase_exit_forward(const ee_head_config* cfg, const Bufs& B, const ee_
 }
 
 // a5: per-V-tile online-softmax partials of S = z W_out^T (logits never stored).
+// a7 strategy: the a5 epilogue stores P~ = exp(S - tile max) (fp16) into the dS
+// buffer and a7 is an elementwise pass (default), or (EE_DS_RECOMPUTE=1) a7
+// recomputes S with a second GEMM (the FlashAttention-style recompute).
+static bool ds_recompute() {
+  static const int v = getenv("EE_DS_RECOMPUTE") ? atoi(getenv("EE_DS_RECOMPUTE")) : 0;
+  return v != 0;
+}
+
 ee_status phase_vocab_stats(const ee_head_config* cfg, const Bufs& B, const ee_head_tensors& P,
                             const __nv_bfloat16* z, long long n, const int32_t* targets,
-                            cudaStream_t st) {
+                            cudaStream_t st, bool store_p = false) {
   const int h = cfg->hidden, Vl = cfg->vocab_end - cfg->vocab_begin;
   GemmArgs a = base_args((int)n, Vl, h);
   a.targets = targets;
@@ -713,8 +721,13 @@ ee_status phase_vocab_stats(const ee_head_config* cfg, const Bufs& B, const ee_h
   a.part_s = B.ps;
   a.part_i = B.pi;
   a.tgt_logit = B.tgt;
+  if (store_p && !ds_recompute()) {
+    a.ds = B.ds;
+    a.ld_ds = Vl;
+  }
   Mat A{z, n, h, h}, Bm{P.w_out, Vl, h, h};
-  Prof p_("a5_vocab_ce_stats", st, 2.0 * n * Vl * h, 2.0 * n * Vl * h, 0);
+  Prof p_("a5_vocab_ce_stats", st, 2.0 * n * Vl * h, 2.0 * n * Vl * h,
+          a.ds ? 2.0 * n * Vl : 0.0);
   EE_CUDA(gemm_run(EPI_CE_STATS, true, true, A, Bm, nullptr, B_PLAIN, 0, a, st));
   return EE_OK;
 }
@@ -726,7 +739,11 @@ ee_status phase_vocab_backward(const ee_head_config* cfg, const Bufs& B, const e
                                cudaStream_t st, const ee_peer_set* rs = nullptr,
                                const GradScatter* gs = nullptr) {
   const int h = cfg->hidden, Vl = cfg->vocab_end - cfg->vocab_begin;
-  {
+  if (!ds_recompute()) {  // a7: dS from the stored P~ (elementwise, in place)
+    Prof p_("a7_ds_from_p", st, 0, 0, 4.0 * n * Vl);
+    EE_CUDA(launch_ce_ds_from_p(B.ds, Vl, n, B.pm, B.lse, B.coef, targets, cfg->vocab_begin,
+                                B.tgt, st));
+  } else {
     GemmArgs a = base_args((int)n, Vl, h);
     a.targets = targets;
     a.vocab_begin = cfg->vocab_begin;
@@ -948,7 +965,7 @@ static ee_status tune_step_impl(const ee_head_config* cfg, const void* const* hi
     const __nv_bfloat16* x = (const __nv_bfloat16*)hidden[i];
     const __nv_bfloat16* z = nullptr;
     if ((s = phase_exit_forward(cfg, B, P, x, n, nullptr, &z, st)) != EE_OK) return s;
-    if ((s = phase_vocab_stats(cfg, B, P, z, n, targets, st)) != EE_OK) return s;
+    if ((s = phase_vocab_stats(cfg, B, P, z, n, targets, st, true)) != EE_OK) return s;
     // a6: lse, coef, per-token aux, L_i
     {
       const ee_step_aux* ax = aux ? &aux[i] : nullptr;
@@ -1336,7 +1353,7 @@ ee_status ee_vp_vocab_stats(const ee_head_config* cfg, const void* z_all, int64_
   { Prof p_("count_valid", st, 0, 0, 4.0 * n_all);
   EE_CUDA(launch_count_valid(targets_all, n_all, cfg->vocab, B.vcount, B.status, st)); }
   if ((s = phase_vocab_stats(cfg, B, *params, (const __nv_bfloat16*)z_all, n_all, targets_all,
-                             st)) != EE_OK)
+                             st, true)) != EE_OK)
     return s;
   Prof p_("vp_local_merge", st, 0, 0, 12.0 * B.L.nb * n_all + 20.0 * n_all);
   EE_CUDA(launch_vp_local_merge(B.pm, B.ps, B.pi, B.tgt, targets_all, B.L.nb, n_all,

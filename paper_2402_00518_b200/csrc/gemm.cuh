@@ -19,6 +19,7 @@
 //              what makes the online-softmax statistics shuffle-free.
 #pragma once
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 #include "ptx.cuh"
 
 namespace ee {
@@ -390,8 +391,13 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
       }
     }
   } else if constexpr (EPI == EPI_CE_STATS) {
+    // Pass 1: the row's max (lowest index on ties), argmax and target logit
+    // over the tile's 256 columns.  Pass 2: sum exp(S - max) and, when
+    // args.ds is set, store P~ = exp(S - max) as fp16 into the dS buffer, so
+    // the backward forms dS = coef (P~ exp(max - lse) - onehot) elementwise
+    // (launch_ce_ds_from_p) instead of recomputing S with a second GEMM.
     const int yl = row_ok ? args.targets[gm] - args.vocab_begin : -1;
-    float mx = -INFINITY, sm = 0.0f, tl = 0.0f;
+    float mx = -INFINITY, tl = 0.0f;
     int am = 0;
     bool has_t = false;
 #pragma unroll 1
@@ -400,30 +406,51 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
       tmem_ld_32x32b_x32(tb + c * 32, v);
       tmem_ld_wait();
       const int gn0 = nb * GEMM_BN + c * 32;
-      float cmax = -INFINITY;
-      int cidx = 0;
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const float x = u2f(v[j]);
-        const bool ok = gn0 + j < args.N;
-        if (ok && x > cmax) {
-          cmax = x;
-          cidx = gn0 + j;
+        if (gn0 + j < args.N && x > mx) {
+          mx = x;
+          am = gn0 + j;
         }
         if (gn0 + j == yl) {
           tl = x;
           has_t = true;
         }
       }
-      if (cmax > mx) {
-        sm *= __expf(mx - cmax);
-        mx = cmax;
-        am = cidx;
-      }
+    }
+    float sm = 0.0f;
+    __half* prow = (row_ok && args.ds) ? reinterpret_cast<__half*>(args.ds) + (long long)gm * args.ld_ds
+                                       : nullptr;
+#pragma unroll 1
+    for (int c = 0; c < GEMM_BN / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tb + c * 32, v);
+      tmem_ld_wait();
+      const int gn0 = nb * GEMM_BN + c * 32;
       float cs = 0.0f;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        if (gn0 + j < args.N) cs += __expf(u2f(v[j]) - mx);
+      for (int j = 0; j < 32; j += 16) {
+        uint32_t w[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int c0 = gn0 + j + 2 * q;
+          const float e0 = c0 < args.N ? __expf(u2f(v[j + 2 * q]) - mx) : 0.0f;
+          const float e1 = c0 + 1 < args.N ? __expf(u2f(v[j + 2 * q + 1]) - mx) : 0.0f;
+          cs += e0 + e1;
+          const __half2 hp = __floats2half2_rn(e0, e1);
+          w[q] = *reinterpret_cast<const uint32_t*>(&hp);
+        }
+        if (prow != nullptr && gn0 + j < args.N) {
+          __half* pd = prow + gn0 + j;
+          if (gn0 + j + 16 <= args.N && aligned32(pd)) {
+            st_global_v8(pd, w);
+          } else {
+            *reinterpret_cast<uint4*>(pd) = make_uint4(w[0], w[1], w[2], w[3]);
+            if (gn0 + j + 8 < args.N)
+              *reinterpret_cast<uint4*>(pd + 8) = make_uint4(w[4], w[5], w[6], w[7]);
+          }
+        }
       }
       sm += cs;
     }

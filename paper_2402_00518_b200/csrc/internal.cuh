@@ -77,6 +77,10 @@ cudaError_t launch_ce_finalize(const float* pm, const float* ps, const int32_t* 
                                cudaStream_t s);
 // wsum_part != NULL: confidence weighting (L = sum w loss / sum w, written to wsum_out)
 // normalize = false: L = sum w loss (the normaliser is applied by the caller later)
+// a7 from the fp16 P~ the a5 epilogue stored in ds: in place -> bf16 dS
+cudaError_t launch_ce_ds_from_p(__nv_bfloat16* ds, int Vl, long long n, const float* pm,
+                                const float* lse, const float* coef, const int32_t* targets,
+                                int vocab_begin, const float* tgt_logit, cudaStream_t s);
 cudaError_t launch_loss_reduce(const float* loss_part, int nparts, const long long* valid_count,
                                const float* wsum_part, float* wsum_out, float* loss_out,
                                DevStatus* st, int exit_index, cudaStream_t s,

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <climits>
+#include <cuda_fp16.h>
 #include "internal.cuh"
 
 namespace ee {
@@ -398,6 +399,55 @@ cudaError_t launch_ce_finalize(const float* pm, const float* ps, const int32_t* 
                                                           valid_count, alpha, lse, coef, aux_lse,
                                                           aux_loss, aux_argmax, aux_conf,
                                                           loss_part, wsum_part);
+  return cudaGetLastError();
+}
+
+// a7 without a second GEMM: the a5 epilogue stored P~[t][v] = exp(S_tv - m_tj)
+// (fp16, m_tj = row t's max over its 256-column tile j, kept in pm[j][t]);
+// here, in place, dS_tv = coef_t (P~_tv exp(m_tj - lse_t) - 1[v = y_t]) as
+// bf16 (the softmax-CE gradient; coef_t = alpha w_t / W).  The target
+// column is recomputed from the fp32 target logit, exp(S_ty - lse_t) - 1, so
+// confident rows (p_y -> 1) keep full relative precision.  One CTA per row,
+// 16-byte accesses.
+__global__ void ce_ds_from_p_kernel(__nv_bfloat16* __restrict__ ds, int Vl, long long n,
+                                    const float* __restrict__ pm, const float* __restrict__ lse,
+                                    const float* __restrict__ coef,
+                                    const int32_t* __restrict__ targets, int vocab_begin,
+                                    const float* __restrict__ tgt_logit) {
+  const long long row = blockIdx.x;
+  const float l = lse[row], cf = coef[row];
+  const int y = targets[row] - vocab_begin;
+  __nv_bfloat16* drow = ds + row * (long long)Vl;
+  const int nch = Vl / 8;
+  for (int c = threadIdx.x; c < nch; c += blockDim.x) {
+    const int j = c >> 5;  // 256-column tile of these 8 columns
+    const float f = cf * __expf(pm[(long long)j * n + row] - l);
+    const uint4 q = *reinterpret_cast<const uint4*>(drow + c * 8);
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+    float d[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 p2 = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
+      d[2 * k] = f * p2.x;
+      d[2 * k + 1] = f * p2.y;
+    }
+    const int yo = y - c * 8;
+    if (yo >= 0 && yo < 8) d[yo] = cf * (__expf(tgt_logit[row] - l) - 1.0f);
+    uint4 o;
+    o.x = pack_bf16(d[0], d[1]);
+    o.y = pack_bf16(d[2], d[3]);
+    o.z = pack_bf16(d[4], d[5]);
+    o.w = pack_bf16(d[6], d[7]);
+    *reinterpret_cast<uint4*>(drow + c * 8) = o;
+  }
+}
+
+cudaError_t launch_ce_ds_from_p(__nv_bfloat16* ds, int Vl, long long n, const float* pm,
+                                const float* lse, const float* coef, const int32_t* targets,
+                                int vocab_begin, const float* tgt_logit, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  ce_ds_from_p_kernel<<<(unsigned)n, 256, 0, s>>>(ds, Vl, n, pm, lse, coef, targets, vocab_begin,
+                                                 tgt_logit);
   return cudaGetLastError();
 }
 
