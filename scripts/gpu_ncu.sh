@@ -2,8 +2,8 @@
 TAG=${1:-r01}
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv \
     python bench.py --quick --steps 1 --warmup 0 > gpurun_out/ncu_launch_$TAG.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:gemm -s 0 -c 10 \
+ncu --set full --clock-control none --import-source on -k regex:gemm -s 0 -c 9 \
     -o gpurun_out/prof_gemm_$TAG python bench.py --quick --steps 1 --warmup 0 > gpurun_out/ncu_full_$TAG.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"rmsnorm|adam|gain_grad|ce_finalize" -s 0 -c 8 \
+ncu --set full --clock-control none --import-source on -k regex:"rmsnorm|adam|gain_grad|ce_finalize|ce_ds_from_p|transpose" -s 0 -c 12 \
     -o gpurun_out/prof_bw_$TAG python bench.py --quick --steps 1 --warmup 0 > gpurun_out/ncu_bw_$TAG.log 2>&1
 ls -la gpurun_out/

@@ -246,3 +246,29 @@ def test_confidence_weighting_data_parallel_shards(gpu_lib, arch):
     from harness import rel_fro
     for k, gk in res.grads.items():
         assert rel_fro(tot_g[k].double().cpu().numpy(), gk) <= 2e-2, k
+
+
+@pytest.mark.parametrize("scale", [64.0, 256.0])
+def test_confident_rows_ds_precision(gpu_lib, scale):
+    """Peaked softmax rows (p_y -> 1, the regime of a well-tuned exit): a7
+    forms dS from the fp16 P~ the a5 epilogue stored, except the target
+    column, which is recomputed from the fp32 target logit; the gradients of
+    these small-gradient rows must still meet the tolerance.  W_out is scaled
+    (by powers of two: the operands stay on the bf16 grid) so the logits
+    spread widely, and the targets are the oracle's argmax."""
+    cfg = S.Cfg(name="small", hidden=128, vocab=1000, ffn=256, arch="mlp", tokens=300, layers=2,
+                after=[1, 2], init="random", seed=12)
+    hidden = S.hidden_states(cfg, 300, seed=3)
+    params = S.head_params(cfg, seed=3)
+    for p in params:
+        p["w_out"] = p["w_out"] * scale
+    t0 = S.targets(cfg, 300, seed=3)
+    res0 = oracle_exit("mlp", params[0], hidden[0], t0, 1.0)
+    targets = torch.from_numpy(np.argmax(res0.act["S"], axis=1).astype(np.int32))
+    loss, grads, aux, status = gpu_step(gpu_lib, cfg, hidden[:1], targets, params[:1], [1.0])
+    assert status == (0, -1)
+    res = oracle_exit("mlp", params[0], hidden[0], targets, 1.0)
+    p_y = np.exp(-res.stats["loss"])
+    assert np.median(p_y) > 0.5                      # the regime under test
+    errs = compare_exit("mlp", res, loss[0].item(), grads[0], aux[0], targets, tag=f"conf{scale}")
+    print(scale, res.loss, float(np.median(p_y)), errs)
