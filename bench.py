@@ -358,12 +358,12 @@ def main():
     gbuf = args.grad_buffers if args.grad_buffers >= 0 else (2 if E > 4 else 0)
     if vp:
         gbuf = 0
-    dp_fused = cfg.arch != "layer" and not vp and (
+    dp_fused = not vp and (
         (dp and args.dp_comm == "fused") or args.force_dp_fused)
     heads = None
     if dp_fused:     # gradient reduce-scatter in the GEMM epilogues + sharded Adam (ZeRO-1)
-        heads = ShardedDPHeads(ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch), n,
-                               rank, world, device=dev)
+        heads = ShardedDPHeads(ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch,
+                                           **attn_kw(cfg)), n, rank, world, device=dev)
         err = None
         try:
             if world > 1:

@@ -358,7 +358,7 @@ ee_status ee_peer_barrier(const ee_peer_set* signals, uint32_t epoch, void* work
  * update complete); and before an arena is written again (2 arenas
  * alternating exits need no extra barrier).  Results are bitwise equal to
  * ee_tune_step + a rank-ordered fp32 all-reduce + ee_adam_update.
- * Uniform token weights, Embedding/Norm/MLP exits (Layer: EE_ERR_UNSUPPORTED).
+ * Uniform token weights; every arch (Layer: also W_q, W_k, W_v, W_o, g_att).
  * Ranks sharing one process (tests): CUDA loads kernels lazily and a load
  * waits for the context's running kernels, so one rank's first launch of a
  * kernel can wait on another rank's spinning barrier; run one world-1 step

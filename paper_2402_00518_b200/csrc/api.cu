@@ -525,9 +525,13 @@ ee_status layer_attn_forward(const ee_head_config* cfg, const Bufs& B, const ee_
 // fused into its dq / dk stores;
 // L10 dW_{q,k,v} = d{q,k,v}^T u1; L11 du1 = dq W_q + dk W_k + dv W_v;
 // L12 dg_att = sum du1 * xhat1 (no dx: frozen backbone).
+struct GradScatter;
+static void set_scatter(GemmArgs& a, const GradScatter* gs, int k, int k1);
+static float* scatter_gain(const GradScatter* gs, int k);
+
 ee_status layer_attn_backward(const ee_head_config* cfg, const Bufs& B, const ee_head_tensors& P,
                               const ee_head_tensors& G, const __nv_bfloat16* x, long long n,
-                              int accumulate, cudaStream_t st) {
+                              int accumulate, cudaStream_t st, const GradScatter* gs = nullptr) {
   const int h = cfg->hidden, Hq = cfg->n_heads, Hkv = cfg->n_kv_heads, hkv = 128 * Hkv;
   const int nparts = (int)((n + NORM_RPB - 1) / NORM_RPB);
   {  // L6: dW_o = dx1^T o  (A = dx1^T K-major copy, B = o MN-major)
@@ -537,6 +541,7 @@ ee_status layer_attn_backward(const ee_head_config* cfg, const Bufs& B, const ee
     a.out0 = (float*)G.w_o;
     a.ldo = h;
     a.accumulate = accumulate;
+    if (gs) set_scatter(a, gs, 10, -1);
     Mat A{B.dyT, h, n, B.L.ldT}, Bm{B.o, n, h, h};
     Prof p_("L6_dw_o", st, 2.0 * n * h * h, 2.0 * n * h * h, 0);
     EE_CUDA(gemm_run(EPI_F32, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
@@ -563,15 +568,17 @@ ee_status layer_attn_backward(const ee_head_config* cfg, const Bufs& B, const ee
     const void* w;
     int N;
     const char *name, *dname;
-  } wg[3] = {{B.dq, G.w_q, P.w_q, h, "L10_dw_q", "L11_du1_q"},
-             {B.dk, G.w_k, P.w_k, hkv, "L10_dw_k", "L11_du1_k"},
-             {B.dv, G.w_v, P.w_v, hkv, "L10_dw_v", "L11_du1_v"}};
+    int k;  // tensor index (ee_head_tensors order)
+  } wg[3] = {{B.dq, G.w_q, P.w_q, h, "L10_dw_q", "L11_du1_q", 7},
+             {B.dk, G.w_k, P.w_k, hkv, "L10_dw_k", "L11_du1_k", 8},
+             {B.dv, G.w_v, P.w_v, hkv, "L10_dw_v", "L11_du1_v", 9}};
   for (const WG& w : wg) {  // L10: dW^T = u1^T d (A = u1^T K-major, B = d MN-major), stored transposed
     GemmArgs a = base_args(h, w.N, (int)n);
     a.out0 = (float*)w.g;
     a.ldo = h;
     a.n_split = w.N;
     a.accumulate = accumulate;
+    if (gs) set_scatter(a, gs, w.k, -1);
     Mat A{B.uT, h, n, B.L.ldT}, Bm{w.d, n, w.N, w.N};
     Prof p_(w.name, st, 2.0 * n * w.N * h, 2.0 * n * w.N * h, 0);
     EE_CUDA(gemm_run(EPI_F32T, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
@@ -589,7 +596,8 @@ ee_status layer_attn_backward(const ee_head_config* cfg, const Bufs& B, const ee
   { Prof p_("L12_gain_grad", st, 0, 0, 6.0 * n * h);
   EE_CUDA(launch_gain_grad(B.dz, x, B.r1, B.dgp, n, h, NORM_RPB, st)); }
   { Prof p_("reduce_cols", st, 0, 0, 4.0 * nparts * h);
-  EE_CUDA(launch_reduce_cols(B.dgp, nparts, h, (float*)G.g_att, accumulate, st)); }
+  EE_CUDA(launch_reduce_cols(B.dgp, nparts, h, gs ? scatter_gain(gs, 6) : (float*)G.g_att,
+                             accumulate, st)); }
   return EE_OK;
 }
 
@@ -617,7 +625,9 @@ static GradScatter make_scatter(const ee_head_config* c, const ee_peer_set& aren
   return g;
 }
 
-static void set_scatter(GemmArgs& a, const GradScatter* gs, int k, int k1 = -1) {
+static float* scatter_gain(const GradScatter* gs, int k) { return gs->p[k][0]; }
+
+static void set_scatter(GemmArgs& a, const GradScatter* gs, int k, int k1) {
   a.scat_rows = gs->chunk[k];
   for (int q = 0; q < MAX_PEERS; ++q) {
     a.scat[q] = gs->p[k][q];
@@ -776,7 +786,7 @@ ee_status phase_vocab_backward(const ee_head_config* cfg, const Bufs& B, const e
     a.ldo = h;
     a.n_split = Vl;
     a.accumulate = accumulate;
-    if (gs) set_scatter(a, gs, 5);
+    if (gs) set_scatter(a, gs, 5, -1);
     Mat A{B.zT, h, n, B.L.ldT}, Bm{B.ds, n, Vl, Vl};
     Prof p_("a9_dw_out", st, 2.0 * n * Vl * h, 2.0 * n * Vl * h, 0);
     EE_CUDA(gemm_run(EPI_F32T, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
@@ -810,7 +820,7 @@ ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee
     a.out0 = (float*)G.w_down;
     a.ldo = F;
     a.accumulate = accumulate;
-    if (gs) set_scatter(a, gs, 3);
+    if (gs) set_scatter(a, gs, 3, -1);
     Mat A{B.dyT, h, n, B.L.ldT}, Bm{B.mact, n, F, F};
     Prof p_("a11_dw_down", st, 2.0 * n * F * h, 2.0 * n * F * h, 0);
     EE_CUDA(gemm_run(EPI_F32, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
@@ -863,7 +873,7 @@ ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee
   { Prof p_("reduce_cols", st, 0, 0, 4.0 * nparts * h);
   EE_CUDA(launch_reduce_cols(B.dgp, nparts, h, gs ? gs->p[0][0] : (float*)G.g_a, accumulate,
                              st)); }
-  if (layer) return layer_attn_backward(cfg, B, P, G, x, n, accumulate, st);
+  if (layer) return layer_attn_backward(cfg, B, P, G, x, n, accumulate, st, gs);
   return EE_OK;
 }
 
@@ -1011,8 +1021,6 @@ ee_status ee_tune_step_rs(const ee_head_config* cfg, const void* const* hidden, 
                           float* loss_out, const ee_step_aux* aux, const int64_t* valid_count,
                           void* workspace, size_t ws_bytes, void* stream) {
   if (!grad_arenas) return fail(EE_ERR_ARG, "grad_arenas required");
-  if (cfg && cfg->arch == EE_ARCH_LAYER)
-    return fail(EE_ERR_UNSUPPORTED, "ee_tune_step_rs: Layer exits use ee_tune_step + all-reduce");
   if (cfg && cfg->token_weighting != EE_WEIGHT_UNIFORM)
     return fail(EE_ERR_UNSUPPORTED, "ee_tune_step_rs: uniform token weights only");
   return tune_step_impl(cfg, hidden, n_tokens, targets, exit_weights, params, nullptr,

@@ -126,10 +126,11 @@ class ShardedDPHeads:
         import paper_2402_00518_b200 as ee
         self.ee, self.spec, self.rank, self.world = ee, spec, rank, world
         self.cfg = ee.make_config(spec.hidden, spec.vocab, spec.ffn, spec.num_exits, spec.arch,
-                                  spec.norm_eps)
+                                  spec.norm_eps, **spec.attn_kwargs())
         self.exit_cfg = ee.make_config(spec.hidden, spec.vocab, spec.ffn, 1, spec.arch,
-                                       spec.norm_eps)
-        shapes = ee.tensor_shapes(spec.hidden, spec.vocab, spec.ffn, spec.arch)
+                                       spec.norm_eps, **spec.attn_kwargs())
+        shapes = ee.tensor_shapes(spec.hidden, spec.vocab, spec.ffn, spec.arch,
+                                  self.cfg.n_kv_heads)
         self.names = [k for k in ee.TENSOR_NAMES if k in shapes]
         self.shapes = shapes
         dev = torch.device(device)

@@ -28,9 +28,20 @@ pytestmark = pytest.mark.gpu
 
 
 def _cfg(arch, seed, exits=3):
+    if arch == "layer":     # 4 sequences of 128 tokens (whole sequences per rank)
+        c = S.get_cfg("tiny_layer", seed=seed)
+        c.tokens = 512
+        return c
     return S.Cfg(name="small", hidden=128, vocab=1000, ffn=256 if arch == "mlp" else 0,
                  arch=arch, tokens=256, layers=exits, after=list(range(1, exits + 1)),
                  init="random", seed=seed)
+
+
+def _attn(cfg):
+    if cfg.arch != "layer":
+        return {}
+    return dict(n_heads=cfg.n_heads, n_kv_heads=cfg.n_kv_heads or cfg.n_heads,
+                seq_len=cfg.seq_len)
 
 
 def _copy_src(params):
@@ -41,7 +52,7 @@ def run_threads(ee, cfg, P, hidden, targets, params, fused, steps=2, n_arenas=2)
     from paper_2402_00518_b200.parallel import ShardedDPHeads
     N, E = targets.numel(), cfg.exits
     nl = N // P
-    spec = ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch)
+    spec = ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch, **_attn(cfg))
     shared = {"P": P, "barrier": threading.Barrier(P), "slots": [None] * P}
     heads = [ShardedDPHeads(spec, nl, r, P, n_arenas=n_arenas) for r in range(P)] if fused \
         else None
@@ -114,11 +125,11 @@ def _warm(ee, cfg, hidden, targets, params):
 
 @pytest.mark.parametrize("arch,P,n_arenas", [("mlp", 2, 2), ("mlp", 4, 2), ("norm", 4, 2),
                                              ("embedding", 2, 2), ("mlp", 1, 2), ("mlp", 3, 1),
-                                             ("mlp", 8, 2)])
+                                             ("mlp", 8, 2), ("layer", 2, 2), ("layer", 4, 2)])
 def test_fused_dp_bitwise_equals_allreduce_path(gpu_lib, arch, P, n_arenas):
     ee = gpu_lib
     cfg = _cfg(arch, 51)
-    N = 240 if P == 3 else 256
+    N = 240 if P == 3 else (cfg.tokens if arch == "layer" else 256)
     hidden = S.hidden_states(cfg, N)
     targets = S.targets(cfg, N)
     params = S.head_params(cfg)
@@ -138,7 +149,7 @@ def test_fused_dp_bitwise_equals_allreduce_path(gpu_lib, arch, P, n_arenas):
                 assert torch.equal(fus[r][1][i][k], want), (r, i, k)
     # first-step losses against the fp64 oracle (parameters = the Copy source)
     for i in range(cfg.exits):
-        res = oracle_exit(arch, params[i], hidden[i], targets, 1.0)
+        res = oracle_exit(arch, params[i], hidden[i], targets, 1.0, attn=S.attn_geometry(cfg))
         assert abs(fus[0][0][0][i].item() - res.loss) / res.loss <= LOSS_RTOL
 
 
