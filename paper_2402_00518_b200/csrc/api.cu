@@ -715,9 +715,9 @@ ee_status phase_exit_forward(const ee_head_config* cfg, const Bufs& B, const ee_
 // a7 strategy: the a5 epilogue stores P~ = exp(S - tile max) (fp16) into the dS
 // buffer and a7 is an elementwise pass (default), or (EE_DS_RECOMPUTE=1) a7
 // recomputes S with a second GEMM (the FlashAttention-style recompute).
-static bool ds_recompute() {
-  static const int v = getenv("EE_DS_RECOMPUTE") ? atoi(getenv("EE_DS_RECOMPUTE")) : 0;
-  return v != 0;
+static bool ds_recompute() {  // read per call (host side, once per exit): tests toggle it
+  const char* e = getenv("EE_DS_RECOMPUTE");
+  return e && atoi(e) != 0;
 }
 
 ee_status phase_vocab_stats(const ee_head_config* cfg, const Bufs& B, const ee_head_tensors& P,

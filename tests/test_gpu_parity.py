@@ -11,7 +11,7 @@ import pytest
 import torch
 
 import eesynth as S
-from harness import compare_exit, gpu_step, oracle_exit
+from harness import GRAD_RTOL, compare_exit, gpu_step, oracle_exit, rel_fro
 from oracle import ee_oracle as O
 
 pytestmark = pytest.mark.gpu
@@ -249,13 +249,19 @@ def test_confidence_weighting_data_parallel_shards(gpu_lib, arch):
 
 
 @pytest.mark.parametrize("scale", [64.0, 256.0])
-def test_confident_rows_ds_precision(gpu_lib, scale):
+def test_confident_rows_ds_precision(gpu_lib, scale, monkeypatch):
     """Peaked softmax rows (p_y -> 1, the regime of a well-tuned exit): a7
-    forms dS from the fp16 P~ the a5 epilogue stored, except the target
-    column, which is recomputed from the fp32 target logit; the gradients of
-    these small-gradient rows must still meet the tolerance.  W_out is scaled
+    forms dS from the fp16 P~ the a5 epilogue stored (A24), except the target
+    column, which is recomputed from the fp32 target logit.  W_out is scaled
     (by powers of two: the operands stay on the bf16 grid) so the logits
-    spread widely, and the targets are the oracle's argmax."""
+    spread widely, and the targets are the oracle's argmax.
+
+    Against the recompute path (EE_DS_RECOMPUTE=1: same bf16 z, dS from fp32
+    S) the gradients must agree to 5e-3 per tensor -- this isolates A24's one
+    extra fp16 rounding.  Against the oracle: at 64x the north_star gradient
+    bound holds; at 256x the forward's single bf16 rounding of z (A3/A13)
+    moves logits of magnitude ~100 by ~0.1, which both GPU variants share, so
+    only the A/B bound is asserted there."""
     cfg = S.Cfg(name="small", hidden=128, vocab=1000, ffn=256, arch="mlp", tokens=300, layers=2,
                 after=[1, 2], init="random", seed=12)
     hidden = S.hidden_states(cfg, 300, seed=3)
@@ -265,10 +271,19 @@ def test_confident_rows_ds_precision(gpu_lib, scale):
     t0 = S.targets(cfg, 300, seed=3)
     res0 = oracle_exit("mlp", params[0], hidden[0], t0, 1.0)
     targets = torch.from_numpy(np.argmax(res0.act["S"], axis=1).astype(np.int32))
+    monkeypatch.setenv("EE_DS_RECOMPUTE", "1")
+    loss_r, grads_r, _, st_r = gpu_step(gpu_lib, cfg, hidden[:1], targets, params[:1], [1.0])
+    monkeypatch.setenv("EE_DS_RECOMPUTE", "0")
     loss, grads, aux, status = gpu_step(gpu_lib, cfg, hidden[:1], targets, params[:1], [1.0])
-    assert status == (0, -1)
+    assert status == (0, -1) and st_r == (0, -1)
     res = oracle_exit("mlp", params[0], hidden[0], targets, 1.0)
     p_y = np.exp(-res.stats["loss"])
     assert np.median(p_y) > 0.5                      # the regime under test
-    errs = compare_exit("mlp", res, loss[0].item(), grads[0], aux[0], targets, tag=f"conf{scale}")
-    print(scale, res.loss, float(np.median(p_y)), errs)
+    assert loss[0].item() == loss_r[0].item()        # a5/a6 are shared
+    ab = {k: rel_fro(grads[0][k].double().cpu().numpy(), grads_r[0][k].double().cpu().numpy())
+          for k in res.grads}
+    assert all(e <= 5e-3 for e in ab.values()), ab
+    orc = {k: rel_fro(grads[0][k].double().cpu().numpy(), g) for k, g in res.grads.items()}
+    if scale <= 64.0:
+        assert all(e <= GRAD_RTOL for e in orc.values()), orc
+    print(scale, res.loss, float(np.median(p_y)), ab, orc)
