@@ -179,3 +179,124 @@ def test_key_encoding_orders_by_value_then_lowest_index():
     assert order == expect
     for (m, i), k in zip(vals, keys):
         assert _unkey(k) == (np.float32(m), i)
+
+
+# ---------------------------------------------------------------------------
+# fused variant (vocab_parallel_step_fused): the host orchestration of the
+# peer-memory all-gather / reduce-scatter, with shared-memory CPU tensors as
+# the peers' buffers and gloo barriers as ee_peer_barrier
+# ---------------------------------------------------------------------------
+
+class SharedPeer:
+    """CPU stand-in of parallel.PeerBuffers: z_all and the dz slots of every
+    rank live in shared memory, so a rank's "NVLink stores" are plain writes."""
+
+    def __init__(self, rank, world, z_tabs, slot_tabs):
+        self.rank, self.world = rank, world
+        self.z_tabs, self.slot_tabs = z_tabs, slot_tabs
+        self.z_all = z_tabs[rank]
+        self.slots = slot_tabs[rank]
+        self.n_all = self.z_all.shape[0]
+        self.n_local = self.n_all // world
+        self.epoch = 0
+
+
+class NumpyFusedPhases(NumpyPhases):
+    def exit_forward_ag(self, hidden, params, peer, n_all):
+        p = {k: v.numpy() for k, v in params.items()}
+        self.act = self.O.exit_forward(self.arch, p, hidden.numpy(), self.eps, self.attn)
+        z = torch.from_numpy(self.act["z"])
+        r0 = peer.rank * peer.n_local
+        for t in peer.z_tabs:                         # the all-gather: stores into every rank
+            t[r0:r0 + peer.n_local].copy_(z)
+
+    def vocab_backward_rs(self, i, z_all, targets_all, key, sums, alpha, W, params, grads, peer,
+                          loss_slot, accumulate, aux=None):
+        dz = torch.zeros(peer.n_all, z_all.shape[1], dtype=torch.float64)
+        self.vocab_backward(i, z_all, targets_all, key, sums, alpha, W, params, grads,
+                            None if self.arch == "embedding" else dz, loss_slot, accumulate, aux)
+        if self.arch != "embedding":                  # the reduce-scatter: rows to their owners
+            nl = peer.n_local
+            for q in range(peer.world):
+                peer.slot_tabs[q][peer.rank].copy_(dz[q * nl:(q + 1) * nl])
+
+    def exit_backward_slots(self, hidden, params, peer, grads, accumulate, n_all):
+        dz = peer.slots[0].clone()
+        for q in range(1, peer.world):                # owner-side sum in rank order
+            dz += peer.slots[q]
+        self.exit_backward(hidden, params, dz, grads, accumulate, n_all)
+
+    def barrier(self, peer):
+        peer.epoch += 1
+        dist.barrier()
+
+
+def _fused_worker(rank, world, port, arch, z_tabs, slot_tabs, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import ee_oracle as O
+        from paper_2402_00518_b200.parallel import TorchComm, vocab_parallel_step_fused
+        rng = np.random.default_rng(2)
+        h, V, F, N, E = 16, 40, 24, z_tabs[0].shape[0], 2
+        params = [{"w_out": rng.normal(0, .5, (V, h))} for _ in range(E)]
+        for p in params:
+            if arch != "embedding":
+                p["g_f"] = 1 + .1 * rng.normal(size=h)
+            if arch == "mlp":
+                p.update(g_a=1 + .1 * rng.normal(size=h), w_gate=rng.normal(0, .5, (F, h)),
+                         w_up=rng.normal(0, .5, (F, h)), w_down=rng.normal(0, .5, (h, F)))
+        xs = [rng.normal(size=(N, h)) for _ in range(E)]
+        y = rng.integers(0, V, N)
+        y[[0, 5]] = -1
+        alphas = [1.0, 0.4]
+        w = 16
+        vb, ve = min(V, rank * w), (V if rank == world - 1 else min(V, (rank + 1) * w))
+        nl = N // world
+        T = lambda a: torch.from_numpy(np.ascontiguousarray(a))
+        prm = [{k: T(v[vb:ve] if k == "w_out" else v) for k, v in p.items()} for p in params]
+        grd = [{k: torch.zeros_like(v) for k, v in p.items()} for p in prm]
+        hid = [T(x[rank * nl:(rank + 1) * nl]) for x in xs]
+        bufs = {"key": torch.zeros(N, dtype=torch.int64),
+                "sums": torch.zeros(N, 2, dtype=torch.float64)}
+        W = torch.tensor([int(np.sum(y != -1))])
+        loss = torch.zeros(E, dtype=torch.float64)
+        peer = SharedPeer(rank, world, z_tabs, slot_tabs)
+        ph = NumpyFusedPhases(O, arch, vb, ve)
+        for _ in range(2):                            # twice: buffer reuse across steps
+            vocab_parallel_step_fused(ph, TorchComm(), peer, arch, hid, torch.from_numpy(y), prm,
+                                      grd, loss, alphas, W, bufs)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, ([g["w_out"].numpy() for g in grd],))
+        if rank == 0:
+            full_l, full_g, _ = O.tune_step(arch, params, xs, y, alphas, 1e-5)
+            ok = np.allclose(loss.numpy(), full_l, rtol=1e-10)
+            ok &= peer.epoch == 2 * (1 + 2 * E)       # barriers per step: 1 + 2 per exit
+            for i in range(E):
+                dw = np.concatenate([gathered[r][0][i] for r in range(world)])
+                ok &= np.allclose(dw, full_g[i]["w_out"], rtol=1e-9, atol=1e-14)
+                for k in full_g[i]:
+                    if k != "w_out":
+                        ok &= np.allclose(grd[i][k].numpy(), full_g[i][k], rtol=1e-9, atol=1e-14)
+            q.put(bool(ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("arch,world", [("mlp", 2), ("norm", 3), ("embedding", 2)])
+def test_fused_vocab_parallel_gloo_matches_full_batch_oracle(arch, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    N, h = 12 * world, 16
+    z_tabs = [torch.zeros(N, h, dtype=torch.float64).share_memory_() for _ in range(world)]
+    slot_tabs = [torch.zeros(world, N // world, h, dtype=torch.float64).share_memory_()
+                 for _ in range(world)]
+    procs = [ctx.Process(target=_fused_worker, args=(r, world, port, arch, z_tabs, slot_tabs, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    assert q.get(timeout=5) is True
