@@ -230,7 +230,9 @@ def workload_config(cfg, world, args):
             **vp_comm_desc(args, vp, world),
             "l2": "inputs larger than L2 (hidden states + exit weights per step >> 126 MB)",
             "optimizer": "Adam (P:374-375), included in the step",
-            "update_schedule": ("per exit, shared gradient buffers (P:261)"
+            "update_schedule": ("per exit, Adam fused into the weight-gradient epilogues "
+                                "(P:261)" if getattr(args, "fused_adam", False) else
+                                "per exit, shared gradient buffers (P:261)"
                                 if getattr(args, "per_exit", False) else
                                 "per exit: tune, barrier, sharded Adam (P:261)"
                                 if getattr(args, "dp_fused", False) else "all exits, then Adam")}
@@ -303,6 +305,9 @@ def main():
                     help="dp, N>1: fused = gradient reduce-scatter in the weight-gradient GEMM "
                          "epilogues + sharded Adam storing the operands to every rank (CUDA-IPC "
                          "peer memory, ZeRO-1); nccl = NCCL all-reduce + full Adam per rank")
+    ap.add_argument("--no-fused-adam", action="store_true",
+                    help="N=1: separate ee_tune_step + ee_adam_update instead of the Adam "
+                         "update fused into the weight-gradient epilogues (A/B)")
     ap.add_argument("--force-dp-fused", action="store_true",
                     help="run the fused DP path at N=1 as well (A/B against the plain step)")
     ap.add_argument("--vp-comm", default="fused", choices=["fused", "nccl"],
@@ -385,7 +390,10 @@ def main():
         heads = ee.ExitHeads(ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch,
                                          vocab_begin=vb, vocab_end=ve, **attn_kw(cfg)), n_all,
                              device=dev, grad_buffers=gbuf if gbuf > 0 else None)
-    per_exit = (not dp_fused) and heads.grad_buffers < E
+    fused_adam = (not multi and not vp and not dp_fused and cfg.arch != "layer"
+                  and not args.no_fused_adam)
+    args.fused_adam = fused_adam
+    per_exit = (not dp_fused) and (not fused_adam) and heads.grad_buffers < E
     args.per_exit = per_exit
     bb = S.backbone(cfg, device=dev)
     src = []
@@ -438,6 +446,9 @@ def main():
 
     def step(it, hid=hidden, tg=targets):
         lr = ee.ee_lr_at(min(it + 1, total_iters), total_iters)
+        if fused_adam:     # one GPU: Adam fused into the weight-gradient epilogues
+            heads.step_adam(hid, tg, lr)
+            return
         if dp_fused:       # exit by exit: tune -> peer barrier -> sharded Adam
             heads.step(hid, tg, lr, all_reduce=dist.all_reduce if multi else None)
             return
@@ -518,8 +529,12 @@ def main():
         loss_host = torch.empty(E, dtype=torch.float32).pin_memory()
         streamed = not multi and not per_exit and not vp and not dp_fused
         if streamed:    # untimed warm-up of the host-input API (staging buffers, copy stream)
-            heads.step_host(h_host, t_host)
-            heads.adam(ee.ee_lr_at(min(args.warmup + args.steps, total_iters), total_iters))
+            lr_w = ee.ee_lr_at(min(args.warmup + args.steps, total_iters), total_iters)
+            if fused_adam:
+                heads.step_host(h_host, t_host, lr=lr_w)
+            else:
+                heads.step_host(h_host, t_host)
+                heads.adam(lr_w)
         torch.cuda.synchronize()
         if multi:
             dist.barrier()
@@ -527,9 +542,13 @@ def main():
         a0.record()
         for it in range(args.steps):
             if streamed:   # public API for host-resident hidden states: H2D overlapped per exit
-                heads.step_host(h_host, t_host)
-                heads.adam(ee.ee_lr_at(min(args.warmup + args.steps + it + 1, total_iters),
-                                       total_iters))
+                lr_e = ee.ee_lr_at(min(args.warmup + args.steps + it + 1, total_iters),
+                                   total_iters)
+                if fused_adam:
+                    heads.step_host(h_host, t_host, lr=lr_e)
+                else:
+                    heads.step_host(h_host, t_host)
+                    heads.adam(lr_e)
             else:
                 for d_, h_ in zip(hidden, h_host):
                     d_.copy_(h_, non_blocking=True)
@@ -544,7 +563,9 @@ def main():
         e2e = {"value": job_tokens / (te.item() / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": sum(h.numel() * 2 for h in hidden) + targets.numel() * 4,
                "d2h_bytes_per_step": E * 4, "ms_per_step": te.item(),
-               "api": ("ExitHeads.step_host (per-exit H2D overlapped with compute) + adam"
+               "api": (("ExitHeads.step_host(lr=...) (per-exit H2D overlapped with compute, "
+                        "Adam fused)" if fused_adam else
+                        "ExitHeads.step_host (per-exit H2D overlapped with compute) + adam")
                        if streamed else "H2D copies + step")}
         del h_host
 

@@ -446,6 +446,26 @@ ee_status ee_adam_update(const ee_head_config* cfg, ee_head_tensors* master,
                          float beta2, float eps, float weight_decay, int64_t step,
                          float grad_scale, void* stream);
 
+/* One tuning step with the Adam update fused into the weight-gradient GEMM
+ * epilogues: "forward computation, backward computation, and parameter update
+ * for each early-exit layer, without any dependency between early exits"
+ * (P:261).  Same as ee_tune_step (accumulate = 0) followed by ee_adam_update
+ * with the same arguments, bit for bit, but the matrix gradients are never
+ * stored: when a dW_out / dW_down / dW_gate|up tile is final, the epilogue
+ * applies Adam to master/m/v at those elements and stores the bf16 operand
+ * (the backward GEMMs that read a weight run before the one that updates it).
+ * The gains' column-sum gradients go through the workspace and a small Adam.
+ * One GPU (the whole gradient is local); Embedding/Norm/MLP exits; uniform or
+ * CONFIDENCE token weights; n_tokens > 0.  operand/master/m/v as in
+ * ee_adam_update, [E] each. */
+ee_status ee_tune_step_adam(const ee_head_config* cfg, const void* const* hidden,
+                            int64_t n_tokens, const int32_t* targets, const float* exit_weights,
+                            ee_head_tensors* operand, ee_head_tensors* master, ee_head_tensors* m,
+                            ee_head_tensors* v, float lr, float beta1, float beta2, float eps,
+                            float weight_decay, int64_t step, float grad_scale, float* loss_out,
+                            const ee_step_aux* aux, const int64_t* valid_count, void* workspace,
+                            size_t ws_bytes, void* stream);
+
 /* SGD: buf = momentum*buf + g (buf may be NULL iff momentum == 0);
  * theta -= lr * buf; operand refreshed as for Adam. */
 ee_status ee_sgd_update(const ee_head_config* cfg, ee_head_tensors* master,

@@ -36,7 +36,8 @@ EXPORTED = ("ee_workspace_size", "ee_init_heads", "ee_tune_step", "ee_count_vali
             "ee_backbone_workspace_size", "ee_backbone_forward", "ee_test_attention",
             "ee_normalize_exit", "ee_vp_exit_forward_ag", "ee_vp_vocab_backward_rs",
             "ee_vp_exit_backward_slots", "ee_peer_barrier", "ee_ipc_get_handle", "ee_ipc_open",
-            "ee_ipc_close", "ee_dp_shard_layout", "ee_tune_step_rs", "ee_adam_update_sharded")
+            "ee_ipc_close", "ee_dp_shard_layout", "ee_tune_step_rs", "ee_adam_update_sharded",
+            "ee_tune_step_adam")
 MAX_PEERS = 8
 
 
@@ -137,6 +138,9 @@ def load(path: str = LIB_PATH):
                                           ctypes.POINTER(ee_step_aux), I32, P, SZ, P]),
         "ee_vp_exit_backward_slots": (I32, [CFG, P, I64, I64, HT, P, I32, HT, I32, P, SZ, P]),
         "ee_peer_barrier": (I32, [ctypes.POINTER(ee_peer_set), ctypes.c_uint32, P, P]),
+        "ee_tune_step_adam": (I32, [CFG, ctypes.POINTER(P), I64, P, ctypes.POINTER(F32), HT, HT,
+                                    HT, HT, F32, F32, F32, F32, F32, I64, F32, P,
+                                    ctypes.POINTER(ee_step_aux), P, P, SZ, P]),
         "ee_dp_shard_layout": (I32, [CFG, I32, I32, I32, ctypes.POINTER(I64),
                                      ctypes.POINTER(I64), ctypes.POINTER(I64),
                                      ctypes.POINTER(I64)]),
@@ -460,6 +464,29 @@ def ee_peer_barrier(signals: ee_peer_set, epoch: int, workspace, stream=None):
                                 _ptr(workspace), _stream(stream)))
 
 
+def ee_tune_step_adam(cfg, hidden, targets, exit_weights, operand, master, m, v, lr, step,
+                      loss_out, workspace, beta1=0.9, beta2=0.95, eps=1e-5, weight_decay=0.0,
+                      grad_scale=1.0, aux=None, valid_count=None, stream=None):
+    """ee_tune_step + ee_adam_update with the update fused into the
+    weight-gradient epilogues; no gradient tensors."""
+    load()
+    E = cfg.num_exits
+    hid = (ctypes.c_void_p * E)(*[h.data_ptr() for h in hidden])
+    w = (ctypes.c_float * E)(*[float(a) for a in exit_weights])
+    ax = None
+    if aux is not None:
+        ax = (ee_step_aux * E)()
+        for i, d in enumerate(aux):
+            for k in AUX_NAMES:
+                t = d.get(k)
+                setattr(ax[i], k, None if t is None else t.data_ptr())
+    _check(_lib.ee_tune_step_adam(ctypes.byref(cfg), hid, targets.numel(), _ptr(targets), w,
+                                  heads(operand), heads(master), heads(m), heads(v), lr, beta1,
+                                  beta2, eps, weight_decay, int(step), grad_scale,
+                                  _ptr(loss_out), ax, _ptr(valid_count), _ptr(workspace),
+                                  workspace.numel(), _stream(stream)))
+
+
 def ee_dp_shard_layout(cfg, world: int, rank: int, tensor: str):
     """(row_begin, rows, arena offset in floats, arena total floats) of `rank`'s
     shard of `tensor` (a TENSOR_NAMES entry) under the fused DP path."""
@@ -679,19 +706,34 @@ class ExitHeads:
         ee_adam_update(self.cfg, self.master, self.operand, self.grads, self.m, self.v, lr,
                        self.step_count, beta1, beta2, eps, weight_decay, grad_scale)
 
+    def step_adam(self, hidden, targets, lr, exit_weights=None, beta1=0.9, beta2=0.95,
+                  eps=1e-5, weight_decay=0.0, grad_scale=1.0):
+        """step() + adam() in one call, the update fused into the weight-gradient
+        epilogues (ee_tune_step_adam).  self.grads are not written."""
+        if targets.numel() > self.max_tokens:
+            raise ValueError("more tokens than the workspace was sized for")
+        w = exit_weights if exit_weights is not None else [1.0] * self.spec.num_exits
+        self.step_count += 1
+        ee_tune_step_adam(self.cfg, hidden, targets, w, self.operand, self.master, self.m, self.v,
+                          lr, self.step_count, self.loss, self.workspace, beta1, beta2, eps,
+                          weight_decay, grad_scale)
+        return self.loss
+
     def adam_exit(self, i, lr, step, beta1=0.9, beta2=0.95, eps=1e-5, weight_decay=0.0,
                   grad_scale=1.0):
         ee_adam_update(self.exit_cfg, self.master[i:i + 1], self.operand[i:i + 1],
                        self.grads[i:i + 1], self.m[i:i + 1], self.v[i:i + 1], lr, step, beta1,
                        beta2, eps, weight_decay, grad_scale)
 
-    def step_host(self, hidden_host, targets_host, exit_weights=None):
+    def step_host(self, hidden_host, targets_host, exit_weights=None, lr=None):
         """One tuning step with the cached hidden states in pinned HOST memory
         (the usual place for them: 4.3 GB per step at the 70B shape).  Exit
         i + 1's hidden states are copied host-to-device on a side stream while
         exit i computes (two device staging buffers, event-ordered), so the
         PCIe/C2C transfer hides under the exit's GEMMs.  Same results as
-        step() on device copies of the same bytes.  Returns the device losses."""
+        step() on device copies of the same bytes.  With lr given, each exit's
+        Adam update is fused into its backward (ee_tune_step_adam; = step_adam()).
+        Returns the device losses."""
         E = self.spec.num_exits
         n, h = hidden_host[0].shape
         if n > self.max_tokens:
@@ -723,8 +765,16 @@ class ExitHeads:
                     bufs[nb_].copy_(hidden_host[i + 1], non_blocking=True)
                     ev_copied[nb_].record(cs)
             st.wait_event(ev_copied[b])
-            ee_tune_step(self.exit_cfg, [bufs[b]], tg, w[i:i + 1], self.operand[i:i + 1],
-                         self.grads[i:i + 1], self.loss[i:i + 1], self.workspace)
+            if lr is None:
+                ee_tune_step(self.exit_cfg, [bufs[b]], tg, w[i:i + 1], self.operand[i:i + 1],
+                             self.grads[i:i + 1], self.loss[i:i + 1], self.workspace)
+            else:
+                if i == 0:
+                    self.step_count += 1
+                ee_tune_step_adam(self.exit_cfg, [bufs[b]], tg, w[i:i + 1],
+                                  self.operand[i:i + 1], self.master[i:i + 1], self.m[i:i + 1],
+                                  self.v[i:i + 1], lr, self.step_count, self.loss[i:i + 1],
+                                  self.workspace)
             ev_free[b].record(st)
         return self.loss
 

@@ -170,7 +170,7 @@ long long tensor_numel(const ee_head_config* c, int k) {
 }
 
 struct Layout {
-  size_t wsum_part, wsum, zT, uT, dyT;
+  size_t wsum_part, wsum, zT, uT, dyT, gsc;
   long long ldT;  // leading dimension of the transposed [h x n] copies (n rounded up to 8)
   size_t status, vcount, loss_part, lse, coef, tgt, pm, ps, pi, z, ds, dz, dgp, ry, u, rx, ab,
       mact, y, dy, total;
@@ -192,6 +192,7 @@ Layout make_layout(const ee_head_config* c, long long n) {
     return r;
   };
   L.status = take(sizeof(DevStatus));
+  L.gsc = take(4 * 2 * (size_t)h);  // fused Adam: g_f / g_a gradients
   L.vcount = take(8);
   L.loss_part = take(4 * (size_t)(L.nfin > 0 ? L.nfin : 1));
   L.wsum_part = take(4 * (size_t)(L.nfin > 0 ? L.nfin : 1));
@@ -418,6 +419,7 @@ struct Bufs {
   float *r1, *lse2, *x1, *dvec;
   // vocab-parallel merge state
   float* m_loc;
+  float* gsc;  // [2 x h] gain gradients of ee_tune_step_adam
   Layout L;
 };
 
@@ -428,6 +430,7 @@ Bufs make_bufs(const ee_head_config* cfg, long long n, void* workspace) {
   uint8_t* ws = (uint8_t*)workspace;
   const bool mlp = cfg->arch >= EE_ARCH_MLP, nrm = cfg->arch != EE_ARCH_EMBEDDING;
   B.status = (DevStatus*)(ws + L.status);
+  B.gsc = (float*)(ws + L.gsc);
   B.vcount = (long long*)(ws + L.vcount);
   B.lse = (float*)(ws + L.lse);
   B.coef = (float*)(ws + L.coef);
@@ -601,6 +604,20 @@ ee_status layer_attn_backward(const ee_head_config* cfg, const Bufs& B, const ee
   return EE_OK;
 }
 
+// Fused Adam (ee_tune_step_adam): per tensor k the state the weight-gradient
+// epilogue updates in place instead of storing the gradient.
+struct AdamFuse {
+  AdamOut t[NTENS];
+  AdamScal sc;
+};
+
+static void set_adam(GemmArgs& a, const AdamFuse* af, int k, int k1) {
+  a.adam_on = 1;
+  a.adam = af->sc;
+  a.adam0 = af->t[k];
+  if (k1 >= 0) a.adam1 = af->t[k1];
+}
+
 // Fused data-parallel gradient routing (ee_tune_step_rs): p[k][q] = where
 // this rank's partial of tensor k's rows owned by rank q go (owner q's arena,
 // slot [rank]); chunk[k] = rows per owner.  Gains: one row, owner 0.
@@ -747,7 +764,7 @@ ee_status phase_vocab_backward(const ee_head_config* cfg, const Bufs& B, const e
                                const ee_head_tensors& G, const __nv_bfloat16* z, long long n,
                                const int32_t* targets, int accumulate, float* dz_out,
                                cudaStream_t st, const ee_peer_set* rs = nullptr,
-                               const GradScatter* gs = nullptr) {
+                               const GradScatter* gs = nullptr, const AdamFuse* af = nullptr) {
   const int h = cfg->hidden, Vl = cfg->vocab_end - cfg->vocab_begin;
   if (!ds_recompute()) {  // a7: dS from the stored P~ (elementwise, in place)
     Prof p_("a7_ds_from_p", st, 0, 0, 4.0 * n * Vl);
@@ -787,6 +804,7 @@ ee_status phase_vocab_backward(const ee_head_config* cfg, const Bufs& B, const e
     a.n_split = Vl;
     a.accumulate = accumulate;
     if (gs) set_scatter(a, gs, 5, -1);
+    if (af) set_adam(a, af, 5, -1);
     Mat A{B.zT, h, n, B.L.ldT}, Bm{B.ds, n, Vl, Vl};
     Prof p_("a9_dw_out", st, 2.0 * n * Vl * h, 2.0 * n * Vl * h, 0);
     EE_CUDA(gemm_run(EPI_F32T, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
@@ -798,7 +816,8 @@ ee_status phase_vocab_backward(const ee_head_config* cfg, const Bufs& B, const e
 ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee_head_tensors& P,
                               const ee_head_tensors& G, const __nv_bfloat16* x, long long n,
                               const float* dz, int accumulate, cudaStream_t st,
-                              int nslots = 1, const GradScatter* gs = nullptr) {
+                              int nslots = 1, const GradScatter* gs = nullptr,
+                              const AdamFuse* af = nullptr) {
   const int h = cfg->hidden, F = cfg->ffn;
   const bool mlp = cfg->arch >= EE_ARCH_MLP, layer = cfg->arch == EE_ARCH_LAYER;
   if (cfg->arch == EE_ARCH_EMBEDDING) return EE_OK;
@@ -809,22 +828,9 @@ ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee
                              (const float*)P.g_f, mlp ? B.dy : nullptr, B.dgp, n, h, NORM_RPB,
                              st, nullptr, nslots, (long long)n * h)); }
   { Prof p_("reduce_cols", st, 0, 0, 4.0 * nparts * h);
-  EE_CUDA(launch_reduce_cols(B.dgp, nparts, h, gs ? gs->p[4][0] : (float*)G.g_f, accumulate,
-                             st)); }
+  EE_CUDA(launch_reduce_cols(B.dgp, nparts, h,
+                             gs ? gs->p[4][0] : af ? B.gsc : (float*)G.g_f, accumulate, st)); }
   if (!mlp) return EE_OK;
-  // a11: dW_down = dy^T M  (A = dy^T K-major copy, B = M MN-major)
-  {
-    { Prof p_("transpose_dy", st, 0, 0, 4.0 * n * h);
-    EE_CUDA(launch_transpose_bf16(B.dy, B.dyT, n, h, B.L.ldT, st)); }
-    GemmArgs a = base_args(h, F, (int)n);
-    a.out0 = (float*)G.w_down;
-    a.ldo = F;
-    a.accumulate = accumulate;
-    if (gs) set_scatter(a, gs, 3, -1);
-    Mat A{B.dyT, h, n, B.L.ldT}, Bm{B.mact, n, F, F};
-    Prof p_("a11_dw_down", st, 2.0 * n * F * h, 2.0 * n * F * h, 0);
-    EE_CUDA(gemm_run(EPI_F32, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
-  }
   // a11: dM = dy W_down; dA = dM B silu'(A), dB = dM silu(A), in place over [A|B]
   {
     GemmArgs a = base_args((int)n, F, h);
@@ -835,7 +841,31 @@ ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee
     Prof p_("a11_dm_swiglu_bwd", st, 2.0 * n * F * h, 2.0 * n * F * h, 0);
     EE_CUDA(gemm_run(EPI_SWIGLU_BWD, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
   }
-  // a12: [dW_gate; dW_up]^T = u^T [dA|dB]  (A = u^T K-major copy, B = [dA|dB]
+  // a11: dW_down = dy^T M  (after dM, which reads W_down: a fused Adam updates it)
+  // dW_down = dy^T M  (A = dy^T K-major copy, B = M MN-major)
+  {
+    { Prof p_("transpose_dy", st, 0, 0, 4.0 * n * h);
+    EE_CUDA(launch_transpose_bf16(B.dy, B.dyT, n, h, B.L.ldT, st)); }
+    GemmArgs a = base_args(h, F, (int)n);
+    a.out0 = (float*)G.w_down;
+    a.ldo = F;
+    a.accumulate = accumulate;
+    if (gs) set_scatter(a, gs, 3, -1);
+    if (af) set_adam(a, af, 3, -1);
+    Mat A{B.dyT, h, n, B.L.ldT}, Bm{B.mact, n, F, F};
+    Prof p_("a11_dw_down", st, 2.0 * n * F * h, 2.0 * n * F * h, 0);
+    EE_CUDA(gemm_run(EPI_F32, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
+  }
+  // a12: du = dA W_gate + dB W_up  (K concatenation over the two weights) -> B.dz
+  {
+    GemmArgs a = base_args((int)n, h, 2 * F);
+    a.out0 = B.dz;
+    a.ldo = h;
+    Mat A{B.ab, n, 2LL * F, 2LL * F}, B0{P.w_gate, F, h, h}, B1{P.w_up, F, h, h};
+    Prof p_("a12_du", st, 4.0 * n * F * h, 4.0 * n * F * h, 0);
+    EE_CUDA(gemm_run(EPI_F32, true, false, A, B0, &B1, B_KSPLIT, F, a, st));
+  }
+  // a12 (after du, which reads W_gate / W_up): [dW_gate; dW_up]^T = u^T [dA|dB]  (A = u^T K-major copy, B = [dA|dB]
   // MN-major), stored transposed; output columns split at F over the two grads
   {
     { Prof p_("transpose_u", st, 0, 0, 4.0 * n * h);
@@ -847,18 +877,10 @@ ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee
     a.ldo = h;
     a.accumulate = accumulate;
     if (gs) set_scatter(a, gs, 1, 2);
+    if (af) set_adam(a, af, 1, 2);
     Mat A{B.uT, h, n, B.L.ldT}, Bm{B.ab, n, 2LL * F, 2LL * F};
     Prof p_("a12_dw_gateup", st, 4.0 * n * F * h, 4.0 * n * F * h, 0);
     EE_CUDA(gemm_run(EPI_F32T, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
-  }
-  // a12: du = dA W_gate + dB W_up  (K concatenation over the two weights) -> B.dz
-  {
-    GemmArgs a = base_args((int)n, h, 2 * F);
-    a.out0 = B.dz;
-    a.ldo = h;
-    Mat A{B.ab, n, 2LL * F, 2LL * F}, B0{P.w_gate, F, h, h}, B1{P.w_up, F, h, h};
-    Prof p_("a12_du", st, 4.0 * n * F * h, 4.0 * n * F * h, 0);
-    EE_CUDA(gemm_run(EPI_F32, true, false, A, B0, &B1, B_KSPLIT, F, a, st));
   }
   if (!layer) {
     // a13: dg_a = sum_t du_t * xhat_t  (no dx: frozen backbone)
@@ -871,7 +893,8 @@ ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee
                                NORM_RPB, st, B.dy));
   }
   { Prof p_("reduce_cols", st, 0, 0, 4.0 * nparts * h);
-  EE_CUDA(launch_reduce_cols(B.dgp, nparts, h, gs ? gs->p[0][0] : (float*)G.g_a, accumulate,
+  EE_CUDA(launch_reduce_cols(B.dgp, nparts, h,
+                             gs ? gs->p[0][0] : af ? B.gsc + h : (float*)G.g_a, accumulate,
                              st)); }
   if (layer) return layer_attn_backward(cfg, B, P, G, x, n, accumulate, st, gs);
   return EE_OK;
@@ -898,14 +921,15 @@ static ee_status tune_step_impl(const ee_head_config* cfg, const void* const* hi
                                 ee_head_tensors* grads, const ee_peer_set* arenas,
                                 int32_t accumulate, float* loss_out, const ee_step_aux* aux,
                                 const int64_t* valid_count, void* workspace, size_t ws_bytes,
-                                void* stream) {
+                                void* stream, const AdamFuse* afuse = nullptr) {
   ee_status s = check_cfg(cfg);
   if (s != EE_OK) return s;
   if (cfg->vocab_begin != 0 || cfg->vocab_end != cfg->vocab)
     return fail(EE_ERR_ARG, "ee_tune_step needs the full vocabulary; use the ee_vp_* phases "
                             "for a vocab-parallel shard");
   const int E = cfg->num_exits;
-  if (!hidden || !exit_weights || !params || (!grads && !arenas) || !loss_out || n_tokens < 0 ||
+  if (!hidden || !exit_weights || !params || (!grads && !arenas && !afuse) || !loss_out ||
+      n_tokens < 0 ||
       (n_tokens > 0 && !targets))
     return fail(EE_ERR_ARG, "NULL argument or n_tokens < 0");
   if (n_tokens > (1LL << 30)) return fail(EE_ERR_SHAPE, "n_tokens too large");
@@ -916,7 +940,8 @@ static ee_status tune_step_impl(const ee_head_config* cfg, const void* const* hi
                                     "ee_normalize_exit");
   for (int i = 0; i < E; ++i) {
     if ((s = check_arch_tensors(cfg, params[i], "params", i)) != EE_OK) return s;
-    if (!arenas && (s = check_arch_tensors(cfg, grads[i], "grads", i)) != EE_OK) return s;
+    if (!arenas && !afuse && (s = check_arch_tensors(cfg, grads[i], "grads", i)) != EE_OK)
+      return s;
     if (arenas) {
       const ee_peer_set& a = arenas[i];
       if (a.world < 1 || a.world > EE_MAX_PEERS || a.rank < 0 || a.rank >= a.world)
@@ -972,6 +997,7 @@ static ee_status tune_step_impl(const ee_head_config* cfg, const void* const* hi
       gsv = make_scatter(cfg, arenas[i]);
       gs = &gsv;
     }
+    const AdamFuse* af = afuse ? &afuse[i] : nullptr;
     const __nv_bfloat16* x = (const __nv_bfloat16*)hidden[i];
     const __nv_bfloat16* z = nullptr;
     if ((s = phase_exit_forward(cfg, B, P, x, n, nullptr, &z, st)) != EE_OK) return s;
@@ -998,12 +1024,66 @@ static ee_status tune_step_impl(const ee_head_config* cfg, const void* const* hi
         EE_CUDA(cudaMemcpyAsync(ax->weight_sum, B.wsum, sizeof(float), cudaMemcpyDeviceToDevice, st));
     }
     if ((s = phase_vocab_backward(cfg, B, P, G, z, n, targets, accumulate, nrm ? B.dz : nullptr,
-                                  st, nullptr, gs)) != EE_OK)
+                                  st, nullptr, gs, af)) != EE_OK)
       return s;
-    if ((s = phase_exit_backward(cfg, B, P, G, x, n, B.dz, accumulate, st, 1, gs)) != EE_OK)
+    if ((s = phase_exit_backward(cfg, B, P, G, x, n, B.dz, accumulate, st, 1, gs, af)) != EE_OK)
       return s;
+    if (af) {  // the gains' Adam (their gradients are column sums, in B.gsc)
+      const int gk[2] = {4, 0};
+      for (int j = 0; j < 2; ++j) {
+        const AdamOut& t = af->t[gk[j]];
+        if (!tensor_needed(cfg, gk[j])) continue;
+        const AdamScal& c = af->sc;
+        Prof p_("a15_adam_gain", st, 0, 0, 30.0 * cfg->hidden);
+        EE_CUDA(launch_adam(t.th, nullptr, (float*)t.op, B.gsc + (size_t)j * cfg->hidden, t.m,
+                            t.v, cfg->hidden, c.lr, c.b1, c.b2, c.eps, c.wd, c.bc1, c.bc2, c.gs,
+                            st));
+      }
+    }
   }
   return EE_OK;
+}
+
+ee_status ee_tune_step_adam(const ee_head_config* cfg, const void* const* hidden,
+                            int64_t n_tokens, const int32_t* targets, const float* exit_weights,
+                            ee_head_tensors* operand, ee_head_tensors* master, ee_head_tensors* m,
+                            ee_head_tensors* v, float lr, float beta1, float beta2, float eps,
+                            float weight_decay, int64_t step, float grad_scale, float* loss_out,
+                            const ee_step_aux* aux, const int64_t* valid_count, void* workspace,
+                            size_t ws_bytes, void* stream) {
+  ee_status s = check_cfg(cfg);
+  if (s != EE_OK) return s;
+  if (cfg->arch == EE_ARCH_LAYER)
+    return fail(EE_ERR_UNSUPPORTED, "ee_tune_step_adam: Layer exits use ee_tune_step + Adam");
+  if (cfg->token_weighting == EE_WEIGHT_CONFIDENCE_SUM)
+    return fail(EE_ERR_UNSUPPORTED, "ee_tune_step_adam: the gradient must be final in the call");
+  if (!operand || !master || !m || !v) return fail(EE_ERR_ARG, "NULL parameter state");
+  if (step < 1) return fail(EE_ERR_ARG, "step must be >= 1");
+  if (n_tokens <= 0) return fail(EE_ERR_SHAPE, "ee_tune_step_adam needs n_tokens > 0");
+  const int E = cfg->num_exits;
+  if (E > 64) return fail(EE_ERR_SHAPE, "at most 64 exits per call");
+  AdamFuse af[64];
+  const float bc1 = (float)(1.0 - std::pow((double)beta1, (double)step));
+  const float bc2 = (float)(1.0 - std::pow((double)beta2, (double)step));
+  for (int i = 0; i < E; ++i) {
+    if ((s = check_arch_tensors(cfg, operand[i], "operand", i)) != EE_OK) return s;
+    if ((s = check_arch_tensors(cfg, master[i], "master", i)) != EE_OK) return s;
+    if ((s = check_arch_tensors(cfg, m[i], "m", i)) != EE_OK) return s;
+    if ((s = check_arch_tensors(cfg, v[i], "v", i)) != EE_OK) return s;
+    memset(&af[i], 0, sizeof(AdamFuse));
+    af[i].sc = AdamScal{lr, beta1, beta2, eps, weight_decay, bc1, bc2, grad_scale};
+    for (int k = 0; k < NTENS; ++k) {
+      const TInfo& ti = kTens[k];
+      if (!tensor_needed(cfg, k)) continue;
+      float* th = (float*)(master[i].*(ti.f));
+      void* op = operand[i].*(ti.f);
+      if (ti.gain && op == (void*)th) op = nullptr;   // gains may alias their master
+      af[i].t[k] = AdamOut{th, (float*)(m[i].*(ti.f)), (float*)(v[i].*(ti.f)),
+                           (__nv_bfloat16*)op};
+    }
+  }
+  return tune_step_impl(cfg, hidden, n_tokens, targets, exit_weights, operand, nullptr, nullptr,
+                        0, loss_out, aux, valid_count, workspace, ws_bytes, stream, af);
 }
 
 ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int64_t n_tokens,

@@ -51,6 +51,27 @@ enum BMode : int {
   B_KSPLIT = 2,  // k < b_ksplit from tmB0, k >= b_ksplit from tmB1 (K concatenation)
 };
 
+// Adam (A14) on one element, with explicit roundings so
+// the standalone adam_kernel and the fused weight-gradient epilogue
+// (ee_tune_step_adam) produce the same bits.
+struct AdamScal {
+  float lr, b1, b2, eps, wd, bc1, bc2, gs;
+};
+__device__ __forceinline__ void adam_update(float& th, float& m, float& v, float g,
+                                            const AdamScal& s) {
+  g = __fmul_rn(s.gs, g);
+  m = __fmaf_rn(s.b1, m, __fmul_rn(__fsub_rn(1.f, s.b1), g));
+  v = __fmaf_rn(s.b2, v, __fmul_rn(__fmul_rn(__fsub_rn(1.f, s.b2), g), g));
+  const float upd = __fdiv_rn(__fdiv_rn(m, s.bc1), __fadd_rn(__fsqrt_rn(__fdiv_rn(v, s.bc2)), s.eps));
+  th = __fsub_rn(__fsub_rn(th, __fmul_rn(s.lr, upd)), __fmul_rn(__fmul_rn(s.lr, s.wd), th));
+}
+// Parameter state one output of a fused-Adam GEMM updates (row-major like the
+// gradient it replaces): fp32 master, moments, bf16 operand copy.
+struct AdamOut {
+  float *th, *m, *v;
+  __nv_bfloat16* op;
+};
+
 struct GemmArgs {
   int M, N, K;  // N = logical output columns (B_PAIR: columns of each of the two halves)
   int m_blocks, n_blocks, k_blocks;
@@ -77,6 +98,12 @@ struct GemmArgs {
   float* scat[8];
   float* scat1[8];
   int scat_rows;
+  // Fused Adam (adam_on; EPI_F32 / EPI_F32T, accumulate = 0): the finished
+  // accumulator tile IS the gradient; instead of storing it, update
+  // adam0 (rows < m_split / columns < n_split) or adam1 in place.
+  int adam_on;
+  AdamScal adam;
+  AdamOut adam0, adam1;
   const __nv_bfloat16* resid;
   long long ld_resid;
   __nv_bfloat16* outb;  // EPI_BF16 output (ldo)
@@ -181,6 +208,26 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
               }
             }
           }
+          if (EPI == EPI_F32 && args.adam_on) {  // fused Adam on the finished gradient
+            const bool lo = gm < args.m_split;
+            const AdamOut& ao = lo ? args.adam0 : args.adam1;
+            const long long e = (long long)(lo ? gm : gm - args.m_split) * args.ldo + gn;
+            const int cnt = full8 ? 8 : 4;
+            float th[8], mm[8], vv[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (q < cnt) { th[q] = ao.th[e + q]; mm[q] = ao.m[e + q]; vv[q] = ao.v[e + q]; }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (q < cnt) {
+                adam_update(th[q], mm[q], vv[q], o[q], args.adam);
+                ao.th[e + q] = th[q]; ao.m[e + q] = mm[q]; ao.v[e + q] = vv[q];
+              }
+#pragma unroll
+            for (int q = 0; q < 8; q += 2)
+              if (q < cnt) *reinterpret_cast<uint32_t*>(ao.op + e + q) = pack_bf16(th[q], th[q + 1]);
+            continue;
+          }
           if (full8 && aligned32(orow + gn)) {
             uint32_t w[8];
 #pragma unroll
@@ -275,7 +322,17 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int gn = gn0 + j;
-          if (gn < args.N) {
+          if (gn < args.N && args.adam_on) {  // fused Adam: element (row n, column m)
+            const bool lo = gn < args.n_split;
+            const AdamOut& ao = lo ? args.adam0 : args.adam1;
+            const long long e = (long long)(lo ? gn : gn - args.n_split) * args.ldo + gm;
+            float th = ao.th[e], mm = ao.m[e], vv = ao.v[e];
+            adam_update(th, mm, vv, u2f(v[j]), args.adam);
+            ao.th[e] = th;
+            ao.m[e] = mm;
+            ao.v[e] = vv;
+            ao.op[e] = __float2bfloat16_rn(th);
+          } else if (gn < args.N) {
             float* o;
             if (args.scat_rows > 0) {  // fused reduce-scatter to the row-block owner
               const bool hi = gn >= args.n_split;

@@ -675,26 +675,57 @@ cudaError_t launch_first_exit(const float* const* conf, int E, long long n, floa
 __global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ src,
                                       __nv_bfloat16* __restrict__ dst, long long R, int C,
                                       long long ldd) {
-  __shared__ __nv_bfloat16 tile[64][64 + 2];
+  // 64 x 64 tile; 16-byte global loads and stores (8 bf16 per access), rows of
+  // the smem tile padded to 33 words so the column gathers are 2-way conflicted
+  __shared__ uint32_t tile[64][33];
   const long long r0 = (long long)blockIdx.y * 64;
   const int c0 = blockIdx.x * 64;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 256 threads: 32 x 8
-  for (int i = ty; i < 64; i += 8) {
-    const long long r = r0 + i;
+  const bool fast = (C % 8) == 0;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int c = c0 + tx * 2 + k;
-      tile[i][tx * 2 + k] = (r < R && c < C) ? src[r * C + c] : __float2bfloat16_rn(0.f);
+  for (int h = 0; h < 2; ++h) {
+    const int ch = threadIdx.x + h * 256;  // 512 chunks of 8 columns
+    const int i = ch >> 3, j = (ch & 7) * 8;
+    const long long r = r0 + i;
+    const int c = c0 + j;
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+    if (r < R) {
+      if (fast && c + 8 <= C) {
+        const uint4 q = *reinterpret_cast<const uint4*>(src + r * C + c);
+        w[0] = q.x; w[1] = q.y; w[2] = q.z; w[3] = q.w;
+      } else {
+        __nv_bfloat16 e[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) e[k] = (c + k < C) ? src[r * C + c + k] : __float2bfloat16_rn(0.f);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[k] = *reinterpret_cast<const uint32_t*>(&e[2 * k]);
+      }
     }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) tile[i][j / 2 + k] = w[k];
   }
   __syncthreads();
-  for (int i = ty; i < 64; i += 8) {
-    const int c = c0 + i;
-    if (c >= C) continue;
+  const __nv_bfloat16* tb = reinterpret_cast<const __nv_bfloat16*>(&tile[0][0]);
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const long long r = r0 + tx * 2 + k;
-      if (r < R) dst[(long long)c * ldd + r] = tile[tx * 2 + k][i];
+  for (int h = 0; h < 2; ++h) {
+    const int ch = threadIdx.x + h * 256;
+    const int oc = ch >> 3, rr = (ch & 7) * 8;  // output row c0 + oc, rows rr..rr+7 of the tile
+    const int c = c0 + oc;
+    if (c >= C) continue;
+    const long long r = r0 + rr;
+    if (r >= R) continue;
+    __nv_bfloat16 e[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) e[k] = tb[(rr + k) * 66 + oc];
+    __nv_bfloat16* d = dst + (long long)c * ldd + r;
+    if (r + 8 <= R && ((reinterpret_cast<uintptr_t>(d) & 15) == 0)) {
+      uint4 q;
+      q.x = *reinterpret_cast<const uint32_t*>(&e[0]);
+      q.y = *reinterpret_cast<const uint32_t*>(&e[2]);
+      q.z = *reinterpret_cast<const uint32_t*>(&e[4]);
+      q.w = *reinterpret_cast<const uint32_t*>(&e[6]);
+      *reinterpret_cast<uint4*>(d) = q;
+    } else {
+      for (int k = 0; k < 8 && r + k < R; ++k) d[k] = e[k];
     }
   }
 }
@@ -729,14 +760,9 @@ __global__ void adam_kernel(float* __restrict__ th, __nv_bfloat16* op_bf16, floa
     const float* gp = &g4.x;
     float* mp = &m4.x;
     float* vp = &v4.x;
+    const AdamScal sc{lr, b1, b2, eps, wd, bc1, bc2, gs};
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float g = gs * gp[k];
-      mp[k] = b1 * mp[k] + (1.f - b1) * g;
-      vp[k] = b2 * vp[k] + (1.f - b2) * g * g;
-      const float upd = (mp[k] / bc1) / (sqrtf(vp[k] / bc2) + eps);
-      tp[k] = tp[k] - lr * upd - lr * wd * tp[k];
-    }
+    for (int k = 0; k < 4; ++k) adam_update(tp[k], mp[k], vp[k], gp[k], sc);
     reinterpret_cast<float4*>(th)[i] = t;
     reinterpret_cast<float4*>(m)[i] = m4;
     reinterpret_cast<float4*>(v)[i] = v4;
@@ -776,14 +802,9 @@ __global__ void adam_sharded_kernel(float* __restrict__ th, const float* __restr
     const float* gp = &g4.x;
     float* mp = &m4.x;
     float* vp = &v4.x;
+    const AdamScal sc{lr, b1, b2, eps, wd, bc1, bc2, gs};
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float g = gs * gp[k];
-      mp[k] = b1 * mp[k] + (1.f - b1) * g;
-      vp[k] = b2 * vp[k] + (1.f - b2) * g * g;
-      const float upd = (mp[k] / bc1) / (sqrtf(vp[k] / bc2) + eps);
-      tp[k] = tp[k] - lr * upd - lr * wd * tp[k];
-    }
+    for (int k = 0; k < 4; ++k) adam_update(tp[k], mp[k], vp[k], gp[k], sc);
     reinterpret_cast<float4*>(th)[i] = t;
     reinterpret_cast<float4*>(m)[i] = m4;
     reinterpret_cast<float4*>(v)[i] = v4;

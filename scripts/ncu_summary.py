@@ -21,8 +21,8 @@ from collections import OrderedDict
 
 # order of gemm_kernel launches within one MLP exit (api.cu)
 MLP_GEMM_ORDER = ["a2_gateup_swiglu", "a3_down_resid", "a5_vocab_ce_stats",
-                  "a8_dz", "a9_dw_out", "a11_dw_down", "a11_dm_swiglu_bwd", "a12_dw_gateup",
-                  "a12_du"]
+                  "a8_dz", "a9_dw_out", "a11_dm_swiglu_bwd", "a11_dw_down", "a12_du",
+                  "a12_dw_gateup"]
 
 
 def short(name):
