@@ -990,7 +990,7 @@ static ee_status tune_step_impl(const ee_head_config* cfg, const void* const* hi
     const ee_head_tensors& P = params[i];
     ee_head_tensors G0;
     memset(&G0, 0, sizeof(G0));
-    const ee_head_tensors& G = arenas ? G0 : grads[i];
+    const ee_head_tensors& G = (arenas || afuse) ? G0 : grads[i];
     GradScatter gsv;
     const GradScatter* gs = nullptr;
     if (arenas) {
