@@ -305,9 +305,10 @@ def main():
                     help="dp, N>1: fused = gradient reduce-scatter in the weight-gradient GEMM "
                          "epilogues + sharded Adam storing the operands to every rank (CUDA-IPC "
                          "peer memory, ZeRO-1); nccl = NCCL all-reduce + full Adam per rank")
-    ap.add_argument("--no-fused-adam", action="store_true",
-                    help="N=1: separate ee_tune_step + ee_adam_update instead of the Adam "
-                         "update fused into the weight-gradient epilogues (A/B)")
+    ap.add_argument("--fused-adam", action="store_true",
+                    help="N=1: Adam fused into the weight-gradient epilogues "
+                         "(ee_tune_step_adam) instead of ee_tune_step + ee_adam_update; "
+                         "measured slower (profiles/r01f_fused_adam_ab.log), so opt-in")
     ap.add_argument("--force-dp-fused", action="store_true",
                     help="run the fused DP path at N=1 as well (A/B against the plain step)")
     ap.add_argument("--vp-comm", default="fused", choices=["fused", "nccl"],
@@ -391,7 +392,7 @@ def main():
                                          vocab_begin=vb, vocab_end=ve, **attn_kw(cfg)), n_all,
                              device=dev, grad_buffers=gbuf if gbuf > 0 else None)
     fused_adam = (not multi and not vp and not dp_fused and cfg.arch != "layer"
-                  and not args.no_fused_adam)
+                  and args.fused_adam)
     args.fused_adam = fused_adam
     per_exit = (not dp_fused) and (not fused_adam) and heads.grad_buffers < E
     args.per_exit = per_exit
