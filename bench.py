@@ -232,6 +232,8 @@ def workload_config(cfg, world, args):
             "optimizer": "Adam (P:374-375), included in the step",
             "update_schedule": ("per exit, Adam fused into the weight-gradient epilogues "
                                 "(P:261)" if getattr(args, "fused_adam", False) else
+                                "per exit, each exit's Adam on a side stream overlapping the "
+                                "next exit (P:261)" if getattr(args, "overlapped", False) else
                                 "per exit, shared gradient buffers (P:261)"
                                 if getattr(args, "per_exit", False) else
                                 "per exit: tune, barrier, sharded Adam (P:261)"
@@ -394,7 +396,10 @@ def main():
     fused_adam = (not multi and not vp and not dp_fused and cfg.arch != "layer"
                   and args.fused_adam)
     args.fused_adam = fused_adam
-    per_exit = (not dp_fused) and (not fused_adam) and heads.grad_buffers < E
+    # one GPU: exit by exit with Adam overlapped on a side stream (any grad-buffer count)
+    overlapped = not multi and not vp and not dp_fused and not fused_adam
+    args.overlapped = overlapped
+    per_exit = (not dp_fused) and (not fused_adam) and (not overlapped) and heads.grad_buffers < E
     args.per_exit = per_exit
     bb = S.backbone(cfg, device=dev)
     src = []
@@ -449,6 +454,9 @@ def main():
         lr = ee.ee_lr_at(min(it + 1, total_iters), total_iters)
         if fused_adam:     # one GPU: Adam fused into the weight-gradient epilogues
             heads.step_adam(hid, tg, lr)
+            return
+        if overlapped:     # exit by exit, each exit's Adam on a side stream overlapping the next
+            heads.step_overlapped(hid, tg, lr)
             return
         if dp_fused:       # exit by exit: tune -> peer barrier -> sharded Adam
             heads.step(hid, tg, lr, all_reduce=dist.all_reduce if multi else None)
@@ -508,6 +516,8 @@ def main():
     e0.record()
     for it in range(args.steps):
         step(args.warmup + it)
+    if hasattr(heads, "join"):
+        heads.join()            # the last side-stream update is inside the timed region
     e1.record()
     torch.cuda.synchronize()
     if multi:
@@ -528,14 +538,10 @@ def main():
         h_host = [h.cpu().pin_memory() for h in hidden]
         t_host = targets.cpu().pin_memory()
         loss_host = torch.empty(E, dtype=torch.float32).pin_memory()
-        streamed = not multi and not per_exit and not vp and not dp_fused
+        streamed = not multi and not vp and not dp_fused
         if streamed:    # untimed warm-up of the host-input API (staging buffers, copy stream)
             lr_w = ee.ee_lr_at(min(args.warmup + args.steps, total_iters), total_iters)
-            if fused_adam:
-                heads.step_host(h_host, t_host, lr=lr_w)
-            else:
-                heads.step_host(h_host, t_host)
-                heads.adam(lr_w)
+            heads.step_host(h_host, t_host, lr=lr_w, fused_adam=fused_adam)
         torch.cuda.synchronize()
         if multi:
             dist.barrier()
@@ -545,17 +551,15 @@ def main():
             if streamed:   # public API for host-resident hidden states: H2D overlapped per exit
                 lr_e = ee.ee_lr_at(min(args.warmup + args.steps + it + 1, total_iters),
                                    total_iters)
-                if fused_adam:
-                    heads.step_host(h_host, t_host, lr=lr_e)
-                else:
-                    heads.step_host(h_host, t_host)
-                    heads.adam(lr_e)
+                heads.step_host(h_host, t_host, lr=lr_e, fused_adam=fused_adam)
             else:
                 for d_, h_ in zip(hidden, h_host):
                     d_.copy_(h_, non_blocking=True)
                 targets.copy_(t_host, non_blocking=True)
                 step(args.warmup + args.steps + it)
             loss_host.copy_(heads.loss, non_blocking=True)
+        if hasattr(heads, "join"):
+            heads.join()
         a1.record()
         torch.cuda.synchronize()
         te = torch.tensor([a0.elapsed_time(a1) / args.steps], device=dev)
@@ -564,9 +568,9 @@ def main():
         e2e = {"value": job_tokens / (te.item() / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": sum(h.numel() * 2 for h in hidden) + targets.numel() * 4,
                "d2h_bytes_per_step": E * 4, "ms_per_step": te.item(),
-               "api": (("ExitHeads.step_host(lr=...) (per-exit H2D overlapped with compute, "
-                        "Adam fused)" if fused_adam else
-                        "ExitHeads.step_host (per-exit H2D overlapped with compute) + adam")
+               "api": ("ExitHeads.step_host(lr=...) (per-exit H2D overlapped with compute, "
+                       + ("Adam fused into the epilogues)" if fused_adam else
+                          "each exit's Adam on a side stream)")
                        if streamed else "H2D copies + step")}
         del h_host
 

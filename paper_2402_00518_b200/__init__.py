@@ -683,6 +683,7 @@ class ExitHeads:
              valid_count=None):
         if targets.numel() > self.max_tokens:
             raise ValueError("more tokens than the workspace was sized for")
+        self.join()
         w = exit_weights if exit_weights is not None else [1.0] * self.spec.num_exits
         ee_tune_step(self.cfg, hidden, targets, w, self.operand, self.grads, self.loss,
                      self.workspace, accumulate=accumulate, aux=aux, valid_count=valid_count)
@@ -691,6 +692,7 @@ class ExitHeads:
     def infer(self, hidden, threshold):
         """Greedy token, confidence per exit and the first exit reaching
         `threshold` (P:381-386).  Returns (argmax [E] list, conf [E] list, first)."""
+        self.join()
         n = hidden[0].shape[0]
         dev = self.loss.device
         am = [torch.empty(n, dtype=torch.int32, device=dev) for _ in range(self.spec.num_exits)]
@@ -702,9 +704,66 @@ class ExitHeads:
     def adam(self, lr, beta1=0.9, beta2=0.95, eps=1e-5, weight_decay=0.0, grad_scale=1.0):
         if self.grad_buffers < self.spec.num_exits:
             raise RuntimeError("shared gradient buffers: use step_per_exit()")
+        self.join()
         self.step_count += 1
         ee_adam_update(self.cfg, self.master, self.operand, self.grads, self.m, self.v, lr,
                        self.step_count, beta1, beta2, eps, weight_decay, grad_scale)
+
+    # ---- Adam overlapped with the next exit (side stream) -------------------
+    def _adam_side(self):
+        if getattr(self, "_side", None) is None:
+            dev = self.loss.device
+            self._side = torch.cuda.Stream(dev)
+            self._adam_done = [None] * self.spec.num_exits   # exit i's operand updated
+            self._buf_done = [None] * self.grad_buffers      # gradient buffer free again
+        return self._side
+
+    def _before_tune(self, i, st):
+        """Stream `st` may run exit i's step once exit i's previous Adam (which
+        writes its operand) and the Adam that last read i's gradient buffer
+        are done."""
+        for ev in (self._adam_done[i], self._buf_done[i % self.grad_buffers]):
+            if ev is not None:
+                st.wait_event(ev)
+
+    def _adam_async(self, i, lr, st, beta1=0.9, beta2=0.95, eps=1e-5, weight_decay=0.0,
+                    grad_scale=1.0):
+        side = self._side
+        ev = torch.cuda.Event()
+        ev.record(st)
+        side.wait_event(ev)
+        ee_adam_update(self.exit_cfg, self.master[i:i + 1], self.operand[i:i + 1],
+                       self.grads[i:i + 1], self.m[i:i + 1], self.v[i:i + 1], lr,
+                       self.step_count, beta1, beta2, eps, weight_decay, grad_scale, stream=side)
+        done = torch.cuda.Event()
+        done.record(side)
+        self._adam_done[i] = done
+        self._buf_done[i % self.grad_buffers] = done
+
+    def step_overlapped(self, hidden, targets, lr, exit_weights=None, valid_count=None,
+                        beta1=0.9, beta2=0.95, eps=1e-5, weight_decay=0.0, grad_scale=1.0):
+        """One step exit by exit with each exit's Adam on a side stream,
+        overlapping the next exit's GEMMs (and, across steps, the next step):
+        exit i's next tune waits only for exit i's Adam.  Same results as
+        step() + adam() (the same kernels on the same data).  Call join()
+        before reading parameters or timing."""
+        E = self.spec.num_exits
+        w = exit_weights if exit_weights is not None else [1.0] * E
+        st = torch.cuda.current_stream(self.loss.device)
+        self._adam_side()
+        self.step_count += 1
+        for i in range(E):
+            self._before_tune(i, st)
+            ee_tune_step(self.exit_cfg, hidden[i:i + 1], targets, w[i:i + 1],
+                         self.operand[i:i + 1], self.grads[i:i + 1], self.loss[i:i + 1],
+                         self.workspace, valid_count=valid_count)
+            self._adam_async(i, lr, st, beta1, beta2, eps, weight_decay, grad_scale)
+        return self.loss
+
+    def join(self, stream=None):
+        """Make `stream` (default: current) wait for the side-stream updates."""
+        if getattr(self, "_side", None) is not None:
+            (stream or torch.cuda.current_stream(self.loss.device)).wait_stream(self._side)
 
     def step_adam(self, hidden, targets, lr, exit_weights=None, beta1=0.9, beta2=0.95,
                   eps=1e-5, weight_decay=0.0, grad_scale=1.0):
@@ -713,6 +772,7 @@ class ExitHeads:
         if targets.numel() > self.max_tokens:
             raise ValueError("more tokens than the workspace was sized for")
         w = exit_weights if exit_weights is not None else [1.0] * self.spec.num_exits
+        self.join()
         self.step_count += 1
         ee_tune_step_adam(self.cfg, hidden, targets, w, self.operand, self.master, self.m, self.v,
                           lr, self.step_count, self.loss, self.workspace, beta1, beta2, eps,
@@ -725,14 +785,17 @@ class ExitHeads:
                        self.grads[i:i + 1], self.m[i:i + 1], self.v[i:i + 1], lr, step, beta1,
                        beta2, eps, weight_decay, grad_scale)
 
-    def step_host(self, hidden_host, targets_host, exit_weights=None, lr=None):
+    def step_host(self, hidden_host, targets_host, exit_weights=None, lr=None,
+                  fused_adam=False):
         """One tuning step with the cached hidden states in pinned HOST memory
         (the usual place for them: 4.3 GB per step at the 70B shape).  Exit
         i + 1's hidden states are copied host-to-device on a side stream while
         exit i computes (two device staging buffers, event-ordered), so the
         PCIe/C2C transfer hides under the exit's GEMMs.  Same results as
-        step() on device copies of the same bytes.  With lr given, each exit's
-        Adam update is fused into its backward (ee_tune_step_adam; = step_adam()).
+        step() on device copies of the same bytes.  With lr given, each exit is
+        updated right after its backward: Adam on a side stream overlapping the
+        next exit (= step_overlapped(); call join() before reading parameters),
+        or fused into the backward's epilogues (fused_adam; = step_adam()).
         Returns the device losses."""
         E = self.spec.num_exits
         n, h = hidden_host[0].shape
@@ -750,6 +813,13 @@ class ExitHeads:
         cs = self._copy_stream
         ev_copied, ev_free = self._ev[0], self._ev[1]
         w = exit_weights if exit_weights is not None else [1.0] * E
+        overlap = lr is not None and not fused_adam
+        if overlap:
+            self._adam_side()
+        else:
+            self.join()
+        if lr is not None:
+            self.step_count += 1
         tg.copy_(targets_host, non_blocking=True)
         cs.wait_stream(st)                      # staging buffers free from the last call
         with torch.cuda.stream(cs):
@@ -765,12 +835,14 @@ class ExitHeads:
                     bufs[nb_].copy_(hidden_host[i + 1], non_blocking=True)
                     ev_copied[nb_].record(cs)
             st.wait_event(ev_copied[b])
-            if lr is None:
+            if lr is None or overlap:
+                if overlap:
+                    self._before_tune(i, st)
                 ee_tune_step(self.exit_cfg, [bufs[b]], tg, w[i:i + 1], self.operand[i:i + 1],
                              self.grads[i:i + 1], self.loss[i:i + 1], self.workspace)
+                if overlap:
+                    self._adam_async(i, lr, st)
             else:
-                if i == 0:
-                    self.step_count += 1
                 ee_tune_step_adam(self.exit_cfg, [bufs[b]], tg, w[i:i + 1],
                                   self.operand[i:i + 1], self.master[i:i + 1], self.m[i:i + 1],
                                   self.v[i:i + 1], lr, self.step_count, self.loss[i:i + 1],
@@ -788,6 +860,7 @@ class ExitHeads:
         E = self.spec.num_exits
         k = self.grad_buffers
         w = exit_weights if exit_weights is not None else [1.0] * E
+        self.join()
         self.step_count += 1
         pending = {}
 

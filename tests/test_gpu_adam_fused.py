@@ -110,3 +110,31 @@ def test_fused_adam_first_moment_matches_oracle_gradient(gpu_lib):
                                  1e-3, 0.9, 0.95, 1e-5, 0.0, 1)
         got = hd.master[0][k].cpu().double().numpy()
         assert np.max(np.abs(got - th)) <= 1e-6 + 1e-6 * np.max(np.abs(th)), k
+
+
+@pytest.mark.parametrize("grad_buffers", [None, 1, 2])
+def test_adam_overlapped_on_side_stream_equals_sequential(gpu_lib, grad_buffers):
+    """step_overlapped: exit i's Adam on a side stream overlapping exit i+1
+    (and the next step), ordered by events -- bitwise the per-exit sequential
+    update, also with shared gradient buffers."""
+    ee = gpu_lib
+    cfg = S.Cfg(name="small", hidden=128, vocab=1000, ffn=256, arch="mlp", tokens=256, layers=3,
+                after=[1, 2, 3], init="random", seed=34)
+    hidden = [x.cuda() for x in S.hidden_states(cfg, 256, seed=7)]
+    targets = S.targets(cfg, 256, seed=7).cuda()
+    params = S.head_params(cfg, seed=7)
+    a = _heads(ee, cfg, params, 256)
+    b = _heads(ee, cfg, params, 256, grad_buffers=grad_buffers)
+    for it in range(3):
+        lr = 1e-3 * (it + 1)
+        a.step(hidden, targets)
+        a.adam(lr)
+        b.step_overlapped(hidden, targets, lr)
+    b.join()
+    torch.cuda.synchronize()
+    assert torch.equal(a.loss, b.loss)
+    sa, sb = _state(a), _state(b)
+    for i in range(cfg.exits):
+        for k in sa[i]:
+            for j in range(4):
+                assert torch.equal(sa[i][k][j], sb[i][k][j]), (i, k, j)
