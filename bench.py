@@ -307,6 +307,9 @@ def main():
                     help="dp, N>1: fused = gradient reduce-scatter in the weight-gradient GEMM "
                          "epilogues + sharded Adam storing the operands to every rank (CUDA-IPC "
                          "peer memory, ZeRO-1); nccl = NCCL all-reduce + full Adam per rank")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="N=1: all exits then Adam on one stream (A/B against the default "
+                         "exit-by-exit step with Adam on a side stream)")
     ap.add_argument("--fused-adam", action="store_true",
                     help="N=1: Adam fused into the weight-gradient epilogues "
                          "(ee_tune_step_adam) instead of ee_tune_step + ee_adam_update; "
@@ -397,7 +400,7 @@ def main():
                   and args.fused_adam)
     args.fused_adam = fused_adam
     # one GPU: exit by exit with Adam overlapped on a side stream (any grad-buffer count)
-    overlapped = not multi and not vp and not dp_fused and not fused_adam
+    overlapped = not multi and not vp and not dp_fused and not fused_adam and not args.no_overlap
     args.overlapped = overlapped
     per_exit = (not dp_fused) and (not fused_adam) and (not overlapped) and heads.grad_buffers < E
     args.per_exit = per_exit
@@ -538,10 +541,14 @@ def main():
         h_host = [h.cpu().pin_memory() for h in hidden]
         t_host = targets.cpu().pin_memory()
         loss_host = torch.empty(E, dtype=torch.float32).pin_memory()
-        streamed = not multi and not vp and not dp_fused
+        streamed = not multi and not vp and not dp_fused and not per_exit
         if streamed:    # untimed warm-up of the host-input API (staging buffers, copy stream)
             lr_w = ee.ee_lr_at(min(args.warmup + args.steps, total_iters), total_iters)
-            heads.step_host(h_host, t_host, lr=lr_w, fused_adam=fused_adam)
+            if overlapped or fused_adam:
+                heads.step_host(h_host, t_host, lr=lr_w, fused_adam=fused_adam)
+            else:
+                heads.step_host(h_host, t_host)
+                heads.adam(lr_w)
         torch.cuda.synchronize()
         if multi:
             dist.barrier()
@@ -551,7 +558,11 @@ def main():
             if streamed:   # public API for host-resident hidden states: H2D overlapped per exit
                 lr_e = ee.ee_lr_at(min(args.warmup + args.steps + it + 1, total_iters),
                                    total_iters)
-                heads.step_host(h_host, t_host, lr=lr_e, fused_adam=fused_adam)
+                if overlapped or fused_adam:
+                    heads.step_host(h_host, t_host, lr=lr_e, fused_adam=fused_adam)
+                else:
+                    heads.step_host(h_host, t_host)
+                    heads.adam(lr_e)
             else:
                 for d_, h_ in zip(hidden, h_host):
                     d_.copy_(h_, non_blocking=True)
