@@ -307,9 +307,10 @@ def main():
                     help="dp, N>1: fused = gradient reduce-scatter in the weight-gradient GEMM "
                          "epilogues + sharded Adam storing the operands to every rank (CUDA-IPC "
                          "peer memory, ZeRO-1); nccl = NCCL all-reduce + full Adam per rank")
-    ap.add_argument("--no-overlap", action="store_true",
-                    help="N=1: all exits then Adam on one stream (A/B against the default "
-                         "exit-by-exit step with Adam on a side stream)")
+    ap.add_argument("--overlap", action="store_true",
+                    help="N=1: exit-by-exit step with each exit's Adam on a side stream "
+                         "(ExitHeads.step_overlapped); measured equal to the default "
+                         "all-exits-then-Adam step (profiles/r01f_adam_overlap_ab.log)")
     ap.add_argument("--fused-adam", action="store_true",
                     help="N=1: Adam fused into the weight-gradient epilogues "
                          "(ee_tune_step_adam) instead of ee_tune_step + ee_adam_update; "
@@ -400,7 +401,7 @@ def main():
                   and args.fused_adam)
     args.fused_adam = fused_adam
     # one GPU: exit by exit with Adam overlapped on a side stream (any grad-buffer count)
-    overlapped = not multi and not vp and not dp_fused and not fused_adam and not args.no_overlap
+    overlapped = not multi and not vp and not dp_fused and not fused_adam and args.overlap
     args.overlapped = overlapped
     per_exit = (not dp_fused) and (not fused_adam) and (not overlapped) and heads.grad_buffers < E
     args.per_exit = per_exit
