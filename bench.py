@@ -501,6 +501,9 @@ def main():
                                heads.loss)
         heads.adam(lr)
 
+    if multi:       # line the ranks up before the first peer barrier (its timeout is 20 s)
+        torch.cuda.synchronize()
+        dist.barrier()
     for it in range(args.warmup):
         step(it)
     torch.cuda.synchronize()
