@@ -651,6 +651,11 @@ def main():
                      "of_datasheet_2250": tflops / 2250.0,
                      "step_flops_alg": F_alg},
         "roofline": roofline,
+        # exit-tokens/s (comparable across exit counts) and the
+        # optimizer's share, reported beside the step that includes it
+        "exit_tokens_per_s": E * job_tokens / (ms / 1e3),
+        "update_ms_per_step": sum(d["ms"] for k, d in kern.items() if k.startswith("a15"))
+                              / args.steps,
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clocks,
