@@ -175,7 +175,7 @@ struct Layout {
   size_t status, vcount, loss_part, lse, coef, tgt, pm, ps, pi, z, ds, dz, dgp, ry, u, rx, ab,
       mact, y, dy, total;
   // Layer exits: attention block activations / gradients
-  size_t u1, r1, q, k, v, o, lse2, x1, da, dq, dk, dv, dvec;
+  size_t u1, r1, q, k, v, o, lse2, x1, da, dq, dk, dv, dvec, rope;
   int nb, nparts, nfin;
 };
 
@@ -240,6 +240,7 @@ Layout make_layout(const ee_head_config* c, long long n) {
     L.dk = take(2 * (size_t)n * hkv);
     L.dv = take(2 * (size_t)n * hkv);
     L.dvec = take(4 * (size_t)n * Hq);
+    L.rope = take(8 * 64 * (size_t)c->seq_len);
   }
   L.total = o;
   return L;
@@ -417,6 +418,7 @@ struct Bufs {
   // Layer exits
   __nv_bfloat16 *u1, *q, *k, *v, *o, *da, *dq, *dk, *dv;
   float *r1, *lse2, *x1, *dvec;
+  float2* rope;
   // vocab-parallel merge state
   float* m_loc;
   float* gsc;  // [2 x h] gain gradients of ee_tune_step_adam
@@ -474,6 +476,7 @@ Bufs make_bufs(const ee_head_config* cfg, long long n, void* workspace) {
     B.dk = (__nv_bfloat16*)(ws + L.dk);
     B.dv = (__nv_bfloat16*)(ws + L.dv);
     B.dvec = (float*)(ws + L.dvec);
+    B.rope = (float2*)(ws + L.rope);
   }
   return B;
 }
@@ -494,6 +497,7 @@ ee_status layer_attn_forward(const ee_head_config* cfg, const Bufs& B, const ee_
     const char* name;
   } projs[3] = {{P.w_q, B.q, h, "L2_q_proj"}, {P.w_k, B.k, hkv, "L2_k_proj"},
                 {P.w_v, B.v, hkv, "L2_v_proj"}};
+  EE_CUDA(launch_rope_table(B.rope, cfg->seq_len, cfg->rope_theta, st));
   for (int j = 0; j < 3; ++j) {  // L3: RoPE fused into the q / k epilogues (fp32, one rounding)
     const Proj& pj = projs[j];
     GemmArgs a = base_args((int)n, pj.N, h);
@@ -502,6 +506,7 @@ ee_status layer_attn_forward(const ee_head_config* cfg, const Bufs& B, const ee_
     if (j < 2) {
       a.rope_seq = cfg->seq_len;
       a.rope_theta = cfg->rope_theta;
+      a.rope_tab = B.rope;
     }
     Mat A{B.u1, n, h, h}, Bm{pj.w, pj.N, h, h};
     Prof p_(pj.name, st, 2.0 * n * pj.N * h, 2.0 * n * pj.N * h, 0);
@@ -562,7 +567,7 @@ ee_status layer_attn_backward(const ee_head_config* cfg, const Bufs& B, const ee
     Prof p_("L8_attn_bwd", st, fe, fa, 0);
     EE_CUDA(launch_attn_bwd(B.q, B.k, B.v, B.o, B.da, B.lse2, B.dvec, B.dq, B.dk, B.dv, n,
                             cfg->seq_len, Hq, Hkv, cfg->rope_theta, st,
-                            attn_tc_mode() != 0)); }  // + L9 RoPE^T fused
+                            attn_tc_mode() != 0, B.rope)); }  // + L9 RoPE^T fused
   { Prof p_("transpose_u1", st, 0, 0, 4.0 * n * h);
   EE_CUDA(launch_transpose_bf16(B.u1, B.uT, n, h, B.L.ldT, st)); }
   struct WG {
@@ -1140,7 +1145,7 @@ static ee_status check_backbone(const ee_backbone_config* c) {
 }
 
 struct BbLayout {
-  size_t x, u, q, k, v, o, ab, m, r, total;
+  size_t x, u, q, k, v, o, ab, m, r, rope, total;
 };
 static BbLayout bb_layout(const ee_backbone_config* c, long long n) {
   BbLayout L{};
@@ -1160,6 +1165,7 @@ static BbLayout bb_layout(const ee_backbone_config* c, long long n) {
   L.ab = take(2 * (size_t)n * 2 * F);
   L.m = take(2 * (size_t)n * F);
   L.r = take(4 * (size_t)(n > 0 ? n : 1));
+  L.rope = take(8 * 64 * (size_t)c->seq_len);
   L.total = off;
   return L;
 }
@@ -1213,6 +1219,8 @@ ee_status ee_backbone_forward(const ee_backbone_config* cfg, const ee_layer_tens
   __nv_bfloat16* ab = (__nv_bfloat16*)(ws + L.ab);
   __nv_bfloat16* mact = (__nv_bfloat16*)(ws + L.m);
   float* r = (float*)(ws + L.r);
+  float2* rope = (float2*)(ws + L.rope);
+  EE_CUDA(launch_rope_table(rope, cfg->seq_len, cfg->rope_theta, st));
   const int h = cfg->hidden, Hq = cfg->n_heads, Hkv = cfg->n_kv_heads, F = cfg->ffn;
   const int hkv = 128 * Hkv;
   { Prof p_("bb_cast_in", st, 0, 0, 6.0 * n * h);
@@ -1236,6 +1244,7 @@ ee_status ee_backbone_forward(const ee_backbone_config* cfg, const ee_layer_tens
       if (j < 2) {
         a.rope_seq = cfg->seq_len;
         a.rope_theta = cfg->rope_theta;
+        a.rope_tab = rope;
       }
       Mat A{u, n, h, h}, B{pj.w, pj.N, h, h};
       Prof p_(pj.name, st, 2.0 * n * pj.N * h, 2.0 * n * pj.N * h, 0);

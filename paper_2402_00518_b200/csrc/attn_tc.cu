@@ -355,15 +355,30 @@ constexpr int FB_SMEM_Q = 1024 + 2 * FA_TILE + FQ_STAGES * 2 * FQ_KT + 256;
 
 // RoPE^T (rotation by -angle) of 32 columns [c0, c0 + 32) (c0 < 64) paired
 // with [c0 + 64, c0 + 96) of one row at position pos.
-__device__ __forceinline__ void rope_t_32(float* a, float* b, int c0, float pos, float theta) {
+// tab: the (cos, sin) row of `pos` of launch_rope_table's table, or NULL
+// (then computed with powf + sincosf in fp32).
+__device__ __forceinline__ void rope_t_32(float* a, float* b, int c0, float pos, float theta,
+                                          const float2* tab) {
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    const float inv = powf(theta, -2.0f * (float)(c0 + i) / 128.0f);
-    float sn, cs;
-    sincosf(pos * inv, &sn, &cs);
-    const float x = a[i], y = b[i];
-    a[i] = x * cs + y * sn;
-    b[i] = y * cs - x * sn;
+  for (int i = 0; i < 32; i += 2) {
+    float csn[4];
+    if (tab) {
+      const float4 t4 = *reinterpret_cast<const float4*>(tab + c0 + i);
+      csn[0] = t4.x; csn[1] = t4.y; csn[2] = t4.z; csn[3] = t4.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float inv = powf(theta, -2.0f * (float)(c0 + i + e) / 128.0f);
+        sincosf(pos * inv, &csn[2 * e + 1], &csn[2 * e]);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const float cs = csn[2 * e], sn = csn[2 * e + 1];
+      const float x = a[i + e], y = b[i + e];
+      a[i + e] = x * cs + y * sn;
+      b[i + e] = y * cs - x * sn;
+    }
   }
 }
 
@@ -371,7 +386,7 @@ __device__ __forceinline__ void rope_t_32(float* a, float* b, int c0, float pos,
 // `pos`, bf16, 256 bytes at dst.
 __device__ __forceinline__ void store_row_bf16(uint32_t tacc, __nv_bfloat16* dst, bool ok,
                                                float scale, float pos, float theta, int c0 = 0,
-                                               int c1 = 2) {
+                                               int c1 = 2, const float2* tab = nullptr) {
 #pragma unroll 1
   for (int c = c0; c < c1; ++c) {
     uint32_t va[32], vb[32];
@@ -385,7 +400,7 @@ __device__ __forceinline__ void store_row_bf16(uint32_t tacc, __nv_bfloat16* dst
       a[i] = __uint_as_float(va[i]) * scale;
       b[i] = __uint_as_float(vb[i]) * scale;
     }
-    if (theta > 0.f) rope_t_32(a, b, c * 32, pos, theta);
+    if (theta > 0.f) rope_t_32(a, b, c * 32, pos, theta, tab);
     if (ok) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -425,7 +440,7 @@ __global__ void __launch_bounds__(384, 1)
                             const float* __restrict__ lse2, const float* __restrict__ Dv,
                             __nv_bfloat16* __restrict__ dk, __nv_bfloat16* __restrict__ dv,
                             int T, int Hq, int Hkv, float scale_log2, float scale,
-                            float rope_theta) {
+                            float rope_theta, const float2* __restrict__ rope_tab) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -621,7 +636,8 @@ __global__ void __launch_bounds__(384, 1)
     const long long ldk = (long long)Hkv * FA_D;
     if (half == 0)
       store_row_bf16(tDK + lane_off, dk + (long long)(k_row0 + kr) * ldk + hk * FA_D, ok, scale,
-                     (float)kpos, rope_theta);
+                     (float)kpos, rope_theta, 0, 2,
+                     rope_tab && ok ? rope_tab + (long long)kpos * 64 : nullptr);
     else
       store_row_bf16(tDV + lane_off, dv + (long long)(k_row0 + kr) * ldk + hk * FA_D, ok, 1.0f,
                      0.f, 0.f);
@@ -646,7 +662,7 @@ __global__ void __launch_bounds__(384, 1)
                           const __grid_constant__ CUtensorMap tmDO,
                           const float* __restrict__ lse2, const float* __restrict__ Dv,
                           __nv_bfloat16* __restrict__ dq, int T, int Hq, int Hkv, float scale_log2,
-                          float scale, float rope_theta) {
+                          float scale, float rope_theta, const float2* __restrict__ rope_tab) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -805,7 +821,8 @@ __global__ void __launch_bounds__(384, 1)
     mbar_wait(acc_done, 0);
     tc_fence_after();
     store_row_bf16(tDQ + lane_off, dq + (long long)(q_row0 + r) * Hq * FA_D + hq * FA_D, ok, scale,
-                   (float)pos, rope_theta, half, half + 1);
+                   (float)pos, rope_theta, half, half + 1,
+                   rope_tab && ok ? rope_tab + (long long)pos * 64 : nullptr);
   }
   tc_fence_before();
   __syncthreads();
@@ -819,7 +836,8 @@ cudaError_t launch_attn_bwd_tc(const __nv_bfloat16* q, const __nv_bfloat16* k,
                                const __nv_bfloat16* v, const __nv_bfloat16* dout,
                                const float* lse2, const float* Dv, __nv_bfloat16* dq,
                                __nv_bfloat16* dk, __nv_bfloat16* dv, long long N, int T, int Hq,
-                               int Hkv, float rope_theta, cudaStream_t s) {
+                               int Hkv, float rope_theta, cudaStream_t s,
+                               const float2* rope_tab) {
   if (N == 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
@@ -846,12 +864,14 @@ cudaError_t launch_attn_bwd_tc(const __nv_bfloat16* q, const __nv_bfloat16* k,
   const unsigned B = (unsigned)(N / T);
   dim3 g1((T + FA_BN - 1) / FA_BN, Hkv, B);
   attn_bwd_dkdv_tc_kernel<<<g1, 384, FB_SMEM_KV, s>>>(tq64, tk, tv, tdo64, lse2, Dv, dk, dv, T, Hq,
-                                                      Hkv, scale_log2, scale, rope_theta);
+                                                      Hkv, scale_log2, scale, rope_theta,
+                                                      rope_tab);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   dim3 g2((T + FA_BM - 1) / FA_BM, Hq, B);
   attn_bwd_dq_tc_kernel<<<g2, 384, FB_SMEM_Q, s>>>(tq128, tk64, tv64, tdo128, lse2, Dv, dq, T, Hq,
-                                                   Hkv, scale_log2, scale, rope_theta);
+                                                   Hkv, scale_log2, scale, rope_theta,
+                                                   rope_tab);
   return cudaGetLastError();
 }
 

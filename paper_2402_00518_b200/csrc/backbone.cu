@@ -501,7 +501,7 @@ cudaError_t launch_attn_bwd(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
                             const __nv_bfloat16* o, const __nv_bfloat16* dout, const float* lse2,
                             float* Dv, __nv_bfloat16* dq, __nv_bfloat16* dk, __nv_bfloat16* dv,
                             long long N, int T, int Hq, int Hkv, float rope_theta,
-                            cudaStream_t s, bool tc) {
+                            cudaStream_t s, bool tc, const float2* rope_tab) {
   if (N == 0) return cudaSuccess;
   const float scale = 1.0f / sqrtf((float)ATT_D);
   const float scale_log2 = 1.4426950408889634f * scale;
@@ -509,7 +509,9 @@ cudaError_t launch_attn_bwd(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
   attn_bwd_dot_kernel<<<(unsigned)((rh * 32 + 255) / 256), 256, 0, s>>>(o, dout, Dv, rh);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  if (tc) return launch_attn_bwd_tc(q, k, v, dout, lse2, Dv, dq, dk, dv, N, T, Hq, Hkv, rope_theta, s);
+  if (tc)
+    return launch_attn_bwd_tc(q, k, v, dout, lse2, Dv, dq, dk, dv, N, T, Hq, Hkv, rope_theta, s,
+                              rope_tab);
   dim3 g1(T / ATT_BK, Hkv, (unsigned)(N / T));
   attn_bwd_dkdv_kernel<<<g1, 128, 0, s>>>(q, k, v, dout, lse2, Dv, dk, dv, T, Hq, Hkv, scale_log2,
                                           scale, rope_theta);

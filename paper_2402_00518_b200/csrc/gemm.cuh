@@ -109,6 +109,7 @@ struct GemmArgs {
   __nv_bfloat16* outb;  // EPI_BF16 output (ldo)
   int rope_seq;         // EPI_BF16: > 0 = apply RoPE (rotate-half, head dim 128; N % 128 == 0)
   float rope_theta;     //   at position row % rope_seq before the bf16 rounding
+  const float2* rope_tab;  // (cos, sin) [rope_seq x 64] (launch_rope_table); NULL: computed
   // SwiGLU
   __nv_bfloat16* ab;  // [M x 2F]: A in columns [0,F), B in [F,2F)
   long long ld_ab;
@@ -263,11 +264,21 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
         for (int q = 0; q < 16; ++q) {
           float ra[2], rb[2];
 #pragma unroll
+          float csn[4];  // cos_i, sin_i, cos_i+1, sin_i+1
+          if (args.rope_tab) {
+            const float4 t4 = *reinterpret_cast<const float4*>(
+                args.rope_tab + (long long)(gm % args.rope_seq) * 64 + c * 32 + 2 * q);
+            csn[0] = t4.x; csn[1] = t4.y; csn[2] = t4.z; csn[3] = t4.w;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const float inv = powf(args.rope_theta, -2.0f * (float)(c * 32 + 2 * q + e) / 128.0f);
+              sincosf(pos * inv, &csn[2 * e + 1], &csn[2 * e]);
+            }
+          }
+#pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int i = c * 32 + 2 * q + e;
-            const float inv = powf(args.rope_theta, -2.0f * (float)i / 128.0f);
-            float sn, cs;
-            sincosf(pos * inv, &sn, &cs);
+            const float cs = csn[2 * e], sn = csn[2 * e + 1];
             const float a = u2f(v0[2 * q + e]), b = u2f(v1[2 * q + e]);
             ra[e] = a * cs - b * sn;
             rb[e] = b * cs + a * sn;

@@ -60,6 +60,8 @@ cudaError_t launch_rmsnorm_bwd(const float* dz, const void* y, bool y_f32, const
                                int h, int rows_per_block, cudaStream_t s,
                                const __nv_bfloat16* add = nullptr,  // dy = add + dx
                                int nslots = 1, long long slot_stride = 0);
+// RoPE (cos, sin) table [T x 64] for the q/k projection epilogues
+cudaError_t launch_rope_table(float2* tab, int T, float theta, cudaStream_t s);
 // stream-ordered barrier over peer signal arrays (int32 [MAX_PEERS] per rank)
 cudaError_t launch_peer_barrier(int* const* sig, int rank, int world, unsigned epoch,
                                 DevStatus* st, cudaStream_t s);
@@ -147,13 +149,15 @@ cudaError_t launch_attn_bwd(const __nv_bfloat16* q, const __nv_bfloat16* k, cons
                             const __nv_bfloat16* o, const __nv_bfloat16* dout, const float* lse2,
                             float* Dv, __nv_bfloat16* dq, __nv_bfloat16* dk, __nv_bfloat16* dv,
                             long long N, int T, int Hq, int Hkv, float rope_theta,
-                            cudaStream_t s, bool tc = false);  // rope_theta > 0: fused RoPE^T
+                            cudaStream_t s, bool tc = false,  // rope_theta > 0: fused RoPE^T
+                            const float2* rope_tab = nullptr);  // (cos, sin) [T x 64] or NULL
 // tcgen05 backward kernels (attn_tc.cu); Dv = rowsum(dO * O) precomputed.
 cudaError_t launch_attn_bwd_tc(const __nv_bfloat16* q, const __nv_bfloat16* k,
                                const __nv_bfloat16* v, const __nv_bfloat16* dout,
                                const float* lse2, const float* Dv, __nv_bfloat16* dq,
                                __nv_bfloat16* dk, __nv_bfloat16* dv, long long N, int T, int Hq,
-                               int Hkv, float rope_theta, cudaStream_t s);
+                               int Hkv, float rope_theta, cudaStream_t s,
+                               const float2* rope_tab = nullptr);
 cudaError_t launch_cast_bf16_f32(const __nv_bfloat16* a, float* b, long long n, cudaStream_t s);
 cudaError_t launch_cast_f32_bf16(const float* a, __nv_bfloat16* b, long long n, cudaStream_t s);
 

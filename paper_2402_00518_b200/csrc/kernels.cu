@@ -234,6 +234,26 @@ cudaError_t launch_rmsnorm_bwd(const float* dz, const void* y, bool y_f32, const
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- RoPE table
+// (cos, sin) of the Llama rotate-half angle pos * theta^(-2i/128) for
+// pos < T, i < 64, evaluated in fp64 and rounded once to fp32 (read by the
+// q/k projection epilogues instead of an fp32 powf + sincosf per element).
+__global__ void rope_table_kernel(float2* __restrict__ tab, int T, double theta) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= T * 64) return;
+  const int pos = idx >> 6, i = idx & 63;
+  const double ang = (double)pos * pow(theta, -2.0 * (double)i / 128.0);
+  double sn, cs;
+  sincos(ang, &sn, &cs);
+  tab[idx] = make_float2((float)cs, (float)sn);
+}
+
+cudaError_t launch_rope_table(float2* tab, int T, float theta, cudaStream_t s) {
+  if (T <= 0) return cudaSuccess;
+  rope_table_kernel<<<(T * 64 + 255) / 256, 256, 0, s>>>(tab, T, (double)theta);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- peer barrier
 // Rank `rank` publishes `epoch` into slot `rank` of every rank's signal array
 // (release at system scope: this stream's earlier kernels, including their
