@@ -812,7 +812,8 @@ ee_status phase_vocab_backward(const ee_head_config* cfg, const Bufs& B, const e
     if (af) set_adam(a, af, 5, -1);
     Mat A{B.zT, h, n, B.L.ldT}, Bm{B.ds, n, Vl, Vl};
     Prof p_("a9_dw_out", st, 2.0 * n * Vl * h, 2.0 * n * Vl * h, 0);
-    EE_CUDA(gemm_run(EPI_F32T, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
+    EE_CUDA(gemm_run(af ? EPI_F32T_ADAM : EPI_F32T, true, false, A, Bm, nullptr, B_PLAIN, 0, a,
+                     st));
   }
   return EE_OK;
 }
@@ -859,7 +860,8 @@ ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee
     if (af) set_adam(a, af, 3, -1);
     Mat A{B.dyT, h, n, B.L.ldT}, Bm{B.mact, n, F, F};
     Prof p_("a11_dw_down", st, 2.0 * n * F * h, 2.0 * n * F * h, 0);
-    EE_CUDA(gemm_run(EPI_F32, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
+    EE_CUDA(gemm_run(af ? EPI_F32_ADAM : EPI_F32, true, false, A, Bm, nullptr, B_PLAIN, 0, a,
+                     st));
   }
   // a12: du = dA W_gate + dB W_up  (K concatenation over the two weights) -> B.dz
   {
@@ -885,7 +887,8 @@ ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee
     if (af) set_adam(a, af, 1, 2);
     Mat A{B.uT, h, n, B.L.ldT}, Bm{B.ab, n, 2LL * F, 2LL * F};
     Prof p_("a12_dw_gateup", st, 4.0 * n * F * h, 4.0 * n * F * h, 0);
-    EE_CUDA(gemm_run(EPI_F32T, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
+    EE_CUDA(gemm_run(af ? EPI_F32T_ADAM : EPI_F32T, true, false, A, Bm, nullptr, B_PLAIN, 0, a,
+                     st));
   }
   if (!layer) {
     // a13: dg_a = sum_t du_t * xhat_t  (no dx: frozen backbone)

@@ -231,6 +231,8 @@ cudaError_t gemm_run(int epi, bool a_kmajor, bool b_kmajor, const Mat& A, const 
   EE_GEMM_CASE(EPI_CE_STATS, false, false)
   EE_GEMM_CASE(EPI_CE_DS, false, false)
   EE_GEMM_CASE(EPI_F32T, false, true)
+  EE_GEMM_CASE(EPI_F32_ADAM, false, true)
+  EE_GEMM_CASE(EPI_F32T_ADAM, false, true)
   EE_GEMM_CASE(EPI_BF16, false, false)
   EE_GEMM_CASE(EPI_BF16, false, true)
 #undef EE_GEMM_CASE

@@ -43,6 +43,8 @@ enum EpiKind : int {
   EPI_CE_DS = 5,       // dS = coef * (exp(S - lse) - onehot(y)) -> bf16
   EPI_F32T = 6,        // out^T: out[n][m] = acc (or +=), columns n >= n_split go to out1
   EPI_BF16 = 7,        // outb[m][n] = bf16(acc)   (backbone projections)
+  EPI_F32_ADAM = 8,    // EPI_F32 whose finished tile is a gradient: Adam in place (adam0/1)
+  EPI_F32T_ADAM = 9,   // EPI_F32T likewise (ee_tune_step_adam)
 };
 
 enum BMode : int {
@@ -165,10 +167,10 @@ __device__ __forceinline__ void store16_bf16(__nv_bfloat16* p, const uint32_t (&
 template <int EPI>
 __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb, int gm, int nb) {
   const bool row_ok = gm < args.M;
-  if constexpr (EPI == EPI_F32 || EPI == EPI_RESID) {
+  if constexpr (EPI == EPI_F32 || EPI == EPI_RESID || EPI == EPI_F32_ADAM) {
     float* orow = nullptr;
     if (row_ok) {
-      if (EPI == EPI_F32 && args.scat_rows > 0) {
+      if (EPI != EPI_RESID && args.scat_rows > 0) {
         const int q = gm / args.scat_rows;
         orow = args.scat[q] + (long long)(gm - q * args.scat_rows) * args.ldo;
       } else {
@@ -209,7 +211,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
               }
             }
           }
-          if (EPI == EPI_F32 && args.adam_on) {  // fused Adam on the finished gradient
+          if constexpr (EPI == EPI_F32_ADAM) {  // fused Adam on the finished gradient
             const bool lo = gm < args.m_split;
             const AdamOut& ao = lo ? args.adam0 : args.adam1;
             const long long e = (long long)(lo ? gm : gm - args.m_split) * args.ldo + gn;
@@ -228,7 +230,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
             for (int q = 0; q < 8; q += 2)
               if (q < cnt) *reinterpret_cast<uint32_t*>(ao.op + e + q) = pack_bf16(th[q], th[q + 1]);
             continue;
-          }
+          } else {
           if (full8 && aligned32(orow + gn)) {
             uint32_t w[8];
 #pragma unroll
@@ -237,6 +239,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
           } else {
             *reinterpret_cast<float4*>(orow + gn) = make_float4(o[0], o[1], o[2], o[3]);
             if (full8) *reinterpret_cast<float4*>(orow + gn + 4) = make_float4(o[4], o[5], o[6], o[7]);
+          }
           }
         }
       }
@@ -318,7 +321,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
         }
       }
     }
-  } else if constexpr (EPI == EPI_F32T) {
+  } else if constexpr (EPI == EPI_F32T || EPI == EPI_F32T_ADAM) {
     // Transposed store: the tile is D' = A'B'^T computed with the operands
     // swapped so that A' is K-major (the fast UMMA path); the caller's output
     // is D'^T.  Thread `row` (m) writes out[n][m]: for each n the 32 threads of
@@ -333,7 +336,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int gn = gn0 + j;
-          if (gn < args.N && args.adam_on) {  // fused Adam: element (row n, column m)
+          if (EPI == EPI_F32T_ADAM && gn < args.N) {  // fused Adam: element (row n, column m)
             const bool lo = gn < args.n_split;
             const AdamOut& ao = lo ? args.adam0 : args.adam1;
             const long long e = (long long)(lo ? gn : gn - args.n_split) * args.ldo + gm;

@@ -119,7 +119,9 @@ __global__ void rmsnorm_fwd_kernel(const TIn* __restrict__ in, const float* __re
       if (ag.n == 0) {
         store8(out + row * h + c * 8, o);
       } else {  // fused all-gather: the same 16 bytes to every rank's z_all (NVLink stores)
-        for (int q = 0; q < ag.n; ++q) store8(ag.p[q] + (ag.row_off + row) * h + c * 8, o);
+#pragma unroll
+        for (int q = 0; q < MAX_PEERS; ++q)  // constant indices: the table stays in param space
+          if (q < ag.n) store8(ag.p[q] + (ag.row_off + row) * h + c * 8, o);
       }
     }
   }
@@ -829,12 +831,16 @@ __global__ void adam_sharded_kernel(float* __restrict__ th, const float* __restr
     reinterpret_cast<float4*>(m)[i] = m4;
     reinterpret_cast<float4*>(v)[i] = v4;
     if (op.f32) {
-      for (int q = 0; q < op.n; ++q) reinterpret_cast<float4*>(op.p[q])[off4 + i] = t;
+#pragma unroll
+      for (int q = 0; q < MAX_PEERS; ++q)
+        if (q < op.n) reinterpret_cast<float4*>(op.p[q])[off4 + i] = t;
     } else {
       uint2 w;
       w.x = pack_bf16(t.x, t.y);
       w.y = pack_bf16(t.z, t.w);
-      for (int q = 0; q < op.n; ++q) reinterpret_cast<uint2*>(op.p[q])[off4 + i] = w;
+#pragma unroll
+      for (int q = 0; q < MAX_PEERS; ++q)
+        if (q < op.n) reinterpret_cast<uint2*>(op.p[q])[off4 + i] = w;
     }
   }
 }
