@@ -583,9 +583,11 @@ def main():
         e2e = {"value": job_tokens / (te.item() / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": sum(h.numel() * 2 for h in hidden) + targets.numel() * 4,
                "d2h_bytes_per_step": E * 4, "ms_per_step": te.item(),
-               "api": ("ExitHeads.step_host(lr=...) (per-exit H2D overlapped with compute, "
-                       + ("Adam fused into the epilogues)" if fused_adam else
-                          "each exit's Adam on a side stream)")
+               "api": (("ExitHeads.step_host(lr=...) (per-exit H2D overlapped with compute, "
+                        + ("Adam fused into the epilogues)" if fused_adam else
+                           "each exit's Adam on a side stream)"))
+                       if streamed and (fused_adam or overlapped) else
+                       "ExitHeads.step_host (per-exit H2D overlapped with compute) + adam"
                        if streamed else "H2D copies + step")}
         del h_host
 
