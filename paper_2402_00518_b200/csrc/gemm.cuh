@@ -215,20 +215,36 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
             const bool lo = gm < args.m_split;
             const AdamOut& ao = lo ? args.adam0 : args.adam1;
             const long long e = (long long)(lo ? gm : gm - args.m_split) * args.ldo + gn;
-            const int cnt = full8 ? 8 : 4;
+            // 8 consecutive elements (e % 8 == 0: ldo and gn are multiples of 8):
+            // 16-byte loads of all three states first, then the update and stores
             float th[8], mm[8], vv[8];
+            const int nq = full8 ? 2 : 1;
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-              if (q < cnt) { th[q] = ao.th[e + q]; mm[q] = ao.m[e + q]; vv[q] = ao.v[e + q]; }
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-              if (q < cnt) {
-                adam_update(th[q], mm[q], vv[q], o[q], args.adam);
-                ao.th[e + q] = th[q]; ao.m[e + q] = mm[q]; ao.v[e + q] = vv[q];
+            for (int h4 = 0; h4 < 2; ++h4)
+              if (h4 < nq) {
+                const float4 a = *reinterpret_cast<const float4*>(ao.th + e + 4 * h4);
+                const float4 b = *reinterpret_cast<const float4*>(ao.m + e + 4 * h4);
+                const float4 c = *reinterpret_cast<const float4*>(ao.v + e + 4 * h4);
+                th[4 * h4] = a.x; th[4 * h4 + 1] = a.y; th[4 * h4 + 2] = a.z; th[4 * h4 + 3] = a.w;
+                mm[4 * h4] = b.x; mm[4 * h4 + 1] = b.y; mm[4 * h4 + 2] = b.z; mm[4 * h4 + 3] = b.w;
+                vv[4 * h4] = c.x; vv[4 * h4 + 1] = c.y; vv[4 * h4 + 2] = c.z; vv[4 * h4 + 3] = c.w;
               }
 #pragma unroll
-            for (int q = 0; q < 8; q += 2)
-              if (q < cnt) *reinterpret_cast<uint32_t*>(ao.op + e + q) = pack_bf16(th[q], th[q + 1]);
+            for (int q = 0; q < 8; ++q)
+              if (q < 4 * nq) adam_update(th[q], mm[q], vv[q], o[q], args.adam);
+#pragma unroll
+            for (int h4 = 0; h4 < 2; ++h4)
+              if (h4 < nq) {
+                *reinterpret_cast<float4*>(ao.th + e + 4 * h4) =
+                    make_float4(th[4 * h4], th[4 * h4 + 1], th[4 * h4 + 2], th[4 * h4 + 3]);
+                *reinterpret_cast<float4*>(ao.m + e + 4 * h4) =
+                    make_float4(mm[4 * h4], mm[4 * h4 + 1], mm[4 * h4 + 2], mm[4 * h4 + 3]);
+                *reinterpret_cast<float4*>(ao.v + e + 4 * h4) =
+                    make_float4(vv[4 * h4], vv[4 * h4 + 1], vv[4 * h4 + 2], vv[4 * h4 + 3]);
+                *reinterpret_cast<uint2*>(ao.op + e + 4 * h4) =
+                    make_uint2(pack_bf16(th[4 * h4], th[4 * h4 + 1]),
+                               pack_bf16(th[4 * h4 + 2], th[4 * h4 + 3]));
+              }
             continue;
           } else {
           if (full8 && aligned32(orow + gn)) {
@@ -332,21 +348,39 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
       tmem_ld_32x32b_x32(tb + c * 32, v);
       tmem_ld_wait();
       const int gn0 = nb * GEMM_BN + c * 32;
-      if (row_ok && gn0 < args.N) {
+      if (EPI == EPI_F32T_ADAM && row_ok && gn0 < args.N) {
+        // fused Adam, element (row n, column m): 16 columns per batch, all 48
+        // state loads issued before the updates and stores (each is a
+        // 128-byte warp-coalesced row segment); batches never straddle n_split
+        // (host: n_split % 16 == 0)
+#pragma unroll
+        for (int jb = 0; jb < 32; jb += 16) {
+          const int gb = gn0 + jb;
+          if (gb >= args.N) continue;
+          const bool lo = gb < args.n_split;
+          const AdamOut& ao = lo ? args.adam0 : args.adam1;
+          const long long e0 = (long long)(lo ? gb : gb - args.n_split) * args.ldo + gm;
+          float th[16], mm[16], vv[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (gb + j < args.N) {
+              const long long e = e0 + (long long)j * args.ldo;
+              th[j] = ao.th[e]; mm[j] = ao.m[e]; vv[j] = ao.v[e];
+            }
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (gb + j < args.N) {
+              adam_update(th[j], mm[j], vv[j], u2f(v[jb + j]), args.adam);
+              const long long e = e0 + (long long)j * args.ldo;
+              ao.th[e] = th[j]; ao.m[e] = mm[j]; ao.v[e] = vv[j];
+              ao.op[e] = __float2bfloat16_rn(th[j]);
+            }
+        }
+      } else if (row_ok && gn0 < args.N) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int gn = gn0 + j;
-          if (EPI == EPI_F32T_ADAM && gn < args.N) {  // fused Adam: element (row n, column m)
-            const bool lo = gn < args.n_split;
-            const AdamOut& ao = lo ? args.adam0 : args.adam1;
-            const long long e = (long long)(lo ? gn : gn - args.n_split) * args.ldo + gm;
-            float th = ao.th[e], mm = ao.m[e], vv = ao.v[e];
-            adam_update(th, mm, vv, u2f(v[j]), args.adam);
-            ao.th[e] = th;
-            ao.m[e] = mm;
-            ao.v[e] = vv;
-            ao.op[e] = __float2bfloat16_rn(th);
-          } else if (gn < args.N) {
+          if (gn < args.N) {
             float* o;
             if (args.scat_rows > 0) {  // fused reduce-scatter to the row-block owner
               const bool hi = gn >= args.n_split;
