@@ -808,6 +808,7 @@ class ExitHeads:
             self._stage_tg = torch.empty(n, dtype=torch.int32, device=dev)
             self._copy_stream = torch.cuda.Stream(dev)
             self._ev = [[torch.cuda.Event(), torch.cuda.Event()] for _ in range(2)]
+            self._stage_used = [False, False]
         bufs = [b[:n] for b in self._stage]
         tg = self._stage_tg[:n]
         cs = self._copy_stream
@@ -821,19 +822,22 @@ class ExitHeads:
         if lr is not None:
             self.step_count += 1
         tg.copy_(targets_host, non_blocking=True)
-        cs.wait_stream(st)                      # staging buffers free from the last call
-        with torch.cuda.stream(cs):
-            bufs[0].copy_(hidden_host[0], non_blocking=True)
-            ev_copied[0].record(cs)
+
+        def stage(b, src):
+            # into staging buffer b once its last reader (this or the previous
+            # call's exit) is done: the first exit of a call is copied while
+            # the previous call's last exit still computes
+            with torch.cuda.stream(cs):
+                if self._stage_used[b]:
+                    cs.wait_event(ev_free[b])
+                bufs[b].copy_(src, non_blocking=True)
+                ev_copied[b].record(cs)
+
+        stage(0, hidden_host[0])
         for i in range(E):
             b = i % 2
             if i + 1 < E:
-                nb_ = (i + 1) % 2
-                with torch.cuda.stream(cs):
-                    if i >= 1:
-                        cs.wait_event(ev_free[nb_])     # exit i-1 done with this buffer
-                    bufs[nb_].copy_(hidden_host[i + 1], non_blocking=True)
-                    ev_copied[nb_].record(cs)
+                stage((i + 1) % 2, hidden_host[i + 1])
             st.wait_event(ev_copied[b])
             if lr is None or overlap:
                 if overlap:
@@ -848,6 +852,7 @@ class ExitHeads:
                                   self.v[i:i + 1], lr, self.step_count, self.loss[i:i + 1],
                                   self.workspace)
             ev_free[b].record(st)
+            self._stage_used[b] = True
         return self.loss
 
     def step_per_exit(self, hidden, targets, lr, exit_weights=None, valid_count=None,

@@ -213,3 +213,26 @@ def test_step_host_streaming_equals_device_step(gpu_lib):
     for i in range(3):
         for k in ga[i]:
             assert torch.equal(ga[i][k], a.grads[i][k]), (i, k)
+
+
+@pytest.mark.parametrize("exits", [2, 3])
+def test_step_host_back_to_back_calls(gpu_lib, exits):
+    """Calls issued back to back without host synchronisation (the next call's
+    first exit is staged while the previous call's last exit computes): each
+    call's losses equal the device step on the same inputs, bitwise, for
+    alternating input sets (a staging-buffer race would mix them)."""
+    cfg = S.Cfg(name="small", hidden=128, vocab=1000, ffn=256, arch="mlp", tokens=300,
+                layers=exits, after=list(range(1, exits + 1)), init="random", seed=43)
+    spec = gpu_lib.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, exits, cfg.arch)
+    a = gpu_lib.ExitHeads(spec, 300)
+    a.init("random", seed=10)
+    sets = [(S.hidden_states(cfg, 300, seed=s), S.targets(cfg, 300, seed=s)) for s in (1, 2)]
+    want = [a.step([h.cuda() for h in hs], t.cuda()).clone() for hs, t in sets]
+    host = [([h.pin_memory() for h in hs], t.pin_memory()) for hs, t in sets]
+    got = []
+    for r in range(4):
+        hs, t = host[r % 2]
+        got.append(a.step_host(hs, t).clone())
+    torch.cuda.synchronize()
+    for r in range(4):
+        assert torch.equal(got[r], want[r % 2]), r
