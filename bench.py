@@ -397,8 +397,7 @@ def main():
         heads = ee.ExitHeads(ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch,
                                          vocab_begin=vb, vocab_end=ve, **attn_kw(cfg)), n_all,
                              device=dev, grad_buffers=gbuf if gbuf > 0 else None)
-    fused_adam = (not multi and not vp and not dp_fused and cfg.arch != "layer"
-                  and args.fused_adam)
+    fused_adam = not multi and not vp and not dp_fused and args.fused_adam
     args.fused_adam = fused_adam
     # one GPU: exit by exit with Adam overlapped on a side stream (any grad-buffer count)
     overlapped = not multi and not vp and not dp_fused and not fused_adam and args.overlap

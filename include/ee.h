@@ -455,8 +455,9 @@ ee_status ee_adam_update(const ee_head_config* cfg, ee_head_tensors* master,
  * applies Adam to master/m/v at those elements and stores the bf16 operand
  * (the backward GEMMs that read a weight run before the one that updates it).
  * The gains' column-sum gradients go through the workspace and a small Adam.
- * One GPU (the whole gradient is local); Embedding/Norm/MLP exits; uniform or
- * CONFIDENCE token weights; n_tokens > 0.  operand/master/m/v as in
+ * One GPU (the whole gradient is local); every arch (Layer: W_o before L6 and
+ * W_q/k/v before L10 are read first); uniform or CONFIDENCE token weights;
+ * n_tokens > 0.  operand/master/m/v as in
  * ee_adam_update, [E] each. */
 ee_status ee_tune_step_adam(const ee_head_config* cfg, const void* const* hidden,
                             int64_t n_tokens, const int32_t* targets, const float* exit_weights,

@@ -192,7 +192,7 @@ Layout make_layout(const ee_head_config* c, long long n) {
     return r;
   };
   L.status = take(sizeof(DevStatus));
-  L.gsc = take(4 * 2 * (size_t)h);  // fused Adam: g_f / g_a gradients
+  L.gsc = take(4 * 3 * (size_t)h);  // fused Adam: g_f / g_a / g_att gradients
   L.vcount = take(8);
   L.loss_part = take(4 * (size_t)(L.nfin > 0 ? L.nfin : 1));
   L.wsum_part = take(4 * (size_t)(L.nfin > 0 ? L.nfin : 1));
@@ -536,12 +536,23 @@ ee_status layer_attn_forward(const ee_head_config* cfg, const Bufs& B, const ee_
 struct GradScatter;
 static void set_scatter(GemmArgs& a, const GradScatter* gs, int k, int k1);
 static float* scatter_gain(const GradScatter* gs, int k);
+struct AdamFuse;
+static void set_adam(GemmArgs& a, const AdamFuse* af, int k, int k1);
 
 ee_status layer_attn_backward(const ee_head_config* cfg, const Bufs& B, const ee_head_tensors& P,
                               const ee_head_tensors& G, const __nv_bfloat16* x, long long n,
-                              int accumulate, cudaStream_t st, const GradScatter* gs = nullptr) {
+                              int accumulate, cudaStream_t st, const GradScatter* gs = nullptr,
+                              const AdamFuse* af = nullptr, float* gain_grad = nullptr) {
   const int h = cfg->hidden, Hq = cfg->n_heads, Hkv = cfg->n_kv_heads, hkv = 128 * Hkv;
   const int nparts = (int)((n + NORM_RPB - 1) / NORM_RPB);
+  {  // L7: da = dx1 W_o  (W_o read MN-major in place; before L6, which may update W_o)
+    GemmArgs a = base_args((int)n, h, h);
+    a.outb = B.da;
+    a.ldo = h;
+    Mat A{B.dy, n, h, h}, Bm{P.w_o, h, h, h};
+    Prof p_("L7_da", st, 2.0 * n * h * h, 2.0 * n * h * h, 0);
+    EE_CUDA(gemm_run(EPI_BF16, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
+  }
   {  // L6: dW_o = dx1^T o  (A = dx1^T K-major copy, B = o MN-major)
     { Prof p_("transpose_dx1", st, 0, 0, 4.0 * n * h);
     EE_CUDA(launch_transpose_bf16(B.dy, B.dyT, n, h, B.L.ldT, st)); }
@@ -550,17 +561,11 @@ ee_status layer_attn_backward(const ee_head_config* cfg, const Bufs& B, const ee
     a.ldo = h;
     a.accumulate = accumulate;
     if (gs) set_scatter(a, gs, 10, -1);
+    if (af) set_adam(a, af, 10, -1);
     Mat A{B.dyT, h, n, B.L.ldT}, Bm{B.o, n, h, h};
     Prof p_("L6_dw_o", st, 2.0 * n * h * h, 2.0 * n * h * h, 0);
-    EE_CUDA(gemm_run(EPI_F32, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
-  }
-  {  // L7: da = dx1 W_o  (W_o read MN-major in place)
-    GemmArgs a = base_args((int)n, h, h);
-    a.outb = B.da;
-    a.ldo = h;
-    Mat A{B.dy, n, h, h}, Bm{P.w_o, h, h, h};
-    Prof p_("L7_da", st, 2.0 * n * h * h, 2.0 * n * h * h, 0);
-    EE_CUDA(gemm_run(EPI_BF16, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
+    EE_CUDA(gemm_run(af ? EPI_F32_ADAM : EPI_F32, true, false, A, Bm, nullptr, B_PLAIN, 0, a,
+                     st));
   }
   { const double fa = 4.0 * (double)n * h * (cfg->seq_len + 1);    // dV, dP, dQ, dK
     const double fe = 7.0 * (double)n * h * (cfg->seq_len + 64);   // + S twice, dP twice
@@ -580,17 +585,6 @@ ee_status layer_attn_backward(const ee_head_config* cfg, const Bufs& B, const ee
   } wg[3] = {{B.dq, G.w_q, P.w_q, h, "L10_dw_q", "L11_du1_q", 7},
              {B.dk, G.w_k, P.w_k, hkv, "L10_dw_k", "L11_du1_k", 8},
              {B.dv, G.w_v, P.w_v, hkv, "L10_dw_v", "L11_du1_v", 9}};
-  for (const WG& w : wg) {  // L10: dW^T = u1^T d (A = u1^T K-major, B = d MN-major), stored transposed
-    GemmArgs a = base_args(h, w.N, (int)n);
-    a.out0 = (float*)w.g;
-    a.ldo = h;
-    a.n_split = w.N;
-    a.accumulate = accumulate;
-    if (gs) set_scatter(a, gs, w.k, -1);
-    Mat A{B.uT, h, n, B.L.ldT}, Bm{w.d, n, w.N, w.N};
-    Prof p_(w.name, st, 2.0 * n * w.N * h, 2.0 * n * w.N * h, 0);
-    EE_CUDA(gemm_run(EPI_F32T, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
-  }
   for (int j = 0; j < 3; ++j) {  // L11: du1 (+)= d W  (W read MN-major in place) -> B.dz
     const WG& w = wg[j];
     GemmArgs a = base_args((int)n, h, w.N);
@@ -601,10 +595,24 @@ ee_status layer_attn_backward(const ee_head_config* cfg, const Bufs& B, const ee
     Prof p_(w.dname, st, 2.0 * n * w.N * h, 2.0 * n * w.N * h, 0);
     EE_CUDA(gemm_run(EPI_F32, true, false, A, Bm, nullptr, B_PLAIN, 0, a, st));
   }
+  for (const WG& w : wg) {  // L10 (after L11, which reads W_q/k/v): dW^T = u1^T d (A = u1^T K-major, B = d MN-major), stored transposed
+    GemmArgs a = base_args(h, w.N, (int)n);
+    a.out0 = (float*)w.g;
+    a.ldo = h;
+    a.n_split = w.N;
+    a.accumulate = accumulate;
+    if (gs) set_scatter(a, gs, w.k, -1);
+    if (af) set_adam(a, af, w.k, -1);
+    Mat A{B.uT, h, n, B.L.ldT}, Bm{w.d, n, w.N, w.N};
+    Prof p_(w.name, st, 2.0 * n * w.N * h, 2.0 * n * w.N * h, 0);
+    EE_CUDA(gemm_run(af ? EPI_F32T_ADAM : EPI_F32T, true, false, A, Bm, nullptr, B_PLAIN, 0, a,
+                     st));
+  }
   { Prof p_("L12_gain_grad", st, 0, 0, 6.0 * n * h);
   EE_CUDA(launch_gain_grad(B.dz, x, B.r1, B.dgp, n, h, NORM_RPB, st)); }
   { Prof p_("reduce_cols", st, 0, 0, 4.0 * nparts * h);
-  EE_CUDA(launch_reduce_cols(B.dgp, nparts, h, gs ? scatter_gain(gs, 6) : (float*)G.g_att,
+  EE_CUDA(launch_reduce_cols(B.dgp, nparts, h,
+                             gs ? scatter_gain(gs, 6) : af ? gain_grad : (float*)G.g_att,
                              accumulate, st)); }
   return EE_OK;
 }
@@ -904,7 +912,7 @@ ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee
   EE_CUDA(launch_reduce_cols(B.dgp, nparts, h,
                              gs ? gs->p[0][0] : af ? B.gsc + h : (float*)G.g_a, accumulate,
                              st)); }
-  if (layer) return layer_attn_backward(cfg, B, P, G, x, n, accumulate, st, gs);
+  if (layer) return layer_attn_backward(cfg, B, P, G, x, n, accumulate, st, gs, af, B.gsc + 2 * h);
   return EE_OK;
 }
 
@@ -1037,8 +1045,8 @@ static ee_status tune_step_impl(const ee_head_config* cfg, const void* const* hi
     if ((s = phase_exit_backward(cfg, B, P, G, x, n, B.dz, accumulate, st, 1, gs, af)) != EE_OK)
       return s;
     if (af) {  // the gains' Adam (their gradients are column sums, in B.gsc)
-      const int gk[2] = {4, 0};
-      for (int j = 0; j < 2; ++j) {
+      const int gk[3] = {4, 0, 6};
+      for (int j = 0; j < 3; ++j) {
         const AdamOut& t = af->t[gk[j]];
         if (!tensor_needed(cfg, gk[j])) continue;
         const AdamScal& c = af->sc;
@@ -1061,8 +1069,6 @@ ee_status ee_tune_step_adam(const ee_head_config* cfg, const void* const* hidden
                             size_t ws_bytes, void* stream) {
   ee_status s = check_cfg(cfg);
   if (s != EE_OK) return s;
-  if (cfg->arch == EE_ARCH_LAYER)
-    return fail(EE_ERR_UNSUPPORTED, "ee_tune_step_adam: Layer exits use ee_tune_step + Adam");
   if (cfg->token_weighting == EE_WEIGHT_CONFIDENCE_SUM)
     return fail(EE_ERR_UNSUPPORTED, "ee_tune_step_adam: the gradient must be final in the call");
   if (!operand || !master || !m || !v) return fail(EE_ERR_ARG, "NULL parameter state");

@@ -138,3 +138,33 @@ def test_adam_overlapped_on_side_stream_equals_sequential(gpu_lib, grad_buffers)
         for k in sa[i]:
             for j in range(4):
                 assert torch.equal(sa[i][k][j], sb[i][k][j]), (i, k, j)
+
+
+def test_fused_adam_layer_exit_bitwise(gpu_lib):
+    """Layer exits (attention block + MLP): the attention weights' updates run
+    after the GEMMs that read them (L7 before L6, L11 before L10); bitwise the
+    separate step + Adam over two steps."""
+    ee = gpu_lib
+    cfg = S.get_cfg("tiny_layer", seed=35)
+    hidden = [x.cuda() for x in S.hidden_states(cfg)]
+    targets = S.targets(cfg).cuda()
+    params = S.head_params(cfg)
+    kw = dict(n_heads=cfg.n_heads, n_kv_heads=cfg.n_kv_heads or cfg.n_heads, seq_len=cfg.seq_len)
+    def mk():
+        hd = ee.ExitHeads(ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, cfg.exits, cfg.arch, **kw),
+                          cfg.tokens)
+        hd.init("copy", copy_src=[{k: v.cuda().float().contiguous() for k, v in p.items()}
+                                  for p in params], src_dtype=torch.float32)
+        return hd
+    a, b = mk(), mk()
+    for it in range(2):
+        a.step(hidden, targets)
+        a.adam(1e-3 * (it + 1))
+        b.step_adam(hidden, targets, 1e-3 * (it + 1))
+    torch.cuda.synchronize()
+    assert torch.equal(a.loss, b.loss)
+    sa, sb = _state(a), _state(b)
+    for i in range(cfg.exits):
+        for k in sa[i]:
+            for j in range(4):
+                assert torch.equal(sa[i][k][j], sb[i][k][j]), (i, k, j)
