@@ -64,3 +64,63 @@ def test_null_arguments_rejected_before_any_device_work():
                          None, 0, None)
     assert r == 1                                             # EE_ERR_ARG
     assert b"NULL" in lib.ee_last_error()
+
+
+@pytest.mark.parametrize("arch", ["embedding", "norm", "mlp", "layer"])
+def test_dp_shard_layout_is_a_partition(arch):
+    """ee_dp_shard_layout (host function of the fused DP path): every tensor's
+    rows are covered exactly once by the P owners' row blocks, each rank's
+    arena blocks are disjoint, in ee_head_tensors order, sized P x rows x C,
+    and tile the arena; tensors the arch lacks own nothing."""
+    ee.load()
+    kw = dict(n_heads=2, n_kv_heads=1, seq_len=128) if arch == "layer" else {}
+    h, V, F = 256, 1000, 384
+    c = ee.make_config(h, V, F, 1, arch, **kw)
+    shapes = ee.tensor_shapes(h, V, F, arch, c.n_kv_heads)
+    for P in (1, 2, 3, 5, 8):
+        for q in range(P):
+            blocks = []
+            for k in ee.TENSOR_NAMES:
+                b, rows, off, total = ee.ee_dp_shard_layout(c, P, q, k)
+                if k not in shapes:
+                    assert rows == 0
+                    continue
+                C = shapes[k][-1]
+                if rows:
+                    blocks.append((off, off + P * rows * C))
+            blocks.sort()
+            pos = 0
+            for lo, hi in blocks:
+                assert lo == pos                               # contiguous, disjoint
+                pos = hi
+            assert pos == total
+        for k, sh in shapes.items():
+            R = 1 if len(sh) == 1 else sh[0]
+            covered = []
+            for q in range(P):
+                b, rows, _, _ = ee.ee_dp_shard_layout(c, P, q, k)
+                covered += list(range(b, b + rows))
+            assert covered == list(range(R)), (P, k)
+    with pytest.raises(ee.EEError):
+        ee.ee_dp_shard_layout(c, 9, 0, "w_out")                # > EE_MAX_PEERS
+
+
+def test_new_entry_points_reject_bad_arguments_without_a_gpu():
+    """Argument validation of the peer-memory / fused-update entry points runs
+    before any device work (synchronous EE_ERR_* codes)."""
+    lib = ee.load()
+    c = ee.make_config(128, 512, 256, 1, "mlp")
+    ps = ee.ee_peer_set()
+    ps.rank, ps.world = 0, 9                                   # > EE_MAX_PEERS
+    assert lib.ee_peer_barrier(ctypes.byref(ps), 1, None, None) == 1
+    ps.world = 1
+    assert lib.ee_peer_barrier(ctypes.byref(ps), 1, None, None) == 1   # NULL workspace
+    assert lib.ee_ipc_get_handle(None, None, None) == 1
+    assert lib.ee_ipc_open(None, 0, None) == 1
+    assert lib.ee_tune_step_rs(ctypes.byref(c), None, 10, None, None, None, None, None, None,
+                               None, None, 0, None) == 1       # NULL grad arenas
+    assert lib.ee_tune_step_adam(ctypes.byref(c), None, 10, None, None, None, None, None, None,
+                                 1e-3, 0.9, 0.95, 1e-5, 0.0, 1, 1.0, None, None, None, None, 0,
+                                 None) == 1                    # NULL parameter state
+    assert lib.ee_vp_exit_backward_slots(ctypes.byref(c), None, 0, 0, None, None, 0, None, 0,
+                                         None, 0, None) == 1   # n_slots = 0
