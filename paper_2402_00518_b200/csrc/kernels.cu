@@ -163,10 +163,8 @@ __global__ void rmsnorm_bwd_kernel(const float* __restrict__ dz, const TY* __res
   }
   const long long r0 = (long long)blockIdx.x * rpb;
   const long long r1 = min(n, r0 + rpb);
-  for (long long row = r0; row < r1; ++row) {
-    const float rr = r[row];
-    float d[NORM_CHUNKS][8], yh[NORM_CHUNKS][8];
-    float dot = 0.f;
+  // Row `row`'s dz (summed over the slots, in slot order) and y into registers.
+  auto load_row = [&](long long row, float (&d)[NORM_CHUNKS][8], float (&yv)[NORM_CHUNKS][8]) {
 #pragma unroll
     for (int i = 0; i < NORM_CHUNKS; ++i) {
       const int c = threadIdx.x + i * blockDim.x;
@@ -178,7 +176,28 @@ __global__ void rmsnorm_bwd_kernel(const float* __restrict__ dz, const TY* __res
 #pragma unroll
           for (int k = 0; k < 8; ++k) d[i][k] += e[k];
         }
-        load8(y + row * h + c * 8, yh[i]);
+        load8(y + row * h + c * 8, yv[i]);
+      }
+    }
+  };
+  float dn[NORM_CHUNKS][8], yn[NORM_CHUNKS][8];  // the next row, loaded one row ahead
+  if (r0 < r1) load_row(r0, dn, yn);
+  for (long long row = r0; row < r1; ++row) {
+    const float rr = r[row];
+    float d[NORM_CHUNKS][8], yh[NORM_CHUNKS][8];
+#pragma unroll
+    for (int i = 0; i < NORM_CHUNKS; ++i)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        d[i][k] = dn[i][k];
+        yh[i][k] = yn[i][k];
+      }
+    if (row + 1 < r1) load_row(row + 1, dn, yn);  // in flight across this row's reduction
+    float dot = 0.f;
+#pragma unroll
+    for (int i = 0; i < NORM_CHUNKS; ++i) {
+      const int c = threadIdx.x + i * blockDim.x;
+      if (c < nchunk) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           yh[i][k] *= rr;
@@ -441,26 +460,40 @@ __global__ void ce_ds_from_p_kernel(__nv_bfloat16* __restrict__ ds, int Vl, long
   const int y = targets[row] - vocab_begin;
   __nv_bfloat16* drow = ds + row * (long long)Vl;
   const int nch = Vl / 8;
-  for (int c = threadIdx.x; c < nch; c += blockDim.x) {
-    const int j = c >> 5;  // 256-column tile of these 8 columns
-    const float f = cf * __expf(pm[(long long)j * n + row] - l);
-    const uint4 q = *reinterpret_cast<const uint4*>(drow + c * 8);
-    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-    float d[8];
+  constexpr int U = 4;  // chunks per thread per iteration: their loads are issued together
+  for (int c0 = threadIdx.x; c0 < nch; c0 += U * blockDim.x) {
+    uint4 q[U];
+    float f[U];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float2 p2 = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
-      d[2 * k] = f * p2.x;
-      d[2 * k + 1] = f * p2.y;
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + u * blockDim.x;
+      if (c < nch) {
+        q[u] = *reinterpret_cast<const uint4*>(drow + c * 8);
+        f[u] = pm[(long long)(c >> 5) * n + row];  // 256-column tile of these 8 columns
+      }
     }
-    const int yo = y - c * 8;
-    if (yo >= 0 && yo < 8) d[yo] = cf * (__expf(tgt_logit[row] - l) - 1.0f);
-    uint4 o;
-    o.x = pack_bf16(d[0], d[1]);
-    o.y = pack_bf16(d[2], d[3]);
-    o.z = pack_bf16(d[4], d[5]);
-    o.w = pack_bf16(d[6], d[7]);
-    *reinterpret_cast<uint4*>(drow + c * 8) = o;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + u * blockDim.x;
+      if (c >= nch) continue;
+      const float fu = cf * __expf(f[u] - l);
+      const uint32_t w[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+      float d[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 p2 = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
+        d[2 * k] = fu * p2.x;
+        d[2 * k + 1] = fu * p2.y;
+      }
+      const int yo = y - c * 8;
+      if (yo >= 0 && yo < 8) d[yo] = cf * (__expf(tgt_logit[row] - l) - 1.0f);
+      uint4 o;
+      o.x = pack_bf16(d[0], d[1]);
+      o.y = pack_bf16(d[2], d[3]);
+      o.z = pack_bf16(d[4], d[5]);
+      o.w = pack_bf16(d[6], d[7]);
+      *reinterpret_cast<uint4*>(drow + c * 8) = o;
+    }
   }
 }
 
