@@ -730,48 +730,40 @@ cudaError_t launch_first_exit(const float* const* conf, int E, long long n, floa
 __global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ src,
                                       __nv_bfloat16* __restrict__ dst, long long R, int C,
                                       long long ldd) {
-  // 128 (rows) x 64 (columns) tile; 16-byte global loads and stores (8 bf16
-  // per access, four per thread in flight); smem rows padded to 33 words so
-  // the column gathers are 2-way conflicted
-  constexpr int TR = 128, NCH = TR * 8 / 256;  // chunks per thread per phase
-  __shared__ uint32_t tile[TR][33];
-  const long long r0 = (long long)blockIdx.y * TR;
+  // 64 x 64 tile; 16-byte global loads and stores (8 bf16 per access), rows of
+  // the smem tile padded to 33 words so the column gathers are 2-way conflicted
+  __shared__ uint32_t tile[64][33];
+  const long long r0 = (long long)blockIdx.y * 64;
   const int c0 = blockIdx.x * 64;
   const bool fast = (C % 8) == 0;
-  uint32_t w[NCH][4];
 #pragma unroll
-  for (int h = 0; h < NCH; ++h) {
-    const int ch = threadIdx.x + h * 256;  // TR * 8 chunks of 8 columns
+  for (int h = 0; h < 2; ++h) {
+    const int ch = threadIdx.x + h * 256;  // 512 chunks of 8 columns
     const int i = ch >> 3, j = (ch & 7) * 8;
     const long long r = r0 + i;
     const int c = c0 + j;
-    w[h][0] = w[h][1] = w[h][2] = w[h][3] = 0u;
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
     if (r < R) {
       if (fast && c + 8 <= C) {
         const uint4 q = *reinterpret_cast<const uint4*>(src + r * C + c);
-        w[h][0] = q.x; w[h][1] = q.y; w[h][2] = q.z; w[h][3] = q.w;
+        w[0] = q.x; w[1] = q.y; w[2] = q.z; w[3] = q.w;
       } else {
         __nv_bfloat16 e[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) e[k] = (c + k < C) ? src[r * C + c + k] : __float2bfloat16_rn(0.f);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) w[h][k] = *reinterpret_cast<const uint32_t*>(&e[2 * k]);
+        for (int k = 0; k < 4; ++k) w[k] = *reinterpret_cast<const uint32_t*>(&e[2 * k]);
       }
     }
-  }
 #pragma unroll
-  for (int h = 0; h < NCH; ++h) {
-    const int ch = threadIdx.x + h * 256;
-    const int i = ch >> 3, j = (ch & 7) * 8;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) tile[i][j / 2 + k] = w[h][k];
+    for (int k = 0; k < 4; ++k) tile[i][j / 2 + k] = w[k];
   }
   __syncthreads();
   const __nv_bfloat16* tb = reinterpret_cast<const __nv_bfloat16*>(&tile[0][0]);
 #pragma unroll
-  for (int h = 0; h < NCH; ++h) {
-    const int ch = threadIdx.x + h * 256;  // 64 output rows x (TR / 8) chunks
-    const int oc = ch / (TR / 8), rr = (ch % (TR / 8)) * 8;
+  for (int h = 0; h < 2; ++h) {
+    const int ch = threadIdx.x + h * 256;
+    const int oc = ch >> 3, rr = (ch & 7) * 8;  // output row c0 + oc, rows rr..rr+7 of the tile
     const int c = c0 + oc;
     if (c >= C) continue;
     const long long r = r0 + rr;
@@ -796,7 +788,7 @@ __global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ src,
 cudaError_t launch_transpose_bf16(const __nv_bfloat16* src, __nv_bfloat16* dst, long long R, int C,
                                   long long ldd, cudaStream_t s) {
   if (R == 0 || C == 0) return cudaSuccess;
-  dim3 grid((C + 63) / 64, (unsigned)((R + 127) / 128));
+  dim3 grid((C + 63) / 64, (unsigned)((R + 63) / 64));
   transpose_bf16_kernel<<<grid, 256, 0, s>>>(src, dst, R, C, ldd);
   return cudaGetLastError();
 }
