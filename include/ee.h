@@ -318,11 +318,17 @@ ee_status ee_vp_vocab_backward_rs(const ee_head_config* cfg, const void* z_all, 
                                   const ee_peer_set* dz_slots, float* loss_out,
                                   const ee_step_aux* aux, int32_t exit_index, void* workspace,
                                   size_t ws_bytes, void* stream);
+/* grad_arenas (NULL: gradients into `grads`): the exit body's gradients are
+ * routed to their owners' arenas as in ee_tune_step_rs (layout of
+ * ee_dp_shard_layout for this cfg; the W_out block is left untouched), for a
+ * sharded update of the replicated exit body (ee_adam_update_sharded with a
+ * tensor_mask without W_out); accumulate must be 0. */
 ee_status ee_vp_exit_backward_slots(const ee_head_config* cfg, const void* hidden,
                                     int64_t n_local, int64_t n_all,
                                     const ee_head_tensors* params, const float* dz_slots,
                                     int32_t n_slots, ee_head_tensors* grads, int32_t accumulate,
-                                    void* workspace, size_t ws_bytes, void* stream);
+                                    const ee_peer_set* grad_arenas, void* workspace,
+                                    size_t ws_bytes, void* stream);
 ee_status ee_peer_barrier(const ee_peer_set* signals, uint32_t epoch, void* workspace,
                           void* stream);
 /* CUDA IPC plumbing for ee_peer_set (host calls, not stream-ordered).
@@ -358,6 +364,9 @@ ee_status ee_peer_barrier(const ee_peer_set* signals, uint32_t epoch, void* work
  * update complete); and before an arena is written again (2 arenas
  * alternating exits need no extra barrier).  Results are bitwise equal to
  * ee_tune_step + a rank-ordered fp32 all-reduce + ee_adam_update.
+ * tensor_mask: bit k (ee_head_tensors order: g_a 0, w_gate 1, w_up 2,
+ * w_down 3, g_f 4, w_out 5, g_att 6, w_q 7, w_k 8, w_v 9, w_o 10) selects the
+ * tensors ee_adam_update_sharded updates; 0 = all.
  * Uniform token weights; every arch (Layer: also W_q, W_k, W_v, W_o, g_att).
  * Ranks sharing one process (tests): CUDA loads kernels lazily and a load
  * waits for the context's running kernels, so one rank's first launch of a
@@ -376,7 +385,7 @@ ee_status ee_adam_update_sharded(const ee_head_config* cfg, int32_t world, int32
                                  ee_head_tensors* m_shard, ee_head_tensors* v_shard,
                                  const ee_peer_set* operands, float lr, float beta1, float beta2,
                                  float eps, float weight_decay, int64_t step, float grad_scale,
-                                 void* stream);
+                                 uint32_t tensor_mask, void* stream);
 
 ee_status ee_ipc_get_handle(const void* dev_ptr, void* handle64, uint64_t* offset);
 ee_status ee_ipc_open(const void* handle64, uint64_t offset, void** dev_ptr);

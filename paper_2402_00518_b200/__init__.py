@@ -136,7 +136,8 @@ def load(path: str = LIB_PATH):
         "ee_vp_vocab_backward_rs": (I32, [CFG, P, I64, P, P, P, F32, P, HT, HT, I32,
                                           ctypes.POINTER(ee_peer_set), P,
                                           ctypes.POINTER(ee_step_aux), I32, P, SZ, P]),
-        "ee_vp_exit_backward_slots": (I32, [CFG, P, I64, I64, HT, P, I32, HT, I32, P, SZ, P]),
+        "ee_vp_exit_backward_slots": (I32, [CFG, P, I64, I64, HT, P, I32, HT, I32,
+                                            ctypes.POINTER(ee_peer_set), P, SZ, P]),
         "ee_peer_barrier": (I32, [ctypes.POINTER(ee_peer_set), ctypes.c_uint32, P, P]),
         "ee_tune_step_adam": (I32, [CFG, ctypes.POINTER(P), I64, P, ctypes.POINTER(F32), HT, HT,
                                     HT, HT, F32, F32, F32, F32, F32, I64, F32, P,
@@ -149,7 +150,7 @@ def load(path: str = LIB_PATH):
                                   P, SZ, P]),
         "ee_adam_update_sharded": (I32, [CFG, I32, I32, ctypes.POINTER(P), HT, HT, HT,
                                          ctypes.POINTER(ee_peer_set), F32, F32, F32, F32, F32,
-                                         I64, F32, P]),
+                                         I64, F32, ctypes.c_uint32, P]),
         "ee_ipc_get_handle": (I32, [P, P, ctypes.POINTER(ctypes.c_uint64)]),
         "ee_ipc_open": (I32, [P, ctypes.c_uint64, ctypes.POINTER(P)]),
         "ee_ipc_close": (I32, [P, ctypes.c_uint64]),
@@ -448,13 +449,17 @@ def ee_vp_vocab_backward_rs(cfg, z_all, targets_all, key_global, sums_global, ex
 
 
 def ee_vp_exit_backward_slots(cfg, hidden, n_all, params, dz_slots, n_slots, grads, workspace,
-                              accumulate=False, stream=None):
-    """a10-a13 with dz = the rank-ordered sum of this rank's n_slots slots."""
+                              accumulate=False, grad_arenas=None, stream=None):
+    """a10-a13 with dz = the rank-ordered sum of this rank's n_slots slots;
+    grad_arenas (ee_peer_set): the body gradients go to their owners' arenas."""
     load()
     n_local = 0 if hidden is None else hidden.shape[0]
     _check(_lib.ee_vp_exit_backward_slots(ctypes.byref(cfg), _ptr(hidden), n_local, int(n_all),
                                           heads([params]), _ptr(dz_slots), int(n_slots),
-                                          heads([grads]), int(bool(accumulate)), _ptr(workspace),
+                                          None if grads is None else heads([grads]),
+                                          int(bool(accumulate)),
+                                          None if grad_arenas is None else
+                                          ctypes.byref(grad_arenas), _ptr(workspace),
                                           workspace.numel(), _stream(stream)))
 
 
@@ -520,7 +525,7 @@ def ee_tune_step_rs(cfg, hidden, targets, exit_weights, params, arenas, loss_out
 
 def ee_adam_update_sharded(cfg, world, rank, arenas_local, master_shard, m_shard, v_shard,
                            operand_sets, lr, step, beta1=0.9, beta2=0.95, eps=1e-5,
-                           weight_decay=0.0, grad_scale=1.0, stream=None):
+                           weight_decay=0.0, grad_scale=1.0, tensors=None, stream=None):
     """Sharded Adam + operand all-gather; operand_sets: per exit a dict
     {name: ee_peer_set of every rank's operand tensor}."""
     load()
@@ -533,6 +538,9 @@ def ee_adam_update_sharded(cfg, world, rank, arenas_local, master_shard, m_shard
     _check(_lib.ee_adam_update_sharded(ctypes.byref(cfg), int(world), int(rank), ar,
                                        heads(master_shard), heads(m_shard), heads(v_shard), ops,
                                        lr, beta1, beta2, eps, weight_decay, int(step), grad_scale,
+                                       ctypes.c_uint32(0 if tensors is None else
+                                                       sum(1 << TENSOR_NAMES.index(k)
+                                                           for k in tensors)),
                                        _stream(stream)))
 
 

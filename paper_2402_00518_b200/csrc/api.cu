@@ -1615,23 +1615,39 @@ ee_status ee_vp_exit_backward_slots(const ee_head_config* cfg, const void* hidde
                                     int64_t n_local, int64_t n_all,
                                     const ee_head_tensors* params, const float* dz_slots,
                                     int32_t n_slots, ee_head_tensors* grads, int32_t accumulate,
-                                    void* workspace, size_t ws_bytes, void* stream) {
+                                    const ee_peer_set* grad_arenas, void* workspace,
+                                    size_t ws_bytes, void* stream) {
   if (n_slots < 1 || n_slots > EE_MAX_PEERS) return fail(EE_ERR_ARG, "n_slots out of range");
   if (dz_slots && !aligned16(dz_slots)) return fail(EE_ERR_ALIGN, "dz_slots misaligned");
   Bufs B;
   ee_status s = vp_common(cfg, n_all, workspace, ws_bytes, &B);
   if (s != EE_OK) return s;
-  if (!params || !grads || n_local < 0 || n_local > n_all ||
+  if (!params || (!grads && !grad_arenas) || n_local < 0 || n_local > n_all ||
       (n_local > 0 && cfg->arch != EE_ARCH_EMBEDDING && (!hidden || !dz_slots)))
     return fail(EE_ERR_ARG, "bad ee_vp_exit_backward_slots arguments");
+  if (grad_arenas) {
+    const ee_peer_set& a = *grad_arenas;
+    if (a.world < 1 || a.world > EE_MAX_PEERS || a.rank < 0 || a.rank >= a.world)
+      return fail(EE_ERR_ARG, "grad_arenas: bad rank/world");
+    for (int q = 0; q < a.world; ++q)
+      if (!a.ptr[q] || !aligned16(a.ptr[q]))
+        return fail(EE_ERR_ALIGN, "grad_arenas.ptr[%d] NULL or misaligned", q);
+    if (accumulate) return fail(EE_ERR_ARG, "grad_arenas: accumulate must be 0");
+  }
   if (ee_status s2 = check_tokens(cfg, n_local); s2 != EE_OK) return s2;
   cudaStream_t st = (cudaStream_t)stream;
   if (n_local == 0) {
+    if (grad_arenas) return fail(EE_ERR_SHAPE, "grad_arenas need n_local > 0");
     if (!accumulate) return zero_grads(cfg, *grads, false, true, st);
     return EE_OK;
   }
-  return phase_exit_backward(cfg, B, *params, *grads, (const __nv_bfloat16*)hidden, n_local,
-                             dz_slots, accumulate, st, n_slots);
+  ee_head_tensors G0;
+  memset(&G0, 0, sizeof(G0));
+  GradScatter gsv;
+  if (grad_arenas) gsv = make_scatter(cfg, *grad_arenas);
+  return phase_exit_backward(cfg, B, *params, grad_arenas ? G0 : *grads,
+                             (const __nv_bfloat16*)hidden, n_local, dz_slots, accumulate, st,
+                             n_slots, grad_arenas ? &gsv : nullptr);
 }
 
 ee_status ee_peer_barrier(const ee_peer_set* signals, uint32_t epoch, void* workspace,
@@ -1802,7 +1818,7 @@ ee_status ee_adam_update_sharded(const ee_head_config* cfg, int32_t world, int32
                                 ee_head_tensors* m_shard, ee_head_tensors* v_shard,
                                 const ee_peer_set* operands, float lr, float beta1, float beta2,
                                 float eps, float wd, int64_t step, float grad_scale,
-                                void* stream) {
+                                uint32_t tensor_mask, void* stream) {
   ee_status s = check_cfg(cfg);
   if (s != EE_OK) return s;
   if (world < 1 || world > EE_MAX_PEERS || rank < 0 || rank >= world || !grad_arenas ||
@@ -1818,6 +1834,7 @@ ee_status ee_adam_update_sharded(const ee_head_config* cfg, int32_t world, int32
       return fail(EE_ERR_ALIGN, "grad_arenas[%d] NULL or misaligned", i);
     for (int k = 0; k < NTENS; ++k) {
       if (!tensor_needed(cfg, k)) continue;
+      if (tensor_mask && !(tensor_mask & (1u << k))) continue;
       long long R, C;
       tensor_rc(cfg, k, &R, &C);
       const long long rows = shard_rows(R, world, rank);

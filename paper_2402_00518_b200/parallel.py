@@ -354,10 +354,11 @@ class GpuPhases:
                                         accumulate=accumulate, aux=aux, exit_index=i,
                                         stream=self.stream)
 
-    def exit_backward_slots(self, hidden, params, peer, grads, accumulate, n_all):
+    def exit_backward_slots(self, hidden, params, peer, grads, accumulate, n_all,
+                            grad_arenas=None):
         self.ee.ee_vp_exit_backward_slots(self.cfg, hidden, n_all, params, peer.slots,
                                           peer.world, grads, self.ws, accumulate=accumulate,
-                                          stream=self.stream)
+                                          grad_arenas=grad_arenas, stream=self.stream)
 
     def barrier(self, peer):
         peer.epoch += 1
@@ -467,9 +468,145 @@ class PeerBuffers:
         self._opened = []
 
 
+class ShardedVPHeads:
+    """Exit heads of one rank under the fused vocab-parallel path with the
+    replicated exit body updated ZeRO-1 style (vocab_parallel_step_fused(...,
+    body=self)): W_out is this rank's [V/P x h] shard (full master, moments,
+    gradient); the body (norm gains, MLP, attention) is held in full as bf16
+    operands (fp32 gains) on every rank but only this rank's row blocks of its
+    fp32 masters and moments, and `n_arenas` arenas collect the other ranks'
+    body-gradient rows (include/ee.h ee_vp_exit_backward_slots grad_arenas,
+    ee_adam_update_sharded tensor_mask).  Call set_lr() before each step."""
+
+    def __init__(self, spec, n_all: int, rank: int, world: int, device="cuda", n_arenas: int = 2):
+        import paper_2402_00518_b200 as ee
+        self.ee, self.spec, self.rank, self.world = ee, spec, rank, world
+        vb, ve = vocab_shard(spec.vocab, world, rank)
+        kw = spec.attn_kwargs()
+        self.cfg = ee.make_config(spec.hidden, spec.vocab, spec.ffn, spec.num_exits, spec.arch,
+                                  spec.norm_eps, vb, ve, **kw)
+        self.exit_cfg = ee.make_config(spec.hidden, spec.vocab, spec.ffn, 1, spec.arch,
+                                       spec.norm_eps, vb, ve, **kw)
+        self.wcfg = ee.make_config(spec.hidden, spec.vocab, 0, 1, "embedding", spec.norm_eps,
+                                   vb, ve)                     # the W_out shard alone
+        shapes = ee.tensor_shapes(spec.hidden, ve - vb, spec.ffn, spec.arch,
+                                  self.cfg.n_kv_heads)
+        self.shapes = shapes
+        self.names = [k for k in ee.TENSOR_NAMES if k in shapes]
+        self.body = [k for k in self.names if k != "w_out"]
+        dev = torch.device(device)
+        E = spec.num_exits
+        self.layout = {k: ee.ee_dp_shard_layout(self.exit_cfg, world, rank, k) for k in self.names}
+        total = self.layout[self.names[0]][3]
+
+        def master_like(k):
+            if k == "w_out":
+                return torch.zeros(shapes[k], dtype=torch.float32, device=dev)
+            return torch.zeros(self.layout[k][1], shapes[k][-1], dtype=torch.float32, device=dev)
+
+        self.operand = [{k: torch.zeros(shapes[k], device=dev,
+                                        dtype=torch.float32 if k.startswith("g_")
+                                        else torch.bfloat16) for k in self.names}
+                        for _ in range(E)]
+        self.master = [{k: master_like(k) for k in self.names} for _ in range(E)]
+        self.m = [{k: master_like(k) for k in self.names} for _ in range(E)]
+        self.v = [{k: master_like(k) for k in self.names} for _ in range(E)]
+        self.grads = [{"w_out": torch.zeros(shapes["w_out"], device=dev)} for _ in range(E)]
+        self.n_arenas = max(1, min(int(n_arenas), E))
+        self.arenas = [torch.zeros(total, dtype=torch.float32, device=dev)
+                       for _ in range(self.n_arenas)]
+        self.workspace = torch.zeros(ee.ee_workspace_size(self.cfg, n_all), dtype=torch.uint8,
+                                     device=dev)
+        self.loss = torch.zeros(E, dtype=torch.float32, device=dev)
+        self.step_count = 0
+        self.lr = 0.0
+        self._opened = []
+
+    def _locals(self):
+        ts = list(self.arenas)
+        for d in self.operand:
+            ts += [d[k] for k in self.body]
+        return ts
+
+    def _set_tables(self, tabs):
+        ee = self.ee
+        na, nb = self.n_arenas, len(self.body)
+        self.arena_sets = [ee.peer_set(self.rank, tabs[j]) for j in range(na)]
+        self.operand_sets = [{k: ee.peer_set(self.rank, tabs[na + i * nb + j])
+                              for j, k in enumerate(self.body)}
+                             for i in range(self.spec.num_exits)]
+
+    def connect_local(self, ranks):
+        tabs, _ = _peer_tables(self.rank, self._locals(), ranks=[r._locals() for r in ranks])
+        self._set_tables(tabs)
+
+    def connect_ipc(self, group=None):
+        tabs, self._opened = _peer_tables(self.rank, self._locals(), group=group)
+        self._set_tables(tabs)
+
+    def close(self):
+        for p, off in self._opened:
+            self.ee.ee_ipc_close(p, off)
+        self._opened = []
+
+    def init(self, mode="copy", copy_src=None, seed=0, std=0.02, src_dtype=torch.bfloat16):
+        """Copy / Random through full-size staging masters (deterministic, so
+        every rank builds the same body operands); keeps this rank's rows."""
+        ee = self.ee
+        dev = self.loss.device
+        E = self.spec.num_exits
+        staging = lambda: {k: torch.zeros(self.shapes[k], dtype=torch.float32, device=dev)
+                           for k in self.names}
+        if mode == "random":
+            full = [staging() for _ in range(E)]
+            ee.ee_init_heads(self.cfg, "random", None, full, self.operand, seed=seed, std=std)
+        else:
+            full = []
+            for i in range(E):
+                f = staging()
+                ee.ee_init_heads(self.exit_cfg, mode, copy_src[i:i + 1], [f],
+                                 self.operand[i:i + 1], src_dtype=src_dtype)
+                full.append(f)
+        for i in range(E):
+            for k in self.names:
+                if k == "w_out":
+                    self.master[i][k].copy_(full[i][k])
+                    continue
+                b, rows = self.layout[k][0], self.layout[k][1]
+                if rows:
+                    self.master[i][k].copy_(full[i][k].reshape(-1, self.shapes[k][-1])[b:b + rows])
+                if k.startswith("g_"):
+                    self.operand[i][k].copy_(full[i][k])
+
+    def set_lr(self, lr):
+        self.lr = lr
+        self.step_count += 1
+
+    def arena_set(self, i):
+        return self.arena_sets[i % self.n_arenas]
+
+    def update(self, i, beta1=0.9, beta2=0.95, eps=1e-5, weight_decay=0.0):
+        """Exit i: sharded Adam of the body rows this rank owns (+ their stores
+        into every rank's operands) and Adam of the local W_out shard."""
+        ee = self.ee
+        if self.body:                                  # (Embedding exits have no body)
+            ee.ee_adam_update_sharded(self.exit_cfg, self.world, self.rank,
+                                      [self.arenas[i % self.n_arenas]], self.master[i:i + 1],
+                                      self.m[i:i + 1], self.v[i:i + 1],
+                                      self.operand_sets[i:i + 1], self.lr, self.step_count,
+                                      beta1, beta2, eps, weight_decay, tensors=self.body)
+        w = lambda d: [{"w_out": d[i]["w_out"]}]
+        ee.ee_adam_update(self.wcfg, w(self.master), w(self.operand), w(self.grads), w(self.m),
+                          w(self.v), self.lr, self.step_count, beta1, beta2, eps, weight_decay)
+
+    def status(self):
+        return self.ee.ee_get_status(self.workspace)
+
+
 def vocab_parallel_step_fused(phases, comm, peer: PeerBuffers, arch: str, hidden_local,
                               targets_all, params, grads, loss: torch.Tensor, exit_weights,
-                              W: torch.Tensor, bufs: dict, accumulate: bool = False, aux=None):
+                              W: torch.Tensor, bufs: dict, accumulate: bool = False, aux=None,
+                              body=None):
     """vocab_parallel_step with the two bulk exchanges inside the kernels:
     a4 stores z into every rank's z_all (all-gather), the a8 epilogue stores
     dz rows into their owners' slots (reduce-scatter; the owner's a10 kernel
@@ -477,10 +614,15 @@ def vocab_parallel_step_fused(phases, comm, peer: PeerBuffers, arch: str, hidden
     stores against the readers: once before the first exit (the previous
     step's readers), after each all-gather and after each reduce-scatter.  The
     CE statistics (8 B + 8 B per token) stay on `comm`, as do the exit-body
-    gradient all-reduces (async).  bufs: key [n_all] int64, sums [n_all x 2]."""
+    gradient all-reduces (async).  bufs: key [n_all] int64, sums [n_all x 2].
+
+    body (ShardedVPHeads): the replicated exit body is updated ZeRO-1 style
+    instead -- its gradient rows go to their owners' arenas in the a11/a12
+    epilogues, and after one more barrier body.update(i) runs the sharded
+    Adam (whose stores are the body operands' all-gather) and the local Adam
+    of the W_out shard; no body all-reduce."""
     key, sums = bufs["key"], bufs["sums"]
     n_all = peer.n_all
-    body = arch != "embedding"
     handles = []
     phases.barrier(peer)
     for i in range(len(hidden_local)):
@@ -494,7 +636,14 @@ def vocab_parallel_step_fused(phases, comm, peer: PeerBuffers, arch: str, hidden
                                  params[i], grads[i], peer, loss[i:i + 1], accumulate,
                                  None if aux is None else aux[i])               # a6-a9 + RS
         phases.barrier(peer)
-        if body:
+        if body is not None:                                  # sharded body update
+            if arch != "embedding":
+                phases.exit_backward_slots(hidden_local[i], params[i], peer, None, False,
+                                           n_all, grad_arenas=body.arena_set(i))  # a10-a13
+            phases.barrier(peer)                              # every partial has landed
+            body.update(i)
+            continue
+        if arch != "embedding":
             phases.exit_backward_slots(hidden_local[i], params[i], peer, grads[i], accumulate,
                                        n_all)                                   # a10-a13
         for k in EXIT_BODY:

@@ -123,4 +123,4 @@ def test_new_entry_points_reject_bad_arguments_without_a_gpu():
                                  1e-3, 0.9, 0.95, 1e-5, 0.0, 1, 1.0, None, None, None, None, 0,
                                  None) == 1                    # NULL parameter state
     assert lib.ee_vp_exit_backward_slots(ctypes.byref(c), None, 0, 0, None, None, 0, None, 0,
-                                         None, 0, None) == 1   # n_slots = 0
+                                         None, None, 0, None) == 1   # n_slots = 0

@@ -268,3 +268,109 @@ def test_fused_vp_two_processes_cuda_ipc(gpu_lib, tmp_path):
         for k in ("g_a", "w_gate", "w_up", "w_down", "g_f"):
             for o in outs:
                 assert rel_fro(o["grads"][i][k].double().numpy(), res.grads[k]) <= GRAD_RTOL, k
+
+
+# ---------------------------------------------------------------------------
+# sharded exit-body update under VP (ShardedVPHeads, body=...)
+# ---------------------------------------------------------------------------
+
+def _run_vp_adam(ee, cfg, P, hidden, targets, params, sharded, steps=2):
+    from paper_2402_00518_b200.parallel import (GpuPhases, PeerBuffers, ShardedVPHeads,
+                                                vocab_parallel_step_fused, vocab_shard)
+    N, h, E = targets.numel(), cfg.hidden, cfg.exits
+    nl = N // P
+    kw = attn_kwargs(cfg)
+    spec = ee.HeadSpec(h, cfg.vocab, cfg.ffn, E, cfg.arch, **kw)
+    shared = {"P": P, "barrier": threading.Barrier(P), "slots": [None] * P}
+    peers = [PeerBuffers(r, P, N, h) for r in range(P)]
+    for b in peers:
+        b.connect_local(peers)
+    zs = [ShardedVPHeads(spec, N, r, P) for r in range(P)] if sharded else None
+    if sharded:
+        for z in zs:
+            z.connect_local(zs)
+    torch.cuda.synchronize()
+    tg = targets.cuda()
+    out, errors = [None] * P, []
+
+    def src(r):
+        vb, ve = vocab_shard(cfg.vocab, P, r)
+        return [{k: (v[vb:ve] if k == "w_out" else v).cuda().float().contiguous()
+                 for k, v in p.items()} for p in params]
+
+    def rank_fn(r):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                comm = StreamThreadComm(shared, r, st)
+                hid = [x[r * nl:(r + 1) * nl].cuda().contiguous() for x in hidden]
+                bufs = {"key": torch.zeros(N, dtype=torch.int64, device="cuda"),
+                        "sums": torch.zeros(N, 2, device="cuda")}
+                W = torch.tensor([int((targets != -1).sum())], dtype=torch.int64, device="cuda")
+                vb, ve = vocab_shard(cfg.vocab, P, r)
+                if sharded:
+                    hd = zs[r]
+                    hd.init("copy", copy_src=src(r), src_dtype=torch.float32)
+                    ph = GpuPhases(ee, hd.exit_cfg, hd.workspace, stream=st)
+                    for it in range(steps):
+                        hd.set_lr(1e-3 * (it + 1))
+                        vocab_parallel_step_fused(ph, comm, peers[r], cfg.arch, hid, tg,
+                                                  hd.operand, hd.grads, hd.loss, [1.0, 0.5], W,
+                                                  bufs, body=hd)
+                    layout = hd.layout
+                else:
+                    hd = ee.ExitHeads(ee.HeadSpec(h, cfg.vocab, cfg.ffn, E, cfg.arch,
+                                                  vocab_begin=vb, vocab_end=ve, **kw), N)
+                    hd.init("copy", copy_src=src(r), src_dtype=torch.float32)
+                    ph = GpuPhases(ee, hd.exit_cfg, hd.workspace, stream=st)
+                    for it in range(steps):
+                        vocab_parallel_step_fused(ph, comm, peers[r], cfg.arch, hid, tg,
+                                                  hd.operand, hd.grads, hd.loss, [1.0, 0.5], W,
+                                                  bufs)
+                        hd.adam(1e-3 * (it + 1))
+                    layout = None
+                st.synchronize()
+                out[r] = ([{k: v.cpu() for k, v in d.items()} for d in hd.operand],
+                          [{k: v.cpu() for k, v in d.items()} for d in hd.master], layout,
+                          hd.loss.cpu(), ee.ee_get_status(hd.workspace, stream=st))
+        except Exception as e:  # surface thread failures
+            errors.append(e)
+            shared["barrier"].abort()
+
+    th = [threading.Thread(target=rank_fn, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    if errors:
+        raise errors[0]
+    return out
+
+
+@pytest.mark.parametrize("arch,P", [("mlp", 2), ("mlp", 4), ("embedding", 2), ("layer", 2)])
+def test_vp_sharded_body_update_bitwise(gpu_lib, arch, P):
+    """VP with the exit body's gradient rows scattered to their owners and a
+    sharded Adam (ZeRO-1 for the replicated body) equals, bit for bit, the
+    fused VP step with the rank-ordered body all-reduce and a full Adam on
+    every rank: all operands on every rank, the W_out shard's master, the
+    body master rows each rank owns."""
+    cfg = _cfg(arch, 37)
+    hidden = S.hidden_states(cfg, 256)
+    targets = S.targets(cfg, 256)
+    params = S.head_params(cfg)
+    _warm_vp = _run_vp_adam(gpu_lib, cfg, 1, hidden, targets, params, sharded=True, steps=1)
+    ref = _run_vp_adam(gpu_lib, cfg, P, hidden, targets, params, sharded=False)
+    got = _run_vp_adam(gpu_lib, cfg, P, hidden, targets, params, sharded=True)
+    for r in range(P):
+        assert got[r][4] == (0, -1), got[r][4]
+        assert torch.equal(got[r][3], ref[r][3])
+        for i in range(cfg.exits):
+            for k, t in ref[r][0][i].items():
+                assert torch.equal(got[r][0][i][k], t), (r, i, k, "operand")
+            for k, full in ref[r][1][i].items():
+                if k == "w_out":
+                    assert torch.equal(got[r][1][i][k], full), (r, i, k)
+                    continue
+                b, rows = got[r][2][k][0], got[r][2][k][1]
+                want = full.reshape(-1, full.shape[-1])[b:b + rows]
+                assert torch.equal(got[r][1][i][k], want), (r, i, k)
