@@ -36,6 +36,8 @@ def main():
     ap.add_argument("--ranks", type=int, default=8)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--sharded-body", action="store_true",
+                    help="ShardedVPHeads: body gradients to owners + sharded Adam")
     a = ap.parse_args()
     ee.load()
     cfg = S.get_cfg(a.config)
@@ -43,15 +45,21 @@ def main():
     n = N // P
     vb, ve = vocab_shard(cfg.vocab, P, 0)
     dev = torch.device("cuda")
-    heads = ee.ExitHeads(ee.HeadSpec(h, cfg.vocab, cfg.ffn, E, cfg.arch, vocab_begin=vb,
-                                     vocab_end=ve), N, device=dev)
+    if a.sharded_body:
+        from paper_2402_00518_b200.parallel import ShardedVPHeads
+        heads = ShardedVPHeads(ee.HeadSpec(h, cfg.vocab, cfg.ffn, E, cfg.arch), N, 0, P,
+                               device=dev)
+        heads.connect_local([heads] * P)
+    else:
+        heads = ee.ExitHeads(ee.HeadSpec(h, cfg.vocab, cfg.ffn, E, cfg.arch, vocab_begin=vb,
+                                         vocab_end=ve), N, device=dev)
     heads.init("random", seed=1)
     hidden = [x[:n].contiguous() for x in S.hidden_states(cfg, N, device=dev)]
     targets = S.targets(cfg, N, device=dev)
     peer = PeerBuffers(0, P, N, h, device=dev)
     peer._tables([peer.z_all] * P, [peer.slots] * P, [peer.sig] * P)
     # the barrier would wait for P - 1 peers that never arrive: every rank is this one
-    phases = GpuPhases(ee, heads.cfg, heads.workspace)
+    phases = GpuPhases(ee, heads.exit_cfg if a.sharded_body else heads.cfg, heads.workspace)
     phases.barrier = lambda pb: None
     bufs = {"key": torch.zeros(N, dtype=torch.int64, device=dev),
             "sums": torch.zeros(N, 2, device=dev)}
@@ -59,6 +67,12 @@ def main():
     ee.ee_count_valid(targets, cfg.vocab, W, heads.workspace)
 
     def step(it):
+        if a.sharded_body:
+            heads.set_lr(1e-4)
+            vocab_parallel_step_fused(phases, LocalComm(), peer, cfg.arch, hidden, targets,
+                                      heads.operand, heads.grads, heads.loss, [1.0] * E, W, bufs,
+                                      body=heads)
+            return
         vocab_parallel_step_fused(phases, LocalComm(), peer, cfg.arch, hidden, targets,
                                   heads.operand, heads.grads, heads.loss, [1.0] * E, W, bufs)
         heads.adam(1e-4)
@@ -82,7 +96,8 @@ def main():
         d[1] += kms
     code, idx = heads.status()
     print(json.dumps({
-        "what": f"rank 0 of {P}: vocab-parallel fused step, compute only (see docstring)",
+        "what": f"rank 0 of {P}: vocab-parallel fused step, compute only (see docstring)"
+                + ("; exit body updated ZeRO-1 style (ShardedVPHeads)" if a.sharded_body else ""),
         "config": a.config, "ranks": P, "tokens_total": N, "tokens_local": n,
         "w_out_shard_rows": ve - vb, "ms_per_step_rank0": ms,
         "projected_job_tokens_per_s_if_comm_hidden": N / (ms / 1e3),
