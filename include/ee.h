@@ -364,6 +364,9 @@ ee_status ee_peer_barrier(const ee_peer_set* signals, uint32_t epoch, void* work
  * update complete); and before an arena is written again (2 arenas
  * alternating exits need no extra barrier).  Results are bitwise equal to
  * ee_tune_step + a rank-ordered fp32 all-reduce + ee_adam_update.
+ * Under a vocab shard (cfg->vocab_begin/end not [0, V): vocab-parallel), W_out
+ * has no arena block (it is never reduced and its row count differs between
+ * ranks); ee_adam_update_sharded then never updates W_out.
  * tensor_mask: bit k (ee_head_tensors order: g_a 0, w_gate 1, w_up 2,
  * w_down 3, g_f 4, w_out 5, g_att 6, w_q 7, w_k 8, w_v 9, w_o 10) selects the
  * tensors ee_adam_update_sharded updates; 0 = all.

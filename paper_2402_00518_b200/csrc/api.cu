@@ -139,10 +139,17 @@ long long shard_rows(long long R, int P, int q) {
 }
 bool tensor_needed(const ee_head_config* c, int k);
 // float offset of tensor k's slot block [P][rows_q x C] in rank q's arena; k = NTENS: total
+// Under a vocab shard (vocab-parallel) W_out is never reduced and its row count
+// differs between ranks, so it has no arena block: every rank must compute the
+// same offsets for every owner.
+static bool in_arena(const ee_head_config* c, int k) {
+  if (!tensor_needed(c, k)) return false;
+  return !(k == 5 && (c->vocab_begin != 0 || c->vocab_end != c->vocab));
+}
 long long arena_offset(const ee_head_config* c, int P, int q, int k) {
   long long off = 0;
   for (int j = 0; j < k; ++j) {
-    if (!tensor_needed(c, j)) continue;
+    if (!in_arena(c, j)) continue;
     long long R, C;
     tensor_rc(c, j, &R, &C);
     off += (long long)P * shard_rows(R, P, q) * C;
@@ -644,7 +651,7 @@ static GradScatter make_scatter(const ee_head_config* c, const ee_peer_set& aren
   memset(&g, 0, sizeof(g));
   const int P = arenas.world;
   for (int k = 0; k < NTENS; ++k) {
-    if (!tensor_needed(c, k)) continue;
+    if (!in_arena(c, k)) continue;
     long long R, C;
     tensor_rc(c, k, &R, &C);
     g.chunk[k] = (int)shard_chunk(R, P);
@@ -1833,7 +1840,7 @@ ee_status ee_adam_update_sharded(const ee_head_config* cfg, int32_t world, int32
     if (!grad_arenas[i] || !aligned16(grad_arenas[i]))
       return fail(EE_ERR_ALIGN, "grad_arenas[%d] NULL or misaligned", i);
     for (int k = 0; k < NTENS; ++k) {
-      if (!tensor_needed(cfg, k)) continue;
+      if (!in_arena(cfg, k)) continue;   // (a vocab shard's W_out has no arena block)
       if (tensor_mask && !(tensor_mask & (1u << k))) continue;
       long long R, C;
       tensor_rc(cfg, k, &R, &C);

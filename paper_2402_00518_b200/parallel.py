@@ -480,11 +480,6 @@ class ShardedVPHeads:
 
     def __init__(self, spec, n_all: int, rank: int, world: int, device="cuda", n_arenas: int = 2):
         import paper_2402_00518_b200 as ee
-        if spec.arch == "layer":
-            # the attention tensors of a Layer exit did not match the all-reduce
-            # path bit for bit under this schedule (MLP tensors do); until that
-            # is understood Layer exits keep the all-reduce body update
-            raise NotImplementedError("ShardedVPHeads: Layer exits use the all-reduce path")
         self.ee, self.spec, self.rank, self.world = ee, spec, rank, world
         vb, ve = vocab_shard(spec.vocab, world, rank)
         kw = spec.attn_kwargs()
@@ -502,7 +497,7 @@ class ShardedVPHeads:
         dev = torch.device(device)
         E = spec.num_exits
         self.layout = {k: ee.ee_dp_shard_layout(self.exit_cfg, world, rank, k) for k in self.names}
-        total = self.layout[self.names[0]][3]
+        total = self.layout[self.names[0]][3]    # (no W_out block under a vocab shard)
 
         def master_like(k):
             if k == "w_out":

@@ -347,7 +347,8 @@ def _run_vp_adam(ee, cfg, P, hidden, targets, params, sharded, steps=2):
     return out
 
 
-@pytest.mark.parametrize("arch,P", [("mlp", 2), ("mlp", 4), ("embedding", 2), ("norm", 4)])
+@pytest.mark.parametrize("arch,P", [("mlp", 2), ("mlp", 4), ("embedding", 2), ("norm", 4),
+                                    ("layer", 2)])
 def test_vp_sharded_body_update_bitwise(gpu_lib, arch, P):
     """VP with the exit body's gradient rows scattered to their owners and a
     sharded Adam (ZeRO-1 for the replicated body) equals, bit for bit, the
