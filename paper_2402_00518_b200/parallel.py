@@ -152,7 +152,7 @@ class ShardedDPHeads:
         self.m = [{k: shard(k) for k in self.names} for _ in range(E)]
         self.v = [{k: shard(k) for k in self.names} for _ in range(E)]
         self.n_arenas = max(1, min(int(n_arenas), E))
-        self.arenas = [torch.zeros(total, dtype=torch.float32, device=dev)
+        self.arenas = [torch.zeros(max(total, 4), dtype=torch.float32, device=dev)
                        for _ in range(self.n_arenas)]
         self.sig = torch.zeros(8, dtype=torch.int32, device=dev)
         self.epoch = 0
@@ -513,7 +513,7 @@ class ShardedVPHeads:
         self.v = [{k: master_like(k) for k in self.names} for _ in range(E)]
         self.grads = [{"w_out": torch.zeros(shapes["w_out"], device=dev)} for _ in range(E)]
         self.n_arenas = max(1, min(int(n_arenas), E))
-        self.arenas = [torch.zeros(total, dtype=torch.float32, device=dev)
+        self.arenas = [torch.zeros(max(total, 4), dtype=torch.float32, device=dev)
                        for _ in range(self.n_arenas)]
         self.workspace = torch.zeros(ee.ee_workspace_size(self.cfg, n_all), dtype=torch.uint8,
                                      device=dev)
