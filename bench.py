@@ -209,6 +209,11 @@ def vp_comm_desc(args, vp, world):
         return {}
     base = "gloo" if getattr(args, "shared_gpu", False) else "NCCL"
     if getattr(args, "vp_comm", "nccl") == "fused":
+        if getattr(args, "vp_zero", False):
+            return {"vp_comm": "z all-gather (a4) and dz reduce-scatter (a8) fused into the "
+                               "kernels, exit-body gradient rows scattered to their owners "
+                               "(a11/a12 epilogues) + sharded Adam storing the body operands "
+                               f"into every rank, over CUDA-IPC peer memory; CE stats: {base}"}
         return {"vp_comm": "z all-gather (a4) and dz reduce-scatter (a8) fused into the kernels "
                            f"over CUDA-IPC peer memory + peer barriers; CE stats, body grads: {base}"}
     return {"vp_comm": f"{base} all-gather / reduce-scatter"}
@@ -230,7 +235,9 @@ def workload_config(cfg, world, args):
             **vp_comm_desc(args, vp, world),
             "l2": "inputs larger than L2 (hidden states + exit weights per step >> 126 MB)",
             "optimizer": "Adam (P:374-375), included in the step",
-            "update_schedule": ("per exit, Adam fused into the weight-gradient epilogues "
+            "update_schedule": ("per exit: W_out shard Adam + sharded exit-body Adam (ZeRO-1; "
+                                "P:261)" if getattr(args, "vp_zero", False) else
+                                "per exit, Adam fused into the weight-gradient epilogues "
                                 "(P:261)" if getattr(args, "fused_adam", False) else
                                 "per exit, each exit's Adam on a side stream overlapping the "
                                 "next exit (P:261)" if getattr(args, "overlapped", False) else
@@ -317,6 +324,9 @@ def main():
                          "measured slower (profiles/r01f_fused_adam_ab.log), so opt-in")
     ap.add_argument("--force-dp-fused", action="store_true",
                     help="run the fused DP path at N=1 as well (A/B against the plain step)")
+    ap.add_argument("--vp-replicated-body", action="store_true",
+                    help="vp fused: all-reduce the exit body's gradients and update it on "
+                         "every rank instead of the sharded (ZeRO-1) body update")
     ap.add_argument("--vp-comm", default="fused", choices=["fused", "nccl"],
                     help="vp: fused = z all-gather / dz reduce-scatter inside the a4 / a8 "
                          "kernels over CUDA-IPC peer memory; nccl = NCCL collectives")
@@ -361,7 +371,7 @@ def main():
     n_all = cfg.tokens if vp else n
     E = cfg.exits
     from paper_2402_00518_b200.parallel import (GpuPhases, LocalComm, PeerBuffers,
-                                                ShardedDPHeads, TorchComm,
+                                                ShardedDPHeads, ShardedVPHeads, TorchComm,
                                                 data_parallel_step, vocab_parallel_step,
                                                 vocab_parallel_step_fused, vocab_shard)
     vb, ve = vocab_shard(cfg.vocab, world, rank) if vp else (0, cfg.vocab)
@@ -393,6 +403,17 @@ def main():
             heads, dp_fused = None, False
             torch.cuda.empty_cache()
     args.dp_fused = dp_fused
+    # VP with the fused collectives: the replicated exit body updated ZeRO-1 style
+    vp_zero = vp and args.vp_comm == "fused" and not args.vp_replicated_body
+    if vp_zero:
+        heads = ShardedVPHeads(ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch,
+                                           **attn_kw(cfg)), n_all, rank, world, device=dev)
+        torch.cuda.synchronize()
+        if world > 1:
+            heads.connect_ipc()
+        else:
+            heads.connect_local([heads])
+    args.vp_zero = vp_zero
     if heads is None:
         heads = ee.ExitHeads(ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch,
                                          vocab_begin=vb, vocab_end=ve, **attn_kw(cfg)), n_all,
@@ -402,7 +423,8 @@ def main():
     # one GPU: exit by exit with Adam overlapped on a side stream (any grad-buffer count)
     overlapped = not multi and not vp and not dp_fused and not fused_adam and args.overlap
     args.overlapped = overlapped
-    per_exit = (not dp_fused) and (not fused_adam) and (not overlapped) and heads.grad_buffers < E
+    per_exit = ((not dp_fused) and (not vp_zero) and (not fused_adam) and (not overlapped)
+                and heads.grad_buffers < E)
     args.per_exit = per_exit
     bb = S.backbone(cfg, device=dev)
     src = []
@@ -444,7 +466,7 @@ def main():
                          "dz_partial": torch.zeros(n_all, cfg.hidden, device=dev),
                          "dz_local": torch.zeros(n, cfg.hidden, device=dev)})
         comm = TorchComm() if world > 1 else LocalComm()
-        phases = GpuPhases(ee, heads.cfg, heads.workspace)
+        phases = GpuPhases(ee, heads.exit_cfg if vp_zero else heads.cfg, heads.workspace)
     else:
         hidden = S.hidden_states(cfg, n, seed=cfg.seed * 100 + rank, device=dev)
         targets = S.targets(cfg, n, seed=cfg.seed * 100 + rank, device=dev)
@@ -478,6 +500,12 @@ def main():
             return
         if vp:
             ee.ee_count_valid(tg, cfg.vocab, vc, heads.workspace)   # W over all tokens
+            if vp_zero:    # body gradients to their owners, sharded Adam per exit
+                heads.set_lr(lr)
+                vocab_parallel_step_fused(phases, comm, peer, cfg.arch, hid, tg, heads.operand,
+                                          heads.grads, heads.loss, [1.0] * E, vc, bufs,
+                                          body=heads)
+                return
             if peer is not None:
                 vocab_parallel_step_fused(phases, comm, peer, cfg.arch, hid, tg, heads.operand,
                                           heads.grads, heads.loss, [1.0] * E, vc, bufs)
