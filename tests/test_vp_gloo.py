@@ -300,3 +300,52 @@ def test_fused_vocab_parallel_gloo_matches_full_batch_oracle(arch, world):
         p.join(timeout=180)
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     assert q.get(timeout=5) is True
+
+
+def test_fused_orchestration_with_sharded_body_call_order():
+    """vocab_parallel_step_fused(..., body=...) (ShardedVPHeads): per exit the
+    body backward writes to the body's arenas (no local gradients, no body
+    all-reduce), then one more peer barrier, then body.update(i); the step
+    starts with one barrier.  Host logic only (recording stand-ins)."""
+    from paper_2402_00518_b200.parallel import vocab_parallel_step_fused
+
+    log = []
+
+    class Rec:
+        def __getattr__(self, name):
+            def f(*a, **k):
+                log.append((name, k.get("grad_arenas")))
+            return f
+
+        def barrier(self, peer):
+            log.append(("barrier", None))
+
+    class Comm:
+        rank, world = 0, 1
+
+        def all_reduce(self, t, op="sum", async_op=False):
+            log.append(("all_reduce_" + op, None))
+
+    class Body:
+        def arena_set(self, i):
+            return f"arena{i % 2}"
+
+        def update(self, i):
+            log.append(("update", i))
+
+    class Peer:
+        n_all, z_all = 8, None
+
+    E = 3
+    vocab_parallel_step_fused(Rec(), Comm(), Peer(), "mlp", [None] * E, None,
+                              [{}] * E, [{"g_a": object()}] * E, torch.zeros(E), [1.0] * E,
+                              None, {"key": None, "sums": None}, body=Body())
+    names = [n for n, _ in log]
+    assert names[0] == "barrier"
+    per_exit = ["exit_forward_ag", "barrier", "vocab_stats", "all_reduce_max", "rescale",
+                "all_reduce_sum", "vocab_backward_rs", "barrier", "exit_backward_slots",
+                "barrier", "update"]
+    assert names[1:] == per_exit * E, names
+    arenas = [a for n, a in log if n == "exit_backward_slots"]
+    assert arenas == ["arena0", "arena1", "arena0"]
+    assert [x for n, x in log if n == "update"] == [0, 1, 2]
