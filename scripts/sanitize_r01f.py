@@ -52,3 +52,18 @@ _, _, _, st = gpu_step(ee, cl, S.hidden_states(cl), S.targets(cl), S.head_params
 assert st == (0, -1), st
 torch.cuda.synchronize()
 print("sanitize run ok")
+# VP with the sharded exit body at world 1 (tensor mask, arenas without W_out)
+from paper_2402_00518_b200.parallel import ShardedVPHeads
+zs = ShardedVPHeads(ee.HeadSpec(192, 2056, 384, 2, "mlp"), 77, 0, 1)
+zs.connect_local([zs])
+zs.init("copy", copy_src=[{k: v.cuda().float().contiguous() for k, v in p.items()} for p in prm],
+        src_dtype=torch.float32)
+pb2 = PeerBuffers(0, 1, 77, 192)
+pb2.connect_local([pb2])
+zs.set_lr(1e-3)
+vocab_parallel_step_fused(GpuPhases(ee, zs.exit_cfg, zs.workspace), LocalComm(), pb2, "mlp",
+                          [x.cuda() for x in hid], tg.cuda(), zs.operand, zs.grads, zs.loss,
+                          [1.0, 0.5], W, {"key": torch.zeros(77, dtype=torch.int64, device="cuda"),
+                                          "sums": torch.zeros(77, 2, device="cuda")}, body=zs)
+torch.cuda.synchronize()
+print("sanitize run 2 ok")
