@@ -204,7 +204,9 @@ def vp_comm_desc(args, vp, world):
                            "sharded Adam storing the new operands into every rank (ZeRO-1), "
                            f"peer barriers; valid count and losses: {base}"}
     if not vp and world > 1:
-        return {"dp_comm": "NCCL all-reduce of fp32 gradients (async, overlapped) + Adam per rank"}
+        base = "gloo" if getattr(args, "shared_gpu", False) else "NCCL"
+        return {"dp_comm": f"{base} all-reduce of fp32 gradients (async, overlapped) + Adam "
+                           "per rank"}
     if not vp or world == 1:
         return {}
     base = "gloo" if getattr(args, "shared_gpu", False) else "NCCL"
