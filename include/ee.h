@@ -219,8 +219,10 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
 
 /* Data-parallel confidence weighting (EE_WEIGHT_CONFIDENCE_SUM): after the
  * caller has summed one exit's grads, its loss and weight_sum over the ranks,
- * divide the exit's fp32 gradients (grads: ONE exit) and *loss (device, may be
- * NULL) by *weight_sum (device scalar; <= 0 -> zeros).  P:326-336, A17. */
+ * divide the exit's fp32 gradients (grads: ONE exit, or NULL: the loss only --
+ * the sharded DP path divides inside ee_adam_update_sharded) and *loss
+ * (device, may be NULL) by *weight_sum (device scalar; <= 0 -> zeros).
+ * P:326-336, A17. */
 ee_status ee_normalize_exit(const ee_head_config* cfg, ee_head_tensors* grads, float* loss,
                             const float* weight_sum, void* stream);
 
@@ -367,6 +369,11 @@ ee_status ee_peer_barrier(const ee_peer_set* signals, uint32_t epoch, void* work
  * Under a vocab shard (cfg->vocab_begin/end not [0, V): vocab-parallel), W_out
  * has no arena block (it is never reduced and its row count differs between
  * ranks); ee_adam_update_sharded then never updates W_out.
+ * grad_divisor (device float [E] or NULL): exit i's summed gradient is
+ * multiplied by 1/grad_divisor[i] (0 if <= 0) before Adam -- dynamic token
+ * weights under DP: ee_tune_step_rs with EE_WEIGHT_CONFIDENCE_SUM, the
+ * weight sums all-reduced by the caller, the losses divided with
+ * ee_normalize_exit(cfg, NULL, loss, weight_sum) (grads may be NULL there).
  * tensor_mask: bit k (ee_head_tensors order: g_a 0, w_gate 1, w_up 2,
  * w_down 3, g_f 4, w_out 5, g_att 6, w_q 7, w_k 8, w_v 9, w_o 10) selects the
  * tensors ee_adam_update_sharded updates; 0 = all.
@@ -388,7 +395,7 @@ ee_status ee_adam_update_sharded(const ee_head_config* cfg, int32_t world, int32
                                  ee_head_tensors* m_shard, ee_head_tensors* v_shard,
                                  const ee_peer_set* operands, float lr, float beta1, float beta2,
                                  float eps, float weight_decay, int64_t step, float grad_scale,
-                                 uint32_t tensor_mask, void* stream);
+                                 uint32_t tensor_mask, const float* grad_divisor, void* stream);
 
 ee_status ee_ipc_get_handle(const void* dev_ptr, void* handle64, uint64_t* offset);
 ee_status ee_ipc_open(const void* handle64, uint64_t offset, void** dev_ptr);

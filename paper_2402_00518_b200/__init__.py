@@ -150,7 +150,7 @@ def load(path: str = LIB_PATH):
                                   P, SZ, P]),
         "ee_adam_update_sharded": (I32, [CFG, I32, I32, ctypes.POINTER(P), HT, HT, HT,
                                          ctypes.POINTER(ee_peer_set), F32, F32, F32, F32, F32,
-                                         I64, F32, ctypes.c_uint32, P]),
+                                         I64, F32, ctypes.c_uint32, P, P]),
         "ee_ipc_get_handle": (I32, [P, P, ctypes.POINTER(ctypes.c_uint64)]),
         "ee_ipc_open": (I32, [P, ctypes.c_uint64, ctypes.POINTER(P)]),
         "ee_ipc_close": (I32, [P, ctypes.c_uint64]),
@@ -352,8 +352,8 @@ def ee_normalize_exit(cfg, grads, loss, weight_sum, stream=None):
     """Divide one exit's gradients (dict) and loss (device [1] or None) by the
     device scalar weight_sum (data-parallel confidence weighting)."""
     load()
-    _check(_lib.ee_normalize_exit(ctypes.byref(cfg), heads([grads]), _ptr(loss), _ptr(weight_sum),
-                                  _stream(stream)))
+    _check(_lib.ee_normalize_exit(ctypes.byref(cfg), None if grads is None else heads([grads]),
+                                  _ptr(loss), _ptr(weight_sum), _stream(stream)))
 
 
 def _aux1(aux):
@@ -525,7 +525,8 @@ def ee_tune_step_rs(cfg, hidden, targets, exit_weights, params, arenas, loss_out
 
 def ee_adam_update_sharded(cfg, world, rank, arenas_local, master_shard, m_shard, v_shard,
                            operand_sets, lr, step, beta1=0.9, beta2=0.95, eps=1e-5,
-                           weight_decay=0.0, grad_scale=1.0, tensors=None, stream=None):
+                           weight_decay=0.0, grad_scale=1.0, tensors=None, grad_divisor=None,
+                           stream=None):
     """Sharded Adam + operand all-gather; operand_sets: per exit a dict
     {name: ee_peer_set of every rank's operand tensor}."""
     load()
@@ -541,7 +542,7 @@ def ee_adam_update_sharded(cfg, world, rank, arenas_local, master_shard, m_shard
                                        ctypes.c_uint32(0 if tensors is None else
                                                        sum(1 << TENSOR_NAMES.index(k)
                                                            for k in tensors)),
-                                       _stream(stream)))
+                                       _ptr(grad_divisor), _stream(stream)))
 
 
 def ee_ipc_get_handle(t: torch.Tensor) -> tuple[bytes, int]:

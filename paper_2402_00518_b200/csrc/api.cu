@@ -1122,8 +1122,9 @@ ee_status ee_tune_step_rs(const ee_head_config* cfg, const void* const* hidden, 
                           float* loss_out, const ee_step_aux* aux, const int64_t* valid_count,
                           void* workspace, size_t ws_bytes, void* stream) {
   if (!grad_arenas) return fail(EE_ERR_ARG, "grad_arenas required");
-  if (cfg && cfg->token_weighting != EE_WEIGHT_UNIFORM)
-    return fail(EE_ERR_UNSUPPORTED, "ee_tune_step_rs: uniform token weights only");
+  if (cfg && cfg->token_weighting == EE_WEIGHT_CONFIDENCE)
+    return fail(EE_ERR_UNSUPPORTED, "ee_tune_step_rs: the confidence normaliser spans the ranks; "
+                                    "use EE_WEIGHT_CONFIDENCE_SUM + grad_divisor");
   return tune_step_impl(cfg, hidden, n_tokens, targets, exit_weights, params, nullptr,
                         grad_arenas, 0, loss_out, aux, valid_count, workspace, ws_bytes, stream);
 }
@@ -1719,11 +1720,11 @@ ee_status ee_normalize_exit(const ee_head_config* cfg, ee_head_tensors* grads, f
                             const float* weight_sum, void* stream) {
   ee_status s = check_cfg(cfg);
   if (s != EE_OK) return s;
-  if (!grads || !weight_sum) return fail(EE_ERR_ARG, "grads/weight_sum NULL");
-  if ((s = check_arch_tensors(cfg, *grads, "grads", 0)) != EE_OK) return s;
+  if ((!grads && !loss) || !weight_sum) return fail(EE_ERR_ARG, "grads+loss/weight_sum NULL");
+  if (grads && (s = check_arch_tensors(cfg, *grads, "grads", 0)) != EE_OK) return s;
   if ((s = check_device()) != EE_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
-  for (int k = 0; k < NTENS; ++k) {
+  for (int k = 0; k < NTENS && grads; ++k) {
     float* g = (float*)(grads->*(kTens[k].f));
     if (!g) continue;
     Prof p_("normalize_exit", st, 0, 0, 8.0 * tensor_numel(cfg, k));
@@ -1825,7 +1826,8 @@ ee_status ee_adam_update_sharded(const ee_head_config* cfg, int32_t world, int32
                                 ee_head_tensors* m_shard, ee_head_tensors* v_shard,
                                 const ee_peer_set* operands, float lr, float beta1, float beta2,
                                 float eps, float wd, int64_t step, float grad_scale,
-                                uint32_t tensor_mask, void* stream) {
+                                uint32_t tensor_mask, const float* grad_divisor,
+                                void* stream) {
   ee_status s = check_cfg(cfg);
   if (s != EE_OK) return s;
   if (world < 1 || world > EE_MAX_PEERS || rank < 0 || rank >= world || !grad_arenas ||
@@ -1868,7 +1870,8 @@ ee_status ee_adam_update_sharded(const ee_head_config* cfg, int32_t world, int32
       Prof p_("a15_adam_sharded", st, 0, 0, (4.0 * world + 24.0 + 2.0 * world) * nel);
       EE_CUDA(launch_adam_sharded(th, slots, world, mm, vv, nel, pp,
                                   (long long)rank * shard_chunk(R, world) * C, lr, beta1, beta2,
-                                  eps, wd, bc1, bc2, grad_scale, st));
+                                  eps, wd, bc1, bc2, grad_scale, st,
+                                  grad_divisor ? grad_divisor + i : nullptr));
     }
   }
   return EE_OK;

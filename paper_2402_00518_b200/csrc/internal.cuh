@@ -171,7 +171,7 @@ struct OpPeers {  // every rank's operand tensor of one parameter (bf16, or fp32
 cudaError_t launch_adam_sharded(float* theta, const float* slots, int P, float* m, float* v,
                                 long long n, const OpPeers& op, long long off, float lr, float b1,
                                 float b2, float eps, float wd, float bc1, float bc2, float gs,
-                                cudaStream_t s);
+                                cudaStream_t s, const float* div = nullptr);
 cudaError_t launch_adam(float* theta, __nv_bfloat16* op_bf16, float* op_f32, const float* grad,
                         float* m, float* v, long long n, float lr, float b1, float b2, float eps,
                         float wd, float bc1, float bc2, float gscale, cudaStream_t s);

@@ -842,7 +842,14 @@ __global__ void adam_sharded_kernel(float* __restrict__ th, const float* __restr
                                     int P, float* __restrict__ m, float* __restrict__ v,
                                     long long n4, OpPeers op, long long off4, float lr, float b1,
                                     float b2, float eps, float wd, float bc1, float bc2,
-                                    float gs) {
+                                    float gs, const float* __restrict__ div) {
+  // dynamic token weights under DP: divide by the global sum of weights
+  // (ee_normalize_exit's arithmetic: x *= 1/d, 0 if d <= 0)
+  float fdiv = 1.f;
+  if (div) {
+    const float d = *div;
+    fdiv = d > 0.f ? 1.0f / d : 0.f;
+  }
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
        i += (long long)gridDim.x * blockDim.x) {
     float4 t = reinterpret_cast<float4*>(th)[i];
@@ -850,6 +857,9 @@ __global__ void adam_sharded_kernel(float* __restrict__ th, const float* __restr
     for (int r = 1; r < P; ++r) {
       const float4 e = reinterpret_cast<const float4*>(slots)[(long long)r * n4 + i];
       g4.x += e.x; g4.y += e.y; g4.z += e.z; g4.w += e.w;
+    }
+    if (div) {
+      g4.x *= fdiv; g4.y *= fdiv; g4.z *= fdiv; g4.w *= fdiv;
     }
     float4 m4 = reinterpret_cast<float4*>(m)[i];
     float4 v4 = reinterpret_cast<float4*>(v)[i];
@@ -881,11 +891,11 @@ __global__ void adam_sharded_kernel(float* __restrict__ th, const float* __restr
 cudaError_t launch_adam_sharded(float* theta, const float* slots, int P, float* m, float* v,
                                 long long n, const OpPeers& op, long long off, float lr, float b1,
                                 float b2, float eps, float wd, float bc1, float bc2, float gs,
-                                cudaStream_t s) {
+                                cudaStream_t s, const float* div) {
   if (n == 0) return cudaSuccess;
   const long long n4 = n / 4;
   adam_sharded_kernel<<<ew_blocks(n4), 256, 0, s>>>(theta, slots, P, m, v, n4, op, off / 4, lr,
-                                                    b1, b2, eps, wd, bc1, bc2, gs);
+                                                    b1, b2, eps, wd, bc1, bc2, gs, div);
   return cudaGetLastError();
 }
 

@@ -125,10 +125,12 @@ class ShardedDPHeads:
                  n_arenas: int = 2):
         import paper_2402_00518_b200 as ee
         self.ee, self.spec, self.rank, self.world = ee, spec, rank, world
+        self.conf = spec.token_weighting == "confidence"   # dynamic weights
+        wt = "confidence_sum" if self.conf else "uniform"
         self.cfg = ee.make_config(spec.hidden, spec.vocab, spec.ffn, spec.num_exits, spec.arch,
-                                  spec.norm_eps, **spec.attn_kwargs())
+                                  spec.norm_eps, token_weighting=wt, **spec.attn_kwargs())
         self.exit_cfg = ee.make_config(spec.hidden, spec.vocab, spec.ffn, 1, spec.arch,
-                                       spec.norm_eps, **spec.attn_kwargs())
+                                       spec.norm_eps, token_weighting=wt, **spec.attn_kwargs())
         shapes = ee.tensor_shapes(spec.hidden, spec.vocab, spec.ffn, spec.arch,
                                   self.cfg.n_kv_heads)
         self.names = [k for k in ee.TENSOR_NAMES if k in shapes]
@@ -159,6 +161,7 @@ class ShardedDPHeads:
         self.workspace = torch.zeros(ee.ee_workspace_size(self.cfg, max_tokens),
                                      dtype=torch.uint8, device=dev)
         self.loss = torch.zeros(E, dtype=torch.float32, device=dev)
+        self.wsum = torch.zeros(E, dtype=torch.float32, device=dev)   # sum_t c_t per exit
         self.step_count = 0
         self._opened = []
 
@@ -240,26 +243,36 @@ class ShardedDPHeads:
         ee = self.ee
         E = self.spec.num_exits
         w = exit_weights if exit_weights is not None else [1.0] * E
-        W = torch.zeros(1, dtype=torch.int64, device=self.loss.device)
-        ee.ee_count_valid(targets, self.spec.vocab, W, self.workspace)
-        if all_reduce is not None:
-            all_reduce(W)
+        W = None
+        if not self.conf:
+            W = torch.zeros(1, dtype=torch.int64, device=self.loss.device)
+            ee.ee_count_valid(targets, self.spec.vocab, W, self.workspace)
+            if all_reduce is not None:
+                all_reduce(W)
         self.step_count += 1
         self.barrier()                       # previous update's operand stores are complete
         for i in range(E):
             j = i % self.n_arenas
+            aux = [{"weight_sum": self.wsum[i:i + 1]}] if self.conf else None
             ee.ee_tune_step_rs(self.exit_cfg, hidden[i:i + 1], targets, w[i:i + 1],
                                self.operand[i:i + 1], [self.arena_sets[j]],
-                               self.loss[i:i + 1], self.workspace, valid_count=W)
+                               self.loss[i:i + 1], self.workspace, aux=aux, valid_count=W)
+            if self.conf and all_reduce is not None:
+                all_reduce(self.wsum[i:i + 1])   # global sum_t c_t: the gradient divisor
             self.barrier()                   # every rank's partials of exit i have landed
             ee.ee_adam_update_sharded(self.exit_cfg, self.world, self.rank, [self.arenas[j]],
                                       self.master[i:i + 1], self.m[i:i + 1], self.v[i:i + 1],
                                       self.operand_sets[i:i + 1], lr, self.step_count, beta1,
-                                      beta2, eps, weight_decay)
+                                      beta2, eps, weight_decay,
+                                      grad_divisor=self.wsum[i:i + 1] if self.conf else None)
             if self.n_arenas == 1 and i + 1 < E:
                 self.barrier()               # arena read by every owner before it is rewritten
         if all_reduce is not None:
             all_reduce(self.loss)
+        if self.conf:                        # L_i = sum c_t loss_t / sum c_t over all ranks
+            for i in range(E):
+                ee.ee_normalize_exit(self.exit_cfg, None, self.loss[i:i + 1],
+                                     self.wsum[i:i + 1])
         return self.loss
 
 

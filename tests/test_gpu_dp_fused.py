@@ -236,3 +236,81 @@ def test_fused_dp_two_processes_cuda_ipc(gpu_lib, tmp_path):
     for i in range(cfg.exits):
         res = oracle_exit("mlp", params[i], hidden[i], targets, 1.0)
         assert abs(outs[0]["loss"][0][i].item() - res.loss) / res.loss <= LOSS_RTOL
+
+
+def test_fused_dp_confidence_weighting_bitwise(gpu_lib):
+    """Dynamic token weights under the fused DP path: ranks run
+    EE_WEIGHT_CONFIDENCE_SUM into the arenas, the weight sums are all-reduced,
+    the sharded Adam divides by them (grad_divisor) and the losses are divided
+    with ee_normalize_exit(grads=NULL) -- bitwise the all-reduce path
+    (rank-ordered sums, ee_normalize_exit on full gradients, Adam)."""
+    ee = gpu_lib
+    from paper_2402_00518_b200.parallel import ShardedDPHeads
+    cfg = _cfg("mlp", 53)
+    P, N, E = 2, 256, cfg.exits
+    nl = N // P
+    hidden = S.hidden_states(cfg, N)
+    targets = S.targets(cfg, N)
+    params = S.head_params(cfg)
+    shared = {"P": P, "barrier": threading.Barrier(P), "slots": [None] * P}
+    heads = [ShardedDPHeads(ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch,
+                                        token_weighting="confidence"), nl, r, P)
+             for r in range(P)]
+    for h in heads:
+        h.connect_local(heads)
+    _warm(ee, cfg, hidden, targets, params)
+    torch.cuda.synchronize()
+    out, errors = [[None, None] for _ in range(P)], []
+
+    def rank_fn(r):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                comm = StreamThreadComm(shared, r, st)
+                hid = [x[r * nl:(r + 1) * nl].cuda().contiguous() for x in hidden]
+                tg = targets[r * nl:(r + 1) * nl].cuda().contiguous()
+                # fused
+                hd = heads[r]
+                hd.init("copy", copy_src=_copy_src(params), src_dtype=torch.float32)
+                for it in range(2):
+                    hd.step(hid, tg, 1e-3 * (it + 1), all_reduce=lambda t: comm.all_reduce(t))
+                out[r][0] = ([{k: v.cpu() for k, v in d.items()} for d in hd.operand],
+                             hd.loss.cpu(), ee.ee_get_status(hd.workspace, stream=st))
+                # all-reduce reference
+                rf = ee.ExitHeads(ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch,
+                                              token_weighting="confidence_sum"), nl)
+                rf.init("copy", copy_src=_copy_src(params), src_dtype=torch.float32)
+                ecfg = ee.make_config(cfg.hidden, cfg.vocab, cfg.ffn, 1, cfg.arch,
+                                      token_weighting="confidence_sum")
+                ws = [torch.zeros(1, device="cuda") for _ in range(E)]
+                for it in range(2):
+                    rf.step(hid, tg, aux=[{"weight_sum": w} for w in ws])
+                    for g in rf.grads:
+                        for t in g.values():
+                            comm.all_reduce(t)
+                    comm.all_reduce(rf.loss)
+                    for i in range(E):
+                        comm.all_reduce(ws[i])
+                        ee.ee_normalize_exit(ecfg, rf.grads[i], rf.loss[i:i + 1], ws[i])
+                    rf.adam(1e-3 * (it + 1))
+                out[r][1] = ([{k: v.cpu() for k, v in d.items()} for d in rf.operand],
+                             rf.loss.cpu(), None)
+                st.synchronize()
+        except Exception as e:  # surface thread failures
+            errors.append(e)
+            shared["barrier"].abort()
+
+    th = [threading.Thread(target=rank_fn, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    if errors:
+        raise errors[0]
+    for r in range(P):
+        got, ref = out[r]
+        assert got[2] == (0, -1)
+        assert torch.equal(got[1], ref[1]), (got[1], ref[1])
+        for i in range(E):
+            for k, t in ref[0][i].items():
+                assert torch.equal(got[0][i][k], t), (r, i, k)
