@@ -258,7 +258,12 @@ def test_fused_dp_confidence_weighting_bitwise(gpu_lib):
              for r in range(P)]
     for h in heads:
         h.connect_local(heads)
-    _warm(ee, cfg, hidden, targets, params)
+    # world-1 confidence step first: loads the kernels this path adds (see _warm)
+    w1 = ShardedDPHeads(ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch,
+                                    token_weighting="confidence"), N, 0, 1)
+    w1.connect_local([w1])
+    w1.init("copy", copy_src=_copy_src(params), src_dtype=torch.float32)
+    w1.step([x.cuda() for x in hidden], targets.cuda(), 1e-3, all_reduce=lambda t: None)
     torch.cuda.synchronize()
     out, errors = [[None, None] for _ in range(P)], []
 
