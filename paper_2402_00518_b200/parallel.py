@@ -1,8 +1,15 @@
-"""Data parallelism over tokens for the exit-head step (host orchestration).
+"""Multi-GPU host orchestration of the exit-head step: data
+parallelism over tokens (`data_parallel_step` over NCCL; `ShardedDPHeads`, the
+fused ZeRO-1 path over peer memory), vocab-parallel W_out
+(`vocab_parallel_step`; `vocab_parallel_step_fused` with `PeerBuffers` and
+`ShardedVPHeads`) and the forward-communication-only pipeline
+(`pipeline_forward_only_step`).  All compute runs in the CUDA library; these
+functions only order its calls and the collectives between them.
 
-EE-Tuning's exits are independent and every token contributes independently to
-an exit's loss, so the step shards along the flat token axis:
-rank r owns tokens [r*N/P, (r+1)*N/P).  The only exchanges are
+Data parallelism: EE-Tuning's exits are independent and every token
+contributes independently to an exit's loss, so the step shards
+along the flat token axis: rank r owns tokens [r*N/P, (r+1)*N/P).  The only
+exchanges of the NCCL path are
 
   1. the global number of valid tokens W (one int64 all-reduce), so every
      rank normalises its loss and gradients by the *global* W (A16);
@@ -459,19 +466,8 @@ class PeerBuffers:
         self._tables([b.z_all for b in ranks], [b.slots for b in ranks], [b.sig for b in ranks])
 
     def connect_ipc(self, group=None):
-        import paper_2402_00518_b200 as ee
-        mine = [ee.ee_ipc_get_handle(t) for t in (self.z_all, self.slots, self.sig)]
-        allh = [None] * self.world
-        dist.all_gather_object(allh, mine, group=group)
-        tabs = [[], [], []]
-        for q in range(self.world):
-            for j, t in enumerate((self.z_all, self.slots, self.sig)):
-                if q == self.rank:
-                    tabs[j].append(t.data_ptr())
-                else:
-                    p = ee.ee_ipc_open(*allh[q][j])
-                    self._opened.append((p, allh[q][j][1]))
-                    tabs[j].append(p)
+        tabs, self._opened = _peer_tables(self.rank, [self.z_all, self.slots, self.sig],
+                                          group=group)
         self._tables(*tabs)
 
     def close(self):
