@@ -377,8 +377,31 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
             }
         }
       } else if (row_ok && gn0 < args.N) {
+        bool done = false;
+        if (args.scat_rows > 0) {
+          // the usual case: the 32 stored rows of this chunk lie in one owner's
+          // block on one side of n_split -> one base pointer, no per-element division
+          const int last = min(gn0 + 31, args.N - 1);
+          const bool hi0 = gn0 >= args.n_split, hi1 = last >= args.n_split;
+          const int r0 = hi0 ? gn0 - args.n_split : gn0;
+          const int r1 = hi1 ? last - args.n_split : last;
+          const int q0 = r0 / args.scat_rows;
+          if (hi0 == hi1 && q0 == r1 / args.scat_rows) {
+            float* base = (hi0 ? args.scat1[q0] : args.scat[q0]) +
+                          (long long)(r0 - q0 * args.scat_rows) * args.ldo + gm;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
+            for (int j = 0; j < 32; ++j) {
+              if (gn0 + j < args.N) {
+                float* o = base + (long long)j * args.ldo;
+                const float val = u2f(v[j]);
+                *o = args.accumulate ? *o + val : val;
+              }
+            }
+            done = true;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 32 && !done; ++j) {
           const int gn = gn0 + j;
           if (gn < args.N) {
             float* o;
