@@ -94,6 +94,15 @@ typedef enum { EE_INIT_COPY = 0, EE_INIT_RANDOM = 1 } ee_init;
  *             sum_t c_t loss_t, grads = gradient of alpha sum_t c_t loss_t,
  *             ee_step_aux.weight_sum = sum_t c_t of this call.  The caller sums
  *             the three over ranks and calls ee_normalize_exit. */
+/* How the backward obtains dS = dL/dS (a7; A24).
+ * RECOMPUTE (default, north_star): a second GEMM recomputes each S tile from
+ *   z and W_out and turns it into dS in the epilogue; the logits never reach
+ *   HBM in any encoding (SURVEY §7 hard part 3: +2hV FLOPs per token).
+ * STORED_P (ablation): the a5 epilogue also stores P~ = exp(S - tile max) as
+ *   fp16 [n x V] and a7 is an elementwise pass over it; fewer FLOPs but the
+ *   [tokens x vocab] probability matrix is written to HBM. */
+typedef enum { EE_DS_RECOMPUTE = 0, EE_DS_STORED_P = 1 } ee_ds_mode;
+
 typedef enum {
   EE_WEIGHT_UNIFORM = 0,
   EE_WEIGHT_CONFIDENCE = 1,
@@ -120,7 +129,8 @@ typedef enum { EE_DTYPE_BF16 = 0, EE_DTYPE_F32 = 1 } ee_dtype;
  *               LAYER only (ignored otherwise): query heads (hidden =
  *               n_heads * 128), key/value heads (divides n_heads; GQA),
  *               sequence length T (multiple of 64; token t of row r sits at
- *               position r % T), RoPE base (Llama-2: 10000). */
+ *               position r % T), RoPE base (Llama-2: 10000).
+ *  ds_mode      ee_ds_mode (0 = EE_DS_RECOMPUTE). */
 typedef struct {
   int32_t hidden, vocab, ffn, num_exits;
   int32_t arch;
@@ -129,6 +139,7 @@ typedef struct {
   int32_t token_weighting;
   int32_t n_heads, n_kv_heads, seq_len;
   float rope_theta;
+  int32_t ds_mode;
 } ee_head_config;
 
 /* Parameters (or gradients, or optimizer moments) of ONE exit.  Device

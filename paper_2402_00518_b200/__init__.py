@@ -53,7 +53,8 @@ class ee_head_config(ctypes.Structure):
                 ("norm_eps", ctypes.c_float), ("vocab_begin", ctypes.c_int32),
                 ("vocab_end", ctypes.c_int32), ("token_weighting", ctypes.c_int32),
                 ("n_heads", ctypes.c_int32), ("n_kv_heads", ctypes.c_int32),
-                ("seq_len", ctypes.c_int32), ("rope_theta", ctypes.c_float)]
+                ("seq_len", ctypes.c_int32), ("rope_theta", ctypes.c_float),
+                ("ds_mode", ctypes.c_int32)]
 
 
 class ee_head_tensors(ctypes.Structure):
@@ -185,12 +186,16 @@ def _stream(stream=None):
 
 
 WEIGHTING = {"uniform": 0, "confidence": 1, "confidence_sum": 2}
+DS_MODE = {"recompute": 0, "stored_p": 1}
 
 
 def make_config(hidden, vocab, ffn, num_exits, arch, norm_eps=1e-5, vocab_begin=0, vocab_end=None,
-                token_weighting="uniform", n_heads=0, n_kv_heads=0, seq_len=0, rope_theta=10000.0):
+                token_weighting="uniform", n_heads=0, n_kv_heads=0, seq_len=0, rope_theta=10000.0,
+                ds_mode="recompute"):
     """ee_head_config; n_heads / n_kv_heads / seq_len / rope_theta are the Layer
-    exit's attention geometry (n_heads defaults to hidden / 128)."""
+    exit's attention geometry (n_heads defaults to hidden / 128); ds_mode is
+    "recompute" (default: S recomputed for dS, logits never in HBM) or
+    "stored_p" (the A24 ablation, include/ee.h ee_ds_mode)."""
     a = ARCH[arch] if isinstance(arch, str) else arch
     if a == ARCH["layer"] and not n_heads:
         n_heads = hidden // 128
@@ -199,7 +204,8 @@ def make_config(hidden, vocab, ffn, num_exits, arch, norm_eps=1e-5, vocab_begin=
     return ee_head_config(hidden, vocab, ffn, num_exits, a, norm_eps, vocab_begin,
                           vocab if vocab_end is None else vocab_end,
                           WEIGHTING[token_weighting] if isinstance(token_weighting, str)
-                          else token_weighting, n_heads, n_kv_heads, seq_len, rope_theta)
+                          else token_weighting, n_heads, n_kv_heads, seq_len, rope_theta,
+                          DS_MODE[ds_mode] if isinstance(ds_mode, str) else ds_mode)
 
 
 def heads(list_of_dicts):
@@ -626,10 +632,12 @@ class HeadSpec:
     n_kv_heads: int = 0           # (default n_heads: no GQA)
     seq_len: int = 0
     rope_theta: float = 10000.0
+    ds_mode: str = "recompute"    # or "stored_p" (A24 ablation)
 
     def attn_kwargs(self):
+        """make_config keywords beyond the shapes: attention geometry and ds_mode."""
         return dict(n_heads=self.n_heads, n_kv_heads=self.n_kv_heads, seq_len=self.seq_len,
-                    rope_theta=self.rope_theta)
+                    rope_theta=self.rope_theta, ds_mode=self.ds_mode)
 
 
 class ExitHeads:
@@ -812,10 +820,17 @@ class ExitHeads:
             raise ValueError("more tokens than the workspace was sized for")
         dev = self.loss.device
         st = torch.cuda.current_stream(dev)
-        if getattr(self, "_stage", None) is None or self._stage[0].shape[0] < n:
-            self._stage = [torch.empty(n, h, dtype=torch.bfloat16, device=dev) for _ in range(2)]
-            self._stage_tg = torch.empty(n, dtype=torch.int32, device=dev)
+        if getattr(self, "_stage", None) is None:
+            # Sized once for max_tokens and never reallocated.  The blocks come
+            # from the caching allocator on `st`, which may hand back memory
+            # that kernels still queued on `st` read (e.g. the inputs of a
+            # preceding async step()); the copy stream's first write must
+            # therefore wait for everything queued on `st` so far.
+            self._stage = [torch.empty(self.max_tokens, h, dtype=torch.bfloat16, device=dev)
+                           for _ in range(2)]
+            self._stage_tg = torch.empty(self.max_tokens, dtype=torch.int32, device=dev)
             self._copy_stream = torch.cuda.Stream(dev)
+            self._copy_stream.wait_stream(st)
             self._ev = [[torch.cuda.Event(), torch.cuda.Event()] for _ in range(2)]
             self._stage_used = [False, False]
         bufs = [b[:n] for b in self._stage]

@@ -88,6 +88,8 @@ ee_status check_cfg(const ee_head_config* c) {
   if (c->token_weighting != EE_WEIGHT_UNIFORM && c->token_weighting != EE_WEIGHT_CONFIDENCE &&
       c->token_weighting != EE_WEIGHT_CONFIDENCE_SUM)
     return fail(EE_ERR_ARG, "unknown token_weighting %d", c->token_weighting);
+  if (c->ds_mode != EE_DS_RECOMPUTE && c->ds_mode != EE_DS_STORED_P)
+    return fail(EE_ERR_ARG, "unknown ds_mode %d", c->ds_mode);
   return EE_OK;
 }
 
@@ -749,13 +751,11 @@ ee_status phase_exit_forward(const ee_head_config* cfg, const Bufs& B, const ee_
 }
 
 // a5: per-V-tile online-softmax partials of S = z W_out^T (logits never stored).
-// a7 strategy: the a5 epilogue stores P~ = exp(S - tile max) (fp16) into the dS
-// buffer and a7 is an elementwise pass (default), or (EE_DS_RECOMPUTE=1) a7
-// recomputes S with a second GEMM (the FlashAttention-style recompute).
-static bool ds_recompute() {  // read per call (host side, once per exit): tests toggle it
-  const char* e = getenv("EE_DS_RECOMPUTE");
-  return e && atoi(e) != 0;
-}
+// a7 strategy (cfg->ds_mode, include/ee.h): EE_DS_RECOMPUTE (default) recomputes
+// S with a second GEMM whose epilogue forms dS (the FlashAttention-style
+// recompute; logits never in HBM); EE_DS_STORED_P has the a5 epilogue store
+// P~ = exp(S - tile max) (fp16) into the dS buffer and a7 is an elementwise pass.
+static bool ds_recompute(const ee_head_config* cfg) { return cfg->ds_mode != EE_DS_STORED_P; }
 
 ee_status phase_vocab_stats(const ee_head_config* cfg, const Bufs& B, const ee_head_tensors& P,
                             const __nv_bfloat16* z, long long n, const int32_t* targets,
@@ -768,7 +768,7 @@ ee_status phase_vocab_stats(const ee_head_config* cfg, const Bufs& B, const ee_h
   a.part_s = B.ps;
   a.part_i = B.pi;
   a.tgt_logit = B.tgt;
-  if (store_p && !ds_recompute()) {
+  if (store_p && !ds_recompute(cfg)) {
     a.ds = B.ds;
     a.ld_ds = Vl;
   }
@@ -786,7 +786,7 @@ ee_status phase_vocab_backward(const ee_head_config* cfg, const Bufs& B, const e
                                cudaStream_t st, const ee_peer_set* rs = nullptr,
                                const GradScatter* gs = nullptr, const AdamFuse* af = nullptr) {
   const int h = cfg->hidden, Vl = cfg->vocab_end - cfg->vocab_begin;
-  if (!ds_recompute()) {  // a7: dS from the stored P~ (elementwise, in place)
+  if (!ds_recompute(cfg)) {  // a7: dS from the stored P~ (elementwise, in place)
     Prof p_("a7_ds_from_p", st, 0, 0, 4.0 * n * Vl);
     EE_CUDA(launch_ce_ds_from_p(B.ds, Vl, n, B.pm, B.lse, B.coef, targets, cfg->vocab_begin,
                                 B.tgt, st));

@@ -497,7 +497,7 @@ class ShardedVPHeads:
         self.exit_cfg = ee.make_config(spec.hidden, spec.vocab, spec.ffn, 1, spec.arch,
                                        spec.norm_eps, vb, ve, **kw)
         self.wcfg = ee.make_config(spec.hidden, spec.vocab, 0, 1, "embedding", spec.norm_eps,
-                                   vb, ve)                     # the W_out shard alone
+                                   vb, ve, ds_mode=spec.ds_mode)                     # the W_out shard alone
         shapes = ee.tensor_shapes(spec.hidden, ve - vb, spec.ffn, spec.arch,
                                   self.cfg.n_kv_heads)
         self.shapes = shapes

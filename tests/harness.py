@@ -32,14 +32,14 @@ def attn_kwargs(cfg):
 
 
 def gpu_step(ee, cfg, hidden, targets, params, exit_weights, accumulate=False, grads=None,
-             eps=1e-5, weighting="uniform"):
+             eps=1e-5, weighting="uniform", ds_mode="recompute"):
     """Run ee_tune_step on the GPU.  hidden: list of bf16 tensors (any device);
     params: list of dicts of fp32 tensors (matrices are cast to bf16 operands).
     Returns (loss[E] tensor, grads list of dicts (device fp32), aux list)."""
     E = len(hidden)
     n = targets.numel()
     c = ee.make_config(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch, eps,
-                       token_weighting=weighting, **attn_kwargs(cfg))
+                       token_weighting=weighting, ds_mode=ds_mode, **attn_kwargs(cfg))
     hid = [h.cuda().contiguous() for h in hidden]
     tg = targets.cuda().to(torch.int32).contiguous()
     ops = [{k: (v.cuda().float().contiguous() if k.startswith("g_") else

@@ -230,9 +230,34 @@ def test_step_host_back_to_back_calls(gpu_lib, exits):
     want = [a.step([h.cuda() for h in hs], t.cuda()).clone() for hs, t in sets]
     host = [([h.pin_memory() for h in hs], t.pin_memory()) for hs, t in sets]
     got = []
-    for r in range(4):
+    for r in range(24):
         hs, t = host[r % 2]
         got.append(a.step_host(hs, t).clone())
     torch.cuda.synchronize()
-    for r in range(4):
+    for r in range(24):
         assert torch.equal(got[r], want[r % 2]), r
+
+
+def test_step_host_after_async_device_step(gpu_lib):
+    """The first step_host call allocates its staging buffers while a device
+    step() whose input tensors were already freed is still queued: the caching
+    allocator may hand those blocks to the staging buffers, so the copy stream
+    must not write them before the queued step has read them (the round-1
+    driver failure).  Fresh objects each round so the first-call path repeats."""
+    cfg = S.Cfg(name="small", hidden=128, vocab=1000, ffn=256, arch="mlp", tokens=300,
+                layers=2, after=[1, 2], init="random", seed=44)
+    spec = gpu_lib.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, 2, cfg.arch)
+    sets = [(S.hidden_states(cfg, 300, seed=s), S.targets(cfg, 300, seed=s)) for s in (1, 2)]
+    host = [([h.pin_memory() for h in hs], t.pin_memory()) for hs, t in sets]
+    ref = None
+    for r in range(6):
+        a = gpu_lib.ExitHeads(spec, 300)
+        a.init("random", seed=10)
+        if ref is None:
+            ref = [a.step([h.cuda() for h in hs], t.cuda()).clone() for hs, t in sets]
+            torch.cuda.synchronize()
+        la = a.step([h.cuda() for h in sets[0][0]], sets[0][1].cuda()).clone()  # inputs freed
+        lb = a.step_host(*host[1]).clone()
+        torch.cuda.synchronize()
+        assert torch.equal(la, ref[0]), r
+        assert torch.equal(lb, ref[1]), r

@@ -17,12 +17,14 @@ from oracle import ee_oracle as O
 pytestmark = pytest.mark.gpu
 
 
-def _run_and_compare(ee, cfg, n, weights, seed=0, params=None, ignore_frac=1 / 64):
+def _run_and_compare(ee, cfg, n, weights, seed=0, params=None, ignore_frac=1 / 64,
+                     ds_mode="recompute"):
     hidden = S.hidden_states(cfg, n, seed=seed)
     targets = S.targets(cfg, n, seed=seed, ignore_frac=ignore_frac)
     if params is None:
         params = S.head_params(cfg, seed=seed)
-    loss, grads, aux, status = gpu_step(ee, cfg, hidden, targets, params, weights)
+    loss, grads, aux, status = gpu_step(ee, cfg, hidden, targets, params, weights,
+                                        ds_mode=ds_mode)
     assert status == (0, -1), status
     errs = []
     for i in range(cfg.exits):
@@ -44,10 +46,11 @@ def test_tiny_config_full(gpu_lib):
     ("mlp", 128, 1000, 384, 300),
     ("mlp", 256, 4104, 512, 1000),
 ])
-def test_small_ragged(gpu_lib, arch, h, V, F, n):
+@pytest.mark.parametrize("ds_mode", ["recompute", "stored_p"])
+def test_small_ragged(gpu_lib, arch, h, V, F, n, ds_mode):
     cfg = S.Cfg(name="small", hidden=h, vocab=V, ffn=F, arch=arch, tokens=n, layers=2,
                 after=[1, 2], init="random", seed=11)
-    _run_and_compare(gpu_lib, cfg, n, [1.0, 0.75])
+    _run_and_compare(gpu_lib, cfg, n, [1.0, 0.75], ds_mode=ds_mode)
 
 
 @pytest.mark.parametrize("name,n,exits", [("7b", 256, 2), ("13b", 192, 2), ("70b", 128, 1)])
@@ -249,14 +252,14 @@ def test_confidence_weighting_data_parallel_shards(gpu_lib, arch):
 
 
 @pytest.mark.parametrize("scale", [64.0, 256.0])
-def test_confident_rows_ds_precision(gpu_lib, scale, monkeypatch):
+def test_confident_rows_ds_precision(gpu_lib, scale):
     """Peaked softmax rows (p_y -> 1, the regime of a well-tuned exit): a7
     forms dS from the fp16 P~ the a5 epilogue stored (A24), except the target
     column, which is recomputed from the fp32 target logit.  W_out is scaled
     (by powers of two: the operands stay on the bf16 grid) so the logits
     spread widely, and the targets are the oracle's argmax.
 
-    Against the recompute path (EE_DS_RECOMPUTE=1: same bf16 z, dS from fp32
+    Against the recompute path (ds_mode "recompute": same bf16 z, dS from fp32
     S) the gradients must agree to 5e-3 per tensor -- this isolates A24's one
     extra fp16 rounding.  Against the oracle: at 64x the north_star gradient
     bound holds; at 256x the forward's single bf16 rounding of z (A3/A13)
@@ -271,10 +274,10 @@ def test_confident_rows_ds_precision(gpu_lib, scale, monkeypatch):
     t0 = S.targets(cfg, 300, seed=3)
     res0 = oracle_exit("mlp", params[0], hidden[0], t0, 1.0)
     targets = torch.from_numpy(np.argmax(res0.act["S"], axis=1).astype(np.int32))
-    monkeypatch.setenv("EE_DS_RECOMPUTE", "1")
-    loss_r, grads_r, _, st_r = gpu_step(gpu_lib, cfg, hidden[:1], targets, params[:1], [1.0])
-    monkeypatch.setenv("EE_DS_RECOMPUTE", "0")
-    loss, grads, aux, status = gpu_step(gpu_lib, cfg, hidden[:1], targets, params[:1], [1.0])
+    loss_r, grads_r, _, st_r = gpu_step(gpu_lib, cfg, hidden[:1], targets, params[:1], [1.0],
+                                        ds_mode="recompute")
+    loss, grads, aux, status = gpu_step(gpu_lib, cfg, hidden[:1], targets, params[:1], [1.0],
+                                        ds_mode="stored_p")
     assert status == (0, -1) and st_r == (0, -1)
     res = oracle_exit("mlp", params[0], hidden[0], targets, 1.0)
     p_y = np.exp(-res.stats["loss"])
@@ -284,6 +287,8 @@ def test_confident_rows_ds_precision(gpu_lib, scale, monkeypatch):
           for k in res.grads}
     assert all(e <= 5e-3 for e in ab.values()), ab
     orc = {k: rel_fro(grads[0][k].double().cpu().numpy(), g) for k, g in res.grads.items()}
+    orc_r = {k: rel_fro(grads_r[0][k].double().cpu().numpy(), g) for k, g in res.grads.items()}
     if scale <= 64.0:
         assert all(e <= GRAD_RTOL for e in orc.values()), orc
+        assert all(e <= GRAD_RTOL for e in orc_r.values()), orc_r
     print(scale, res.loss, float(np.median(p_y)), ab, orc)

@@ -354,6 +354,50 @@ def test_P13_adam_first_step_closed_form():
     np.testing.assert_allclose(s, th - 0.5 * g, rtol=1e-15)
 
 
+@pytest.mark.parametrize("wd", [0.0, 0.01])
+@pytest.mark.parametrize("grad_scale", [1.0, 0.25])
+def test_P13_adam_multi_step_against_torch_optim(wd, grad_scale):
+    """P:374-375 (Adam, beta1 0.9, beta2 0.95, eps 1e-5) over 6 steps with fresh
+    random gradients each step, against torch.optim.AdamW in fp64 (decoupled
+    weight decay; = torch.optim.Adam at wd 0).  Pins the moment decays and the
+    bias corrections at t > 1, which the t = 1 closed form cannot see (a
+    beta1/beta2 swap in v passes P13 and fails here)."""
+    rng = _rng(140)
+    th0 = rng.normal(size=(7, 33))
+    lrs = [1e-3, 5e-4, 2e-3, 1e-4, 7e-4, 3e-4]
+    t = torch.tensor(th0, dtype=torch.float64, requires_grad=True)
+    opt = torch.optim.AdamW([t], lr=lrs[0], betas=(0.9, 0.95), eps=1e-5, weight_decay=wd)
+    th, m, v = th0.copy(), np.zeros_like(th0), np.zeros_like(th0)
+    for step, lr in enumerate(lrs, start=1):
+        g = rng.normal(size=th0.shape) * 10 ** rng.uniform(-4, 1, th0.shape)
+        th, m, v = O.adam_update(th, g, m, v, lr, 0.9, 0.95, 1e-5, wd, step, grad_scale)
+        for grp in opt.param_groups:
+            grp["lr"] = lr
+        t.grad = torch.tensor(g * grad_scale)
+        opt.step()
+        np.testing.assert_allclose(th, t.detach().numpy(), rtol=1e-12, atol=1e-15)
+        st = opt.state[t]
+        np.testing.assert_allclose(m, st["exp_avg"].numpy(), rtol=1e-13, atol=0)
+        np.testing.assert_allclose(v, st["exp_avg_sq"].numpy(), rtol=1e-13, atol=0)
+
+
+@pytest.mark.parametrize("momentum", [0.0, 0.9])
+def test_P13_sgd_momentum_against_torch_optim(momentum):
+    """SGD (the ee_sgd_update alternative) with heavy-ball momentum b = mu b + g
+    (b_1 = g), theta -= lr b, over 5 steps against torch.optim.SGD in fp64."""
+    rng = _rng(141)
+    th0 = rng.normal(size=(5, 17))
+    t = torch.tensor(th0, dtype=torch.float64, requires_grad=True)
+    opt = torch.optim.SGD([t], lr=0.1, momentum=momentum)
+    th, buf = th0.copy(), None
+    for _ in range(5):
+        g = rng.normal(size=th0.shape)
+        th, buf = O.sgd_update(th, g, buf, 0.1, momentum, grad_scale=0.5)
+        t.grad = torch.tensor(0.5 * g)
+        opt.step()
+        np.testing.assert_allclose(th, t.detach().numpy(), rtol=1e-13, atol=1e-15)
+
+
 # --------------------------------------------------------------------------- P14
 def test_P14_lr_schedule_and_token_budget():
     T = 40000                                                          # P:368
