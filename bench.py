@@ -3,18 +3,26 @@
 
 One "step" = one pass of the whole hot path: for every
 exit, the exit-head forward, softmax cross-entropy, backward into the exit
-parameters (ee_tune_step), plus the Adam update of all exit parameters
-(ee_adam_update).  Default workload (N=1): the 70B-shaped head set of
-BASELINE.json configs[3] (h 8192, V 32000, F 28672, 4 MLP exits, 32 x 2048
-tokens), unsharded W_out; synthetic seeded inputs (eesynth), Copy init from a
-synthetic backbone.
+parameters, plus the Adam update of all exit parameters.
+
+Default workload at EVERY N (strong scaling, so the driver's per-N values
+compare): BASELINE.json configs[4] / SURVEY C4, `70b_dp` -- 70B-shaped heads
+(h 8192, V 32000, F 28672), 8 MLP exits at layers 10..80, 65 536 global tokens
+(32 x 2048) split over the N ranks, unsharded W_out; synthetic seeded inputs
+(eesynth), Copy init from a synthetic backbone.  The step is the fused
+data-parallel path (parallel.ShardedDPHeads: gradient reduce-scatter fused into
+the weight-gradient GEMM epilogues over CUDA-IPC peer memory, sharded Adam
+whose operand stores are the all-gather, ZeRO-1) at every N, N = 1 included.
+dS is recomputed (ds_mode "recompute": no [tokens x vocab] matrix in HBM);
+the stored-P~ ablation (A24) is timed beside it at N = 1.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config 70b_dp|70b|13b|7b|13b_layer] [--parallel dp|vp]
+                  [--scaling strong|weak] [--ds-mode recompute|stored_p]
 
-N > 1 (torchrun, one process per GPU): data parallel over tokens, 32 x 2048
-tokens per GPU (weak scaling); the global valid-token count and every exit's
-gradients are all-reduced over NCCL, each exit's all-reduce overlapping the
-next exit's compute.  Rank 0 prints one JSON line.
+--gpus N > 1 without WORLD_SIZE in the environment re-launches this script
+under torch.distributed.run with N ranks (127.0.0.1); under torchrun --gpus
+must equal WORLD_SIZE.  Rank 0 prints one JSON line.
 """
 
 from __future__ import annotations

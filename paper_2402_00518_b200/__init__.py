@@ -640,6 +640,59 @@ class HeadSpec:
                     rope_theta=self.rope_theta, ds_mode=self.ds_mode)
 
 
+class HostStager:
+    """Streams per-exit hidden states from pinned host memory to the device
+    for the host-input step APIs (ExitHeads.step_host, ShardedDPHeads.step
+    with hidden_host): exit i + 1's copy runs on a copy stream while exit i
+    computes, through two device staging buffers ordered by events.
+
+    Protocol per step: tg = begin(hidden_host, targets_host, st); then for each
+    exit i: buf = get(i, st) (stream st waits for exit i's copy and exit
+    i + 1's copy is issued), launch exit i's work on st reading buf, release(i,
+    st).  The buffers are sized once (max_tokens rows) and never reallocated;
+    the copy stream waits for the allocating stream before its first write, so
+    blocks the caching allocator recycled from work still queued on that
+    stream are not overwritten early."""
+
+    def __init__(self, max_tokens: int, hidden: int, device):
+        st = torch.cuda.current_stream(device)
+        self.bufs = [torch.empty(max_tokens, hidden, dtype=torch.bfloat16, device=device)
+                     for _ in range(2)]
+        self.tg = torch.empty(max_tokens, dtype=torch.int32, device=device)
+        self.cs = torch.cuda.Stream(device)
+        self.cs.wait_stream(st)
+        self.copied = [torch.cuda.Event(), torch.cuda.Event()]
+        self.free = [torch.cuda.Event(), torch.cuda.Event()]
+        self.used = [False, False]
+        self.src = None
+
+    def _stage(self, i):
+        b = i % 2
+        with torch.cuda.stream(self.cs):
+            if self.used[b]:         # the previous reader of buffer b (this or the last call)
+                self.cs.wait_event(self.free[b])
+            self.bufs[b][:self.n].copy_(self.src[i], non_blocking=True)
+            self.copied[b].record(self.cs)
+
+    def begin(self, hidden_host, targets_host, st):
+        self.src = hidden_host
+        self.n = hidden_host[0].shape[0]
+        tg = self.tg[:self.n]
+        tg.copy_(targets_host, non_blocking=True)   # on st: ordered after st's earlier readers
+        self._stage(0)
+        return tg
+
+    def get(self, i, st):
+        if i + 1 < len(self.src):
+            self._stage(i + 1)
+        st.wait_event(self.copied[i % 2])
+        return self.bufs[i % 2][:self.n]
+
+    def release(self, i, st):
+        self.free[i % 2].record(st)
+        self.used[i % 2] = True
+
+
 class ExitHeads:
     """The exit-head parameter store of one EE-Tuning run on one GPU.
 
@@ -807,36 +860,21 @@ class ExitHeads:
         """One tuning step with the cached hidden states in pinned HOST memory
         (the usual place for them: 4.3 GB per step at the 70B shape).  Exit
         i + 1's hidden states are copied host-to-device on a side stream while
-        exit i computes (two device staging buffers, event-ordered), so the
-        PCIe/C2C transfer hides under the exit's GEMMs.  Same results as
+        exit i computes (HostStager: two device staging buffers, event-ordered),
+        so the PCIe/C2C transfer hides under the exit's GEMMs.  Same results as
         step() on device copies of the same bytes.  With lr given, each exit is
         updated right after its backward: Adam on a side stream overlapping the
         next exit (= step_overlapped(); call join() before reading parameters),
         or fused into the backward's epilogues (fused_adam; = step_adam()).
         Returns the device losses."""
         E = self.spec.num_exits
-        n, h = hidden_host[0].shape
+        n = hidden_host[0].shape[0]
         if n > self.max_tokens:
             raise ValueError("more tokens than the workspace was sized for")
         dev = self.loss.device
         st = torch.cuda.current_stream(dev)
-        if getattr(self, "_stage", None) is None:
-            # Sized once for max_tokens and never reallocated.  The blocks come
-            # from the caching allocator on `st`, which may hand back memory
-            # that kernels still queued on `st` read (e.g. the inputs of a
-            # preceding async step()); the copy stream's first write must
-            # therefore wait for everything queued on `st` so far.
-            self._stage = [torch.empty(self.max_tokens, h, dtype=torch.bfloat16, device=dev)
-                           for _ in range(2)]
-            self._stage_tg = torch.empty(self.max_tokens, dtype=torch.int32, device=dev)
-            self._copy_stream = torch.cuda.Stream(dev)
-            self._copy_stream.wait_stream(st)
-            self._ev = [[torch.cuda.Event(), torch.cuda.Event()] for _ in range(2)]
-            self._stage_used = [False, False]
-        bufs = [b[:n] for b in self._stage]
-        tg = self._stage_tg[:n]
-        cs = self._copy_stream
-        ev_copied, ev_free = self._ev[0], self._ev[1]
+        if getattr(self, "_stager", None) is None:
+            self._stager = HostStager(self.max_tokens, self.spec.hidden, dev)
         w = exit_weights if exit_weights is not None else [1.0] * E
         overlap = lr is not None and not fused_adam
         if overlap:
@@ -845,38 +883,22 @@ class ExitHeads:
             self.join()
         if lr is not None:
             self.step_count += 1
-        tg.copy_(targets_host, non_blocking=True)
-
-        def stage(b, src):
-            # into staging buffer b once its last reader (this or the previous
-            # call's exit) is done: the first exit of a call is copied while
-            # the previous call's last exit still computes
-            with torch.cuda.stream(cs):
-                if self._stage_used[b]:
-                    cs.wait_event(ev_free[b])
-                bufs[b].copy_(src, non_blocking=True)
-                ev_copied[b].record(cs)
-
-        stage(0, hidden_host[0])
+        tg = self._stager.begin(hidden_host, targets_host, st)
         for i in range(E):
-            b = i % 2
-            if i + 1 < E:
-                stage((i + 1) % 2, hidden_host[i + 1])
-            st.wait_event(ev_copied[b])
+            buf = self._stager.get(i, st)
             if lr is None or overlap:
                 if overlap:
                     self._before_tune(i, st)
-                ee_tune_step(self.exit_cfg, [bufs[b]], tg, w[i:i + 1], self.operand[i:i + 1],
+                ee_tune_step(self.exit_cfg, [buf], tg, w[i:i + 1], self.operand[i:i + 1],
                              self.grads[i:i + 1], self.loss[i:i + 1], self.workspace)
                 if overlap:
                     self._adam_async(i, lr, st)
             else:
-                ee_tune_step_adam(self.exit_cfg, [bufs[b]], tg, w[i:i + 1],
+                ee_tune_step_adam(self.exit_cfg, [buf], tg, w[i:i + 1],
                                   self.operand[i:i + 1], self.master[i:i + 1], self.m[i:i + 1],
                                   self.v[i:i + 1], lr, self.step_count, self.loss[i:i + 1],
                                   self.workspace)
-            ev_free[b].record(st)
-            self._stage_used[b] = True
+            self._stager.release(i, st)
         return self.loss
 
     def step_per_exit(self, hidden, targets, lr, exit_weights=None, valid_count=None,

@@ -167,6 +167,7 @@ class ShardedDPHeads:
         self.epoch = 0
         self.workspace = torch.zeros(ee.ee_workspace_size(self.cfg, max_tokens),
                                      dtype=torch.uint8, device=dev)
+        self.workspace_tokens = int(max_tokens)
         self.loss = torch.zeros(E, dtype=torch.float32, device=dev)
         self.wsum = torch.zeros(E, dtype=torch.float32, device=dev)   # sum_t c_t per exit
         self.step_count = 0
@@ -247,6 +248,25 @@ class ShardedDPHeads:
         """One tuning step + Adam on this rank's tokens.  all_reduce(t) sums a
         small tensor over the ranks in place (the valid-token count before the
         step, the per-exit losses after); None = one rank."""
+        return self._step(lambda i: hidden[i], None, targets, lr, all_reduce, exit_weights,
+                          beta1, beta2, eps, weight_decay)
+
+    def step_host(self, hidden_host, targets_host, lr, all_reduce=None, exit_weights=None,
+                  beta1=0.9, beta2=0.95, eps=1e-5, weight_decay=0.0):
+        """step() with this rank's hidden states and targets in pinned host
+        memory: exit i + 1's H2D copy overlaps exit i's compute (HostStager)."""
+        ee = self.ee
+        dev = self.loss.device
+        st = torch.cuda.current_stream(dev)
+        if getattr(self, "_stager", None) is None:
+            self._stager = ee.HostStager(self.workspace_tokens, self.spec.hidden, dev)
+        stg = self._stager
+        tg = stg.begin(hidden_host, targets_host, st)
+        return self._step(lambda i: stg.get(i, st), lambda i: stg.release(i, st), tg, lr,
+                          all_reduce, exit_weights, beta1, beta2, eps, weight_decay)
+
+    def _step(self, hidden_of, release, targets, lr, all_reduce, exit_weights, beta1, beta2,
+              eps, weight_decay):
         ee = self.ee
         E = self.spec.num_exits
         w = exit_weights if exit_weights is not None else [1.0] * E
@@ -261,9 +281,11 @@ class ShardedDPHeads:
         for i in range(E):
             j = i % self.n_arenas
             aux = [{"weight_sum": self.wsum[i:i + 1]}] if self.conf else None
-            ee.ee_tune_step_rs(self.exit_cfg, hidden[i:i + 1], targets, w[i:i + 1],
+            ee.ee_tune_step_rs(self.exit_cfg, [hidden_of(i)], targets, w[i:i + 1],
                                self.operand[i:i + 1], [self.arena_sets[j]],
                                self.loss[i:i + 1], self.workspace, aux=aux, valid_count=W)
+            if release is not None:
+                release(i)
             if self.conf and all_reduce is not None:
                 all_reduce(self.wsum[i:i + 1])   # global sum_t c_t: the gradient divisor
             self.barrier()                   # every rank's partials of exit i have landed
