@@ -132,73 +132,125 @@ def attn_kw(cfg):
                 seq_len=cfg.seq_len)
 
 
-def cpu_oracle_inputs(cfg, n_sub, seed):
-    """Bounded sample of the workload for the fp64 oracle: the first exit's
-    parameters at full h, V, F and n_sub tokens (seeded eesynth draws)."""
-    import numpy as np
-    import eesynth as S
-    from eesynth import to_f64
-    one = S.Cfg(name=cfg.name, hidden=cfg.hidden, vocab=cfg.vocab, ffn=cfg.ffn, arch=cfg.arch,
-                tokens=n_sub, layers=cfg.layers, after=cfg.after[:1], init=cfg.init, seed=cfg.seed,
-                n_heads=cfg.n_heads, n_kv_heads=cfg.n_kv_heads,
-                seq_len=min(cfg.seq_len, n_sub) if cfg.arch == "layer" else 0)
-    p = S.head_params(one, seed=seed)[0]
-    p64 = {}
-    for k in list(p):
-        p64[k] = to_f64(p.pop(k))
-    x = to_f64(S.hidden_states(one, n_sub, seed=seed)[0])
-    y = S.targets(one, n_sub, seed=seed).numpy().astype(np.int64)
-    return p64, x, y
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
-def cpu_oracle_time(cfg, inputs):
-    """Times the fp64 oracle (as it stands) on one exit of the sample.
-    Returns (seconds, threads used)."""
-    from oracle import ee_oracle as O
+class OracleSample:
+    """Bounded sample of the workload for the fp64 oracle: the config's exits
+    at full h, V, F on n_sub tokens, each exit with its own seeded hidden
+    states.  The exits share ONE seeded parameter draw (widened to fp64 once:
+    7.7 GB at the 70B shape; drawing a set takes ~10 s on the host), which
+    does not change the oracle's work: its time does not depend on the
+    values.  Timing covers only oracle.exit_loss_and_grads (forward, CE and
+    backward of an exit)."""
+
+    def __init__(self, cfg, n_sub, seed):
+        import numpy as np
+        import eesynth as S
+        from eesynth import to_f64
+        self.cfg, self.n_sub = cfg, n_sub
+        one = S.Cfg(name=cfg.name, hidden=cfg.hidden, vocab=cfg.vocab, ffn=cfg.ffn,
+                    arch=cfg.arch, tokens=n_sub, layers=cfg.layers, after=list(cfg.after),
+                    init=cfg.init, seed=cfg.seed, n_heads=cfg.n_heads,
+                    n_kv_heads=cfg.n_kv_heads,
+                    seq_len=min(cfg.seq_len, n_sub) if cfg.arch == "layer" else 0)
+        self.x = [to_f64(t) for t in S.hidden_states(one, n_sub, seed=seed)]
+        self.y = S.targets(one, n_sub, seed=seed).numpy().astype(np.int64)
+        one.after = one.after[:1]
+        one.exits = 1
+        p = S.head_params(one, seed=seed)[0]
+        self.params = {k: to_f64(p.pop(k)) for k in list(p)}
+
+    def run(self, exits=None):
+        """Seconds of oracle compute over `exits` (indices; default all)."""
+        import eesynth as S
+        from oracle import ee_oracle as O
+        at = None
+        if self.cfg.arch == "layer":     # the sample is one sequence of n_sub tokens
+            at = dict(S.attn_geometry(self.cfg), seq_len=self.n_sub)
+        total = 0.0
+        for i in (range(self.cfg.exits) if exits is None else exits):
+            t0 = time.perf_counter()
+            O.exit_loss_and_grads(self.cfg.arch, self.params, self.x[i], self.y, 1.0, 1e-5,
+                                  attn=at)
+            total += time.perf_counter() - t0
+        return total
+
+
+def oracle_threads():
     try:
         from threadpoolctl import threadpool_info
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] or [os.cpu_count()])
+        return max([i.get("num_threads", 1) for i in threadpool_info()] or [os.cpu_count()])
     except Exception:
-        cores = os.cpu_count()
-    import eesynth as S
-    p64, x, y = inputs
-    at = None
-    if cfg.arch == "layer":     # the sample is one sequence of len(x) tokens
-        at = dict(S.attn_geometry(cfg), seq_len=x.shape[0])
-    t0 = time.perf_counter()
-    O.exit_loss_and_grads(cfg.arch, p64, x, y, 1.0, 1e-5, attn=at)
-    return time.perf_counter() - t0, cores
+        return os.cpu_count()
 
 
-def cpu_oracle_sample(cfg, n_sub, seed):
-    return cpu_oracle_time(cfg, cpu_oracle_inputs(cfg, n_sub, seed))
+def cpu_baseline(cfg, args):
+    """The fp64 oracle on this host's cores: all exits on n_sub tokens with
+    every BLAS thread, and one exit with one thread (threadpoolctl)."""
+    smp = OracleSample(cfg, args.cpu_tokens, seed=cfg.seed)
+    t_all = smp.run()
+    cores = oracle_threads()
+    out = {"value": args.cpu_tokens / t_all, "unit": "tokens/s", "cores": cores,
+           "kind": "oracle", "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+           "sample": f"fp64 oracle (oracle/ee_oracle.py as it stands), all {cfg.exits} exits of "
+                     f"{cfg.name} on {args.cpu_tokens} tokens at full h/V/F (own hidden states, "
+                     f"one shared parameter draw); {t_all:.2f} s with {cores} BLAS threads; "
+                     f"Adam not included",
+           "seconds": t_all}
+    try:
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=1):
+            t1 = smp.run(exits=[0])
+        out["one_core"] = {"value": args.cpu_tokens / (t1 * cfg.exits), "unit": "tokens/s",
+                           "cores": 1, "seconds_one_exit": t1,
+                           "sample": f"exit 1 of {cfg.exits} on {args.cpu_tokens} tokens, one "
+                                     f"BLAS thread; value = tokens / (t x {cfg.exits} exits)"}
+    except Exception as ex:
+        out["one_core"] = {"value": None, "error": repr(ex)}
+    return out
 
 
 def run_reference(args, cfg, rank, world):
-    """--impl reference: the oracle on the host cores (bounded sample per step)."""
+    """--impl reference: the fp64 oracle as it stands on the host cores, rank 0
+    only (other ranks exit 0).  Bounded so the driver's --steps K --warmup W
+    run ends in minutes: step k runs ONE exit, exit k mod E, on n_sub =
+    --ref-tokens tokens at full h/V/F, and ms_per_step is that step's
+    measured time.  value = tokens/s of the whole E-exit step at that rate =
+    n_sub / (E x mean step time); exit_tokens_per_s = n_sub / mean step time."""
     if rank != 0:
         return
-    n_sub = args.cpu_tokens
+    n_sub = args.ref_tokens
+    smp = OracleSample(cfg, n_sub, seed=cfg.seed)
     times = []
-    cores = None
-    inputs = cpu_oracle_inputs(cfg, n_sub, seed=cfg.seed)
     for i in range(args.warmup + args.steps):
-        t, cores = cpu_oracle_time(cfg, inputs)
+        t = smp.run(exits=[i % cfg.exits])
         if i >= args.warmup:
             times.append(t)
-    t_step = statistics.mean(times) * cfg.exits       # all exits of the step
-    value = n_sub / t_step
-    sample = (f"fp64 oracle, exit 1 of {cfg.exits} on {n_sub} tokens at full h/V/F, "
-              f"scaled x{cfg.exits} exits; Adam not included"
-              + ("; Layer exit: one sequence of that many tokens (the T-dependent attention "
-                 "core is ~2% of the per-token work at T = 2048)" if cfg.arch == "layer" else ""))
+    t_step = statistics.mean(times)
+    value = n_sub / (t_step * cfg.exits)
+    cores = oracle_threads()
+    sample = (f"fp64 oracle (oracle/ee_oracle.py as it stands); each step one exit of "
+              f"{cfg.exits} (rotating) of {cfg.name} on {n_sub} tokens at full h/V/F; value = "
+              f"tokens / (E x step time); one shared parameter draw; Adam not included")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": t_step * 1e3, "higher_is_better": True,
+            "scaling": "strong" if args.scaling == "strong" else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(cfg, 1, args),
+            "exit_tokens_per_s": n_sub / t_step,
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores,
-                             "kind": "oracle", "sample": sample},
+                             "kind": "oracle", "sample": sample, "cpu_model": cpu_model(),
+                             "nproc": os.cpu_count()},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -229,19 +281,35 @@ def vp_comm_desc(args, vp, world):
     return {"vp_comm": f"{base} all-gather / reduce-scatter"}
 
 
+def tokens_per_rank(cfg, world, args):
+    """Strong scaling (default; always for vp): the config's global tokens
+    split over the ranks.  Weak scaling: the config's tokens on every rank."""
+    if args.parallel == "vp" or args.scaling == "strong":
+        if cfg.tokens % world:
+            raise SystemExit(f"{cfg.tokens} tokens do not split over {world} ranks")
+        return cfg.tokens // world
+    return cfg.tokens
+
+
+DS_LABEL = {"recompute": "recompute (a second S GEMM forms dS; no [tokens x vocab] matrix in HBM)",
+            "stored_p": "stored fp16 P~ [tokens x vocab] in HBM (A24 ablation)"}
+
+
 def workload_config(cfg, world, args):
-    vp = getattr(args, "parallel", "dp") == "vp"
-    tok = cfg.tokens // world if vp else cfg.tokens
+    vp = args.parallel == "vp"
+    tok = tokens_per_rank(cfg, world, args)
+    global_tokens = cfg.tokens if (vp or args.scaling == "strong") else cfg.tokens * world
     return {"workload": f"{cfg.name}: h {cfg.hidden}, V {cfg.vocab}, F {cfg.ffn}, "
-                        f"{cfg.exits} {cfg.arch} exits, {tok} tokens/GPU, "
-                        f"{cfg.init} init, " + (f"W_out vocab-parallel over {world}" if vp
-                                                else "W_out unsharded"),
-            "global_batch": (cfg.tokens // 2048) * (1 if vp else world), "seq_len": 2048,
+                        f"{cfg.exits} {cfg.arch} exits, {global_tokens} global tokens, "
+                        f"{tok} tokens/GPU, {cfg.init} init, "
+                        + (f"W_out vocab-parallel over {world}" if vp else "W_out unsharded"),
+            "global_batch": max(1, global_tokens // 2048), "seq_len": 2048,
             "tokens_per_gpu": tok, "exits": cfg.exits,
             "parallelism": f"vp{world}" if vp else f"dp{world}",
-            "collectives": ("none" if world == 1 else
+            "ds": DS_LABEL[args.ds_mode],
+            "collectives": ("none (one rank)" if world == 1 else
                             "gloo, ranks sharing one GPU (test mode)" if getattr(args, "shared_gpu", False)
-                            else "NCCL (torch.distributed)"),
+                            else "NCCL (torch.distributed) for the small ones"),
             **vp_comm_desc(args, vp, world),
             "l2": "inputs larger than L2 (hidden states + exit weights per step >> 126 MB)",
             "optimizer": "Adam (P:374-375), included in the step",
@@ -253,7 +321,8 @@ def workload_config(cfg, world, args):
                                 "next exit (P:261)" if getattr(args, "overlapped", False) else
                                 "per exit, shared gradient buffers (P:261)"
                                 if getattr(args, "per_exit", False) else
-                                "per exit: tune, barrier, sharded Adam (P:261)"
+                                "per exit: tune with the gradient rows stored to their owners, "
+                                "peer barrier, sharded Adam (ZeRO-1; P:261)"
                                 if getattr(args, "dp_fused", False) else "all exits, then Adam")}
 
 
@@ -302,15 +371,59 @@ def bench_backbone(ee, torch, cfg, args, dev):
             "attention_share": att / ms}
 
 
+def free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def launch_ranks(args):
+    """--gpus N > 1 outside torchrun: re-run this script under
+    torch.distributed.run with N ranks on 127.0.0.1.  Under torchrun, --gpus
+    must equal WORLD_SIZE (a mismatch would time the wrong job)."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is None:
+        if args.gpus > 1:
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                   f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+                   f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+            print("[bench] launching: " + " ".join(cmd), file=sys.stderr, flush=True)
+            sys.exit(subprocess.run(cmd).returncode)
+        return
+    if int(ws) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; pass --gpus {ws}")
+
+
+def rank_evidence(torch, dev, rank):
+    p = torch.cuda.get_device_properties(dev)
+    return {"rank": rank, "device": dev.index, "name": p.name,
+            "pci_bus_id": getattr(p, "pci_bus_id", None),
+            "uuid": str(getattr(p, "uuid", "")), "host": os.uname().nodename,
+            "visible": os.environ.get("CUDA_VISIBLE_DEVICES")}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="70b")
-    ap.add_argument("--tokens", type=int, default=0, help="override tokens per GPU")
-    ap.add_argument("--cpu-tokens", type=int, default=32)
+    ap.add_argument("--config", default="70b_dp")
+    ap.add_argument("--tokens", type=int, default=0,
+                    help="override the config's tokens (global under strong scaling)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="dp: strong = the config's global tokens split over the ranks "
+                         "(default); weak = the config's tokens on every rank")
+    ap.add_argument("--ds-mode", default="recompute", choices=["recompute", "stored_p"],
+                    help="a7: recompute S for dS (default, north_star) or the stored-P~ "
+                         "ablation (A24)")
+    ap.add_argument("--no-ds-ablation", action="store_true",
+                    help="N=1: skip timing the other ds_mode beside the headline")
+    ap.add_argument("--cpu-tokens", type=int, default=32,
+                    help="token sample of the fp64 oracle in cpu_baseline (all exits)")
+    ap.add_argument("--ref-tokens", type=int, default=32,
+                    help="--impl reference: tokens of the one exit each step runs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quick", action="store_true", help="ncu/profiling run: no extras")
@@ -318,22 +431,18 @@ def main():
                     help="also time the frozen backbone partial forward (NEXT #3, P:260) over "
                          "this many Llama-2 layers of the config's shape (70b: 20 = 1/4 depth)")
     ap.add_argument("--grad-buffers", type=int, default=-1,
-                    help="k < exits: exits share k gradient buffers and are updated one by one "
-                         "(P:261); default 2 when the config has more than 4 exits")
-    ap.add_argument("--dp-comm", default="fused", choices=["fused", "nccl"],
-                    help="dp, N>1: fused = gradient reduce-scatter in the weight-gradient GEMM "
+                    help="non-fused paths, k < exits: exits share k gradient buffers and are "
+                         "updated one by one (P:261); default 2 when the config has > 4 exits")
+    ap.add_argument("--dp-comm", default="fused", choices=["fused", "nccl", "plain"],
+                    help="dp: fused = gradient reduce-scatter in the weight-gradient GEMM "
                          "epilogues + sharded Adam storing the operands to every rank (CUDA-IPC "
-                         "peer memory, ZeRO-1); nccl = NCCL all-reduce + full Adam per rank")
+                         "peer memory, ZeRO-1; used at N=1 too); nccl = NCCL all-reduce + full "
+                         "Adam per rank; plain = N=1 only: ExitHeads step + Adam (no DP machinery)")
     ap.add_argument("--overlap", action="store_true",
-                    help="N=1: exit-by-exit step with each exit's Adam on a side stream "
-                         "(ExitHeads.step_overlapped); measured equal to the default "
-                         "all-exits-then-Adam step (profiles/r01f_adam_overlap_ab.log)")
+                    help="plain N=1: exit-by-exit step with each exit's Adam on a side stream")
     ap.add_argument("--fused-adam", action="store_true",
-                    help="N=1: Adam fused into the weight-gradient epilogues "
-                         "(ee_tune_step_adam) instead of ee_tune_step + ee_adam_update; "
-                         "measured slower (profiles/r01f_fused_adam_ab.log), so opt-in")
-    ap.add_argument("--force-dp-fused", action="store_true",
-                    help="run the fused DP path at N=1 as well (A/B against the plain step)")
+                    help="plain N=1: Adam fused into the weight-gradient epilogues "
+                         "(ee_tune_step_adam)")
     ap.add_argument("--vp-replicated-body", action="store_true",
                     help="vp fused: all-reduce the exit body's gradients and update it on "
                          "every rank instead of the sharded (ZeRO-1) body update")
@@ -341,9 +450,10 @@ def main():
                     help="vp: fused = z all-gather / dz reduce-scatter inside the a4 / a8 "
                          "kernels over CUDA-IPC peer memory; nccl = NCCL collectives")
     ap.add_argument("--parallel", default="dp", choices=["dp", "vp"],
-                    help="N>1: dp = data parallel over tokens (weak scaling); vp = W_out "
-                         "vocab-parallel with the distributed softmax-CE (strong scaling)")
+                    help="dp = data parallel over tokens; vp = W_out vocab-parallel with the "
+                         "distributed softmax-CE (configs[3]: --config 70b --parallel vp)")
     args = ap.parse_args()
+    launch_ranks(args)
 
     import torch
     import torch.distributed as dist
@@ -370,14 +480,22 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")           # per-rank init evidence (stderr)
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if shared_gpu:
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
     multi = world > 1
+    ev = rank_evidence(torch, dev, rank)
+    ranks = [ev]
+    if multi:
+        ranks = [None] * world
+        dist.all_gather_object(ranks, ev)
+    print(f"[bench] rank {rank}/{world}: {ev}", file=sys.stderr, flush=True)
     vp = args.parallel == "vp"
     dp = world > 1 and not vp
-    n = cfg.tokens // world if vp else cfg.tokens       # tokens of this rank's exit bodies
+    n = tokens_per_rank(cfg, world, args)               # tokens of this rank's exit bodies
     n_all = cfg.tokens if vp else n
     E = cfg.exits
     from paper_2402_00518_b200.parallel import (GpuPhases, LocalComm, PeerBuffers,
@@ -385,23 +503,28 @@ def main():
                                                 data_parallel_step, vocab_parallel_step,
                                                 vocab_parallel_step_fused, vocab_shard)
     vb, ve = vocab_shard(cfg.vocab, world, rank) if vp else (0, cfg.vocab)
+    spec_kw = dict(ds_mode=args.ds_mode, **attn_kw(cfg))
 
     # ---- parameter store, Copy init from a synthetic backbone
+    if args.dp_comm == "plain" and multi:
+        raise SystemExit("--dp-comm plain is the one-GPU path")
     gbuf = args.grad_buffers if args.grad_buffers >= 0 else (2 if E > 4 else 0)
     if vp:
         gbuf = 0
-    dp_fused = not vp and (
-        (dp and args.dp_comm == "fused") or args.force_dp_fused)
+    dp_fused = not vp and args.dp_comm == "fused"
     heads = None
+    peer_map = None
     if dp_fused:     # gradient reduce-scatter in the GEMM epilogues + sharded Adam (ZeRO-1)
         heads = ShardedDPHeads(ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch,
-                                           **attn_kw(cfg)), n, rank, world, device=dev)
+                                           **spec_kw), n, rank, world, device=dev)
         err = None
         try:
             if world > 1:
                 heads.connect_ipc()
+                peer_map = {"kind": "CUDA IPC", "opened_peer_mappings": len(heads._opened)}
             else:
                 heads.connect_local([heads])
+                peer_map = {"kind": "local (one rank)"}
         except Exception as e:       # agree on the fallback on every rank
             err = e
         ok = torch.tensor([0 if err else 1], device=dev)
@@ -417,7 +540,7 @@ def main():
     vp_zero = vp and args.vp_comm == "fused" and not args.vp_replicated_body
     if vp_zero:
         heads = ShardedVPHeads(ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch,
-                                           **attn_kw(cfg)), n_all, rank, world, device=dev)
+                                           **spec_kw), n_all, rank, world, device=dev)
         torch.cuda.synchronize()
         if world > 1:
             heads.connect_ipc()
@@ -426,11 +549,10 @@ def main():
     args.vp_zero = vp_zero
     if heads is None:
         heads = ee.ExitHeads(ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch,
-                                         vocab_begin=vb, vocab_end=ve, **attn_kw(cfg)), n_all,
+                                         vocab_begin=vb, vocab_end=ve, **spec_kw), n_all,
                              device=dev, grad_buffers=gbuf if gbuf > 0 else None)
     fused_adam = not multi and not vp and not dp_fused and args.fused_adam
     args.fused_adam = fused_adam
-    # one GPU: exit by exit with Adam overlapped on a side stream (any grad-buffer count)
     overlapped = not multi and not vp and not dp_fused and not fused_adam and args.overlap
     args.overlapped = overlapped
     per_exit = ((not dp_fused) and (not vp_zero) and (not fused_adam) and (not overlapped)
@@ -478,15 +600,19 @@ def main():
         comm = TorchComm() if world > 1 else LocalComm()
         phases = GpuPhases(ee, heads.exit_cfg if vp_zero else heads.cfg, heads.workspace)
     else:
+        # strong scaling: rank r holds tokens [r n, (r+1) n) of the global batch
+        # (each rank draws its own shard; seeds differ per rank)
         hidden = S.hidden_states(cfg, n, seed=cfg.seed * 100 + rank, device=dev)
         targets = S.targets(cfg, n, seed=cfg.seed * 100 + rank, device=dev)
     vc = torch.zeros(1, dtype=torch.int64, device=dev)
     job_tokens = n_all if vp else n * world
     total_iters = 40000
-    one_cfg = ee.make_config(cfg.hidden, cfg.vocab, cfg.ffn, 1, cfg.arch, **attn_kw(cfg))
+    one_cfg = ee.make_config(cfg.hidden, cfg.vocab, cfg.ffn, 1, cfg.arch, **spec_kw)
+    all_reduce = dist.all_reduce if multi else None
 
-    def step(it, hid=hidden, tg=targets):
-        lr = ee.ee_lr_at(min(it + 1, total_iters), total_iters)
+    def step(it, hid=hidden, tg=targets, lr=None):
+        if lr is None:
+            lr = ee.ee_lr_at(min(it + 1, total_iters), total_iters)
         if fused_adam:     # one GPU: Adam fused into the weight-gradient epilogues
             heads.step_adam(hid, tg, lr)
             return
@@ -494,7 +620,7 @@ def main():
             heads.step_overlapped(hid, tg, lr)
             return
         if dp_fused:       # exit by exit: tune -> peer barrier -> sharded Adam
-            heads.step(hid, tg, lr, all_reduce=dist.all_reduce if multi else None)
+            heads.step(hid, tg, lr, all_reduce=all_reduce)
             return
         if per_exit:       # exit-by-exit update with shared gradient buffers
             W = None
@@ -538,14 +664,32 @@ def main():
                                heads.loss)
         heads.adam(lr)
 
-    if multi:       # line the ranks up before the first peer barrier (its timeout is 20 s)
+    def sync():
         torch.cuda.synchronize()
-        dist.barrier()
+        if multi:
+            dist.barrier()
+
+    def timed(fn, steps):
+        """Device time per step of `steps` calls of fn(it): CUDA events on the
+        launching stream, barrier + synchronize on both sides, max over ranks."""
+        sync()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for it in range(steps):
+            fn(it)
+        if hasattr(heads, "join"):
+            heads.join()            # the last side-stream update is inside the timed region
+        e1.record()
+        sync()
+        t = torch.tensor([e0.elapsed_time(e1) / steps], device=dev)
+        if multi:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    sync()          # line the ranks up before the first peer barrier (its timeout is 20 s)
     for it in range(args.warmup):
         step(it)
-    torch.cuda.synchronize()
-    if multi:
-        dist.barrier()
+    sync()
 
     # ---- timed region (device time, CUDA events on the launching stream)
     sampler = ClockSampler(local)
@@ -553,28 +697,36 @@ def main():
     time.sleep(0.3)
     l0 = ee.ee_launch_count()
     ee.ee_profile_start()
-    torch.cuda.synchronize()
-    if multi:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for it in range(args.steps):
-        step(args.warmup + it)
-    if hasattr(heads, "join"):
-        heads.join()            # the last side-stream update is inside the timed region
-    e1.record()
-    torch.cuda.synchronize()
-    if multi:
-        dist.barrier()
+    ms = timed(lambda it: step(args.warmup + it), args.steps)
     prof = ee.ee_profile_stop()
     launches = ee.ee_launch_count() - l0
     clocks = sampler.stop()
-    ms = e0.elapsed_time(e1) / args.steps
-    t = torch.tensor([ms], device=dev)
-    if multi:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = t.item()
     code, idx = heads.status()
+    it_done = args.warmup + args.steps
+
+    # ---- the other ds_mode, timed the same way beside the headline (N = 1)
+    ablation = None
+    if world == 1 and not args.quick and not args.no_ds_ablation and not vp:
+        other = "stored_p" if args.ds_mode == "recompute" else "recompute"
+        cfgs = [getattr(heads, "cfg", None), getattr(heads, "exit_cfg", None)]
+        for c in cfgs:
+            if c is not None:
+                c.ds_mode = ee.DS_MODE[other]
+        one_cfg.ds_mode = ee.DS_MODE[other]
+        step(it_done)
+        sampler2 = ClockSampler(local)
+        sampler2.start()
+        ms_o = timed(lambda it: step(it_done + 1 + it), args.steps)
+        cl2 = sampler2.stop()
+        for c in cfgs:
+            if c is not None:
+                c.ds_mode = ee.DS_MODE[args.ds_mode]
+        one_cfg.ds_mode = ee.DS_MODE[args.ds_mode]
+        it_done += 1 + args.steps
+        ablation = {"ds": DS_LABEL[other], "value": job_tokens / (ms_o / 1e3),
+                    "unit": "tokens/s", "ms_per_step": ms_o,
+                    "pct_of_burst_peak": step_flops(cfg, n) / (ms_o / 1e3) / 1e12
+                    / load_peaks()["bf16_tflops"], "sm_mhz": cl2.get("sm_mhz")}
 
     # ---- end to end through the public API with host buffers
     e2e = None
@@ -582,51 +734,70 @@ def main():
         h_host = [h.cpu().pin_memory() for h in hidden]
         t_host = targets.cpu().pin_memory()
         loss_host = torch.empty(E, dtype=torch.float32).pin_memory()
-        streamed = not multi and not vp and not dp_fused and not per_exit
-        if streamed:    # untimed warm-up of the host-input API (staging buffers, copy stream)
-            lr_w = ee.ee_lr_at(min(args.warmup + args.steps, total_iters), total_iters)
-            if overlapped or fused_adam:
-                heads.step_host(h_host, t_host, lr=lr_w, fused_adam=fused_adam)
-            else:
-                heads.step_host(h_host, t_host)
-                heads.adam(lr_w)
-        torch.cuda.synchronize()
-        if multi:
-            dist.barrier()
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record()
-        for it in range(args.steps):
-            if streamed:   # public API for host-resident hidden states: H2D overlapped per exit
-                lr_e = ee.ee_lr_at(min(args.warmup + args.steps + it + 1, total_iters),
-                                   total_iters)
-                if overlapped or fused_adam:
-                    heads.step_host(h_host, t_host, lr=lr_e, fused_adam=fused_adam)
+        # two input sets without a second copy in host memory: set B feeds
+        # exit i the hidden states of exit (i+1) mod E (a staging race that
+        # mixed buffers or calls would change the losses)
+        perm = [(i + 1) % E for i in range(E)]
+        sets_host = [(h_host, t_host), ([h_host[j] for j in perm], t_host)]
+        sets_dev = [(hidden, targets), ([hidden[j] for j in perm], targets)]
+        streamed = not vp and not per_exit and (dp_fused or not multi)
+        check = None
+        if streamed:
+            # correctness of the host-input path on alternating sets, lr = 0
+            # (Adam with lr 0 leaves the parameters bitwise unchanged)
+            def dev_step(hs, tg):
+                if dp_fused:
+                    heads.step(hs, tg, 0.0, all_reduce=all_reduce)
                 else:
-                    heads.step_host(h_host, t_host)
-                    heads.adam(lr_e)
+                    heads.step(hs, tg)
+                return heads.loss.clone()
+
+            def host_step(hs, tg, lr):
+                if dp_fused:
+                    heads.step_host(hs, tg, lr, all_reduce=all_reduce)
+                elif overlapped or fused_adam:
+                    heads.step_host(hs, tg, lr=lr, fused_adam=fused_adam)
+                else:
+                    heads.step_host(hs, tg)
+                    if lr is not None:
+                        heads.adam(lr)
+                return heads.loss
+
+            want = [dev_step(*sets_dev[k]) for k in range(2)]
+            got = [host_step(*sets_host[r % 2], 0.0 if (dp_fused or overlapped or fused_adam)
+                             else None).clone() for r in range(4)]
+            sync()
+            ok = all(torch.equal(got[r], want[r % 2]) for r in range(4))
+            check = {"alternating_sets_bitwise_equal_device_step": ok,
+                     "loss_set_a": [round(float(v), 6) for v in want[0].tolist()],
+                     "loss_set_b": [round(float(v), 6) for v in want[1].tolist()]}
+            if not ok:
+                print(f"[bench] e2e check FAILED: {got} vs {want}", file=sys.stderr, flush=True)
+        sync()
+
+        def e2e_step(it):
+            hs, tg = sets_host[it % 2]
+            lr = ee.ee_lr_at(min(it_done + it + 1, total_iters), total_iters)
+            if streamed:      # per-exit H2D overlapped with the previous exit's compute
+                host_step(hs, tg, lr)
             else:
+                hd, td = sets_dev[it % 2]
                 for d_, h_ in zip(hidden, h_host):
                     d_.copy_(h_, non_blocking=True)
                 targets.copy_(t_host, non_blocking=True)
-                step(args.warmup + args.steps + it)
+                step(it_done + it, hid=hd, tg=td, lr=lr)
             loss_host.copy_(heads.loss, non_blocking=True)
-        if hasattr(heads, "join"):
-            heads.join()
-        a1.record()
-        torch.cuda.synchronize()
-        te = torch.tensor([a0.elapsed_time(a1) / args.steps], device=dev)
-        if multi:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": job_tokens / (te.item() / 1e3), "unit": "tokens/s",
+        te = timed(e2e_step, args.steps)
+        e2e = {"value": job_tokens / (te / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": sum(h.numel() * 2 for h in hidden) + targets.numel() * 4,
-               "d2h_bytes_per_step": E * 4, "ms_per_step": te.item(),
-               "api": (("ExitHeads.step_host(lr=...) (per-exit H2D overlapped with compute, "
-                        + ("Adam fused into the epilogues)" if fused_adam else
-                           "each exit's Adam on a side stream)"))
-                       if streamed and (fused_adam or overlapped) else
-                       "ExitHeads.step_host (per-exit H2D overlapped with compute) + adam"
-                       if streamed else "H2D copies + step")}
-        del h_host
+               "d2h_bytes_per_step": E * 4, "ms_per_step": te,
+               "inputs": "pinned host memory, two alternating input sets",
+               "api": ("ShardedDPHeads.step_host (per-exit H2D overlapped with compute)"
+                       if dp_fused and streamed else
+                       "ExitHeads.step_host (per-exit H2D overlapped with compute)"
+                       if streamed else "H2D copies + step"),
+               "check": check}
+        del h_host, sets_host
 
     if rank != 0:
         if multi:
@@ -681,24 +852,29 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "strong" if vp else "weak", "vs_baseline": None,
+        "higher_is_better": True,
+        "scaling": "strong" if (vp or args.scaling == "strong") else "weak",
+        "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (seeded eesynth inputs, Copy init from a synthetic backbone)",
         "config": workload_config(cfg, world, args),
         "pct_peak": {"algorithmic_tflops_per_gpu": tflops,
                      "of_burst": tflops / peaks["bf16_tflops"],
                      "of_sustained": tflops / peaks["bf16_tflops_sustained"],
                      "of_datasheet_2250": tflops / 2250.0,
-                     "step_flops_alg": F_alg},
+                     "step_flops_alg_per_gpu": F_alg / (world if vp else 1)},
         "roofline": roofline,
         # exit-tokens/s (comparable across exit counts) and the
         # optimizer's share, reported beside the step that includes it
         "exit_tokens_per_s": E * job_tokens / (ms / 1e3),
         "update_ms_per_step": sum(d["ms"] for k, d in kern.items() if k.startswith("a15"))
                               / args.steps,
+        "ds_ablation": ablation,
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clocks,
         "status": code,
+        "ranks": ranks,
+        "peer_map": peer_map,
         "loss_last_step": [round(float(v), 6) for v in heads.loss.tolist()],
         "kernels": kernels,
     }
@@ -706,12 +882,7 @@ def main():
         line["backbone_forward"] = bench_backbone(ee, torch, cfg, args, dev)
     if world == 1 and not args.no_cpu_baseline and not args.quick:
         try:
-            t_or, cores = cpu_oracle_sample(cfg, args.cpu_tokens, seed=cfg.seed)
-            v = args.cpu_tokens / (t_or * E)
-            line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle",
-                                    "sample": f"fp64 oracle, exit 1 of {E} on {args.cpu_tokens} "
-                                              f"tokens at full h/V/F ({t_or:.1f} s), scaled "
-                                              f"x{E} exits"}
+            line["cpu_baseline"] = cpu_baseline(cfg, args)
         except Exception as ex:  # never let the baseline kill the GPU number
             line["cpu_baseline"] = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(),
                                     "kind": "oracle", "sample": f"failed: {ex!r}"}
