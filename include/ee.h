@@ -201,6 +201,55 @@ ee_status ee_init_heads(const ee_head_config* cfg, int32_t init, const ee_head_t
                         int32_t src_dtype, uint64_t seed, float std,
                         ee_head_tensors* master_fp32, ee_head_tensors* operand_bf16, void* stream);
 
+/* In-library communicator (§2.2 "Support for 3D
+ * parallelism").  Opaque; created once per rank by ee_comm_create
+ * and passed to ee_tune_step, which then runs a whole data-parallel (DP) or
+ * vocab-parallel (VP) step over the `world` ranks of a node in one call.
+ * Every exchange is this library's own kernels over NVLink peer memory (CUDA
+ * IPC mappings of each rank's symmetric ARENA): stores from the producing
+ * GEMM epilogues / norm kernels, rank-ordered (deterministic) reductions of
+ * the small vectors, and stream-ordered device barriers (ee_peer_barrier
+ * semantics, ~20 s timeout -> EE_ERR_PEER).  No NCCL, no host sync.
+ *
+ * Setup (per rank, host calls):
+ *   1. ee_comm_arena_size(cfg, mode, world, n_local, &bytes);
+ *   2. allocate `bytes` of device memory, 256-byte aligned, ZERO-FILLED, and
+ *      keep it alive as long as the comm;
+ *   3. ee_ipc_get_handle(arena) and exchange the (handle, offset) pairs with
+ *      the other ranks by any host transport (a TCP store, MPI, files);
+ *      ee_ipc_open each peer's pair (one process per GPU; ranks sharing a
+ *      process may pass the peers' device pointers directly);
+ *   4. ee_comm_create(&comm, cfg, mode, world, rank, n_local, arenas, bytes)
+ *      with arenas[q] = rank q's arena in this process (arenas[rank] = own).
+ * Every rank must have completed step 4 before any rank's first step, and
+ * all ranks must issue the same sequence of ee_tune_step(comm) calls.
+ *
+ * DP (EE_COMM_DP; cfg unsharded): hidden/targets are this rank's n_local
+ *   tokens (Layer exits: whole sequences).  W = the global valid count
+ *   (unless valid_count is given); the weight-gradient GEMM epilogues store
+ *   each gradient row into its owner's arena (fused reduce-scatter), the owner
+ *   sums the P slots in rank order and every rank gathers the reduced rows:
+ *   grads[i] = the gradient over ALL ranks' tokens, bitwise identical on every
+ *   rank; loss_out[i] = the global loss.  CONFIDENCE weighting normalises by
+ *   the global sum_t c_t (A17).  aux: this rank's tokens.
+ * VP (EE_COMM_VP; cfg->vocab_begin/end = this rank's W_out row shard):
+ *   hidden/targets are this rank's n_local tokens; the library all-gathers
+ *   the targets and z (in the a4 kernel's stores), runs the distributed
+ *   softmax-CE (rank-ordered MAX of the (max, argmax) key, SUM of the
+ *   rescaled sum-exp and target logit), stores dz rows into their owners'
+ *   slots (a8 epilogue) and reduces the exit body's gradients as in DP.
+ *   grads[i].w_out = this rank's shard; body grads identical on every rank;
+ *   loss_out[i] = the global loss; aux arrays are [world * n_local] (all
+ *   tokens).  The workspace must be sized for world * n_local tokens.
+ * n_local is fixed at creation; accumulate adds the reduced gradients. */
+typedef struct ee_comm ee_comm;
+typedef enum { EE_COMM_DP = 0, EE_COMM_VP = 1 } ee_comm_mode;
+ee_status ee_comm_arena_size(const ee_head_config* cfg, int32_t mode, int32_t world,
+                             int64_t n_local, size_t* bytes);
+ee_status ee_comm_create(ee_comm** comm, const ee_head_config* cfg, int32_t mode, int32_t world,
+                         int32_t rank, int64_t n_local, void* const* arenas, size_t arena_bytes);
+ee_status ee_comm_destroy(ee_comm* comm);
+
 /* One EE-Tuning step over all exits: per exit i, forward of the
  * exit head on hidden[i], softmax cross-entropy against `targets`, and the
  * gradient of exit_weights[i] * L_i w.r.t. the exit's parameters only (the
@@ -220,13 +269,15 @@ ee_status ee_init_heads(const ee_head_config* cfg, int32_t init, const ee_head_t
  *                  valid tokens (data parallelism, A16).  NULL = count the
  *                  local targets.
  *   workspace      device scratch of ws_bytes >= ee_workspace_size().
+ *   comm           NULL = one GPU; else the DP / VP step over the ranks of
+ *                  the communicator (ee_comm_create above).
  * Device-detected errors: a target outside [-1, V) -> EE_ERR_VOCAB; a
  * non-finite loss -> EE_ERR_DIVERGED with the exit index (ee_get_status). */
 ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int64_t n_tokens,
                        const int32_t* targets, const float* exit_weights,
                        const ee_head_tensors* params, ee_head_tensors* grads, int32_t accumulate,
                        float* loss_out, const ee_step_aux* aux, const int64_t* valid_count,
-                       void* workspace, size_t ws_bytes, void* stream);
+                       void* workspace, size_t ws_bytes, const ee_comm* comm, void* stream);
 
 /* Data-parallel confidence weighting (EE_WEIGHT_CONFIDENCE_SUM): after the
  * caller has summed one exit's grads, its loss and weight_sum over the ranks,

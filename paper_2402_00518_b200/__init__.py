@@ -37,7 +37,7 @@ EXPORTED = ("ee_workspace_size", "ee_init_heads", "ee_tune_step", "ee_count_vali
             "ee_normalize_exit", "ee_vp_exit_forward_ag", "ee_vp_vocab_backward_rs",
             "ee_vp_exit_backward_slots", "ee_peer_barrier", "ee_ipc_get_handle", "ee_ipc_open",
             "ee_ipc_close", "ee_dp_shard_layout", "ee_tune_step_rs", "ee_adam_update_sharded",
-            "ee_tune_step_adam")
+            "ee_tune_step_adam", "ee_comm_arena_size", "ee_comm_create", "ee_comm_destroy")
 MAX_PEERS = 8
 
 
@@ -107,7 +107,11 @@ def load(path: str = LIB_PATH):
         "ee_workspace_size": (I32, [CFG, I64, ctypes.POINTER(SZ)]),
         "ee_init_heads": (I32, [CFG, I32, HT, I32, ctypes.c_uint64, F32, HT, HT, P]),
         "ee_tune_step": (I32, [CFG, ctypes.POINTER(P), I64, P, ctypes.POINTER(F32), HT, HT, I32,
-                               P, ctypes.POINTER(ee_step_aux), P, P, SZ, P]),
+                               P, ctypes.POINTER(ee_step_aux), P, P, SZ, P, P]),
+        "ee_comm_arena_size": (I32, [CFG, I32, I32, I64, ctypes.POINTER(SZ)]),
+        "ee_comm_create": (I32, [ctypes.POINTER(P), CFG, I32, I32, I32, I64, ctypes.POINTER(P),
+                                 SZ]),
+        "ee_comm_destroy": (I32, [P]),
         "ee_count_valid": (I32, [P, I64, I32, P, P, SZ, P]),
         "ee_adam_update": (I32, [CFG, HT, HT, HT, HT, HT, F32, F32, F32, F32, F32, I64, F32, P]),
         "ee_sgd_update": (I32, [CFG, HT, HT, HT, HT, F32, F32, F32, P]),
@@ -239,7 +243,9 @@ def ee_init_heads(cfg, init, copy_src, master, operand, seed=0, std=0.02, src_dt
 
 
 def ee_tune_step(cfg, hidden, targets, exit_weights, params, grads, loss_out, workspace,
-                 accumulate=False, aux=None, valid_count=None, stream=None):
+                 accumulate=False, aux=None, valid_count=None, stream=None, comm=None):
+    """One step over all exits (include/ee.h); comm (a Comm) runs the DP / VP
+    step over the communicator's ranks in the same call."""
     load()
     E = cfg.num_exits
     hid = (ctypes.c_void_p * E)(*[h.data_ptr() for h in hidden])
@@ -255,7 +261,93 @@ def ee_tune_step(cfg, hidden, targets, exit_weights, params, grads, loss_out, wo
     _check(_lib.ee_tune_step(ctypes.byref(cfg), hid, n, _ptr(targets), w, heads(params),
                              heads(grads), int(bool(accumulate)), _ptr(loss_out), ax,
                              _ptr(valid_count), _ptr(workspace), workspace.numel(),
-                             _stream(stream)))
+                             None if comm is None else comm.handle, _stream(stream)))
+
+
+COMM_MODE = {"dp": 0, "vp": 1}
+
+
+def ee_comm_arena_size(cfg, mode, world, n_local) -> int:
+    load()
+    b = ctypes.c_size_t(0)
+    _check(_lib.ee_comm_arena_size(ctypes.byref(cfg), COMM_MODE[mode], world, n_local,
+                                   ctypes.byref(b)))
+    return b.value
+
+
+class Comm:
+    """The in-library communicator of one rank (include/ee.h ee_comm_*): a
+    zero-filled symmetric arena (torch allocation), the other ranks' arenas
+    mapped into this process, and the library handle.  After construction on
+    every rank, ee_tune_step(..., comm=c) runs a whole DP / VP step.
+
+    exchange(obj) -> [obj of rank 0, ..., obj of rank world-1] is any host
+    transport (store_exchange over a TCPStore, dist.all_gather_object, ...);
+    it carries the CUDA IPC handles.  Ranks sharing one process (tests) use
+    Comm.local instead."""
+
+    def __init__(self, cfg, mode, world, rank, n_local, exchange=None, device="cuda",
+                 _arenas=None):
+        load()
+        self.mode, self.world, self.rank, self.n_local = mode, world, rank, n_local
+        self.bytes = ee_comm_arena_size(cfg, mode, world, n_local)
+        self._opened = []
+        if _arenas is None:
+            self._raw = torch.zeros(self.bytes + 256, dtype=torch.uint8, device=device)
+            self.arena = self._raw[(-self._raw.data_ptr()) % 256:][:self.bytes]
+            torch.cuda.synchronize(device)     # zero-filled before any peer can write
+            mine = ee_ipc_get_handle(self.arena) if world > 1 else None
+            allh = exchange(mine) if world > 1 else [mine]
+            ptrs = []
+            for q in range(world):
+                if q == rank:
+                    ptrs.append(self.arena.data_ptr())
+                else:
+                    p = ee_ipc_open(*allh[q])
+                    self._opened.append((p, allh[q][1]))
+                    ptrs.append(p)
+        else:
+            self.arena = _arenas[rank]
+            ptrs = [a.data_ptr() for a in _arenas]
+        arr = (ctypes.c_void_p * world)(*ptrs)
+        h = ctypes.c_void_p()
+        _check(_lib.ee_comm_create(ctypes.byref(h), ctypes.byref(cfg), COMM_MODE[mode], world,
+                                   rank, n_local, arr, self.bytes))
+        self.handle = h
+
+    @classmethod
+    def local(cls, cfgs, mode, world, n_local, device="cuda"):
+        """All ranks' comms inside one process (ranks emulated by threads /
+        streams on one GPU): cfgs[r] is rank r's config."""
+        b = ee_comm_arena_size(cfgs[0], mode, world, n_local)
+        raws = [torch.zeros(b + 256, dtype=torch.uint8, device=device) for _ in range(world)]
+        ars = [r[(-r.data_ptr()) % 256:][:b] for r in raws]
+        torch.cuda.synchronize(device)
+        out = [cls(cfgs[r], mode, world, r, n_local, _arenas=ars) for r in range(world)]
+        for c in out:
+            c._raws = raws
+        return out
+
+    def close(self):
+        if self.handle:
+            _lib.ee_comm_destroy(self.handle)
+            self.handle = None
+        for p, off in self._opened:
+            ee_ipc_close(p, off)
+        self._opened = []
+
+
+def store_exchange(store, rank: int, world: int, prefix: str):
+    """An exchange() for Comm over a torch.distributed Store (e.g. TCPStore):
+    no process group needed."""
+    import pickle
+    n = [0]
+
+    def ex(obj):
+        n[0] += 1
+        store.set(f"{prefix}/{n[0]}/{rank}", pickle.dumps(obj))
+        return [pickle.loads(store.get(f"{prefix}/{n[0]}/{q}")) for q in range(world)]
+    return ex
 
 
 def ee_exit_infer(cfg, hidden, params, threshold, argmax_out, conf_out, workspace,

@@ -8,7 +8,7 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = [os.path.join(HERE, "csrc", f) for f in ("api.cu", "gemm.cu", "kernels.cu", "backbone.cu",
-                                                   "attn_tc.cu", "skinny.cu")]
+                                                   "attn_tc.cu", "skinny.cu", "comm.cu")]
 HDR = [os.path.join(HERE, "csrc", f) for f in ("ptx.cuh", "gemm.cuh", "internal.cuh")] + [
     os.path.join(HERE, "..", "include", "ee.h")]
 OUT = os.path.join(HERE, "libee_b200.so")
@@ -35,14 +35,30 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compiles every translation unit in parallel (nvcc -c), then links."""
     if not force and up_to_date():
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT + ".tmp", *SRC]
-    if verbose:
-        print(" ".join(cmd))
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [nvcc(), *flags, "-c", "-o", obj, src]
+        if verbose:
+            print(" ".join(cmd))
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src}:\n{r.stdout}\n{r.stderr}")
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(SRC)) as ex:
+        objs = list(ex.map(compile_one, SRC))
+    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT + ".tmp", *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
-        raise RuntimeError(f"nvcc failed:\n{r.stdout}\n{r.stderr}")
+        raise RuntimeError(f"nvcc link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(OUT + ".tmp", OUT)
     return OUT
 

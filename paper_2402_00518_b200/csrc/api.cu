@@ -357,6 +357,15 @@ GemmArgs base_args(int M, int N, int K) {
 
 }  // namespace
 
+namespace ee {
+ee_status comm_fail(ee_status s, const char* msg) { return fail(s, "%s", msg); }
+ee_status comm_tune_step(const ee_comm* c, const ee_head_config* cfg, const void* const* hidden,
+                         int64_t n_tokens, const int32_t* targets, const float* exit_weights,
+                         const ee_head_tensors* params, ee_head_tensors* grads, int32_t accumulate,
+                         float* loss_out, const ee_step_aux* aux, const int64_t* valid_count,
+                         void* workspace, size_t ws_bytes, void* stream);   // comm.cu
+}  // namespace ee
+
 extern "C" {
 
 const char* ee_last_error(void) { return g_last_error.c_str(); }
@@ -1111,7 +1120,19 @@ ee_status ee_tune_step(const ee_head_config* cfg, const void* const* hidden, int
                        const int32_t* targets, const float* exit_weights,
                        const ee_head_tensors* params, ee_head_tensors* grads, int32_t accumulate,
                        float* loss_out, const ee_step_aux* aux, const int64_t* valid_count,
-                       void* workspace, size_t ws_bytes, void* stream) {
+                       void* workspace, size_t ws_bytes, const ee_comm* comm, void* stream) {
+  if (comm) {
+    ee_status s = check_cfg(cfg);
+    if (s != EE_OK) return s;
+    if ((s = check_device()) != EE_OK) return s;
+    for (int i = 0; i < cfg->num_exits; ++i) {
+      if (!params || !grads) return fail(EE_ERR_ARG, "NULL params/grads");
+      if ((s = check_arch_tensors(cfg, params[i], "params", i)) != EE_OK) return s;
+      if ((s = check_arch_tensors(cfg, grads[i], "grads", i)) != EE_OK) return s;
+    }
+    return comm_tune_step(comm, cfg, hidden, n_tokens, targets, exit_weights, params, grads,
+                          accumulate, loss_out, aux, valid_count, workspace, ws_bytes, stream);
+  }
   return tune_step_impl(cfg, hidden, n_tokens, targets, exit_weights, params, grads, nullptr,
                         accumulate, loss_out, aux, valid_count, workspace, ws_bytes, stream);
 }

@@ -3,6 +3,8 @@ symbol include/ee.h declares, and its pure host functions / argument
 validation behave (no compute calls)."""
 
 import ctypes
+
+import numpy as np
 import math
 import os
 import re
@@ -61,7 +63,7 @@ def test_null_arguments_rejected_before_any_device_work():
     lib = ee.load()
     c = ee.make_config(128, 512, 0, 1, "norm")
     r = lib.ee_tune_step(ctypes.byref(c), None, 10, None, None, None, None, 0, None, None, None,
-                         None, 0, None)
+                         None, 0, None, None)
     assert r == 1                                             # EE_ERR_ARG
     assert b"NULL" in lib.ee_last_error()
 
@@ -124,3 +126,37 @@ def test_new_entry_points_reject_bad_arguments_without_a_gpu():
                                  None) == 1                    # NULL parameter state
     assert lib.ee_vp_exit_backward_slots(ctypes.byref(c), None, 0, 0, None, None, 0, None, 0,
                                          None, None, 0, None) == 1   # n_slots = 0
+
+
+@pytest.mark.parametrize("arch", ["embedding", "norm", "mlp", "layer"])
+def test_comm_arena_size_and_create_without_a_gpu(arch):
+    """ee_comm_* host logic (include/ee.h): the arena holds the barrier
+    signals, the small reductions, two gradient arenas of the fused
+    reduce-scatter (at least one full gradient set each) and, under VP, the
+    all-gathered targets / z, the CE statistics and the dz slots; creation
+    validates its arguments and never touches the device."""
+    ee.load()
+    h, V, F = 256, 1000, 384
+    kw = dict(n_heads=2, n_kv_heads=1, seq_len=64) if arch == "layer" else {}
+    c = ee.make_config(h, V, F, 2, arch, **kw)
+    shapes = ee.tensor_shapes(h, V, F, arch, 1 if arch == "layer" else 0)
+    full = sum(int(np.prod(s)) for s in shapes.values()) * 4
+    for P in (1, 2, 3, 8):
+        b = ee.ee_comm_arena_size(c, "dp", P, 128)
+        assert b >= 2 * full
+        bv = ee.ee_comm_arena_size(ee.make_config(h, V, F, 2, arch, 1e-5, 0, 504, **kw), "vp",
+                                   P, 128)
+        n_all = 128 * P
+        assert bv >= n_all * (4 + 2 * h + 32)
+    lib = ee.lib() if hasattr(ee, "lib") else ee.load()
+    h_ = ctypes.c_void_p()
+    fake = (ctypes.c_void_p * 2)(0x100000, 0x200000)
+    b = ee.ee_comm_arena_size(c, "dp", 2, 128)
+    assert lib.ee_comm_create(ctypes.byref(h_), ctypes.byref(c), 0, 2, 0, 128, fake, b) == 0
+    assert lib.ee_comm_destroy(h_) == 0
+    assert lib.ee_comm_create(ctypes.byref(h_), ctypes.byref(c), 0, 2, 2, 128, fake, b) == 1
+    assert lib.ee_comm_create(ctypes.byref(h_), ctypes.byref(c), 0, 2, 0, 128, fake, b - 1) == 8
+    bad = (ctypes.c_void_p * 2)(0x100010, 0x200000)                  # not 256-byte aligned
+    assert lib.ee_comm_create(ctypes.byref(h_), ctypes.byref(c), 0, 2, 0, 128, bad, b) == 3
+    shard = ee.make_config(h, V, F, 2, arch, 1e-5, 0, 504, **kw)      # DP needs full W_out
+    assert lib.ee_comm_create(ctypes.byref(h_), ctypes.byref(shard), 0, 2, 0, 128, fake, b) == 1
