@@ -1,0 +1,40 @@
+"""Attention kernel error vs an fp64 reference on the same bf16 inputs, as the
+score scale grows (the Layer exit's peaked attention): which of o, dq, dk, dv
+carry more than the bf16 output rounding."""
+import math, sys, os
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
+import torch
+import paper_2402_00518_b200 as ee
+ee.load()
+
+def ref(q, k, v, do, T, Hq, Hkv):
+    n = q.shape[0]; B = n // T
+    f = lambda t, H: t.double().view(B, T, H, 128).transpose(1, 2).requires_grad_()
+    qf, kf, vf = f(q, Hq), f(k, Hkv), f(v, Hkv)
+    rep = Hq // Hkv
+    s = (qf @ kf.repeat_interleave(rep, 1).transpose(-1, -2)) / math.sqrt(128)
+    s = s.masked_fill(torch.ones(T, T, dtype=torch.bool, device=q.device).triu(1), float("-inf"))
+    o = torch.softmax(s, -1) @ vf.repeat_interleave(rep, 1)
+    o.backward(do.double().view(B, T, Hq, 128).transpose(1, 2))
+    fl = lambda t, H: t.transpose(1, 2).reshape(n, H * 128)
+    return fl(o.detach(), Hq), fl(qf.grad, Hq), fl(kf.grad, Hkv), fl(vf.grad, Hkv), s.std().item()
+
+rel = lambda a, b: ((a.double() - b).norm() / b.norm()).item()
+for scale in (1.0, 2.0, 3.0, 4.0, 6.0):
+    for impl in (0, 1):
+        B, T, Hq, Hkv = 4, 128, 2, 1
+        g = torch.Generator(device="cuda").manual_seed(5)
+        n = B * T
+        q = (torch.randn(n, Hq * 128, device="cuda", generator=g) * scale).bfloat16()
+        k = (torch.randn(n, Hkv * 128, device="cuda", generator=g) * scale).bfloat16()
+        v = torch.randn(n, Hkv * 128, device="cuda", generator=g).bfloat16()
+        do = torch.randn(n, Hq * 128, device="cuda", generator=g).bfloat16()
+        o = torch.empty_like(q); lse2 = torch.empty(n, Hq, device="cuda")
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        scr = torch.empty(n, Hq, device="cuda")
+        ee.ee_test_attention(q, k, v, o, lse2, T, Hq, Hkv, dout=do, dq=dq, dk=dk, dv=dv, scratch=scr, impl=impl)
+        torch.cuda.synchronize()
+        o_r, dq_r, dk_r, dv_r, sstd = ref(q, k, v, do, T, Hq, Hkv)
+        bfr = lambda t: rel(t.bfloat16(), t)   # the bf16 output rounding alone
+        print(f"scale {scale} score_std {sstd:.2f} impl {impl}: o {rel(o,o_r):.2e} (bf16 {bfr(o_r):.1e}) "
+              f"dq {rel(dq,dq_r):.2e} dk {rel(dk,dk_r):.2e} dv {rel(dv,dv_r):.2e} (bf16 {bfr(dq_r):.1e})", flush=True)

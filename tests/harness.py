@@ -20,6 +20,15 @@ from oracle import ee_oracle as O
 
 LOSS_RTOL = 1e-3
 GRAD_RTOL = 2e-2
+# Layer exits (NEXT #2) only: the pre-attention gain's gradient sits at the
+# error floor of bf16 GEMM operands -- the fp64 emulation with nothing but the
+# kernel's bf16 roundings reaches 1.5-3.0e-2 on it (A27,
+# tests/test_bf16_floor.py) -- so its bound is 5e-2 (every other tensor 2e-2).
+LAYER_GAIN_RTOL = 5e-2
+
+
+def grad_rtol(arch, k):
+    return LAYER_GAIN_RTOL if (arch == "layer" and k == "g_att") else GRAD_RTOL
 TENSORS = ("g_a", "w_gate", "w_up", "w_down", "g_f", "w_out", "g_att", "w_q", "w_k", "w_v", "w_o")
 
 
@@ -97,7 +106,7 @@ def compare_exit(arch, res, loss_gpu, grads_gpu, aux_gpu, targets, tag=""):
     for k, g in res.grads.items():
         e = rel_fro(grads_gpu[k].double().cpu().numpy(), g)
         out[f"grad_{k}"] = e
-        assert e <= GRAD_RTOL, (tag, k, e)
+        assert e <= grad_rtol(arch, k), (tag, k, e)
     t = targets.cpu().numpy()
     valid = t != -1
     lse = aux_gpu["lse"].double().cpu().numpy()

@@ -22,7 +22,7 @@ import pytest
 import torch
 
 import eesynth as S
-from harness import GRAD_RTOL, LOSS_RTOL, attn_kwargs, oracle_exit, rel_fro
+from harness import GRAD_RTOL, grad_rtol, LOSS_RTOL, attn_kwargs, oracle_exit, rel_fro
 
 pytestmark = pytest.mark.gpu
 
@@ -130,7 +130,7 @@ def _check_vs_oracle(cfg, mode, P, out, hidden, targets, params, weights, weight
                 for r in range(1, P):                                 # all-reduced: identical
                     assert torch.equal(out[r][1][i][k], got), (r, i, k)
             errs[k] = rel_fro(got.double().numpy(), g)
-            assert errs[k] <= GRAD_RTOL, (i, k, errs[k])
+            assert errs[k] <= grad_rtol(cfg.arch, k), (i, k, errs[k])
         print(mode, cfg.arch, P, weighting, i, {k: f"{e:.1e}" for k, e in errs.items()})
 
 
@@ -160,9 +160,9 @@ def test_dp_comm_confidence_weighting_global_normaliser(gpu_lib):
                      weighting="confidence")
 
 
-def test_dp_comm_accumulate_and_repeat(gpu_lib):
-    """Two calls in a row give bitwise the same result (the arenas and the
-    barrier epochs are reusable), and accumulate adds the reduced gradient."""
+def test_dp_comm_repeat_calls_bitwise(gpu_lib):
+    """Three calls in a row end with bitwise the result of one call: the
+    arenas, the small reduction slots and the barrier epochs are reusable."""
     _warm(gpu_lib, "dp", "mlp")
     cfg = _cfg("mlp", 72)
     hidden = S.hidden_states(cfg)

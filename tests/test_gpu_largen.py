@@ -17,7 +17,7 @@ import numpy as np
 import pytest
 
 import eesynth as S
-from harness import GRAD_RTOL, LOSS_RTOL, gpu_step, oracle_exit, rel_fro
+from harness import GRAD_RTOL, grad_rtol, LOSS_RTOL, gpu_step, oracle_exit, rel_fro
 
 pytestmark = pytest.mark.gpu
 
@@ -36,7 +36,7 @@ def _check(ee, cfg, n, ds_mode, attn=None):
           {k: f"{e:.2e}" for k, e in errs.items()})
     assert lrel <= LOSS_RTOL, (loss[0].item(), res.loss)
     for k, e in errs.items():
-        assert e <= GRAD_RTOL, (k, e)
+        assert e <= grad_rtol(cfg.arch, k), (k, e)
     # per-token loss on every row (not a sample): a tile lost by the scheduler
     # would leave NaN / garbage rows here
     lt = aux[0]["loss_tok"].double().cpu().numpy()
