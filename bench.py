@@ -371,6 +371,163 @@ def bench_backbone(ee, torch, cfg, args, dev):
             "attention_share": att / ms}
 
 
+def run_pipeline(args, cfg, world, rank, local, torch, dist, ee, S):
+    """--parallel pp: one EE-Tuning iteration of the paper's customised
+    pipeline schedule "with forward communication only" (Fig. 3)
+    including the frozen backbone's partial forward: the backbone's
+    layers 1..max(exit layer) are split into `world` contiguous stages; per
+    microbatch, stage s receives the activation from s-1, runs its layers
+    (ee_backbone_forward, keeping the hidden states at its exits), sends the
+    result to s+1 and then runs forward, loss and backward of its own exits
+    (ee_tune_step, gradients accumulated over the microbatches, global valid
+    count); Adam on its exits after the last microbatch.  Nothing is sent
+    backward and no backbone activation is kept.  Synthetic backbone weights
+    (N(0, 0.02^2), Llama-2 shapes), random exit init.  value = global tokens
+    per second of the whole iteration (backbone + exits)."""
+    from paper_2402_00518_b200.parallel import pipeline_forward_only_step
+    ndev = torch.cuda.device_count()
+    shared_gpu = world > ndev
+    torch.cuda.set_device(local % ndev)
+    dev = torch.device("cuda", local % ndev)
+    multi = world > 1
+    if multi:
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    h, F, T = cfg.hidden, cfg.ffn, 2048
+    nh, nkv = LLAMA2[h]
+    Ltot = max(cfg.after)
+    per = -(-Ltot // world)
+    lb, le = min(Ltot, rank * per), min(Ltot, (rank + 1) * per)
+    mine = [i for i, a in enumerate(cfg.after) if lb < a <= le]
+    N = cfg.tokens
+    if N % (args.micro * T):
+        raise SystemExit(f"{N} tokens do not split into {args.micro} microbatches of whole "
+                         f"{T}-token sequences")
+    mb = N // args.micro
+    g = torch.Generator(device=dev).manual_seed(1000 + rank)
+
+    def r(*shape):
+        return (torch.randn(*shape, generator=g, device=dev) * 0.02).to(torch.bfloat16)
+    layers = [{"g_att": 1 + 0.1 * torch.randn(h, generator=g, device=dev),
+               "w_q": r(h, h), "w_k": r(128 * nkv, h), "w_v": r(128 * nkv, h), "w_o": r(h, h),
+               "g_mlp": 1 + 0.1 * torch.randn(h, generator=g, device=dev),
+               "w_gate": r(F, h), "w_up": r(F, h), "w_down": r(h, F)} for _ in range(le - lb)]
+    bc = ee.make_backbone_config(h, nh, nkv, F, T)
+    wsb = torch.zeros(ee.ee_backbone_workspace_size(bc, mb), dtype=torch.uint8, device=dev)
+    heads = None
+    if mine:
+        heads = ee.ExitHeads(ee.HeadSpec(h, cfg.vocab, F, len(mine), cfg.arch,
+                                         ds_mode=args.ds_mode), mb, device=dev)
+        heads.init("random", seed=7 + rank)
+    x0 = S.hidden_states(S.Cfg(name=cfg.name, hidden=h, vocab=cfg.vocab, ffn=F, arch=cfg.arch,
+                               tokens=N, layers=1, after=[1], init="random", seed=cfg.seed),
+                         N, seed=cfg.seed, device=dev)[0] if rank == 0 else None
+    targets = S.targets(cfg, N, seed=cfg.seed, device=dev)
+    W = torch.zeros(1, dtype=torch.int64, device=dev)
+    ee.ee_count_valid(targets, cfg.vocab, W, wsb)           # every stage sees every target
+    outs_idx = sorted({cfg.after[i] - lb for i in mine} | {le - lb})
+    bufs = {j: torch.empty(mb, h, dtype=torch.bfloat16, device=dev) for j in outs_idx}
+    recv_buf = torch.empty(mb, h, dtype=torch.bfloat16, device=dev)
+    total_iters = 40000
+
+    def send(m, t):
+        if shared_gpu:
+            return dist.isend(t.cpu(), dst=rank + 1)
+        return dist.isend(t, dst=rank + 1)
+
+    def recv(m):
+        if shared_gpu:
+            c = torch.empty(mb, h, dtype=torch.bfloat16)
+            dist.recv(c, src=rank - 1)
+            recv_buf.copy_(c)
+        else:
+            dist.recv(recv_buf, src=rank - 1)
+        return recv_buf
+
+    def fwd(m, x_in):
+        x = x0[m * mb:(m + 1) * mb] if x_in is None else x_in
+        ee.ee_backbone_forward(bc, layers, x, outs_idx, [bufs[j] for j in outs_idx], wsb)
+        return bufs[le - lb]
+
+    def exits(m):
+        if heads is None:
+            return
+        heads.step([bufs[cfg.after[i] - lb] for i in mine], targets[m * mb:(m + 1) * mb],
+                   accumulate=m > 0, valid_count=W)
+
+    def step(it):
+        pipeline_forward_only_step(rank, world, args.micro, fwd, exits,
+                                   send if rank + 1 < world else None,
+                                   recv if rank > 0 else None,
+                                   (lambda: heads.adam(ee.ee_lr_at(min(it + 1, total_iters),
+                                                                   total_iters)))
+                                   if heads is not None else None)
+
+    def sync():
+        torch.cuda.synchronize()
+        if multi:
+            dist.barrier()
+
+    sync()
+    for it in range(args.warmup):
+        step(it)
+    sync()
+    sampler = ClockSampler(local % ndev)
+    sampler.start()
+    time.sleep(0.3)
+    l0 = ee.ee_launch_count()
+    ee.ee_profile_start()
+    sync()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for it in range(args.steps):
+        step(args.warmup + it)
+    e1.record()
+    sync()
+    prof = ee.ee_profile_stop()
+    launches = ee.ee_launch_count() - l0
+    clocks = sampler.stop()
+    t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+    if multi:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.item()
+    fl = torch.tensor([sum(p[3] for p in prof) / args.steps], dtype=torch.float64, device=dev)
+    bb = torch.tensor([sum(p[1] for p in prof if p[0].startswith("bb_")) / args.steps],
+                      dtype=torch.float64, device=dev)
+    if multi:
+        dist.all_reduce(fl)
+    status = heads.status() if heads is not None else (0, -1)
+    if rank == 0:
+        peaks = load_peaks()
+        tf = fl.item() / (ms / 1e3) / 1e12 / world
+        line = {"metric": METRIC, "value": N / (ms / 1e3), "unit": "tokens/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "bf16", "data": "synthetic (seeded backbone weights and inputs)",
+                "config": {"workload": f"{cfg.name}: frozen backbone layers 1..{Ltot} (h {h}, "
+                                       f"heads {nh}/{nkv} kv, F {F}) + {cfg.exits} {cfg.arch} "
+                                       f"exits at layers {cfg.after}, {N} tokens per step "
+                                       f"({args.micro} microbatches of {mb})",
+                           "global_batch": N // T, "seq_len": T,
+                           "parallelism": f"pp{world} (forward-communication-only schedule, "
+                                          "P:294-303)",
+                           "stage_layers": f"{per} layers per stage",
+                           "ds": DS_LABEL[args.ds_mode],
+                           "l2": "inputs larger than L2",
+                           "optimizer": "Adam on each stage's exits after the last microbatch"},
+                "pct_peak": {"algorithmic_tflops_per_gpu": tf,
+                             "of_burst": tf / peaks["bf16_tflops"],
+                             "step_flops_alg": fl.item()},
+                "backbone_ms_rank0": bb.item(),
+                "gpu_launches": launches, "clocks": clocks, "status": status}
+        print(json.dumps(line), flush=True)
+    if multi:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def free_port():
     import socket
     with socket.socket() as so:
@@ -449,9 +606,13 @@ def main():
     ap.add_argument("--vp-comm", default="fused", choices=["fused", "nccl"],
                     help="vp: fused = z all-gather / dz reduce-scatter inside the a4 / a8 "
                          "kernels over CUDA-IPC peer memory; nccl = NCCL collectives")
-    ap.add_argument("--parallel", default="dp", choices=["dp", "vp"],
+    ap.add_argument("--parallel", default="dp", choices=["dp", "vp", "pp"],
                     help="dp = data parallel over tokens; vp = W_out vocab-parallel with the "
-                         "distributed softmax-CE (configs[3]: --config 70b --parallel vp)")
+                         "distributed softmax-CE (configs[3]: --config 70b --parallel vp); pp = "
+                         "the paper's forward-communication-only pipeline with the frozen "
+                         "backbone's partial forward (P:294-303, P:260; e.g. --config 13b_q)")
+    ap.add_argument("--micro", type=int, default=8,
+                    help="pp: microbatches per step (whole 2048-token sequences each)")
     args = ap.parse_args()
     launch_ranks(args)
 
@@ -473,6 +634,9 @@ def main():
 
     import paper_2402_00518_b200 as ee
     ee.load()
+    if args.parallel == "pp":
+        run_pipeline(args, cfg, world, rank, local, torch, dist, ee, S)
+        return
     ndev = torch.cuda.device_count()
     shared_gpu = world > ndev            # test mode: several ranks on one GPU (gloo)
     args.shared_gpu = shared_gpu

@@ -34,6 +34,13 @@ CONFIGS = {
     # whole sequences (causal attention within each).
     "tiny_layer": dict(hidden=256, vocab=1000, ffn=384, arch="layer", tokens=2 * 128, layers=2,
                        after=[1, 2], init="copy", seed=5, n_heads=2, n_kv_heads=1, seq_len=128),
+    # the paper's end-to-end 13B conversion: ONE MLP exit
+    # at 1/4 depth, batch 16 x 2048 -- the --parallel pp bench runs the frozen
+    # backbone's partial forward (layers 1..10) and the exit's tuning
+    "13b_q": dict(hidden=5120, vocab=32000, ffn=13824, arch="mlp", tokens=16 * 2048,
+                  layers=40, after=[10], init="random", seed=7),
+    "70b_q": dict(hidden=8192, vocab=32000, ffn=28672, arch="mlp", tokens=16 * 2048,
+                  layers=80, after=[20], init="random", seed=8),
     # the paper's architecture comparison: 13B with 8 exits at 1/8 .. 8/8 depth
     # (P:465), batch 16 x 2048
     "13b_layer": dict(hidden=5120, vocab=32000, ffn=13824, arch="layer", tokens=16 * 2048,

@@ -5,13 +5,20 @@ right after (gradients accumulated over microbatches, global valid count);
 the activation crosses the stage boundary in bf16 through a channel (the
 NCCL/gloo transport itself is tests/test_pp_gloo.py).  Equals the
 single-process run (full backbone, all exits, full batch) within the
-north_star tolerances."""
+north_star tolerances, and is anchored to the fp64 oracle: the hidden states
+each stage hands its exit match oracle.backbone_forward (the partial forward of
+P:260; test_gpu_backbone's bound), and each stage's accumulated loss and
+gradients match oracle.exit_loss_and_grads on exactly those hidden states over
+the full batch with the global valid count (north_star bounds)."""
 
+import numpy as np
 import pytest
 import torch
 
 import eesynth as S
-from harness import rel_fro
+from eesynth import to_f64
+from harness import GRAD_RTOL, LOSS_RTOL, oracle_exit, rel_fro
+from oracle import ee_oracle as O
 from test_gpu_backbone import _layers
 
 pytestmark = pytest.mark.gpu
@@ -48,6 +55,7 @@ def test_pipeline_forward_only_two_stages(gpu_lib):
     # ---- pipeline: stage s owns layers [2s+1, 2s+2] and the exit after layer 2s+2
     channel = []
     stage_loss, stage_grads = [], []
+    captured = [[], []]
     for stage in range(2):
         heads = ee.ExitHeads(ee.HeadSpec(h, V, F, 1, "mlp"), mb, adam=False)
         for k, v in params[stage].items():
@@ -64,6 +72,7 @@ def test_pipeline_forward_only_two_stages(gpu_lib):
             y = torch.empty(mb, h, dtype=torch.bfloat16, device="cuda")
             ee.ee_backbone_forward(bcfg, my_layers, x, [2], [y], wsb)
             out[m] = y                                  # this stage's exit sits after its last layer
+            captured[stage].append(y.clone())
             return y
 
         def exits(m):
@@ -84,3 +93,16 @@ def test_pipeline_forward_only_two_stages(gpu_lib):
         for k in stage_grads[i]:
             assert rel_fro(stage_grads[i][k].double().cpu().numpy(),
                            ref.grads[i][k].double().cpu().numpy()) <= 2e-2, (i, k)
+
+    # ---- oracle anchor: the partial forward and each stage's exit
+    l64 = [{k: to_f64(v.cpu()) for k, v in L.items()} for L in layers]
+    want_h = O.backbone_forward(l64, to_f64(x0.cpu()), T, nh, nkv, [2, 4], 1e-5)
+    tg = targets.cpu()
+    for s_ in range(2):
+        got_h = torch.cat(captured[s_]).cpu()
+        assert rel_fro(to_f64(got_h), want_h[s_]) <= 2e-2, s_
+        res = oracle_exit("mlp", params[s_], got_h, tg, 1.0)
+        assert abs(stage_loss[s_] - res.loss) <= LOSS_RTOL * res.loss, (s_, stage_loss[s_], res.loss)
+        for k, g in res.grads.items():
+            e = rel_fro(stage_grads[s_][k].double().cpu().numpy(), g)
+            assert e <= GRAD_RTOL, (s_, k, e)
