@@ -19,8 +19,8 @@ import subprocess
 import sys
 from collections import OrderedDict
 
-# order of gemm_kernel launches within one MLP exit (api.cu)
-MLP_GEMM_ORDER = ["a2_gateup_swiglu", "a3_down_resid", "a5_vocab_ce_stats",
+# order of gemm_kernel launches within one MLP exit (api.cu; ds_mode recompute)
+MLP_GEMM_ORDER = ["a2_gateup_swiglu", "a3_down_resid", "a5_vocab_ce_stats", "a7_ds_recompute",
                   "a8_dz", "a9_dw_out", "a11_dm_swiglu_bwd", "a11_dw_down", "a12_du",
                   "a12_dw_gateup"]
 
