@@ -1,12 +1,13 @@
 """One rank of the fused data-parallel step (ShardedDPHeads, ZeRO-1) at P ranks
-on one GPU (compute only): the rank's own 65 536 tokens (weak scaling), the
+on one GPU (compute only): the rank's own tokens (--strong: the config's
+global tokens / P, the bench default; else all of them: weak scaling), the
 gradient rows scattered by the weight-gradient epilogues (every peer pointer
 aliases this rank's own arena, so the stores land locally instead of over
 NVLink), the sharded Adam over 1/P of the parameters with its operand stores
 (P copies into the same local tensors).  Barriers and the two small
 all-reduces are no-ops.  Measures the per-rank kernels, not NVLink.
 
-  python scripts/dp_emulate.py [--config 70b] [--ranks 8]
+  python scripts/dp_emulate.py [--config 70b_dp] [--ranks 8] [--strong]
 """
 import argparse
 import json
@@ -29,10 +30,12 @@ def main():
     ap.add_argument("--ranks", type=int, default=8)
     ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--strong", action="store_true")
     a = ap.parse_args()
     ee.load()
     cfg = S.get_cfg(a.config)
-    P, N, E = a.ranks, cfg.tokens, cfg.exits
+    P, E = a.ranks, cfg.exits
+    N = cfg.tokens // P if a.strong else cfg.tokens
     dev = torch.device("cuda")
     heads = ShardedDPHeads(ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch), N, 0, P,
                            device=dev)
@@ -59,6 +62,7 @@ def main():
     print(json.dumps({
         "what": f"rank 0 of {P}: fused DP (ZeRO-1) step, compute only (see docstring)",
         "config": a.config, "ranks": P, "tokens_per_rank": N, "ms_per_step_rank0": ms,
+        "scaling": "strong" if a.strong else "weak",
         "projected_job_tokens_per_s_if_comm_hidden": P * N / (ms / 1e3),
         "status": heads.status(),
         "kernels_ms_per_step": {k: round(v / a.steps, 3)

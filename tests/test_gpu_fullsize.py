@@ -170,3 +170,46 @@ def test_full_size_layer_exit_one_sequence_vs_oracle(gpu_lib):
     assert torch.equal(loss, loss2)
     for k in grads[0]:
         assert torch.equal(grads[0][k], grads2[0][k]), k
+
+
+@pytest.mark.parametrize("name", ["70b", "13b"])
+def test_full_size_long_k_equals_sum_of_short_k_shards(gpu_lib, name):
+    """P10 (linearity over tokens, P:183-188 + A16) at the bench's full size:
+    the step on all N tokens -- weight-gradient GEMMs with K = N >= 16384 on
+    the static wave-barrier schedule over thousands of pair tiles -- equals
+    the sum of the steps on N/8-token shards (K = 8192: the dynamic tile
+    schedule, a different code path) accumulated with the global valid count,
+    to fp32 summation-order tolerance on every gradient tensor.  The shard
+    path is itself pinned to the oracle (test_gpu_parity, test_gpu_largen)."""
+    ee = gpu_lib
+    cfg = _one_exit(name)
+    n = cfg.tokens
+    hidden = [h.contiguous() for h in S.hidden_states(cfg, n, device="cuda")]
+    targets = S.targets(cfg, n, device="cuda")
+    params = S.head_params(cfg, device="cuda")
+    c = ee.make_config(cfg.hidden, cfg.vocab, cfg.ffn, 1, cfg.arch)
+    ops = [{k: (v.float().contiguous() if k.startswith("g_") else v.to(torch.bfloat16).contiguous())
+            for k, v in params[0].items()}]
+    del params
+    ws = torch.zeros(ee.ee_workspace_size(c, n), dtype=torch.uint8, device="cuda")
+    full = [{k: torch.empty(v.shape, device="cuda") for k, v in ops[0].items()}]
+    loss_full = torch.zeros(1, device="cuda")
+    ee.ee_tune_step(c, hidden, targets, [1.0], ops, full, loss_full, ws)
+    W = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ee.ee_count_valid(targets, cfg.vocab, W, ws)
+    shard = [{k: torch.empty(v.shape, device="cuda") for k, v in ops[0].items()}]
+    loss_sum, loss_s = 0.0, torch.zeros(1, device="cuda")
+    m = n // 8
+    for s in range(8):
+        ee.ee_tune_step(c, [hidden[0][s * m:(s + 1) * m]], targets[s * m:(s + 1) * m], [1.0], ops,
+                        shard, loss_s, ws, accumulate=s > 0, valid_count=W)
+        loss_sum += loss_s.item()
+    torch.cuda.synchronize()
+    assert ee.ee_get_status(ws) == (0, -1)
+    assert abs(loss_full.item() - loss_sum) <= 1e-5 * loss_full.item()
+    errs = {}
+    for k in full[0]:
+        a, b = full[0][k].double(), shard[0][k].double()
+        errs[k] = ((a - b).norm() / b.norm()).item()
+        assert errs[k] <= 1e-4, (k, errs[k])
+    print(name, {k: f"{e:.1e}" for k, e in errs.items()})
