@@ -319,3 +319,35 @@ def test_fused_dp_confidence_weighting_bitwise(gpu_lib):
         for i in range(E):
             for k, t in ref[0][i].items():
                 assert torch.equal(got[0][i][k], t), (r, i, k)
+
+
+def test_sharded_step_host_equals_device_step(gpu_lib):
+    """ShardedDPHeads.step_host (the bench's e2e API at every N: per-exit H2D
+    on a copy stream, HostStager) gives bitwise the device step's losses and
+    parameters, on alternating input sets issued back to back."""
+    from paper_2402_00518_b200.parallel import ShardedDPHeads
+    ee = gpu_lib
+    cfg = _cfg("mlp", 31)
+    spec = ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, cfg.exits, cfg.arch)
+    params = S.head_params(cfg)
+    sets = [(S.hidden_states(cfg, 256, seed=s), S.targets(cfg, 256, seed=s)) for s in (1, 2)]
+    runs = []
+    for host in (False, True):
+        hd = ShardedDPHeads(spec, 256, 0, 1)
+        hd.connect_local([hd])
+        hd.init("copy", copy_src=_copy_src(params), src_dtype=torch.float32)
+        losses = []
+        for it in range(6):
+            hs, t = sets[it % 2]
+            if host:
+                hd.step_host([h.pin_memory() for h in hs], t.pin_memory(), 1e-3)
+            else:
+                hd.step([h.cuda() for h in hs], t.cuda(), 1e-3)
+            losses.append(hd.loss.clone())
+        torch.cuda.synchronize()
+        runs.append((losses, [{k: v.clone() for k, v in d.items()} for d in hd.operand]))
+    for a, b in zip(runs[0][0], runs[1][0]):
+        assert torch.equal(a, b)
+    for i in range(cfg.exits):
+        for k in runs[0][1][i]:
+            assert torch.equal(runs[0][1][i][k], runs[1][1][i][k]), (i, k)
