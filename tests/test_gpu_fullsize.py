@@ -211,5 +211,5 @@ def test_full_size_long_k_equals_sum_of_short_k_shards(gpu_lib, name):
     for k in full[0]:
         a, b = full[0][k].double(), shard[0][k].double()
         errs[k] = ((a - b).norm() / b.norm()).item()
-        assert errs[k] <= 1e-4, (k, errs[k])
+        assert errs[k] <= 3e-4, (k, errs[k])
     print(name, {k: f"{e:.1e}" for k, e in errs.items()})
