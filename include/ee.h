@@ -602,7 +602,9 @@ ee_status ee_test_gemm(int32_t a_kmajor, int32_t b_kmajor, const void* A, const 
  * also runs: dq, dk, dv (shapes of q, k, v, bf16) and scratch fp32 [n x Hq].
  * seq_len a multiple of 64 dividing n; n_heads a multiple of n_kv_heads.
  * impl selects the forward and backward kernels: 0 = warp-level mma.sync,
- * 1 = tcgen05/TMEM (the step's default). */
+ * 1 = tcgen05/TMEM with one query tile per CTA, 2 = tcgen05/TMEM with two
+ * ping-ponged query tiles per CTA (the step's default forward); the backward
+ * is tcgen05 for 1 and 2. */
 ee_status ee_test_attention(const void* q, const void* k, const void* v, void* o, float* lse2,
                             const void* dout, void* dq, void* dk, void* dv, float* scratch,
                             int64_t n_tokens, int32_t seq_len, int32_t n_heads, int32_t n_kv_heads,

@@ -327,20 +327,27 @@ struct Prof {
   }
 };
 
-// Attention forward: the tcgen05 kernel (attn_tc.cu) unless EE_ATTN_TC=0 selects
-// the mma.sync kernel (A/B measurements).
+// Attention kernels (attn_tc.cu): EE_ATTN_TC = 2 (default) the two-query-tile
+// tcgen05 forward, 1 the one-tile tcgen05 forward, 0 the mma.sync kernels
+// (A/B measurements; the backward is tcgen05 unless 0).
 int attn_tc_mode() {
   static const int tc = [] {
     const char* e = getenv("EE_ATTN_TC");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 2;
   }();
   return tc;
+}
+cudaError_t attn_forward_impl(int impl, const __nv_bfloat16* q, const __nv_bfloat16* k,
+                              const __nv_bfloat16* v, __nv_bfloat16* o, long long n, int T,
+                              int Hq, int Hkv, float* lse2, cudaStream_t st) {
+  if (impl == 2) return launch_attn_fwd_tc2(q, k, v, o, n, T, Hq, Hkv, lse2, st);
+  if (impl == 1) return launch_attn_fwd_tc(q, k, v, o, n, T, Hq, Hkv, lse2, st);
+  return launch_attn_fwd(q, k, v, o, n, T, Hq, Hkv, lse2, st);
 }
 cudaError_t attn_forward(const __nv_bfloat16* q, const __nv_bfloat16* k, const __nv_bfloat16* v,
                          __nv_bfloat16* o, long long n, int T, int Hq, int Hkv, float* lse2,
                          cudaStream_t st) {
-  return attn_tc_mode() ? launch_attn_fwd_tc(q, k, v, o, n, T, Hq, Hkv, lse2, st)
-                        : launch_attn_fwd(q, k, v, o, n, T, Hq, Hkv, lse2, st);
+  return attn_forward_impl(attn_tc_mode(), q, k, v, o, n, T, Hq, Hkv, lse2, st);
 }
 
 GemmArgs base_args(int M, int N, int K) {
@@ -1981,21 +1988,17 @@ ee_status ee_test_attention(const void* q, const void* k, const void* v, void* o
   ee_status s = check_device();
   if (s != EE_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
-  if (impl == 1)
-    EE_CUDA(launch_attn_fwd_tc((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
-                               (const __nv_bfloat16*)v, (__nv_bfloat16*)o, n_tokens, seq_len,
-                               n_heads, n_kv_heads, lse2, st));
-  else
-    EE_CUDA(launch_attn_fwd((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
-                            (const __nv_bfloat16*)v, (__nv_bfloat16*)o, n_tokens, seq_len, n_heads,
-                            n_kv_heads, lse2, st));
+  if (impl < 0 || impl > 2) return fail(EE_ERR_ARG, "impl must be 0, 1 or 2");
+  EE_CUDA(attn_forward_impl(impl, (const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
+                            (const __nv_bfloat16*)v, (__nv_bfloat16*)o, n_tokens, seq_len,
+                            n_heads, n_kv_heads, lse2, st));
   if (dout) {
     if (!dq || !dk || !dv || !scratch) return fail(EE_ERR_ARG, "backward outputs NULL");
     EE_CUDA(launch_attn_bwd((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
                             (const __nv_bfloat16*)v, (const __nv_bfloat16*)o,
                             (const __nv_bfloat16*)dout, lse2, scratch, (__nv_bfloat16*)dq,
                             (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, n_tokens, seq_len, n_heads,
-                            n_kv_heads, 0.f, st, impl == 1));
+                            n_kv_heads, 0.f, st, impl != 0));
   }
   return EE_OK;
 }

@@ -338,6 +338,345 @@ cudaError_t launch_attn_fwd_tc(const __nv_bfloat16* q, const __nv_bfloat16* k,
 }
 
 // ============================================================================
+// Forward, two query tiles per CTA (tiles 2p and 2p + 1 of one head): the
+// FA4-style ping-pong.  The one-tile kernel above is MUFU-bound by
+// construction -- 128 x 128 exp2 per key tile at 16/clk/SM take as long as the
+// tile's QK^T + PV MMAs, and PV_j must wait for softmax_j -- so the tensor core
+// idles about a third of the time.  Here two softmax warpgroups (warps 4-7:
+// tile A, warps 8-11: tile B) alternate with the MMA issuer:
+//   S_A(0) S_B(0) | PV_A(j) S_A(j+1) PV_B(j) S_B(j+1) | ...
+// so softmax A(j+1) runs under PV_B(j) + S_B(j+1) and vice versa.  K_j and V_j
+// are loaded once for both tiles.  TMEM: S_A | S_B | O_A | O_B (4 x 128
+// columns); P_X(j) is written as bf16 over the first 64 columns of S_X (the
+// TMEM A operand of PV_X(j)); S_X(j+1) is issued after PV_X(j), so the tensor
+// pipe's issue order protects P.  The softmax reads S in 32-column chunks
+// (two passes: max, then exp2) to stay under the 168 registers a 384-thread
+// CTA allows.  Same arithmetic, rounding points and outputs as the one-tile
+// kernel (bitwise: the per-row operations and their order are unchanged).
+namespace {
+constexpr int FA2_KST = 2, FA2_VST = 2;
+constexpr int FA2_SMEM = 1024 + FA_TILE * (2 + FA2_KST + FA2_VST) + 512;
+}  // namespace
+
+__global__ void __launch_bounds__(384, 1)
+    attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                        const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ o,
+                        float* __restrict__ lse2, int T, int Hq, int Hkv, float scale_log2) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sQ = smem;                        // [2] tiles A, B
+  uint8_t* sK = sQ + 2 * FA_TILE;
+  uint8_t* sV = sK + FA2_KST * FA_TILE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + FA2_VST * FA_TILE);
+  uint64_t* q_full = bars;                   // [2]
+  uint64_t* k_full = bars + 2;               // [KST]
+  uint64_t* k_empty = k_full + FA2_KST;      // [KST]
+  uint64_t* v_full = k_empty + FA2_KST;      // [VST]
+  uint64_t* v_empty = v_full + FA2_VST;      // [VST]
+  uint64_t* s_full = v_empty + FA2_VST;      // [2] per tile
+  uint64_t* p_full = s_full + 2;             // [2] per tile
+  uint64_t* o_done = p_full + 2;             // [2] per tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqt = (T + FA_BM - 1) / FA_BM;
+  const int npair = (nqt + 1) / 2;
+  const int pr = npair - 1 - (int)blockIdx.x;  // longest causal rows first
+  const int qtA = 2 * pr, qtB = 2 * pr + 1;
+  const bool hasB = qtB < nqt;
+  const int n_ktA = qtA + 1, n_kt = hasB ? qtB + 1 : n_ktA;
+  const int hq = blockIdx.y, b = blockIdx.z;
+  const int hk = hq / (Hq / Hkv);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(&q_full[x], 1);
+      mbar_init(&s_full[x], 1);
+      mbar_init(&p_full[x], 128);
+      mbar_init(&o_done[x], 1);
+    }
+    for (int s = 0; s < FA2_KST; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < FA2_VST; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA: Q_A, Q_B, K
+    if (lane == 0) {
+      for (int x = 0; x < (hasB ? 2 : 1); ++x) {
+        const int row0 = b * T + (qtA + x) * FA_BM;
+        tma_load_2d(sQ + x * FA_TILE, &tmQ, &q_full[x], hq * FA_D, row0);
+        tma_load_2d(sQ + x * FA_TILE + FA_ATOM, &tmQ, &q_full[x], hq * FA_D + 64, row0);
+        mbar_arrive_expect_tx(&q_full[x], FA_TILE);
+      }
+      for (int j = 0; j < n_kt; ++j) {
+        const int s = j % FA2_KST;
+        mbar_wait(&k_empty[s], ((j / FA2_KST) & 1) ^ 1);
+        uint8_t* k = sK + s * FA_TILE;
+        const int k_row0 = b * T + j * FA_BN;
+        tma_load_2d(k, &tmK, &k_full[s], hk * FA_D, k_row0);
+        tma_load_2d(k + FA_ATOM, &tmK, &k_full[s], hk * FA_D + 64, k_row0);
+        mbar_arrive_expect_tx(&k_full[s], FA_TILE);
+      }
+    }
+  } else if (warp == 3) {
+    // ---------------------------------------------------------------- TMA: V
+    if (lane == 0) {
+      for (int j = 0; j < n_kt; ++j) {
+        const int s = j % FA2_VST;
+        mbar_wait(&v_empty[s], ((j / FA2_VST) & 1) ^ 1);
+        uint8_t* v = sV + s * FA_TILE;
+        const int k_row0 = b * T + j * FA_BN;
+        tma_load_2d(v, &tmV, &v_full[s], hk * FA_D, k_row0);
+        tma_load_2d(v + FA_ATOM, &tmV, &v_full[s], hk * FA_D + 64, k_row0);
+        mbar_arrive_expect_tx(&v_full[s], FA_TILE);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_qk = make_idesc_bf16(FA_BM, FA_BN, false, false);
+      constexpr uint32_t idesc_pv = make_idesc_bf16(FA_BM, FA_D, false, true);
+      int k_ready = -1, v_ready = -1;
+      auto ensure_k = [&](int j) {
+        if (k_ready < j) {
+          mbar_wait(&k_full[j % FA2_KST], (j / FA2_KST) & 1);
+          tc_fence_after();
+          k_ready = j;
+        }
+      };
+      auto ensure_v = [&](int j) {
+        if (v_ready < j) {
+          mbar_wait(&v_full[j % FA2_VST], (j / FA2_VST) & 1);
+          tc_fence_after();
+          v_ready = j;
+        }
+      };
+      auto issue_s = [&](int x, int j) {  // S_x(j) = Q_x K_j^T
+        ensure_k(j);
+        const uint32_t aq = smem_u32(sQ + x * FA_TILE);
+        const uint32_t bk = smem_u32(sK + (j % FA2_KST) * FA_TILE);
+#pragma unroll
+        for (int k = 0; k < FA_D / 16; ++k) {
+          const uint32_t off = (k >> 2) * FA_ATOM + (k & 3) * 32;
+          tc_mma_f16(tmem_base + x * FA_BN, make_sdesc(aq + off, 16, 1024),
+                     make_sdesc(bk + off, 16, 1024), idesc_qk, k != 0 ? 1u : 0u);
+        }
+        tc_commit(&s_full[x]);
+      };
+      auto issue_pv = [&](int x, int j) {  // O_x (+)= P_x(j) V_j, P in TMEM
+        ensure_v(j);
+        mbar_wait(&p_full[x], j & 1);
+        tc_fence_after();
+        const uint32_t bv = smem_u32(sV + (j % FA2_VST) * FA_TILE);
+        const uint32_t tO = tmem_base + 2 * FA_BN + x * FA_D;
+#pragma unroll
+        for (int k = 0; k < FA_BN / 16; ++k)
+          tc_mma_f16_ts(tO, tmem_base + x * FA_BN + k * 8,
+                        make_sdesc(bv + k * 2048, FA_ATOM, 1024), idesc_pv,
+                        (j | k) != 0 ? 1u : 0u);
+        tc_commit(&o_done[x]);
+      };
+      mbar_wait(&q_full[0], 0);
+      if (hasB) mbar_wait(&q_full[1], 0);
+      issue_s(0, 0);
+      if (hasB) issue_s(1, 0);
+      tc_commit(&k_empty[0]);
+      for (int j = 0; j < n_kt; ++j) {
+        if (j < n_ktA) {
+          issue_pv(0, j);
+          if (!hasB) tc_commit(&v_empty[j % FA2_VST]);
+          if (j + 1 < n_ktA) {
+            issue_s(0, j + 1);
+            if (!hasB) tc_commit(&k_empty[(j + 1) % FA2_KST]);
+          }
+        }
+        if (hasB) {
+          issue_pv(1, j);
+          tc_commit(&v_empty[j % FA2_VST]);
+          if (j + 1 < n_kt) {
+            issue_s(1, j + 1);
+            tc_commit(&k_empty[(j + 1) % FA2_KST]);
+          }
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------------------------------------------------------- softmax (tile x)
+    const int x = (warp - 4) >> 2;
+    if (x == 1 && !hasB) goto done;
+    {
+      const int qt = qtA + x, nk = qt + 1;
+      const int ew = (warp - 4) & 3;
+      const int r = ew * 32 + lane;  // query row within the tile = TMEM lane
+      const uint32_t lane_off = static_cast<uint32_t>(ew * 32) << 16;
+      const uint32_t ts = tmem_base + x * FA_BN + lane_off;
+      const uint32_t tO = tmem_base + 2 * FA_BN + x * FA_D + lane_off;
+      float m_ref = -INFINITY, l = 0.f;
+      for (int j = 0; j < nk; ++j) {
+        mbar_wait(&s_full[x], j & 1);
+        tc_fence_after();
+        const bool diag = j == qt;
+        // pass 1: row max over the four 32-column chunks (8 independent chains)
+        float m8[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) m8[e] = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < FA_BN / 32; ++c) {
+          uint32_t sr[32];
+          tmem_ld_32x32b_x32(ts + c * 32, sr);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            float v = __uint_as_float(sr[i]);
+            if (diag && c * 32 + i > r) v = -INFINITY;
+            m8[i & 7] = fmaxf(m8[i & 7], v);
+          }
+        }
+        float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                         fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+        mx *= scale_log2;
+        bool grow = false;
+        float alpha = 1.0f;
+        if (j == 0) {
+          m_ref = mx;
+        } else {
+          grow = mx > m_ref + FA_RESCALE;
+          if (grow) {
+            alpha = ex2_approx(m_ref - mx);
+            l *= alpha;
+            m_ref = mx;
+          }
+        }
+        const bool any_grow = __any_sync(0xffffffffu, grow);
+        // pass 2: P = 2^(s * scale - m_ref) chunk by chunk; chunk c's 16 packed
+        // bf16x2 words overwrite columns [16c, 16c + 16) of S, already read
+        float l8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int c = 0; c < FA_BN / 32; ++c) {
+          uint32_t sr[32];
+          tmem_ld_32x32b_x32(ts + c * 32, sr);
+          tmem_ld_wait();
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float s0 = __uint_as_float(sr[2 * i]), s1 = __uint_as_float(sr[2 * i + 1]);
+            if (diag && c * 32 + 2 * i > r) s0 = -INFINITY;
+            if (diag && c * 32 + 2 * i + 1 > r) s1 = -INFINITY;
+            const float p0 = ex2_approx(fmaf(s0, scale_log2, -m_ref));
+            const float p1 = ex2_approx(fmaf(s1, scale_log2, -m_ref));
+            l8[(2 * i) & 7] += p0;
+            l8[(2 * i + 1) & 7] += p1;
+            pk[i] = pack_bf16(p0, p1);
+          }
+          tmem_st_32x32b_x16(ts + c * 16, pk);
+        }
+        l += ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
+        if (j > 0) {
+          mbar_wait(&o_done[x], (j - 1) & 1);  // PV_x(j-1) done (implied by s_full; explicit)
+          tc_fence_after();
+        }
+        if (any_grow) {
+#pragma unroll 1
+          for (int c = 0; c < FA_D / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(tO + c * 32, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+            tmem_st_32x32b_x32(tO + c * 32, v);
+          }
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&p_full[x]);
+      }
+      // ---------------------------------------------------------------- epilogue
+      mbar_wait(&o_done[x], (nk - 1) & 1);
+      tc_fence_after();
+      const int q_row0 = b * T + qt * FA_BM;
+      const int pos = qt * FA_BM + r;
+      const bool ok = pos < T;
+      const float inv_l = 1.0f / l;
+      __nv_bfloat16* orow = o + (long long)(q_row0 + r) * Hq * FA_D + hq * FA_D;
+#pragma unroll 1
+      for (int c = 0; c < FA_D / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tO + c * 32, v);
+        tmem_ld_wait();
+        if (ok) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t w[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              w[q] = pack_bf16(__uint_as_float(v[h * 16 + 2 * q]) * inv_l,
+                               __uint_as_float(v[h * 16 + 2 * q + 1]) * inv_l);
+            __nv_bfloat16* dst = orow + c * 32 + h * 16;
+            if (aligned32(dst)) {
+              st_global_v8(dst, w);
+            } else {
+              *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+              *reinterpret_cast<uint4*>(dst + 8) = make_uint4(w[4], w[5], w[6], w[7]);
+            }
+          }
+        }
+      }
+      if (ok && lse2 != nullptr) lse2[(long long)(q_row0 + r) * Hq + hq] = m_ref + log2f(l);
+    }
+  }
+done:
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+cudaError_t launch_attn_fwd_tc2(const __nv_bfloat16* q, const __nv_bfloat16* k,
+                                const __nv_bfloat16* v, __nv_bfloat16* o, long long N, int T,
+                                int Hq, int Hkv, float* lse2, cudaStream_t s) {
+  if (N == 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_tc2_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, FA2_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  CUtensorMap tq, tk, tv;
+  const Mat Q{q, N, (long long)Hq * FA_D, (long long)Hq * FA_D};
+  const Mat K{k, N, (long long)Hkv * FA_D, (long long)Hkv * FA_D};
+  const Mat V{v, N, (long long)Hkv * FA_D, (long long)Hkv * FA_D};
+  if (!make_tmap(&tq, Q, 64, FA_BM) || !make_tmap(&tk, K, 64, FA_BN) || !make_tmap(&tv, V, 64, FA_BN))
+    return cudaErrorInvalidValue;
+  const float scale_log2 = 1.4426950408889634f / sqrtf((float)FA_D);
+  const int nqt = (T + FA_BM - 1) / FA_BM;
+  dim3 grid((nqt + 1) / 2, Hq, (unsigned)(N / T));
+  attn_fwd_tc2_kernel<<<grid, 384, FA2_SMEM, s>>>(tq, tk, tv, o, lse2, T, Hq, Hkv, scale_log2);
+  return cudaGetLastError();
+}
+
+// ============================================================================
 // Backward (FlashAttention-2 split, deterministic: no float atomics).  With
 // lse2 from the forward and Dv = rowsum(dO * O) (attn_bwd_dot_kernel):
 //   P = 2^(s S - lse2), dP = dO V^T, dS = P (dP - Dv),

@@ -142,6 +142,10 @@ cudaError_t launch_infer_finalize_wide(const float* pm, const float* ps, const i
                                        cudaStream_t s);
 // tcgen05 flash-attention forward (attn_tc.cu): same contract as launch_attn_fwd,
 // seq_len a multiple of 64, lse2 required.
+// the two-query-tile (ping-pong) variant of the same forward
+cudaError_t launch_attn_fwd_tc2(const __nv_bfloat16* q, const __nv_bfloat16* k,
+                                const __nv_bfloat16* v, __nv_bfloat16* o, long long N, int T,
+                                int Hq, int Hkv, float* lse2, cudaStream_t s);
 cudaError_t launch_attn_fwd_tc(const __nv_bfloat16* q, const __nv_bfloat16* k,
                                const __nv_bfloat16* v, __nv_bfloat16* o, long long N, int T,
                                int Hq, int Hkv, float* lse2, cudaStream_t s);

@@ -34,7 +34,7 @@ def _rel(a, b):
     return ((a.float() - b.float()).norm() / b.float().norm()).item()
 
 
-@pytest.mark.parametrize("impl", [0, 1], ids=["mma_sync", "tcgen05"])
+@pytest.mark.parametrize("impl", [0, 1, 2], ids=["mma_sync", "tcgen05", "tcgen05_2tile"])
 @pytest.mark.parametrize("B,T,Hq,Hkv", [(2, 128, 4, 2), (1, 256, 2, 2), (3, 64, 8, 1),
                                         (1, 512, 4, 1), (2, 192, 2, 1), (1, 2048, 1, 1)])
 def test_attention_fwd_bwd_vs_fp32_autograd(gpu_lib, B, T, Hq, Hkv, impl):
@@ -69,7 +69,7 @@ def test_attention_fwd_bwd_vs_fp32_autograd(gpu_lib, B, T, Hq, Hkv, impl):
     assert torch.equal(dq, dq2) and torch.equal(dk, dk2) and torch.equal(dv, dv2)
 
 
-@pytest.mark.parametrize("impl", [0, 1], ids=["mma_sync", "tcgen05"])
+@pytest.mark.parametrize("impl", [0, 1, 2], ids=["mma_sync", "tcgen05", "tcgen05_2tile"])
 def test_attention_first_token_attends_only_to_itself(gpu_lib, impl):
     """Causal special case: row t = 0 of every sequence has o = v_0 exactly (up to
     the bf16 output rounding), lse = s_00, and dK/dV rows of the last key only
@@ -91,3 +91,27 @@ def test_attention_first_token_attends_only_to_itself(gpu_lib, impl):
             assert torch.equal(o[r, h * 128:(h + 1) * 128], v[r, :128])
             s00 = (q[r, h * 128:(h + 1) * 128].float() @ k[r, :128].float()) / math.sqrt(128)
             assert abs(lse2[r, h].item() * math.log(2.0) - s00.item()) <= 1e-3 * max(1, abs(s00))
+
+
+@pytest.mark.parametrize("B,T,Hq,Hkv", [(2, 128, 4, 2), (1, 384, 2, 1), (3, 64, 8, 1),
+                                        (1, 2048, 2, 2), (2, 192, 2, 1)])
+def test_two_tile_forward_bitwise_equals_one_tile(gpu_lib, B, T, Hq, Hkv):
+    """The ping-pong forward (two query tiles per CTA, impl 2) performs the same
+    per-row operations in the same order as the one-tile kernel: o and lse2
+    must be bitwise equal, including odd tile counts (T = 384, 192: the last
+    CTA has one tile) and T = 64 (a single partial tile)."""
+    ee = gpu_lib
+    g = torch.Generator(device="cuda").manual_seed(T + Hq)
+    n = B * T
+    q = (torch.randn(n, Hq * 128, device="cuda", generator=g) * 3).bfloat16()
+    k = (torch.randn(n, Hkv * 128, device="cuda", generator=g) * 3).bfloat16()
+    v = torch.randn(n, Hkv * 128, device="cuda", generator=g).bfloat16()
+    outs = []
+    for impl in (1, 2):
+        o = torch.full_like(q, float("nan"))
+        lse2 = torch.full((n, Hq), float("nan"), device="cuda")
+        ee.ee_test_attention(q, k, v, o, lse2, T, Hq, Hkv, impl=impl)
+        torch.cuda.synchronize()
+        outs.append((o, lse2))
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][1], outs[1][1])

@@ -97,17 +97,19 @@ def _run(ee, cfg, mode, P, hidden, targets, params, weights, weighting="uniform"
 _warmed = set()
 
 
-def _warm(ee, mode, arch):
-    """A world-1 comm step first: CUDA loads kernels lazily and a module load
-    waits for the context's running kernels, so a thread-rank's first launch
-    could otherwise wait behind another rank's spinning barrier (include/ee.h)."""
-    if (mode, arch) in _warmed:
+def _warm(ee, mode, arch, weighting="uniform"):
+    """A world-1 comm step first, with the same arch and token weighting:
+    CUDA loads kernels lazily and a module load waits for the context's
+    running kernels, so a thread-rank's first launch of a kernel could
+    otherwise wait behind another rank's spinning barrier (include/ee.h)."""
+    if (mode, arch, weighting) in _warmed:
         return
     cfg = _cfg(arch, 1)
     n = 256 if arch == "layer" else 64
     hidden = S.hidden_states(cfg, n)
-    _run(ee, cfg, mode, 1, hidden, S.targets(cfg, n), S.head_params(cfg), [1.0, 1.0])
-    _warmed.add((mode, arch))
+    _run(ee, cfg, mode, 1, hidden, S.targets(cfg, n), S.head_params(cfg), [1.0, 1.0],
+         weighting=weighting)
+    _warmed.add((mode, arch, weighting))
 
 
 def _check_vs_oracle(cfg, mode, P, out, hidden, targets, params, weights, weighting="uniform"):
@@ -149,7 +151,7 @@ def test_dp_comm_one_call_matches_oracle(gpu_lib, arch, P):
 def test_dp_comm_confidence_weighting_global_normaliser(gpu_lib):
     """P:326-336 / App. B.3: w_t = c_t detached, normalised by sum_t c_t over
     the tokens of ALL ranks (A17)."""
-    _warm(gpu_lib, "dp", "mlp")
+    _warm(gpu_lib, "dp", "mlp", "confidence")
     cfg = _cfg("mlp", 71)
     hidden = S.hidden_states(cfg)
     targets = S.targets(cfg)
@@ -189,7 +191,7 @@ def test_vp_comm_one_call_matches_oracle(gpu_lib, arch, P):
 
 
 def test_vp_comm_confidence_weighting(gpu_lib):
-    _warm(gpu_lib, "vp", "mlp")
+    _warm(gpu_lib, "vp", "mlp", "confidence")
     cfg = _cfg("mlp", 73)
     hidden = S.hidden_states(cfg)
     targets = S.targets(cfg)
