@@ -349,15 +349,60 @@ cudaError_t launch_attn_fwd_tc(const __nv_bfloat16* q, const __nv_bfloat16* k,
 // are loaded once for both tiles.  TMEM: S_A | S_B | O_A | O_B (4 x 128
 // columns); P_X(j) is written as bf16 over the first 64 columns of S_X (the
 // TMEM A operand of PV_X(j)); S_X(j+1) is issued after PV_X(j), so the tensor
-// pipe's issue order protects P.  The softmax reads S in 32-column chunks
-// (two passes: max, then exp2) to stay under the 168 registers a 384-thread
-// CTA allows.  Same arithmetic, rounding points and outputs as the one-tile
-// kernel (bitwise: the per-row operations and their order are unchanged).
+// pipe's issue order protects P.  setmaxnreg moves registers from the
+// producer / MMA warpgroup to the softmax warpgroups, which hold a whole S row.
+// Same arithmetic, rounding points and outputs as the one-tile kernel
+// (bitwise: the per-row operations and their order are unchanged).
+// 2^x on the FMA pipe (FA4's trick to take part of the exp2 load off the
+// 16/clk/SM MUFU unit): x = n + f with n = rint(x) from the 1.5 * 2^23 magic
+// constant, 2^f by a degree-3 minimax polynomial on [-0.5, 0.5] (max relative
+// error 7.5e-5, below the bf16 rounding of P, 2^-9), and 2^n added to the
+// exponent field with one integer multiply-add (the magic constant has zero
+// low 22 bits, so bits(t) << 23 = n << 23 mod 2^32).  x >= -125 (clamped):
+// only used on tiles without masked (-inf) entries, where x >= -(2^8 + ...).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -125.0f);
+  const float t = x + 12582912.0f;
+  const float f = x - (t - 12582912.0f);
+  const float p = fmaf(fmaf(fmaf(0.0551716685f, f, 0.2426111549f), f, 0.6932609677f), f,
+                       0.9999280572f);
+  return __int_as_float(__float_as_int(t) * (1 << 23) + __float_as_int(p));
+}
+
+// Blackwell packed / 3-input fp32 ops (FMNMX3, FFMA2, FADD2): the two-tile
+// softmax is issue-bound, and these halve its max / scale / sum instructions
+// with the same per-element IEEE roundings as fmaxf / fmaf / fadd.
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned long long f2pack(float a, float b) {
+  unsigned long long v;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "f"(a), "f"(b));
+  return v;
+}
+__device__ __forceinline__ void f2unpack(unsigned long long v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
 namespace {
 constexpr int FA2_KST = 2, FA2_VST = 2;
 constexpr int FA2_SMEM = 1024 + FA_TILE * (2 + FA2_KST + FA2_VST) + 512;
 }  // namespace
 
+template <int POLY>
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                         const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ o,
@@ -418,8 +463,12 @@ __global__ void __launch_bounds__(384, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  // registers: 56 for the producer / MMA warpgroup, 224 for the two softmax
+  // warpgroups (4 x 32 x 56 + 8 x 32 x 224 <= 64 K), which hold a whole
+  // 128-column S row each
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA: Q_A, Q_B, K
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
     if (lane == 0) {
       for (int x = 0; x < (hasB ? 2 : 1); ++x) {
         const int row0 = b * T + (qtA + x) * FA_BM;
@@ -439,6 +488,7 @@ __global__ void __launch_bounds__(384, 1)
     }
   } else if (warp == 3) {
     // ---------------------------------------------------------------- TMA: V
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
     if (lane == 0) {
       for (int j = 0; j < n_kt; ++j) {
         const int s = j % FA2_VST;
@@ -452,6 +502,7 @@ __global__ void __launch_bounds__(384, 1)
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
     if (lane == 0) {
       constexpr uint32_t idesc_qk = make_idesc_bf16(FA_BM, FA_BN, false, false);
       constexpr uint32_t idesc_pv = make_idesc_bf16(FA_BM, FA_D, false, true);
@@ -519,8 +570,11 @@ __global__ void __launch_bounds__(384, 1)
         }
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp == 2) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+  } else {
     // ---------------------------------------------------------------- softmax (tile x)
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
     const int x = (warp - 4) >> 2;
     if (x == 1 && !hasB) goto done;
     {
@@ -535,22 +589,33 @@ __global__ void __launch_bounds__(384, 1)
         mbar_wait(&s_full[x], j & 1);
         tc_fence_after();
         const bool diag = j == qt;
-        // pass 1: row max over the four 32-column chunks (8 independent chains)
+        // the whole 128-column row in registers (setmaxnreg above): four TMEM
+        // loads in flight, one wait; the causal mask only on the diagonal tile
+        uint32_t sr[FA_BN];
+        tmem_ld_32x32b_x32(ts, *reinterpret_cast<uint32_t(*)[32]>(sr));
+        tmem_ld_32x32b_x32(ts + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+        tmem_ld_32x32b_x32(ts + 64, *reinterpret_cast<uint32_t(*)[32]>(sr + 64));
+        tmem_ld_32x32b_x32(ts + 96, *reinterpret_cast<uint32_t(*)[32]>(sr + 96));
+        tmem_ld_wait();
+        float sv[FA_BN];
+#pragma unroll
+        for (int i = 0; i < FA_BN; ++i) sv[i] = __uint_as_float(sr[i]);
+        if (diag) {
+#pragma unroll
+          for (int i = 0; i < FA_BN; ++i)
+            if (i > r) sv[i] = -INFINITY;
+        }
+        // row max: 8 independent chains of 3-input max (exact, so the same
+        // value as the one-tile kernel's 2-input chains)
         float m8[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) m8[e] = -INFINITY;
+        for (int e = 0; e < 8; ++e) m8[e] = sv[e];
 #pragma unroll
-        for (int c = 0; c < FA_BN / 32; ++c) {
-          uint32_t sr[32];
-          tmem_ld_32x32b_x32(ts + c * 32, sr);
-          tmem_ld_wait();
+        for (int i = 8; i + 16 <= FA_BN; i += 16)
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            float v = __uint_as_float(sr[i]);
-            if (diag && c * 32 + i > r) v = -INFINITY;
-            m8[i & 7] = fmaxf(m8[i & 7], v);
-          }
-        }
+          for (int e = 0; e < 8; ++e) m8[e] = fmax3f(m8[e], sv[i + e], sv[i + 8 + e]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) m8[e] = fmaxf(m8[e], sv[FA_BN - 8 + e]);
         float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
                          fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
         mx *= scale_log2;
@@ -567,28 +632,47 @@ __global__ void __launch_bounds__(384, 1)
           }
         }
         const bool any_grow = __any_sync(0xffffffffu, grow);
-        // pass 2: P = 2^(s * scale - m_ref) chunk by chunk; chunk c's 16 packed
-        // bf16x2 words overwrite columns [16c, 16c + 16) of S, already read
+        uint32_t pk[FA_BN / 2];
         float l8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (POLY == 0) {  // packed: x = s * scale - m (FFMA2), l chains (FADD2)
+          const unsigned long long sc2 = f2pack(scale_log2, scale_log2);
+          const unsigned long long nm2 = f2pack(-m_ref, -m_ref);
+          unsigned long long l2[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-        for (int c = 0; c < FA_BN / 32; ++c) {
-          uint32_t sr[32];
-          tmem_ld_32x32b_x32(ts + c * 32, sr);
-          tmem_ld_wait();
-          uint32_t pk[16];
+          for (int i = 0; i < FA_BN / 2; ++i) {
+            float x0, x1;
+            f2unpack(ffma2(f2pack(sv[2 * i], sv[2 * i + 1]), sc2, nm2), x0, x1);
+            const float p0 = ex2_approx(x0), p1 = ex2_approx(x1);
+            l2[i & 3] = fadd2(l2[i & 3], f2pack(p0, p1));   // chains (2i)&7, (2i+1)&7
+            pk[i] = pack_bf16(p0, p1);
+          }
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            float s0 = __uint_as_float(sr[2 * i]), s1 = __uint_as_float(sr[2 * i + 1]);
-            if (diag && c * 32 + 2 * i > r) s0 = -INFINITY;
-            if (diag && c * 32 + 2 * i + 1 > r) s1 = -INFINITY;
-            const float p0 = ex2_approx(fmaf(s0, scale_log2, -m_ref));
-            const float p1 = ex2_approx(fmaf(s1, scale_log2, -m_ref));
+          for (int c = 0; c < 4; ++c) f2unpack(l2[c], l8[2 * c], l8[2 * c + 1]);
+        } else if (!diag) {  // every POLY-th pair of exp2 on the FMA pipe
+#pragma unroll
+          for (int i = 0; i < FA_BN / 2; ++i) {
+            const bool poly = (i % (POLY > 0 ? POLY : 1)) == (POLY > 0 ? POLY : 1) - 1;
+            const float x0 = fmaf(sv[2 * i], scale_log2, -m_ref);
+            const float x1 = fmaf(sv[2 * i + 1], scale_log2, -m_ref);
+            const float p0 = poly ? ex2_poly(x0) : ex2_approx(x0);
+            const float p1 = poly ? ex2_poly(x1) : ex2_approx(x1);
             l8[(2 * i) & 7] += p0;
             l8[(2 * i + 1) & 7] += p1;
             pk[i] = pack_bf16(p0, p1);
           }
-          tmem_st_32x32b_x16(ts + c * 16, pk);
+        } else {
+#pragma unroll
+          for (int i = 0; i < FA_BN / 2; ++i) {
+            const float p0 = ex2_approx(fmaf(sv[2 * i], scale_log2, -m_ref));
+            const float p1 = ex2_approx(fmaf(sv[2 * i + 1], scale_log2, -m_ref));
+            l8[(2 * i) & 7] += p0;
+            l8[(2 * i + 1) & 7] += p1;
+            pk[i] = pack_bf16(p0, p1);
+          }
         }
+        // P over the first 64 columns of S_x (read into registers above)
+        tmem_st_32x32b_x32(ts, *reinterpret_cast<const uint32_t(*)[32]>(pk));
+        tmem_st_32x32b_x32(ts + 32, *reinterpret_cast<const uint32_t(*)[32]>(pk + 32));
         l += ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
         if (j > 0) {
           mbar_wait(&o_done[x], (j - 1) & 1);  // PV_x(j-1) done (implied by s_full; explicit)
@@ -656,12 +740,20 @@ cudaError_t launch_attn_fwd_tc2(const __nv_bfloat16* q, const __nv_bfloat16* k,
                                 const __nv_bfloat16* v, __nv_bfloat16* o, long long N, int T,
                                 int Hq, int Hkv, float* lse2, cudaStream_t s) {
   if (N == 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_tc2_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, FA2_SMEM);
+  // EE_ATTN_POLY = k: every k-th pair of exp2 of the off-diagonal tiles on the
+  // FMA pipe (0 = all on MUFU: bitwise the one-tile kernel's outputs)
+  static const int poly = [] {
+    const char* e = getenv("EE_ATTN_POLY");
+    return e ? atoi(e) : 0;
+  }();
+  auto kern = poly == 2 ? attn_fwd_tc2_kernel<2> : poly == 3 ? attn_fwd_tc2_kernel<3>
+            : poly == 4 ? attn_fwd_tc2_kernel<4> : attn_fwd_tc2_kernel<0>;
+  static bool attr[5] = {false, false, false, false, false};
+  const int pi = (poly >= 2 && poly <= 4) ? poly : 0;
+  if (!attr[pi]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, FA2_SMEM);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr[pi] = true;
   }
   CUtensorMap tq, tk, tv;
   const Mat Q{q, N, (long long)Hq * FA_D, (long long)Hq * FA_D};
@@ -672,7 +764,7 @@ cudaError_t launch_attn_fwd_tc2(const __nv_bfloat16* q, const __nv_bfloat16* k,
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)FA_D);
   const int nqt = (T + FA_BM - 1) / FA_BM;
   dim3 grid((nqt + 1) / 2, Hq, (unsigned)(N / T));
-  attn_fwd_tc2_kernel<<<grid, 384, FA2_SMEM, s>>>(tq, tk, tv, o, lse2, T, Hq, Hkv, scale_log2);
+  kern<<<grid, 384, FA2_SMEM, s>>>(tq, tk, tv, o, lse2, T, Hq, Hkv, scale_log2);
   return cudaGetLastError();
 }
 
