@@ -577,7 +577,7 @@ def main():
                          "ablation (A24)")
     ap.add_argument("--no-ds-ablation", action="store_true",
                     help="N=1: skip timing the other ds_mode beside the headline")
-    ap.add_argument("--cpu-tokens", type=int, default=32,
+    ap.add_argument("--cpu-tokens", type=int, default=64,
                     help="token sample of the fp64 oracle in cpu_baseline (all exits)")
     ap.add_argument("--ref-tokens", type=int, default=32,
                     help="--impl reference: tokens of the one exit each step runs")

@@ -27,10 +27,24 @@
 #include <string>
 #include <atomic>
 #include <vector>
+#include <nvtx3/nvToolsExt.h>
 #include "../../include/ee.h"
 #include "internal.cuh"
 
 using namespace ee;
+
+namespace ee {
+// NVTX range on the calling host thread (per exit and per phase of the step;
+// a no-op unless a profiler such as nsys is attached).
+struct Nvtx {
+  explicit Nvtx(const char* fmt, int i = -1) {
+    char b[96];
+    if (i >= 0) snprintf(b, sizeof(b), fmt, i); else snprintf(b, sizeof(b), "%s", fmt);
+    nvtxRangePushA(b);
+  }
+  ~Nvtx() { nvtxRangePop(); }
+};
+}  // namespace ee
 
 namespace {
 
@@ -1039,8 +1053,11 @@ static ee_status tune_step_impl(const ee_head_config* cfg, const void* const* hi
     const AdamFuse* af = afuse ? &afuse[i] : nullptr;
     const __nv_bfloat16* x = (const __nv_bfloat16*)hidden[i];
     const __nv_bfloat16* z = nullptr;
-    if ((s = phase_exit_forward(cfg, B, P, x, n, nullptr, &z, st)) != EE_OK) return s;
-    if ((s = phase_vocab_stats(cfg, B, P, z, n, targets, st, true)) != EE_OK) return s;
+    Nvtx nv_exit("ee exit %d", i);
+    { Nvtx nv_("exit forward (a1-a4)");
+    if ((s = phase_exit_forward(cfg, B, P, x, n, nullptr, &z, st)) != EE_OK) return s; }
+    { Nvtx nv_("vocab GEMM + online-softmax stats (a5)");
+    if ((s = phase_vocab_stats(cfg, B, P, z, n, targets, st, true)) != EE_OK) return s; }
     // a6: lse, coef, per-token aux, L_i
     {
       const ee_step_aux* ax = aux ? &aux[i] : nullptr;
@@ -1062,11 +1079,13 @@ static ee_status tune_step_impl(const ee_head_config* cfg, const void* const* hi
       if (ax && ax->weight_sum)
         EE_CUDA(cudaMemcpyAsync(ax->weight_sum, B.wsum, sizeof(float), cudaMemcpyDeviceToDevice, st));
     }
+    { Nvtx nv_("vocab backward (a7-a9)");
     if ((s = phase_vocab_backward(cfg, B, P, G, z, n, targets, accumulate, nrm ? B.dz : nullptr,
                                   st, nullptr, gs, af)) != EE_OK)
-      return s;
+      return s; }
+    { Nvtx nv_("exit backward (a10-a13)");
     if ((s = phase_exit_backward(cfg, B, P, G, x, n, B.dz, accumulate, st, 1, gs, af)) != EE_OK)
-      return s;
+      return s; }
     if (af) {  // the gains' Adam (their gradients are column sums, in B.gsc)
       const int gk[3] = {4, 0, 6};
       for (int j = 0; j < 3; ++j) {

@@ -16,6 +16,7 @@
 // No NCCL and no host synchronisation: everything is stream-ordered, and
 // ranks are ordered against each other by ee_peer_barrier.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <cstdint>
 #include <cstring>
 #include <new>
@@ -185,6 +186,8 @@ ee_status peer_reduce(const ee_comm* c, size_t off, long long n, T* out, cudaStr
 }
 
 ee_status barrier(ee_comm* c, void* ws, cudaStream_t st) {
+  nvtxRangePushA("ee_comm barrier");
+  struct Pop { ~Pop() { nvtxRangePop(); } } pop_;
   ee_peer_set sig;
   memset(&sig, 0, sizeof(sig));
   sig.rank = c->rank;
@@ -208,6 +211,8 @@ ee_peer_set pset(const ee_comm* c, size_t off) {
 ee_status reduce_gather(ee_comm* c, const ee_head_config* c1, int j, ee_head_tensors* grads,
                         int accumulate, void* ws, cudaStream_t st) {
   const int P = c->world;
+  nvtxRangePushA("ee_comm gradient reduce + gather");
+  struct Pop { ~Pop() { nvtxRangePop(); } } pop_;
   COMM_TRY(barrier(c, ws, st));
   float* own = (float*)(c->arena[c->rank] + c->off_grad[j]);
   for (int k = 0; k < NT; ++k) {
