@@ -1011,6 +1011,7 @@ def main():
                     "peak_source": peaks["source"] + ", sustained (kernel timed inside a long step)"}
 
     F_alg = step_flops(cfg, n_all if vp else n)          # per GPU for dp, whole job for vp
+    exec_tflops = sum(d["flops_exec"] for d in kern.values()) / args.steps / (ms / 1e3) / 1e12
     tflops = F_alg / (ms / 1e3) / 1e12 / (world if vp else 1)
     value = job_tokens / (ms / 1e3)
     line = {
@@ -1025,7 +1026,11 @@ def main():
                      "of_burst": tflops / peaks["bf16_tflops"],
                      "of_sustained": tflops / peaks["bf16_tflops_sustained"],
                      "of_datasheet_2250": tflops / 2250.0,
-                     "step_flops_alg_per_gpu": F_alg / (world if vp else 1)},
+                     "step_flops_alg_per_gpu": F_alg / (world if vp else 1),
+                     # executed tensor work incl. the dS recompute GEMM (not credited above)
+                     "executed_tflops_per_gpu": exec_tflops,
+                     "executed_of_burst": exec_tflops / peaks["bf16_tflops"],
+                     "peak_source": peaks["source"]},
         "roofline": roofline,
         # exit-tokens/s (comparable across exit counts) and the
         # optimizer's share, reported beside the step that includes it
