@@ -257,6 +257,11 @@ def run_reference(args, cfg, rank, world):
 
 
 def vp_comm_desc(args, vp, world):
+    if getattr(args, "lib_comm", False):
+        return {"dp_comm": "ee_tune_step(comm): the in-library communicator -- gradient rows "
+                           "stored to their owners in the weight-gradient epilogues, owner-side "
+                           "rank-ordered sums, NVLink gather of the reduced rows, rank-ordered "
+                           "small reductions, device barriers (no NCCL on the step); Adam per rank"}
     if getattr(args, "dp_fused", False):
         base = "gloo" if getattr(args, "shared_gpu", False) else "NCCL"
         return {"dp_comm": "gradient reduce-scatter fused into the weight-gradient GEMM epilogues "
@@ -323,7 +328,9 @@ def workload_config(cfg, world, args):
                                 if getattr(args, "per_exit", False) else
                                 "per exit: tune with the gradient rows stored to their owners, "
                                 "peer barrier, sharded Adam (ZeRO-1; P:261)"
-                                if getattr(args, "dp_fused", False) else "all exits, then Adam")}
+                                if getattr(args, "dp_fused", False) else
+                                "all exits in one ee_tune_step(comm) call, then Adam"
+                                if getattr(args, "lib_comm", False) else "all exits, then Adam")}
 
 
 LLAMA2 = {4096: (32, 32), 5120: (40, 40), 8192: (64, 8)}   # hidden -> (heads, kv heads) [ext]
@@ -590,11 +597,13 @@ def main():
     ap.add_argument("--grad-buffers", type=int, default=-1,
                     help="non-fused paths, k < exits: exits share k gradient buffers and are "
                          "updated one by one (P:261); default 2 when the config has > 4 exits")
-    ap.add_argument("--dp-comm", default="fused", choices=["fused", "nccl", "plain"],
+    ap.add_argument("--dp-comm", default="fused", choices=["fused", "nccl", "plain", "lib"],
                     help="dp: fused = gradient reduce-scatter in the weight-gradient GEMM "
                          "epilogues + sharded Adam storing the operands to every rank (CUDA-IPC "
                          "peer memory, ZeRO-1; used at N=1 too); nccl = NCCL all-reduce + full "
-                         "Adam per rank; plain = N=1 only: ExitHeads step + Adam (no DP machinery)")
+                         "Adam per rank; plain = N=1 only: ExitHeads step + Adam (no DP machinery); "
+                         "lib = one ee_tune_step(comm) call per step (the in-library DP "
+                         "communicator: all-reduced gradients on every rank) + Adam per rank")
     ap.add_argument("--overlap", action="store_true",
                     help="plain N=1: exit-by-exit step with each exit's Adam on a side stream")
     ap.add_argument("--fused-adam", action="store_true",
@@ -673,7 +682,7 @@ def main():
     if args.dp_comm == "plain" and multi:
         raise SystemExit("--dp-comm plain is the one-GPU path")
     gbuf = args.grad_buffers if args.grad_buffers >= 0 else (2 if E > 4 else 0)
-    if vp:
+    if vp or args.dp_comm == "lib":
         gbuf = 0
     dp_fused = not vp and args.dp_comm == "fused"
     heads = None
@@ -715,12 +724,20 @@ def main():
         heads = ee.ExitHeads(ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, E, cfg.arch,
                                          vocab_begin=vb, vocab_end=ve, **spec_kw), n_all,
                              device=dev, grad_buffers=gbuf if gbuf > 0 else None)
+    lib_comm = None
+    if not vp and args.dp_comm == "lib":
+        ex = (lambda obj: (lambda out: (dist.all_gather_object(out, obj), out)[1])([None] * world)) \
+            if multi else None
+        lib_comm = ee.Comm(heads.cfg, "dp", world, rank, n, exchange=ex, device=dev)
+        peer_map = {"kind": "ee_comm arena over CUDA IPC" if multi else "ee_comm (one rank)",
+                    "arena_bytes": lib_comm.bytes}
+    args.lib_comm = lib_comm is not None
     fused_adam = not multi and not vp and not dp_fused and args.fused_adam
     args.fused_adam = fused_adam
     overlapped = not multi and not vp and not dp_fused and not fused_adam and args.overlap
     args.overlapped = overlapped
     per_exit = ((not dp_fused) and (not vp_zero) and (not fused_adam) and (not overlapped)
-                and heads.grad_buffers < E)
+                and lib_comm is None and heads.grad_buffers < E)
     args.per_exit = per_exit
     bb = S.backbone(cfg, device=dev)
     src = []
@@ -812,6 +829,9 @@ def main():
             else:
                 vocab_parallel_step(phases, comm, cfg.arch, hid, tg, heads.operand, heads.grads,
                                     heads.loss, [1.0] * E, vc, bufs)
+        elif lib_comm is not None:     # the whole DP step in one C-ABI call (ee_comm)
+            ee.ee_tune_step(heads.cfg, hid, tg, [1.0] * E, heads.operand, heads.grads,
+                            heads.loss, heads.workspace, comm=lib_comm)
         elif not dp:
             heads.step(hid, tg)
         else:
@@ -904,7 +924,7 @@ def main():
         perm = [(i + 1) % E for i in range(E)]
         sets_host = [(h_host, t_host), ([h_host[j] for j in perm], t_host)]
         sets_dev = [(hidden, targets), ([hidden[j] for j in perm], targets)]
-        streamed = not vp and not per_exit and (dp_fused or not multi)
+        streamed = not vp and not per_exit and lib_comm is None and (dp_fused or not multi)
         check = None
         if streamed:
             # correctness of the host-input path on alternating sets, lr = 0
