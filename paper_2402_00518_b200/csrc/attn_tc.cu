@@ -778,7 +778,11 @@ cudaError_t launch_attn_fwd_tc2(const __nv_bfloat16* q, const __nv_bfloat16* k,
 namespace {
 constexpr int FB_BQ = 64;                       // queries per step of the dK/dV kernel
 constexpr int FB_QT = FB_BQ * FA_D * 2;         // 16 KB: two 8 KB SW128 atoms
-constexpr int FB_SMEM_KV = 1024 + 2 * FA_TILE + 2 * 2 * FB_QT + 2 * 2 * FB_BQ * 4 + 256;
+#ifndef EE_FB_QST
+#define EE_FB_QST 4                                 // Q / dO ring stages of the dK/dV kernel
+#endif
+constexpr int FB_QST = EE_FB_QST;
+constexpr int FB_SMEM_KV = 1024 + 2 * FA_TILE + FB_QST * 2 * FB_QT + 2 * 2 * FB_BQ * 4 + 512;
 constexpr int FQ_BK = 64;                       // keys per step of the dQ kernel
 constexpr int FQ_KT = FQ_BK * FA_D * 2;         // 16 KB K or V tile
 constexpr int FQ_STAGES = 4;
@@ -860,7 +864,7 @@ __device__ __forceinline__ void store_row_bf16(uint32_t tacc, __nv_bfloat16* dst
 
 // dK, dV: one CTA per (128-key tile, kv head, sequence); loops over the query
 // heads of the GQA group and the 64-query tiles at or after the key tile.
-//   warp 0 TMA (K, V once; Q_i, dO_i double-buffered), warp 1 MMA,
+//   warp 0 TMA (K, V once; Q_i, dO_i in a FB_QST-stage ring), warp 1 MMA,
 //   warps 4..7 one thread per key row (TMEM lane).
 // TMEM: S^T [128 x 64] | dP^T [128 x 64] | dK [128 x 128] | dV [128 x 128].
 __global__ void __launch_bounds__(384, 1)
@@ -877,18 +881,18 @@ __global__ void __launch_bounds__(384, 1)
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sK = smem;
   uint8_t* sV = sK + FA_TILE;
-  uint8_t* sQ = sV + FA_TILE;          // [2] x 16 KB
-  uint8_t* sDO = sQ + 2 * FB_QT;       // [2] x 16 KB
-  float* sL = reinterpret_cast<float*>(sDO + 2 * FB_QT);  // [2][64]
+  uint8_t* sQ = sV + FA_TILE;          // [FB_QST] x 16 KB
+  uint8_t* sDO = sQ + FB_QST * FB_QT;  // [FB_QST] x 16 KB
+  float* sL = reinterpret_cast<float*>(sDO + FB_QST * FB_QT);  // [2][64]
   float* sD = sL + 2 * FB_BQ;                              // [2][64]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 2 * FB_BQ);
   uint64_t* kv_full = bars;
-  uint64_t* qd_full = bars + 1;   // [2]
-  uint64_t* qd_empty = bars + 3;  // [2]
-  uint64_t* sdp_full = bars + 5;  // [2]
-  uint64_t* pds_full = bars + 7;  // [2], per P^T/dS^T buffer (see attn_bwd_dq_tc_kernel)
-  uint64_t* acc_done = bars + 9;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* qd_full = bars + 1;              // [FB_QST]
+  uint64_t* qd_empty = qd_full + FB_QST;     // [FB_QST]
+  uint64_t* sdp_full = qd_empty + FB_QST;    // [2]
+  uint64_t* pds_full = sdp_full + 2;         // [2], per P^T/dS^T buffer (see attn_bwd_dq_tc_kernel)
+  uint64_t* acc_done = pds_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kt = blockIdx.x, hk = blockIdx.y, b = blockIdx.z;
@@ -905,7 +909,7 @@ __global__ void __launch_bounds__(384, 1)
     tma_prefetch_desc(&tmV);
     tma_prefetch_desc(&tmDO);
     mbar_init(kv_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < FB_QST; ++s) {
       mbar_init(&qd_full[s], 1);
       mbar_init(&qd_empty[s], 1);
     }
@@ -935,10 +939,10 @@ __global__ void __launch_bounds__(384, 1)
       tma_load_2d(sV + FA_ATOM, &tmV, kv_full, hk * FA_D + 64, k_row0);
       mbar_arrive_expect_tx(kv_full, 2 * FA_TILE);
       for (int it = 0; it < n_it; ++it) {
-        const int s = it & 1;
+        const int s = it % FB_QST;
         const int hq = hk * grp + it / per_head;
         const int q_row0 = b * T + (q64_0 + it % per_head) * FB_BQ;
-        mbar_wait(&qd_empty[s], ((it >> 1) & 1) ^ 1);
+        mbar_wait(&qd_empty[s], ((it / FB_QST) & 1) ^ 1);
         uint8_t* q = sQ + s * FB_QT;
         uint8_t* d = sDO + s * FB_QT;
         tma_load_2d(q, &tmQ, &qd_full[s], hq * FA_D, q_row0);
@@ -958,11 +962,11 @@ __global__ void __launch_bounds__(384, 1)
       // S^T / dP^T of step `it` into TMEM buffer it & 1, issued one step ahead
       // so the tensor core works while the softmax threads process the last one
       auto issue_sdp = [&](int it) {
-        const int s = it & 1;
-        mbar_wait(&qd_full[s], (it >> 1) & 1);
+        const int qs = it % FB_QST;
+        mbar_wait(&qd_full[qs], (it / FB_QST) & 1);
         tc_fence_after();
-        const uint32_t bq = smem_u32(sQ + s * FB_QT), bd = smem_u32(sDO + s * FB_QT);
-        const uint32_t tS = tmem_base + s * 128, tDP = tS + 64;
+        const uint32_t bq = smem_u32(sQ + qs * FB_QT), bd = smem_u32(sDO + qs * FB_QT);
+        const uint32_t tS = tmem_base + (it & 1) * 128, tDP = tS + 64;
 #pragma unroll
         for (int k = 0; k < FA_D / 16; ++k) {  // S^T = K Q^T, dP^T = V dO^T (K-major, K = d)
           const uint32_t offa = (k >> 2) * FA_ATOM + (k & 3) * 32;
@@ -972,7 +976,7 @@ __global__ void __launch_bounds__(384, 1)
           tc_mma_f16(tDP, make_sdesc(av + offa, 16, 1024), make_sdesc(bd + offb, 16, 1024),
                      idesc_s, k != 0 ? 1u : 0u);
         }
-        tc_commit(&sdp_full[s]);
+        tc_commit(&sdp_full[it & 1]);
       };
       if (n_it > 0) issue_sdp(0);
       for (int it = 0; it < n_it; ++it) {
@@ -980,7 +984,8 @@ __global__ void __launch_bounds__(384, 1)
         if (it + 1 < n_it) issue_sdp(it + 1);
         mbar_wait(&pds_full[s], (it >> 1) & 1);
         tc_fence_after();
-        const uint32_t bq = smem_u32(sQ + s * FB_QT), bd = smem_u32(sDO + s * FB_QT);
+        const int qs = it % FB_QST;
+        const uint32_t bq = smem_u32(sQ + qs * FB_QT), bd = smem_u32(sDO + qs * FB_QT);
         const uint32_t tPt = tmem_base + s * 128, tDSt = tPt + 64;
 #pragma unroll
         for (int k = 0; k < FB_BQ / 16; ++k) {  // dV += P^T dO, dK += dS^T Q (A in TMEM, K = q)
@@ -992,7 +997,7 @@ __global__ void __launch_bounds__(384, 1)
           tc_mma_f16_ts(tDK, tDSt + offa, make_sdesc(bq + offb, FB_QT / 2, 1024), idesc_acc,
                         (it | k) != 0 ? 1u : 0u);
         }
-        tc_commit(&qd_empty[s]);
+        tc_commit(&qd_empty[qs]);
       }
       tc_commit(acc_done);
     }
