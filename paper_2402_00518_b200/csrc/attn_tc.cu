@@ -502,8 +502,9 @@ __global__ void __launch_bounds__(384, 1)
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
+    // (the whole warp runs the loop; elect.sync issues: ptx.cuh tc_mma_f16_w)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
-    if (lane == 0) {
+    {
       constexpr uint32_t idesc_qk = make_idesc_bf16(FA_BM, FA_BN, false, false);
       constexpr uint32_t idesc_pv = make_idesc_bf16(FA_BM, FA_D, false, true);
       int k_ready = -1, v_ready = -1;
@@ -528,10 +529,10 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int k = 0; k < FA_D / 16; ++k) {
           const uint32_t off = (k >> 2) * FA_ATOM + (k & 3) * 32;
-          tc_mma_f16(tmem_base + x * FA_BN, make_sdesc(aq + off, 16, 1024),
+          tc_mma_f16_w(tmem_base + x * FA_BN, make_sdesc(aq + off, 16, 1024),
                      make_sdesc(bk + off, 16, 1024), idesc_qk, k != 0 ? 1u : 0u);
         }
-        tc_commit(&s_full[x]);
+        tc_commit_w(&s_full[x]);
       };
       auto issue_pv = [&](int x, int j) {  // O_x (+)= P_x(j) V_j, P in TMEM
         ensure_v(j);
@@ -541,31 +542,31 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t tO = tmem_base + 2 * FA_BN + x * FA_D;
 #pragma unroll
         for (int k = 0; k < FA_BN / 16; ++k)
-          tc_mma_f16_ts(tO, tmem_base + x * FA_BN + k * 8,
+          tc_mma_f16_ts_w(tO, tmem_base + x * FA_BN + k * 8,
                         make_sdesc(bv + k * 2048, FA_ATOM, 1024), idesc_pv,
                         (j | k) != 0 ? 1u : 0u);
-        tc_commit(&o_done[x]);
+        tc_commit_w(&o_done[x]);
       };
       mbar_wait(&q_full[0], 0);
       if (hasB) mbar_wait(&q_full[1], 0);
       issue_s(0, 0);
       if (hasB) issue_s(1, 0);
-      tc_commit(&k_empty[0]);
+      tc_commit_w(&k_empty[0]);
       for (int j = 0; j < n_kt; ++j) {
         if (j < n_ktA) {
           issue_pv(0, j);
-          if (!hasB) tc_commit(&v_empty[j % FA2_VST]);
+          if (!hasB) tc_commit_w(&v_empty[j % FA2_VST]);
           if (j + 1 < n_ktA) {
             issue_s(0, j + 1);
-            if (!hasB) tc_commit(&k_empty[(j + 1) % FA2_KST]);
+            if (!hasB) tc_commit_w(&k_empty[(j + 1) % FA2_KST]);
           }
         }
         if (hasB) {
           issue_pv(1, j);
-          tc_commit(&v_empty[j % FA2_VST]);
+          tc_commit_w(&v_empty[j % FA2_VST]);
           if (j + 1 < n_kt) {
             issue_s(1, j + 1);
-            tc_commit(&k_empty[(j + 1) % FA2_KST]);
+            tc_commit_w(&k_empty[(j + 1) % FA2_KST]);
           }
         }
       }
@@ -953,7 +954,7 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // whole warp; elect.sync issues (ptx.cuh tc_mma_f16_w)
       constexpr uint32_t idesc_s = make_idesc_bf16(FA_BN, FB_BQ, false, false);   // 128 x 64
       constexpr uint32_t idesc_acc = make_idesc_bf16(FA_BN, FA_D, false, true);   // 128 x 128
       const uint32_t ak = smem_u32(sK), av = smem_u32(sV);
@@ -967,16 +968,18 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         const uint32_t bq = smem_u32(sQ + qs * FB_QT), bd = smem_u32(sDO + qs * FB_QT);
         const uint32_t tS = tmem_base + (it & 1) * 128, tDP = tS + 64;
+        // descriptors built once; the k-step offsets (< 64 KB, 16-byte units)
+        // are added to the start-address field (no carry out of its 14 bits)
+        const uint64_t dk0 = make_sdesc(ak, 16, 1024), dv0 = make_sdesc(av, 16, 1024);
+        const uint64_t dq0 = make_sdesc(bq, 16, 1024), ddo0 = make_sdesc(bd, 16, 1024);
 #pragma unroll
         for (int k = 0; k < FA_D / 16; ++k) {  // S^T = K Q^T, dP^T = V dO^T (K-major, K = d)
-          const uint32_t offa = (k >> 2) * FA_ATOM + (k & 3) * 32;
-          const uint32_t offb = (k >> 2) * (FB_QT / 2) + (k & 3) * 32;
-          tc_mma_f16(tS, make_sdesc(ak + offa, 16, 1024), make_sdesc(bq + offb, 16, 1024), idesc_s,
-                     k != 0 ? 1u : 0u);
-          tc_mma_f16(tDP, make_sdesc(av + offa, 16, 1024), make_sdesc(bd + offb, 16, 1024),
-                     idesc_s, k != 0 ? 1u : 0u);
+          const uint32_t offa = ((k >> 2) * FA_ATOM + (k & 3) * 32) >> 4;
+          const uint32_t offb = ((k >> 2) * (FB_QT / 2) + (k & 3) * 32) >> 4;
+          tc_mma_f16_w(tS, dk0 + offa, dq0 + offb, idesc_s, k != 0 ? 1u : 0u);
+          tc_mma_f16_w(tDP, dv0 + offa, ddo0 + offb, idesc_s, k != 0 ? 1u : 0u);
         }
-        tc_commit(&sdp_full[it & 1]);
+        tc_commit_w(&sdp_full[it & 1]);
       };
       if (n_it > 0) issue_sdp(0);
       for (int it = 0; it < n_it; ++it) {
@@ -987,19 +990,18 @@ __global__ void __launch_bounds__(384, 1)
         const int qs = it % FB_QST;
         const uint32_t bq = smem_u32(sQ + qs * FB_QT), bd = smem_u32(sDO + qs * FB_QT);
         const uint32_t tPt = tmem_base + s * 128, tDSt = tPt + 64;
+        const uint64_t ddo0 = make_sdesc(bd, FB_QT / 2, 1024), dq0 = make_sdesc(bq, FB_QT / 2, 1024);
 #pragma unroll
         for (int k = 0; k < FB_BQ / 16; ++k) {  // dV += P^T dO, dK += dS^T Q (A in TMEM, K = q)
           // queries 16k.. sit at column 32*(k/2) + 8*(k%2) (each warpgroup's slab)
           const uint32_t offa = (k >> 1) * 32 + (k & 1) * 8;
-          const uint32_t offb = k * 2048;
-          tc_mma_f16_ts(tDV, tPt + offa, make_sdesc(bd + offb, FB_QT / 2, 1024), idesc_acc,
-                        (it | k) != 0 ? 1u : 0u);
-          tc_mma_f16_ts(tDK, tDSt + offa, make_sdesc(bq + offb, FB_QT / 2, 1024), idesc_acc,
-                        (it | k) != 0 ? 1u : 0u);
+          const uint32_t offb = (k * 2048) >> 4;
+          tc_mma_f16_ts_w(tDV, tPt + offa, ddo0 + offb, idesc_acc, (it | k) != 0 ? 1u : 0u);
+          tc_mma_f16_ts_w(tDK, tDSt + offa, dq0 + offb, idesc_acc, (it | k) != 0 ? 1u : 0u);
         }
-        tc_commit(&qd_empty[qs]);
+        tc_commit_w(&qd_empty[qs]);
       }
-      tc_commit(acc_done);
+      tc_commit_w(acc_done);
     }
   } else if (warp >= 4) {
     // two softmax warpgroups: warps w and w + 4 share TMEM lanes 32 (w % 4) ..
@@ -1173,7 +1175,7 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // whole warp; elect.sync issues (ptx.cuh tc_mma_f16_w)
       constexpr uint32_t idesc_s = make_idesc_bf16(FA_BM, FQ_BK, false, false);   // 128 x 64
       constexpr uint32_t idesc_dq = make_idesc_bf16(FA_BM, FA_D, false, true);    // 128 x 128
       const uint32_t aq = smem_u32(sQ), ado = smem_u32(sDO);
@@ -1184,16 +1186,16 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         const uint32_t bk = smem_u32(sK + s * FQ_KT), bv = smem_u32(sV + s * FQ_KT);
         const uint32_t tS = tmem_base + (j % 3) * 128, tDP = tS + 64;
+        const uint64_t dq0 = make_sdesc(aq, 16, 1024), ddo0 = make_sdesc(ado, 16, 1024);
+        const uint64_t dk0 = make_sdesc(bk, 16, 1024), dv0 = make_sdesc(bv, 16, 1024);
 #pragma unroll
         for (int k = 0; k < FA_D / 16; ++k) {  // S = Q K^T, dP = dO V^T  (K = d)
-          const uint32_t offa = (k >> 2) * FA_ATOM + (k & 3) * 32;
-          const uint32_t offb = (k >> 2) * (FQ_KT / 2) + (k & 3) * 32;
-          tc_mma_f16(tS, make_sdesc(aq + offa, 16, 1024), make_sdesc(bk + offb, 16, 1024), idesc_s,
-                     k != 0 ? 1u : 0u);
-          tc_mma_f16(tDP, make_sdesc(ado + offa, 16, 1024), make_sdesc(bv + offb, 16, 1024),
-                     idesc_s, k != 0 ? 1u : 0u);
+          const uint32_t offa = ((k >> 2) * FA_ATOM + (k & 3) * 32) >> 4;
+          const uint32_t offb = ((k >> 2) * (FQ_KT / 2) + (k & 3) * 32) >> 4;
+          tc_mma_f16_w(tS, dq0 + offa, dk0 + offb, idesc_s, k != 0 ? 1u : 0u);
+          tc_mma_f16_w(tDP, ddo0 + offa, dv0 + offb, idesc_s, k != 0 ? 1u : 0u);
         }
-        tc_commit(&sdp_full[j % 3]);
+        tc_commit_w(&sdp_full[j % 3]);
       };
       issue_sdp(0);
       if (n_kt > 1) issue_sdp(1);
@@ -1205,14 +1207,14 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         const int s = j % FQ_STAGES;
         const uint32_t bk = smem_u32(sK + s * FQ_KT), tDS = tmem_base + (j % 3) * 128;
+        const uint64_t dkm = make_sdesc(bk, FQ_KT / 2, 1024);
 #pragma unroll
         for (int k = 0; k < FQ_BK / 16; ++k)  // dQ += dS K  (dS in TMEM; K MN-major, LBO 8 KB)
-          tc_mma_f16_ts(tDQ, tDS + (k >> 1) * 32 + (k & 1) * 8,
-                        make_sdesc(bk + k * 2048, FQ_KT / 2, 1024), idesc_dq,
-                        (j | k) != 0 ? 1u : 0u);
-        tc_commit(&kv_empty[s]);
+          tc_mma_f16_ts_w(tDQ, tDS + (k >> 1) * 32 + (k & 1) * 8, dkm + ((k * 2048) >> 4),
+                          idesc_dq, (j | k) != 0 ? 1u : 0u);
+        tc_commit_w(&kv_empty[s]);
       }
-      tc_commit(acc_done);
+      tc_commit_w(acc_done);
     }
   } else if (warp >= 4) {
     // two softmax warpgroups: key columns [0, 32) and [32, 64) of every step
