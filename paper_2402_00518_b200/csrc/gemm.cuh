@@ -1010,14 +1010,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader only)
-    if (leader && lane == 0) {
+    // The whole warp runs the loop (descriptors in uniform registers) and
+    // elect.sync issues each tcgen05 instruction; lane 0 alone consumes the
+    // tile schedule and broadcasts it.
+    if (leader) {
       constexpr uint32_t idesc = make_idesc_bf16(256, GEMM_BN, A_MN, B_MN);
       int s = 0;
       uint32_t ph = 0;
       int acc = 0;
       uint32_t acc_ph = 0;
-      for (int tile = first_tile(false); tile >= 0 && tile < num_tiles;
-           tile = next_tile(tile, false)) {
+      auto mma_tile = [&](int prev, bool first) -> int {
+        int t = 0;
+        if (lane == 0) t = first ? first_tile(false) : next_tile(prev, false);
+        return __shfl_sync(0xffffffffu, t, 0);
+      };
+      for (int tile = mma_tile(0, true); tile >= 0 && tile < num_tiles;
+           tile = mma_tile(tile, false)) {
         mbar_wait(&tempty[acc], acc_ph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * GEMM_BN;
@@ -1035,16 +1043,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
               const uint32_t bh = b_addr + hh * 16384;
               const uint64_t bd = B_MN ? make_sdesc(bh + k * 2048, 8192, 1024)
                                        : make_sdesc(bh + k * 32, 16, 1024);
-              tc_mma_f16_2sm(d_tmem + hh * GEMM_BN, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+              tc_mma_f16_2sm_w(d_tmem + hh * GEMM_BN, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
             }
           }
-          tc_commit_2sm(&empty[s], 0x3);
+          tc_commit_2sm_w(&empty[s], 0x3);
           if (++s == G2_STAGES) {
             s = 0;
             ph ^= 1;
           }
         }
-        tc_commit_2sm(&tfull[acc], 0x3);
+        tc_commit_2sm_w(&tfull[acc], 0x3);
         if (++acc == C::NACC) {
           acc = 0;
           acc_ph ^= 1;
