@@ -213,3 +213,36 @@ def test_full_size_long_k_equals_sum_of_short_k_shards(gpu_lib, name):
         errs[k] = ((a - b).norm() / b.norm()).item()
         assert errs[k] <= 3e-4, (k, errs[k])
     print(name, {k: f"{e:.1e}" for k, e in errs.items()})
+
+
+def test_full_size_bench_path_equals_plain_step(gpu_lib):
+    """The bench's launch configuration at full size (70B head, 65 536 tokens,
+    the fused ZeRO-1 path at world 1: gradient rows stored by the scatter
+    epilogues into the arena, peer barrier, sharded Adam storing the operands)
+    gives bitwise the losses and updated parameters of the plain path
+    (ee_tune_step + ee_adam_update), which the tests above pin to the oracle."""
+    from paper_2402_00518_b200.parallel import ShardedDPHeads
+    ee = gpu_lib
+    cfg = _one_exit("70b")
+    n = cfg.tokens
+    spec = ee.HeadSpec(cfg.hidden, cfg.vocab, cfg.ffn, 1, cfg.arch)
+    src = [{k: v for k, v in S.head_params(cfg, device="cuda")[0].items()}]
+    hidden = [h.contiguous() for h in S.hidden_states(cfg, n, device="cuda")]
+    targets = S.targets(cfg, n, device="cuda")
+    plain = ee.ExitHeads(spec, n)
+    plain.init("copy", copy_src=src, src_dtype=torch.float32)
+    lp = plain.step(hidden, targets).clone()
+    plain.adam(1e-4)
+    torch.cuda.synchronize()
+    ops = {k: v.clone() for k, v in plain.operand[0].items()}
+    del plain
+    torch.cuda.empty_cache()
+    heads = ShardedDPHeads(spec, n, 0, 1)
+    heads.connect_local([heads])
+    heads.init("copy", copy_src=src, src_dtype=torch.float32)
+    ls = heads.step(hidden, targets, 1e-4).clone()
+    torch.cuda.synchronize()
+    assert heads.status() == (0, -1)
+    assert torch.equal(lp, ls), (lp, ls)
+    for k, v in ops.items():
+        assert torch.equal(heads.operand[0][k], v), k
