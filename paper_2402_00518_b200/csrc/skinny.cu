@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(32 * SK_WARPS * SK_KS) skinny_kernel(SkinnyArg
       const long long o = (long long)tk * a.ldo + n;
       if constexpr (MODE == SK_SWIGLU) {
         const float v = d0[e], u = d1[e];
-        a.outb[o] = __float2bfloat16_rn(v / (1.0f + __expf(-v)) * u);
+        a.outb[o] = __float2bfloat16_rn(__fdividef(v, 1.0f + __expf(-v)) * u);
       } else if constexpr (MODE == SK_RESID) {
         a.out[o] = d0[e] + __bfloat162float(a.resid[(long long)tk * a.ldr + n]);
       } else {
