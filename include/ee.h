@@ -87,8 +87,10 @@ typedef enum { EE_INIT_COPY = 0, EE_INIT_RANDOM = 1 } ee_init;
  *             w_t = c_t = max softmax probability of the exit at token t,
  *             detached (a constant in the backward); L_i = sum_t c_t loss_t /
  *             sum_t c_t (normalisation: DESIGN.md A17).  Needs all tokens of
- *             the batch in one call (ee_tune_step without valid_count, or the
- *             ee_vp_* phases); a DP shard returns EE_ERR_UNSUPPORTED.
+ *             the batch in one call (ee_tune_step without valid_count, the
+ *             ee_vp_* phases, or ee_tune_step with a communicator, which
+ *             normalises by the global sum); a DP shard with valid_count
+ *             returns EE_ERR_UNSUPPORTED.
  * CONFIDENCE_SUM: the same weights, normaliser left to the caller (data
  *             parallelism: sum_t c_t spans every rank's tokens): loss_out =
  *             sum_t c_t loss_t, grads = gradient of alpha sum_t c_t loss_t,
@@ -123,7 +125,9 @@ typedef enum { EE_DTYPE_BF16 = 0, EE_DTYPE_F32 = 1 } ee_dtype;
  *               the rows [vocab_begin, vocab_end) of W_out held by this call
  *               (a vocab-parallel shard, 0 <= begin < end <= V, width a
  *               multiple of 8).  ee_tune_step needs the full vocabulary
- *               [0, V); shards are driven through the ee_vp_* phases.
+ *               [0, V) unless it runs with a vocab-parallel communicator
+ *               (EE_COMM_VP); shards can also be driven through the ee_vp_*
+ *               phases.
  *  token_weighting  ee_token_weighting.
  *  n_heads, n_kv_heads, seq_len, rope_theta
  *               LAYER only (ignored otherwise): query heads (hidden =
