@@ -409,6 +409,8 @@ def run_pipeline(args, cfg, world, rank, local, torch, dist, ee, S):
     lb, le = min(Ltot, rank * per), min(Ltot, (rank + 1) * per)
     mine = [i for i, a in enumerate(cfg.after) if lb < a <= le]
     N = cfg.tokens
+    if args.micro <= 0:
+        args.micro = 1 if world == 1 else min(N // T, 2 * world)
     if N % (args.micro * T):
         raise SystemExit(f"{N} tokens do not split into {args.micro} microbatches of whole "
                          f"{T}-token sequences")
@@ -620,8 +622,9 @@ def main():
                          "distributed softmax-CE (configs[3]: --config 70b --parallel vp); pp = "
                          "the paper's forward-communication-only pipeline with the frozen "
                          "backbone's partial forward (P:294-303, P:260; e.g. --config 13b_q)")
-    ap.add_argument("--micro", type=int, default=8,
-                    help="pp: microbatches per step (whole 2048-token sequences each)")
+    ap.add_argument("--micro", type=int, default=0,
+                    help="pp: microbatches per step (whole 2048-token sequences each); 0 = one "
+                         "per step on one stage (larger GEMMs), 2 x stages otherwise (bubble)")
     args = ap.parse_args()
     launch_ranks(args)
 
