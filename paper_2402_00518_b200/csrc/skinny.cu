@@ -66,19 +66,38 @@ __global__ void __launch_bounds__(32 * SK_WARPS * SK_KS) skinny_kernel(SkinnyArg
   // K slices interleaved in 32 * SK_UNROLL-wide blocks
   constexpr int KB = 32 * SK_UNROLL;
   int k = ks * KB;
-  for (; k + KB <= a.K; k += SK_KS * KB) {
-    uint4 wv[SK_UNROLL], uv[SK_UNROLL], xv[SK_UNROLL], xw[SK_UNROLL];
+  // software-pipelined: block i + 1's loads are issued before block i's MMAs
+  // (registers carried across iterations), so ptxas cannot interleave loads
+  // and uses and 2 x SK_UNROLL weight loads per thread stay in flight
+  uint4 wv[SK_UNROLL], uv[SK_UNROLL], xv[SK_UNROLL], xw[SK_UNROLL];
+  auto load_block = [&](int kk, uint4 (&w)[SK_UNROLL], uint4 (&u1)[SK_UNROLL],
+                        uint4 (&x0)[SK_UNROLL], uint4 (&x1)[SK_UNROLL]) {
 #pragma unroll
     for (int u = 0; u < SK_UNROLL; ++u) {
-      wv[u] = ld_stream(w0 + k + 32 * u);
-      if (MODE == SK_SWIGLU) uv[u] = ld_stream(w1 + k + 32 * u);
-      xv[u] = tok ? __ldg(reinterpret_cast<const uint4*>(xr + k + 32 * u)) : zero;
-      xw[u] = tok1 ? __ldg(reinterpret_cast<const uint4*>(xr1 + k + 32 * u)) : zero;
+      w[u] = ld_stream(w0 + kk + 32 * u);
+      if (MODE == SK_SWIGLU) u1[u] = ld_stream(w1 + kk + 32 * u);
+      x0[u] = tok ? __ldg(reinterpret_cast<const uint4*>(xr + kk + 32 * u)) : zero;
+      x1[u] = tok1 ? __ldg(reinterpret_cast<const uint4*>(xr1 + kk + 32 * u)) : zero;
     }
+  };
+  if (k + KB <= a.K) load_block(k, wv, uv, xv, xw);
+  for (; k + KB <= a.K; k += SK_KS * KB) {
+    uint4 wn[SK_UNROLL], un[SK_UNROLL], xn[SK_UNROLL], xm[SK_UNROLL];
+    const bool more = k + SK_KS * KB + KB <= a.K;
+    if (more) load_block(k + SK_KS * KB, wn, un, xn, xm);
 #pragma unroll
     for (int u = 0; u < SK_UNROLL; ++u) {
       mma_chunk(d0, xv[u], xw[u], wv[u]);
       if (MODE == SK_SWIGLU) mma_chunk(d1, xv[u], xw[u], uv[u]);
+    }
+    if (more) {
+#pragma unroll
+      for (int u = 0; u < SK_UNROLL; ++u) {
+        wv[u] = wn[u];
+        if (MODE == SK_SWIGLU) uv[u] = un[u];
+        xv[u] = xn[u];
+        xw[u] = xm[u];
+      }
     }
   }
   if (k < a.K) {  // this slice's partial last block (K % 8 == 0; zeros past K)
