@@ -109,14 +109,20 @@ class ClockSampler:
 
 
 def step_flops(cfg, n):
-    """Algorithmic FLOPs of one step: 6hV (+18hF for MLP) per
-    token per exit; Embedding exits have no dz GEMM (4hV).  Layer exits add
+    """Algorithmic FLOPs of one step: 6hV per token per exit
+    (Embedding exits have no dz GEMM: 4hV), +14hF for an MLP exit (6hF
+    forward, dM / dW_down / dW_gate|up 8hF backward: du is not needed, its
+    only consumer dg_a is formed from the dW GEMM's accumulators, DESIGN.md
+    §3 A28) and +18hF for a Layer exit (du feeds the attention
+    block's gradient).  Layer exits add
     the attention projections, 6 (2h^2 + 2h hkv), and the causal attention
     core, 6h(T+1)/... = 2h(T+1) forward + 4h(T+1) backward (dV, dP, dQ, dK;
     the recomputed S and dP are not counted)."""
     h, V, F = cfg.hidden, cfg.vocab, cfg.ffn
     per = (4 if cfg.arch == "embedding" else 6) * h * V
-    if cfg.arch in ("mlp", "layer"):
+    if cfg.arch == "mlp":
+        per += 14 * h * F
+    if cfg.arch == "layer":
         per += 18 * h * F
     if cfg.arch == "layer":
         hkv = 128 * (cfg.n_kv_heads or cfg.n_heads)

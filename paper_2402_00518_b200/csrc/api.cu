@@ -234,7 +234,10 @@ Layout make_layout(const ee_head_config* c, long long n) {
   if (c->arch != EE_ARCH_EMBEDDING) {
     L.z = take(2 * (size_t)n * h);
     L.dz = take(4 * (size_t)n * h);
-    L.dgp = take(4 * (size_t)(L.nparts > 0 ? L.nparts : 1) * h);
+    // column-sum partials: RMSNorm row blocks, or (MLP exits) dW-GEMM column blocks
+    size_t gp = (size_t)(L.nparts > 0 ? L.nparts : 1);
+    if (c->arch == EE_ARCH_MLP && n > 0) gp = std::max(gp, (size_t)((2 * F + GEMM_BN - 1) / GEMM_BN));
+    L.dgp = take(4 * gp * h);
     L.ry = take(4 * n);
   }
   L.u1 = L.r1 = L.q = L.k = L.v = L.o = L.lse2 = L.x1 = L.da = L.dq = L.dk = L.dv = L.dvec = 0;
@@ -908,8 +911,11 @@ ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee
     EE_CUDA(gemm_run(af ? EPI_F32_ADAM : EPI_F32, true, false, A, Bm, nullptr, B_PLAIN, 0, a,
                      st));
   }
-  // a12: du = dA W_gate + dB W_up  (K concatenation over the two weights) -> B.dz
-  {
+  // a12: du = dA W_gate + dB W_up  (K concatenation over the two weights) -> B.dz.
+  // Layer exits only: du feeds dx1 (the attention block's gradient).  An MLP
+  // exit needs du only for dg_a = sum_t du_t (.) x^_t, which the dW GEMM below
+  // produces from its own accumulators (gain identity, DESIGN.md §3 A28).
+  if (layer) {
     GemmArgs a = base_args((int)n, h, 2 * F);
     a.out0 = B.dz;
     a.ldo = h;
@@ -918,11 +924,26 @@ ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee
     EE_CUDA(gemm_run(EPI_F32, true, false, A, B0, &B1, B_KSPLIT, F, a, st));
   }
   // a12 (after du, which reads W_gate / W_up): [dW_gate; dW_up]^T = u^T [dA|dB]  (A = u^T K-major copy, B = [dA|dB]
-  // MN-major), stored transposed; output columns split at F over the two grads
+  // MN-major), stored transposed; output columns split at F over the two grads.
+  // MLP exits: A = x^T (x^ = x r, RMSNorm without its gain) and the epilogue
+  // scales row j by g_a[j] (u = g_a (.) x^) and emits, per 256-column block,
+  // sum_f W[f][j] acc[j][f] = the block's share of dg_a[j] (a13 without du).
+  const int gblocks = (2 * F + GEMM_BN - 1) / GEMM_BN;
   {
-    { Prof p_("transpose_u", st, 0, 0, 4.0 * n * h);
-    EE_CUDA(launch_transpose_bf16(B.u, B.uT, n, h, B.L.ldT, st)); }
+    if (layer) {
+      Prof p_("transpose_u", st, 0, 0, 4.0 * n * h);
+      EE_CUDA(launch_transpose_bf16(B.u, B.uT, n, h, B.L.ldT, st));
+    } else {
+      Prof p_("transpose_xhat", st, 0, 0, 4.0 * n * h + 4.0 * n);
+      EE_CUDA(launch_transpose_bf16(x, B.uT, n, h, B.L.ldT, st, B.rx));
+    }
     GemmArgs a = base_args(h, 2 * F, (int)n);
+    if (!layer) {
+      a.row_scale = (const float*)P.g_a;
+      a.gain_part = B.dgp;
+      a.gain_w0 = (const __nv_bfloat16*)P.w_gate;
+      a.gain_w1 = (const __nv_bfloat16*)P.w_up;
+    }
     a.out0 = (float*)G.w_gate;
     a.out1 = (float*)G.w_up;
     a.n_split = F;
@@ -935,18 +956,17 @@ ee_status phase_exit_backward(const ee_head_config* cfg, const Bufs& B, const ee
     EE_CUDA(gemm_run(af ? EPI_F32T_ADAM : EPI_F32T, true, false, A, Bm, nullptr, B_PLAIN, 0, a,
                      st));
   }
-  if (!layer) {
-    // a13: dg_a = sum_t du_t * xhat_t  (no dx: frozen backbone)
-    { Prof p_("a13_gain_grad", st, 0, 0, 6.0 * n * h);
-    EE_CUDA(launch_gain_grad(B.dz, x, B.rx, B.dgp, n, h, NORM_RPB, st)); }
-  } else {
+  if (layer) {
     // a13 (Layer): dg_a and dx1 = dy + RMSNorm_a^T(du), written over dy in place
     Prof p_("a13_rmsnorm_bwd_resid", st, 0, 0, 14.0 * n * h);
     EE_CUDA(launch_rmsnorm_bwd(B.dz, B.x1, true, B.rx, (const float*)P.g_a, B.dy, B.dgp, n, h,
                                NORM_RPB, st, B.dy));
   }
-  { Prof p_("reduce_cols", st, 0, 0, 4.0 * nparts * h);
-  EE_CUDA(launch_reduce_cols(B.dgp, nparts, h,
+  // a13: dg_a = column sums of the partials (RMSNorm-backward row blocks for
+  // Layer exits, dW-GEMM column blocks for MLP exits; no dx: frozen backbone)
+  const int gparts = layer ? nparts : (n > 0 ? gblocks : 0);
+  { Prof p_("reduce_cols", st, 0, 0, 4.0 * gparts * h);
+  EE_CUDA(launch_reduce_cols(B.dgp, gparts, h,
                              gs ? gs->p[0][0] : af ? B.gsc + h : (float*)G.g_a, accumulate,
                              st)); }
   if (layer) return layer_attn_backward(cfg, B, P, G, x, n, accumulate, st, gs, af, B.gsc + 2 * h);

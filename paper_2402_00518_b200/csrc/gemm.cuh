@@ -106,6 +106,18 @@ struct GemmArgs {
   int adam_on;
   AdamScal adam;
   AdamOut adam0, adam1;
+  // EPI_F32T / EPI_F32T_ADAM gain identity (MLP exits; DESIGN.md §3 A28):
+  // when row_scale != NULL every accumulator row m is
+  // multiplied by row_scale[m] before it is stored or updated (dW_gate|up =
+  // g_a (.) ([dA|dB]^T x^) when the A operand is x^ = x r), and, when
+  // gain_part != NULL, gain_part[nb * M + m] receives sum over the tile's
+  // columns n of gw(n)[n'][m] * acc[m][n] (unscaled; gw = gain_w0 for
+  // n < n_split, n' = n, else gain_w1, n' = n - n_split; bf16 [rows x M]):
+  // the pre-MLP gain's gradient sum_t du_t (.) x^_t without forming du.
+  const float* row_scale;
+  float* gain_part;
+  const __nv_bfloat16* gain_w0;
+  const __nv_bfloat16* gain_w1;
   const __nv_bfloat16* resid;
   long long ld_resid;
   __nv_bfloat16* outb;  // EPI_BF16 output (ldo)
@@ -342,12 +354,30 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
     // swapped so that A' is K-major (the fast UMMA path); the caller's output
     // is D'^T.  Thread `row` (m) writes out[n][m]: for each n the 32 threads of
     // a warp store 32 consecutive floats (one 128-byte line).
+    float gsum = 0.f;   // gain identity: this row's sum over the tile's columns
 #pragma unroll 1
     for (int c = 0; c < GEMM_BN / 32; ++c) {
       uint32_t v[32];
       tmem_ld_32x32b_x32(tb + c * 32, v);
       tmem_ld_wait();
       const int gn0 = nb * GEMM_BN + c * 32;
+      if (args.row_scale != nullptr && row_ok) {
+        // gw[n'][m] over the 32 threads of a warp (consecutive m) is one
+        // coalesced 64-byte segment per n
+        const float rs = args.row_scale[gm];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int gn = gn0 + j;
+          const float a = u2f(v[j]);
+          if (args.gain_part != nullptr && gn < args.N) {
+            const __nv_bfloat16* w = gn < args.n_split
+                                         ? args.gain_w0 + (long long)gn * args.M + gm
+                                         : args.gain_w1 + (long long)(gn - args.n_split) * args.M + gm;
+            gsum = fmaf(__bfloat162float(*w), a, gsum);
+          }
+          v[j] = __float_as_uint(a * rs);
+        }
+      }
       if (EPI == EPI_F32T_ADAM && row_ok && gn0 < args.N) {
         // fused Adam, element (row n, column m): 16 columns per batch, all 48
         // state loads issued before the updates and stores (each is a
@@ -420,6 +450,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
         }
       }
     }
+    if (args.gain_part != nullptr && row_ok) args.gain_part[(long long)nb * args.M + gm] = gsum;
   } else if constexpr (EPI == EPI_SWIGLU_FWD) {
     const int F = args.ffn;
 #pragma unroll 1

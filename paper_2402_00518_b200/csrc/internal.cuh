@@ -108,7 +108,8 @@ cudaError_t launch_vp_finalize(const long long* key_global, const float* sums,
                                float* loss_part, float* wsum_part, int nblocks, cudaStream_t s);
 
 cudaError_t launch_transpose_bf16(const __nv_bfloat16* src, __nv_bfloat16* dst, long long R, int C,
-                                  long long ldd, cudaStream_t s);
+                                  long long ldd, cudaStream_t s,
+                                  const float* rscale = nullptr);
 
 cudaError_t launch_first_exit(const float* const* conf, int E, long long n, float tau,
                               int32_t* out, cudaStream_t s);

@@ -727,9 +727,11 @@ cudaError_t launch_first_exit(const float* const* conf, int E, long long n, floa
 // 128-byte coalesced reads and writes.  Gives the weight-gradient GEMMs a
 // K-major copy of their token-major activation operand (u, z, dy), so their
 // A operand takes the K-major UMMA path.
+// dst[c][r] = src[r][c] (rscale == NULL) or bf16(src[r][c] * rscale[r]) -- the
+// latter is x^ = x r (RMSNorm before its gain), transposed, for the gain identity
 __global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ src,
                                       __nv_bfloat16* __restrict__ dst, long long R, int C,
-                                      long long ldd) {
+                                      long long ldd, const float* __restrict__ rscale) {
   // 64 x 64 tile; 16-byte global loads and stores (8 bf16 per access), rows of
   // the smem tile padded to 33 words so the column gathers are 2-way conflicted
   __shared__ uint32_t tile[64][33];
@@ -753,6 +755,12 @@ __global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ src,
         for (int k = 0; k < 8; ++k) e[k] = (c + k < C) ? src[r * C + c + k] : __float2bfloat16_rn(0.f);
 #pragma unroll
         for (int k = 0; k < 4; ++k) w[k] = *reinterpret_cast<const uint32_t*>(&e[2 * k]);
+      }
+      if (rscale != nullptr) {
+        const float rr = rscale[r];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          w[k] = pack_bf16(__uint_as_float(w[k] << 16) * rr, __uint_as_float(w[k] & 0xFFFF0000u) * rr);
       }
     }
 #pragma unroll
@@ -786,10 +794,10 @@ __global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ src,
 }
 
 cudaError_t launch_transpose_bf16(const __nv_bfloat16* src, __nv_bfloat16* dst, long long R, int C,
-                                  long long ldd, cudaStream_t s) {
+                                  long long ldd, cudaStream_t s, const float* rscale) {
   if (R == 0 || C == 0) return cudaSuccess;
   dim3 grid((C + 63) / 64, (unsigned)((R + 63) / 64));
-  transpose_bf16_kernel<<<grid, 256, 0, s>>>(src, dst, R, C, ldd);
+  transpose_bf16_kernel<<<grid, 256, 0, s>>>(src, dst, R, C, ldd, rscale);
   return cudaGetLastError();
 }
 
