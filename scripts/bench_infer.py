@@ -18,13 +18,15 @@ h, V, F, E = cfg.hidden, cfg.vocab, cfg.ffn, cfg.exits
 heads = ee.ExitHeads(ee.HeadSpec(h, V, F, E, cfg.arch), max_tokens=4096, adam=False)
 heads.init("random", seed=1)
 w_bytes = 2 * (V * h + (3 * F * h if cfg.arch == "mlp" else 0))   # bf16 operands per exit
-for M in (1, 8, 16, 64, 512):
+Ms = [int(v) for v in __import__('os').environ.get('EE_INFER_M', '1,8,16,64,512').split(',')]
+reps = int(__import__('os').environ.get('EE_INFER_REPS', '10'))
+for M in Ms:
     hidden = [x.cuda() for x in S.hidden_states(cfg, M)]
     for _ in range(3):
         heads.infer(hidden, 0.9)
     torch.cuda.synchronize()
     ts = []
-    for _ in range(10):
+    for _ in range(reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         heads.infer(hidden, 0.9)

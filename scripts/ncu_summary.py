@@ -19,10 +19,10 @@ import subprocess
 import sys
 from collections import OrderedDict
 
-# order of gemm_kernel launches within one MLP exit (api.cu; ds_mode recompute)
+# order of gemm_kernel launches within one MLP exit (api.cu; ds_mode recompute;
+# no a12_du GEMM since the gain identity, A28)
 MLP_GEMM_ORDER = ["a2_gateup_swiglu", "a3_down_resid", "a5_vocab_ce_stats", "a7_ds_recompute",
-                  "a8_dz", "a9_dw_out", "a11_dm_swiglu_bwd", "a11_dw_down", "a12_du",
-                  "a12_dw_gateup"]
+                  "a8_dz", "a9_dw_out", "a11_dm_swiglu_bwd", "a11_dw_down", "a12_dw_gateup"]
 
 
 def short(name):
