@@ -1392,7 +1392,8 @@ static ee_status infer_decode_exit(const ee_head_config* cfg, const Bufs& B,
     bool yf32 = false;
     if (cfg->arch == EE_ARCH_MLP) {
       { Prof p_("dec_rmsnorm_a", st, 0, 0, 4.0 * n * h + 4.0 * h);
-      EE_CUDA(launch_rmsnorm_fwd(x, false, (const float*)P.g_a, cfg->norm_eps, B.u, B.rx, n, h, st)); }
+      EE_CUDA(launch_rmsnorm_fwd(x, false, (const float*)P.g_a, cfg->norm_eps, B.u, B.rx, n, h, st,
+                                 nullptr, true)); }
       {
         SkinnyArgs a{};
         a.x = B.u; a.ldx = h; a.W0 = (const __nv_bfloat16*)P.w_gate;
@@ -1411,7 +1412,8 @@ static ee_status infer_decode_exit(const ee_head_config* cfg, const Bufs& B,
       yf32 = true;
     }
     { Prof p_("dec_rmsnorm_f", st, 0, 0, 4.0 * n * h + 4.0 * h);
-    EE_CUDA(launch_rmsnorm_fwd(yin, yf32, (const float*)P.g_f, cfg->norm_eps, B.z, B.ry, n, h, st)); }
+    EE_CUDA(launch_rmsnorm_fwd(yin, yf32, (const float*)P.g_f, cfg->norm_eps, B.z, B.ry, n, h, st,
+                               nullptr, true)); }
     z = B.z;
   }
   SkinnyArgs a{};

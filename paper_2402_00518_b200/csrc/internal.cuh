@@ -3,9 +3,38 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include "gemm.cuh"
 
 namespace ee {
+
+// Launch with programmatic stream serialization (PDL, the decode chain): the
+// kernel may start while the previous kernel of the stream drains, so it must
+// call griddep_wait() (ptx.cuh) before touching memory that kernel writes or
+// reads.  EE_PDL=0 launches normally (A/B).
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("EE_PDL");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // Device status word at the head of the workspace (ee_get_status).
 struct DevStatus {
@@ -51,7 +80,7 @@ struct PeerSig {
 // (ag != NULL: out is ignored and each z row goes to every ag->p[q])
 cudaError_t launch_rmsnorm_fwd(const void* in, bool in_f32, const float* g, float eps,
                                __nv_bfloat16* out, float* r, long long n, int h, cudaStream_t s,
-                               const PeerRows* ag = nullptr);
+                               const PeerRows* ag = nullptr, bool pdl = false);
 // rmsnorm backward: dz fp32, y (bf16/fp32), r, g -> dy bf16 (nullable), dg partials.
 // dz = sum over nslots slabs dz + k*slot_stride, k = 0..nslots-1 in order
 // (the fused reduce-scatter's owner-side sum).

@@ -95,6 +95,8 @@ __global__ void rmsnorm_fwd_kernel(const TIn* __restrict__ in, const float* __re
   __shared__ float red[33];
   const long long row = blockIdx.x;
   const int nchunk = h / 8;
+  griddep_launch();  // no-ops unless launched with PDL (the decode chain)
+  griddep_wait();
   float x[NORM_CHUNKS][8];
   float ss = 0.f;
 #pragma unroll
@@ -130,11 +132,18 @@ __global__ void rmsnorm_fwd_kernel(const TIn* __restrict__ in, const float* __re
 
 cudaError_t launch_rmsnorm_fwd(const void* in, bool in_f32, const float* g, float eps,
                                __nv_bfloat16* out, float* r, long long n, int h, cudaStream_t s,
-                               const PeerRows* ag) {
+                               const PeerRows* ag, bool pdl) {
   if (n == 0) return cudaSuccess;
   const int t = norm_threads(h);
   PeerRows pr{};
   if (ag) pr = *ag;
+  if (pdl) {
+    if (in_f32)
+      return launch_pdl(rmsnorm_fwd_kernel<float>, dim3((unsigned)n), dim3(t), 0, s,
+                        (const float*)in, g, eps, out, r, h, pr);
+    return launch_pdl(rmsnorm_fwd_kernel<__nv_bfloat16>, dim3((unsigned)n), dim3(t), 0, s,
+                      (const __nv_bfloat16*)in, g, eps, out, r, h, pr);
+  }
   if (in_f32)
     rmsnorm_fwd_kernel<float><<<(unsigned)n, t, 0, s>>>((const float*)in, g, eps, out, r, h, pr);
   else
@@ -704,6 +713,7 @@ struct ConfPtrs {
 };
 __global__ void first_exit_kernel(ConfPtrs c, int E, long long n, float tau, int32_t* out) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  griddep_wait();  // PDL launch (launch_first_exit)
   if (t >= n) return;
   int f = -1;
   for (int i = 0; i < E; ++i)
@@ -718,8 +728,8 @@ cudaError_t launch_first_exit(const float* const* conf, int E, long long n, floa
                               int32_t* out, cudaStream_t s) {
   ConfPtrs c;
   for (int i = 0; i < E && i < 64; ++i) c.p[i] = conf[i];
-  first_exit_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c, E, n, tau, out);
-  return cudaGetLastError();
+  return launch_pdl(first_exit_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, c, E,
+                    n, tau, out);
 }
 
 // ---------------------------------------------------------------- transpose

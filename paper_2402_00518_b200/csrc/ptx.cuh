@@ -59,6 +59,20 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
       : "memory");
 }
 
+// ---------------------------------------------------------------- PDL
+// Programmatic dependent launch (kernels launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): griddep_wait blocks until
+// the preceding kernel of the stream has completed and its writes are visible
+// (a no-op without a programmatic dependency); griddep_launch lets the next
+// kernel of the stream start launching (its CTAs then run their prologue --
+// e.g. weight prefetch -- until their own griddep_wait).
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");

@@ -50,3 +50,41 @@ def test_exit_infer_matches_oracle(gpu_lib, arch, h, V, F, n):
             assert fg[t] == first_o[t], t
         expect_gpu = next((i for i in range(3) if cfg_np[i, t] >= tau), -1)
         assert fg[t] == expect_gpu
+
+
+@pytest.mark.parametrize("arch,h,V,F,n", [("mlp", 2048, 8008, 5760, 1), ("mlp", 2048, 8008, 5760, 16),
+                                          ("mlp", 1088, 4104, 2944, 11), ("norm", 4096, 32000, 0, 8),
+                                          ("embedding", 4096, 32000, 0, 2)])
+def test_exit_infer_decode_stream_k(gpu_lib, arch, h, V, F, n):
+    """Decode shapes whose (row block, k chunk) units outnumber the CTAs, so the
+    stream-K ranges split row blocks between CTAs (skinny.cu fix-up pool; K
+    tails: F = 5760, 2944 and h = 1088 are not multiples of the 256-wide k chunk):
+    oracle parity, and two calls bitwise equal."""
+    ee = gpu_lib
+    E = 2
+    cfg = S.Cfg(name="dec", hidden=h, vocab=V, ffn=F, arch=arch, tokens=n, layers=E,
+                after=list(range(1, E + 1)), init="random", seed=77)
+    hidden = S.hidden_states(cfg, n)
+    params = S.head_params(cfg)
+    c = ee.make_config(h, V, F, E, arch)
+    ops = [{k: (v.cuda().float() if k.startswith("g_") else v.cuda().to(torch.bfloat16))
+            for k, v in p.items()} for p in params]
+    ws = torch.zeros(ee.ee_workspace_size(c, n), dtype=torch.uint8, device="cuda")
+    p64 = [{k: to_f64(v) for k, v in p.items()} for p in params]
+    outs = []
+    for _ in range(2):
+        am = [torch.zeros(n, dtype=torch.int32, device="cuda") for _ in range(E)]
+        cf = [torch.zeros(n, device="cuda") for _ in range(E)]
+        first = torch.zeros(n, dtype=torch.int32, device="cuda")
+        ee.ee_exit_infer(c, [x.cuda() for x in hidden], ops, 0.5, am, cf, ws, first_exit=first)
+        torch.cuda.synchronize()
+        outs.append((am, cf, first))
+    for i in range(E):
+        assert torch.equal(outs[0][0][i], outs[1][0][i]) and torch.equal(outs[0][1][i], outs[1][1][i])
+    assert torch.equal(outs[0][2], outs[1][2])
+    am, cf, _ = outs[0]
+    _, cf_o, _ = O.exit_infer(arch, p64, [to_f64(x) for x in hidden], 0.5, 1e-5)
+    for i in range(E):
+        S_i = O.exit_forward(arch, p64[i], to_f64(hidden[i]), 1e-5)["S"]
+        check_argmax(am[i].cpu().numpy(), S_i)
+        assert np.max(np.abs(cf[i].cpu().numpy() - cf_o[i])) <= 2e-2
