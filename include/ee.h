@@ -474,11 +474,14 @@ ee_status ee_ipc_close(void* dev_ptr, uint64_t offset);
  * confidence reaches `threshold`, or -1 (threshold 1 disables early exits,
  * P:385).  hidden[i]: device bf16 [n_tokens x h]; outputs device [n_tokens].
  * n_tokens > 16 (or Layer exits): the tuning step's forward kernels (a1-a6).
- * n_tokens <= 16 (decode): weight-streaming "skinny" kernels (warp-level bf16
- * MMA over 128-bit streaming loads, fused SwiGLU / residual / per-block
- * online-softmax statistics) and a wide finalize; same results up to fp32
- * summation order.  No loss, no gradients.  Env EE_INFER_SKINNY=0 forces the
- * GEMM path. */
+ * n_tokens <= 16 (decode): weight-streaming "skinny" kernels (TMA-fed
+ * shared-memory ring, warp-level bf16 MMA, stream-K over one persistent CTA
+ * per SM, fused SwiGLU / residual / per-block online-softmax statistics,
+ * programmatic dependent launch) and a wide finalize; same results up to fp32
+ * summation order, bitwise reproducible call to call.  No loss, no gradients.
+ * The stream-K fix-up uses a library-global pool of 16 slots: at most 16
+ * decode calls may EXECUTE concurrently (calls on one stream never overlap).
+ * Env EE_INFER_SKINNY=0 forces the GEMM path, EE_PDL=0 plain launches. */
 ee_status ee_exit_infer(const ee_head_config* cfg, const void* const* hidden, int64_t n_tokens,
                         const ee_head_tensors* params, float threshold, int32_t* const* argmax_out,
                         float* const* conf_out, int32_t* first_exit, void* workspace,
