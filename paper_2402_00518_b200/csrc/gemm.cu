@@ -183,8 +183,8 @@ cudaError_t gemm_run(int epi, bool a_kmajor, bool b_kmajor, const Mat& A, const 
   // 256 x 512 pair tiles for the long-K GEMMs (EE_GEMM_WIDE=1): 25% fewer
   // operand bytes per FLOP on paper, but measured 7% slower per step at the
   // power cap (profiles/r01_wide_ab.log), so off by default
-  static const int wide_env = env_int("EE_GEMM_WIDE", 0);  // measured slower (profiles/r01_wide_ab.log)
-  const bool wide = cta_pair && wide_env && b_mode != B_PAIR && args.K >= 16384 &&
+  static const int wide_env = env_int("EE_GEMM_WIDE", 0);  // measured slower (profiles/r01_wide_ab.log); 2: any K (experiment)
+  const bool wide = cta_pair && wide_env && b_mode != B_PAIR && (args.K >= 16384 || wide_env == 2) &&
                     (epi == EPI_F32 || epi == EPI_F32T || epi == EPI_RESID);
   const int bn = (b_mode == B_PAIR) ? GEMM_BN / 2 : (wide ? 2 * GEMM_BN : GEMM_BN);
   args.n_blocks = (args.N + bn - 1) / bn;

@@ -79,7 +79,7 @@ struct GemmArgs {
   int m_blocks, n_blocks, k_blocks;
   int b_mode, b_ksplit, group_m;
   int hint_a, hint_b;
-  int epi_sleep;  // epilogue waits with a suspend-time hint instead of spinning
+  int epi_sleep;  // epilogue accumulator wait: 0 spin, 1 try_wait suspend hint, >= 2 poll + nanosleep(epi_sleep ns)
   int* tile_counter;  // CTA-pair kernel: dynamic tile schedule counter (zeroed per launch), or NULL
   int* wave_counter;  // CTA-pair kernel, static schedule: per-wave soft barrier counter, or NULL
   unsigned long long* trace;  // debug: per-tile (globaltimer << 8 | smid) at accumulator-ready, or NULL  // L2 policy of the A / B TMA loads: -1 none, 0 normal, 1 evict_last, 2 evict_first
@@ -809,7 +809,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tile_coords(args, tile, mb, nb);
       const int gm = mb * GEMM_BM + row;
       const bool row_ok = gm < args.M;
-      if (args.epi_sleep) mbar_wait_sleep(&tfull[acc], acc_ph); else mbar_wait(&tfull[acc], acc_ph);
+      if (args.epi_sleep >= 2)
+        mbar_wait_backoff(&tfull[acc], acc_ph, (uint32_t)args.epi_sleep);
+      else if (args.epi_sleep)
+        mbar_wait_sleep(&tfull[acc], acc_ph);
+      else
+        mbar_wait(&tfull[acc], acc_ph);
       tc_fence_after();
       const uint32_t tb = tmem_base + acc * GEMM_BN + (static_cast<uint32_t>(ew * 32) << 16);
       if (args.trace && threadIdx.x == 128) args.trace[tile] = trace_stamp();
@@ -1112,7 +1117,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
          tile = warp_tile(tile, false)) {
       int mb, nb;
       tile_coords(args, tile, mb, nb);
-      if (args.epi_sleep) mbar_wait_sleep(&tfull[acc], acc_ph); else mbar_wait(&tfull[acc], acc_ph);
+      if (args.epi_sleep >= 2)
+        mbar_wait_backoff(&tfull[acc], acc_ph, (uint32_t)args.epi_sleep);
+      else if (args.epi_sleep)
+        mbar_wait_sleep(&tfull[acc], acc_ph);
+      else
+        mbar_wait(&tfull[acc], acc_ph);
       tc_fence_after();
       const uint32_t tb = tmem_base + acc * GEMM_BN + (static_cast<uint32_t>(ew * 32) << 16);
       if (args.trace && threadIdx.x == 128 && rank == 0) args.trace[tile] = trace_stamp();

@@ -58,6 +58,28 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
       "r"(parity), "r"(10000000)
       : "memory");
 }
+// Non-blocking phase test, and a poll loop with a fixed back-off between tests.
+// mbar_wait_sleep's try_wait suspend hint compiles to NANOSLEEP.SYNCS, which
+// wakes on every mbarrier event of the CTA: in the GEMM (a barrier completes
+// every ~500 cycles) its loop still ran once per ~70 cycles per epilogue warp
+// and was 40% of all instructions the kernel issued (ncu source page,
+// profiles/r02z3_gemm_vs_cublas.md).  A plain nanosleep is not woken early.
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  while (!mbar_test(bar, parity)) __nanosleep(ns);
+}
 
 // ---------------------------------------------------------------- PDL
 // Programmatic dependent launch (kernels launched with
