@@ -1128,8 +1128,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       if (args.trace && threadIdx.x == 128 && rank == 0) args.trace[tile] = trace_stamp();
 #pragma unroll 1
       for (int hh = 0; hh < NB2; ++hh)
-        epilogue_tile<EPI>(args, tb + hh * GEMM_BN, mb * 256 + (int)rank * 128 + row,
-                           nb * NB2 + hh);
+        if ((nb * NB2 + hh) * GEMM_BN < args.N)  // a 512-wide tile's second half may lie past N
+          epilogue_tile<EPI>(args, tb + hh * GEMM_BN, mb * 256 + (int)rank * 128 + row,
+                             nb * NB2 + hh);
       tc_fence_before();
       mbar_arrive_cluster(acc ? te1 : te0);
       if (++acc == C::NACC) {

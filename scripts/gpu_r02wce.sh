@@ -1,0 +1,16 @@
+#!/bin/bash
+# r02wce: 256 x 512 tiles for the CE GEMMs (a5 stats, a7 dS; EE_GEMM_WIDE_CE=1): parity, then interleaved C4 / C2 A/B.
+TAG=${1:-r02wce}
+mkdir -p gpurun_out
+EE_GEMM_WIDE_CE=1 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_largen.py tests/test_gpu_fullsize.py -q -x > gpurun_out/${TAG}_pytest.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/${TAG}_pytest.log
+tail -2 gpurun_out/${TAG}_pytest.log
+for rep in 1 2; do
+  for w in 0 1; do
+    EE_GEMM_WIDE_CE=$w timeout 600 python bench.py --no-cpu-baseline --no-ds-ablation --no-e2e > gpurun_out/${TAG}_c4_w${w}_$rep.json 2>> gpurun_out/${TAG}.err
+    EE_GEMM_WIDE_CE=$w timeout 600 python bench.py --config 13b --dp-comm plain --no-cpu-baseline --no-ds-ablation --no-e2e > gpurun_out/${TAG}_c2_w${w}_$rep.json 2>> gpurun_out/${TAG}.err
+  done
+done
+for f in gpurun_out/${TAG}_c*.json; do python -c "
+import json; d=json.loads(open('$f').read().strip().splitlines()[-1])
+k=d['kernels']; print('$f', round(d['value']), round(d['ms_per_step'],1), d['clocks']['sm_mhz'], ' '.join(f'{n}:{v[\"tflops_exec\"]:.0f}' for n,v in k.items() if v.get('tflops_exec')))"; done
