@@ -1128,7 +1128,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       if (args.trace && threadIdx.x == 128 && rank == 0) args.trace[tile] = trace_stamp();
 #pragma unroll 1
       for (int hh = 0; hh < NB2; ++hh)
-        if ((nb * NB2 + hh) * GEMM_BN < args.N)  // a 512-wide tile's second half may lie past N
+        // a 512-wide tile's second half may lie past N (NB2 = 2 only: with B_PAIR
+        // the tile columns are 128 + 128 of two matrices and N counts one of them)
+        if (NB2 == 1 || (nb * NB2 + hh) * GEMM_BN < args.N)
           epilogue_tile<EPI>(args, tb + hh * GEMM_BN, mb * 256 + (int)rank * 128 + row,
                              nb * NB2 + hh);
       tc_fence_before();
