@@ -1041,7 +1041,8 @@ def main():
         pk = peaks["bf16_tflops_sustained"] if long_region else peaks["bf16_tflops"]
         roofline = {"bound": "tensor", "kernel": dom, "achieved": ach,
                     "peak": pk, "unit": "TFLOP/s",
-                    "frac": ach / pk, "traffic": traffic,
+                    "frac": ach / pk, "frac_of_burst": ach / peaks["bf16_tflops"],
+                    "traffic": traffic,
                     "algorithmic_flops_per_launch": per_launch_flops,
                     "peak_source": peaks["source"] + (
                         ", sustained (kernel timed inside a timed region of >= 1 s)" if long_region
