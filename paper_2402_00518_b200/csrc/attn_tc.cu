@@ -396,6 +396,11 @@ __device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsign
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
+__device__ __forceinline__ unsigned long long fmul2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
 
 namespace {
 constexpr int FA2_KST = 2, FA2_VST = 2;
@@ -1029,8 +1034,8 @@ __global__ void __launch_bounds__(384, 1)
       const int qpos0 = (q64_0 + it % per_head) * FB_BQ;
       float* L = sL + (it & 1) * FB_BQ;
       float* D = sD + (it & 1) * FB_BQ;
-      if (tid < 2 * FB_BQ) {
-        (tid < FB_BQ ? L : D)[tid & (FB_BQ - 1)] = stat_next;
+      if (tid < 2 * FB_BQ) {  // staged negated: the packed FMA / add below take -lse2, -Dv
+        (tid < FB_BQ ? L : D)[tid & (FB_BQ - 1)] = -stat_next;
         if (it + 1 < n_it) stat_next = stat_of(it + 1);
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
@@ -1043,20 +1048,45 @@ __global__ void __launch_bounds__(384, 1)
         tmem_ld_32x32b_x32(tDP + lane_off + c * 32, vp);
         tmem_ld_wait();
         uint32_t wp[16], wd[16];
+        // the causal / sequence-end mask only on the tiles that need it
+        // (CTA-uniform); packed f32x2 FMA / add / mul with the same per-element
+        // roundings as fmaf / fadd / fmul (the softmax is issue-bound: ncu,
+        // profiles/r02attn)
+        const bool need_mask = qpos0 < kt * FA_BN + FA_BN || qpos0 + FB_BQ > T;
+        const unsigned long long sc2 = f2pack(scale_log2, scale_log2);
+        // -lse2 / -Dv of this half's 32 query columns: explicit shared loads (the
+        // generic float2 loads compiled to LD.E through the global path, ncu
+        // stall_lg, profiles/r02attn)
+        float nlv[32], ndv[32];
+        const uint32_t la = smem_u32(L + c * 32), da = smem_u32(D + c * 32);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                       : "=f"(nlv[4 * q]), "=f"(nlv[4 * q + 1]), "=f"(nlv[4 * q + 2]), "=f"(nlv[4 * q + 3])
+                       : "r"(la + 16 * q));
+          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                       : "=f"(ndv[4 * q]), "=f"(ndv[4 * q + 1]), "=f"(ndv[4 * q + 2]), "=f"(ndv[4 * q + 3])
+                       : "r"(da + 16 * q));
+        }
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-          float p2[2], d2[2];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int col = c * 32 + 2 * q + e;
-            const int qpos = qpos0 + col;
-            float p = ex2_approx(__uint_as_float(vs[2 * q + e]) * scale_log2 - L[col]);
-            if (qpos < kpos || qpos >= T) p = 0.f;
-            p2[e] = p;
-            d2[e] = p * (__uint_as_float(vp[2 * q + e]) - D[col]);
+          const float2 nl = make_float2(nlv[2 * q], nlv[2 * q + 1]);
+          const float2 nd = make_float2(ndv[2 * q], ndv[2 * q + 1]);
+          float x0, x1, p0, p1, d0, d1;
+          f2unpack(ffma2(f2pack(__uint_as_float(vs[2 * q]), __uint_as_float(vs[2 * q + 1])), sc2,
+                         f2pack(nl.x, nl.y)), x0, x1);
+          p0 = ex2_approx(x0);
+          p1 = ex2_approx(x1);
+          if (need_mask) {
+            const int qpos = qpos0 + c * 32 + 2 * q;
+            if (qpos < kpos || qpos >= T) p0 = 0.f;
+            if (qpos + 1 < kpos || qpos + 1 >= T) p1 = 0.f;
           }
-          wp[q] = pack_bf16(p2[0], p2[1]);
-          wd[q] = pack_bf16(d2[0], d2[1]);
+          const unsigned long long t2 = fadd2(
+              f2pack(__uint_as_float(vp[2 * q]), __uint_as_float(vp[2 * q + 1])), f2pack(nd.x, nd.y));
+          f2unpack(fmul2(f2pack(p0, p1), t2), d0, d1);
+          wp[q] = pack_bf16(p0, p1);
+          wd[q] = pack_bf16(d0, d1);
         }
         // P^T and dS^T as TMEM A operands: this warpgroup's 32 query columns,
         // packed bf16x2, over the first 16 columns of its own fp32 slab of the
@@ -1236,17 +1266,27 @@ __global__ void __launch_bounds__(384, 1)
         tmem_ld_32x32b_x32(tDP + c * 32, vp);
         tmem_ld_wait();
         uint32_t wd[16];
+        // mask only on the key tiles at the diagonal or rows past T (CTA-uniform);
+        // packed f32x2 ops, same per-element roundings (profiles/r02attn)
+        const bool need_mask = j * FQ_BK + FQ_BK - 1 > qt * FA_BM || qt * FA_BM + FA_BM > T;
+        const unsigned long long sc2 = f2pack(scale_log2, scale_log2);
+        const unsigned long long nl2 = f2pack(-Lr, -Lr), nd2 = f2pack(-Dr, -Dr);
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-          float d2[2];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int kpos = j * FQ_BK + c * 32 + 2 * q + e;
-            float p = ex2_approx(fmaf(__uint_as_float(vs[2 * q + e]), scale_log2, -Lr));
-            if (kpos > pos || !ok) p = 0.f;
-            d2[e] = p * (__uint_as_float(vp[2 * q + e]) - Dr);
+          float x0, x1, p0, p1, d0, d1;
+          f2unpack(ffma2(f2pack(__uint_as_float(vs[2 * q]), __uint_as_float(vs[2 * q + 1])), sc2,
+                         nl2), x0, x1);
+          p0 = ex2_approx(x0);
+          p1 = ex2_approx(x1);
+          if (need_mask) {
+            const int kpos = j * FQ_BK + c * 32 + 2 * q;
+            if (kpos > pos || !ok) p0 = 0.f;
+            if (kpos + 1 > pos || !ok) p1 = 0.f;
           }
-          wd[q] = pack_bf16(d2[0], d2[1]);
+          const unsigned long long t2 =
+              fadd2(f2pack(__uint_as_float(vp[2 * q]), __uint_as_float(vp[2 * q + 1])), nd2);
+          f2unpack(fmul2(f2pack(p0, p1), t2), d0, d1);
+          wd[q] = pack_bf16(d0, d1);
         }
         // dS as a TMEM A operand: packed into the first 16 columns of this
         // warpgroup's fp32 slab of the S buffer (read above)
