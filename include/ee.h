@@ -53,7 +53,8 @@ typedef enum {
   EE_ERR_STRUCTURE = 6,   /* Copy init: a source module is missing        */
   EE_ERR_DIVERGED = 7,    /* non-finite loss (device-detected, carries exit idx)  */
   EE_ERR_WORKSPACE = 8,   /* workspace NULL or smaller than ee_workspace_size()   */
-  EE_ERR_CUDA = 9,        /* a CUDA runtime/driver call failed                    */
+  EE_ERR_CUDA = 9,        /* a CUDA runtime/driver call failed; device: a decode
+                             stream-K fix-up wait timed out (ee_exit_infer)     */
   EE_ERR_NCCL = 10,       /* reserved for the in-library collectives              */
   EE_ERR_UNSUPPORTED = 11,/* no sm_100 device                                     */
   EE_ERR_PEER = 12        /* a peer rank did not reach ee_peer_barrier (device)    */
@@ -480,7 +481,8 @@ ee_status ee_ipc_close(void* dev_ptr, uint64_t offset);
  * programmatic dependent launch) and a wide finalize; same results up to fp32
  * summation order, bitwise reproducible call to call.  No loss, no gradients.
  * The stream-K fix-up uses a library-global pool of 16 slots: at most 16
- * decode calls may EXECUTE concurrently (calls on one stream never overlap).
+ * decode calls may EXECUTE concurrently (calls on one stream never overlap);
+ * a fix-up wait bounded at 5 s reports EE_ERR_CUDA through ee_get_status.
  * Env EE_INFER_SKINNY=0 forces the GEMM path, EE_PDL=0 plain launches. */
 ee_status ee_exit_infer(const ee_head_config* cfg, const void* const* hidden, int64_t n_tokens,
                         const ee_head_tensors* params, float threshold, int32_t* const* argmax_out,

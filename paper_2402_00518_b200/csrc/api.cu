@@ -1396,14 +1396,14 @@ static ee_status infer_decode_exit(const ee_head_config* cfg, const Bufs& B,
                                  nullptr, true)); }
       {
         SkinnyArgs a{};
-        a.x = B.u; a.ldx = h; a.W0 = (const __nv_bfloat16*)P.w_gate;
+        a.x = B.u; a.ldx = h; a.st = B.status; a.W0 = (const __nv_bfloat16*)P.w_gate;
         a.W1 = (const __nv_bfloat16*)P.w_up; a.K = h; a.N = F; a.outb = B.mact; a.ldo = F;
         Prof p_("dec_gateup_swiglu", st, 4.0 * n * F * h, 4.0 * n * F * h, 4.0 * F * h);
         EE_CUDA(launch_skinny(SK_SWIGLU, a, M, st));
       }
       {
         SkinnyArgs a{};
-        a.x = B.mact; a.ldx = F; a.W0 = (const __nv_bfloat16*)P.w_down; a.K = F; a.N = h;
+        a.x = B.mact; a.ldx = F; a.st = B.status; a.W0 = (const __nv_bfloat16*)P.w_down; a.K = F; a.N = h;
         a.out = B.y; a.ldo = h; a.resid = x; a.ldr = h;
         Prof p_("dec_down_resid", st, 2.0 * n * F * h, 2.0 * n * F * h, 2.0 * F * h);
         EE_CUDA(launch_skinny(SK_RESID, a, M, st));
@@ -1417,7 +1417,7 @@ static ee_status infer_decode_exit(const ee_head_config* cfg, const Bufs& B,
     z = B.z;
   }
   SkinnyArgs a{};
-  a.x = z; a.ldx = h; a.W0 = (const __nv_bfloat16*)P.w_out; a.K = h; a.N = Vl;
+  a.x = z; a.ldx = h; a.st = B.status; a.W0 = (const __nv_bfloat16*)P.w_out; a.K = h; a.N = Vl;
   a.pm = pm; a.ps = ps; a.pi = pi; a.vocab_begin = cfg->vocab_begin;
   Prof p_("dec_vocab_ce", st, 2.0 * n * Vl * h, 2.0 * n * Vl * h, 2.0 * Vl * h);
   EE_CUDA(launch_skinny(SK_CE, a, M, st));

@@ -164,6 +164,7 @@ struct SkinnyArgs {
   float *pm, *ps;           // CE: [blocks x M] partial max / sum-exp
   int32_t* pi;              //     partial argmax (global vocab index)
   int vocab_begin;
+  DevStatus* st;            // stream-K fix-up wait timeout -> EE_ERR_CUDA (or NULL)
 };
 cudaError_t launch_skinny(int mode, const SkinnyArgs& a, int M, cudaStream_t s);
 int skinny_blocks(int N);

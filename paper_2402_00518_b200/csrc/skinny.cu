@@ -249,7 +249,19 @@ __global__ void __launch_bounds__(SD_THREADS, 1)
     // finisher: add the contributions of the later CTAs starting inside rb, in CTA order
     for (long long q = cta + 1; q < G; ++q) {
       if (p.units * q / G >= rb_end) break;
-      while (ld_acquire_u32(&g_sd_flag[p.slot][q]) != p.epoch) __nanosleep(32);
+      // bounded wait: the contributor is resident or about to be (one CTA per
+      // SM, grid <= SMs); only co-running kernels that never yield could hold
+      // it off, and then the call fails (status) instead of hanging
+      if (ld_acquire_u32(&g_sd_flag[p.slot][q]) != p.epoch) {
+        const unsigned long long t0 = globaltimer_ns();
+        while (ld_acquire_u32(&g_sd_flag[p.slot][q]) != p.epoch) {
+          __nanosleep(32);
+          if (globaltimer_ns() - t0 > 5000000000ull) {
+            if (p.a.st && tid == 0) set_status(p.a.st, 9 /* EE_ERR_CUDA */, -1);
+            break;
+          }
+        }
+      }
       const float4 v = __ldcg(&g_sd_part[p.slot][q][0][tid]);
       d0[0] += v.x; d0[1] += v.y; d0[2] += v.z; d0[3] += v.w;
       const float4 w = __ldcg(&g_sd_part[p.slot][q][1][tid]);
