@@ -1001,8 +1001,10 @@ __global__ void __launch_bounds__(384, 1)
           // queries 16k.. sit at column 32*(k/2) + 8*(k%2) (each warpgroup's slab)
           const uint32_t offa = (k >> 1) * 32 + (k & 1) * 8;
           const uint32_t offb = (k * 2048) >> 4;
+#ifndef EE_EXPT_NO_DVDK  // timing experiment (profiles/r02attn), never in the product build
           tc_mma_f16_ts_w(tDV, tPt + offa, ddo0 + offb, idesc_acc, (it | k) != 0 ? 1u : 0u);
           tc_mma_f16_ts_w(tDK, tDSt + offa, dq0 + offb, idesc_acc, (it | k) != 0 ? 1u : 0u);
+#endif
         }
         tc_commit_w(&qd_empty[qs]);
       }
@@ -1041,6 +1043,13 @@ __global__ void __launch_bounds__(384, 1)
       asm volatile("bar.sync 1, 256;" ::: "memory");
       mbar_wait(&sdp_full[it & 1], (it >> 1) & 1);
       tc_fence_after();
+#ifdef EE_EXPT_NO_SOFTMAX  // timing experiment (profiles/r02attn), never in the product build
+      if (true) {
+        tc_fence_before();
+        mbar_arrive(&pds_full[it & 1]);
+        continue;
+      }
+#endif
       {
         const int c = half;
         uint32_t vs[32], vp[32];
