@@ -1,5 +1,5 @@
 #!/bin/bash
-# r02wce: 256 x 512 tiles for the CE GEMMs (a5 stats, a7 dS; EE_GEMM_WIDE_CE=1): parity, then interleaved C4 / C2 A/B.
+# ${TAG}: 256 x 512 tiles for the CE GEMMs (a5 stats, a7 dS; EE_GEMM_WIDE_CE=1): parity, then interleaved C4 / C2 A/B.
 TAG=${1:-r02wce}
 mkdir -p gpurun_out
 EE_GEMM_WIDE_CE=1 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_largen.py tests/test_gpu_fullsize.py -q -x > gpurun_out/${TAG}_pytest.log 2>&1
