@@ -88,3 +88,45 @@ def test_exit_infer_decode_stream_k(gpu_lib, arch, h, V, F, n):
         S_i = O.exit_forward(arch, p64[i], to_f64(hidden[i]), 1e-5)["S"]
         check_argmax(am[i].cpu().numpy(), S_i)
         assert np.max(np.abs(cf[i].cpu().numpy() - cf_o[i])) <= 2e-2
+
+
+def test_exit_infer_decode_concurrent_streams(gpu_lib):
+    """Decode calls executing concurrently on several streams (each with its own
+    workspace) share the library's stream-K fix-up pool by slot: every stream's
+    results equal its serial run bitwise (include/ee.h: up to 16 concurrently
+    executing calls)."""
+    ee = gpu_lib
+    h, V, F, E, n = 2048, 8008, 5760, 2, 3
+    cfg = S.Cfg(name="dec", hidden=h, vocab=V, ffn=F, arch="mlp", tokens=n, layers=E,
+                after=[1, 2], init="random", seed=91)
+    params = S.head_params(cfg)
+    c = ee.make_config(h, V, F, E, "mlp")
+    ops = [{k: (v.cuda().float() if k.startswith("g_") else v.cuda().to(torch.bfloat16))
+            for k, v in p.items()} for p in params]
+    nstreams = 6
+    inputs = [[x.cuda() for x in S.hidden_states(cfg, n, seed=200 + s)] for s in range(nstreams)]
+    ws = [torch.zeros(ee.ee_workspace_size(c, n), dtype=torch.uint8, device="cuda")
+          for _ in range(nstreams)]
+
+    def outs():
+        return ([torch.zeros(n, dtype=torch.int32, device="cuda") for _ in range(E)],
+                [torch.zeros(n, device="cuda") for _ in range(E)])
+    serial = []
+    for s in range(nstreams):
+        am, cf = outs()
+        ee.ee_exit_infer(c, inputs[s], ops, 0.5, am, cf, ws[s])
+        torch.cuda.synchronize()
+        serial.append((am, cf))
+    streams = [torch.cuda.Stream() for _ in range(nstreams)]
+    conc = [outs() for _ in range(nstreams)]
+    torch.cuda.synchronize()
+    for rep in range(3):
+        for s in range(nstreams):
+            with torch.cuda.stream(streams[s]):
+                ee.ee_exit_infer(c, inputs[s], ops, 0.5, conc[s][0], conc[s][1], ws[s],
+                                 stream=streams[s])
+        torch.cuda.synchronize()
+        for s in range(nstreams):
+            for i in range(E):
+                assert torch.equal(conc[s][0][i], serial[s][0][i]), (rep, s, i)
+                assert torch.equal(conc[s][1][i], serial[s][1][i]), (rep, s, i)
