@@ -365,18 +365,30 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
         // gw[n'][m] over the 32 threads of a warp (consecutive m) is one
         // coalesced 64-byte segment per n
         const float rs = args.row_scale[gm];
+        if (args.gain_part != nullptr) {
+          // the 32 weight values first (read-only loads, all in flight at once),
+          // then the fixed-order FMA chain: issued one by one behind the FMAs
+          // they exposed a full L2 latency each, and at K = 8192 (DP over 8
+          // ranks) the epilogue outlasted the mainloop (ncu, profiles/r02dp8)
+          // (asm volatile keeps the 32 loads in issue order ahead of their first
+          // use -- with plain loads nvcc reused one register and waited on
+          // each; indices past N are clamped, their products skipped)
+          uint16_t wraw[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int gn = gn0 + j;
-          const float a = u2f(v[j]);
-          if (args.gain_part != nullptr && gn < args.N) {
+          for (int j = 0; j < 32; ++j) {
+            const int gn = min(gn0 + j, args.N - 1);
             const __nv_bfloat16* w = gn < args.n_split
                                          ? args.gain_w0 + (long long)gn * args.M + gm
                                          : args.gain_w1 + (long long)(gn - args.n_split) * args.M + gm;
-            gsum = fmaf(__bfloat162float(*w), a, gsum);
+            asm volatile("ld.global.nc.u16 %0, [%1];" : "=h"(wraw[j]) : "l"(w));
           }
-          v[j] = __float_as_uint(a * rs);
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (gn0 + j < args.N)
+              gsum = fmaf(__uint_as_float(static_cast<uint32_t>(wraw[j]) << 16), u2f(v[j]), gsum);
         }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(u2f(v[j]) * rs);
       }
       if (EPI == EPI_F32T_ADAM && row_ok && gn0 < args.N) {
         // fused Adam, element (row n, column m): 16 columns per batch, all 48
@@ -1117,6 +1129,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
          tile = warp_tile(tile, false)) {
       int mb, nb;
       tile_coords(args, tile, mb, nb);
+      if constexpr (EPI == EPI_F32T && NB2 == 1) {
+        // gain identity (A28): this tile's epilogue reads W[n][m] for its 256
+        // columns n and this CTA's 128 rows m (256 B per row).  Prefetch them
+        // into L2 while the mainloop runs: read cold, the 64-byte pieces at a
+        // 16 KB stride exposed DRAM latency chunk by chunk and at K = 8192 (DP
+        // over 8 ranks) the epilogue outlasted the mainloop 4x (profiles/r02dp8)
+        if (args.gain_part != nullptr && lane == 0) {
+          const int m0 = mb * 256 + (int)rank * 128;
+          if (m0 < args.M) {
+            const uint32_t bytes = (uint32_t)(min(128, args.M - m0) * 2);
+            for (int i = ew; i < GEMM_BN; i += 4) {
+              const int gn = nb * GEMM_BN + i;
+              if (gn >= args.N) break;
+              const __nv_bfloat16* w = gn < args.n_split
+                                           ? args.gain_w0 + (long long)gn * args.M + m0
+                                           : args.gain_w1 + (long long)(gn - args.n_split) * args.M + m0;
+              bulk_prefetch_l2(w, bytes);
+            }
+          }
+        }
+      }
       if (args.epi_sleep >= 2)
         mbar_wait_backoff(&tfull[acc], acc_ph, (uint32_t)args.epi_sleep);
       else if (args.epi_sleep)
