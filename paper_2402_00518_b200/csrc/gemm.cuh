@@ -518,50 +518,64 @@ __device__ __forceinline__ void epilogue_tile(const GemmArgs& args, uint32_t tb,
       const int f0 = nb * GEMM_BN + c * 32;
       if (row_ok && f0 < args.N) {
         __nv_bfloat16* arow = args.ab + (long long)gm * args.ld_ab;
+        // both 16-column halves' A / B loads first, then the math, then the
+        // stores: the in-place stores (asm volatile, "memory") otherwise kept
+        // the second half's loads behind the first half's stores -- one memory
+        // latency per 16 columns
+        uint32_t qa[2][8], qb[2][8];
+        bool v8[2];
 #pragma unroll
-        for (int j = 0; j < 32; j += 16) {
-          __nv_bfloat16* pa_ = arow + f0 + j;
-          __nv_bfloat16* pb_ = arow + F + f0 + j;
-          const bool v8 = aligned32(pa_) && aligned32(pb_);
-          uint32_t qa[8], qb[8], wa[8], wb[8];
-          if (v8) {
-            ld_global_v8(pa_, qa);
-            ld_global_v8(pb_, qb);
+        for (int hf = 0; hf < 2; ++hf) {
+          __nv_bfloat16* pa_ = arow + f0 + 16 * hf;
+          __nv_bfloat16* pb_ = arow + F + f0 + 16 * hf;
+          v8[hf] = aligned32(pa_) && aligned32(pb_);
+          if (v8[hf]) {
+            ld_global_v8(pa_, qa[hf]);
+            ld_global_v8(pb_, qb[hf]);
           } else {
             const uint4 a0 = *reinterpret_cast<const uint4*>(pa_);
             const uint4 a1 = *reinterpret_cast<const uint4*>(pa_ + 8);
             const uint4 b0 = *reinterpret_cast<const uint4*>(pb_);
             const uint4 b1 = *reinterpret_cast<const uint4*>(pb_ + 8);
-            qa[0] = a0.x; qa[1] = a0.y; qa[2] = a0.z; qa[3] = a0.w;
-            qa[4] = a1.x; qa[5] = a1.y; qa[6] = a1.z; qa[7] = a1.w;
-            qb[0] = b0.x; qb[1] = b0.y; qb[2] = b0.z; qb[3] = b0.w;
-            qb[4] = b1.x; qb[5] = b1.y; qb[6] = b1.z; qb[7] = b1.w;
+            qa[hf][0] = a0.x; qa[hf][1] = a0.y; qa[hf][2] = a0.z; qa[hf][3] = a0.w;
+            qa[hf][4] = a1.x; qa[hf][5] = a1.y; qa[hf][6] = a1.z; qa[hf][7] = a1.w;
+            qb[hf][0] = b0.x; qb[hf][1] = b0.y; qb[hf][2] = b0.z; qb[hf][3] = b0.w;
+            qb[hf][4] = b1.x; qb[hf][5] = b1.y; qb[hf][6] = b1.z; qb[hf][7] = b1.w;
           }
+        }
+        uint32_t wa[2][8], wb[2][8];
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             float da[2], db[2];
 #pragma unroll
             for (int h2 = 0; h2 < 2; ++h2) {
-              const float a = h2 ? bf16hi(qa[q]) : bf16lo(qa[q]);
-              const float b = h2 ? bf16hi(qb[q]) : bf16lo(qb[q]);
-              const float dm = u2f(v[j + 2 * q + h2]);
+              const float a = h2 ? bf16hi(qa[hf][q]) : bf16lo(qa[hf][q]);
+              const float b = h2 ? bf16hi(qb[hf][q]) : bf16lo(qb[hf][q]);
+              const float dm = u2f(v[16 * hf + 2 * q + h2]);
               // fast division: with the IEEE one this epilogue outlasted the
               // next tile's mainloop at K = 5120 (13B: 1.09 -> 1.3 PFLOP/s)
               const float sg = __fdividef(1.0f, 1.0f + __expf(-a));
               db[h2] = dm * a * sg;
               da[h2] = dm * b * sg * (1.0f + a * (1.0f - sg));
             }
-            wa[q] = pack_bf16(da[0], da[1]);
-            wb[q] = pack_bf16(db[0], db[1]);
+            wa[hf][q] = pack_bf16(da[0], da[1]);
+            wb[hf][q] = pack_bf16(db[0], db[1]);
           }
-          if (v8) {
-            st_global_v8(pa_, wa);
-            st_global_v8(pb_, wb);
+        }
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          __nv_bfloat16* pa_ = arow + f0 + 16 * hf;
+          __nv_bfloat16* pb_ = arow + F + f0 + 16 * hf;
+          if (v8[hf]) {
+            st_global_v8(pa_, wa[hf]);
+            st_global_v8(pb_, wb[hf]);
           } else {
-            *reinterpret_cast<uint4*>(pa_) = make_uint4(wa[0], wa[1], wa[2], wa[3]);
-            *reinterpret_cast<uint4*>(pa_ + 8) = make_uint4(wa[4], wa[5], wa[6], wa[7]);
-            *reinterpret_cast<uint4*>(pb_) = make_uint4(wb[0], wb[1], wb[2], wb[3]);
-            *reinterpret_cast<uint4*>(pb_ + 8) = make_uint4(wb[4], wb[5], wb[6], wb[7]);
+            *reinterpret_cast<uint4*>(pa_) = make_uint4(wa[hf][0], wa[hf][1], wa[hf][2], wa[hf][3]);
+            *reinterpret_cast<uint4*>(pa_ + 8) = make_uint4(wa[hf][4], wa[hf][5], wa[hf][6], wa[hf][7]);
+            *reinterpret_cast<uint4*>(pb_) = make_uint4(wb[hf][0], wb[hf][1], wb[hf][2], wb[hf][3]);
+            *reinterpret_cast<uint4*>(pb_ + 8) = make_uint4(wb[hf][4], wb[hf][5], wb[hf][6], wb[hf][7]);
           }
         }
       }
