@@ -37,7 +37,7 @@ namespace ee {
 namespace {
 constexpr int SD_ROWS = 32;                      // weight rows per row block (= CE block)
 constexpr int SD_KC = 256;                       // k per stage: 4 swizzle atoms of 64
-constexpr int SD_ATOMS = SD_KC / 64;  // 4 (the atom sums below are written out for 4)
+constexpr int SD_ATOMS = SD_KC / 64;            // 4 (the atom sums below are written out for 4)
 constexpr int SD_W_ATOM = SD_ROWS * 128;         // 4 KB: 32 rows x 128 B
 constexpr int SD_CONSUMERS = 4;                  // warps 0-3, 8 weight rows each
 constexpr int SD_THREADS = 32 * (SD_CONSUMERS + 1);  // + warp 4: TMA producer
@@ -46,8 +46,9 @@ constexpr int SD_SLOTS = 16;                     // launches in flight sharing t
 
 // Stage = NW weight tiles + the [M x 256] activation slice (one 1 KB swizzle
 // atom per 64 k for M <= 8 tokens, 2 KB for M <= 16); as many stages as fit in
-// ~200 KB of shared memory: the bytes in flight per SM are what sets the
-// stream's bandwidth (96 KB in flight: 4.2 TB/s, 128 KB: 6.5 TB/s; r02x).
+// ~200 KB of shared memory.  (Measured, profiles/r02x: going from 96 to 200 KB
+// in flight did not move a one-tile-per-stage stream off 4.2 TB/s -- two
+// far-apart tiles per stage did, see the kernel.)
 template <int M, int NW>
 struct SdCfg {
   static constexpr int W_BYTES = NW * SD_ATOMS * SD_W_ATOM;
